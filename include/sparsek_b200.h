@@ -1,0 +1,191 @@
+/* sparsek_b200.h — the C-ABI drop-in boundary of the B200 SparseK attention path.
+ *
+ * Plain pointers and sizes only; every call takes a cudaStream_t (passed as
+ * void*) and returns an skb_status. Errors never fall back to a CPU path: a
+ * failing call returns non-zero and skb_last_error() (thread-local) says why.
+ *
+ * Each entry point names the reference interface it replaces (paths relative
+ * to the reference tree, proj/...):
+ *
+ *   skb_score_fwd      detail::score_one / score_tokens
+ *                      proj/include/sparsek/selection.hpp:55-56,69-96,
+ *                      TimestepNormState::push proj/src/selection.cpp:13-20
+ *   skb_score_bwd      scores->raw pullback + dw_score + the dx term
+ *                      proj/src/attention.cpp:482-516,564
+ *   skb_select         StreamState::push (prefix tau) proj/src/stream.cpp:72-152 +
+ *                      SparseKvCache::exit_window/admit_to_cache (top-floor(k)
+ *                      retention) proj/src/cache.cpp:136-179 + snapshot/gates :285-311
+ *   skb_attn_fwd       SparseKvCache::forward_chunk pass 2 proj/src/cache.cpp:315-394
+ *                      (the attention inside sparsek_attention, attention.hpp:81-85)
+ *   skb_attn_bwd       sparsek_attention_backward core proj/src/attention.cpp:259-316
+ *                      + selection pullback (JVP) :447-479
+ *   skb_sparsek*       sparsek / sparsek_jvp / topk_hard
+ *                      proj/include/sparsek/sparsek_op.hpp:47-66
+ *   skb_cache_*        SparseKvCache + generate_step proj/include/sparsek/cache.hpp:21-102,
+ *                      proj/src/cache.cpp:570-577
+ *
+ * Tensor layout: Q/K/V/O/dO/dQ/dK/dV are [B, L, H, p] contiguous — the
+ * reference's row-major [L, D] per sequence with head h in columns
+ * [h*p, (h+1)*p) (proj/include/sparsek/attention.hpp:36). Scores u are
+ * float64 [B, L], as the reference keeps them (selection.hpp:72-74).
+ */
+#ifndef SPARSEK_B200_H
+#define SPARSEK_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes mirror the reference error taxonomy (proj/include/sparsek/common.hpp:9-25). */
+typedef enum {
+    SKB_OK = 0,
+    SKB_ESHAPE = 1,    /* ShapeError    */
+    SKB_EARG = 2,      /* ArgumentError */
+    SKB_ENUMERIC = 3,  /* NumericError  */
+    SKB_ECONFIG = 4,   /* ConfigError   */
+    SKB_EIO = 5,       /* IoError       */
+    SKB_ECUDA = 6      /* CUDA runtime / launch failure */
+} skb_status;
+
+typedef enum { SKB_F32 = 0, SKB_BF16 = 1, SKB_F64 = 2 } skb_dtype;
+
+/* Execution-path flags. The tensor-core (tcgen05) path is used for BF16 by
+ * default; F32/F64 always run the CUDA-core gather path. */
+#define SKB_FLAG_FORCE_GATHER 1u /* run BF16 on the CUDA-core gather kernels */
+
+/* AttnConfig (proj/include/sparsek/attention.hpp:18-32) at the Q/K/V/u level. */
+typedef struct skb_attn_desc {
+    int64_t batch;     /* B: independent sequences                      */
+    int64_t seq_len;   /* L                                             */
+    int64_t heads;     /* H                                             */
+    int64_t head_dim;  /* p = d_model / heads                           */
+    double k;          /* selection budget (real); 0 = pure window      */
+    int64_t window;    /* sliding-window size w                         */
+    double scale;      /* 0 -> 1/sqrt(p)                                */
+    int32_t key_mode;  /* 0 KeyMode::hard, 1 KeyMode::soft              */
+    int32_t mask_mode; /* 0 MaskApply::soft, 1 MaskApply::straight_through */
+    int32_t dtype;     /* skb_dtype of Q/K/V/O/dO/dQ/dK/dV             */
+    uint32_t flags;    /* SKB_FLAG_*                                    */
+} skb_attn_desc;
+
+/* ScoringParams (proj/include/sparsek/selection.hpp:19-27) minus w_score. */
+typedef struct skb_scoring {
+    int32_t norm_mode;     /* 0 none, 1 timestep_norm                   */
+    int32_t slope_order;   /* 0 slope_then_norm, 1 norm_then_slope      */
+    int32_t slope_enabled; /* 0/1                                       */
+    int32_t reserved;
+    double slope_eps;      /* > 0                                       */
+} skb_scoring;
+
+/* Where skb_select puts its products inside the caller's workspace (byte
+ * offsets). leave[b*L + j] = the push time at which position j leaves the
+ * top-floor(k) set (== j when it never enters, == L-w when it never leaves);
+ * tau[b*L + t] = the threshold after push t (-inf while t+1 < k); nfrac is the
+ * fractional-support size |{j<=t : 0 < u_j - tau_t < 1}|; qb_list holds, per
+ * 128-query block, the ascending union of the selected sets its queries read. */
+typedef struct skb_select_layout {
+    uint64_t leave;       /* int32  [B, L]                 */
+    uint64_t leave_ceil;  /* int32  [B, L] (rank ceil(k))  */
+    uint64_t tau;         /* double [B, L]  (push time)    */
+    uint64_t nfrac;       /* int32  [B, L]  (push time)    */
+    uint64_t qb_count;    /* int32  [B, NQB]               */
+    uint64_t qb_list;     /* int32  [B, NQB, qb_cap]       */
+    uint64_t ever_count;  /* int32  [B]                    */
+    uint64_t ever_list;   /* int32  [B, L] ever-selected keys, ascending */
+    uint64_t misc;        /* int32 scratch (overflow queue) */
+    uint64_t scratch;     /* double scratch (overflow chunks) */
+    uint64_t total_bytes;
+    int64_t qblock;       /* queries per block (128)       */
+    int64_t nqb;          /* ceil(L / qblock)              */
+    int64_t qb_cap;       /* floor(k) + qblock             */
+} skb_select_layout;
+
+const char* skb_last_error(void);
+int skb_version(void);
+
+/* ---- K1: scoring (raw = x.w in float64, Welford prefix norm, slope) ------ */
+/* x: [B, L, D] of x_dtype; w: float64 [D]; outputs float64 [B, L]. Exact
+ * sequential Welford order per sequence (bit-identical arithmetic to the
+ * reference when x rows and w match). */
+int skb_score_fwd(int64_t B, int64_t L, int64_t D, int32_t x_dtype, const void* x,
+                  const double* w, const skb_scoring* sc, double* raw, double* u, double* mean,
+                  double* sdev, void* stream);
+/* gu: float64 [B, L] -> graw [B, L]; dw_score float64 [D] (= sum over B and
+ * positions of graw * x); dx (optional, x_dtype [B, L, D]) += graw * w. */
+int skb_score_bwd(int64_t B, int64_t L, int64_t D, int32_t x_dtype, const void* x,
+                  const double* w, const skb_scoring* sc, const double* gu, const double* raw,
+                  const double* mean, const double* sdev, double* graw, double* dw_score,
+                  void* dx, void* stream);
+
+/* ---- K2: prefix SparseK threshold + top-floor(k) retention --------------- */
+int skb_select_layout_of(const skb_attn_desc* d, skb_select_layout* out);
+int skb_select(const skb_attn_desc* d, const double* u, void* ws, void* stream);
+
+/* ---- K3/K4: gated sparse attention over Sel_i U window ------------------- */
+/* lse: float64 [B, H, L] = maxa + log(denom) per (query, head). */
+int skb_attn_fwd(const skb_attn_desc* d, const void* q, const void* k, const void* v,
+                 const double* u, const void* sel_ws, void* o, double* lse, void* stream);
+int skb_attn_bwd_workspace_size(const skb_attn_desc* d, size_t* bytes);
+/* du: float64 [B, L] gradient w.r.t. the scores u (selection JVP included). */
+int skb_attn_bwd(const skb_attn_desc* d, const void* q, const void* k, const void* v,
+                 const void* o, const void* dout, const double* lse, const double* u,
+                 const void* sel_ws, void* dq, void* dk, void* dv, double* du, void* ws,
+                 void* stream);
+
+/* ---- SparseK operator (batched rows) ------------------------------------ */
+/* z: float64 [n, m]; p: [n, m]; tau: [n] (-inf when infeasible); counts [n];
+ * flags[n]: bit0 degenerate, bit1 infeasible. */
+int skb_sparsek(int64_t n, int64_t m, const double* z, double k, double* p, double* tau,
+                int64_t* u_count, int64_t* w_count, int32_t* flags, void* stream);
+int skb_sparsek_jvp(int64_t n, int64_t m, const double* z, double k, const double* v,
+                    double* out, void* stream);
+int skb_topk_hard(int64_t n, int64_t m, const double* z, int64_t k, double* out, void* stream);
+
+/* ---- K5: constant-(floor(k)+w) KV cache for decoding --------------------- */
+typedef struct skb_cache skb_cache;
+/* d->seq_len = maximum number of positions a sequence may see. */
+int skb_cache_create(const skb_attn_desc* d, skb_cache** out);
+int skb_cache_destroy(skb_cache* c);
+/* One decode step for all B sequences: q/k/v [B, H, p] (dtype), u float64 [B]
+ * (the new tokens' frozen scores) -> o [B, H, p]. */
+int skb_cache_step(skb_cache* c, const void* q, const void* k, const void* v, const double* u,
+                   void* o, void* stream);
+/* Host-visible state for tests/inspection: retained positions (ascending
+ * selected then window), count, tau, positions seen, peak retained. */
+int skb_cache_state(skb_cache* c, int64_t b, int32_t* positions, int64_t* count, double* tau,
+                    int64_t* seen, int64_t* peak, void* stream);
+
+
+/* ---- Incremental SparseK stream on the device (Algorithm 2) ------------- */
+/* StreamState (proj/include/sparsek/stream.hpp:26-72, proj/src/stream.cpp:72-192):
+ * the same push/scan, with the survivors kept as a sorted device array. */
+typedef struct skb_stream skb_stream;
+typedef struct skb_stream_info {
+    double tau;          /* -inf while t < k                         */
+    int64_t t;           /* elements pushed                           */
+    int64_t survivors;   /* |heap_s|                                  */
+    int64_t saturated;   /* |heap_f|                                  */
+    uint64_t cap_drops;  /* survivors dropped by a bounded heap       */
+    uint64_t heap_ops;
+    double k;
+} skb_stream_info;
+/* capacity = maximum number of pushes; heap_cap 0 = unbounded. */
+int skb_stream_create(double k, int64_t heap_cap, int64_t capacity, skb_stream** out);
+int skb_stream_destroy(skb_stream* s);
+/* Push z[0..n) (device float64) in order; per push the threshold after it and
+ * whether it entered the survivors (device outputs, either may be NULL). */
+int skb_stream_push(skb_stream* s, const double* z, int64_t n, double* tau_out,
+                    uint8_t* inserted_out, void* stream);
+int skb_stream_query(skb_stream* s, skb_stream_info* out, void* stream);
+/* Host copies: survivor values/indices in ascending index order (|survivors|
+ * entries) and the evicted flag of every pushed index (t entries). */
+int skb_stream_survivors(skb_stream* s, double* values, int64_t* indices, uint8_t* evicted,
+                         void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPARSEK_B200_H */

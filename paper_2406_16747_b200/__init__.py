@@ -1,0 +1,26 @@
+"""B200-native SparseK attention (arXiv 2406.16747): the reference's operator
+API and Python bindings over hand-written sm_100a kernels.
+
+* Reference-compatible surface (``_sparsek``, proj/bindings/module.cpp):
+  ``sparsek, sparsek_jvp, Stream, attention, dense_attention`` and the error
+  types — see ``api.py``.
+* Torch-level core (device tensors, autograd): ``ops``.
+"""
+from ._lib import ArgumentError, ConfigError, IoError, NumericError, ShapeError  # noqa: F401
+from .api import (  # noqa: F401
+    Stream,
+    __version__,
+    attention,
+    attention_grads,
+    dense_attention,
+    sparsek,
+    sparsek_jvp,
+    topk_hard,
+)
+from . import ops  # noqa: F401
+
+__all__ = [
+    "ArgumentError", "ConfigError", "NumericError", "ShapeError", "IoError", "Stream",
+    "__version__", "attention", "attention_grads", "dense_attention", "sparsek", "sparsek_jvp",
+    "topk_hard", "ops",
+]

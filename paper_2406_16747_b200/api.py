@@ -1,0 +1,202 @@
+"""The reference's Python surface (``_sparsek``, proj/bindings/module.cpp:79-180),
+re-implemented over the B200 kernels.
+
+Same names, keyword arguments, return shapes and exception types as the
+reference module, so ``import paper_2406_16747_b200 as sparsek`` is a drop-in for
+``import sparsek``. Inputs are numpy arrays / sequences (copied to the GPU);
+every computation runs in libsparsek_b200.so or cuBLAS (the D x D projections).
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+
+from . import _lib, ops
+from ._lib import ArgumentError, ConfigError, NumericError, ShapeError
+
+__version__ = "0.1.0"
+
+
+def _dev():
+    if not torch.cuda.is_available():
+        raise _lib.CudaError("paper_2406_16747_b200 needs a CUDA device (no CPU fallback)")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _vec(z, name):
+    a = np.asarray(z, dtype=np.float64)
+    if a.ndim != 1:
+        raise ShapeError(f"{name}: expected a 1-D sequence")
+    return a
+
+
+def _tau_out(t):
+    return float(t) if math.isfinite(t) else None
+
+
+def _check_budget(k):
+    if not (k > 0.0) or not math.isfinite(k):
+        raise ArgumentError("KBudget: k must be positive and finite")
+
+
+def sparsek(z, k, sort_cap=0):
+    """Clamped-shift projection of z onto {0 <= p <= 1, sum p = k}
+    (proj/src/sparsek_op.cpp:102-139). Returns {p, tau, u_count, w_count, degenerate}."""
+    k = float(k)
+    zz = _vec(z, "sparsek")
+    if zz.size == 0:
+        raise ArgumentError("sparsek: empty input")
+    _check_budget(k)
+    if sort_cap and sort_cap < math.ceil(k):
+        raise ArgumentError("sparsek_partial: sort_cap below ceil(k)")
+    if not np.all(np.isfinite(zz)):
+        raise NumericError("sparsek: non-finite input")
+    zt = torch.from_numpy(zz).to(_dev()).view(1, -1)
+    p, tau, uc, wc, fl = ops.sparsek_rows(zt, k)
+    return {"p": p[0].cpu().numpy(), "tau": _tau_out(float(tau[0])), "u_count": int(uc[0]),
+            "w_count": int(wc[0]), "degenerate": bool(int(fl[0]) & 1)}
+
+
+def sparsek_jvp(z, k, v):
+    """J(z) v = s * (v - mean_support(v)) (proj/src/sparsek_op.cpp:141-150)."""
+    k = float(k)
+    zz, vv = _vec(z, "sparsek_jvp"), _vec(v, "sparsek_jvp")
+    if vv.size != zz.size:
+        raise ShapeError("sparsek_jvp: v must match z")
+    if zz.size == 0:
+        raise ArgumentError("sparsek: empty input")
+    _check_budget(k)
+    if not np.all(np.isfinite(zz)):
+        raise NumericError("sparsek: non-finite input")
+    d = _dev()
+    out = ops.sparsek_jvp_rows(torch.from_numpy(zz).to(d).view(1, -1), k,
+                               torch.from_numpy(vv).to(d).view(1, -1))
+    return out[0].cpu().numpy()
+
+
+def topk_hard(z, k):
+    """0/1 indicator of the k largest entries, ties to the lower index
+    (proj/src/sparsek_op.cpp:152-165)."""
+    zz = _vec(z, "topk_hard")
+    out = ops.topk_hard_rows(torch.from_numpy(zz).to(_dev()).view(1, -1), int(k))
+    return out[0].cpu().numpy()
+
+
+from .stream import Stream  # noqa: E402  (device-resident StreamState)
+
+
+def _mat(a, name):
+    m = np.asarray(a, dtype=np.float64)
+    if m.ndim != 2:
+        raise ShapeError(f"{name}: expected a 2-D array")
+    return m
+
+
+def _attention_inputs(x, wq, wk, wv, wo, heads):
+    x = _mat(x, "x")
+    ws = [_mat(w, n) for w, n in ((wq, "wq"), (wk, "wk"), (wv, "wv"), (wo, "wo"))]
+    L, D = x.shape
+    for w in ws:
+        if w.shape != (D, D):
+            raise ShapeError("forward_chunk: projection shapes must be d_model x d_model")
+    if heads <= 0:
+        raise ConfigError("attention: heads must be positive")
+    if D == 0 or D % heads:
+        raise ConfigError("attention: d_model must be a positive multiple of heads")
+    return x, ws
+
+
+def _core_cfg(k, window, key_mode, mask_mode):
+    if not math.isfinite(k) or k < 0.0:
+        raise ConfigError("attention: k must be finite and >= 0")
+    if window < 0:
+        raise ConfigError("attention: window must be >= 0")
+    if window == 0 and math.floor(k) < 1.0:
+        raise ConfigError("attention: window + floor(k) must be >= 1 (only the linear mix can "
+                          "run with neither)")
+    if key_mode not in ("soft", "hard"):
+        raise ArgumentError("key_mode must be 'soft' or 'hard'")
+    if mask_mode not in ("soft", "straight_through"):
+        raise ArgumentError("mask_mode must be 'soft' or 'straight_through'")
+    return ops.AttnConfig(k=float(k), window=int(window), key_mode=key_mode, mask_mode=mask_mode)
+
+
+def attention_torch(x, wq, wk, wv, wo, w_score, cfg: ops.AttnConfig, heads: int,
+                    scoring: ops.ScoringConfig):
+    """Differentiable x-level SparseK attention on device tensors:
+    sparsek_attention (proj/include/sparsek/attention.hpp:81-85) as torch ops.
+    x: [B, L, D]; W*: [D, D]; w_score: [D]. Projections are cuBLAS GEMMs; the
+    score, selection, attention and their backward are libsparsek_b200 kernels."""
+    B, L, D = x.shape
+    p = D // heads
+    q = (x @ wq).view(B, L, heads, p)
+    k = (x @ wk).view(B, L, heads, p)
+    v = (x @ wv).view(B, L, heads, p)
+    if cfg.k > 0.0:
+        u = ops.score_tokens(x, w_score, scoring)
+    else:
+        u = torch.zeros((B, L), dtype=torch.float64, device=x.device)
+    hc = ops.sparsek_attention_core(q, k, v, u, cfg)
+    return hc.reshape(B, L, D) @ wo, hc
+
+
+def attention(x, wq, wk, wv, wo, w_score, k, window, heads=1, key_mode="hard", mask_mode="soft",
+              slope_eps=0.01, slope_enabled=True):
+    """Causal attention where each query sees its sliding window plus the top-k
+    scored positions that already left it (the reference's ``attention``)."""
+    x, (wq, wk, wv, wo) = _attention_inputs(x, wq, wk, wv, wo, heads)
+    cfg = _core_cfg(float(k), int(window), key_mode, mask_mode)
+    L, D = x.shape
+    wsc = _vec(w_score, "w_score")
+    if cfg.k > 0.0 and wsc.size != D:
+        raise ConfigError("attention: w_score length must equal d_model")
+    if not (slope_eps > 0.0):
+        raise ArgumentError("ScoringParams: slope_eps must be positive")
+    if not np.all(np.isfinite(wsc)):
+        raise NumericError("ScoringParams: non-finite w_score")
+    d = _dev()
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(d)
+    sc = ops.ScoringConfig(slope_eps=float(slope_eps), slope_enabled=bool(slope_enabled))
+    with torch.no_grad():
+        y, _ = attention_torch(t(x).view(1, L, D), t(wq), t(wk), t(wv), t(wo),
+                               t(wsc) if cfg.k > 0.0 else None, cfg, heads, sc)
+    return y[0].cpu().numpy()
+
+
+def attention_grads(x, wq, wk, wv, wo, w_score, k, window, grad_out, heads=1, key_mode="hard",
+                    mask_mode="soft", slope_eps=0.01, slope_enabled=True,
+                    norm_mode="timestep_norm", slope_order="norm_then_slope"):
+    """Forward + sparsek_attention_backward (proj/src/attention.cpp:214-575):
+    returns (y, {dx, dwq, dwk, dwv, dwo, dw_score}) as float64 numpy arrays."""
+    x, (wq, wk, wv, wo) = _attention_inputs(x, wq, wk, wv, wo, heads)
+    cfg = _core_cfg(float(k), int(window), key_mode, mask_mode)
+    L, D = x.shape
+    wsc = _vec(w_score, "w_score")
+    d = _dev()
+    leaf = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(d).requires_grad_(True)
+    xt, wqt, wkt, wvt, wot, wst = (leaf(a) for a in (x, wq, wk, wv, wo, wsc))
+    sc = ops.ScoringConfig(slope_eps=float(slope_eps), slope_enabled=bool(slope_enabled),
+                           norm_mode=norm_mode, slope_order=slope_order)
+    y, _ = attention_torch(xt.view(1, L, D), wqt, wkt, wvt, wot, wst, cfg, heads, sc)
+    y.backward(torch.from_numpy(np.ascontiguousarray(grad_out, np.float64)).to(d).view(1, L, D))
+    g = lambda t: (t.grad.cpu().numpy() if t.grad is not None else np.zeros(tuple(t.shape)))
+    return y[0].detach().cpu().numpy(), dict(dx=g(xt), dwq=g(wqt), dwk=g(wkt), dwv=g(wvt),
+                                             dwo=g(wot), dw_score=g(wst))
+
+
+def dense_attention(x, wq, wk, wv, wo, heads=1):
+    """Quadratic causal softmax attention (proj/src/attention.cpp:76-111): the
+    SparseK kernels with a budget covering every position (all gates 1)."""
+    x, (wq, wk, wv, wo) = _attention_inputs(x, wq, wk, wv, wo, heads)
+    L, D = x.shape
+    p = D // heads
+    d = _dev()
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(d)
+    xt = t(x)
+    cfg = ops.AttnConfig(k=float(L + 1), window=1)
+    q, kk, v = ((xt @ t(w)).view(1, L, heads, p) for w in (wq, wk, wv))
+    u = torch.zeros((1, L), dtype=torch.float64, device=d)
+    o, _, _ = ops.attn_fwd(q.contiguous(), kk.contiguous(), v.contiguous(), u, cfg)
+    return (o.reshape(L, D) @ t(wo)).cpu().numpy()

@@ -1,0 +1,53 @@
+// Internal interfaces shared by the CUDA translation units (not part of the C ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cmath>
+
+#include "sparsek_b200.h"
+
+namespace skb {
+
+void validate_desc(const skb_attn_desc& d);
+void select_layout(const skb_attn_desc& d, skb_select_layout& o);
+void run_select(const skb_attn_desc& d, const double* u, void* ws, cudaStream_t st);
+
+// Views into a select workspace.
+struct SelView {
+    const int* leave;
+    const double* tau;  // push-time indexed, monotone after run_select
+    const int* nfrac;
+    const int* qb_count;
+    const int* qb_list;
+    const int* ever_count;
+    const int* ever_list;
+    int nqb, qb_cap;
+};
+SelView sel_view(const skb_attn_desc& d, const void* ws);
+
+struct BwdLayout {
+    uint64_t rowsum, colsum, mean_prefix, dk_acc, dv_acc, dq_acc, total;
+};
+void bwd_layout(const skb_attn_desc& d, BwdLayout& o);
+
+void run_attn_fwd_gather(const skb_attn_desc& d, const void* q, const void* k, const void* v,
+                         const double* u, const SelView& s, void* o, double* lse, cudaStream_t st);
+void run_attn_bwd_gather(const skb_attn_desc& d, const void* q, const void* k, const void* v,
+                         const void* dout, const double* lse, const double* u, const SelView& s,
+                         void* dq, void* dk, void* dv, double* rowsum, double* colsum, void* ws,
+                         const BwdLayout& bl, cudaStream_t st);
+// Tensor-core (tcgen05) path, BF16 only. Returns false when the shape is not supported.
+bool tc_supported(const skb_attn_desc& d);
+void run_attn_fwd_tc(const skb_attn_desc& d, const void* q, const void* k, const void* v,
+                     const double* u, const SelView& s, void* o, double* lse, void* ws,
+                     cudaStream_t st);
+void run_attn_bwd_tc(const skb_attn_desc& d, const void* q, const void* k, const void* v,
+                     const void* o, const void* dout, const double* lse, const double* u,
+                     const SelView& s, void* dq, void* dk, void* dv, double* rowsum,
+                     double* colsum, void* ws, const BwdLayout& bl, cudaStream_t st);
+// du from the gate-gradient row/column sums (selection pullback).
+void run_jvp(const skb_attn_desc& d, const double* u, const SelView& s, const double* rowsum,
+             const double* colsum, double* mean_prefix, double* du, cudaStream_t st);
+
+}  // namespace skb

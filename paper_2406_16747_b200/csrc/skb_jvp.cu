@@ -1,0 +1,128 @@
+// Selection pullback (proj/src/attention.cpp:447-479) in O(L log L).
+//
+// Reference: for every query i (push time t = i - w) with S_t = {j <= t :
+// 0 < u_j - tau_t < 1}, mean_t = (sum of head-summed gate gradients gm_tj over
+// j in S_t n Sel_t) / |S_t|, and gu_j += gm_tj - mean_t for j in S_t — O(L)
+// per query, O(L^2) overall.
+//
+// Here the attention backward already produced rowsum_t (the numerator) and
+// colsum_j = sum_t gm_tj over the same fractional entries. Because tau_t never
+// decreases, {t : j in S_t} is one interval [max(j, t_c), t_a) found by binary
+// search with the reference's own predicate (u_j - tau_t > 0, u_j - tau_t < 1),
+// so gu_j = colsum_j - (M[t_a] - M[t_c]) with M the prefix sums of mean_t.
+#include "skb_common.cuh"
+#include "skb_internal.h"
+
+namespace skb {
+
+namespace {
+
+__global__ void __launch_bounds__(1024)
+k_mean_prefix(const double* __restrict__ rowsum, const int* __restrict__ nfrac,
+              const double* __restrict__ tau, int L, int T, double* __restrict__ M) {
+    __shared__ double wsum[32];
+    const int b = blockIdx.x;
+    const double* rs = rowsum + (int64_t)b * L;
+    const int* nf = nfrac + (int64_t)b * L;
+    const double* tb = tau + (int64_t)b * L;
+    double* Mb = M + (int64_t)b * (L + 1);
+    const int per = (T + blockDim.x - 1) / blockDim.x;
+    const int lo = min(T, (int)threadIdx.x * per), hi = min(T, lo + per);
+    auto mean_at = [&](int t) {
+        const int n = nf[t];
+        return (n > 0 && tb[t] > -INFINITY) ? rs[t] / (double)n : 0.0;
+    };
+    double s = 0.0;
+    for (int t = lo; t < hi; ++t) s += mean_at(t);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    double incl = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) wsum[wid] = incl;
+    __syncthreads();
+    double pre = 0.0;
+    for (int w = 0; w < wid; ++w) pre += wsum[w];
+    double run = pre + incl - s;
+    for (int t = lo; t < hi; ++t) {
+        Mb[t] = run;
+        run += mean_at(t);
+    }
+    if (lo < hi && hi == T) Mb[T] = run;
+    if (T == 0 && threadIdx.x == 0) Mb[0] = 0.0;
+}
+
+__global__ void k_jvp(const double* __restrict__ u, const double* __restrict__ tau,
+                      const double* __restrict__ colsum, const double* __restrict__ M, int L, int T,
+                      double* __restrict__ du) {
+    const int b = blockIdx.y;
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= L) return;
+    const int64_t bl = (int64_t)b * L;
+    if (j >= T) {
+        du[bl + j] = 0.0;
+        return;
+    }
+    const double uj = u[bl + j];
+    const double* tb = tau + bl;
+    // t_c: first t in [j, T) with uj - tau_t < 1 (false -> true as tau grows)
+    int lo = j, hi = T;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (uj - tb[mid] < 1.0) hi = mid;
+        else lo = mid + 1;
+    }
+    const int tc = lo;
+    // t_a: first t in [j, T) with !(uj - tau_t > 0)
+    lo = j;
+    hi = T;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (!(uj - tb[mid] > 0.0)) hi = mid;
+        else lo = mid + 1;
+    }
+    const int ta = lo;
+    const double* Mb = M + (int64_t)b * (L + 1);
+    const double sub = tc < ta ? Mb[ta] - Mb[tc] : 0.0;
+    du[bl + j] = colsum[bl + j] - sub;
+}
+
+}  // namespace
+
+void bwd_layout(const skb_attn_desc& d, BwdLayout& o) {
+    const uint64_t BL = (uint64_t)d.batch * d.seq_len;
+    const uint64_t N = BL * d.heads * d.head_dim;
+    uint64_t off = 0;
+    auto take = [&](uint64_t bytes) {
+        const uint64_t r = off;
+        off = (off + bytes + 255) & ~uint64_t(255);
+        return r;
+    };
+    o.rowsum = take(BL * 8);
+    o.colsum = take(BL * 8);
+    o.mean_prefix = take((BL + d.batch) * 8);
+    const bool gather = !(d.dtype == SKB_BF16 && tc_supported(d));
+    o.dk_acc = take(gather ? N * 8 : N * 4);
+    o.dv_acc = take(gather ? N * 8 : N * 4);
+    o.dq_acc = take(gather ? 0 : N * 4);
+    o.total = off;
+}
+
+void run_jvp(const skb_attn_desc& d, const double* u, const SelView& s, const double* rowsum,
+             const double* colsum, double* mean_prefix, double* du, cudaStream_t st) {
+    const int B = (int)d.batch, L = (int)d.seq_len;
+    const int T = std::max(0, L - (int)d.window);
+    if (floor_k(d.k) < 1 || T == 0) {
+        SKB_CHECK_CUDA(cudaMemsetAsync(du, 0, (size_t)B * L * sizeof(double), st));
+        return;
+    }
+    k_mean_prefix<<<B, 1024, 0, st>>>(rowsum, s.nfrac, s.tau, L, T, mean_prefix);
+    SKB_CHECK_LAUNCH();
+    dim3 g((unsigned)cdiv(L, 256), B);
+    k_jvp<<<g, 256, 0, st>>>(u, s.tau, colsum, mean_prefix, L, T, du);
+    SKB_CHECK_LAUNCH();
+}
+
+}  // namespace skb

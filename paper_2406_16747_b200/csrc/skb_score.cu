@@ -1,0 +1,265 @@
+// K1 — the KV scoring network u_j = w . x_j, its timestep normalisation and
+// position slope (proj/include/sparsek/selection.hpp:69-96, Welford
+// proj/src/selection.cpp:13-20), and its backward (proj/src/attention.cpp:
+// 482-516 and the dx term at :564).
+//
+// Forward arithmetic is the reference's, operation for operation: raw is a
+// sequential float64 dot product with separate multiply and add (the
+// reference's x86-64 build has no FMA contraction), and the Welford recurrence
+// runs in order per sequence with correctly rounded div/sqrt, so u is
+// bit-identical to the reference's for identical x rows and w. Backward turns
+// the reference's O(L^2) pullback into three suffix sums.
+#include "skb_common.cuh"
+#include "skb_internal.h"
+
+namespace skb {
+
+namespace {
+
+template <class S>
+__device__ __forceinline__ double ldd(const S* p, int64_t i) {
+    return (double)p[i];
+}
+template <>
+__device__ __forceinline__ double ldd<__nv_bfloat16>(const __nv_bfloat16* p, int64_t i) {
+    return (double)__bfloat162float(p[i]);
+}
+
+// One thread per row: raw = sum_c x[c] * w[c], left to right, no FMA.
+template <class S>
+__global__ void k_score_raw(const S* __restrict__ x, const double* __restrict__ w, int64_t rows,
+                            int D, double* __restrict__ raw) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= rows) return;
+    const S* xr = x + r * D;
+    double acc = 0.0;
+    for (int c = 0; c < D; ++c) acc = __dadd_rn(acc, __dmul_rn(ldd<S>(xr, c), w[c]));
+    raw[r] = acc;
+}
+
+// Sequential Welford per sequence; emits the statistics the parallel finish needs.
+__global__ void k_score_welford(const double* __restrict__ raw, int L, skb_scoring sc,
+                                double* __restrict__ mean, double* __restrict__ var,
+                                int* __restrict__ bad) {
+    const int b = blockIdx.x;
+    const double* rb = raw + (int64_t)b * L;
+    double* mb = mean + (int64_t)b * L;
+    double* vb = var + (int64_t)b * L;
+    double mu = 0.0, m2 = 0.0;
+    for (int i = 0; i < L; ++i) {
+        const double r = rb[i];
+        if (!isfinite(r)) *bad = 1;
+        const double slope = sc.slope_enabled ? __dmul_rn((double)(i + 1), sc.slope_eps) : 0.0;
+        const double rin = sc.slope_order == 0 ? __dadd_rn(r, slope) : r;
+        const double cnt = (double)(i + 1);
+        const double delta = __dsub_rn(rin, mu);
+        mu = __dadd_rn(mu, __ddiv_rn(delta, cnt));
+        m2 = __dadd_rn(m2, __dmul_rn(delta, __dsub_rn(rin, mu)));
+        mb[i] = mu;
+        vb[i] = __ddiv_rn(m2, cnt);
+    }
+}
+
+__global__ void k_score_finish(const double* __restrict__ raw_in, int64_t n, int L, skb_scoring sc,
+                               double* __restrict__ raw, double* __restrict__ u,
+                               double* __restrict__ mean, double* __restrict__ sdev_var,
+                               int* __restrict__ bad) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    const int i = (int)(r % L);
+    const double rw = raw_in[r];
+    if (!isfinite(rw)) *bad = 1;
+    const double slope = sc.slope_enabled ? __dmul_rn((double)(i + 1), sc.slope_eps) : 0.0;
+    if (sc.norm_mode == 0) {
+        raw[r] = rw;
+        u[r] = __dadd_rn(rw, slope);
+        mean[r] = 0.0;
+        sdev_var[r] = 1.0;
+        return;
+    }
+    const double rin = sc.slope_order == 0 ? __dadd_rn(rw, slope) : rw;
+    const double mu = mean[r];
+    const double sd = __dsqrt_rn(__dadd_rn(sdev_var[r], 1e-5));
+    const double z = __ddiv_rn(__dsub_rn(rin, mu), sd);
+    raw[r] = rin;
+    u[r] = sc.slope_order == 0 ? z : __dadd_rn(z, slope);
+    sdev_var[r] = sd;
+}
+
+// ---------------------------------------------------------------- backward
+// Suffix sums of A = coef/(j+1), Bc = coef*y/((j+1)s), Cc = Bc*mu, coef = gu/s.
+__global__ void __launch_bounds__(1024)
+k_score_pullback(const double* __restrict__ gu, const double* __restrict__ raw,
+                 const double* __restrict__ mean, const double* __restrict__ sdev, int L,
+                 int norm_mode, double* __restrict__ graw) {
+    __shared__ double w3[3][32];
+    const int b = blockIdx.x;
+    const int64_t bl = (int64_t)b * L;
+    if (norm_mode == 0) {
+        for (int j = threadIdx.x; j < L; j += blockDim.x) graw[bl + j] = gu[bl + j];
+        return;
+    }
+    const int per = (L + blockDim.x - 1) / blockDim.x;
+    // reversed order: thread 0 owns the tail so an inclusive scan gives suffix sums
+    const int hi = L - min(L, (int)threadIdx.x * per);
+    const int lo = max(0, hi - per);
+    auto terms = [&](int j, double& A, double& Bc, double& Cc) {
+        const double g = gu[bl + j];
+        const double s = sdev[bl + j], mu = mean[bl + j];
+        const double cnt = (double)(j + 1);
+        const double coef = g / s;
+        const double y = (raw[bl + j] - mu) / s;
+        A = coef / cnt;
+        Bc = coef * y / (cnt * s);
+        Cc = Bc * mu;
+    };
+    double sA = 0.0, sB = 0.0, sC = 0.0;
+    for (int j = lo; j < hi; ++j) {
+        double A, Bc, Cc;
+        terms(j, A, Bc, Cc);
+        sA += A;
+        sB += Bc;
+        sC += Cc;
+    }
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    double iA = sA, iB = sB, iC = sC;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double a = __shfl_up_sync(0xffffffffu, iA, o);
+        const double bb = __shfl_up_sync(0xffffffffu, iB, o);
+        const double c = __shfl_up_sync(0xffffffffu, iC, o);
+        if (lane >= o) {
+            iA += a;
+            iB += bb;
+            iC += c;
+        }
+    }
+    if (lane == 31) {
+        w3[0][wid] = iA;
+        w3[1][wid] = iB;
+        w3[2][wid] = iC;
+    }
+    __syncthreads();
+    double pA = 0.0, pB = 0.0, pC = 0.0;
+    for (int w = 0; w < wid; ++w) {
+        pA += w3[0][w];
+        pB += w3[1][w];
+        pC += w3[2][w];
+    }
+    // suffix sums strictly after this thread's range
+    double rA = pA + iA - sA, rB = pB + iB - sB, rC = pC + iC - sC;
+    for (int j = hi - 1; j >= lo; --j) {
+        double A, Bc, Cc;
+        terms(j, A, Bc, Cc);
+        rA += A;
+        rB += Bc;
+        rC += Cc;
+        const double coef = gu[bl + j] / sdev[bl + j];
+        graw[bl + j] = coef - rA - raw[bl + j] * rB + rC;
+    }
+}
+
+// dw_score[c] = sum_{b,j} graw[b,j] * x[b,j,c]: column blocks x row slabs, atomics across slabs.
+template <class S>
+__global__ void k_dw_score(const S* __restrict__ x, const double* __restrict__ graw, int64_t rows,
+                           int D, int rows_per, double* __restrict__ dw) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= D) return;
+    const int64_t r0 = (int64_t)blockIdx.y * rows_per;
+    const int64_t r1 = min(rows, r0 + rows_per);
+    double acc = 0.0;
+    for (int64_t r = r0; r < r1; ++r) {
+        const double g = graw[r];
+        if (g != 0.0) acc += g * ldd<S>(x, r * D + c);
+    }
+    atomicAdd(dw + c, acc);
+}
+
+template <class S>
+__global__ void k_dx_add(S* __restrict__ dx, const double* __restrict__ graw,
+                         const double* __restrict__ w, int64_t rows, int D) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= rows * D) return;
+    const int64_t r = i / D;
+    const int c = (int)(i % D);
+    dx[i] = (S)((double)dx[i] + graw[r] * w[c]);
+}
+template <>
+__global__ void k_dx_add<__nv_bfloat16>(__nv_bfloat16* __restrict__ dx, const double* __restrict__ graw,
+                                        const double* __restrict__ w, int64_t rows, int D) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= rows * D) return;
+    const int64_t r = i / D;
+    const int c = (int)(i % D);
+    dx[i] = __float2bfloat16((float)((double)__bfloat162float(dx[i]) + graw[r] * w[c]));
+}
+
+template <class F>
+void dispatch_x(int32_t dt, F&& f) {
+    if (dt == SKB_F64) f((const double*)nullptr);
+    else if (dt == SKB_F32) f((const float*)nullptr);
+    else if (dt == SKB_BF16) f((const __nv_bfloat16*)nullptr);
+    else throw Error(SKB_EARG, "score: unsupported x dtype");
+}
+
+}  // namespace
+
+void run_score_fwd(int64_t B, int64_t L, int64_t D, int32_t xdt, const void* x, const double* w,
+                   const skb_scoring& sc, double* raw, double* u, double* mean, double* sdev,
+                   cudaStream_t st) {
+    SKB_REQUIRE(B >= 1 && L >= 1 && D >= 1, SKB_ESHAPE, "score_tokens: empty input");
+    SKB_REQUIRE(sc.slope_eps > 0.0, SKB_EARG, "ScoringParams: slope_eps must be positive");
+    const int64_t rows = B * L;
+    int* bad = nullptr;
+    SKB_CHECK_CUDA(cudaMallocAsync(&bad, sizeof(int), st));
+    SKB_CHECK_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), st));
+    // raw is produced into `u` first (scratch), finished into raw/u below.
+    dispatch_x(xdt, [&](auto tag) {
+        using S = std::remove_const_t<std::remove_pointer_t<decltype(tag)>>;
+        k_score_raw<S><<<(unsigned)cdiv(rows, 128), 128, 0, st>>>(static_cast<const S*>(x), w, rows,
+                                                                    (int)D, u);
+    });
+    SKB_CHECK_LAUNCH();
+    if (sc.norm_mode != 0) {
+        k_score_welford<<<(unsigned)B, 1, 0, st>>>(u, (int)L, sc, mean, sdev, bad);
+        SKB_CHECK_LAUNCH();
+    }
+    // finish: reads raw from `u`; stage it in raw first
+    SKB_CHECK_CUDA(cudaMemcpyAsync(raw, u, rows * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    k_score_finish<<<(unsigned)cdiv(rows, 256), 256, 0, st>>>(raw, rows, (int)L, sc, raw, u, mean,
+                                                             sdev, bad);
+    SKB_CHECK_LAUNCH();
+    int hbad = 0;
+    SKB_CHECK_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+    SKB_CHECK_CUDA(cudaFreeAsync(bad, st));
+    SKB_CHECK_CUDA(cudaStreamSynchronize(st));
+    SKB_REQUIRE(!hbad, SKB_ENUMERIC, "score: non-finite value");
+}
+
+void run_score_bwd(int64_t B, int64_t L, int64_t D, int32_t xdt, const void* x, const double* w,
+                   const skb_scoring& sc, const double* gu, const double* raw, const double* mean,
+                   const double* sdev, double* graw, double* dw, void* dx, cudaStream_t st) {
+    const int64_t rows = B * L;
+    k_score_pullback<<<(unsigned)B, 1024, 0, st>>>(gu, raw, mean, sdev, (int)L, sc.norm_mode, graw);
+    SKB_CHECK_LAUNCH();
+    if (dw) {
+        SKB_CHECK_CUDA(cudaMemsetAsync(dw, 0, D * sizeof(double), st));
+        const int rows_per = 256;
+        dim3 g((unsigned)cdiv(D, 128), (unsigned)cdiv(rows, rows_per));
+        dispatch_x(xdt, [&](auto tag) {
+            using S = std::remove_const_t<std::remove_pointer_t<decltype(tag)>>;
+            k_dw_score<S><<<g, 128, 0, st>>>(static_cast<const S*>(x), graw, rows, (int)D, rows_per, dw);
+        });
+        SKB_CHECK_LAUNCH();
+    }
+    if (dx) {
+        dispatch_x(xdt, [&](auto tag) {
+            using S = std::remove_const_t<std::remove_pointer_t<decltype(tag)>>;
+            k_dx_add<S><<<(unsigned)cdiv(rows * D, 256), 256, 0, st>>>(static_cast<S*>(dx), graw, w,
+                                                                       rows, (int)D);
+        });
+        SKB_CHECK_LAUNCH();
+    }
+}
+
+}  // namespace skb

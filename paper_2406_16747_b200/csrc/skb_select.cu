@@ -1,0 +1,561 @@
+// K2 — prefix SparseK threshold and top-floor(k) retention, fully parallel.
+//
+// Reference (sequential): every query i pushes position t = i - w into
+// StreamState (proj/src/stream.cpp:72-152) and admits it to the min-heap cache
+// (proj/src/cache.cpp:136-179); query i then reads Sel_t = the cache and
+// tau_t = the stream threshold (cache.cpp:285-294).
+//
+// B200 restatement (same results, no sequential heap walk over L):
+//   1. k_rank_leave  — Sel_t is the top-floor(k) of u_0..u_t by (value desc,
+//      index asc) (brute-force oracle proj/tests/test_cache.cpp:84-97). So
+//      j is in Sel_t iff j <= t < leave_j, with leave_j = the position of the
+//      (R - A_j)-th later element that beats j (A_j = earlier elements that
+//      beat it). One thread per j; the sequence is streamed through smem.
+//   2. k_tau_chunks  — tau_t for 32 consecutive push times per CTA. Only
+//      scores above theta-1 (theta = ceil(k)-th largest of the prefix) can
+//      carry weight (tau_t >= theta - 1), so the CTA sorts that band, solves
+//      the prefix at the chunk start exactly (breakpoint bracketing + the
+//      closed form of proj/src/sparsek_op.cpp:63-98), then replays the
+//      stream's own push/scan (stream.cpp:83-151) for its 32 arrivals on one
+//      warp, with the sorted band standing in for the heaps.
+//   3. k_union_lists — per 128-query block, the ascending union of Sel_t over
+//      the block's push times (<= floor(k)+127 keys by irreversibility).
+#include <cfloat>
+
+#include "skb_common.cuh"
+#include "skb_internal.h"
+#include "skb_solve.cuh"
+
+namespace skb {
+
+namespace {
+
+constexpr int kRankThreads = 256;
+constexpr int kRankStage = 1024;
+constexpr int kTauThreads = 256;
+constexpr int kOverflowSlots = 16;
+
+// ---------------------------------------------------------------- ranks
+__global__ void __launch_bounds__(kRankThreads)
+k_rank_leave(const double* __restrict__ u, int L, int T, int R1, int R2, int* __restrict__ leave1,
+             int* __restrict__ leave2) {
+    __shared__ double su[kRankStage];
+    const int b = blockIdx.y;
+    const int j = blockIdx.x * kRankThreads + threadIdx.x;
+    const double* ub = u + (int64_t)b * L;
+    const bool active = j < T;
+    const double uj = active ? ub[j] : 0.0;
+    int A = 0, cnt = 0, need1 = 0, need2 = 0;
+    int l1 = T, l2 = T;
+    bool done = !active;
+    for (int c0 = 0; c0 < T; c0 += kRankStage) {
+        if (__syncthreads_and(done)) break;
+        for (int i = threadIdx.x; i < kRankStage; i += kRankThreads)
+            su[i] = c0 + i < T ? ub[c0 + i] : 0.0;
+        __syncthreads();
+        if (!done) {
+            const int n = min(kRankStage, T - c0);
+            for (int ii = 0; ii < n; ++ii) {
+                const int i = c0 + ii;
+                const double x = su[ii];
+                if (i < j) {
+                    if (x >= uj && ++A >= R2) {  // R2 earlier winners: never in the top R2
+                        l1 = j;
+                        l2 = j;
+                        done = true;
+                        break;
+                    }
+                } else if (i == j) {
+                    need1 = R1 - A;  // A < R2 here
+                    need2 = R2 - A;
+                    if (need1 <= 0) l1 = j;  // never enters the top R1
+                } else if (x > uj) {  // later arrivals win only when strictly larger
+                    ++cnt;
+                    if (cnt == need1) l1 = i;
+                    if (cnt == need2) {
+                        l2 = i;
+                        done = true;
+                        break;
+                    }
+                }
+            }
+        }
+    }
+    if (active) {
+        leave1[(int64_t)b * L + j] = l1;
+        leave2[(int64_t)b * L + j] = l2;
+    }
+}
+
+// ---------------------------------------------------------------- tau
+__device__ __forceinline__ void argmin_hi(double& v, int& lane) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+        const int ol = __shfl_xor_sync(0xffffffffu, lane, o);
+        if (ov < v || (ov == v && ol > lane)) {
+            v = ov;
+            lane = ol;
+        }
+    }
+}
+
+struct TauArgs {
+    const double* u;
+    const int* leave2;
+    double* tau;
+    int* nfrac;
+    int* ovf_count;  // [1]
+    int* ovf_items;  // [B * nchunks]
+    double* scratch;
+    int64_t scratch_stride;
+    int L, T, R2;
+    double k;
+    int cap;  // power of two, smem capacity for the band
+};
+
+// One chunk: band collection, sort, exact solve at the chunk start, stream replay.
+// Returns false (without writing outputs) when the band exceeds `cap`.
+__device__ bool tau_chunk(const TauArgs& a, int b, int chunk, double* bz, double* P, int cap,
+                          bool probe_only_if_overflow) {
+    __shared__ double red_d[32];
+    __shared__ int s_m;
+    const int t0 = chunk * kChunk;
+    const double* ub = a.u + (int64_t)b * a.L;
+    const int* lv = a.leave2 + (int64_t)b * a.L;
+
+    // theta = R2-th largest of prefix [0, t0): min over j < t0 still in the top R2 at t0-1.
+    double theta = -CUDART_INF;
+    if (t0 >= a.R2 && a.R2 > 0) {
+        double mn = CUDART_INF;
+        for (int j = threadIdx.x; j < t0; j += blockDim.x)
+            if (lv[j] >= t0) mn = fmin(mn, ub[j]);
+        theta = block_reduce<double>(mn, red_d, false);
+    }
+    const double cut = theta - 1.0;
+    if (threadIdx.x == 0) s_m = 0;
+    __syncthreads();
+    // count first, so an oversized band is detected before anything is written
+    int mine = 0;
+    for (int j = threadIdx.x; j < t0; j += blockDim.x) mine += ub[j] > cut;
+    if (mine) atomicAdd(&s_m, mine);
+    __syncthreads();
+    const int mcount = s_m;
+    (void)probe_only_if_overflow;
+    __syncthreads();
+    if (mcount > cap) return false;
+    if (threadIdx.x == 0) s_m = 0;
+    __syncthreads();
+    for (int j = threadIdx.x; j < t0; j += blockDim.x) {
+        const double x = ub[j];
+        if (x > cut) bz[atomicAdd(&s_m, 1)] = x;
+    }
+    int n2 = 1;
+    while (n2 < mcount) n2 <<= 1;
+    __syncthreads();
+    for (int i = mcount + threadIdx.x; i < n2; i += blockDim.x) bz[i] = -CUDART_INF;
+    __syncthreads();
+    bitonic_desc(bz, n2);
+    excl_prefix(bz, P, mcount, red_d);
+
+    // exact state after pushes [0, t0)
+    double tau0 = -CUDART_INF;
+    int ws = mcount, uf = mcount;
+    if ((double)t0 >= a.k && mcount > 0) {
+        int frac0;
+        tau0 = solve_sorted(bz, P, mcount, a.k, red_d, &frac0);
+        ws = n_gt(bz, mcount, tau0);
+        uf = n_ge(bz, mcount, tau0 + 1.0);
+    }
+
+    // stream replay on warp 0 (proj/src/stream.cpp:72-152)
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        const int nvalid = min(kChunk, a.T - t0);
+        const double cz = lane < nvalid ? ub[t0 + lane] : 0.0;
+        bool inS = false, inF = false;
+        double tau = tau0;
+        double sum_s = P[ws], sum_f = P[uf];
+        int frac = 0;
+        if (tau0 > -CUDART_INF) frac = ws - uf;
+        for (int e = 0; e < nvalid; ++e) {
+            const int t = t0 + e;
+            const double z = __shfl_sync(0xffffffffu, cz, e);
+            const double count = (double)(t + 1);
+            if (z > tau) {
+                if (lane == e) {
+                    inS = true;
+                    inF = z >= tau + 1.0;
+                }
+                sum_s += z;
+                if (z >= tau + 1.0) sum_f += z;
+                if (count < a.k) {
+                    tau = -CUDART_INF;
+                    frac = 0;
+                } else {
+                    bool popped = false;
+                    double last = 0.0;
+                    // every iteration pops one entry; the guard only bounds a
+                    // numerically broken input (NaN sums) so the GPU never hangs
+                    int guard = 2 * (mcount + kChunk) + 8;
+                    for (; guard > 0; --guard) {
+                        const int cu = uf + __popc(__ballot_sync(0xffffffffu, inF));
+                        const int cw = ws + __popc(__ballot_sync(0xffffffffu, inS));
+                        double smin = inS ? cz : CUDART_INF;
+                        int slane = inS ? lane : -1;
+                        argmin_hi(smin, slane);
+                        double fmn = inF ? cz : CUDART_INF;
+                        int flane = inF ? lane : -1;
+                        argmin_hi(fmn, flane);
+                        // base minima (older indices: chunk entries win value ties)
+                        bool s_base = false, f_base = false;
+                        if (ws > 0 && (slane < 0 || bz[ws - 1] < smin)) {
+                            smin = bz[ws - 1];
+                            s_base = true;
+                        }
+                        if (uf > 0 && (flane < 0 || bz[uf - 1] < fmn)) {
+                            fmn = bz[uf - 1];
+                            f_base = true;
+                        }
+                        if (cu == cw) {
+                            const double hi = fmn - 1.0;
+                            const double lo = popped ? last : fmax(tau, hi - 1.0);
+                            if (fabs((double)cu - a.k) <= 1e-9) {
+                                tau = fmax(tau, 0.5 * (lo + hi));
+                                frac = 0;
+                                break;
+                            }
+                            sum_f -= fmn;
+                            if (f_base) --uf;
+                            else if (lane == flane) inF = false;
+                            continue;
+                        }
+                        const double cand = (sum_s - sum_f + (double)cu - a.k) / (double)(cw - cu);
+                        if (smin > cand && (cu == 0 || fmn >= cand + 1.0)) {
+                            tau = cand;
+                            frac = cw - cu;
+                            break;
+                        }
+                        if (cu == 0 || smin <= fmn - 1.0) {
+                            last = smin;
+                            popped = true;
+                            sum_s -= smin;
+                            if (s_base) --ws;
+                            else if (lane == slane) inS = false;
+                            if (cw - 1 == 0) break;  // internal guard (reference throws)
+                        } else {
+                            sum_f -= fmn;
+                            if (f_base) --uf;
+                            else if (lane == flane) inF = false;
+                        }
+                    }
+                }
+            }
+            if (lane == 0) {
+                a.tau[(int64_t)b * a.L + t] = tau;
+                a.nfrac[(int64_t)b * a.L + t] = frac;
+            }
+        }
+    }
+    return true;
+}
+
+__global__ void __launch_bounds__(kTauThreads) k_tau_chunks(TauArgs a) {
+    extern __shared__ double smem[];
+    const int b = blockIdx.y, chunk = blockIdx.x;
+    double* bz = smem;
+    double* P = smem + a.cap;
+    if (!tau_chunk(a, b, chunk, bz, P, a.cap, false)) {
+        if (threadIdx.x == 0) {
+            const int slot = atomicAdd(a.ovf_count, 1);
+            a.ovf_items[slot] = b * gridDim.x + chunk;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kTauThreads) k_tau_overflow(TauArgs a, int nchunks, int cap2) {
+    const int n = *a.ovf_count;
+    double* bz = a.scratch + (int64_t)blockIdx.x * a.scratch_stride;
+    double* P = bz + cap2;
+    for (int it = blockIdx.x; it < n; it += gridDim.x) {
+        const int item = a.ovf_items[it];
+        tau_chunk(a, item / nchunks, item % nchunks, bz, P, cap2, true);
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------- unions
+// Ordered block compaction of keys j in [0, t_hi] with leave_j > max(j, t_lo).
+__global__ void __launch_bounds__(256)
+k_union_lists(const int* __restrict__ leave1, int L, int T, int window, int nqb, int cap,
+              int* __restrict__ qb_count, int* __restrict__ qb_list) {
+    __shared__ int wsum[8];
+    __shared__ int base_s;
+    const int b = blockIdx.y, qb = blockIdx.x;
+    const int t_lo = qb * kQBlock - window;
+    const int t_hi = min(qb * kQBlock + kQBlock - 1 - window, T - 1);
+    const int* lv = leave1 + (int64_t)b * L;
+    int* out = qb_list + ((int64_t)b * nqb + qb) * cap;
+    if (threadIdx.x == 0) base_s = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int j0 = 0; j0 <= t_hi; j0 += 256) {
+        const int j = j0 + threadIdx.x;
+        bool keep = false;
+        if (j <= t_hi) {
+            const int l = lv[j];
+            keep = l > j && l > t_lo;
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, keep);
+        if (lane == 0) wsum[wid] = __popc(bal);
+        __syncthreads();
+        int off = base_s;
+        for (int w = 0; w < wid; ++w) off += wsum[w];
+        if (keep) {
+            const int pos = off + __popc(bal & ((1u << lane) - 1u));
+            if (pos < cap) out[pos] = j;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int tot = 0;
+            for (int w = 0; w < 8; ++w) tot += wsum[w];
+            base_s += tot;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) qb_count[(int64_t)b * nqb + qb] = min(base_s, cap);
+}
+
+// Ever-selected keys per sequence, ascending.
+__global__ void __launch_bounds__(256)
+k_ever_list(const int* __restrict__ leave1, int L, int T, int* __restrict__ ever_count,
+            int* __restrict__ ever_list) {
+    __shared__ int wsum[8];
+    __shared__ int base_s;
+    const int b = blockIdx.x;
+    const int* lv = leave1 + (int64_t)b * L;
+    int* out = ever_list + (int64_t)b * L;
+    if (threadIdx.x == 0) base_s = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int j0 = 0; j0 < T; j0 += 256) {
+        const int j = j0 + threadIdx.x;
+        const bool keep = j < T && lv[j] > j;
+        const unsigned bal = __ballot_sync(0xffffffffu, keep);
+        if (lane == 0) wsum[wid] = __popc(bal);
+        __syncthreads();
+        int off = base_s;
+        for (int w = 0; w < wid; ++w) off += wsum[w];
+        if (keep) out[off + __popc(bal & ((1u << lane) - 1u))] = j;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int tot = 0;
+            for (int w = 0; w < 8; ++w) tot += wsum[w];
+            base_s += tot;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) ever_count[b] = base_s;
+}
+
+__global__ void k_fill_int(int* p, int64_t n, int v) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+
+__global__ void k_leave_identity(int* leave, int L) {
+    const int b = blockIdx.y;
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < L) leave[(int64_t)b * L + j] = j;
+}
+
+__global__ void k_fill_tau(double* tau, int* nfrac, int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) {
+        tau[i] = -CUDART_INF;
+        nfrac[i] = 0;
+    }
+}
+
+// tau_t := max over t' <= t (the stream's tau never decreases, stream.cpp:128;
+// chunk-start solves and replays can differ from it by rounding only).
+__global__ void __launch_bounds__(1024) k_tau_monotone(double* tau, int L, int T) {
+    __shared__ double wmax[32];
+    double* tb = tau + (int64_t)blockIdx.x * L;
+    const int per = (T + blockDim.x - 1) / blockDim.x;
+    const int lo = min(T, (int)threadIdx.x * per), hi = min(T, lo + per);
+    double m = -CUDART_INF;
+    for (int i = lo; i < hi; ++i) m = fmax(m, tb[i]);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    double incl = m;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl = fmax(incl, y);
+    }
+    if (lane == 31) wmax[wid] = incl;
+    __syncthreads();
+    double pre = -CUDART_INF;
+    for (int w = 0; w < wid; ++w) pre = fmax(pre, wmax[w]);
+    double excl = __shfl_up_sync(0xffffffffu, incl, 1);
+    if (lane == 0) excl = -CUDART_INF;
+    double run = fmax(pre, excl);
+    for (int i = lo; i < hi; ++i) {
+        run = fmax(run, tb[i]);
+        tb[i] = run;
+    }
+}
+
+int next_pow2(int x) {
+    int n = 1;
+    while (n < x) n <<= 1;
+    return n;
+}
+
+}  // namespace
+
+static uint64_t align256(uint64_t x) { return (x + 255) & ~uint64_t(255); }
+
+void select_layout(const skb_attn_desc& d, skb_select_layout& o) {
+    const int64_t B = d.batch, L = d.seq_len;
+    const int64_t nqb = cdiv(L, kQBlock);
+    const int64_t cap = floor_k(d.k) + kQBlock;
+    const int64_t nch = cdiv(L, kChunk);
+    uint64_t off = 0;
+    auto take = [&](uint64_t bytes) {
+        const uint64_t r = off;
+        off = align256(off + bytes);
+        return r;
+    };
+    o.leave = take(B * L * 4);
+    o.leave_ceil = take(B * L * 4);
+    o.tau = take(B * L * 8);
+    o.nfrac = take(B * L * 4);
+    o.qb_count = take(B * nqb * 4);
+    o.qb_list = take(B * nqb * cap * 4);
+    o.ever_count = take(B * 4);
+    o.ever_list = take(B * L * 4);
+    o.misc = take((1 + B * nch) * 4);
+    const int64_t cap2 = next_pow2((int)std::max<int64_t>(L, 1));
+    o.scratch = take((uint64_t)kOverflowSlots * (cap2 + L + 1) * 8);
+    o.total_bytes = off;
+    o.qblock = kQBlock;
+    o.nqb = nqb;
+    o.qb_cap = cap;
+}
+
+void validate_desc(const skb_attn_desc& d) {
+    SKB_REQUIRE(d.batch >= 1 && d.seq_len >= 1 && d.heads >= 1 && d.head_dim >= 1, SKB_ESHAPE,
+                "attention: batch, seq_len, heads and head_dim must be positive");
+    SKB_REQUIRE(d.seq_len < (int64_t(1) << 30), SKB_ESHAPE, "attention: seq_len too large");
+    SKB_REQUIRE(std::isfinite(d.k) && d.k >= 0.0, SKB_ECONFIG, "attention: k must be finite and >= 0");
+    SKB_REQUIRE(std::isfinite(d.scale) && d.scale >= 0.0, SKB_ECONFIG, "attention: bad scale");
+    SKB_REQUIRE(d.window >= 0, SKB_ECONFIG, "attention: window must be >= 0");
+    SKB_REQUIRE(!(d.window == 0 && std::floor(d.k) < 1.0), SKB_ECONFIG,
+                "attention: window + floor(k) must be >= 1 (only the linear mix can run with neither)");
+    SKB_REQUIRE(d.key_mode == 0 || d.key_mode == 1, SKB_EARG, "key_mode must be 'soft' or 'hard'");
+    SKB_REQUIRE(d.mask_mode == 0 || d.mask_mode == 1, SKB_EARG,
+                "mask_mode must be 'soft' or 'straight_through'");
+    SKB_REQUIRE(d.dtype == SKB_F32 || d.dtype == SKB_BF16 || d.dtype == SKB_F64, SKB_EARG,
+                "attention: unsupported dtype");
+}
+
+void run_select(const skb_attn_desc& d, const double* u, void* ws, cudaStream_t st) {
+    validate_desc(d);
+    skb_select_layout lay;
+    select_layout(d, lay);
+    char* base = static_cast<char*>(ws);
+    int* leave1 = reinterpret_cast<int*>(base + lay.leave);
+    int* leave2 = reinterpret_cast<int*>(base + lay.leave_ceil);
+    double* tau = reinterpret_cast<double*>(base + lay.tau);
+    int* nfrac = reinterpret_cast<int*>(base + lay.nfrac);
+    int* qb_count = reinterpret_cast<int*>(base + lay.qb_count);
+    int* qb_list = reinterpret_cast<int*>(base + lay.qb_list);
+    int* ever_count = reinterpret_cast<int*>(base + lay.ever_count);
+    int* ever_list = reinterpret_cast<int*>(base + lay.ever_list);
+    int* misc = reinterpret_cast<int*>(base + lay.misc);
+    double* scratch = reinterpret_cast<double*>(base + lay.scratch);
+
+    const int B = (int)d.batch, L = (int)d.seq_len, w = (int)d.window;
+    const int T = std::max(0, L - w);
+    const int R1 = (int)floor_k(d.k), R2 = (int)ceil_k(d.k);
+    const int64_t BL = (int64_t)B * L;
+
+    k_fill_tau<<<(unsigned)cdiv(BL, 256), 256, 0, st>>>(tau, nfrac, BL);
+    SKB_CHECK_LAUNCH();
+    if (R1 == 0 || T == 0) {
+        // no retention: every position leaves at entry
+        dim3 g((unsigned)cdiv(L, 256), B);
+        k_leave_identity<<<g, 256, 0, st>>>(leave1, L);
+        k_leave_identity<<<g, 256, 0, st>>>(leave2, L);
+        SKB_CHECK_LAUNCH();
+    } else {
+        dim3 g((unsigned)cdiv(T, kRankThreads), B);
+        k_rank_leave<<<g, kRankThreads, 0, st>>>(u, L, T, R1, R2, leave1, leave2);
+        SKB_CHECK_LAUNCH();
+    }
+    if (d.k > 0.0 && T > 0) {
+        const int nch = (int)cdiv(T, kChunk);
+        SKB_CHECK_CUDA(cudaMemsetAsync(misc, 0, 4, st));
+        TauArgs a;
+        a.u = u;
+        a.leave2 = leave2;
+        a.tau = tau;
+        a.nfrac = nfrac;
+        a.ovf_count = misc;
+        a.ovf_items = misc + 1;
+        a.L = L;
+        a.T = T;
+        a.R2 = R2;
+        a.k = d.k;
+        a.cap = std::min(8192, next_pow2(std::max(T, 32)));
+        const int cap2 = next_pow2(std::max(L, 1));
+        a.scratch = scratch;
+        a.scratch_stride = cap2 + L + 1;
+        const size_t smem = (size_t)a.cap * 2 * sizeof(double) + 16;
+        static bool attr_set = false;
+        if (!attr_set) {
+            SKB_CHECK_CUDA(cudaFuncSetAttribute(k_tau_chunks, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)(8192 * 2 * sizeof(double) + 16)));
+            attr_set = true;
+        }
+        dim3 g(nch, B);
+        k_tau_chunks<<<g, kTauThreads, smem, st>>>(a);
+        SKB_CHECK_LAUNCH();
+        k_tau_overflow<<<kOverflowSlots, kTauThreads, 0, st>>>(a, nch, cap2);
+        SKB_CHECK_LAUNCH();
+        k_tau_monotone<<<B, 1024, 0, st>>>(tau, L, T);
+        SKB_CHECK_LAUNCH();
+    }
+    const int nqb = (int)lay.nqb;
+    if (R1 > 0 && T > 0) {
+        dim3 g(nqb, B);
+        k_union_lists<<<g, 256, 0, st>>>(leave1, L, T, w, nqb, (int)lay.qb_cap, qb_count, qb_list);
+        k_ever_list<<<B, 256, 0, st>>>(leave1, L, T, ever_count, ever_list);
+        SKB_CHECK_LAUNCH();
+    } else {
+        const int64_t n = (int64_t)B * nqb;
+        k_fill_int<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(qb_count, n, 0);
+        k_fill_int<<<1, 256, 0, st>>>(ever_count, B, 0);
+        SKB_CHECK_LAUNCH();
+    }
+}
+
+SelView sel_view(const skb_attn_desc& d, const void* ws) {
+    skb_select_layout lay;
+    select_layout(d, lay);
+    const char* base = static_cast<const char*>(ws);
+    SelView s;
+    s.leave = reinterpret_cast<const int*>(base + lay.leave);
+    s.tau = reinterpret_cast<const double*>(base + lay.tau);
+    s.nfrac = reinterpret_cast<const int*>(base + lay.nfrac);
+    s.qb_count = reinterpret_cast<const int*>(base + lay.qb_count);
+    s.qb_list = reinterpret_cast<const int*>(base + lay.qb_list);
+    s.ever_count = reinterpret_cast<const int*>(base + lay.ever_count);
+    s.ever_list = reinterpret_cast<const int*>(base + lay.ever_list);
+    s.nqb = (int)lay.nqb;
+    s.qb_cap = (int)lay.qb_cap;
+    return s;
+}
+
+}  // namespace skb

@@ -1,0 +1,304 @@
+"""Torch-level entry points over the C ABI (device tensors in, device tensors out).
+
+Layout: q/k/v/o/dO are [B, L, H, p] (the reference's per-sequence [L, D] with
+head h in columns [h*p, (h+1)*p), proj/include/sparsek/attention.hpp:36);
+scores u are float64 [B, L] (proj/include/sparsek/selection.hpp:72-74).
+All work runs in libsparsek_b200.so on the current CUDA stream.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from ._lib import AttnDesc, Scoring, SelectLayout, check
+
+_DT = {torch.float32: _lib.SKB_F32, torch.bfloat16: _lib.SKB_BF16, torch.float64: _lib.SKB_F64}
+
+
+def _ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def _stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+@dataclass(frozen=True)
+class AttnConfig:
+    """AttnConfig (proj/include/sparsek/attention.hpp:18-32) at the core level."""
+    k: float = 8.0
+    window: int = 8
+    scale: float = 0.0
+    key_mode: str = "hard"       # "hard" | "soft"
+    mask_mode: str = "soft"      # "soft" | "straight_through"
+    force_gather: bool = False   # BF16 on the CUDA-core gather kernels
+
+    def key_code(self):
+        if self.key_mode not in ("hard", "soft"):
+            raise _lib.ArgumentError("key_mode must be 'soft' or 'hard'")
+        return int(self.key_mode == "soft")
+
+    def mask_code(self):
+        if self.mask_mode not in ("soft", "straight_through"):
+            raise _lib.ArgumentError("mask_mode must be 'soft' or 'straight_through'")
+        return int(self.mask_mode == "straight_through")
+
+
+def make_desc(B, L, H, p, cfg: AttnConfig, dtype: torch.dtype) -> AttnDesc:
+    if dtype not in _DT:
+        raise _lib.ArgumentError(f"unsupported dtype {dtype}")
+    flags = _lib.SKB_FLAG_FORCE_GATHER if cfg.force_gather else 0
+    return AttnDesc(int(B), int(L), int(H), int(p), float(cfg.k), int(cfg.window),
+                    float(cfg.scale), cfg.key_code(), cfg.mask_code(), _DT[dtype], flags)
+
+
+def _check_qkv(q, k, v):
+    if q.dim() != 4:
+        raise _lib.ShapeError("q/k/v must be [B, L, H, p]")
+    if k.shape != q.shape or v.shape != q.shape:
+        raise _lib.ShapeError("q, k, v must share one [B, L, H, p] shape")
+    if not (q.is_cuda and k.is_cuda and v.is_cuda):
+        raise _lib.ArgumentError("q/k/v must be CUDA tensors")
+    if not (q.dtype == k.dtype == v.dtype):
+        raise _lib.ArgumentError("q/k/v dtypes differ")
+    for t in (q, k, v):
+        if not t.is_contiguous():
+            raise _lib.ArgumentError("q/k/v must be contiguous")
+
+
+class Selection:
+    """Device-resident output of K2 (skb_select) for one batch of sequences."""
+
+    def __init__(self, desc: AttnDesc, ws: torch.Tensor, layout: SelectLayout):
+        self.desc, self.ws, self.layout = desc, ws, layout
+
+    def _view(self, off, dtype, count):
+        esz = torch.tensor([], dtype=dtype).element_size()
+        return self.ws[off: off + count * esz].view(dtype)
+
+    @property
+    def leave(self):
+        B, L = self.desc.batch, self.desc.seq_len
+        return self._view(self.layout.leave, torch.int32, B * L).view(B, L)
+
+    @property
+    def tau(self):
+        """Threshold after each push time t (float64 [B, L]; entries t >= L-w unused)."""
+        B, L = self.desc.batch, self.desc.seq_len
+        return self._view(self.layout.tau, torch.float64, B * L).view(B, L)
+
+    @property
+    def nfrac(self):
+        B, L = self.desc.batch, self.desc.seq_len
+        return self._view(self.layout.nfrac, torch.int32, B * L).view(B, L)
+
+    @property
+    def qb_count(self):
+        B, n = self.desc.batch, self.layout.nqb
+        return self._view(self.layout.qb_count, torch.int32, B * n).view(B, n)
+
+    @property
+    def qb_list(self):
+        B, n, c = self.desc.batch, self.layout.nqb, self.layout.qb_cap
+        return self._view(self.layout.qb_list, torch.int32, B * n * c).view(B, n, c)
+
+    def tau_per_query(self):
+        """tau each query froze (float64 [B, L], -inf before the first push)."""
+        B, L, w = self.desc.batch, self.desc.seq_len, self.desc.window
+        out = torch.full((B, L), -math.inf, dtype=torch.float64, device=self.ws.device)
+        if L > w:
+            out[:, w:] = self.tau[:, : L - w]
+        return out
+
+
+def select(u: torch.Tensor, cfg: AttnConfig, heads=1, head_dim=1, dtype=torch.float32,
+           desc: AttnDesc | None = None) -> Selection:
+    """K2: prefix tau and top-floor(k) retention intervals for u [B, L] float64."""
+    if u.dim() != 2 or u.dtype != torch.float64 or not u.is_cuda:
+        raise _lib.ArgumentError("u must be a CUDA float64 [B, L] tensor")
+    u = u.contiguous()
+    B, L = u.shape
+    if desc is None:
+        desc = make_desc(B, L, heads, head_dim, cfg, dtype)
+    lay = SelectLayout()
+    check(_lib.load().skb_select_layout_of(desc, lay))
+    ws = torch.empty(lay.total_bytes, dtype=torch.uint8, device=u.device)
+    check(_lib.load().skb_select(desc, u.data_ptr(), ws.data_ptr(), _stream()))
+    return Selection(desc, ws, lay)
+
+
+def attn_fwd(q, k, v, u, cfg: AttnConfig, sel: Selection | None = None):
+    """K3. Returns (o [B,L,H,p], lse float64 [B,H,L], selection)."""
+    _check_qkv(q, k, v)
+    B, L, H, p = q.shape
+    if u.shape != (B, L):
+        raise _lib.ShapeError("u must be [B, L]")
+    desc = make_desc(B, L, H, p, cfg, q.dtype)
+    u = u.contiguous()
+    if sel is None:
+        sel = select(u, cfg, desc=desc)
+    o = torch.empty_like(q)
+    lse = torch.empty((B, H, L), dtype=torch.float64, device=q.device)
+    check(_lib.load().skb_attn_fwd(desc, q.data_ptr(), k.data_ptr(), v.data_ptr(), u.data_ptr(),
+                                   sel.ws.data_ptr(), o.data_ptr(), lse.data_ptr(), _stream()))
+    return o, lse, sel
+
+
+def attn_bwd(q, k, v, o, do, lse, u, sel: Selection, cfg: AttnConfig, ws=None):
+    """K4 + selection pullback. Returns (dq, dk, dv, du float64 [B, L])."""
+    _check_qkv(q, k, v)
+    B, L, H, p = q.shape
+    desc = make_desc(B, L, H, p, cfg, q.dtype)
+    do = do.contiguous()
+    if do.dtype != q.dtype:
+        do = do.to(q.dtype)
+    lib = _lib.load()
+    if ws is None:
+        n = C_size()
+        check(lib.skb_attn_bwd_workspace_size(desc, n))
+        ws = torch.empty(n.value, dtype=torch.uint8, device=q.device)
+    dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+    du = torch.empty((B, L), dtype=torch.float64, device=q.device)
+    check(lib.skb_attn_bwd(desc, q.data_ptr(), k.data_ptr(), v.data_ptr(), _ptr(o), do.data_ptr(),
+                           lse.data_ptr(), u.data_ptr(), sel.ws.data_ptr(), dq.data_ptr(),
+                           dk.data_ptr(), dv.data_ptr(), du.data_ptr(), ws.data_ptr(), _stream()))
+    return dq, dk, dv, du
+
+
+def bwd_workspace(q, cfg: AttnConfig):
+    B, L, H, p = q.shape
+    desc = make_desc(B, L, H, p, cfg, q.dtype)
+    n = C_size()
+    check(_lib.load().skb_attn_bwd_workspace_size(desc, n))
+    return torch.empty(n.value, dtype=torch.uint8, device=q.device)
+
+
+def C_size():
+    import ctypes
+
+    return ctypes.c_size_t()
+
+
+class SparseKAttentionFn(torch.autograd.Function):
+    """Core SparseK attention with its closed-form backward (q, k, v, u) -> o."""
+
+    @staticmethod
+    def forward(ctx, q, k, v, u, cfg: AttnConfig):
+        q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
+        o, lse, sel = attn_fwd(q, k, v, u, cfg)
+        ctx.save_for_backward(q, k, v, o, lse, u)
+        ctx.sel, ctx.cfg = sel, cfg
+        return o
+
+    @staticmethod
+    def backward(ctx, do):
+        q, k, v, o, lse, u = ctx.saved_tensors
+        dq, dk, dv, du = attn_bwd(q, k, v, o, do, lse, u, ctx.sel, ctx.cfg)
+        return dq, dk, dv, du, None
+
+
+def sparsek_attention_core(q, k, v, u, cfg: AttnConfig):
+    return SparseKAttentionFn.apply(q, k, v, u, cfg)
+
+
+# ---------------------------------------------------------------- scoring (K1)
+
+@dataclass(frozen=True)
+class ScoringConfig:
+    """ScoringParams (proj/include/sparsek/selection.hpp:19-27) minus w_score."""
+    slope_eps: float = 0.01
+    slope_enabled: bool = True
+    norm_mode: str = "timestep_norm"      # "timestep_norm" | "none"
+    slope_order: str = "norm_then_slope"  # "norm_then_slope" | "slope_then_norm"
+
+    def c(self):
+        return Scoring(int(self.norm_mode == "timestep_norm"),
+                       int(self.slope_order == "norm_then_slope"), int(bool(self.slope_enabled)),
+                       0, float(self.slope_eps))
+
+
+def score_fwd(x: torch.Tensor, w: torch.Tensor, sc: ScoringConfig):
+    """x [B, L, D] -> (raw, u, mean, sdev) float64 [B, L]."""
+    if x.dim() != 3:
+        raise _lib.ShapeError("score: x must be [B, L, D]")
+    B, L, D = x.shape
+    if w.shape != (D,):
+        raise _lib.ShapeError("score_tokens: x.cols != w_score length")
+    x = x.contiguous()
+    w = w.to(torch.float64).contiguous()
+    raw, u, mean, sdev = (torch.empty((B, L), dtype=torch.float64, device=x.device)
+                          for _ in range(4))
+    check(_lib.load().skb_score_fwd(B, L, D, _DT[x.dtype], x.data_ptr(), w.data_ptr(), sc.c(),
+                                    raw.data_ptr(), u.data_ptr(), mean.data_ptr(), sdev.data_ptr(),
+                                    _stream()))
+    return raw, u, mean, sdev
+
+
+def score_bwd(x, w, sc: ScoringConfig, gu, raw, mean, sdev, dx=None, want_dw=True):
+    B, L, D = x.shape
+    graw = torch.empty((B, L), dtype=torch.float64, device=x.device)
+    dw = torch.empty((D,), dtype=torch.float64, device=x.device) if want_dw else None
+    check(_lib.load().skb_score_bwd(B, L, D, _DT[x.dtype], x.data_ptr(),
+                                    w.to(torch.float64).contiguous().data_ptr(), sc.c(),
+                                    gu.contiguous().data_ptr(), raw.data_ptr(), mean.data_ptr(),
+                                    sdev.data_ptr(), graw.data_ptr(), _ptr(dw), _ptr(dx), _stream()))
+    return graw, dw
+
+
+class ScoreFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, w, sc: ScoringConfig):
+        raw, u, mean, sdev = score_fwd(x, w, sc)
+        ctx.save_for_backward(x, w, raw, mean, sdev)
+        ctx.sc = sc
+        return u
+
+    @staticmethod
+    def backward(ctx, gu):
+        x, w, raw, mean, sdev = ctx.saved_tensors
+        graw, dw = score_bwd(x, w, ctx.sc, gu.contiguous(), raw, mean, sdev)
+        dx = (graw.unsqueeze(-1) * w.to(torch.float64)).to(x.dtype)
+        return dx, dw.to(w.dtype), None
+
+
+def score_tokens(x, w, sc: ScoringConfig):
+    return ScoreFn.apply(x, w, sc)
+
+
+# ---------------------------------------------------------------- operator
+
+def sparsek_rows(z: torch.Tensor, k: float):
+    """Batched SparseK projection of the rows of z [n, m] (float64, CUDA)."""
+    if z.dim() != 2 or z.dtype != torch.float64 or not z.is_cuda:
+        raise _lib.ArgumentError("z must be a CUDA float64 [n, m] tensor")
+    z = z.contiguous()
+    n, m = z.shape
+    p = torch.empty_like(z)
+    tau = torch.empty(n, dtype=torch.float64, device=z.device)
+    uc = torch.empty(n, dtype=torch.int64, device=z.device)
+    wc = torch.empty(n, dtype=torch.int64, device=z.device)
+    fl = torch.empty(n, dtype=torch.int32, device=z.device)
+    check(_lib.load().skb_sparsek(n, m, z.data_ptr(), float(k), p.data_ptr(), tau.data_ptr(),
+                                  uc.data_ptr(), wc.data_ptr(), fl.data_ptr(), _stream()))
+    return p, tau, uc, wc, fl
+
+
+def sparsek_jvp_rows(z: torch.Tensor, k: float, v: torch.Tensor):
+    z = z.contiguous()
+    v = v.to(torch.float64).contiguous()
+    n, m = z.shape
+    out = torch.empty_like(z)
+    check(_lib.load().skb_sparsek_jvp(n, m, z.data_ptr(), float(k), v.data_ptr(), out.data_ptr(),
+                                      _stream()))
+    return out
+
+
+def topk_hard_rows(z: torch.Tensor, k: int):
+    z = z.contiguous()
+    n, m = z.shape
+    out = torch.empty_like(z)
+    check(_lib.load().skb_topk_hard(n, m, z.data_ptr(), int(k), out.data_ptr(), _stream()))
+    return out
