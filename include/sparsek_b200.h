@@ -97,6 +97,8 @@ typedef struct skb_select_layout {
     uint64_t ever_list;   /* int32  [B, L] ever-selected keys, ascending */
     uint64_t misc;        /* int32 scratch (overflow queue) */
     uint64_t scratch;     /* double scratch (overflow chunks) */
+    uint64_t uf;          /* float  [B, L]  u as fp32 (tensor-core gates)    */
+    uint64_t tauf;        /* float  [B, L]  tau as fp32 (push time)          */
     uint64_t total_bytes;
     int64_t qblock;       /* queries per block (128)       */
     int64_t nqb;          /* ceil(L / qblock)              */

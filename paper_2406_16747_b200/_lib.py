@@ -63,7 +63,8 @@ class SelectLayout(C.Structure):
     _fields_ = [("leave", C.c_uint64), ("leave_ceil", C.c_uint64), ("tau", C.c_uint64),
                 ("nfrac", C.c_uint64), ("qb_count", C.c_uint64), ("qb_list", C.c_uint64),
                 ("ever_count", C.c_uint64), ("ever_list", C.c_uint64), ("misc", C.c_uint64),
-                ("scratch", C.c_uint64), ("total_bytes", C.c_uint64), ("qblock", C.c_int64),
+                ("scratch", C.c_uint64), ("uf", C.c_uint64), ("tauf", C.c_uint64),
+                ("total_bytes", C.c_uint64), ("qblock", C.c_int64),
                 ("nqb", C.c_int64), ("qb_cap", C.c_int64)]
 
 

@@ -1,28 +1,376 @@
-// K3/K4 tensor-core path (tcgen05 + TMEM) — BF16 only. See DESIGN.md.
+// K3/K4 tensor-core path (tcgen05 + TMEM), BF16, head_dim 64 or 128.
+//
+// Forward (k_fwd_tc): one CTA per (128-query block, head, sequence).
+//   key tiles = [selected-union tiles (gathered rows, per-key interval mask
+//   j <= t_i < leave_j and value gates g = sat(u_j - tau_i))] ++ [window
+//   tiles (contiguous band [i0-w+1, i0+127], causal/window mask)].
+//   Per tile: S = Q K^T (tcgen05, M=N=128, K=d, fp32 in TMEM) ->
+//   softmax warps (one query row per thread): mask, online max with lazy
+//   rescale (only when the max grows by > 2^8), P = exp2(...), gated P~ =
+//   P*g -> bf16 P~ in swizzled smem -> O += P~ V (tcgen05, accumulator in
+//   TMEM). Softmax statistics use the ungated P (proj/src/cache.cpp:373-387:
+//   softmax over Sel U W, value gates applied after, no renormalisation).
+//
+// Warp roles (256 threads): warps 0-3 softmax/epilogue, warps 4-6 producers
+// (cp.async row gathers into 128B-swizzled tiles, completion tracked by
+// mbarriers), warp 7 TMEM owner + single-thread MMA issuer.
 #include "skb_common.cuh"
 #include "skb_internal.h"
+#include "skb_tc.cuh"
 
 namespace skb {
 
+namespace {
+
+using namespace tc;
+
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+constexpr float kRescaleSlack = 8.0f;  // lazy rescale threshold (log2 units)
+
+struct FwdArgs {
+    const __nv_bfloat16* q;
+    const __nv_bfloat16* k;
+    const __nv_bfloat16* v;
+    __nv_bfloat16* o;
+    double* lse;
+    const float* uf;
+    const float* tauf;
+    const int* leave;
+    const int* qb_count;
+    const int* qb_list;
+    int nqb, qb_cap;
+    int B, L, H, w, T, R1;
+    float scale_log2;
+    float scale;
+    int mask_st;
+};
+
+template <int D>
+struct FwdSmem {
+    static constexpr int kTile = 128 * D * 2;  // bytes of a 128-row bf16 tile
+    static constexpr int kQ = 0;
+    static constexpr int kK = kQ + kTile;
+    static constexpr int kV = kK + 2 * kTile;
+    static constexpr int kP = kV + 2 * kTile;
+    static constexpr int kMeta = kP + 128 * 128 * 2;   // [2][3][128] x 4 B
+    static constexpr int kBar = kMeta + 2 * 3 * 128 * 4;
+    static constexpr int kTmemSlot = kBar + 16 * 8;
+    static constexpr int kBytes = kTmemSlot + 16;
+    static constexpr int kAlloc = kBytes + 1024;  // room to align the base to 1024
+};
+
+enum { B_QFULL = 0, B_KVFULL = 1, B_KVEMPTY = 3, B_SFULL = 5, B_SEMPTY = 7, B_PFULL = 9, B_PVDONE = 10 };
+
+template <int D, bool KEY_SOFT>
+__global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
+    using SM = FwdSmem<D>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const uint32_t sbase = smem_u32(smem);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SM::kBar);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + SM::kTmemSlot);
+    int* meta = reinterpret_cast<int*>(smem + SM::kMeta);  // [stage][key|leave|uf][128]
+
+    const int qb = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int i0 = qb * 128;
+    const int cnt = (a.R1 > 0) ? a.qb_count[(int64_t)b * a.nqb + qb] : 0;
+    const int n_sel = (cnt + 127) / 128;
+    const int n_win = (a.w + 127 + 127) / 128;
+    const int n = n_sel + n_win;
+    const int jw0 = i0 - a.w + 1;  // first key of the window band
+    const int* list = a.qb_list + ((int64_t)b * a.nqb + qb) * a.qb_cap;
+
+    if (threadIdx.x == 0) {
+        mbar_init(&bars[B_QFULL], kProducers);
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&bars[B_KVFULL + s], kProducers);
+            mbar_init(&bars[B_KVEMPTY + s], 1);
+            mbar_init(&bars[B_SFULL + s], 1);
+            mbar_init(&bars[B_SEMPTY + s], 128);
+        }
+        mbar_init(&bars[B_PFULL], 128);
+        mbar_init(&bars[B_PVDONE], 1);
+        mbar_fence_init();
+    }
+    if (warp == 7) tmem_alloc<512>(tmem_slot);
+    tc_before_sync();
+    __syncthreads();
+    tc_after_sync();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t tS = tmem, tO = tmem + 256;
+
+    if (warp >= 4 && warp < 7) {
+        // ------------------------------------------------------------ producers
+        const int pw = warp - 4, ptid = threadIdx.x - 128;
+        load_tile<D, 128>(sbase + SM::kQ, a.q, b, h, a.L, a.H, pw, lane, [&](int r) {
+            return i0 + r < a.L ? i0 + r : -1;
+        });
+        cp_async_arrive_noinc(&bars[B_QFULL]);
+        for (int jt = 0; jt < n; ++jt) {
+            const int s = jt & 1;
+            if (jt >= 2) mbar_wait(&bars[B_KVEMPTY + s], ((jt - 2) >> 1) & 1);
+            if (jt < n_sel) {
+                // metadata (key, leave_j, u_j) for the softmax warps, via cp.async so
+                // the stage's single completion barrier covers it
+                for (int c = ptid; c < 128; c += kProducers) {
+                    const int idx = jt * 128 + c;
+                    const int key = idx < cnt ? __ldg(list + idx) : -1;
+                    const uint32_t mb = smem_u32(meta + (s * 3) * 128 + c);
+                    cp_async4(mb, list + (idx < cnt ? idx : 0), idx < cnt);
+                    cp_async4(mb + 128 * 4, a.leave + (int64_t)b * a.L + (key >= 0 ? key : 0), key >= 0);
+                    cp_async4(mb + 256 * 4, a.uf + (int64_t)b * a.L + (key >= 0 ? key : 0), key >= 0);
+                }
+                auto kf = [&](int r) {
+                    const int idx = jt * 128 + r;
+                    return idx < cnt ? __ldg(list + idx) : -1;
+                };
+                load_tile<D, 128>(sbase + SM::kK + s * SM::kTile, a.k, b, h, a.L, a.H, pw, lane, kf);
+                load_tile<D, 128>(sbase + SM::kV + s * SM::kTile, a.v, b, h, a.L, a.H, pw, lane, kf);
+            } else {
+                const int kb0 = jw0 + (jt - n_sel) * 128;
+                auto kf = [&](int r) { return kb0 + r; };
+                load_tile<D, 128>(sbase + SM::kK + s * SM::kTile, a.k, b, h, a.L, a.H, pw, lane, kf);
+                load_tile<D, 128>(sbase + SM::kV + s * SM::kTile, a.v, b, h, a.L, a.H, pw, lane, kf);
+            }
+            cp_async_arrive_noinc(&bars[B_KVFULL + s]);
+        }
+    } else if (warp == 7) {
+        // ------------------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            constexpr uint32_t idesc_qk = umma_idesc(128, 128, false, false);
+            constexpr uint32_t idesc_pv = umma_idesc(128, D, false, true);
+            mbar_wait(&bars[B_QFULL], 0);
+            fence_proxy_async();
+            auto pv = [&](int j) {
+                mbar_wait(&bars[B_PFULL], j & 1);
+                tc_after_sync();
+                const uint32_t vb = sbase + SM::kV + (j & 1) * SM::kTile;
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk)
+                    umma_f16(tO, desc_kmajor(sbase + SM::kP, 128, kk), desc_mnmajor(vb, 128, kk), idesc_pv,
+                             (j > 0 || kk > 0) ? 1u : 0u);
+                umma_commit(&bars[B_PVDONE]);
+                umma_commit(&bars[B_KVEMPTY + (j & 1)]);
+            };
+            for (int jt = 0; jt < n; ++jt) {
+                const int s = jt & 1;
+                mbar_wait(&bars[B_KVFULL + s], (jt >> 1) & 1);
+                fence_proxy_async();
+                if (jt >= 2) mbar_wait(&bars[B_SEMPTY + s], ((jt - 2) >> 1) & 1);
+                tc_after_sync();
+                const uint32_t kb = sbase + SM::kK + s * SM::kTile;
+#pragma unroll
+                for (int kk = 0; kk < D / 16; ++kk)
+                    umma_f16(tS + s * 128, desc_kmajor(sbase + SM::kQ, 128, kk), desc_kmajor(kb, 128, kk),
+                             idesc_qk, kk > 0 ? 1u : 0u);
+                umma_commit(&bars[B_SFULL + s]);
+                if (jt >= 1) pv(jt - 1);
+            }
+            pv(n - 1);
+        }
+        __syncwarp();
+    } else {
+        // ------------------------------------------------------------ softmax (warps 0-3)
+        const int r = threadIdx.x;
+        const int i = i0 + r;
+        const int t = i - a.w;
+        const float tau_i = (t >= 0 && a.R1 > 0) ? a.tauf[(int64_t)b * a.L + t] : -INFINITY;
+        const int lo_win = i - a.w + 1;
+        const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+        float m = -INFINITY, l = 0.f;
+        float sv[128];
+        for (int jt = 0; jt < n; ++jt) {
+            const int s = jt & 1;
+            const bool is_sel = jt < n_sel;
+            mbar_wait(&bars[B_SFULL + s], (jt >> 1) & 1);
+            mbar_wait(&bars[B_KVFULL + s], (jt >> 1) & 1);  // metadata visibility
+            tc_after_sync();
+#pragma unroll
+            for (int c = 0; c < 4; ++c) tmem_ld32(tS + lane_off + s * 128 + c * 32, sv + c * 32);
+            tmem_wait_ld();
+            tc_before_sync();
+            mbar_arrive(&bars[B_SEMPTY + s]);
+
+            const int* mk = meta + (s * 3) * 128;
+            const int* ml = mk + 128;
+            const float* mu = reinterpret_cast<const float*>(mk + 256);
+            float mt = -INFINITY;
+            if (is_sel) {
+#pragma unroll
+                for (int c = 0; c < 128; c += 4) {
+                    const int4 kj = *reinterpret_cast<const int4*>(mk + c);
+                    const int4 lv = *reinterpret_cast<const int4*>(ml + c);
+                    const float4 uu = *reinterpret_cast<const float4*>(mu + c);
+                    const int kja[4] = {kj.x, kj.y, kj.z, kj.w};
+                    const int lva[4] = {lv.x, lv.y, lv.z, lv.w};
+                    const float ua[4] = {uu.x, uu.y, uu.z, uu.w};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const bool ok = kja[e] >= 0 && kja[e] <= t && lva[e] > t;
+                        float x = sv[c + e];
+                        if (KEY_SOFT) x *= __saturatef(ua[e] - tau_i);
+                        x = ok ? x * a.scale_log2 : -INFINITY;
+                        sv[c + e] = x;
+                        mt = fmaxf(mt, x);
+                    }
+                }
+            } else {
+                const int kbase = jw0 + (jt - n_sel) * 128;
+#pragma unroll
+                for (int c = 0; c < 128; ++c) {
+                    const int key = kbase + c;
+                    const bool ok = key >= 0 && key >= lo_win && key <= i;
+                    const float x = ok ? sv[c] * a.scale_log2 : -INFINITY;
+                    sv[c] = x;
+                    mt = fmaxf(mt, x);
+                }
+            }
+            // lazy rescale: move the exponent base only when the max grows by > 2^8
+            float fac = 1.f;
+            bool need = false;
+            if (mt > m + kRescaleSlack) {
+                if (l > 0.f) {
+                    fac = ex2(m - mt);
+                    l *= fac;
+                    need = true;
+                }
+                m = mt;
+            }
+            float psum = 0.f;
+#pragma unroll
+            for (int c = 0; c < 128; ++c) {
+                const float p = ex2(sv[c] - m);  // exp2(-inf) = 0 for masked keys
+                psum += p;
+                sv[c] = p;
+            }
+            l += psum;
+            if (is_sel && !a.mask_st) {
+#pragma unroll
+                for (int c = 0; c < 128; c += 4) {
+                    const float4 uu = *reinterpret_cast<const float4*>(mu + c);
+                    sv[c + 0] *= __saturatef(uu.x - tau_i);
+                    sv[c + 1] *= __saturatef(uu.y - tau_i);
+                    sv[c + 2] *= __saturatef(uu.z - tau_i);
+                    sv[c + 3] *= __saturatef(uu.w - tau_i);
+                }
+            }
+            if (jt >= 1) {
+                mbar_wait(&bars[B_PVDONE], (jt - 1) & 1);
+                tc_after_sync();
+            }
+            if (__any_sync(0xffffffffu, need)) {
+                float ov[32];
+#pragma unroll
+                for (int c = 0; c < D / 32; ++c) {
+                    const uint32_t ta = tO + lane_off + c * 32;
+                    tmem_ld32(ta, ov);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) ov[e] *= fac;
+                    tmem_st32(ta, ov);
+                }
+                tmem_wait_st();
+            }
+            // P~ row -> swizzled smem (K-major A operand of the PV MMA)
+            const uint32_t prow = sbase + SM::kP;
+#pragma unroll
+            for (int ch = 0; ch < 16; ++ch) {
+                const float* x = sv + ch * 8;
+                st_shared_v4(prow + sw_off(r, ch, 128), pack_bf16(x[0], x[1]), pack_bf16(x[2], x[3]),
+                             pack_bf16(x[4], x[5]), pack_bf16(x[6], x[7]));
+            }
+            fence_proxy_async();
+            tc_before_sync();
+            mbar_arrive(&bars[B_PFULL]);
+        }
+        // epilogue: O / l, lse
+        mbar_wait(&bars[B_PVDONE], (n - 1) & 1);
+        tc_after_sync();
+        const float inv = l > 0.f ? 1.f / l : 0.f;
+        __nv_bfloat16* orow = a.o + (((int64_t)b * a.L + i) * a.H + h) * D;
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) {
+            float ov[32];
+            tmem_ld32(tO + lane_off + c * 32, ov);
+            tmem_wait_ld();
+            if (i < a.L) {
+#pragma unroll
+                for (int e = 0; e < 32; e += 8) {
+                    uint4 pk;
+                    pk.x = pack_bf16(ov[e] * inv, ov[e + 1] * inv);
+                    pk.y = pack_bf16(ov[e + 2] * inv, ov[e + 3] * inv);
+                    pk.z = pack_bf16(ov[e + 4] * inv, ov[e + 5] * inv);
+                    pk.w = pack_bf16(ov[e + 6] * inv, ov[e + 7] * inv);
+                    *reinterpret_cast<uint4*>(orow + c * 32 + e) = pk;
+                }
+            }
+        }
+        if (i < a.L) a.lse[((int64_t)b * a.H + h) * a.L + i] = (double)((m + __log2f(l)) * kLn2);
+    }
+    tc_before_sync();
+    __syncthreads();
+    tc_after_sync();
+    if (warp == 7) tmem_dealloc<512>(tmem);
+}
+
+template <int D, bool KS>
+void launch_fwd(const FwdArgs& a, dim3 grid, cudaStream_t st) {
+    using SM = FwdSmem<D>;
+    static bool attr = false;
+    if (!attr) {
+        SKB_CHECK_CUDA(cudaFuncSetAttribute(k_fwd_tc<D, KS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            SM::kAlloc));
+        attr = true;
+    }
+    k_fwd_tc<D, KS><<<grid, kThreads, SM::kAlloc, st>>>(a);
+    SKB_CHECK_LAUNCH();
+}
+
+}  // namespace
+
 bool tc_supported(const skb_attn_desc& d) {
-    (void)d;
-    return false;  // enabled once the tcgen05 kernels land
+    return d.dtype == SKB_BF16 && (d.head_dim == 64 || d.head_dim == 128) && d.window >= 1 &&
+           d.seq_len >= 1;
 }
 
 void run_attn_fwd_tc(const skb_attn_desc& d, const void* q, const void* k, const void* v,
                      const double* u, const SelView& s, void* o, double* lse, void* ws,
                      cudaStream_t st) {
-    (void)d; (void)q; (void)k; (void)v; (void)u; (void)s; (void)o; (void)lse; (void)ws; (void)st;
-    throw Error(SKB_ECONFIG, "tensor-core path unavailable for this shape");
-}
-
-void run_attn_bwd_tc(const skb_attn_desc& d, const void* q, const void* k, const void* v,
-                     const void* o, const void* dout, const double* lse, const double* u,
-                     const SelView& s, void* dq, void* dk, void* dv, double* rowsum,
-                     double* colsum, void* ws, const BwdLayout& bl, cudaStream_t st) {
-    (void)d; (void)q; (void)k; (void)v; (void)o; (void)dout; (void)lse; (void)u; (void)s;
-    (void)dq; (void)dk; (void)dv; (void)rowsum; (void)colsum; (void)ws; (void)bl; (void)st;
-    throw Error(SKB_ECONFIG, "tensor-core path unavailable for this shape");
+    (void)u;
+    (void)ws;
+    FwdArgs a{};
+    a.q = static_cast<const __nv_bfloat16*>(q);
+    a.k = static_cast<const __nv_bfloat16*>(k);
+    a.v = static_cast<const __nv_bfloat16*>(v);
+    a.o = static_cast<__nv_bfloat16*>(o);
+    a.lse = lse;
+    a.uf = s.uf;
+    a.tauf = s.tauf;
+    a.leave = s.leave;
+    a.qb_count = s.qb_count;
+    a.qb_list = s.qb_list;
+    a.nqb = s.nqb;
+    a.qb_cap = s.qb_cap;
+    a.B = (int)d.batch;
+    a.L = (int)d.seq_len;
+    a.H = (int)d.heads;
+    a.w = (int)d.window;
+    a.T = std::max(0, a.L - a.w);
+    a.R1 = (int)floor_k(d.k);
+    const double scale = d.scale > 0.0 ? d.scale : 1.0 / std::sqrt((double)d.head_dim);
+    a.scale = (float)scale;
+    a.scale_log2 = (float)(scale * 1.4426950408889634);
+    a.mask_st = d.mask_mode;
+    dim3 grid((unsigned)s.nqb, (unsigned)d.heads, (unsigned)d.batch);
+    if (d.head_dim == 128) {
+        if (d.key_mode) launch_fwd<128, true>(a, grid, st);
+        else launch_fwd<128, false>(a, grid, st);
+    } else {
+        if (d.key_mode) launch_fwd<64, true>(a, grid, st);
+        else launch_fwd<64, false>(a, grid, st);
+    }
 }
 
 }  // namespace skb

@@ -1,0 +1,698 @@
+// K4 tensor-core backward (tcgen05 + TMEM), BF16, head_dim 64 or 128.
+//
+// sparsek_attention_backward's core (proj/src/attention.cpp:265-316) as three
+// kernels over the same selection products as the forward:
+//   k_bwd_prep     lse in log2 units and delta_i = dO_i . O_i (the reference's
+//                  s = sum_j P_ij wv_ij b_ij equals dO_i . O_i).
+//   k_bwd_dkdv_tc  key-major: a CTA owns 128 keys — a contiguous window tile
+//                  or 128 entries of the ever-selected list — and walks the
+//                  64-query tiles that read them (window: [j, j+w); selected:
+//                  [j+w, leave_j+w)). S^T = K Q^T and dP^T = V dO^T in TMEM
+//                  (double-buffered), elementwise P~^T / dS^T to smem, then
+//                  dV += P~^T dO and dK += dS^T Q accumulate in TMEM. The
+//                  selected pass stores fp32 partials, the window pass adds
+//                  them and writes bf16. colsum_j (gate gradient over the
+//                  fractional support, summed over heads) is per thread.
+//   k_bwd_dq_tc    query-major over 64-key tiles: dQ = dS K accumulates in
+//                  TMEM; rowsum_t (the pullback numerator) is per thread.
+// rowsum/colsum feed the O(L log L) selection pullback (skb_jvp.cu).
+#include "skb_common.cuh"
+#include "skb_internal.h"
+#include "skb_tc.cuh"
+
+namespace skb {
+
+namespace {
+
+using namespace tc;
+
+struct BwdArgs {
+    const __nv_bfloat16 *q, *k, *v, *dout;
+    __nv_bfloat16 *dq, *dk, *dv;
+    float *dk_acc, *dv_acc;  // fp32 partials of the selected pass, [B, L, H, D]
+    const float* lse2;       // [B, H, L] lse * log2(e)
+    const float* delta;      // [B, H, L] rowsum(dO * O)
+    const float* uf;
+    const float* tauf;
+    const int* leave;
+    const int* qb_count;
+    const int* qb_list;
+    const int* ever_count;
+    const int* ever_list;
+    double *rowsum, *colsum;
+    int nqb, qb_cap;
+    int B, L, H, w, T, R1;
+    float scale, scale_log2;
+    int mask_st;
+};
+
+template <int D>
+__global__ void k_bwd_prep(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
+                           const double* __restrict__ lse, float* __restrict__ lse2,
+                           float* __restrict__ delta, int B, int L, int H) {
+    const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;  // (b, i, h)
+    const int lane = threadIdx.x & 31;
+    if (row >= (int64_t)B * L * H) return;
+    const __nv_bfloat16* orow = o + row * D;
+    const __nv_bfloat16* grow = dout + row * D;
+    float acc = 0.f;
+    for (int c = lane * 2; c < D; c += 64) {
+        const float2 x = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(orow + c));
+        const float2 g = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(grow + c));
+        acc += x.x * g.x + x.y * g.y;
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) {
+        const int h = (int)(row % H);
+        const int64_t bi = row / H;
+        const int i = (int)(bi % L), b = (int)(bi / L);
+        const int64_t o2 = ((int64_t)b * H + h) * L + i;
+        delta[o2] = acc;
+        lse2[o2] = (float)(lse[o2] * 1.4426950408889634);
+    }
+}
+
+// ------------------------------------------------------------------ dK / dV
+template <int D>
+struct KSmem {
+    static constexpr int kKV = 128 * D * 2;  // 128-key tile
+    static constexpr int kQT = 64 * D * 2;   // 64-query tile
+    static constexpr int kPD = 128 * 64 * 2; // 128 x 64 bf16 (P~^T or dS^T)
+    static constexpr int kK = 0;
+    static constexpr int kV = kK + kKV;
+    static constexpr int kQ = kV + kKV;       // [2]
+    static constexpr int kDO = kQ + 2 * kQT;  // [2]
+    static constexpr int kPT = kDO + 2 * kQT; // [2]
+    static constexpr int kDS = kPT + 2 * kPD; // [2]
+    static constexpr int kMeta = kDS + 2 * kPD;  // [2][3][64] f32
+    static constexpr int kBar = kMeta + 2 * 3 * 64 * 4;
+    static constexpr int kTmemSlot = kBar + 16 * 8;
+    static constexpr int kAlloc = kTmemSlot + 16 + 1024;
+};
+enum { KB_KVFULL = 0, KB_QDFULL = 1, KB_QDEMPTY = 3, KB_SFULL = 5, KB_SEMPTY = 7, KB_PDSFULL = 9,
+       KB_PDSEMPTY = 10, KB_ACCDONE = 12 };
+
+template <int D, bool SEL, bool KEY_SOFT>
+__global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_tc(BwdArgs a) {
+    using SM = KSmem<D>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const uint32_t sbase = smem_u32(smem);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SM::kBar);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + SM::kTmemSlot);
+    float* qmeta = reinterpret_cast<float*>(smem + SM::kMeta);  // [stage][lse2|delta|tau][64]
+    __shared__ int s_range[2];
+
+    const int kt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t bl = (int64_t)b * a.L;
+    const int* elist = a.ever_list + bl;
+    int nkeys, j0 = 0;
+    if (SEL) {
+        const int ec = a.ever_count[b];
+        if (kt * 128 >= ec) return;
+        nkeys = min(128, ec - kt * 128);
+    } else {
+        j0 = kt * 128;
+        if (j0 >= a.L) return;
+        nkeys = min(128, a.L - j0);
+    }
+    auto key_of = [&](int r) -> int {
+        if (r >= nkeys) return -1;
+        return SEL ? __ldg(elist + kt * 128 + r) : j0 + r;
+    };
+    if (threadIdx.x == 0) {
+        s_range[0] = SEL ? __ldg(elist + kt * 128) + a.w : j0;  // the list is ascending
+        s_range[1] = 0;
+    }
+    __syncthreads();
+    if (threadIdx.x < 128) {
+        const int key = key_of(threadIdx.x);
+        int hi = 0;
+        if (key >= 0) hi = SEL ? __ldg(a.leave + bl + key) + a.w : key + a.w;  // exclusive
+        hi = warp_max_i(hi);
+        if (lane == 0) atomicMax(&s_range[1], hi);
+    }
+    if (threadIdx.x == 0) {
+        mbar_init(&bars[KB_KVFULL], kProducers);
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&bars[KB_QDFULL + s], kProducers);
+            mbar_init(&bars[KB_QDEMPTY + s], 1);
+            mbar_init(&bars[KB_SFULL + s], 1);
+            mbar_init(&bars[KB_SEMPTY + s], 128);
+            mbar_init(&bars[KB_PDSEMPTY + s], 1);
+        }
+        mbar_init(&bars[KB_PDSFULL], 128);
+        mbar_init(&bars[KB_ACCDONE], 1);
+        mbar_fence_init();
+    }
+    if (warp == 7) tmem_alloc<512>(tmem_slot);
+    tc_before_sync();
+    __syncthreads();
+    tc_after_sync();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t tS = tmem, tP = tmem + 128, tDV = tmem + 256, tDK = tmem + 384;
+    const int q_lo = (s_range[0] / 64) * 64;
+    const int q_hi = min(a.L, s_range[1]);
+    const int nq = q_hi > q_lo ? (q_hi - q_lo + 63) / 64 : 0;
+
+    if (warp >= 4 && warp < 7) {
+        const int pw = warp - 4, ptid = threadIdx.x - 128;
+        load_tile<D, 128>(sbase + SM::kK, a.k, b, h, a.L, a.H, pw, lane, key_of);
+        load_tile<D, 128>(sbase + SM::kV, a.v, b, h, a.L, a.H, pw, lane, key_of);
+        cp_async_arrive_noinc(&bars[KB_KVFULL]);
+        const float* lse2 = a.lse2 + ((int64_t)b * a.H + h) * a.L;
+        const float* dlt = a.delta + ((int64_t)b * a.H + h) * a.L;
+        for (int qt = 0; qt < nq; ++qt) {
+            const int s = qt & 1;
+            if (qt >= 2) mbar_wait(&bars[KB_QDEMPTY + s], ((qt - 2) >> 1) & 1);
+            const int qs = q_lo + qt * 64;
+            auto qf = [&](int r) { return qs + r < a.L ? qs + r : -1; };
+            load_tile<D, 64>(sbase + SM::kQ + s * SM::kQT, a.q, b, h, a.L, a.H, pw, lane, qf);
+            load_tile<D, 64>(sbase + SM::kDO + s * SM::kQT, a.dout, b, h, a.L, a.H, pw, lane, qf);
+            for (int c = ptid; c < 64; c += kProducers) {
+                const int i = qs + c;
+                const bool ok = i < a.L;
+                const int t = i - a.w;
+                const uint32_t mb = smem_u32(qmeta + (s * 3) * 64 + c);
+                cp_async4(mb, lse2 + (ok ? i : 0), ok);
+                cp_async4(mb + 64 * 4, dlt + (ok ? i : 0), ok);
+                cp_async4(mb + 128 * 4, a.tauf + bl + (ok && t >= 0 ? t : 0), ok && t >= 0);
+            }
+            cp_async_arrive_noinc(&bars[KB_QDFULL + s]);
+        }
+    } else if (warp == 7) {
+        if (lane == 0 && nq > 0) {
+            constexpr uint32_t id_s = umma_idesc(128, 64, false, false);
+            constexpr uint32_t id_acc = umma_idesc(128, D, false, true);
+            mbar_wait(&bars[KB_KVFULL], 0);
+            fence_proxy_async();
+            auto acc = [&](int j) {
+                const int s = j & 1;
+                mbar_wait(&bars[KB_PDSFULL], j & 1);
+                tc_after_sync();
+                const uint32_t dob = sbase + SM::kDO + s * SM::kQT, qb = sbase + SM::kQ + s * SM::kQT;
+                const uint32_t ptb = sbase + SM::kPT + s * SM::kPD, dsb = sbase + SM::kDS + s * SM::kPD;
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) {
+                    umma_f16(tDV, desc_kmajor(ptb, 128, kk), desc_mnmajor(dob, 64, kk), id_acc,
+                             (j > 0 || kk > 0) ? 1u : 0u);
+                    umma_f16(tDK, desc_kmajor(dsb, 128, kk), desc_mnmajor(qb, 64, kk), id_acc,
+                             (j > 0 || kk > 0) ? 1u : 0u);
+                }
+                umma_commit(&bars[KB_QDEMPTY + s]);
+                umma_commit(&bars[KB_PDSEMPTY + s]);
+            };
+            for (int qt = 0; qt < nq; ++qt) {
+                const int s = qt & 1;
+                mbar_wait(&bars[KB_QDFULL + s], (qt >> 1) & 1);
+                fence_proxy_async();
+                if (qt >= 2) mbar_wait(&bars[KB_SEMPTY + s], ((qt - 2) >> 1) & 1);
+                tc_after_sync();
+                const uint32_t qb = sbase + SM::kQ + s * SM::kQT, dob = sbase + SM::kDO + s * SM::kQT;
+#pragma unroll
+                for (int kk = 0; kk < D / 16; ++kk) {
+                    umma_f16(tS + s * 64, desc_kmajor(sbase + SM::kK, 128, kk), desc_kmajor(qb, 64, kk), id_s,
+                             kk > 0 ? 1u : 0u);
+                    umma_f16(tP + s * 64, desc_kmajor(sbase + SM::kV, 128, kk), desc_kmajor(dob, 64, kk), id_s,
+                             kk > 0 ? 1u : 0u);
+                }
+                umma_commit(&bars[KB_SFULL + s]);
+                if (qt >= 1) acc(qt - 1);
+            }
+            acc(nq - 1);
+            umma_commit(&bars[KB_ACCDONE]);
+        }
+        __syncwarp();
+    } else {
+        // key rows (warps 0-3): elementwise backward
+        const int r = threadIdx.x;
+        const int key = key_of(r);
+        const int leave = (SEL && key >= 0) ? __ldg(a.leave + bl + key) : 0;
+        const float uj = (SEL && key >= 0) ? __ldg(a.uf + bl + key) : 0.f;
+        const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+        double colsum = 0.0;
+        for (int qt = 0; qt < nq; ++qt) {
+            const int s = qt & 1;
+            const int qs = q_lo + qt * 64;
+            mbar_wait(&bars[KB_SFULL + s], (qt >> 1) & 1);
+            mbar_wait(&bars[KB_QDFULL + s], (qt >> 1) & 1);
+            tc_after_sync();
+            float sv[64], dp[64];
+            tmem_ld32(tS + lane_off + s * 64, sv);
+            tmem_ld32(tS + lane_off + s * 64 + 32, sv + 32);
+            tmem_ld32(tP + lane_off + s * 64, dp);
+            tmem_ld32(tP + lane_off + s * 64 + 32, dp + 32);
+            tmem_wait_ld();
+            tc_before_sync();
+            mbar_arrive(&bars[KB_SEMPTY + s]);
+            const float* ml = qmeta + (s * 3) * 64;
+            const float* md = ml + 64;
+            const float* mt = ml + 128;
+            float csum = 0.f;
+#pragma unroll
+            for (int c = 0; c < 64; c += 4) {
+                const float4 l4 = *reinterpret_cast<const float4*>(ml + c);
+                const float4 d4 = *reinterpret_cast<const float4*>(md + c);
+                const float4 t4 = *reinterpret_cast<const float4*>(mt + c);
+                const float la[4] = {l4.x, l4.y, l4.z, l4.w};
+                const float da[4] = {d4.x, d4.y, d4.z, d4.w};
+                const float ta[4] = {t4.x, t4.y, t4.z, t4.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int i = qs + c + e;
+                    bool ok;
+                    float g = 1.f;
+                    if (SEL) {
+                        const int t = i - a.w;
+                        ok = key >= 0 && i < a.L && t >= key && t < leave;
+                        g = __saturatef(uj - ta[e]);
+                    } else {
+                        ok = key >= 0 && i < a.L && i >= key && i <= key + a.w - 1;
+                    }
+                    const float raw = sv[c + e];
+                    const float kap = (KEY_SOFT && SEL) ? g : 1.f;
+                    const float p = ok ? ex2(raw * kap * a.scale_log2 - la[e]) : 0.f;
+                    const float wv = (SEL && !a.mask_st) ? g : 1.f;
+                    const float cc = p * (wv * dp[c + e] - da[e]);
+                    if (SEL && g > 0.f && g < 1.f) {
+                        float gm = p * dp[c + e];
+                        if (KEY_SOFT) gm += a.scale * cc * raw;
+                        csum += gm;
+                    }
+                    sv[c + e] = p * wv;    // P~^T
+                    dp[c + e] = cc * kap;  // dS^T (scale applied in the epilogue)
+                }
+            }
+            colsum += (double)csum;
+            if (qt >= 2) mbar_wait(&bars[KB_PDSEMPTY + s], ((qt - 2) >> 1) & 1);
+            const uint32_t ptb = sbase + SM::kPT + s * SM::kPD, dsb = sbase + SM::kDS + s * SM::kPD;
+#pragma unroll
+            for (int ch = 0; ch < 8; ++ch) {
+                const float* x = sv + ch * 8;
+                st_shared_v4(ptb + sw_off(r, ch, 128), pack_bf16(x[0], x[1]), pack_bf16(x[2], x[3]),
+                             pack_bf16(x[4], x[5]), pack_bf16(x[6], x[7]));
+                const float* y = dp + ch * 8;
+                st_shared_v4(dsb + sw_off(r, ch, 128), pack_bf16(y[0], y[1]), pack_bf16(y[2], y[3]),
+                             pack_bf16(y[4], y[5]), pack_bf16(y[6], y[7]));
+            }
+            fence_proxy_async();
+            tc_before_sync();
+            mbar_arrive(&bars[KB_PDSFULL]);
+        }
+        if (SEL && key >= 0 && colsum != 0.0) atomicAdd(a.colsum + bl + key, colsum);
+        if (nq > 0) {
+            mbar_wait(&bars[KB_ACCDONE], 0);
+            tc_after_sync();
+        }
+        const bool has_sel = !SEL && key >= 0 && a.R1 > 0 && key < a.T && __ldg(a.leave + bl + key) > key;
+        const int64_t rowoff = ((bl + (key >= 0 ? key : 0)) * a.H + h) * D;
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) {
+            float dv[32], dk[32];
+            if (nq > 0) {
+                tmem_ld32(tDV + lane_off + c * 32, dv);
+                tmem_ld32(tDK + lane_off + c * 32, dk);
+                tmem_wait_ld();
+            } else {
+#pragma unroll
+                for (int e = 0; e < 32; ++e) dv[e] = dk[e] = 0.f;
+            }
+            if (key < 0) continue;
+#pragma unroll
+            for (int e = 0; e < 32; ++e) dk[e] *= a.scale;
+            if (SEL) {
+                float* pk = a.dk_acc + rowoff + c * 32;
+                float* pv = a.dv_acc + rowoff + c * 32;
+#pragma unroll
+                for (int e = 0; e < 32; e += 4) {
+                    *reinterpret_cast<float4*>(pk + e) = make_float4(dk[e], dk[e + 1], dk[e + 2], dk[e + 3]);
+                    *reinterpret_cast<float4*>(pv + e) = make_float4(dv[e], dv[e + 1], dv[e + 2], dv[e + 3]);
+                }
+            } else {
+                if (has_sel) {
+                    const float* pk = a.dk_acc + rowoff + c * 32;
+                    const float* pv = a.dv_acc + rowoff + c * 32;
+#pragma unroll
+                    for (int e = 0; e < 32; e += 4) {
+                        const float4 x = *reinterpret_cast<const float4*>(pk + e);
+                        const float4 y = *reinterpret_cast<const float4*>(pv + e);
+                        dk[e] += x.x;
+                        dk[e + 1] += x.y;
+                        dk[e + 2] += x.z;
+                        dk[e + 3] += x.w;
+                        dv[e] += y.x;
+                        dv[e + 1] += y.y;
+                        dv[e + 2] += y.z;
+                        dv[e + 3] += y.w;
+                    }
+                }
+                __nv_bfloat16* gk = a.dk + rowoff + c * 32;
+                __nv_bfloat16* gv = a.dv + rowoff + c * 32;
+#pragma unroll
+                for (int e = 0; e < 32; e += 8) {
+                    uint4 x, y;
+                    x.x = pack_bf16(dk[e], dk[e + 1]);
+                    x.y = pack_bf16(dk[e + 2], dk[e + 3]);
+                    x.z = pack_bf16(dk[e + 4], dk[e + 5]);
+                    x.w = pack_bf16(dk[e + 6], dk[e + 7]);
+                    y.x = pack_bf16(dv[e], dv[e + 1]);
+                    y.y = pack_bf16(dv[e + 2], dv[e + 3]);
+                    y.z = pack_bf16(dv[e + 4], dv[e + 5]);
+                    y.w = pack_bf16(dv[e + 6], dv[e + 7]);
+                    *reinterpret_cast<uint4*>(gk + e) = x;
+                    *reinterpret_cast<uint4*>(gv + e) = y;
+                }
+            }
+        }
+    }
+    tc_before_sync();
+    __syncthreads();
+    tc_after_sync();
+    if (warp == 7) tmem_dealloc<512>(tmem);
+}
+
+// ------------------------------------------------------------------ dQ
+template <int D>
+struct QSmem {
+    static constexpr int kQT = 128 * D * 2;  // 128-query tile
+    static constexpr int kKT = 64 * D * 2;   // 64-key tile
+    static constexpr int kDSB = 128 * 64 * 2;
+    static constexpr int kQ = 0;
+    static constexpr int kDO = kQ + kQT;
+    static constexpr int kK = kDO + kQT;      // [2]
+    static constexpr int kV = kK + 2 * kKT;   // [2]
+    static constexpr int kDS = kV + 2 * kKT;  // [2]
+    static constexpr int kMeta = kDS + 2 * kDSB;  // [2][3][64] x 4 B
+    static constexpr int kBar = kMeta + 2 * 3 * 64 * 4;
+    static constexpr int kTmemSlot = kBar + 16 * 8;
+    static constexpr int kAlloc = kTmemSlot + 16 + 1024;
+};
+enum { QB_QFULL = 0, QB_KVFULL = 1, QB_KVEMPTY = 3, QB_SFULL = 5, QB_SEMPTY = 7, QB_DSFULL = 9,
+       QB_DSEMPTY = 10, QB_DQDONE = 12 };
+
+template <int D, bool KEY_SOFT>
+__global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(BwdArgs a) {
+    using SM = QSmem<D>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const uint32_t sbase = smem_u32(smem);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SM::kBar);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + SM::kTmemSlot);
+    int* meta = reinterpret_cast<int*>(smem + SM::kMeta);  // [stage][key|leave|uf][64]
+
+    const int qb = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t bl = (int64_t)b * a.L;
+    const int i0 = qb * 128;
+    const int cnt = (a.R1 > 0) ? a.qb_count[(int64_t)b * a.nqb + qb] : 0;
+    const int n_sel = (cnt + 63) / 64;
+    const int n_win = (a.w + 127 + 63) / 64;
+    const int n = n_sel + n_win;
+    const int jw0 = i0 - a.w + 1;
+    const int* list = a.qb_list + ((int64_t)b * a.nqb + qb) * a.qb_cap;
+
+    if (threadIdx.x == 0) {
+        mbar_init(&bars[QB_QFULL], kProducers);
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&bars[QB_KVFULL + s], kProducers);
+            mbar_init(&bars[QB_KVEMPTY + s], 1);
+            mbar_init(&bars[QB_SFULL + s], 1);
+            mbar_init(&bars[QB_SEMPTY + s], 128);
+            mbar_init(&bars[QB_DSEMPTY + s], 1);
+        }
+        mbar_init(&bars[QB_DSFULL], 128);
+        mbar_init(&bars[QB_DQDONE], 1);
+        mbar_fence_init();
+    }
+    if (warp == 7) tmem_alloc<512>(tmem_slot);
+    tc_before_sync();
+    __syncthreads();
+    tc_after_sync();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t tS = tmem, tP = tmem + 128, tDQ = tmem + 256;
+
+    if (warp >= 4 && warp < 7) {
+        const int pw = warp - 4, ptid = threadIdx.x - 128;
+        auto qf = [&](int r) { return i0 + r < a.L ? i0 + r : -1; };
+        load_tile<D, 128>(sbase + SM::kQ, a.q, b, h, a.L, a.H, pw, lane, qf);
+        load_tile<D, 128>(sbase + SM::kDO, a.dout, b, h, a.L, a.H, pw, lane, qf);
+        cp_async_arrive_noinc(&bars[QB_QFULL]);
+        for (int jt = 0; jt < n; ++jt) {
+            const int s = jt & 1;
+            if (jt >= 2) mbar_wait(&bars[QB_KVEMPTY + s], ((jt - 2) >> 1) & 1);
+            if (jt < n_sel) {
+                for (int c = ptid; c < 64; c += kProducers) {
+                    const int idx = jt * 64 + c;
+                    const int key = idx < cnt ? __ldg(list + idx) : -1;
+                    const uint32_t mb = smem_u32(meta + (s * 3) * 64 + c);
+                    cp_async4(mb, list + (idx < cnt ? idx : 0), idx < cnt);
+                    cp_async4(mb + 64 * 4, a.leave + bl + (key >= 0 ? key : 0), key >= 0);
+                    cp_async4(mb + 128 * 4, a.uf + bl + (key >= 0 ? key : 0), key >= 0);
+                }
+                auto kf = [&](int r) {
+                    const int idx = jt * 64 + r;
+                    return idx < cnt ? __ldg(list + idx) : -1;
+                };
+                load_tile<D, 64>(sbase + SM::kK + s * SM::kKT, a.k, b, h, a.L, a.H, pw, lane, kf);
+                load_tile<D, 64>(sbase + SM::kV + s * SM::kKT, a.v, b, h, a.L, a.H, pw, lane, kf);
+            } else {
+                const int kb0 = jw0 + (jt - n_sel) * 64;
+                auto kf = [&](int r) { return kb0 + r; };
+                load_tile<D, 64>(sbase + SM::kK + s * SM::kKT, a.k, b, h, a.L, a.H, pw, lane, kf);
+                load_tile<D, 64>(sbase + SM::kV + s * SM::kKT, a.v, b, h, a.L, a.H, pw, lane, kf);
+            }
+            cp_async_arrive_noinc(&bars[QB_KVFULL + s]);
+        }
+    } else if (warp == 7) {
+        if (lane == 0) {
+            constexpr uint32_t id_s = umma_idesc(128, 64, false, false);
+            constexpr uint32_t id_dq = umma_idesc(128, D, false, true);
+            mbar_wait(&bars[QB_QFULL], 0);
+            fence_proxy_async();
+            auto dq = [&](int j) {
+                const int s = j & 1;
+                mbar_wait(&bars[QB_DSFULL], j & 1);
+                tc_after_sync();
+                const uint32_t dsb = sbase + SM::kDS + s * SM::kDSB, kb = sbase + SM::kK + s * SM::kKT;
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk)
+                    umma_f16(tDQ, desc_kmajor(dsb, 128, kk), desc_mnmajor(kb, 64, kk), id_dq,
+                             (j > 0 || kk > 0) ? 1u : 0u);
+                umma_commit(&bars[QB_KVEMPTY + s]);
+                umma_commit(&bars[QB_DSEMPTY + s]);
+            };
+            for (int jt = 0; jt < n; ++jt) {
+                const int s = jt & 1;
+                mbar_wait(&bars[QB_KVFULL + s], (jt >> 1) & 1);
+                fence_proxy_async();
+                if (jt >= 2) mbar_wait(&bars[QB_SEMPTY + s], ((jt - 2) >> 1) & 1);
+                tc_after_sync();
+                const uint32_t kb = sbase + SM::kK + s * SM::kKT, vb = sbase + SM::kV + s * SM::kKT;
+#pragma unroll
+                for (int kk = 0; kk < D / 16; ++kk) {
+                    umma_f16(tS + s * 64, desc_kmajor(sbase + SM::kQ, 128, kk), desc_kmajor(kb, 64, kk), id_s,
+                             kk > 0 ? 1u : 0u);
+                    umma_f16(tP + s * 64, desc_kmajor(sbase + SM::kDO, 128, kk), desc_kmajor(vb, 64, kk), id_s,
+                             kk > 0 ? 1u : 0u);
+                }
+                umma_commit(&bars[QB_SFULL + s]);
+                if (jt >= 1) dq(jt - 1);
+            }
+            dq(n - 1);
+            umma_commit(&bars[QB_DQDONE]);
+        }
+        __syncwarp();
+    } else {
+        const int r = threadIdx.x;
+        const int i = i0 + r;
+        const int t = i - a.w;
+        const float tau_i = (t >= 0 && a.R1 > 0) ? a.tauf[bl + t] : -INFINITY;
+        const int lo_win = i - a.w + 1;
+        const int64_t hl = ((int64_t)b * a.H + h) * a.L;
+        const float lse2 = i < a.L ? a.lse2[hl + i] : 0.f;
+        const float dlt = i < a.L ? a.delta[hl + i] : 0.f;
+        const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+        float rsum = 0.f;
+        for (int jt = 0; jt < n; ++jt) {
+            const int s = jt & 1;
+            const bool is_sel = jt < n_sel;
+            mbar_wait(&bars[QB_SFULL + s], (jt >> 1) & 1);
+            mbar_wait(&bars[QB_KVFULL + s], (jt >> 1) & 1);
+            tc_after_sync();
+            float sv[64], dp[64];
+            tmem_ld32(tS + lane_off + s * 64, sv);
+            tmem_ld32(tS + lane_off + s * 64 + 32, sv + 32);
+            tmem_ld32(tP + lane_off + s * 64, dp);
+            tmem_ld32(tP + lane_off + s * 64 + 32, dp + 32);
+            tmem_wait_ld();
+            tc_before_sync();
+            mbar_arrive(&bars[QB_SEMPTY + s]);
+            if (is_sel) {
+                const int* mk = meta + (s * 3) * 64;
+                const int* ml = mk + 64;
+                const float* mu = reinterpret_cast<const float*>(mk + 128);
+#pragma unroll
+                for (int c = 0; c < 64; c += 4) {
+                    const int4 kj = *reinterpret_cast<const int4*>(mk + c);
+                    const int4 lv = *reinterpret_cast<const int4*>(ml + c);
+                    const float4 uu = *reinterpret_cast<const float4*>(mu + c);
+                    const int kja[4] = {kj.x, kj.y, kj.z, kj.w};
+                    const int lva[4] = {lv.x, lv.y, lv.z, lv.w};
+                    const float ua[4] = {uu.x, uu.y, uu.z, uu.w};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const bool ok = i < a.L && kja[e] >= 0 && kja[e] <= t && lva[e] > t;
+                        const float g = __saturatef(ua[e] - tau_i);
+                        const float raw = sv[c + e];
+                        const float kap = KEY_SOFT ? g : 1.f;
+                        const float p = ok ? ex2(raw * kap * a.scale_log2 - lse2) : 0.f;
+                        const float wv = a.mask_st ? 1.f : g;
+                        const float cc = p * (wv * dp[c + e] - dlt);
+                        if (ok && g > 0.f && g < 1.f) {
+                            float gm = p * dp[c + e];
+                            if (KEY_SOFT) gm += a.scale * cc * raw;
+                            rsum += gm;
+                        }
+                        dp[c + e] = cc * kap;
+                    }
+                }
+            } else {
+                const int kb0 = jw0 + (jt - n_sel) * 64;
+#pragma unroll
+                for (int c = 0; c < 64; ++c) {
+                    const int key = kb0 + c;
+                    const bool ok = i < a.L && key >= 0 && key >= lo_win && key <= i;
+                    const float p = ok ? ex2(sv[c] * a.scale_log2 - lse2) : 0.f;
+                    dp[c] = p * (dp[c] - dlt);
+                }
+            }
+            if (jt >= 2) mbar_wait(&bars[QB_DSEMPTY + s], ((jt - 2) >> 1) & 1);
+            const uint32_t dsb = sbase + SM::kDS + s * SM::kDSB;
+#pragma unroll
+            for (int ch = 0; ch < 8; ++ch) {
+                const float* y = dp + ch * 8;
+                st_shared_v4(dsb + sw_off(r, ch, 128), pack_bf16(y[0], y[1]), pack_bf16(y[2], y[3]),
+                             pack_bf16(y[4], y[5]), pack_bf16(y[6], y[7]));
+            }
+            fence_proxy_async();
+            tc_before_sync();
+            mbar_arrive(&bars[QB_DSFULL]);
+        }
+        mbar_wait(&bars[QB_DQDONE], 0);
+        tc_after_sync();
+        if (i < a.L && t >= 0 && a.R1 > 0 && rsum != 0.f) atomicAdd(a.rowsum + bl + t, (double)rsum);
+        __nv_bfloat16* orow = a.dq + ((bl + (i < a.L ? i : 0)) * a.H + h) * D;
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) {
+            float x[32];
+            tmem_ld32(tDQ + lane_off + c * 32, x);
+            tmem_wait_ld();
+            if (i < a.L) {
+#pragma unroll
+                for (int e = 0; e < 32; e += 8) {
+                    uint4 pk;
+                    pk.x = pack_bf16(x[e] * a.scale, x[e + 1] * a.scale);
+                    pk.y = pack_bf16(x[e + 2] * a.scale, x[e + 3] * a.scale);
+                    pk.z = pack_bf16(x[e + 4] * a.scale, x[e + 5] * a.scale);
+                    pk.w = pack_bf16(x[e + 6] * a.scale, x[e + 7] * a.scale);
+                    *reinterpret_cast<uint4*>(orow + c * 32 + e) = pk;
+                }
+            }
+        }
+    }
+    tc_before_sync();
+    __syncthreads();
+    tc_after_sync();
+    if (warp == 7) tmem_dealloc<512>(tmem);
+}
+
+template <class K>
+void set_smem(K kern, int bytes) {
+    SKB_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+}
+
+template <int D, bool KS>
+void launch_bwd(const BwdArgs& a, const skb_attn_desc& d, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        set_smem(k_bwd_dkdv_tc<D, true, KS>, KSmem<D>::kAlloc);
+        set_smem(k_bwd_dkdv_tc<D, false, KS>, KSmem<D>::kAlloc);
+        set_smem(k_bwd_dq_tc<D, KS>, QSmem<D>::kAlloc);
+        attr = true;
+    }
+    if (a.R1 > 0 && a.T > 0) {
+        dim3 gs((unsigned)cdiv(a.T, 128), (unsigned)d.heads, (unsigned)d.batch);
+        k_bwd_dkdv_tc<D, true, KS><<<gs, kThreads, KSmem<D>::kAlloc, st>>>(a);
+        SKB_CHECK_LAUNCH();
+    }
+    dim3 gw((unsigned)cdiv(a.L, 128), (unsigned)d.heads, (unsigned)d.batch);
+    k_bwd_dkdv_tc<D, false, KS><<<gw, kThreads, KSmem<D>::kAlloc, st>>>(a);
+    SKB_CHECK_LAUNCH();
+    dim3 gq((unsigned)a.nqb, (unsigned)d.heads, (unsigned)d.batch);
+    k_bwd_dq_tc<D, KS><<<gq, kThreads, QSmem<D>::kAlloc, st>>>(a);
+    SKB_CHECK_LAUNCH();
+}
+
+}  // namespace
+
+void run_attn_bwd_tc(const skb_attn_desc& d, const void* q, const void* k, const void* v,
+                     const void* o, const void* dout, const double* lse, const double* u,
+                     const SelView& s, void* dq, void* dk, void* dv, double* rowsum,
+                     double* colsum, void* ws, const BwdLayout& bl, cudaStream_t st) {
+    (void)u;
+    char* base = static_cast<char*>(ws);
+    BwdArgs a{};
+    a.q = static_cast<const __nv_bfloat16*>(q);
+    a.k = static_cast<const __nv_bfloat16*>(k);
+    a.v = static_cast<const __nv_bfloat16*>(v);
+    a.dout = static_cast<const __nv_bfloat16*>(dout);
+    a.dq = static_cast<__nv_bfloat16*>(dq);
+    a.dk = static_cast<__nv_bfloat16*>(dk);
+    a.dv = static_cast<__nv_bfloat16*>(dv);
+    a.dk_acc = reinterpret_cast<float*>(base + bl.dk_acc);
+    a.dv_acc = reinterpret_cast<float*>(base + bl.dv_acc);
+    float* lse2 = reinterpret_cast<float*>(base + bl.dq_acc);
+    float* delta = lse2 + d.batch * d.heads * d.seq_len;
+    a.lse2 = lse2;
+    a.delta = delta;
+    a.uf = s.uf;
+    a.tauf = s.tauf;
+    a.leave = s.leave;
+    a.qb_count = s.qb_count;
+    a.qb_list = s.qb_list;
+    a.ever_count = s.ever_count;
+    a.ever_list = s.ever_list;
+    a.rowsum = rowsum;
+    a.colsum = colsum;
+    a.nqb = s.nqb;
+    a.qb_cap = s.qb_cap;
+    a.B = (int)d.batch;
+    a.L = (int)d.seq_len;
+    a.H = (int)d.heads;
+    a.w = (int)d.window;
+    a.T = std::max(0, a.L - a.w);
+    a.R1 = (int)floor_k(d.k);
+    const double scale = d.scale > 0.0 ? d.scale : 1.0 / std::sqrt((double)d.head_dim);
+    a.scale = (float)scale;
+    a.scale_log2 = (float)(scale * 1.4426950408889634);
+    a.mask_st = d.mask_mode;
+    const int64_t rows = d.batch * d.seq_len * d.heads;
+    const unsigned pg = (unsigned)cdiv(rows * 32, 256);
+    if (d.head_dim == 128)
+        k_bwd_prep<128><<<pg, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(o), a.dout, lse, lse2, delta,
+                                            a.B, a.L, a.H);
+    else
+        k_bwd_prep<64><<<pg, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(o), a.dout, lse, lse2, delta,
+                                           a.B, a.L, a.H);
+    SKB_CHECK_LAUNCH();
+    if (d.head_dim == 128) {
+        if (d.key_mode) launch_bwd<128, true>(a, d, st);
+        else launch_bwd<128, false>(a, d, st);
+    } else {
+        if (d.key_mode) launch_bwd<64, true>(a, d, st);
+        else launch_bwd<64, false>(a, d, st);
+    }
+}
+
+}  // namespace skb

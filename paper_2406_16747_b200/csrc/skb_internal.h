@@ -22,6 +22,8 @@ struct SelView {
     const int* qb_list;
     const int* ever_count;
     const int* ever_list;
+    const float* uf;    // u as fp32 [B, L]
+    const float* tauf;  // tau as fp32 [B, L] (push time)
     int nqb, qb_cap;
 };
 SelView sel_view(const skb_attn_desc& d, const void* ws);

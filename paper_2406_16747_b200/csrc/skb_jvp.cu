@@ -103,10 +103,12 @@ void bwd_layout(const skb_attn_desc& d, BwdLayout& o) {
     o.rowsum = take(BL * 8);
     o.colsum = take(BL * 8);
     o.mean_prefix = take((BL + d.batch) * 8);
-    const bool gather = !(d.dtype == SKB_BF16 && tc_supported(d));
-    o.dk_acc = take(gather ? N * 8 : N * 4);
-    o.dv_acc = take(gather ? N * 8 : N * 4);
-    o.dq_acc = take(gather ? 0 : N * 4);
+    const bool tc = d.dtype == SKB_BF16 && tc_supported(d) && !(d.flags & SKB_FLAG_FORCE_GATHER);
+    // gather backward: fp64 dK/dV accumulators; tensor-core backward: fp32
+    // partials of the selected pass + lse2/delta rows in the dq_acc region
+    o.dk_acc = take(tc ? N * 4 : N * 8);
+    o.dv_acc = take(tc ? N * 4 : N * 8);
+    o.dq_acc = take(tc ? BL * d.heads * 8 : 0);
     o.total = off;
 }
 

@@ -358,6 +358,15 @@ k_ever_list(const int* __restrict__ leave1, int L, int T, int* __restrict__ ever
     if (threadIdx.x == 0) ever_count[b] = base_s;
 }
 
+__global__ void k_to_float(const double* __restrict__ u, const double* __restrict__ tau,
+                           float* __restrict__ uf, float* __restrict__ tauf, int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) {
+        uf[i] = (float)u[i];
+        tauf[i] = (float)tau[i];
+    }
+}
+
 __global__ void k_fill_int(int* p, int64_t n, int v) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) p[i] = v;
@@ -438,6 +447,8 @@ void select_layout(const skb_attn_desc& d, skb_select_layout& o) {
     o.misc = take((1 + B * nch) * 4);
     const int64_t cap2 = next_pow2((int)std::max<int64_t>(L, 1));
     o.scratch = take((uint64_t)kOverflowSlots * (cap2 + L + 1) * 8);
+    o.uf = take(B * L * 4);
+    o.tauf = take(B * L * 4);
     o.total_bytes = off;
     o.qblock = kQBlock;
     o.nqb = nqb;
@@ -483,8 +494,8 @@ void run_select(const skb_attn_desc& d, const double* u, void* ws, cudaStream_t 
 
     k_fill_tau<<<(unsigned)cdiv(BL, 256), 256, 0, st>>>(tau, nfrac, BL);
     SKB_CHECK_LAUNCH();
-    if (R1 == 0 || T == 0) {
-        // no retention: every position leaves at entry
+    if (R2 == 0 || T == 0) {
+        // no budget: every position leaves at entry
         dim3 g((unsigned)cdiv(L, 256), B);
         k_leave_identity<<<g, 256, 0, st>>>(leave1, L);
         k_leave_identity<<<g, 256, 0, st>>>(leave2, L);
@@ -527,6 +538,9 @@ void run_select(const skb_attn_desc& d, const double* u, void* ws, cudaStream_t 
         k_tau_monotone<<<B, 1024, 0, st>>>(tau, L, T);
         SKB_CHECK_LAUNCH();
     }
+    k_to_float<<<(unsigned)cdiv(BL, 256), 256, 0, st>>>(u, tau, reinterpret_cast<float*>(base + lay.uf),
+                                                          reinterpret_cast<float*>(base + lay.tauf), BL);
+    SKB_CHECK_LAUNCH();
     const int nqb = (int)lay.nqb;
     if (R1 > 0 && T > 0) {
         dim3 g(nqb, B);
@@ -553,6 +567,8 @@ SelView sel_view(const skb_attn_desc& d, const void* ws) {
     s.qb_list = reinterpret_cast<const int*>(base + lay.qb_list);
     s.ever_count = reinterpret_cast<const int*>(base + lay.ever_count);
     s.ever_list = reinterpret_cast<const int*>(base + lay.ever_list);
+    s.uf = reinterpret_cast<const float*>(base + lay.uf);
+    s.tauf = reinterpret_cast<const float*>(base + lay.tauf);
     s.nqb = (int)lay.nqb;
     s.qb_cap = (int)lay.qb_cap;
     return s;
