@@ -239,9 +239,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
                 m = mt;
             }
             float psum = 0.f;
+            const float mb = m == -INFINITY ? 0.f : m;  // fully masked so far: avoid -inf - -inf
 #pragma unroll
             for (int c = 0; c < 128; ++c) {
-                const float p = ex2(sv[c] - m);  // exp2(-inf) = 0 for masked keys
+                const float p = ex2(sv[c] - mb);  // exp2(-inf) = 0 for masked keys
                 psum += p;
                 sv[c] = p;
             }
