@@ -54,7 +54,8 @@ struct FwdSmem {
     static constexpr int kV = kK + 2 * kTile;
     static constexpr int kP = kV + 2 * kTile;
     static constexpr int kMeta = kP + 128 * 128 * 2;   // [2][3][128] x 4 B
-    static constexpr int kBar = kMeta + 2 * 3 * 128 * 4;
+    static constexpr int kFlags = kMeta + 2 * 3 * 128 * 4;  // [2][4] int per-tile flags
+    static constexpr int kBar = kFlags + 2 * 4 * 4;
     static constexpr int kTmemSlot = kBar + 16 * 8;
     static constexpr int kBytes = kTmemSlot + 16;
     static constexpr int kAlloc = kBytes + 1024;  // room to align the base to 1024
@@ -71,6 +72,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SM::kBar);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + SM::kTmemSlot);
     int* meta = reinterpret_cast<int*>(smem + SM::kMeta);  // [stage][key|leave|uf][128]
+    int* tflags = reinterpret_cast<int*>(smem + SM::kFlags);  // [stage][producer warp]
 
     const int qb = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -85,7 +87,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
     if (threadIdx.x == 0) {
         mbar_init(&bars[B_QFULL], kProducers);
         for (int s = 0; s < 2; ++s) {
-            mbar_init(&bars[B_KVFULL + s], kProducers);
+            // 96 cp.async completions + 96 plain arrivals (which release the tile flags)
+            mbar_init(&bars[B_KVFULL + s], 2 * kProducers);
             mbar_init(&bars[B_KVEMPTY + s], 1);
             mbar_init(&bars[B_SFULL + s], 1);
             mbar_init(&bars[B_SEMPTY + s], 128);
@@ -112,8 +115,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
             const int s = jt & 1;
             if (jt >= 2) mbar_wait(&bars[B_KVEMPTY + s], ((jt - 2) >> 1) & 1);
             if (jt < n_sel) {
-                // metadata (key, leave_j, u_j) for the softmax warps, via cp.async so
-                // the stage's single completion barrier covers it
+                // metadata (key, leave_j, u_j) for the softmax warps via cp.async, plus
+                // tile flags: bit0 = every key valid for every query of the block
+                // (j <= t_lo and leave_j > t_hi), bit1 = every gate saturated
+                // (u_j >= tau(t_hi) + 1), which let the softmax skip masks/gates.
+                const int t_lo = i0 - a.w;
+                const int t_hi = min(i0 + 127, a.L - 1) - a.w;
+                const float tau_hi = t_hi >= 0 ? __ldg(a.tauf + (int64_t)b * a.L + t_hi) : -INFINITY;
+                bool all_ok = true, all_sat = true;
                 for (int c = ptid; c < 128; c += kProducers) {
                     const int idx = jt * 128 + c;
                     const int key = idx < cnt ? __ldg(list + idx) : -1;
@@ -121,7 +130,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
                     cp_async4(mb, list + (idx < cnt ? idx : 0), idx < cnt);
                     cp_async4(mb + 128 * 4, a.leave + (int64_t)b * a.L + (key >= 0 ? key : 0), key >= 0);
                     cp_async4(mb + 256 * 4, a.uf + (int64_t)b * a.L + (key >= 0 ? key : 0), key >= 0);
+                    if (key >= 0) {
+                        const int lv = __ldg(a.leave + (int64_t)b * a.L + key);
+                        const float uu = __ldg(a.uf + (int64_t)b * a.L + key);
+                        all_ok = all_ok && key <= t_lo && lv > t_hi;
+                        all_sat = all_sat && uu >= tau_hi + 1.f;
+                    } else {
+                        all_ok = false;
+                    }
                 }
+                all_ok = __all_sync(0xffffffffu, all_ok);
+                all_sat = __all_sync(0xffffffffu, all_sat);
+                if (lane == 0) tflags[s * 4 + pw] = (all_ok ? 1 : 0) | (all_sat ? 2 : 0);
                 auto kf = [&](int r) {
                     const int idx = jt * 128 + r;
                     return idx < cnt ? __ldg(list + idx) : -1;
@@ -134,6 +154,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
                 load_tile<D, 128>(sbase + SM::kK + s * SM::kTile, a.k, b, h, a.L, a.H, pw, lane, kf);
                 load_tile<D, 128>(sbase + SM::kV + s * SM::kTile, a.v, b, h, a.L, a.H, pw, lane, kf);
             }
+            mbar_arrive(&bars[B_KVFULL + s]);
             cp_async_arrive_noinc(&bars[B_KVFULL + s]);
         }
     } else if (warp == 7) {
@@ -196,37 +217,44 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
             const int* mk = meta + (s * 3) * 128;
             const int* ml = mk + 128;
             const float* mu = reinterpret_cast<const float*>(mk + 256);
-            float mt = -INFINITY;
+            int fl = 0;
             if (is_sel) {
+                fl = tflags[s * 4] & tflags[s * 4 + 1] & tflags[s * 4 + 2];
+                if (!(fl & 1)) {  // per-key interval mask j <= t < leave_j
 #pragma unroll
-                for (int c = 0; c < 128; c += 4) {
-                    const int4 kj = *reinterpret_cast<const int4*>(mk + c);
-                    const int4 lv = *reinterpret_cast<const int4*>(ml + c);
-                    const float4 uu = *reinterpret_cast<const float4*>(mu + c);
-                    const int kja[4] = {kj.x, kj.y, kj.z, kj.w};
-                    const int lva[4] = {lv.x, lv.y, lv.z, lv.w};
-                    const float ua[4] = {uu.x, uu.y, uu.z, uu.w};
+                    for (int c = 0; c < 128; c += 4) {
+                        const int4 kj = *reinterpret_cast<const int4*>(mk + c);
+                        const int4 lv = *reinterpret_cast<const int4*>(ml + c);
+                        sv[c + 0] = (kj.x <= t && lv.x > t) ? sv[c + 0] : -INFINITY;
+                        sv[c + 1] = (kj.y <= t && lv.y > t) ? sv[c + 1] : -INFINITY;
+                        sv[c + 2] = (kj.z <= t && lv.z > t) ? sv[c + 2] : -INFINITY;
+                        sv[c + 3] = (kj.w <= t && lv.w > t) ? sv[c + 3] : -INFINITY;
+                    }
+                }
+                if (KEY_SOFT) {  // gated logits (proj/src/cache.cpp:368-369)
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const bool ok = kja[e] >= 0 && kja[e] <= t && lva[e] > t;
-                        float x = sv[c + e];
-                        if (KEY_SOFT) x *= __saturatef(ua[e] - tau_i);
-                        x = ok ? x * a.scale_log2 : -INFINITY;
-                        sv[c + e] = x;
-                        mt = fmaxf(mt, x);
+                    for (int c = 0; c < 128; c += 4) {
+                        const float4 uu = *reinterpret_cast<const float4*>(mu + c);
+                        sv[c + 0] *= __saturatef(uu.x - tau_i);
+                        sv[c + 1] *= __saturatef(uu.y - tau_i);
+                        sv[c + 2] *= __saturatef(uu.z - tau_i);
+                        sv[c + 3] *= __saturatef(uu.w - tau_i);
                     }
                 }
             } else {
-                const int kbase = jw0 + (jt - n_sel) * 128;
+                // window band of this row inside the tile: columns [cmin, cmax]
+                const int kb = jw0 + (jt - n_sel) * 128;
+                const int cmin = max(0, max(lo_win, 0) - kb);
+                const int cmax = min(127, i - kb);
+                if (__any_sync(0xffffffffu, cmin > 0 || cmax < 127)) {
 #pragma unroll
-                for (int c = 0; c < 128; ++c) {
-                    const int key = kbase + c;
-                    const bool ok = key >= 0 && key >= lo_win && key <= i;
-                    const float x = ok ? sv[c] * a.scale_log2 : -INFINITY;
-                    sv[c] = x;
-                    mt = fmaxf(mt, x);
+                    for (int c = 0; c < 128; ++c) sv[c] = (c >= cmin && c <= cmax) ? sv[c] : -INFINITY;
                 }
             }
+            float mr = -INFINITY;
+#pragma unroll
+            for (int c = 0; c < 128; ++c) mr = fmaxf(mr, sv[c]);
+            const float mt = mr * a.scale_log2;  // scale > 0: max commutes with scaling
             // lazy rescale: move the exponent base only when the max grows by > 2^8
             float fac = 1.f;
             bool need = false;
@@ -242,12 +270,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
             const float mb = m == -INFINITY ? 0.f : m;  // fully masked so far: avoid -inf - -inf
 #pragma unroll
             for (int c = 0; c < 128; ++c) {
-                const float p = ex2(sv[c] - mb);  // exp2(-inf) = 0 for masked keys
+                const float p = ex2(fmaf(sv[c], a.scale_log2, -mb));  // masked: exp2(-inf) = 0
                 psum += p;
                 sv[c] = p;
             }
             l += psum;
-            if (is_sel && !a.mask_st) {
+            if (is_sel && !a.mask_st && !(fl & 2)) {  // value gates (cache.cpp:381-382)
 #pragma unroll
                 for (int c = 0; c < 128; c += 4) {
                     const float4 uu = *reinterpret_cast<const float4*>(mu + c);

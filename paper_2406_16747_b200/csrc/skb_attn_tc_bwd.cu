@@ -250,38 +250,50 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_tc(BwdArgs a) {
             const float* md = ml + 64;
             const float* mt = ml + 128;
             float csum = 0.f;
+            // queries reading this key form one interval: window [j, j+w), selected
+            // [j+w, leave_j+w) (proj/src/cache.cpp:259-311) -> columns [cmin, cmax]
+            const int lo_i = SEL ? key + a.w : key;
+            const int hi_i = min(a.L, SEL ? leave + a.w : key + a.w);  // exclusive
+            const int cmin = key >= 0 ? max(0, lo_i - qs) : 64;
+            const int cmax = key >= 0 ? min(63, hi_i - 1 - qs) : -1;
+            const bool full = __all_sync(0xffffffffu, cmin <= 0 && cmax >= 63);
+            // gates all saturated for this key over the tile (tau is nondecreasing)
+            bool sat = true;
+            if (SEL) {
+                const int clast = min(63, a.L - 1 - qs);
+                sat = __all_sync(0xffffffffu, key < 0 || uj >= mt[clast] + 1.f);
+            }
 #pragma unroll
             for (int c = 0; c < 64; c += 4) {
                 const float4 l4 = *reinterpret_cast<const float4*>(ml + c);
                 const float4 d4 = *reinterpret_cast<const float4*>(md + c);
-                const float4 t4 = *reinterpret_cast<const float4*>(mt + c);
                 const float la[4] = {l4.x, l4.y, l4.z, l4.w};
                 const float da[4] = {d4.x, d4.y, d4.z, d4.w};
-                const float ta[4] = {t4.x, t4.y, t4.z, t4.w};
+                float ta[4] = {0.f, 0.f, 0.f, 0.f};
+                if (SEL && !sat) {
+                    const float4 t4 = *reinterpret_cast<const float4*>(mt + c);
+                    ta[0] = t4.x;
+                    ta[1] = t4.y;
+                    ta[2] = t4.z;
+                    ta[3] = t4.w;
+                }
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
-                    const int i = qs + c + e;
-                    bool ok;
-                    float g = 1.f;
-                    if (SEL) {
-                        const int t = i - a.w;
-                        ok = key >= 0 && i < a.L && t >= key && t < leave;
-                        g = __saturatef(uj - ta[e]);
-                    } else {
-                        ok = key >= 0 && i < a.L && i >= key && i <= key + a.w - 1;
-                    }
-                    const float raw = sv[c + e];
+                    const int cc_ = c + e;
+                    const bool ok = full || (cc_ >= cmin && cc_ <= cmax);
+                    const float g = (SEL && !sat) ? __saturatef(uj - ta[e]) : 1.f;
+                    const float raw = sv[cc_];
                     const float kap = (KEY_SOFT && SEL) ? g : 1.f;
-                    const float p = ok ? ex2(raw * kap * a.scale_log2 - la[e]) : 0.f;
+                    const float p = ok ? ex2(fmaf(raw * kap, a.scale_log2, -la[e])) : 0.f;
                     const float wv = (SEL && !a.mask_st) ? g : 1.f;
-                    const float cc = p * (wv * dp[c + e] - da[e]);
-                    if (SEL && g > 0.f && g < 1.f) {
-                        float gm = p * dp[c + e];
+                    const float cc = p * fmaf(wv, dp[cc_], -da[e]);
+                    if (SEL && !sat && g > 0.f && g < 1.f) {
+                        float gm = p * dp[cc_];
                         if (KEY_SOFT) gm += a.scale * cc * raw;
                         csum += gm;
                     }
-                    sv[c + e] = p * wv;    // P~^T
-                    dp[c + e] = cc * kap;  // dS^T (scale applied in the epilogue)
+                    sv[cc_] = p * wv;    // P~^T
+                    dp[cc_] = cc * kap;  // dS^T (scale applied in the epilogue)
                 }
             }
             colsum += (double)csum;
@@ -384,7 +396,8 @@ struct QSmem {
     static constexpr int kV = kK + 2 * kKT;   // [2]
     static constexpr int kDS = kV + 2 * kKT;  // [2]
     static constexpr int kMeta = kDS + 2 * kDSB;  // [2][3][64] x 4 B
-    static constexpr int kBar = kMeta + 2 * 3 * 64 * 4;
+    static constexpr int kFlags = kMeta + 2 * 3 * 64 * 4;  // [2][4] int
+    static constexpr int kBar = kFlags + 2 * 4 * 4;
     static constexpr int kTmemSlot = kBar + 16 * 8;
     static constexpr int kAlloc = kTmemSlot + 16 + 1024;
 };
@@ -400,6 +413,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(BwdArgs a) {
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SM::kBar);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + SM::kTmemSlot);
     int* meta = reinterpret_cast<int*>(smem + SM::kMeta);  // [stage][key|leave|uf][64]
+    int* tflags = reinterpret_cast<int*>(smem + SM::kFlags);  // [stage][producer warp]
 
     const int qb = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -415,7 +429,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(BwdArgs a) {
     if (threadIdx.x == 0) {
         mbar_init(&bars[QB_QFULL], kProducers);
         for (int s = 0; s < 2; ++s) {
-            mbar_init(&bars[QB_KVFULL + s], kProducers);
+            mbar_init(&bars[QB_KVFULL + s], 2 * kProducers);  // cp.async + flag release
             mbar_init(&bars[QB_KVEMPTY + s], 1);
             mbar_init(&bars[QB_SFULL + s], 1);
             mbar_init(&bars[QB_SEMPTY + s], 128);
@@ -442,6 +456,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(BwdArgs a) {
             const int s = jt & 1;
             if (jt >= 2) mbar_wait(&bars[QB_KVEMPTY + s], ((jt - 2) >> 1) & 1);
             if (jt < n_sel) {
+                const int t_lo = i0 - a.w;
+                const int t_hi = min(i0 + 127, a.L - 1) - a.w;
+                const float tau_hi = t_hi >= 0 ? __ldg(a.tauf + bl + t_hi) : -INFINITY;
+                bool all_ok = true, all_sat = true;
                 for (int c = ptid; c < 64; c += kProducers) {
                     const int idx = jt * 64 + c;
                     const int key = idx < cnt ? __ldg(list + idx) : -1;
@@ -449,7 +467,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(BwdArgs a) {
                     cp_async4(mb, list + (idx < cnt ? idx : 0), idx < cnt);
                     cp_async4(mb + 64 * 4, a.leave + bl + (key >= 0 ? key : 0), key >= 0);
                     cp_async4(mb + 128 * 4, a.uf + bl + (key >= 0 ? key : 0), key >= 0);
+                    if (key >= 0) {
+                        all_ok = all_ok && key <= t_lo && __ldg(a.leave + bl + key) > t_hi;
+                        all_sat = all_sat && __ldg(a.uf + bl + key) >= tau_hi + 1.f;
+                    } else {
+                        all_ok = false;
+                    }
                 }
+                all_ok = __all_sync(0xffffffffu, all_ok);
+                all_sat = __all_sync(0xffffffffu, all_sat);
+                if (lane == 0) tflags[s * 4 + pw] = (all_ok ? 1 : 0) | (all_sat ? 2 : 0);
                 auto kf = [&](int r) {
                     const int idx = jt * 64 + r;
                     return idx < cnt ? __ldg(list + idx) : -1;
@@ -462,6 +489,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(BwdArgs a) {
                 load_tile<D, 64>(sbase + SM::kK + s * SM::kKT, a.k, b, h, a.L, a.H, pw, lane, kf);
                 load_tile<D, 64>(sbase + SM::kV + s * SM::kKT, a.v, b, h, a.L, a.H, pw, lane, kf);
             }
+            mbar_arrive(&bars[QB_KVFULL + s]);
             cp_async_arrive_noinc(&bars[QB_KVFULL + s]);
         }
     } else if (warp == 7) {
@@ -532,6 +560,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(BwdArgs a) {
                 const int* mk = meta + (s * 3) * 64;
                 const int* ml = mk + 64;
                 const float* mu = reinterpret_cast<const float*>(mk + 128);
+                const int fl = tflags[s * 4] & tflags[s * 4 + 1] & tflags[s * 4 + 2];
+                const bool all_ok = (fl & 1) != 0, all_sat = (fl & 2) != 0;
 #pragma unroll
                 for (int c = 0; c < 64; c += 4) {
                     const int4 kj = *reinterpret_cast<const int4*>(mk + c);
@@ -542,14 +572,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(BwdArgs a) {
                     const float ua[4] = {uu.x, uu.y, uu.z, uu.w};
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
-                        const bool ok = i < a.L && kja[e] >= 0 && kja[e] <= t && lva[e] > t;
-                        const float g = __saturatef(ua[e] - tau_i);
+                        const bool ok = i < a.L && (all_ok || (kja[e] <= t && lva[e] > t));
+                        const float g = all_sat ? 1.f : __saturatef(ua[e] - tau_i);
                         const float raw = sv[c + e];
                         const float kap = KEY_SOFT ? g : 1.f;
-                        const float p = ok ? ex2(raw * kap * a.scale_log2 - lse2) : 0.f;
+                        const float p = ok ? ex2(fmaf(raw * kap, a.scale_log2, -lse2)) : 0.f;
                         const float wv = a.mask_st ? 1.f : g;
-                        const float cc = p * (wv * dp[c + e] - dlt);
-                        if (ok && g > 0.f && g < 1.f) {
+                        const float cc = p * fmaf(wv, dp[c + e], -dlt);
+                        if (!all_sat && ok && g > 0.f && g < 1.f) {
                             float gm = p * dp[c + e];
                             if (KEY_SOFT) gm += a.scale * cc * raw;
                             rsum += gm;
@@ -558,12 +588,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(BwdArgs a) {
                     }
                 }
             } else {
-                const int kb0 = jw0 + (jt - n_sel) * 64;
+                const int kb = jw0 + (jt - n_sel) * 64;
+                const int cmin = max(0, max(lo_win, 0) - kb);
+                const int cmax = min(63, i - kb);
+                const bool full = __all_sync(0xffffffffu, cmin <= 0 && cmax >= 63 && i < a.L);
 #pragma unroll
                 for (int c = 0; c < 64; ++c) {
-                    const int key = kb0 + c;
-                    const bool ok = i < a.L && key >= 0 && key >= lo_win && key <= i;
-                    const float p = ok ? ex2(sv[c] * a.scale_log2 - lse2) : 0.f;
+                    const bool ok = full || (i < a.L && c >= cmin && c <= cmax);
+                    const float p = ok ? ex2(fmaf(sv[c], a.scale_log2, -lse2)) : 0.f;
                     dp[c] = p * (dp[c] - dlt);
                 }
             }

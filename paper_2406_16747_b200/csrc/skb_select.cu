@@ -36,10 +36,14 @@ constexpr int kTauThreads = 256;
 constexpr int kOverflowSlots = 16;
 
 // ---------------------------------------------------------------- ranks
+// One thread per position j. The sequence streams through shared memory in
+// stages; within a stage every thread scans 8 values per step (broadcast
+// reads, branch-free counts) and only drops to a per-element walk inside the
+// single 8-group where a count crosses its target.
 __global__ void __launch_bounds__(kRankThreads)
 k_rank_leave(const double* __restrict__ u, int L, int T, int R1, int R2, int* __restrict__ leave1,
              int* __restrict__ leave2) {
-    __shared__ double su[kRankStage];
+    __shared__ __align__(16) double su[kRankStage];
     const int b = blockIdx.y;
     const int j = blockIdx.x * kRankThreads + threadIdx.x;
     const double* ub = u + (int64_t)b * L;
@@ -47,38 +51,77 @@ k_rank_leave(const double* __restrict__ u, int L, int T, int R1, int R2, int* __
     const double uj = active ? ub[j] : 0.0;
     int A = 0, cnt = 0, need1 = 0, need2 = 0;
     int l1 = T, l2 = T;
-    bool done = !active;
+    bool done = !active, past = false;  // past: A final, counting later beaters
     for (int c0 = 0; c0 < T; c0 += kRankStage) {
         if (__syncthreads_and(done)) break;
-        for (int i = threadIdx.x; i < kRankStage; i += kRankThreads)
-            su[i] = c0 + i < T ? ub[c0 + i] : 0.0;
+        for (int i = threadIdx.x; i < kRankStage; i += kRankThreads) su[i] = c0 + i < T ? ub[c0 + i] : 0.0;
         __syncthreads();
-        if (!done) {
-            const int n = min(kRankStage, T - c0);
-            for (int ii = 0; ii < n; ++ii) {
-                const int i = c0 + ii;
-                const double x = su[ii];
-                if (i < j) {
-                    if (x >= uj && ++A >= R2) {  // R2 earlier winners: never in the top R2
-                        l1 = j;
-                        l2 = j;
-                        done = true;
-                        break;
-                    }
-                } else if (i == j) {
-                    need1 = R1 - A;  // A < R2 here
-                    need2 = R2 - A;
-                    if (need1 <= 0) l1 = j;  // never enters the top R1
-                } else if (x > uj) {  // later arrivals win only when strictly larger
-                    ++cnt;
-                    if (cnt == need1) l1 = i;
-                    if (cnt == need2) {
-                        l2 = i;
-                        done = true;
-                        break;
-                    }
+        if (done) continue;
+        const int n = min(kRankStage, T - c0);
+        int ii = 0;
+        if (!past) {
+            // earlier elements: count x >= u_j up to j (exclusive)
+            const int stop = min(n, j - c0);
+            for (; ii + 8 <= stop; ii += 8) {
+                const double2 x0 = *reinterpret_cast<const double2*>(su + ii);
+                const double2 x1 = *reinterpret_cast<const double2*>(su + ii + 2);
+                const double2 x2 = *reinterpret_cast<const double2*>(su + ii + 4);
+                const double2 x3 = *reinterpret_cast<const double2*>(su + ii + 6);
+                A += (x0.x >= uj) + (x0.y >= uj) + (x1.x >= uj) + (x1.y >= uj) + (x2.x >= uj) + (x2.y >= uj) +
+                     (x3.x >= uj) + (x3.y >= uj);
+            }
+            for (; ii < stop; ++ii) A += su[ii] >= uj;
+            if (A >= R2) {  // R2 earlier winners: never in the top R2 (nor the top R1)
+                l1 = j;
+                l2 = j;
+                done = true;
+                continue;
+            }
+            if (stop < n) {  // j lies in this stage
+                need1 = R1 - A;
+                need2 = R2 - A;
+                if (need1 <= 0) l1 = j;
+                past = true;
+                ii = stop + 1;
+            } else {
+                continue;
+            }
+        }
+        // later elements: strictly larger values beat j; find the need1-th and need2-th
+        auto hit = [&](double x, int i) {
+            if (x > uj) {
+                ++cnt;
+                if (cnt == need1) l1 = i;
+                if (cnt == need2) {
+                    l2 = i;
+                    done = true;
                 }
             }
+        };
+        for (; ii < n && (ii & 7); ++ii) {
+            hit(su[ii], c0 + ii);
+            if (done) break;
+        }
+        if (done) continue;
+        for (; ii + 8 <= n; ii += 8) {
+            const double2 x0 = *reinterpret_cast<const double2*>(su + ii);
+            const double2 x1 = *reinterpret_cast<const double2*>(su + ii + 2);
+            const double2 x2 = *reinterpret_cast<const double2*>(su + ii + 4);
+            const double2 x3 = *reinterpret_cast<const double2*>(su + ii + 6);
+            const int g = (x0.x > uj) + (x0.y > uj) + (x1.x > uj) + (x1.y > uj) + (x2.x > uj) + (x2.y > uj) +
+                          (x3.x > uj) + (x3.y > uj);
+            const int nxt = cnt < need1 ? need1 : need2;
+            if (cnt + g >= nxt) {  // a target falls in this group: walk it
+                for (int e = 0; e < 8 && !done; ++e) hit(su[ii + e], c0 + ii + e);
+                if (done) break;
+            } else {
+                cnt += g;
+            }
+        }
+        if (done) continue;
+        for (; ii < n; ++ii) {
+            hit(su[ii], c0 + ii);
+            if (done) break;
         }
     }
     if (active) {
@@ -168,27 +211,45 @@ __device__ bool tau_chunk(const TauArgs& a, int b, int chunk, double* bz, double
         uf = n_ge(bz, mcount, tau0 + 1.0);
     }
 
-    // stream replay on warp 0 (proj/src/stream.cpp:72-152)
+    // stream replay (proj/src/stream.cpp:72-152) for the chunk's arrivals. The
+    // survivors are the sorted band prefix bz[0, ws) plus chunk entries; the
+    // chunk's <= 32 values are ranked once (value desc, earlier arrival first,
+    // i.e. heap order reversed) so set membership is a bitmask and the minima
+    // are bit scans — one thread, no shuffles per pop.
+    __shared__ double s_cv[kChunk];
+    __shared__ int s_rank[kChunk];
+    const int nvalid = min(kChunk, a.T - t0);
     if (threadIdx.x < 32) {
         const int lane = threadIdx.x;
-        const int nvalid = min(kChunk, a.T - t0);
-        const double cz = lane < nvalid ? ub[t0 + lane] : 0.0;
-        bool inS = false, inF = false;
+        const double cz = lane < nvalid ? ub[t0 + lane] : -CUDART_INF;
+        int rank = 0;
+        for (int e = 0; e < nvalid; ++e) {
+            const double y = __shfl_sync(0xffffffffu, cz, e);
+            rank += (y > cz) || (y == cz && e < lane);
+        }
+        if (lane < nvalid) {
+            s_cv[rank] = cz;
+            s_rank[lane] = rank;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t smask = 0, fmask = 0;
         double tau = tau0;
         double sum_s = P[ws], sum_f = P[uf];
-        int frac = 0;
-        if (tau0 > -CUDART_INF) frac = ws - uf;
+        int frac = (tau0 > -CUDART_INF) ? ws - uf : 0;
         for (int e = 0; e < nvalid; ++e) {
             const int t = t0 + e;
-            const double z = __shfl_sync(0xffffffffu, cz, e);
+            const int rk = s_rank[e];
+            const double z = s_cv[rk];
             const double count = (double)(t + 1);
             if (z > tau) {
-                if (lane == e) {
-                    inS = true;
-                    inF = z >= tau + 1.0;
-                }
+                smask |= 1u << rk;
                 sum_s += z;
-                if (z >= tau + 1.0) sum_f += z;
+                if (z >= tau + 1.0) {
+                    fmask |= 1u << rk;
+                    sum_f += z;
+                }
                 if (count < a.k) {
                     tau = -CUDART_INF;
                     frac = 0;
@@ -197,26 +258,16 @@ __device__ bool tau_chunk(const TauArgs& a, int b, int chunk, double* bz, double
                     double last = 0.0;
                     // every iteration pops one entry; the guard only bounds a
                     // numerically broken input (NaN sums) so the GPU never hangs
-                    int guard = 2 * (mcount + kChunk) + 8;
-                    for (; guard > 0; --guard) {
-                        const int cu = uf + __popc(__ballot_sync(0xffffffffu, inF));
-                        const int cw = ws + __popc(__ballot_sync(0xffffffffu, inS));
-                        double smin = inS ? cz : CUDART_INF;
-                        int slane = inS ? lane : -1;
-                        argmin_hi(smin, slane);
-                        double fmn = inF ? cz : CUDART_INF;
-                        int flane = inF ? lane : -1;
-                        argmin_hi(fmn, flane);
-                        // base minima (older indices: chunk entries win value ties)
-                        bool s_base = false, f_base = false;
-                        if (ws > 0 && (slane < 0 || bz[ws - 1] < smin)) {
-                            smin = bz[ws - 1];
-                            s_base = true;
-                        }
-                        if (uf > 0 && (flane < 0 || bz[uf - 1] < fmn)) {
-                            fmn = bz[uf - 1];
-                            f_base = true;
-                        }
+                    for (int guard = 2 * (mcount + kChunk) + 8; guard > 0; --guard) {
+                        const int cu = uf + __popc(fmask);
+                        const int cw = ws + __popc(smask);
+                        // minima: chunk entries (later indices) pop first on value ties
+                        const int sr = smask ? 31 - __clz(smask) : -1;
+                        const int fr = fmask ? 31 - __clz(fmask) : -1;
+                        bool s_chunk = sr >= 0 && (ws == 0 || s_cv[sr] <= bz[ws - 1]);
+                        bool f_chunk = fr >= 0 && (uf == 0 || s_cv[fr] <= bz[uf - 1]);
+                        const double smin = s_chunk ? s_cv[sr] : (ws > 0 ? bz[ws - 1] : CUDART_INF);
+                        const double fmn = f_chunk ? s_cv[fr] : (uf > 0 ? bz[uf - 1] : CUDART_INF);
                         if (cu == cw) {
                             const double hi = fmn - 1.0;
                             const double lo = popped ? last : fmax(tau, hi - 1.0);
@@ -226,8 +277,8 @@ __device__ bool tau_chunk(const TauArgs& a, int b, int chunk, double* bz, double
                                 break;
                             }
                             sum_f -= fmn;
-                            if (f_base) --uf;
-                            else if (lane == flane) inF = false;
+                            if (f_chunk) fmask &= ~(1u << fr);
+                            else --uf;
                             continue;
                         }
                         const double cand = (sum_s - sum_f + (double)cu - a.k) / (double)(cw - cu);
@@ -240,21 +291,19 @@ __device__ bool tau_chunk(const TauArgs& a, int b, int chunk, double* bz, double
                             last = smin;
                             popped = true;
                             sum_s -= smin;
-                            if (s_base) --ws;
-                            else if (lane == slane) inS = false;
+                            if (s_chunk) smask &= ~(1u << sr);
+                            else --ws;
                             if (cw - 1 == 0) break;  // internal guard (reference throws)
                         } else {
                             sum_f -= fmn;
-                            if (f_base) --uf;
-                            else if (lane == flane) inF = false;
+                            if (f_chunk) fmask &= ~(1u << fr);
+                            else --uf;
                         }
                     }
                 }
             }
-            if (lane == 0) {
-                a.tau[(int64_t)b * a.L + t] = tau;
-                a.nfrac[(int64_t)b * a.L + t] = frac;
-            }
+            a.tau[(int64_t)b * a.L + t] = tau;
+            a.nfrac[(int64_t)b * a.L + t] = frac;
         }
     }
     return true;
