@@ -1,19 +1,21 @@
-// K3/K4 tensor-core path (tcgen05 + TMEM), BF16, head_dim 64 or 128.
+// K3 tensor-core forward (tcgen05 + TMEM), BF16, head_dim 64 or 128.
 //
-// Forward (k_fwd_tc): one CTA per (128-query block, head, sequence).
-//   key tiles = [selected-union tiles (gathered rows, per-key interval mask
-//   j <= t_i < leave_j and value gates g = sat(u_j - tau_i))] ++ [window
-//   tiles (contiguous band [i0-w+1, i0+127], causal/window mask)].
-//   Per tile: S = Q K^T (tcgen05, M=N=128, K=d, fp32 in TMEM) ->
-//   softmax warps (one query row per thread): mask, online max with lazy
-//   rescale (only when the max grows by > 2^8), P = exp2(...), gated P~ =
-//   P*g -> bf16 P~ in swizzled smem -> O += P~ V (tcgen05, accumulator in
-//   TMEM). Softmax statistics use the ungated P (proj/src/cache.cpp:373-387:
-//   softmax over Sel U W, value gates applied after, no renormalisation).
+// One CTA per (128-query block, head, sequence). Key tiles of 128 rows:
+//   [selected-union tiles: gathered rows, per-key interval mask
+//    j <= t_i < leave_j, value gates g = sat(u_j - tau_i)]
+//   ++ [window tiles: the contiguous band [i0-w+1, i0+127], band mask].
+// Per tile: S = Q K^T (tcgen05, M=N=128, K=d, fp32 in TMEM, double-buffered)
+// -> two math warpgroups, each owning 64 of the 128 columns of every row:
+// mask, row max (exchanged through smem), lazy rescale (the exponent base
+// moves only when the max grows by > 2^8), P = exp2(.), gated P~ = P*g ->
+// bf16 P~ in 128B-swizzled smem -> O += P~ V (tcgen05, accumulator in TMEM).
+// Softmax statistics use the ungated P: proj/src/cache.cpp:358-393 (softmax
+// over Sel U W, value gates applied after, no renormalisation).
 //
-// Warp roles (256 threads): warps 0-3 softmax/epilogue, warps 4-6 producers
-// (cp.async row gathers into 128B-swizzled tiles, completion tracked by
-// mbarriers), warp 7 TMEM owner + single-thread MMA issuer.
+// Producers fill K/V stages with cp.async row gathers (completion tracked by
+// mbarriers) and publish two per-tile flags so most tiles skip the mask and
+// the gates entirely: bit0 = every key valid for every query of the block,
+// bit1 = every gate saturated (u_j >= tau(t_hi) + 1).
 #include "skb_common.cuh"
 #include "skb_internal.h"
 #include "skb_tc.cuh"
@@ -24,7 +26,6 @@ namespace {
 
 using namespace tc;
 
-constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 constexpr float kRescaleSlack = 8.0f;  // lazy rescale threshold (log2 units)
 
@@ -42,7 +43,6 @@ struct FwdArgs {
     int nqb, qb_cap;
     int B, L, H, w, T, R1;
     float scale_log2;
-    float scale;
     int mask_st;
 };
 
@@ -53,9 +53,10 @@ struct FwdSmem {
     static constexpr int kK = kQ + kTile;
     static constexpr int kV = kK + 2 * kTile;
     static constexpr int kP = kV + 2 * kTile;
-    static constexpr int kMeta = kP + 128 * 128 * 2;   // [2][3][128] x 4 B
-    static constexpr int kFlags = kMeta + 2 * 3 * 128 * 4;  // [2][4] int per-tile flags
-    static constexpr int kBar = kFlags + 2 * 4 * 4;
+    static constexpr int kMeta = kP + 128 * 128 * 2;   // [2][key|leave|uf][128] x 4 B
+    static constexpr int kFlags = kMeta + 2 * 3 * 128 * 4;  // [2][4]
+    static constexpr int kRed = kFlags + 2 * 4 * 4;     // [2 parity][2 halves][128] f32
+    static constexpr int kBar = kRed + 2 * 2 * 128 * 4;
     static constexpr int kTmemSlot = kBar + 16 * 8;
     static constexpr int kBytes = kTmemSlot + 16;
     static constexpr int kAlloc = kBytes + 1024;  // room to align the base to 1024
@@ -71,11 +72,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
     const uint32_t sbase = smem_u32(smem);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SM::kBar);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + SM::kTmemSlot);
-    int* meta = reinterpret_cast<int*>(smem + SM::kMeta);  // [stage][key|leave|uf][128]
-    int* tflags = reinterpret_cast<int*>(smem + SM::kFlags);  // [stage][producer warp]
+    int* meta = reinterpret_cast<int*>(smem + SM::kMeta);
+    int* tflags = reinterpret_cast<int*>(smem + SM::kFlags);
+    float* red = reinterpret_cast<float*>(smem + SM::kRed);
 
     const int qb = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t bl = (int64_t)b * a.L;
     const int i0 = qb * 128;
     const int cnt = (a.R1 > 0) ? a.qb_count[(int64_t)b * a.nqb + qb] : 0;
     const int n_sel = (cnt + 127) / 128;
@@ -91,50 +94,43 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
             mbar_init(&bars[B_KVFULL + s], 2 * kProducers);
             mbar_init(&bars[B_KVEMPTY + s], 1);
             mbar_init(&bars[B_SFULL + s], 1);
-            mbar_init(&bars[B_SEMPTY + s], 128);
+            mbar_init(&bars[B_SEMPTY + s], kMath);
         }
-        mbar_init(&bars[B_PFULL], 128);
+        mbar_init(&bars[B_PFULL], kMath);
         mbar_init(&bars[B_PVDONE], 1);
         mbar_fence_init();
     }
-    if (warp == 7) tmem_alloc<512>(tmem_slot);
+    if (warp == kMmaWarp) tmem_alloc<512>(tmem_slot);
     tc_before_sync();
     __syncthreads();
     tc_after_sync();
     const uint32_t tmem = *tmem_slot;
     const uint32_t tS = tmem, tO = tmem + 256;
 
-    if (warp >= 4 && warp < 7) {
+    if (warp >= kProdWarp0 && warp < kMmaWarp) {
         // ------------------------------------------------------------ producers
-        const int pw = warp - 4, ptid = threadIdx.x - 128;
-        load_tile<D, 128>(sbase + SM::kQ, a.q, b, h, a.L, a.H, pw, lane, [&](int r) {
-            return i0 + r < a.L ? i0 + r : -1;
-        });
+        const int pw = warp - kProdWarp0, ptid = threadIdx.x - kProdWarp0 * 32;
+        load_tile<D, 128>(sbase + SM::kQ, a.q, b, h, a.L, a.H, pw, lane,
+                          [&](int r) { return i0 + r < a.L ? i0 + r : -1; });
         cp_async_arrive_noinc(&bars[B_QFULL]);
+        const int t_lo = i0 - a.w;
+        const int t_hi = min(i0 + 127, a.L - 1) - a.w;
+        const float tau_hi = (t_hi >= 0 && a.R1 > 0) ? __ldg(a.tauf + bl + t_hi) : -INFINITY;
         for (int jt = 0; jt < n; ++jt) {
             const int s = jt & 1;
             if (jt >= 2) mbar_wait(&bars[B_KVEMPTY + s], ((jt - 2) >> 1) & 1);
             if (jt < n_sel) {
-                // metadata (key, leave_j, u_j) for the softmax warps via cp.async, plus
-                // tile flags: bit0 = every key valid for every query of the block
-                // (j <= t_lo and leave_j > t_hi), bit1 = every gate saturated
-                // (u_j >= tau(t_hi) + 1), which let the softmax skip masks/gates.
-                const int t_lo = i0 - a.w;
-                const int t_hi = min(i0 + 127, a.L - 1) - a.w;
-                const float tau_hi = t_hi >= 0 ? __ldg(a.tauf + (int64_t)b * a.L + t_hi) : -INFINITY;
                 bool all_ok = true, all_sat = true;
                 for (int c = ptid; c < 128; c += kProducers) {
                     const int idx = jt * 128 + c;
                     const int key = idx < cnt ? __ldg(list + idx) : -1;
                     const uint32_t mb = smem_u32(meta + (s * 3) * 128 + c);
                     cp_async4(mb, list + (idx < cnt ? idx : 0), idx < cnt);
-                    cp_async4(mb + 128 * 4, a.leave + (int64_t)b * a.L + (key >= 0 ? key : 0), key >= 0);
-                    cp_async4(mb + 256 * 4, a.uf + (int64_t)b * a.L + (key >= 0 ? key : 0), key >= 0);
+                    cp_async4(mb + 128 * 4, a.leave + bl + (key >= 0 ? key : 0), key >= 0);
+                    cp_async4(mb + 256 * 4, a.uf + bl + (key >= 0 ? key : 0), key >= 0);
                     if (key >= 0) {
-                        const int lv = __ldg(a.leave + (int64_t)b * a.L + key);
-                        const float uu = __ldg(a.uf + (int64_t)b * a.L + key);
-                        all_ok = all_ok && key <= t_lo && lv > t_hi;
-                        all_sat = all_sat && uu >= tau_hi + 1.f;
+                        all_ok = all_ok && key <= t_lo && __ldg(a.leave + bl + key) > t_hi;
+                        all_sat = all_sat && __ldg(a.uf + bl + key) >= tau_hi + 1.f;
                     } else {
                         all_ok = false;
                     }
@@ -157,7 +153,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
             mbar_arrive(&bars[B_KVFULL + s]);
             cp_async_arrive_noinc(&bars[B_KVFULL + s]);
         }
-    } else if (warp == 7) {
+    } else if (warp == kMmaWarp) {
         // ------------------------------------------------------------ MMA issuer
         if (lane == 0) {
             constexpr uint32_t idesc_qk = umma_idesc(128, 128, false, false);
@@ -193,36 +189,39 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
         }
         __syncwarp();
     } else {
-        // ------------------------------------------------------------ softmax (warps 0-3)
-        const int r = threadIdx.x;
+        // ------------------------------------------------------------ math (warps 0-7)
+        const int hf = warp >> 2;                // column half: 0 -> cols 0..63, 1 -> 64..127
+        const int r = ((warp & 3) << 5) | lane;  // tile row = TMEM lane
+        const int c0 = hf * 64;
         const int i = i0 + r;
         const int t = i - a.w;
-        const float tau_i = (t >= 0 && a.R1 > 0) ? a.tauf[(int64_t)b * a.L + t] : -INFINITY;
-        const int lo_win = i - a.w + 1;
-        const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
-        float m = -INFINITY, l = 0.f;
-        float sv[128];
+        const float tau_i = (t >= 0 && a.R1 > 0) ? a.tauf[bl + t] : -INFINITY;
+        const int lo_win = max(i - a.w + 1, 0);
+        const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+        const float sl2 = a.scale_log2;
+        float m = -INFINITY, l = 0.f;  // l: this half's partial row sum
+        float sv[64];
         for (int jt = 0; jt < n; ++jt) {
             const int s = jt & 1;
             const bool is_sel = jt < n_sel;
             mbar_wait(&bars[B_SFULL + s], (jt >> 1) & 1);
-            mbar_wait(&bars[B_KVFULL + s], (jt >> 1) & 1);  // metadata visibility
+            mbar_wait(&bars[B_KVFULL + s], (jt >> 1) & 1);  // metadata + flags visibility
             tc_after_sync();
-#pragma unroll
-            for (int c = 0; c < 4; ++c) tmem_ld32(tS + lane_off + s * 128 + c * 32, sv + c * 32);
+            tmem_ld32(tS + lane_off + s * 128 + c0, sv);
+            tmem_ld32(tS + lane_off + s * 128 + c0 + 32, sv + 32);
             tmem_wait_ld();
             tc_before_sync();
             mbar_arrive(&bars[B_SEMPTY + s]);
 
-            const int* mk = meta + (s * 3) * 128;
+            const int* mk = meta + (s * 3) * 128 + c0;
             const int* ml = mk + 128;
             const float* mu = reinterpret_cast<const float*>(mk + 256);
-            int fl = 0;
+            int fl = 3;
             if (is_sel) {
                 fl = tflags[s * 4] & tflags[s * 4 + 1] & tflags[s * 4 + 2];
                 if (!(fl & 1)) {  // per-key interval mask j <= t < leave_j
 #pragma unroll
-                    for (int c = 0; c < 128; c += 4) {
+                    for (int c = 0; c < 64; c += 4) {
                         const int4 kj = *reinterpret_cast<const int4*>(mk + c);
                         const int4 lv = *reinterpret_cast<const int4*>(ml + c);
                         sv[c + 0] = (kj.x <= t && lv.x > t) ? sv[c + 0] : -INFINITY;
@@ -233,7 +232,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
                 }
                 if (KEY_SOFT) {  // gated logits (proj/src/cache.cpp:368-369)
 #pragma unroll
-                    for (int c = 0; c < 128; c += 4) {
+                    for (int c = 0; c < 64; c += 4) {
                         const float4 uu = *reinterpret_cast<const float4*>(mu + c);
                         sv[c + 0] *= __saturatef(uu.x - tau_i);
                         sv[c + 1] *= __saturatef(uu.y - tau_i);
@@ -242,42 +241,49 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
                     }
                 }
             } else {
-                // window band of this row inside the tile: columns [cmin, cmax]
-                const int kb = jw0 + (jt - n_sel) * 128;
-                const int cmin = max(0, max(lo_win, 0) - kb);
-                const int cmax = min(127, i - kb);
-                if (__any_sync(0xffffffffu, cmin > 0 || cmax < 127)) {
+                // this row's window band inside the tile: columns [cmin, cmax]
+                const int kb = jw0 + (jt - n_sel) * 128 + c0;
+                const int cmin = lo_win - kb;
+                const int cmax = i - kb;
+                if (__any_sync(0xffffffffu, cmin > 0 || cmax < 63)) {
 #pragma unroll
-                    for (int c = 0; c < 128; ++c) sv[c] = (c >= cmin && c <= cmax) ? sv[c] : -INFINITY;
+                    for (int c = 0; c < 64; ++c) sv[c] = (c >= cmin && c <= cmax) ? sv[c] : -INFINITY;
                 }
             }
-            float mr = -INFINITY;
+            // row max over both halves
+            float mr = sv[0];
 #pragma unroll
-            for (int c = 0; c < 128; ++c) mr = fmaxf(mr, sv[c]);
-            const float mt = mr * a.scale_log2;  // scale > 0: max commutes with scaling
-            // lazy rescale: move the exponent base only when the max grows by > 2^8
+            for (int c = 1; c < 64; ++c) mr = fmaxf(mr, sv[c]);
+            float* rb = red + (jt & 1) * 256;
+            rb[hf * 128 + r] = mr;
+            math_bar();
+            mr = fmaxf(mr, rb[(hf ^ 1) * 128 + r]);
+            const float mt = mr * sl2;  // scale > 0: max commutes with scaling
             float fac = 1.f;
             bool need = false;
             if (mt > m + kRescaleSlack) {
-                if (l > 0.f) {
+                if (m != -INFINITY) {
                     fac = ex2(m - mt);
                     l *= fac;
                     need = true;
                 }
                 m = mt;
             }
-            float psum = 0.f;
-            const float mb = m == -INFINITY ? 0.f : m;  // fully masked so far: avoid -inf - -inf
+            const float nmb = m == -INFINITY ? 0.f : -m;  // fully masked so far: avoid -inf - -inf
+            float ps0 = 0.f, ps1 = 0.f;
 #pragma unroll
-            for (int c = 0; c < 128; ++c) {
-                const float p = ex2(fmaf(sv[c], a.scale_log2, -mb));  // masked: exp2(-inf) = 0
-                psum += p;
-                sv[c] = p;
+            for (int c = 0; c < 64; c += 2) {
+                const float p0 = ex2(fmaf(sv[c], sl2, nmb));  // masked: exp2(-inf) = 0
+                const float p1 = ex2(fmaf(sv[c + 1], sl2, nmb));
+                ps0 += p0;
+                ps1 += p1;
+                sv[c] = p0;
+                sv[c + 1] = p1;
             }
-            l += psum;
+            l += ps0 + ps1;
             if (is_sel && !a.mask_st && !(fl & 2)) {  // value gates (cache.cpp:381-382)
 #pragma unroll
-                for (int c = 0; c < 128; c += 4) {
+                for (int c = 0; c < 64; c += 4) {
                     const float4 uu = *reinterpret_cast<const float4*>(mu + c);
                     sv[c + 0] *= __saturatef(uu.x - tau_i);
                     sv[c + 1] *= __saturatef(uu.y - tau_i);
@@ -289,11 +295,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
                 mbar_wait(&bars[B_PVDONE], (jt - 1) & 1);
                 tc_after_sync();
             }
-            if (__any_sync(0xffffffffu, need)) {
+            if (__any_sync(0xffffffffu, need)) {  // rescale this half's O columns
                 float ov[32];
 #pragma unroll
-                for (int c = 0; c < D / 32; ++c) {
-                    const uint32_t ta = tO + lane_off + c * 32;
+                for (int c = 0; c < D / 64; ++c) {
+                    const uint32_t ta = tO + lane_off + hf * (D / 2) + c * 32;
                     tmem_ld32(ta, ov);
                     tmem_wait_ld();
 #pragma unroll
@@ -302,27 +308,31 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
                 }
                 tmem_wait_st();
             }
-            // P~ row -> swizzled smem (K-major A operand of the PV MMA)
-            const uint32_t prow = sbase + SM::kP;
+            // P~ (this half's 64 keys = one swizzle atom column) -> smem
+            const uint32_t pb = sbase + SM::kP + hf * (128 * 128);
 #pragma unroll
-            for (int ch = 0; ch < 16; ++ch) {
+            for (int ch = 0; ch < 8; ++ch) {
                 const float* x = sv + ch * 8;
-                st_shared_v4(prow + sw_off(r, ch, 128), pack_bf16(x[0], x[1]), pack_bf16(x[2], x[3]),
+                st_shared_v4(pb + r * 128 + ((ch ^ (r & 7)) << 4), pack_bf16(x[0], x[1]), pack_bf16(x[2], x[3]),
                              pack_bf16(x[4], x[5]), pack_bf16(x[6], x[7]));
             }
             fence_proxy_async();
             tc_before_sync();
             mbar_arrive(&bars[B_PFULL]);
         }
-        // epilogue: O / l, lse
+        // epilogue: O / l, lse. The row's l is the sum of both halves' partials.
+        float* rb = red + (n & 1) * 256;
+        rb[hf * 128 + r] = l;
+        math_bar();
+        const float lrow = l + rb[(hf ^ 1) * 128 + r];
         mbar_wait(&bars[B_PVDONE], (n - 1) & 1);
         tc_after_sync();
-        const float inv = l > 0.f ? 1.f / l : 0.f;
-        __nv_bfloat16* orow = a.o + (((int64_t)b * a.L + i) * a.H + h) * D;
+        const float inv = lrow > 0.f ? 1.f / lrow : 0.f;
+        __nv_bfloat16* orow = a.o + ((bl + (i < a.L ? i : 0)) * a.H + h) * D + hf * (D / 2);
 #pragma unroll
-        for (int c = 0; c < D / 32; ++c) {
+        for (int c = 0; c < D / 64; ++c) {
             float ov[32];
-            tmem_ld32(tO + lane_off + c * 32, ov);
+            tmem_ld32(tO + lane_off + hf * (D / 2) + c * 32, ov);
             tmem_wait_ld();
             if (i < a.L) {
 #pragma unroll
@@ -336,12 +346,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
                 }
             }
         }
-        if (i < a.L) a.lse[((int64_t)b * a.H + h) * a.L + i] = (double)((m + __log2f(l)) * kLn2);
+        if (hf == 0 && i < a.L) a.lse[((int64_t)b * a.H + h) * a.L + i] = (double)((m + __log2f(lrow)) * kLn2);
     }
     tc_before_sync();
     __syncthreads();
     tc_after_sync();
-    if (warp == 7) tmem_dealloc<512>(tmem);
+    if (warp == kMmaWarp) tmem_dealloc<512>(tmem);
 }
 
 template <int D, bool KS>
@@ -389,7 +399,6 @@ void run_attn_fwd_tc(const skb_attn_desc& d, const void* q, const void* k, const
     a.T = std::max(0, a.L - a.w);
     a.R1 = (int)floor_k(d.k);
     const double scale = d.scale > 0.0 ? d.scale : 1.0 / std::sqrt((double)d.head_dim);
-    a.scale = (float)scale;
     a.scale_log2 = (float)(scale * 1.4426950408889634);
     a.mask_st = d.mask_mode;
     dim3 grid((unsigned)s.nqb, (unsigned)d.heads, (unsigned)d.batch);

@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_tc(BwdArgs a) {
         s_range[1] = 0;
     }
     __syncthreads();
-    if (threadIdx.x < 128) {
+    if (threadIdx.x < 128) {  // warps 0-3 cover the 128 keys
         const int key = key_of(threadIdx.x);
         int hi = 0;
         if (key >= 0) hi = SEL ? __ldg(a.leave + bl + key) + a.w : key + a.w;  // exclusive
@@ -139,14 +139,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_tc(BwdArgs a) {
             mbar_init(&bars[KB_QDFULL + s], kProducers);
             mbar_init(&bars[KB_QDEMPTY + s], 1);
             mbar_init(&bars[KB_SFULL + s], 1);
-            mbar_init(&bars[KB_SEMPTY + s], 128);
+            mbar_init(&bars[KB_SEMPTY + s], kMath);
             mbar_init(&bars[KB_PDSEMPTY + s], 1);
         }
-        mbar_init(&bars[KB_PDSFULL], 128);
+        mbar_init(&bars[KB_PDSFULL], kMath);
         mbar_init(&bars[KB_ACCDONE], 1);
         mbar_fence_init();
     }
-    if (warp == 7) tmem_alloc<512>(tmem_slot);
+    if (warp == kMmaWarp) tmem_alloc<512>(tmem_slot);
     tc_before_sync();
     __syncthreads();
     tc_after_sync();
@@ -156,8 +156,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_tc(BwdArgs a) {
     const int q_hi = min(a.L, s_range[1]);
     const int nq = q_hi > q_lo ? (q_hi - q_lo + 63) / 64 : 0;
 
-    if (warp >= 4 && warp < 7) {
-        const int pw = warp - 4, ptid = threadIdx.x - 128;
+    if (warp >= kProdWarp0 && warp < kMmaWarp) {
+        const int pw = warp - kProdWarp0, ptid = threadIdx.x - kProdWarp0 * 32;
         load_tile<D, 128>(sbase + SM::kK, a.k, b, h, a.L, a.H, pw, lane, key_of);
         load_tile<D, 128>(sbase + SM::kV, a.v, b, h, a.L, a.H, pw, lane, key_of);
         cp_async_arrive_noinc(&bars[KB_KVFULL]);
@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_tc(BwdArgs a) {
             }
             cp_async_arrive_noinc(&bars[KB_QDFULL + s]);
         }
-    } else if (warp == 7) {
+    } else if (warp == kMmaWarp) {
         if (lane == 0 && nq > 0) {
             constexpr uint32_t id_s = umma_idesc(128, 64, false, false);
             constexpr uint32_t id_acc = umma_idesc(128, D, false, true);
@@ -225,46 +225,45 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_tc(BwdArgs a) {
         }
         __syncwarp();
     } else {
-        // key rows (warps 0-3): elementwise backward
-        const int r = threadIdx.x;
+        // key rows: two math warpgroups, each owning 32 of the 64 query columns
+        const int hf = warp >> 2;
+        const int r = ((warp & 3) << 5) | lane;
         const int key = key_of(r);
         const int leave = (SEL && key >= 0) ? __ldg(a.leave + bl + key) : 0;
         const float uj = (SEL && key >= 0) ? __ldg(a.uf + bl + key) : 0.f;
-        const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
-        double colsum = 0.0;
+        const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+        const float sl2 = a.scale_log2;
+        // queries reading this key form one interval: window [j, j+w), selected
+        // [j+w, leave_j+w) (proj/src/cache.cpp:259-311)
+        const int lo_i = SEL ? key + a.w : key;
+        const int hi_i = min(a.L, SEL ? leave + a.w : key + a.w);  // exclusive
+        float colsum = 0.f;
         for (int qt = 0; qt < nq; ++qt) {
             const int s = qt & 1;
-            const int qs = q_lo + qt * 64;
+            const int qs = q_lo + qt * 64 + hf * 32;  // first query of this thread's columns
             mbar_wait(&bars[KB_SFULL + s], (qt >> 1) & 1);
             mbar_wait(&bars[KB_QDFULL + s], (qt >> 1) & 1);
             tc_after_sync();
-            float sv[64], dp[64];
-            tmem_ld32(tS + lane_off + s * 64, sv);
-            tmem_ld32(tS + lane_off + s * 64 + 32, sv + 32);
-            tmem_ld32(tP + lane_off + s * 64, dp);
-            tmem_ld32(tP + lane_off + s * 64 + 32, dp + 32);
+            float sv[32], dp[32];
+            tmem_ld32(tS + lane_off + s * 64 + hf * 32, sv);
+            tmem_ld32(tP + lane_off + s * 64 + hf * 32, dp);
             tmem_wait_ld();
             tc_before_sync();
             mbar_arrive(&bars[KB_SEMPTY + s]);
-            const float* ml = qmeta + (s * 3) * 64;
+            const float* ml = qmeta + (s * 3) * 64 + hf * 32;
             const float* md = ml + 64;
             const float* mt = ml + 128;
-            float csum = 0.f;
-            // queries reading this key form one interval: window [j, j+w), selected
-            // [j+w, leave_j+w) (proj/src/cache.cpp:259-311) -> columns [cmin, cmax]
-            const int lo_i = SEL ? key + a.w : key;
-            const int hi_i = min(a.L, SEL ? leave + a.w : key + a.w);  // exclusive
-            const int cmin = key >= 0 ? max(0, lo_i - qs) : 64;
-            const int cmax = key >= 0 ? min(63, hi_i - 1 - qs) : -1;
-            const bool full = __all_sync(0xffffffffu, cmin <= 0 && cmax >= 63);
-            // gates all saturated for this key over the tile (tau is nondecreasing)
-            bool sat = true;
+            const int cmin = key >= 0 ? lo_i - qs : 32;
+            const int cmax = key >= 0 ? hi_i - 1 - qs : -1;
+            const bool full = __all_sync(0xffffffffu, cmin <= 0 && cmax >= 31);
+            bool sat = true;  // all gates of this key saturated over these columns (tau nondecreasing)
             if (SEL) {
-                const int clast = min(63, a.L - 1 - qs);
+                const int clast = max(0, min(31, a.L - 1 - qs));
                 sat = __all_sync(0xffffffffu, key < 0 || uj >= mt[clast] + 1.f);
             }
+            float csum = 0.f;
 #pragma unroll
-            for (int c = 0; c < 64; c += 4) {
+            for (int c = 0; c < 32; c += 4) {
                 const float4 l4 = *reinterpret_cast<const float4*>(ml + c);
                 const float4 d4 = *reinterpret_cast<const float4*>(md + c);
                 const float la[4] = {l4.x, l4.y, l4.z, l4.w};
@@ -280,51 +279,52 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_tc(BwdArgs a) {
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                     const int cc_ = c + e;
-                    const bool ok = full || (cc_ >= cmin && cc_ <= cmax);
+                    const float raw = (full || (cc_ >= cmin && cc_ <= cmax)) ? sv[cc_] : -INFINITY;
                     const float g = (SEL && !sat) ? __saturatef(uj - ta[e]) : 1.f;
-                    const float raw = sv[cc_];
                     const float kap = (KEY_SOFT && SEL) ? g : 1.f;
-                    const float p = ok ? ex2(fmaf(raw * kap, a.scale_log2, -la[e])) : 0.f;
+                    const float p = ex2(fmaf(raw * kap, sl2, -la[e]));  // masked: 0
                     const float wv = (SEL && !a.mask_st) ? g : 1.f;
                     const float cc = p * fmaf(wv, dp[cc_], -da[e]);
-                    if (SEL && !sat && g > 0.f && g < 1.f) {
+                    if (SEL && !sat) {
                         float gm = p * dp[cc_];
-                        if (KEY_SOFT) gm += a.scale * cc * raw;
-                        csum += gm;
+                        if (KEY_SOFT) gm += a.scale * cc * sv[cc_];
+                        csum += (g > 0.f && g < 1.f) ? gm : 0.f;
                     }
                     sv[cc_] = p * wv;    // P~^T
                     dp[cc_] = cc * kap;  // dS^T (scale applied in the epilogue)
                 }
             }
-            colsum += (double)csum;
+            colsum += csum;
             if (qt >= 2) mbar_wait(&bars[KB_PDSEMPTY + s], ((qt - 2) >> 1) & 1);
             const uint32_t ptb = sbase + SM::kPT + s * SM::kPD, dsb = sbase + SM::kDS + s * SM::kPD;
 #pragma unroll
-            for (int ch = 0; ch < 8; ++ch) {
+            for (int ch = 0; ch < 4; ++ch) {
+                const int pc = ((hf * 4 + ch) ^ (r & 7)) << 4;
                 const float* x = sv + ch * 8;
-                st_shared_v4(ptb + sw_off(r, ch, 128), pack_bf16(x[0], x[1]), pack_bf16(x[2], x[3]),
+                st_shared_v4(ptb + r * 128 + pc, pack_bf16(x[0], x[1]), pack_bf16(x[2], x[3]),
                              pack_bf16(x[4], x[5]), pack_bf16(x[6], x[7]));
                 const float* y = dp + ch * 8;
-                st_shared_v4(dsb + sw_off(r, ch, 128), pack_bf16(y[0], y[1]), pack_bf16(y[2], y[3]),
+                st_shared_v4(dsb + r * 128 + pc, pack_bf16(y[0], y[1]), pack_bf16(y[2], y[3]),
                              pack_bf16(y[4], y[5]), pack_bf16(y[6], y[7]));
             }
             fence_proxy_async();
             tc_before_sync();
             mbar_arrive(&bars[KB_PDSFULL]);
         }
-        if (SEL && key >= 0 && colsum != 0.0) atomicAdd(a.colsum + bl + key, colsum);
+        if (SEL && key >= 0 && colsum != 0.f) atomicAdd(a.colsum + bl + key, (double)colsum);
         if (nq > 0) {
             mbar_wait(&bars[KB_ACCDONE], 0);
             tc_after_sync();
         }
         const bool has_sel = !SEL && key >= 0 && a.R1 > 0 && key < a.T && __ldg(a.leave + bl + key) > key;
-        const int64_t rowoff = ((bl + (key >= 0 ? key : 0)) * a.H + h) * D;
+        const int64_t rowoff = ((bl + (key >= 0 ? key : 0)) * a.H + h) * D + hf * (D / 2);
 #pragma unroll
-        for (int c = 0; c < D / 32; ++c) {
+        for (int c = 0; c < D / 64; ++c) {
             float dv[32], dk[32];
+            const int col = hf * (D / 2) + c * 32;
             if (nq > 0) {
-                tmem_ld32(tDV + lane_off + c * 32, dv);
-                tmem_ld32(tDK + lane_off + c * 32, dk);
+                tmem_ld32(tDV + lane_off + col, dv);
+                tmem_ld32(tDK + lane_off + col, dk);
                 tmem_wait_ld();
             } else {
 #pragma unroll
@@ -381,7 +381,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_tc(BwdArgs a) {
     tc_before_sync();
     __syncthreads();
     tc_after_sync();
-    if (warp == 7) tmem_dealloc<512>(tmem);
+    if (warp == kMmaWarp) tmem_dealloc<512>(tmem);
 }
 
 // ------------------------------------------------------------------ dQ
@@ -432,22 +432,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(BwdArgs a) {
             mbar_init(&bars[QB_KVFULL + s], 2 * kProducers);  // cp.async + flag release
             mbar_init(&bars[QB_KVEMPTY + s], 1);
             mbar_init(&bars[QB_SFULL + s], 1);
-            mbar_init(&bars[QB_SEMPTY + s], 128);
+            mbar_init(&bars[QB_SEMPTY + s], kMath);
             mbar_init(&bars[QB_DSEMPTY + s], 1);
         }
-        mbar_init(&bars[QB_DSFULL], 128);
+        mbar_init(&bars[QB_DSFULL], kMath);
         mbar_init(&bars[QB_DQDONE], 1);
         mbar_fence_init();
     }
-    if (warp == 7) tmem_alloc<512>(tmem_slot);
+    if (warp == kMmaWarp) tmem_alloc<512>(tmem_slot);
     tc_before_sync();
     __syncthreads();
     tc_after_sync();
     const uint32_t tmem = *tmem_slot;
     const uint32_t tS = tmem, tP = tmem + 128, tDQ = tmem + 256;
 
-    if (warp >= 4 && warp < 7) {
-        const int pw = warp - 4, ptid = threadIdx.x - 128;
+    if (warp >= kProdWarp0 && warp < kMmaWarp) {
+        const int pw = warp - kProdWarp0, ptid = threadIdx.x - kProdWarp0 * 32;
         auto qf = [&](int r) { return i0 + r < a.L ? i0 + r : -1; };
         load_tile<D, 128>(sbase + SM::kQ, a.q, b, h, a.L, a.H, pw, lane, qf);
         load_tile<D, 128>(sbase + SM::kDO, a.dout, b, h, a.L, a.H, pw, lane, qf);
@@ -492,7 +492,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(BwdArgs a) {
             mbar_arrive(&bars[QB_KVFULL + s]);
             cp_async_arrive_noinc(&bars[QB_KVFULL + s]);
         }
-    } else if (warp == 7) {
+    } else if (warp == kMmaWarp) {
         if (lane == 0) {
             constexpr uint32_t id_s = umma_idesc(128, 64, false, false);
             constexpr uint32_t id_dq = umma_idesc(128, D, false, true);
@@ -532,15 +532,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(BwdArgs a) {
         }
         __syncwarp();
     } else {
-        const int r = threadIdx.x;
+        // query rows: two math warpgroups, each owning 32 of the 64 key columns
+        const int hf = warp >> 2;
+        const int r = ((warp & 3) << 5) | lane;
         const int i = i0 + r;
         const int t = i - a.w;
         const float tau_i = (t >= 0 && a.R1 > 0) ? a.tauf[bl + t] : -INFINITY;
-        const int lo_win = i - a.w + 1;
+        const int lo_win = max(i - a.w + 1, 0);
         const int64_t hl = ((int64_t)b * a.H + h) * a.L;
-        const float lse2 = i < a.L ? a.lse2[hl + i] : 0.f;
+        const float nlse2 = i < a.L ? -a.lse2[hl + i] : -INFINITY;  // i >= L: every p = 0
         const float dlt = i < a.L ? a.delta[hl + i] : 0.f;
-        const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+        const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+        const float sl2 = a.scale_log2;
         float rsum = 0.f;
         for (int jt = 0; jt < n; ++jt) {
             const int s = jt & 1;
@@ -548,64 +551,75 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(BwdArgs a) {
             mbar_wait(&bars[QB_SFULL + s], (jt >> 1) & 1);
             mbar_wait(&bars[QB_KVFULL + s], (jt >> 1) & 1);
             tc_after_sync();
-            float sv[64], dp[64];
-            tmem_ld32(tS + lane_off + s * 64, sv);
-            tmem_ld32(tS + lane_off + s * 64 + 32, sv + 32);
-            tmem_ld32(tP + lane_off + s * 64, dp);
-            tmem_ld32(tP + lane_off + s * 64 + 32, dp + 32);
+            float sv[32], dp[32];
+            tmem_ld32(tS + lane_off + s * 64 + hf * 32, sv);
+            tmem_ld32(tP + lane_off + s * 64 + hf * 32, dp);
             tmem_wait_ld();
             tc_before_sync();
             mbar_arrive(&bars[QB_SEMPTY + s]);
             if (is_sel) {
-                const int* mk = meta + (s * 3) * 64;
+                const int* mk = meta + (s * 3) * 64 + hf * 32;
                 const int* ml = mk + 64;
                 const float* mu = reinterpret_cast<const float*>(mk + 128);
                 const int fl = tflags[s * 4] & tflags[s * 4 + 1] & tflags[s * 4 + 2];
-                const bool all_ok = (fl & 1) != 0, all_sat = (fl & 2) != 0;
+                if (!(fl & 1)) {  // per-key interval mask j <= t < leave_j
 #pragma unroll
-                for (int c = 0; c < 64; c += 4) {
-                    const int4 kj = *reinterpret_cast<const int4*>(mk + c);
-                    const int4 lv = *reinterpret_cast<const int4*>(ml + c);
-                    const float4 uu = *reinterpret_cast<const float4*>(mu + c);
-                    const int kja[4] = {kj.x, kj.y, kj.z, kj.w};
-                    const int lva[4] = {lv.x, lv.y, lv.z, lv.w};
-                    const float ua[4] = {uu.x, uu.y, uu.z, uu.w};
+                    for (int c = 0; c < 32; c += 4) {
+                        const int4 kj = *reinterpret_cast<const int4*>(mk + c);
+                        const int4 lv = *reinterpret_cast<const int4*>(ml + c);
+                        sv[c + 0] = (kj.x <= t && lv.x > t) ? sv[c + 0] : -INFINITY;
+                        sv[c + 1] = (kj.y <= t && lv.y > t) ? sv[c + 1] : -INFINITY;
+                        sv[c + 2] = (kj.z <= t && lv.z > t) ? sv[c + 2] : -INFINITY;
+                        sv[c + 3] = (kj.w <= t && lv.w > t) ? sv[c + 3] : -INFINITY;
+                    }
+                }
+                if (!(fl & 2)) {  // fractional gates present
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const bool ok = i < a.L && (all_ok || (kja[e] <= t && lva[e] > t));
-                        const float g = all_sat ? 1.f : __saturatef(ua[e] - tau_i);
-                        const float raw = sv[c + e];
-                        const float kap = KEY_SOFT ? g : 1.f;
-                        const float p = ok ? ex2(fmaf(raw * kap, a.scale_log2, -lse2)) : 0.f;
-                        const float wv = a.mask_st ? 1.f : g;
-                        const float cc = p * fmaf(wv, dp[c + e], -dlt);
-                        if (!all_sat && ok && g > 0.f && g < 1.f) {
+                    for (int c = 0; c < 32; c += 4) {
+                        const float4 uu = *reinterpret_cast<const float4*>(mu + c);
+                        const float ua[4] = {uu.x, uu.y, uu.z, uu.w};
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const float g = __saturatef(ua[e] - tau_i);
+                            const float raw = sv[c + e];
+                            const float kap = KEY_SOFT ? g : 1.f;
+                            const float p = ex2(fmaf(raw * kap, sl2, nlse2));
+                            const float wv = a.mask_st ? 1.f : g;
+                            const float cc = p * fmaf(wv, dp[c + e], -dlt);
                             float gm = p * dp[c + e];
                             if (KEY_SOFT) gm += a.scale * cc * raw;
-                            rsum += gm;
+                            rsum += (g > 0.f && g < 1.f) ? gm : 0.f;
+                            dp[c + e] = cc * kap;
                         }
-                        dp[c + e] = cc * kap;
+                    }
+                } else {  // all gates 1: plain softmax backward
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) {
+                        const float p = ex2(fmaf(sv[c], sl2, nlse2));
+                        dp[c] = p * (dp[c] - dlt);
                     }
                 }
             } else {
-                const int kb = jw0 + (jt - n_sel) * 64;
-                const int cmin = max(0, max(lo_win, 0) - kb);
-                const int cmax = min(63, i - kb);
-                const bool full = __all_sync(0xffffffffu, cmin <= 0 && cmax >= 63 && i < a.L);
+                const int kb = jw0 + (jt - n_sel) * 64 + hf * 32;
+                const int cmin = lo_win - kb;
+                const int cmax = i - kb;
+                if (__any_sync(0xffffffffu, cmin > 0 || cmax < 31)) {
 #pragma unroll
-                for (int c = 0; c < 64; ++c) {
-                    const bool ok = full || (i < a.L && c >= cmin && c <= cmax);
-                    const float p = ok ? ex2(fmaf(sv[c], a.scale_log2, -lse2)) : 0.f;
+                    for (int c = 0; c < 32; ++c) sv[c] = (c >= cmin && c <= cmax) ? sv[c] : -INFINITY;
+                }
+#pragma unroll
+                for (int c = 0; c < 32; ++c) {
+                    const float p = ex2(fmaf(sv[c], sl2, nlse2));
                     dp[c] = p * (dp[c] - dlt);
                 }
             }
             if (jt >= 2) mbar_wait(&bars[QB_DSEMPTY + s], ((jt - 2) >> 1) & 1);
             const uint32_t dsb = sbase + SM::kDS + s * SM::kDSB;
 #pragma unroll
-            for (int ch = 0; ch < 8; ++ch) {
+            for (int ch = 0; ch < 4; ++ch) {
                 const float* y = dp + ch * 8;
-                st_shared_v4(dsb + sw_off(r, ch, 128), pack_bf16(y[0], y[1]), pack_bf16(y[2], y[3]),
-                             pack_bf16(y[4], y[5]), pack_bf16(y[6], y[7]));
+                st_shared_v4(dsb + r * 128 + (((hf * 4 + ch) ^ (r & 7)) << 4), pack_bf16(y[0], y[1]),
+                             pack_bf16(y[2], y[3]), pack_bf16(y[4], y[5]), pack_bf16(y[6], y[7]));
             }
             fence_proxy_async();
             tc_before_sync();
@@ -614,11 +628,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(BwdArgs a) {
         mbar_wait(&bars[QB_DQDONE], 0);
         tc_after_sync();
         if (i < a.L && t >= 0 && a.R1 > 0 && rsum != 0.f) atomicAdd(a.rowsum + bl + t, (double)rsum);
-        __nv_bfloat16* orow = a.dq + ((bl + (i < a.L ? i : 0)) * a.H + h) * D;
+        __nv_bfloat16* orow = a.dq + ((bl + (i < a.L ? i : 0)) * a.H + h) * D + hf * (D / 2);
 #pragma unroll
-        for (int c = 0; c < D / 32; ++c) {
+        for (int c = 0; c < D / 64; ++c) {
             float x[32];
-            tmem_ld32(tDQ + lane_off + c * 32, x);
+            tmem_ld32(tDQ + lane_off + hf * (D / 2) + c * 32, x);
             tmem_wait_ld();
             if (i < a.L) {
 #pragma unroll
@@ -636,7 +650,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(BwdArgs a) {
     tc_before_sync();
     __syncthreads();
     tc_after_sync();
-    if (warp == 7) tmem_dealloc<512>(tmem);
+    if (warp == kMmaWarp) tmem_dealloc<512>(tmem);
 }
 
 template <class K>

@@ -31,14 +31,16 @@ __device__ __forceinline__ void mbar_fence_init() {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// try_wait with a suspend-time hint: a waiting warp sleeps in hardware instead
+// of spinning through issue slots the math warps need.
 __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
     uint32_t ok;
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
         "selp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(ok)
-        : "r"(addr), "r"(parity)
+        : "r"(addr), "r"(parity), "r"(1000000u)
         : "memory");
     return ok != 0;
 }
@@ -48,7 +50,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     const uint32_t addr = smem_u32(bar);
     uint32_t spins = 0;
     while (!mbar_try_wait(addr, parity)) {
-        if (++spins > (1u << 28)) __trap();
+        if (++spins > (1u << 24)) __trap();
     }
 }
 // cp.async completion of this thread's prior copies arrives on the barrier.
@@ -189,11 +191,18 @@ __device__ __forceinline__ float ex2(float x) {
 }
 
 // ------------------------------------------------------------------ CTA shape
-// 256 threads: warps 0-3 math (one TMEM lane / tile row each), warps 4-6
-// producers (cp.async), warp 7 TMEM owner + single-thread MMA issuer. 256
-// (not 288) keeps the 255-register budget per thread.
-constexpr int kThreads = 256;
+// 384 threads: warps 0-3 and 4-7 are two math warpgroups that split every
+// tile's columns (each thread owns one TMEM lane = tile row and half the
+// columns, so each SM sub-partition runs two math warps), warps 8-10 are
+// cp.async producers, warp 11 owns TMEM and issues tcgen05.mma (one thread).
+constexpr int kThreads = 384;
+constexpr int kMath = 256;
 constexpr int kProducers = 96;
+constexpr int kProdWarp0 = 8;
+constexpr int kMmaWarp = 11;
+
+// Named barrier over the 256 math threads (id 1; 0 is __syncthreads).
+__device__ __forceinline__ void math_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
 // Load an R-row tile of a [B, L, H, D] bf16 tensor into the swizzled layout.
 // keyfn(row) gives the source row (< 0 or >= L: zero-filled). The producer

@@ -173,7 +173,7 @@ def test_selection_long_sequence(cuda, oracle, kind):
     for t in (0, 1, kf - 2, kf - 1, kf, kf + 1, T // 3, T // 2, T - 2, T - 1):
         if t < 0 or t >= T:
             continue
-        members = np.nonzero((np.arange(T) <= t) & (leave > t))[0]
+        members = np.nonzero((np.arange(T) <= t) & (leave[:T] > t))[0]
         pref = np.arange(t + 1)
         best = pref[np.lexsort((pref, -u[: t + 1]))][: min(kf, t + 1)]
         np.testing.assert_array_equal(members, np.sort(best))
