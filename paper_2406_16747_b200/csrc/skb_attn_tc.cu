@@ -120,6 +120,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
             const int s = jt & 1;
             if (jt >= 2) mbar_wait(&bars[B_KVEMPTY + s], ((jt - 2) >> 1) & 1);
             if (jt < n_sel) {
+                // the row gathers first: they are the long pole
+                auto kf = [&](int r) {
+                    const int idx = jt * 128 + r;
+                    return idx < cnt ? __ldg(list + idx) : -1;
+                };
+                load_tile<D, 128>(sbase + SM::kK + s * SM::kTile, a.k, b, h, a.L, a.H, pw, lane, kf);
+                load_tile<D, 128>(sbase + SM::kV + s * SM::kTile, a.v, b, h, a.L, a.H, pw, lane, kf);
                 bool all_ok = true, all_sat = true;
                 for (int c = ptid; c < 128; c += kProducers) {
                     const int idx = jt * 128 + c;
@@ -138,12 +145,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
                 all_ok = __all_sync(0xffffffffu, all_ok);
                 all_sat = __all_sync(0xffffffffu, all_sat);
                 if (lane == 0) tflags[s * 4 + pw] = (all_ok ? 1 : 0) | (all_sat ? 2 : 0);
-                auto kf = [&](int r) {
-                    const int idx = jt * 128 + r;
-                    return idx < cnt ? __ldg(list + idx) : -1;
-                };
-                load_tile<D, 128>(sbase + SM::kK + s * SM::kTile, a.k, b, h, a.L, a.H, pw, lane, kf);
-                load_tile<D, 128>(sbase + SM::kV + s * SM::kTile, a.v, b, h, a.L, a.H, pw, lane, kf);
             } else {
                 const int kb0 = jw0 + (jt - n_sel) * 128;
                 auto kf = [&](int r) { return kb0 + r; };
@@ -219,6 +220,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
             int fl = 3;
             if (is_sel) {
                 fl = tflags[s * 4] & tflags[s * 4 + 1] & tflags[s * 4 + 2];
+                if (KEY_SOFT) {  // gated logits (proj/src/cache.cpp:368-369)
+#pragma unroll
+                    for (int c = 0; c < 64; c += 4) {
+                        const float4 uu = *reinterpret_cast<const float4*>(mu + c);
+                        sv[c + 0] *= __saturatef(uu.x - tau_i);
+                        sv[c + 1] *= __saturatef(uu.y - tau_i);
+                        sv[c + 2] *= __saturatef(uu.z - tau_i);
+                        sv[c + 3] *= __saturatef(uu.w - tau_i);
+                    }
+                }
                 if (!(fl & 1)) {  // per-key interval mask j <= t < leave_j
 #pragma unroll
                     for (int c = 0; c < 64; c += 4) {
@@ -228,16 +239,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
                         sv[c + 1] = (kj.y <= t && lv.y > t) ? sv[c + 1] : -INFINITY;
                         sv[c + 2] = (kj.z <= t && lv.z > t) ? sv[c + 2] : -INFINITY;
                         sv[c + 3] = (kj.w <= t && lv.w > t) ? sv[c + 3] : -INFINITY;
-                    }
-                }
-                if (KEY_SOFT) {  // gated logits (proj/src/cache.cpp:368-369)
-#pragma unroll
-                    for (int c = 0; c < 64; c += 4) {
-                        const float4 uu = *reinterpret_cast<const float4*>(mu + c);
-                        sv[c + 0] *= __saturatef(uu.x - tau_i);
-                        sv[c + 1] *= __saturatef(uu.y - tau_i);
-                        sv[c + 2] *= __saturatef(uu.z - tau_i);
-                        sv[c + 3] *= __saturatef(uu.w - tau_i);
                     }
                 }
             } else {

@@ -279,10 +279,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_tc(BwdArgs a) {
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                     const int cc_ = c + e;
-                    const float raw = (full || (cc_ >= cmin && cc_ <= cmax)) ? sv[cc_] : -INFINITY;
                     const float g = (SEL && !sat) ? __saturatef(uj - ta[e]) : 1.f;
                     const float kap = (KEY_SOFT && SEL) ? g : 1.f;
-                    const float p = ex2(fmaf(raw * kap, sl2, -la[e]));  // masked: 0
+                    const float x = (full || (cc_ >= cmin && cc_ <= cmax)) ? sv[cc_] * kap : -INFINITY;
+                    const float p = ex2(fmaf(x, sl2, -la[e]));  // masked: 0
                     const float wv = (SEL && !a.mask_st) ? g : 1.f;
                     const float cc = p * fmaf(wv, dp[cc_], -da[e]);
                     if (SEL && !sat) {
@@ -456,6 +456,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(BwdArgs a) {
             const int s = jt & 1;
             if (jt >= 2) mbar_wait(&bars[QB_KVEMPTY + s], ((jt - 2) >> 1) & 1);
             if (jt < n_sel) {
+                // the row gathers first: they are the long pole
+                auto kf = [&](int r) {
+                    const int idx = jt * 64 + r;
+                    return idx < cnt ? __ldg(list + idx) : -1;
+                };
+                load_tile<D, 64>(sbase + SM::kK + s * SM::kKT, a.k, b, h, a.L, a.H, pw, lane, kf);
+                load_tile<D, 64>(sbase + SM::kV + s * SM::kKT, a.v, b, h, a.L, a.H, pw, lane, kf);
                 const int t_lo = i0 - a.w;
                 const int t_hi = min(i0 + 127, a.L - 1) - a.w;
                 const float tau_hi = t_hi >= 0 ? __ldg(a.tauf + bl + t_hi) : -INFINITY;
@@ -477,12 +484,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(BwdArgs a) {
                 all_ok = __all_sync(0xffffffffu, all_ok);
                 all_sat = __all_sync(0xffffffffu, all_sat);
                 if (lane == 0) tflags[s * 4 + pw] = (all_ok ? 1 : 0) | (all_sat ? 2 : 0);
-                auto kf = [&](int r) {
-                    const int idx = jt * 64 + r;
-                    return idx < cnt ? __ldg(list + idx) : -1;
-                };
-                load_tile<D, 64>(sbase + SM::kK + s * SM::kKT, a.k, b, h, a.L, a.H, pw, lane, kf);
-                load_tile<D, 64>(sbase + SM::kV + s * SM::kKT, a.v, b, h, a.L, a.H, pw, lane, kf);
             } else {
                 const int kb0 = jw0 + (jt - n_sel) * 64;
                 auto kf = [&](int r) { return kb0 + r; };
@@ -583,7 +584,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(BwdArgs a) {
                             const float g = __saturatef(ua[e] - tau_i);
                             const float raw = sv[c + e];
                             const float kap = KEY_SOFT ? g : 1.f;
-                            const float p = ex2(fmaf(raw * kap, sl2, nlse2));
+                            // masked logits are -inf: keep them -inf under a zero gate
+                            const float x = (KEY_SOFT && raw == -INFINITY) ? raw : raw * kap;
+                            const float p = ex2(fmaf(x, sl2, nlse2));
                             const float wv = a.mask_st ? 1.f : g;
                             const float cc = p * fmaf(wv, dp[c + e], -dlt);
                             float gm = p * dp[c + e];

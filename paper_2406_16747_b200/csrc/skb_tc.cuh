@@ -207,18 +207,32 @@ __device__ __forceinline__ void math_bar() { asm volatile("bar.sync 1, 256;" :::
 // Load an R-row tile of a [B, L, H, D] bf16 tensor into the swizzled layout.
 // keyfn(row) gives the source row (< 0 or >= L: zero-filled). The producer
 // warps stride over row groups (one group = the rows a warp covers per copy).
+// All row keys are fetched first (independent loads, one latency), then the
+// copies are issued — a gathered key must not sit on each copy's critical path.
 template <int D, int R, class KeyFn>
 __device__ __forceinline__ void load_tile(uint32_t dst, const __nv_bfloat16* base, int b, int h, int L, int H,
                                           int pw, int lane, KeyFn keyfn) {
     constexpr int kChunks = D / 8;              // 16-byte chunks per row
     constexpr int kRowsPerIter = 32 / kChunks;  // rows per warp per copy
+    constexpr int kGroups = R / kRowsPerIter;
+    constexpr int kPW = kProducers / 32;
+    constexpr int kIters = (kGroups + kPW - 1) / kPW;
     const int sub = lane / kChunks, ch = lane % kChunks;
-    for (int g = pw; g < R / kRowsPerIter; g += kProducers / 32) {
-        const int r = g * kRowsPerIter + sub;
-        const int key = keyfn(r);
-        const bool ok = key >= 0 && key < L;
-        const __nv_bfloat16* src = base + (((int64_t)b * L + (ok ? key : 0)) * H + h) * D + ch * 8;
-        cp_async16(dst + sw_off(r, ch, R), src, ok);
+    int keys[kIters];
+#pragma unroll
+    for (int it = 0; it < kIters; ++it) {
+        const int g = pw + kPW * it;
+        keys[it] = g < kGroups ? keyfn(g * kRowsPerIter + sub) : -1;
+    }
+#pragma unroll
+    for (int it = 0; it < kIters; ++it) {
+        const int g = pw + kPW * it;
+        if (g < kGroups) {
+            const int r = g * kRowsPerIter + sub;
+            const bool ok = keys[it] >= 0 && keys[it] < L;
+            const __nv_bfloat16* src = base + (((int64_t)b * L + (ok ? keys[it] : 0)) * H + h) * D + ch * 8;
+            cp_async16(dst + sw_off(r, ch, R), src, ok);
+        }
     }
 }
 
