@@ -57,12 +57,13 @@ struct FwdSmem {
     static constexpr int kFlags = kMeta + 2 * 3 * 128 * 4;  // [2][4]
     static constexpr int kRed = kFlags + 2 * 4 * 4;     // [2 parity][2 halves][128] f32
     static constexpr int kBar = kRed + 2 * 2 * 128 * 4;
-    static constexpr int kTmemSlot = kBar + 16 * 8;
+    static constexpr int kTmemSlot = kBar + 16 * 8;  // 15 barriers
     static constexpr int kBytes = kTmemSlot + 16;
     static constexpr int kAlloc = kBytes + 1024;  // room to align the base to 1024
 };
 
-enum { B_QFULL = 0, B_KVFULL = 1, B_KVEMPTY = 3, B_SFULL = 5, B_SEMPTY = 7, B_PFULL = 9, B_PVDONE = 10 };
+enum { B_QFULL = 0, B_KFULL = 1, B_KEMPTY = 3, B_SFULL = 5, B_SEMPTY = 7, B_PFULL = 9, B_PVDONE = 10,
+       B_VFULL = 11, B_VEMPTY = 13 };
 
 template <int D, bool KEY_SOFT>
 __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
@@ -90,9 +91,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
     if (threadIdx.x == 0) {
         mbar_init(&bars[B_QFULL], kProducers);
         for (int s = 0; s < 2; ++s) {
-            // 96 cp.async completions + 96 plain arrivals (which release the tile flags)
-            mbar_init(&bars[B_KVFULL + s], 2 * kProducers);
-            mbar_init(&bars[B_KVEMPTY + s], 1);
+            // V: 96 cp.async completions + 96 plain arrivals (which release the tile flags)
+            mbar_init(&bars[B_KFULL + s], kProducers);
+            mbar_init(&bars[B_KEMPTY + s], 1);
+            mbar_init(&bars[B_VFULL + s], 2 * kProducers);
+            mbar_init(&bars[B_VEMPTY + s], 1);
             mbar_init(&bars[B_SFULL + s], 1);
             mbar_init(&bars[B_SEMPTY + s], kMath);
         }
@@ -116,17 +119,27 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
         const int t_lo = i0 - a.w;
         const int t_hi = min(i0 + 127, a.L - 1) - a.w;
         const float tau_hi = (t_hi >= 0 && a.R1 > 0) ? __ldg(a.tauf + bl + t_hi) : -INFINITY;
+        // K is released by the QK^T commit and V by the PV commit, so the K ring
+        // runs ahead of V: the next K gather starts as soon as a QK^T retires.
         for (int jt = 0; jt < n; ++jt) {
             const int s = jt & 1;
-            if (jt >= 2) mbar_wait(&bars[B_KVEMPTY + s], ((jt - 2) >> 1) & 1);
-            if (jt < n_sel) {
-                // the row gathers first: they are the long pole
-                auto kf = [&](int r) {
+            const bool sel = jt < n_sel;
+            const int kb0 = jw0 + (jt - n_sel) * 128;
+            auto kf = [&](int r) {
+                if (sel) {
                     const int idx = jt * 128 + r;
                     return idx < cnt ? __ldg(list + idx) : -1;
-                };
-                load_tile<D, 128>(sbase + SM::kK + s * SM::kTile, a.k, b, h, a.L, a.H, pw, lane, kf);
-                load_tile<D, 128>(sbase + SM::kV + s * SM::kTile, a.v, b, h, a.L, a.H, pw, lane, kf);
+                }
+                return kb0 + r;
+            };
+            if (jt >= 2) mbar_wait(&bars[B_KEMPTY + s], ((jt - 2) >> 1) & 1);
+            load_tile<D, 128>(sbase + SM::kK + s * SM::kTile, a.k, b, h, a.L, a.H, pw, lane, kf);
+            cp_async_arrive_noinc(&bars[B_KFULL + s]);
+            // V stage: rows + the tile's metadata/flags (read by the softmax, so they
+            // must live until PV(jt) retires)
+            if (jt >= 2) mbar_wait(&bars[B_VEMPTY + s], ((jt - 2) >> 1) & 1);
+            load_tile<D, 128>(sbase + SM::kV + s * SM::kTile, a.v, b, h, a.L, a.H, pw, lane, kf);
+            if (sel) {
                 bool all_ok = true, all_sat = true;
                 for (int c = ptid; c < 128; c += kProducers) {
                     const int idx = jt * 128 + c;
@@ -145,14 +158,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
                 all_ok = __all_sync(0xffffffffu, all_ok);
                 all_sat = __all_sync(0xffffffffu, all_sat);
                 if (lane == 0) tflags[s * 4 + pw] = (all_ok ? 1 : 0) | (all_sat ? 2 : 0);
-            } else {
-                const int kb0 = jw0 + (jt - n_sel) * 128;
-                auto kf = [&](int r) { return kb0 + r; };
-                load_tile<D, 128>(sbase + SM::kK + s * SM::kTile, a.k, b, h, a.L, a.H, pw, lane, kf);
-                load_tile<D, 128>(sbase + SM::kV + s * SM::kTile, a.v, b, h, a.L, a.H, pw, lane, kf);
             }
-            mbar_arrive(&bars[B_KVFULL + s]);
-            cp_async_arrive_noinc(&bars[B_KVFULL + s]);
+            mbar_arrive(&bars[B_VFULL + s]);
+            cp_async_arrive_noinc(&bars[B_VFULL + s]);
         }
     } else if (warp == kMmaWarp) {
         // ------------------------------------------------------------ MMA issuer
@@ -162,7 +170,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
             mbar_wait(&bars[B_QFULL], 0);
             fence_proxy_async();
             auto pv = [&](int j) {
+                mbar_wait(&bars[B_VFULL + (j & 1)], (j >> 1) & 1);
                 mbar_wait(&bars[B_PFULL], j & 1);
+                fence_proxy_async();
                 tc_after_sync();
                 const uint32_t vb = sbase + SM::kV + (j & 1) * SM::kTile;
 #pragma unroll
@@ -170,11 +180,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
                     umma_f16(tO, desc_kmajor(sbase + SM::kP, 128, kk), desc_mnmajor(vb, 128, kk), idesc_pv,
                              (j > 0 || kk > 0) ? 1u : 0u);
                 umma_commit(&bars[B_PVDONE]);
-                umma_commit(&bars[B_KVEMPTY + (j & 1)]);
+                umma_commit(&bars[B_VEMPTY + (j & 1)]);
             };
             for (int jt = 0; jt < n; ++jt) {
                 const int s = jt & 1;
-                mbar_wait(&bars[B_KVFULL + s], (jt >> 1) & 1);
+                mbar_wait(&bars[B_KFULL + s], (jt >> 1) & 1);
                 fence_proxy_async();
                 if (jt >= 2) mbar_wait(&bars[B_SEMPTY + s], ((jt - 2) >> 1) & 1);
                 tc_after_sync();
@@ -184,6 +194,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
                     umma_f16(tS + s * 128, desc_kmajor(sbase + SM::kQ, 128, kk), desc_kmajor(kb, 128, kk),
                              idesc_qk, kk > 0 ? 1u : 0u);
                 umma_commit(&bars[B_SFULL + s]);
+                umma_commit(&bars[B_KEMPTY + s]);
                 if (jt >= 1) pv(jt - 1);
             }
             pv(n - 1);
@@ -206,7 +217,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
             const int s = jt & 1;
             const bool is_sel = jt < n_sel;
             mbar_wait(&bars[B_SFULL + s], (jt >> 1) & 1);
-            mbar_wait(&bars[B_KVFULL + s], (jt >> 1) & 1);  // metadata + flags visibility
+            mbar_wait(&bars[B_VFULL + s], (jt >> 1) & 1);  // metadata + flags visibility
             tc_after_sync();
             tmem_ld32(tS + lane_off + s * 128 + c0, sv);
             tmem_ld32(tS + lane_off + s * 128 + c0 + 32, sv + 32);

@@ -385,6 +385,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_tc(BwdArgs a) {
 }
 
 // ------------------------------------------------------------------ dQ
+constexpr int kNS = 3;  // K/V ring depth of the dQ kernel
+
 template <int D>
 struct QSmem {
     static constexpr int kQT = 128 * D * 2;  // 128-query tile
@@ -392,17 +394,17 @@ struct QSmem {
     static constexpr int kDSB = 128 * 64 * 2;
     static constexpr int kQ = 0;
     static constexpr int kDO = kQ + kQT;
-    static constexpr int kK = kDO + kQT;      // [2]
-    static constexpr int kV = kK + 2 * kKT;   // [2]
-    static constexpr int kDS = kV + 2 * kKT;  // [2]
-    static constexpr int kMeta = kDS + 2 * kDSB;  // [2][3][64] x 4 B
-    static constexpr int kFlags = kMeta + 2 * 3 * 64 * 4;  // [2][4] int
-    static constexpr int kBar = kFlags + 2 * 4 * 4;
-    static constexpr int kTmemSlot = kBar + 16 * 8;
+    static constexpr int kK = kDO + kQT;            // [kNS]
+    static constexpr int kV = kK + kNS * kKT;       // [kNS]
+    static constexpr int kDS = kV + kNS * kKT;      // [2]
+    static constexpr int kMeta = kDS + 2 * kDSB;    // [kNS][3][64] x 4 B
+    static constexpr int kFlags = kMeta + kNS * 3 * 64 * 4;  // [kNS][4] int
+    static constexpr int kBar = kFlags + kNS * 4 * 4;
+    static constexpr int kTmemSlot = kBar + 24 * 8;
     static constexpr int kAlloc = kTmemSlot + 16 + 1024;
 };
-enum { QB_QFULL = 0, QB_KVFULL = 1, QB_KVEMPTY = 3, QB_SFULL = 5, QB_SEMPTY = 7, QB_DSFULL = 9,
-       QB_DSEMPTY = 10, QB_DQDONE = 12 };
+enum { QB_QFULL = 0, QB_KVFULL = 1, QB_KVEMPTY = 4, QB_SFULL = 7, QB_SEMPTY = 9, QB_DSFULL = 11,
+       QB_DSEMPTY = 12, QB_DQDONE = 14 };
 
 template <int D, bool KEY_SOFT>
 __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(BwdArgs a) {
@@ -428,9 +430,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(BwdArgs a) {
 
     if (threadIdx.x == 0) {
         mbar_init(&bars[QB_QFULL], kProducers);
-        for (int s = 0; s < 2; ++s) {
+        for (int s = 0; s < kNS; ++s) {
             mbar_init(&bars[QB_KVFULL + s], 2 * kProducers);  // cp.async + flag release
             mbar_init(&bars[QB_KVEMPTY + s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
             mbar_init(&bars[QB_SFULL + s], 1);
             mbar_init(&bars[QB_SEMPTY + s], kMath);
             mbar_init(&bars[QB_DSEMPTY + s], 1);
@@ -453,8 +457,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(BwdArgs a) {
         load_tile<D, 128>(sbase + SM::kDO, a.dout, b, h, a.L, a.H, pw, lane, qf);
         cp_async_arrive_noinc(&bars[QB_QFULL]);
         for (int jt = 0; jt < n; ++jt) {
-            const int s = jt & 1;
-            if (jt >= 2) mbar_wait(&bars[QB_KVEMPTY + s], ((jt - 2) >> 1) & 1);
+            const int s = jt % kNS;  // K/V stage
+            if (jt >= kNS) mbar_wait(&bars[QB_KVEMPTY + s], ((jt - kNS) / kNS) & 1);
             if (jt < n_sel) {
                 // the row gathers first: they are the long pole
                 auto kf = [&](int r) {
@@ -500,24 +504,24 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(BwdArgs a) {
             mbar_wait(&bars[QB_QFULL], 0);
             fence_proxy_async();
             auto dq = [&](int j) {
-                const int s = j & 1;
+                const int s = j & 1, ks = j % kNS;
                 mbar_wait(&bars[QB_DSFULL], j & 1);
                 tc_after_sync();
-                const uint32_t dsb = sbase + SM::kDS + s * SM::kDSB, kb = sbase + SM::kK + s * SM::kKT;
+                const uint32_t dsb = sbase + SM::kDS + s * SM::kDSB, kb = sbase + SM::kK + ks * SM::kKT;
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk)
                     umma_f16(tDQ, desc_kmajor(dsb, 128, kk), desc_mnmajor(kb, 64, kk), id_dq,
                              (j > 0 || kk > 0) ? 1u : 0u);
-                umma_commit(&bars[QB_KVEMPTY + s]);
+                umma_commit(&bars[QB_KVEMPTY + ks]);
                 umma_commit(&bars[QB_DSEMPTY + s]);
             };
             for (int jt = 0; jt < n; ++jt) {
-                const int s = jt & 1;
-                mbar_wait(&bars[QB_KVFULL + s], (jt >> 1) & 1);
+                const int s = jt & 1, ks = jt % kNS;
+                mbar_wait(&bars[QB_KVFULL + ks], (jt / kNS) & 1);
                 fence_proxy_async();
                 if (jt >= 2) mbar_wait(&bars[QB_SEMPTY + s], ((jt - 2) >> 1) & 1);
                 tc_after_sync();
-                const uint32_t kb = sbase + SM::kK + s * SM::kKT, vb = sbase + SM::kV + s * SM::kKT;
+                const uint32_t kb = sbase + SM::kK + ks * SM::kKT, vb = sbase + SM::kV + ks * SM::kKT;
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk) {
                     umma_f16(tS + s * 64, desc_kmajor(sbase + SM::kQ, 128, kk), desc_kmajor(kb, 64, kk), id_s,
@@ -549,8 +553,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(BwdArgs a) {
         for (int jt = 0; jt < n; ++jt) {
             const int s = jt & 1;
             const bool is_sel = jt < n_sel;
+            const int ks = jt % kNS;
             mbar_wait(&bars[QB_SFULL + s], (jt >> 1) & 1);
-            mbar_wait(&bars[QB_KVFULL + s], (jt >> 1) & 1);
+            mbar_wait(&bars[QB_KVFULL + ks], (jt / kNS) & 1);
             tc_after_sync();
             float sv[32], dp[32];
             tmem_ld32(tS + lane_off + s * 64 + hf * 32, sv);
@@ -559,10 +564,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(BwdArgs a) {
             tc_before_sync();
             mbar_arrive(&bars[QB_SEMPTY + s]);
             if (is_sel) {
-                const int* mk = meta + (s * 3) * 64 + hf * 32;
+                const int* mk = meta + (ks * 3) * 64 + hf * 32;
                 const int* ml = mk + 64;
                 const float* mu = reinterpret_cast<const float*>(mk + 128);
-                const int fl = tflags[s * 4] & tflags[s * 4 + 1] & tflags[s * 4 + 2];
+                const int fl = tflags[ks * 4] & tflags[ks * 4 + 1] & tflags[ks * 4 + 2];
                 if (!(fl & 1)) {  // per-key interval mask j <= t < leave_j
 #pragma unroll
                     for (int c = 0; c < 32; c += 4) {
@@ -590,7 +595,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(BwdArgs a) {
                             const float wv = a.mask_st ? 1.f : g;
                             const float cc = p * fmaf(wv, dp[c + e], -dlt);
                             float gm = p * dp[c + e];
-                            if (KEY_SOFT) gm += a.scale * cc * raw;
+                            if (KEY_SOFT) gm += a.scale * cc * (raw == -INFINITY ? 0.f : raw);
                             rsum += (g > 0.f && g < 1.f) ? gm : 0.f;
                             dp[c + e] = cc * kap;
                         }
