@@ -46,24 +46,25 @@ struct FwdArgs {
     int mask_st;
 };
 
+constexpr int kKS = 3;  // K ring depth (V ring: 2). P~ lives in TMEM, not smem.
+
 template <int D>
 struct FwdSmem {
     static constexpr int kTile = 128 * D * 2;  // bytes of a 128-row bf16 tile
     static constexpr int kQ = 0;
-    static constexpr int kK = kQ + kTile;
-    static constexpr int kV = kK + 2 * kTile;
-    static constexpr int kP = kV + 2 * kTile;
-    static constexpr int kMeta = kP + 128 * 128 * 2;   // [2][key|leave|uf][128] x 4 B
+    static constexpr int kK = kQ + kTile;          // [kKS]
+    static constexpr int kV = kK + kKS * kTile;    // [2]
+    static constexpr int kMeta = kV + 2 * kTile;   // [2][key|leave|uf][128] x 4 B
     static constexpr int kFlags = kMeta + 2 * 3 * 128 * 4;  // [2][4]
     static constexpr int kRed = kFlags + 2 * 4 * 4;     // [2 parity][2 halves][128] f32
     static constexpr int kBar = kRed + 2 * 2 * 128 * 4;
-    static constexpr int kTmemSlot = kBar + 16 * 8;  // 15 barriers
+    static constexpr int kTmemSlot = kBar + 24 * 8;
     static constexpr int kBytes = kTmemSlot + 16;
     static constexpr int kAlloc = kBytes + 1024;  // room to align the base to 1024
 };
 
-enum { B_QFULL = 0, B_KFULL = 1, B_KEMPTY = 3, B_SFULL = 5, B_SEMPTY = 7, B_PFULL = 9, B_PVDONE = 10,
-       B_VFULL = 11, B_VEMPTY = 13 };
+enum { B_QFULL = 0, B_KFULL = 1, B_KEMPTY = 4, B_SFULL = 7, B_SEMPTY = 9, B_PFULL = 11, B_PVDONE = 12,
+       B_VFULL = 13, B_VEMPTY = 15 };  // 17 barriers
 
 template <int D, bool KEY_SOFT>
 __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
@@ -90,10 +91,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
 
     if (threadIdx.x == 0) {
         mbar_init(&bars[B_QFULL], kProducers);
-        for (int s = 0; s < 2; ++s) {
-            // V: 96 cp.async completions + 96 plain arrivals (which release the tile flags)
+        for (int s = 0; s < kKS; ++s) {
             mbar_init(&bars[B_KFULL + s], kProducers);
             mbar_init(&bars[B_KEMPTY + s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            // V: 96 cp.async completions + 96 plain arrivals (which release the tile flags)
             mbar_init(&bars[B_VFULL + s], 2 * kProducers);
             mbar_init(&bars[B_VEMPTY + s], 1);
             mbar_init(&bars[B_SFULL + s], 1);
@@ -132,9 +135,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
                 }
                 return kb0 + r;
             };
-            if (jt >= 2) mbar_wait(&bars[B_KEMPTY + s], ((jt - 2) >> 1) & 1);
-            load_tile<D, 128>(sbase + SM::kK + s * SM::kTile, a.k, b, h, a.L, a.H, pw, lane, kf);
-            cp_async_arrive_noinc(&bars[B_KFULL + s]);
+            const int ks = jt % kKS;
+            if (jt >= kKS) mbar_wait(&bars[B_KEMPTY + ks], ((jt - kKS) / kKS) & 1);
+            load_tile<D, 128>(sbase + SM::kK + ks * SM::kTile, a.k, b, h, a.L, a.H, pw, lane, kf);
+            cp_async_arrive_noinc(&bars[B_KFULL + ks]);
             // V stage: rows + the tile's metadata/flags (read by the softmax, so they
             // must live until PV(jt) retires)
             if (jt >= 2) mbar_wait(&bars[B_VEMPTY + s], ((jt - 2) >> 1) & 1);
@@ -175,26 +179,27 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
                 fence_proxy_async();
                 tc_after_sync();
                 const uint32_t vb = sbase + SM::kV + (j & 1) * SM::kTile;
+                const uint32_t pa = tS + (j & 1) * 128;  // P~ packed over this tile's S columns
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk)
-                    umma_f16(tO, desc_kmajor(sbase + SM::kP, 128, kk), desc_mnmajor(vb, 128, kk), idesc_pv,
-                             (j > 0 || kk > 0) ? 1u : 0u);
+                    umma_f16_ts(tO, pa + kk * 8, desc_mnmajor(vb, 128, kk), idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
                 umma_commit(&bars[B_PVDONE]);
                 umma_commit(&bars[B_VEMPTY + (j & 1)]);
             };
             for (int jt = 0; jt < n; ++jt) {
                 const int s = jt & 1;
-                mbar_wait(&bars[B_KFULL + s], (jt >> 1) & 1);
+                const int ks = jt % kKS;
+                mbar_wait(&bars[B_KFULL + ks], (jt / kKS) & 1);
                 fence_proxy_async();
                 if (jt >= 2) mbar_wait(&bars[B_SEMPTY + s], ((jt - 2) >> 1) & 1);
                 tc_after_sync();
-                const uint32_t kb = sbase + SM::kK + s * SM::kTile;
+                const uint32_t kb = sbase + SM::kK + ks * SM::kTile;
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk)
                     umma_f16(tS + s * 128, desc_kmajor(sbase + SM::kQ, 128, kk), desc_kmajor(kb, 128, kk),
                              idesc_qk, kk > 0 ? 1u : 0u);
                 umma_commit(&bars[B_SFULL + s]);
-                umma_commit(&bars[B_KEMPTY + s]);
+                umma_commit(&bars[B_KEMPTY + ks]);
                 if (jt >= 1) pv(jt - 1);
             }
             pv(n - 1);
@@ -320,15 +325,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
                 }
                 tmem_wait_st();
             }
-            // P~ (this half's 64 keys = one swizzle atom column) -> smem
-            const uint32_t pb = sbase + SM::kP + hf * (128 * 128);
+            // P~ (this half's 64 keys) -> TMEM over this tile's consumed S columns,
+            // packed bf16x2: the A operand of the PV MMA
+            {
+                uint32_t pk[16];
 #pragma unroll
-            for (int ch = 0; ch < 8; ++ch) {
-                const float* x = sv + ch * 8;
-                st_shared_v4(pb + r * 128 + ((ch ^ (r & 7)) << 4), pack_bf16(x[0], x[1]), pack_bf16(x[2], x[3]),
-                             pack_bf16(x[4], x[5]), pack_bf16(x[6], x[7]));
+                for (int e = 0; e < 16; ++e) pk[e] = pack_bf16(sv[2 * e], sv[2 * e + 1]);
+                tmem_st16u(tS + lane_off + s * 128 + hf * 32, pk);
+#pragma unroll
+                for (int e = 0; e < 16; ++e) pk[e] = pack_bf16(sv[32 + 2 * e], sv[33 + 2 * e]);
+                tmem_st16u(tS + lane_off + s * 128 + hf * 32 + 16, pk);
+                tmem_wait_st();
             }
-            fence_proxy_async();
             tc_before_sync();
             mbar_arrive(&bars[B_PFULL]);
         }
