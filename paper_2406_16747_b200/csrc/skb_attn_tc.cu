@@ -54,17 +54,17 @@ struct FwdSmem {
     static constexpr int kQ = 0;
     static constexpr int kK = kQ + kTile;          // [kKS]
     static constexpr int kV = kK + kKS * kTile;    // [2]
-    static constexpr int kMeta = kV + 2 * kTile;   // [2][key|leave|uf][128] x 4 B
-    static constexpr int kFlags = kMeta + 2 * 3 * 128 * 4;  // [2][4]
-    static constexpr int kRed = kFlags + 2 * 4 * 4;     // [2 parity][2 halves][128] f32
+    static constexpr int kMeta = kV + 2 * kTile;   // [kKS][key|leave|uf][128] x 4 B
+    static constexpr int kFlags = kMeta + kKS * 3 * 128 * 4;  // [kKS][4]
+    static constexpr int kRed = kFlags + kKS * 4 * 4;   // [2 parity][2 halves][128] f32
     static constexpr int kBar = kRed + 2 * 2 * 128 * 4;
-    static constexpr int kTmemSlot = kBar + 24 * 8;
+    static constexpr int kTmemSlot = kBar + 24 * 8;  // 23 barriers
     static constexpr int kBytes = kTmemSlot + 16;
     static constexpr int kAlloc = kBytes + 1024;  // room to align the base to 1024
 };
 
 enum { B_QFULL = 0, B_KFULL = 1, B_KEMPTY = 4, B_SFULL = 7, B_SEMPTY = 9, B_PFULL = 11, B_PVDONE = 12,
-       B_VFULL = 13, B_VEMPTY = 15 };  // 17 barriers
+       B_VFULL = 13, B_VEMPTY = 15, B_MFULL = 17, B_MEMPTY = 20 };  // 23 barriers
 
 template <int D, bool KEY_SOFT>
 __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
@@ -94,10 +94,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
         for (int s = 0; s < kKS; ++s) {
             mbar_init(&bars[B_KFULL + s], kProducers);
             mbar_init(&bars[B_KEMPTY + s], 1);
+            // metadata: 96 cp.async completions + 96 plain arrivals (which release the flags)
+            mbar_init(&bars[B_MFULL + s], 2 * kProducers);
+            mbar_init(&bars[B_MEMPTY + s], kMath);
         }
         for (int s = 0; s < 2; ++s) {
-            // V: 96 cp.async completions + 96 plain arrivals (which release the tile flags)
-            mbar_init(&bars[B_VFULL + s], 2 * kProducers);
+            mbar_init(&bars[B_VFULL + s], kProducers);
             mbar_init(&bars[B_VEMPTY + s], 1);
             mbar_init(&bars[B_SFULL + s], 1);
             mbar_init(&bars[B_SEMPTY + s], kMath);
@@ -122,49 +124,54 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
         const int t_lo = i0 - a.w;
         const int t_hi = min(i0 + 127, a.L - 1) - a.w;
         const float tau_hi = (t_hi >= 0 && a.R1 > 0) ? __ldg(a.tauf + bl + t_hi) : -INFINITY;
-        // K is released by the QK^T commit and V by the PV commit, so the K ring
-        // runs ahead of V: the next K gather starts as soon as a QK^T retires.
-        for (int jt = 0; jt < n; ++jt) {
-            const int s = jt & 1;
-            const bool sel = jt < n_sel;
-            const int kb0 = jw0 + (jt - n_sel) * 128;
-            auto kf = [&](int r) {
-                if (sel) {
-                    const int idx = jt * 128 + r;
-                    return idx < cnt ? __ldg(list + idx) : -1;
-                }
-                return kb0 + r;
-            };
-            const int ks = jt % kKS;
-            if (jt >= kKS) mbar_wait(&bars[B_KEMPTY + ks], ((jt - kKS) / kKS) & 1);
-            load_tile<D, 128>(sbase + SM::kK + ks * SM::kTile, a.k, b, h, a.L, a.H, pw, lane, kf);
-            cp_async_arrive_noinc(&bars[B_KFULL + ks]);
-            // V stage: rows + the tile's metadata/flags (read by the softmax, so they
-            // must live until PV(jt) retires)
-            if (jt >= 2) mbar_wait(&bars[B_VEMPTY + s], ((jt - 2) >> 1) & 1);
-            load_tile<D, 128>(sbase + SM::kV + s * SM::kTile, a.v, b, h, a.L, a.H, pw, lane, kf);
-            if (sel) {
-                bool all_ok = true, all_sat = true;
-                for (int c = ptid; c < 128; c += kProducers) {
-                    const int idx = jt * 128 + c;
-                    const int key = idx < cnt ? __ldg(list + idx) : -1;
-                    const uint32_t mb = smem_u32(meta + (s * 3) * 128 + c);
-                    cp_async4(mb, list + (idx < cnt ? idx : 0), idx < cnt);
-                    cp_async4(mb + 128 * 4, a.leave + bl + (key >= 0 ? key : 0), key >= 0);
-                    cp_async4(mb + 256 * 4, a.uf + bl + (key >= 0 ? key : 0), key >= 0);
-                    if (key >= 0) {
-                        all_ok = all_ok && key <= t_lo && __ldg(a.leave + bl + key) > t_hi;
-                        all_sat = all_sat && __ldg(a.uf + bl + key) >= tau_hi + 1.f;
-                    } else {
-                        all_ok = false;
-                    }
-                }
-                all_ok = __all_sync(0xffffffffu, all_ok);
-                all_sat = __all_sync(0xffffffffu, all_sat);
-                if (lane == 0) tflags[s * 4 + pw] = (all_ok ? 1 : 0) | (all_sat ? 2 : 0);
+        // K is released by the QK^T commit, the metadata by the math warps once
+        // they are done with the tile, V by the PV commit. K + metadata run one
+        // tile ahead of V so a softmax never waits for a V gather.
+        auto keyfn = [&](int jt, int r) {
+            if (jt < n_sel) {
+                const int idx = jt * 128 + r;
+                return idx < cnt ? __ldg(list + idx) : -1;
             }
-            mbar_arrive(&bars[B_VFULL + s]);
-            cp_async_arrive_noinc(&bars[B_VFULL + s]);
+            return jw0 + (jt - n_sel) * 128 + r;
+        };
+        for (int jt = 0; jt <= n; ++jt) {
+            if (jt < n) {
+                const int ks = jt % kKS;
+                if (jt >= kKS) mbar_wait(&bars[B_KEMPTY + ks], ((jt - kKS) / kKS) & 1);
+                load_tile<D, 128>(sbase + SM::kK + ks * SM::kTile, a.k, b, h, a.L, a.H, pw, lane,
+                                  [&](int r) { return keyfn(jt, r); });
+                cp_async_arrive_noinc(&bars[B_KFULL + ks]);
+                if (jt >= kKS) mbar_wait(&bars[B_MEMPTY + ks], ((jt - kKS) / kKS) & 1);
+                if (jt < n_sel) {
+                    bool all_ok = true, all_sat = true;
+                    for (int c = ptid; c < 128; c += kProducers) {
+                        const int idx = jt * 128 + c;
+                        const int key = idx < cnt ? __ldg(list + idx) : -1;
+                        const uint32_t mb = smem_u32(meta + (ks * 3) * 128 + c);
+                        cp_async4(mb, list + (idx < cnt ? idx : 0), idx < cnt);
+                        cp_async4(mb + 128 * 4, a.leave + bl + (key >= 0 ? key : 0), key >= 0);
+                        cp_async4(mb + 256 * 4, a.uf + bl + (key >= 0 ? key : 0), key >= 0);
+                        if (key >= 0) {
+                            all_ok = all_ok && key <= t_lo && __ldg(a.leave + bl + key) > t_hi;
+                            all_sat = all_sat && __ldg(a.uf + bl + key) >= tau_hi + 1.f;
+                        } else {
+                            all_ok = false;
+                        }
+                    }
+                    all_ok = __all_sync(0xffffffffu, all_ok);
+                    all_sat = __all_sync(0xffffffffu, all_sat);
+                    if (lane == 0) tflags[ks * 4 + pw] = (all_ok ? 1 : 0) | (all_sat ? 2 : 0);
+                }
+                mbar_arrive(&bars[B_MFULL + ks]);
+                cp_async_arrive_noinc(&bars[B_MFULL + ks]);
+            }
+            if (jt >= 1) {
+                const int j = jt - 1, vs = j & 1;
+                if (j >= 2) mbar_wait(&bars[B_VEMPTY + vs], ((j - 2) >> 1) & 1);
+                load_tile<D, 128>(sbase + SM::kV + vs * SM::kTile, a.v, b, h, a.L, a.H, pw, lane,
+                                  [&](int r) { return keyfn(j, r); });
+                cp_async_arrive_noinc(&bars[B_VFULL + vs]);
+            }
         }
     } else if (warp == kMmaWarp) {
         // ------------------------------------------------------------ MMA issuer
@@ -222,7 +229,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
             const int s = jt & 1;
             const bool is_sel = jt < n_sel;
             mbar_wait(&bars[B_SFULL + s], (jt >> 1) & 1);
-            mbar_wait(&bars[B_VFULL + s], (jt >> 1) & 1);  // metadata + flags visibility
+            const int ks = jt % kKS;
+            mbar_wait(&bars[B_MFULL + ks], (jt / kKS) & 1);  // metadata + flags visibility
             tc_after_sync();
             tmem_ld32(tS + lane_off + s * 128 + c0, sv);
             tmem_ld32(tS + lane_off + s * 128 + c0 + 32, sv + 32);
@@ -230,12 +238,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
             tc_before_sync();
             mbar_arrive(&bars[B_SEMPTY + s]);
 
-            const int* mk = meta + (s * 3) * 128 + c0;
+            const int* mk = meta + (ks * 3) * 128 + c0;
             const int* ml = mk + 128;
             const float* mu = reinterpret_cast<const float*>(mk + 256);
             int fl = 3;
             if (is_sel) {
-                fl = tflags[s * 4] & tflags[s * 4 + 1] & tflags[s * 4 + 2];
+                fl = tflags[ks * 4] & tflags[ks * 4 + 1] & tflags[ks * 4 + 2];
                 if (KEY_SOFT) {  // gated logits (proj/src/cache.cpp:368-369)
 #pragma unroll
                     for (int c = 0; c < 64; c += 4) {
@@ -338,6 +346,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
                 tmem_wait_st();
             }
             tc_before_sync();
+            mbar_arrive(&bars[B_MEMPTY + ks]);
             mbar_arrive(&bars[B_PFULL]);
         }
         // epilogue: O / l, lse. The row's l is the sum of both halves' partials.
