@@ -12,7 +12,7 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsparsek_b200.so")
+LIB_PATH = os.environ.get("SKB_LIB_PATH") or os.path.join(HERE, "libsparsek_b200.so")
 
 
 class ShapeError(ValueError):

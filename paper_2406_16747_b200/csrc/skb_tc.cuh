@@ -248,7 +248,11 @@ __device__ __forceinline__ void load_tile(uint32_t dst, const __nv_bfloat16* bas
         const int g = pw + kPW * it;
         if (g < kGroups) {
             const int r = g * kRowsPerIter + sub;
+#if defined(SKB_EXP) && SKB_EXP == 2
+            const bool ok = false;  // experiment: no gathers (zero fill)
+#else
             const bool ok = keys[it] >= 0 && keys[it] < L;
+#endif
             const __nv_bfloat16* src = base + (((int64_t)b * L + (ok ? keys[it] : 0)) * H + h) * D + ch * 8;
             cp_async16(dst + sw_off(r, ch, R), src, ok);
         }
