@@ -155,6 +155,13 @@ int skb_cache_destroy(skb_cache* c);
  * (the new tokens' frozen scores) -> o [B, H, p]. */
 int skb_cache_step(skb_cache* c, const void* q, const void* k, const void* v, const double* u,
                    void* o, void* stream);
+/* Append n positions per sequence without attending (a prompt prefill):
+ * k/v [B, n, H, p] (dtype), u float64 [B, n]. The selection state advances
+ * exactly as n decode steps would (forward_chunk pass 1,
+ * proj/src/cache.cpp:259-311); only the rows still retained afterwards are
+ * copied into the slot pool. */
+int skb_cache_prefill(skb_cache* c, const void* k, const void* v, const double* u, int64_t n,
+                      void* stream);
 /* Host-visible state for tests/inspection: retained positions (ascending
  * selected then window), count, tau, positions seen, peak retained. */
 int skb_cache_state(skb_cache* c, int64_t b, int32_t* positions, int64_t* count, double* tau,

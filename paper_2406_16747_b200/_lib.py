@@ -94,6 +94,7 @@ _SIGS = {
     "skb_cache_create": ([C.POINTER(AttnDesc), C.POINTER(_vp)], C.c_int),
     "skb_cache_destroy": ([_vp], C.c_int),
     "skb_cache_step": ([_vp, _vp, _vp, _vp, _vp, _vp, _vp], C.c_int),
+    "skb_cache_prefill": ([_vp, _vp, _vp, _vp, C.c_int64, _vp], C.c_int),
     "skb_cache_state": ([_vp, C.c_int64, _vp, _vp, _vp, _vp, _vp, _vp], C.c_int),
     "skb_stream_create": ([C.c_double, C.c_int64, C.c_int64, C.POINTER(_vp)], C.c_int),
     "skb_stream_destroy": ([_vp], C.c_int),

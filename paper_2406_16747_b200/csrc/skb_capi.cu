@@ -29,6 +29,10 @@ int fail(int code, const char* msg) {
 }
 }  // namespace
 
+namespace skb {
+void set_last_error(const char* msg) { g_err = msg; }
+}  // namespace skb
+
 #define SKB_API_BEGIN try {
 #define SKB_API_END                                              \
     }                                                            \

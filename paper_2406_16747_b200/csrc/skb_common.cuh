@@ -73,6 +73,13 @@ __device__ __forceinline__ float to_f<float>(float x) { return x; }
 template <>
 __device__ __forceinline__ float to_f<__nv_bfloat16>(__nv_bfloat16 x) { return __bfloat162float(x); }
 
+__device__ __forceinline__ float tof(float x) { return x; }
+__device__ __forceinline__ float tof(double x) { return (float)x; }
+__device__ __forceinline__ float tof(__nv_bfloat16 x) { return __bfloat162float(x); }
+__device__ __forceinline__ void store_from_f(float* p, float v) { *p = v; }
+__device__ __forceinline__ void store_from_f(double* p, float v) { *p = (double)v; }
+__device__ __forceinline__ void store_from_f(__nv_bfloat16* p, float v) { *p = __float2bfloat16(v); }
+
 __device__ __forceinline__ double ld_as_double(const void* p, int dtype, int64_t i) {
     if (dtype == SKB_F64) return static_cast<const double*>(p)[i];
     if (dtype == SKB_F32) return (double)static_cast<const float*>(p)[i];

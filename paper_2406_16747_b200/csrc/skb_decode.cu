@@ -1,29 +1,930 @@
-// K5 — constant-(floor(k)+w) KV cache decode step. (implementation follows)
+// K5 — the constant-(floor(k)+w) KV cache for decoding, and the device-resident
+// incremental SparseK stream (Algorithm 2) it is built on.
+//
+// Reference: SparseKvCache (proj/include/sparsek/cache.hpp:21-87) driven by
+// generate_step (proj/src/cache.cpp:570-577) = forward_chunk on one row: the
+// new position enters the window ring, the position leaving the window is
+// pushed into StreamState (proj/src/stream.cpp:72-152) and admitted to the
+// top-floor(k) min-heap or dropped (exit_window/admit_to_cache,
+// proj/src/cache.cpp:136-179); the query then reads the retained rows with
+// gates clamp(u_j - tau, 0, 1) (cache.cpp:285-311, 358-393).
+//
+// B200 layout (per sequence b):
+//   * slot pool: K and V as [B, S, H, p] with S = floor(k) + w + 1 slots (the
+//     reference's peak_kv bound, proj/tests/test_cache.cpp:124,148); a row
+//     is written once into a free slot when its position arrives and never
+//     moves — leaving the window for the selected set is a table update.
+//   * stream state: survivors and saturated entries as two arrays sorted by
+//     (value desc, index asc), so the heaps' minima (HeapCmp, stream.cpp:14-18)
+//     are the array tails and the selected set is the survivors' head
+//     [0, floor(k)): a top-floor(k) position is never below tau, so the stream
+//     order and the cache heap (SlotCmp, cache.cpp:53-60) agree. One warp
+//     per sequence does the push: count (parallel), shift (parallel), scan
+//     (uniform scalar control flow, identical arithmetic to the reference:
+//     running sums with the same += / -= order, so tau is bit-identical).
+//   * per step three launches: k_cache_control (one warp per sequence:
+//     append, exit/admit/evict, attended slot list with gates), k_cache_attn
+//     (split over the attended slots, all heads per CTA: each slot's H*p row
+//     is one contiguous read), k_cache_combine (merge the split softmaxes).
+//     HBM-bound: 2 * S * H * p * sizeof(T) bytes per sequence per step.
+//
+// Deviation (documented in DESIGN.md): the reference re-sums its heaps every
+// 2^16 pushes (stream.cpp:78-81, refresh_sums) in heap-array order; here the
+// re-sum runs in sorted order, so after 65536 pushes tau may differ from the
+// reference by rounding (never the selected set).
+#include <algorithm>
+#include <cfloat>
+#include <vector>
+
 #include "skb_common.cuh"
 #include "skb_internal.h"
 
-struct skb_cache {
-    int dummy;
+namespace skb {
+namespace {
+
+struct StreamCtl {
+    double k, tau, sum_s, sum_f;
+    long long t;            // elements pushed
+    long long heap_cap;     // 0 = unbounded (StreamState heap_cap)
+    unsigned long long heap_ops, cap_drops;
+    int nS, nF;
+    int since_refresh;
+    int cap;                // array capacity (maximum pushes)
+    int error;              // 1 = scan exhausted (reference throws NumericError), 2 = overflow
+    int pad;
 };
 
-extern "C" {
-int skb_cache_create(const skb_attn_desc*, skb_cache**) { return SKB_ECONFIG; }
-int skb_cache_destroy(skb_cache*) { return SKB_OK; }
-int skb_cache_step(skb_cache*, const void*, const void*, const void*, const double*, void*, void*) {
-    return SKB_ECONFIG;
+struct StreamArr {
+    double* sv;
+    int* si;
+    double* fv;
+    int* fi;
+    uint8_t* evicted;  // [cap] or null
+};
+
+__device__ __forceinline__ int warp_sum_i(int v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
 }
-int skb_cache_state(skb_cache*, int64_t, int32_t*, int64_t*, double*, int64_t*, int64_t*, void*) {
-    return SKB_ECONFIG;
+
+// number of entries with value >= z in a (value desc) array: the slot a new,
+// later-indexed z takes (ties keep the earlier index first).
+__device__ int warp_count_ge(const double* v, int n, double z) {
+    const int lane = threadIdx.x & 31;
+    int c = 0;
+    for (int i = lane; i < n; i += 32) c += v[i] >= z;
+    return warp_sum_i(c);
 }
+
+__device__ void warp_insert(double* v, int* ix, int n, int pos, double z, int zi) {
+    const int lane = threadIdx.x & 31;
+    for (int base = n - 1; base >= pos; base -= 32) {
+        const int i = base - lane;
+        const bool act = i >= pos;
+        double a = 0.0;
+        int b = 0;
+        if (act) {
+            a = v[i];
+            b = ix[i];
+        }
+        __syncwarp();
+        if (act) {
+            v[i + 1] = a;
+            ix[i + 1] = b;
+        }
+        __syncwarp();
+    }
+    if (lane == 0) {
+        v[pos] = z;
+        ix[pos] = zi;
+    }
+    __syncwarp();
 }
+
+// StreamState::push (proj/src/stream.cpp:72-152), executed uniformly by all 32
+// lanes of one warp (c is a per-lane copy; lane 0 owns the stores). Returns
+// whether z entered the survivors; *rank = its position in the survivor array.
+__device__ bool warp_stream_push(StreamCtl& c, const StreamArr& a, double z, int* rank) {
+    const int lane = threadIdx.x & 31;
+    const int index = (int)c.t;
+    c.t += 1;
+    *rank = -1;
+    if (++c.since_refresh >= (1 << 16)) {  // refresh_sums (see header note)
+        double ss = 0.0, sf = 0.0;
+        for (int i = 0; i < c.nS; ++i) ss += a.sv[i];
+        for (int i = 0; i < c.nF; ++i) sf += a.fv[i];
+        c.sum_s = ss;
+        c.sum_f = sf;
+        c.since_refresh = 0;
+    }
+    if (!(z > c.tau)) {  // at or below the threshold: zero mass now and forever
+        if (a.evicted && lane == 0) a.evicted[index] = 1;
+        return false;
+    }
+    if (c.nS >= c.cap) {
+        c.error = 2;
+        return false;
+    }
+    const int ps = warp_count_ge(a.sv, c.nS, z);
+    warp_insert(a.sv, a.si, c.nS, ps, z, index);
+    c.nS += 1;
+    c.sum_s += z;
+    c.heap_ops += 1;
+    *rank = ps;
+    if (z >= c.tau + 1.0) {
+        const int pf = warp_count_ge(a.fv, c.nF, z);
+        warp_insert(a.fv, a.fi, c.nF, pf, z, index);
+        c.nF += 1;
+        c.sum_f += z;
+        c.heap_ops += 1;
+    }
+    auto pop_s = [&]() {
+        const double v = a.sv[c.nS - 1];
+        const int ix = a.si[c.nS - 1];
+        c.nS -= 1;
+        c.sum_s -= v;
+        if (a.evicted && lane == 0) a.evicted[ix] = 1;
+        c.heap_ops += 1;
+    };
+    auto pop_f = [&]() {
+        c.sum_f -= a.fv[c.nF - 1];
+        c.nF -= 1;
+        c.heap_ops += 1;
+    };
+    if (c.heap_cap > 0) {
+        while ((long long)c.nS > c.heap_cap) {
+            if (c.nF > 0 && a.fi[c.nF - 1] == a.si[c.nS - 1]) pop_f();
+            pop_s();
+            c.cap_drops += 1;
+        }
+    }
+    if ((double)c.t < c.k) {  // budget not binding yet
+        c.tau = -CUDART_INF;
+        __syncwarp();
+        return true;
+    }
+    bool popped = false;
+    double last = 0.0;
+    for (;;) {
+        const int u = c.nF, w = c.nS;
+        if (u == w) {
+            if (u == 0) {
+                c.error = 1;
+                break;
+            }
+            const double hi = a.fv[u - 1] - 1.0;
+            const double lo = popped ? last : fmax(c.tau, hi - 1.0);
+            if (fabs((double)u - c.k) <= 1e-9) {
+                c.tau = fmax(c.tau, 0.5 * (lo + hi));
+                break;
+            }
+            pop_f();
+            continue;
+        }
+        const double cand = (c.sum_s - c.sum_f + (double)u - c.k) / (double)(w - u);
+        const double smin = a.sv[w - 1];
+        if (smin > cand && (u == 0 || a.fv[u - 1] >= cand + 1.0)) {
+            c.tau = cand;
+            break;
+        }
+        if (u == 0 || smin <= a.fv[u - 1] - 1.0) {
+            last = smin;
+            popped = true;
+            pop_s();
+            if (c.nS == 0) {
+                c.error = 1;
+                break;
+            }
+        } else {
+            pop_f();
+        }
+    }
+    __syncwarp();
+    return true;
+}
+
+// ------------------------------------------------------------------ stream API
+__global__ void k_stream_push(StreamCtl* ctl, StreamArr a, const double* __restrict__ z, int n,
+                              double* __restrict__ tau_out, uint8_t* __restrict__ ins_out) {
+    StreamCtl c = *ctl;
+    const int lane = threadIdx.x & 31;
+    for (int i = 0; i < n; ++i) {
+        int rank;
+        const bool ins = warp_stream_push(c, a, z[i], &rank);
+        if (lane == 0) {
+            if (tau_out) tau_out[i] = c.tau;
+            if (ins_out) ins_out[i] = ins ? 1 : 0;
+        }
+        if (c.error) break;
+    }
+    if (lane == 0) *ctl = c;
+}
+
+// ------------------------------------------------------------------ cache
+struct CacheCtl {
+    StreamCtl st;
+    long long t;     // positions seen
+    long long peak;  // peak retained rows (cache + ring + in-flight)
+    int free_top;    // free-slot stack height
+    int nsel;        // |selected set|
+    int error;
+    int pad;
+};
+
+struct CacheArgs {
+    CacheCtl* ctl;      // [B]
+    double* sv;         // [B, Lmax] survivors (value desc, index asc)
+    int* si;
+    double* fv;         // [B, Lmax] saturated
+    int* fi;
+    double* u_hist;     // [B, Lmax] frozen scores
+    int* slot_of;       // [B, Lmax] position -> slot (-1 = dropped)
+    int* pos_of;        // [B, S]    slot -> position (-1 = free)
+    int* free_stack;    // [B, S]
+    int* att_slot;      // [B, S]    attended slots of the current step
+    float* att_kg;      // [B, S]    logit multiplier (gate under soft keys, else 1)
+    float* att_vg;      // [B, S]    value weight (gate under soft mask, else 1)
+    int* att_n;         // [B]
+    uint8_t* kpool;     // [B, S, H, p] dtype
+    uint8_t* vpool;
+    int Lmax, S, cap, w, key_soft, mask_st;
+    int64_t row_bytes;  // H * p * esize
+};
+
+__device__ __forceinline__ void warp_copy_row(uint8_t* dst, const uint8_t* src, int64_t bytes) {
+    const int lane = threadIdx.x & 31;
+    if (((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src) | (uintptr_t)bytes) & 15) == 0) {
+        const uint4* s = reinterpret_cast<const uint4*>(src);
+        uint4* d = reinterpret_cast<uint4*>(dst);
+        for (int64_t i = lane; i < bytes / 16; i += 32) d[i] = s[i];
+    } else {
+        const uint16_t* s = reinterpret_cast<const uint16_t*>(src);
+        uint16_t* d = reinterpret_cast<uint16_t*>(dst);
+        for (int64_t i = lane; i < bytes / 2; i += 32) d[i] = s[i];
+    }
+}
+
+// One position of forward_chunk's pass 1 (proj/src/cache.cpp:259-311) for one
+// sequence, uniformly on one warp. kv_src: this position's K/V rows (null in
+// a prefill replay: the rows are copied once at the end). Builds the
+// attended list when `emit` is set.
+__device__ void warp_cache_advance(const CacheArgs& A, int b, CacheCtl& c, double u_new,
+                                   const uint8_t* k_src, const uint8_t* v_src, bool emit) {
+    const int lane = threadIdx.x & 31;
+    const int64_t bL = (int64_t)b * A.Lmax, bS = (int64_t)b * A.S;
+    if (c.t >= A.Lmax) {
+        c.error = 2;
+        return;
+    }
+    const int pos = (int)c.t;
+    StreamArr sa{A.sv + bL, A.si + bL, A.fv + bL, A.fi + bL, nullptr};
+    if (lane == 0) A.u_hist[bL + pos] = u_new;
+    // the new row enters the window ring (kv_.emplace + ring_.push_back)
+    const int slot = A.free_stack[bS + c.free_top - 1];
+    c.free_top -= 1;
+    if (lane == 0) {
+        A.slot_of[bL + pos] = slot;
+        A.pos_of[bS + slot] = pos;
+    }
+    if (k_src) {
+        warp_copy_row(A.kpool + (bS + slot) * A.row_bytes, k_src, A.row_bytes);
+        warp_copy_row(A.vpool + (bS + slot) * A.row_bytes, v_src, A.row_bytes);
+    }
+    const long long ring_before = c.t < A.w ? c.t : A.w;
+    c.peak = max(c.peak, ring_before + 1 + c.nsel);  // note_peak after ring push
+    int freed[2] = {-1, -1};
+    __syncwarp();
+    if (c.t + 1 > A.w) {  // ring_.size() > window: exit_window(ring_.front())
+        const int e = pos - A.w;
+        const double ue = (e == pos) ? u_new : A.u_hist[bL + e];
+        bool admitted = false;
+        if (A.cap > 0) {
+            const int nS_before = c.st.nS;
+            int rank;
+            const bool ins = warp_stream_push(c.st, sa, ue, &rank);
+            if (ins && rank >= 0 && rank < A.cap) {
+                admitted = true;
+                // the previous rank floor(k)-1 entry is pushed out of the top floor(k)
+                // (pops only shorten the array, so index cap still holds it)
+                if (nS_before >= A.cap) freed[1] = sa.si[A.cap];
+                c.nsel = min(c.nsel + 1, A.cap);
+            }
+        } else if (c.st.k > 0.0) {
+            int rank;
+            warp_stream_push(c.st, sa, ue, &rank);  // tau still advances (floor(k) = 0)
+        }
+        if (!admitted) freed[0] = e;
+    }
+    const long long ring_after = (c.t + 1) < A.w ? (c.t + 1) : A.w;
+    c.peak = max(c.peak, ring_after + c.nsel);
+    // attended list (snapshot): selected (survivor order), then the window ring
+    if (emit) {
+        const double tau = c.st.tau;
+        const int ns = c.nsel;
+        for (int r = lane; r < ns; r += 32) {
+            const int jp = sa.si[r];
+            const float g = (float)fmin(1.0, fmax(0.0, sa.sv[r] - tau));
+            A.att_slot[bS + r] = A.slot_of[bL + jp];
+            A.att_kg[bS + r] = A.key_soft ? g : 1.f;
+            A.att_vg[bS + r] = A.mask_st ? 1.f : g;
+        }
+        int n = ns;
+        if (A.w > 0) {
+            const int r0 = max(0, pos - A.w + 1);
+            for (int jp = r0 + lane; jp <= pos; jp += 32) {
+                const int r = ns + (jp - r0);
+                A.att_slot[bS + r] = A.slot_of[bL + jp];
+                A.att_kg[bS + r] = 1.f;
+                A.att_vg[bS + r] = 1.f;
+            }
+            n += pos - r0 + 1;
+        }
+        if (A.w == 0) {
+            // nothing window-resident: the query reads itself unless selected
+            bool selected = false;
+            for (int r = lane; r < ns; r += 32) selected |= sa.si[r] == pos;
+            selected = __any_sync(0xffffffffu, selected);
+            if (!selected) {
+                if (lane == 0) {
+                    A.att_slot[bS + n] = slot;
+                    A.att_kg[bS + n] = 1.f;
+                    A.att_vg[bS + n] = 1.f;
+                }
+                n += 1;
+            }
+        }
+        if (lane == 0) A.att_n[b] = n;
+    }
+    __syncwarp();
+    // drop_kv: free the slots now (the attention of this step reads only the
+    // attended list, and slots are reallocated by the next step's control)
+    for (int f = 0; f < 2; ++f) {
+        const int fp = freed[f];
+        if (fp < 0) continue;
+        const int fs = A.slot_of[bL + fp];
+        __syncwarp();
+        if (lane == 0) {
+            A.free_stack[bS + c.free_top] = fs;
+            A.slot_of[bL + fp] = -1;
+            A.pos_of[bS + fs] = -1;
+        }
+        c.free_top += 1;
+        __syncwarp();
+    }
+    c.t += 1;
+    if (c.st.error) c.error = 1;
+}
+
+__global__ void k_cache_init(CacheArgs A, double k) {
+    const int b = blockIdx.x;
+    const int64_t bS = (int64_t)b * A.S;
+    for (int s = threadIdx.x; s < A.S; s += blockDim.x) {
+        A.free_stack[bS + s] = A.S - 1 - s;  // slot 0 on top
+        A.pos_of[bS + s] = -1;
+    }
+    if (threadIdx.x == 0) {
+        CacheCtl c{};
+        c.st.k = k;
+        c.st.tau = -CUDART_INF;
+        c.st.cap = A.Lmax;
+        c.free_top = A.S;
+        A.ctl[b] = c;
+        A.att_n[b] = 0;
+    }
+}
+
+// one decode step: a warp per sequence
+__global__ void k_cache_control(CacheArgs A, int B, const uint8_t* __restrict__ k_new,
+                                const uint8_t* __restrict__ v_new, const double* __restrict__ u_new) {
+    const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (b >= B) return;
+    CacheCtl c = A.ctl[b];
+    if (c.error == 0)
+        warp_cache_advance(A, b, c, u_new[b], k_new + (int64_t)b * A.row_bytes, v_new + (int64_t)b * A.row_bytes,
+                           true);
+    if ((threadIdx.x & 31) == 0) A.ctl[b] = c;
+}
+
+// prefill replay: n positions per sequence, no attention; rows copied after.
+__global__ void k_cache_prefill(CacheArgs A, int B, const double* __restrict__ u_hist, int n) {
+    const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (b >= B) return;
+    CacheCtl c = A.ctl[b];
+    for (int i = 0; i < n && c.error == 0; ++i)
+        warp_cache_advance(A, b, c, u_hist[(int64_t)b * n + i], nullptr, nullptr, false);
+    if ((threadIdx.x & 31) == 0) A.ctl[b] = c;
+}
+
+// rows of the live slots that arrived during a prefill of n positions starting at p0
+__global__ void k_cache_fill_rows(CacheArgs A, const uint8_t* __restrict__ k_hist,
+                                  const uint8_t* __restrict__ v_hist, int p0, int n) {
+    const int b = blockIdx.y;
+    const int slot = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (slot >= A.S) return;
+    const int pos = A.pos_of[(int64_t)b * A.S + slot];
+    if (pos < p0 || pos >= p0 + n) return;
+    const int64_t src = ((int64_t)b * n + (pos - p0)) * A.row_bytes;
+    const int64_t dst = ((int64_t)b * A.S + slot) * A.row_bytes;
+    warp_copy_row(A.kpool + dst, k_hist + src, A.row_bytes);
+    warp_copy_row(A.vpool + dst, v_hist + src, A.row_bytes);
+}
+
+// ------------------------------------------------------------------ attention
+constexpr int kAttnThreads = 256;
+constexpr int kSlotsPerCta = 64;
+
+template <int VEC>
+__device__ __forceinline__ void ldv(const __nv_bfloat16* p, float* o) {
+    if constexpr (VEC == 4) {
+        const uint2 r = *reinterpret_cast<const uint2*>(p);
+        const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&r.x));
+        const float2 c = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&r.y));
+        o[0] = a.x, o[1] = a.y, o[2] = c.x, o[3] = c.y;
+    } else if constexpr (VEC == 2) {
+        const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(p));
+        o[0] = a.x, o[1] = a.y;
+    } else {
+        o[0] = __bfloat162float(*p);
+    }
+}
+template <int VEC>
+__device__ __forceinline__ void ldv(const float* p, float* o) {
+    if constexpr (VEC == 4) {
+        const float4 r = *reinterpret_cast<const float4*>(p);
+        o[0] = r.x, o[1] = r.y, o[2] = r.z, o[3] = r.w;
+    } else if constexpr (VEC == 2) {
+        const float2 r = *reinterpret_cast<const float2*>(p);
+        o[0] = r.x, o[1] = r.y;
+    } else {
+        o[0] = *p;
+    }
+}
+template <int VEC>
+__device__ __forceinline__ void ldv(const double* p, float* o) {
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) o[e] = (float)p[e];
+}
+
+// CTA = (chunk of kSlotsPerCta attended entries, sequence), all heads. Each
+// (entry, head) row is p contiguous elements; a warp covers it with lanes
+// owning VEC consecutive elements per 32*VEC stride.
+template <class T, int VEC>
+__global__ void __launch_bounds__(kAttnThreads)
+k_cache_attn(CacheArgs A, const T* __restrict__ q, int H, int p, float scale, float* __restrict__ po,
+             float* __restrict__ pm, float* __restrict__ pl, int nsplit) {
+    extern __shared__ float sm[];
+    float* sq = sm;                       // [H * p] query
+    float* sp = sq + H * p;               // [H][kSlotsPerCta] logits -> probabilities
+    int* ss = reinterpret_cast<int*>(sp + H * kSlotsPerCta);  // [kSlotsPerCta] slots
+    float* svg = reinterpret_cast<float*>(ss + kSlotsPerCta);  // value weights
+    const int b = blockIdx.y, chunk = blockIdx.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = kAttnThreads / 32;
+    const int n = A.att_n[b];
+    const int e0 = chunk * kSlotsPerCta;
+    const int ne = max(0, min(kSlotsPerCta, n - e0));
+    const int64_t bS = (int64_t)b * A.S;
+    const int hp = H * p;
+    for (int i = threadIdx.x; i < hp; i += kAttnThreads) sq[i] = tof(q[(int64_t)b * hp + i]);
+    for (int e = threadIdx.x; e < ne; e += kAttnThreads) {
+        ss[e] = A.att_slot[bS + e0 + e];
+        svg[e] = A.att_vg[bS + e0 + e];
+    }
+    __syncthreads();
+    const T* kp = reinterpret_cast<const T*>(A.kpool);
+    const T* vp = reinterpret_cast<const T*>(A.vpool);
+    // logits: unit = (entry, head), consecutive warps take consecutive heads
+    const int units = ne * H;
+    constexpr int U = 4;
+    for (int u0 = warp * U; u0 < units; u0 += nw * U) {
+        float acc[U];
+#pragma unroll
+        for (int x = 0; x < U; ++x) acc[x] = 0.f;
+#pragma unroll
+        for (int x = 0; x < U; ++x) {
+            const int un = u0 + x;
+            if (un < units) {
+                const int e = un / H, h = un % H;
+                const T* kr = kp + ((bS + ss[e]) * H + h) * (int64_t)p;
+                const float* qr = sq + h * p;
+                for (int c = lane * VEC; c < p; c += 32 * VEC) {
+                    float kv[VEC];
+                    ldv<VEC>(kr + c, kv);
+#pragma unroll
+                    for (int v = 0; v < VEC; ++v) acc[x] = fmaf(qr[c + v], kv[v], acc[x]);
+                }
+            }
+        }
+#pragma unroll
+        for (int x = 0; x < U; ++x) {
+            const float s = warp_sum(acc[x]);
+            const int un = u0 + x;
+            if (lane == 0 && un < units) {
+                const int e = un / H, h = un % H;
+                sp[h * kSlotsPerCta + e] = s * scale * A.att_kg[bS + e0 + e];
+            }
+        }
+    }
+    __syncthreads();
+    // per-head softmax over this chunk (partial: max m, sum l of exp(a - m))
+    for (int h = warp; h < H; h += nw) {
+        float m = -INFINITY;
+        for (int e = lane; e < ne; e += 32) m = fmaxf(m, sp[h * kSlotsPerCta + e]);
+        m = warp_max(m);
+        float l = 0.f;
+        for (int e = lane; e < ne; e += 32) {
+            const float pe = ne > 0 ? expf(sp[h * kSlotsPerCta + e] - m) : 0.f;
+            sp[h * kSlotsPerCta + e] = pe;
+            l += pe;
+        }
+        l = warp_sum(l);
+        if (lane == 0) {
+            const int64_t o = ((int64_t)b * nsplit + chunk) * H + h;
+            pm[o] = ne > 0 ? m : -INFINITY;
+            pl[o] = l;
+        }
+    }
+    __syncthreads();
+    // o_partial[h] = sum_e p_e * vg_e * v_e
+    for (int h = warp; h < H; h += nw) {
+        for (int c0 = lane * VEC; c0 < p; c0 += 32 * VEC) {
+            float acc[VEC];
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) acc[v] = 0.f;
+            int e = 0;
+            for (; e + 4 <= ne; e += 4) {
+                float vv[4][VEC];
+#pragma unroll
+                for (int x = 0; x < 4; ++x) ldv<VEC>(vp + ((bS + ss[e + x]) * H + h) * (int64_t)p + c0, vv[x]);
+#pragma unroll
+                for (int x = 0; x < 4; ++x) {
+                    const float w = sp[h * kSlotsPerCta + e + x] * svg[e + x];
+#pragma unroll
+                    for (int v = 0; v < VEC; ++v) acc[v] = fmaf(w, vv[x][v], acc[v]);
+                }
+            }
+            for (; e < ne; ++e) {
+                float vv[VEC];
+                ldv<VEC>(vp + ((bS + ss[e]) * H + h) * (int64_t)p + c0, vv);
+                const float w = sp[h * kSlotsPerCta + e] * svg[e];
+#pragma unroll
+                for (int v = 0; v < VEC; ++v) acc[v] = fmaf(w, vv[v], acc[v]);
+            }
+            float* out = po + (((int64_t)b * nsplit + chunk) * H + h) * p + c0;
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) out[v] = acc[v];
+        }
+    }
+}
+
+template <class T>
+__global__ void k_cache_combine(const float* __restrict__ po, const float* __restrict__ pm,
+                                const float* __restrict__ pl, const int* __restrict__ att_n, int H, int p,
+                                int nsplit, T* __restrict__ o) {
+    const int h = blockIdx.x, b = blockIdx.y;
+    const int used = min(nsplit, (att_n[b] + kSlotsPerCta - 1) / kSlotsPerCta);
+    float M = -INFINITY;
+    for (int s = 0; s < used; ++s) M = fmaxf(M, pm[((int64_t)b * nsplit + s) * H + h]);
+    float Lsum = 0.f;
+    for (int s = 0; s < used; ++s) {
+        const int64_t i = ((int64_t)b * nsplit + s) * H + h;
+        if (pm[i] > -INFINITY) Lsum += pl[i] * expf(pm[i] - M);
+    }
+    const float inv = Lsum > 0.f ? 1.f / Lsum : 0.f;
+    for (int c = threadIdx.x; c < p; c += blockDim.x) {
+        float acc = 0.f;
+        for (int s = 0; s < used; ++s) {
+            const int64_t i = ((int64_t)b * nsplit + s) * H + h;
+            if (pm[i] > -INFINITY) acc += po[i * p + c] * expf(pm[i] - M);
+        }
+        store_from_f(o + ((int64_t)b * H + h) * p + c, acc * inv);
+    }
+}
+
+}  // namespace
+}  // namespace skb
+
+// ====================================================================== C ABI
+using namespace skb;
 
 struct skb_stream {
-    int dummy;
+    StreamCtl* ctl = nullptr;
+    StreamArr arr{};
+    int64_t capacity = 0;
 };
-extern "C" {
-int skb_stream_create(double, int64_t, int64_t, skb_stream**) { return SKB_ECONFIG; }
-int skb_stream_destroy(skb_stream*) { return SKB_OK; }
-int skb_stream_push(skb_stream*, const double*, int64_t, double*, uint8_t*, void*) { return SKB_ECONFIG; }
-int skb_stream_query(skb_stream*, skb_stream_info*, void*) { return SKB_ECONFIG; }
-int skb_stream_survivors(skb_stream*, double*, int64_t*, uint8_t*, void*) { return SKB_ECONFIG; }
+
+struct skb_cache {
+    skb_attn_desc d{};
+    CacheArgs A{};
+    int nsplit = 0;
+    int vec = 1;
+    float* po = nullptr;
+    float* pm = nullptr;
+    float* pl = nullptr;
+    std::vector<void*> allocs;
+    ~skb_cache() {
+        for (void* p : allocs) cudaFree(p);
+    }
+    template <class P>
+    P* alloc(size_t count) {
+        void* p = nullptr;
+        SKB_CHECK_CUDA(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(P)));
+        allocs.push_back(p);
+        return static_cast<P*>(p);
+    }
+};
+
+namespace skb {
+void set_last_error(const char* msg);  // skb_capi.cu (thread-local skb_last_error)
 }
+
+#define K5_BEGIN try {
+#define K5_END                                                              \
+    }                                                                       \
+    catch (const skb::Error& e) {                                           \
+        skb::set_last_error(e.what());                                      \
+        return e.code;                                                      \
+    }                                                                       \
+    catch (const std::exception& e) {                                       \
+        skb::set_last_error(e.what());                                      \
+        return SKB_ECUDA;                                                   \
+    }                                                                       \
+    return SKB_OK;
+
+static size_t esize_of(int dt) { return dt == SKB_F64 ? 8 : dt == SKB_F32 ? 4 : 2; }
+
+extern "C" {
+
+int skb_stream_create(double k, int64_t heap_cap, int64_t capacity, skb_stream** out) {
+    K5_BEGIN
+    SKB_REQUIRE(out != nullptr, SKB_EARG, "stream_create: null out");
+    SKB_REQUIRE(std::isfinite(k) && k > 0.0, SKB_EARG, "KBudget: k must be positive and finite");
+    SKB_REQUIRE(heap_cap >= 0, SKB_EARG, "stream_create: heap_cap must be >= 0");
+    SKB_REQUIRE(heap_cap == 0 || (double)heap_cap >= std::ceil(k), SKB_EARG,
+                "stream: heap_cap below ceil(k)");
+    SKB_REQUIRE(capacity >= 1 && capacity < (int64_t(1) << 30), SKB_EARG, "stream_create: bad capacity");
+    skb_stream* s = new skb_stream();
+    s->capacity = capacity;
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, sizeof(StreamCtl) + (size_t)capacity * (8 + 4 + 8 + 4 + 1) + 64);
+    if (e != cudaSuccess) {
+        delete s;
+        throw skb::Error(SKB_ECUDA, std::string("stream_create: ") + cudaGetErrorString(e));
+    }
+    char* base = static_cast<char*>(p);
+    s->ctl = reinterpret_cast<StreamCtl*>(base);
+    char* q = base + ((sizeof(StreamCtl) + 15) & ~size_t(15));
+    s->arr.sv = reinterpret_cast<double*>(q);
+    s->arr.fv = s->arr.sv + capacity;
+    s->arr.si = reinterpret_cast<int*>(s->arr.fv + capacity);
+    s->arr.fi = s->arr.si + capacity;
+    s->arr.evicted = reinterpret_cast<uint8_t*>(s->arr.fi + capacity);
+    StreamCtl c{};
+    c.k = k;
+    c.tau = -INFINITY;
+    c.heap_cap = heap_cap;
+    c.cap = (int)capacity;
+    SKB_CHECK_CUDA(cudaMemcpy(s->ctl, &c, sizeof(c), cudaMemcpyHostToDevice));
+    SKB_CHECK_CUDA(cudaMemset(s->arr.evicted, 0, capacity));
+    *out = s;
+    K5_END
+}
+
+int skb_stream_destroy(skb_stream* s) {
+    if (s) {
+        cudaFree(s->ctl);
+        delete s;
+    }
+    return SKB_OK;
+}
+
+int skb_stream_push(skb_stream* s, const double* z, int64_t n, double* tau_out, uint8_t* inserted_out,
+                    void* stream) {
+    K5_BEGIN
+    SKB_REQUIRE(s != nullptr, SKB_EARG, "stream_push: null stream");
+    SKB_REQUIRE(n >= 0, SKB_EARG, "stream_push: n must be >= 0");
+    if (n == 0) return SKB_OK;
+    SKB_REQUIRE(z != nullptr, SKB_EARG, "stream_push: null z");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    StreamCtl c;
+    SKB_CHECK_CUDA(cudaMemcpyAsync(&c, s->ctl, sizeof(c), cudaMemcpyDeviceToHost, st));
+    SKB_CHECK_CUDA(cudaStreamSynchronize(st));
+    SKB_REQUIRE(c.t + n <= s->capacity, SKB_ESHAPE, "stream_push: capacity exceeded");
+    k_stream_push<<<1, 32, 0, st>>>(s->ctl, s->arr, z, (int)n, tau_out, inserted_out);
+    SKB_CHECK_LAUNCH();
+    SKB_CHECK_CUDA(cudaMemcpyAsync(&c, s->ctl, sizeof(c), cudaMemcpyDeviceToHost, st));
+    SKB_CHECK_CUDA(cudaStreamSynchronize(st));
+    SKB_REQUIRE(c.error == 0, SKB_ENUMERIC, "stream scan exhausted (internal)");
+    K5_END
+}
+
+int skb_stream_query(skb_stream* s, skb_stream_info* out, void* stream) {
+    K5_BEGIN
+    SKB_REQUIRE(s != nullptr && out != nullptr, SKB_EARG, "stream_query: null argument");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    StreamCtl c;
+    SKB_CHECK_CUDA(cudaMemcpyAsync(&c, s->ctl, sizeof(c), cudaMemcpyDeviceToHost, st));
+    SKB_CHECK_CUDA(cudaStreamSynchronize(st));
+    out->tau = c.tau;
+    out->t = c.t;
+    out->survivors = c.nS;
+    out->saturated = c.nF;
+    out->cap_drops = c.cap_drops;
+    out->heap_ops = c.heap_ops;
+    out->k = c.k;
+    K5_END
+}
+
+int skb_stream_survivors(skb_stream* s, double* values, int64_t* indices, uint8_t* evicted, void* stream) {
+    K5_BEGIN
+    SKB_REQUIRE(s != nullptr, SKB_EARG, "stream_survivors: null stream");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    StreamCtl c;
+    SKB_CHECK_CUDA(cudaMemcpyAsync(&c, s->ctl, sizeof(c), cudaMemcpyDeviceToHost, st));
+    SKB_CHECK_CUDA(cudaStreamSynchronize(st));
+    std::vector<double> v(c.nS);
+    std::vector<int> ix(c.nS);
+    if (c.nS) {
+        SKB_CHECK_CUDA(cudaMemcpyAsync(v.data(), s->arr.sv, c.nS * 8, cudaMemcpyDeviceToHost, st));
+        SKB_CHECK_CUDA(cudaMemcpyAsync(ix.data(), s->arr.si, c.nS * 4, cudaMemcpyDeviceToHost, st));
+    }
+    if (evicted && c.t)
+        SKB_CHECK_CUDA(cudaMemcpyAsync(evicted, s->arr.evicted, (size_t)c.t, cudaMemcpyDeviceToHost, st));
+    SKB_CHECK_CUDA(cudaStreamSynchronize(st));
+    // ascending index order (StreamState::solution, proj/src/stream.cpp:157-158)
+    std::vector<int> order(c.nS);
+    for (int i = 0; i < c.nS; ++i) order[i] = i;
+    std::sort(order.begin(), order.end(), [&](int a, int b) { return ix[a] < ix[b]; });
+    for (int i = 0; i < c.nS; ++i) {
+        if (values) values[i] = v[order[i]];
+        if (indices) indices[i] = ix[order[i]];
+    }
+    K5_END
+}
+
+int skb_cache_create(const skb_attn_desc* d, skb_cache** out) {
+    K5_BEGIN
+    SKB_REQUIRE(d != nullptr && out != nullptr, SKB_EARG, "cache_create: null argument");
+    skb::validate_desc(*d);
+    const int64_t B = d->batch, Lmax = d->seq_len, H = d->heads, p = d->head_dim;
+    const int cap = (int)floor_k(d->k);
+    const int64_t S = cap + d->window + 1;
+    SKB_REQUIRE(S < (int64_t(1) << 24), SKB_ECONFIG, "cache: floor(k) + window too large");
+    auto* c = new skb_cache();
+    try {
+        c->d = *d;
+        CacheArgs& A = c->A;
+        A.Lmax = (int)Lmax;
+        A.S = (int)S;
+        A.cap = cap;
+        A.w = (int)d->window;
+        A.key_soft = d->key_mode;
+        A.mask_st = d->mask_mode;
+        A.row_bytes = H * p * (int64_t)esize_of(d->dtype);
+        A.ctl = c->alloc<CacheCtl>(B);
+        A.sv = c->alloc<double>(B * Lmax);
+        A.si = c->alloc<int>(B * Lmax);
+        A.fv = c->alloc<double>(B * Lmax);
+        A.fi = c->alloc<int>(B * Lmax);
+        A.u_hist = c->alloc<double>(B * Lmax);
+        A.slot_of = c->alloc<int>(B * Lmax);
+        A.pos_of = c->alloc<int>(B * S);
+        A.free_stack = c->alloc<int>(B * S);
+        A.att_slot = c->alloc<int>(B * S);
+        A.att_kg = c->alloc<float>(B * S);
+        A.att_vg = c->alloc<float>(B * S);
+        A.att_n = c->alloc<int>(B);
+        A.kpool = c->alloc<uint8_t>((size_t)(B * S) * A.row_bytes);
+        A.vpool = c->alloc<uint8_t>((size_t)(B * S) * A.row_bytes);
+        SKB_CHECK_CUDA(cudaMemset(A.kpool, 0, (size_t)(B * S) * A.row_bytes));
+        SKB_CHECK_CUDA(cudaMemset(A.vpool, 0, (size_t)(B * S) * A.row_bytes));
+        c->nsplit = (int)cdiv(S, kSlotsPerCta);
+        c->po = c->alloc<float>(B * c->nsplit * H * p);
+        c->pm = c->alloc<float>(B * c->nsplit * H);
+        c->pl = c->alloc<float>(B * c->nsplit * H);
+        c->vec = (p % 128 == 0) ? 4 : (p % 64 == 0) ? 2 : 1;
+        k_cache_init<<<(unsigned)B, 256>>>(A, d->k);
+        SKB_CHECK_LAUNCH();
+        SKB_CHECK_CUDA(cudaDeviceSynchronize());
+    } catch (...) {
+        delete c;
+        throw;
+    }
+    *out = c;
+    K5_END
+}
+
+int skb_cache_destroy(skb_cache* c) {
+    delete c;
+    return SKB_OK;
+}
+
+}  // extern "C"
+
+template <class T>
+static void cache_attend(skb_cache* c, const void* q, void* o, cudaStream_t st) {
+    const skb_attn_desc& d = c->d;
+    const int H = (int)d.heads, p = (int)d.head_dim;
+    const float scale = (float)(d.scale > 0.0 ? d.scale : 1.0 / std::sqrt((double)p));
+    const size_t smem = (size_t)H * p * 4 + (size_t)H * kSlotsPerCta * 4 + kSlotsPerCta * 8;
+    SKB_REQUIRE(smem <= 200 * 1024, SKB_ECONFIG, "cache: heads * head_dim too large for the decode kernel");
+    dim3 g((unsigned)c->nsplit, (unsigned)d.batch);
+    auto launch = [&](auto kern) {
+        if (smem > 48 * 1024)
+            SKB_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        kern<<<g, kAttnThreads, smem, st>>>(c->A, static_cast<const T*>(q), H, p, scale, c->po, c->pm, c->pl,
+                                            c->nsplit);
+    };
+    if (c->vec == 4) launch(k_cache_attn<T, 4>);
+    else if (c->vec == 2) launch(k_cache_attn<T, 2>);
+    else launch(k_cache_attn<T, 1>);
+    SKB_CHECK_LAUNCH();
+    k_cache_combine<T><<<dim3((unsigned)H, (unsigned)d.batch), 128, 0, st>>>(c->po, c->pm, c->pl, c->A.att_n, H,
+                                                                             p, c->nsplit, static_cast<T*>(o));
+    SKB_CHECK_LAUNCH();
+}
+
+extern "C" {
+
+int skb_cache_step(skb_cache* c, const void* q, const void* k, const void* v, const double* u, void* o,
+                   void* stream) {
+    K5_BEGIN
+    SKB_REQUIRE(c != nullptr, SKB_EARG, "cache_step: null cache");
+    SKB_REQUIRE(q && k && v && o, SKB_EARG, "cache_step: null tensor");
+    SKB_REQUIRE(u != nullptr || c->d.k == 0.0, SKB_EARG, "cache_step: null scores");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int B = (int)c->d.batch;
+    const double* uu = u;
+    if (!uu) {  // k = 0: scores idle (proj/src/cache.cpp:219-227)
+        static thread_local double* zeros = nullptr;
+        static thread_local int nz = 0;
+        if (nz < B) {
+            if (zeros) cudaFree(zeros);
+            SKB_CHECK_CUDA(cudaMalloc(&zeros, B * sizeof(double)));
+            SKB_CHECK_CUDA(cudaMemset(zeros, 0, B * sizeof(double)));
+            nz = B;
+        }
+        uu = zeros;
+    }
+    k_cache_control<<<(unsigned)cdiv(B, 4), 128, 0, st>>>(c->A, B, static_cast<const uint8_t*>(k),
+                                                          static_cast<const uint8_t*>(v), uu);
+    SKB_CHECK_LAUNCH();
+    if (c->d.dtype == SKB_BF16) cache_attend<__nv_bfloat16>(c, q, o, st);
+    else if (c->d.dtype == SKB_F32) cache_attend<float>(c, q, o, st);
+    else cache_attend<double>(c, q, o, st);
+    K5_END
+}
+
+int skb_cache_prefill(skb_cache* c, const void* k, const void* v, const double* u, int64_t n, void* stream) {
+    K5_BEGIN
+    SKB_REQUIRE(c != nullptr, SKB_EARG, "cache_prefill: null cache");
+    SKB_REQUIRE(n >= 0, SKB_EARG, "cache_prefill: n must be >= 0");
+    if (n == 0) return SKB_OK;
+    SKB_REQUIRE(k && v, SKB_EARG, "cache_prefill: null tensor");
+    SKB_REQUIRE(u != nullptr, SKB_EARG, "cache_prefill: null scores");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int B = (int)c->d.batch;
+    CacheCtl c0;
+    SKB_CHECK_CUDA(cudaMemcpyAsync(&c0, c->A.ctl, sizeof(c0), cudaMemcpyDeviceToHost, st));
+    SKB_CHECK_CUDA(cudaStreamSynchronize(st));
+    SKB_REQUIRE(c0.t + n <= c->A.Lmax, SKB_ESHAPE, "cache_prefill: more positions than seq_len");
+    k_cache_prefill<<<(unsigned)cdiv(B, 4), 128, 0, st>>>(c->A, B, u, (int)n);
+    SKB_CHECK_LAUNCH();
+    dim3 g((unsigned)cdiv(c->A.S, 8), (unsigned)B);
+    k_cache_fill_rows<<<g, 256, 0, st>>>(c->A, static_cast<const uint8_t*>(k), static_cast<const uint8_t*>(v),
+                                         (int)c0.t, (int)n);
+    SKB_CHECK_LAUNCH();
+    K5_END
+}
+
+int skb_cache_state(skb_cache* c, int64_t b, int32_t* positions, int64_t* count, double* tau, int64_t* seen,
+                    int64_t* peak, void* stream) {
+    K5_BEGIN
+    SKB_REQUIRE(c != nullptr, SKB_EARG, "cache_state: null cache");
+    SKB_REQUIRE(b >= 0 && b < c->d.batch, SKB_EARG, "cache_state: batch index out of range");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const CacheArgs& A = c->A;
+    CacheCtl cc;
+    SKB_CHECK_CUDA(cudaMemcpyAsync(&cc, A.ctl + b, sizeof(cc), cudaMemcpyDeviceToHost, st));
+    SKB_CHECK_CUDA(cudaStreamSynchronize(st));
+    SKB_REQUIRE(cc.error == 0, cc.error == 2 ? SKB_ESHAPE : SKB_ENUMERIC,
+                cc.error == 2 ? "cache: more positions than seq_len" : "stream scan exhausted (internal)");
+    std::vector<int> sel(cc.nsel);
+    if (cc.nsel)
+        SKB_CHECK_CUDA(cudaMemcpyAsync(sel.data(), A.si + b * A.Lmax, cc.nsel * 4, cudaMemcpyDeviceToHost, st));
+    SKB_CHECK_CUDA(cudaStreamSynchronize(st));
+    std::sort(sel.begin(), sel.end());
+    // retained_positions: cache (ascending) then the window ring (proj/src/cache.cpp:585-589)
+    std::vector<int> out(sel.begin(), sel.end());
+    const long long r0 = std::max<long long>(0, cc.t - A.w);
+    for (long long jp = r0; jp < cc.t; ++jp) out.push_back((int)jp);
+    if (positions)
+        for (size_t i = 0; i < out.size(); ++i) positions[i] = out[i];
+    if (count) *count = (int64_t)out.size();
+    if (tau) *tau = cc.st.tau;
+    if (seen) *seen = cc.t;
+    if (peak) *peak = cc.peak;
+    K5_END
+}
+
+}  // extern "C"

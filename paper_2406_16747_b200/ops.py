@@ -302,3 +302,75 @@ def topk_hard_rows(z: torch.Tensor, k: int):
     out = torch.empty_like(z)
     check(_lib.load().skb_topk_hard(n, m, z.data_ptr(), int(k), out.data_ptr(), _stream()))
     return out
+
+
+# ---------------------------------------------------------------- decode (K5)
+
+class DecodeCache:
+    """Constant-(floor(k)+w) KV cache for generation over skb_cache_*:
+    SparseKvCache + generate_step (proj/include/sparsek/cache.hpp:21-102,
+    proj/src/cache.cpp:570-577) at the q/k/v/u level for a batch of B
+    sequences. ``step`` consumes one new position per sequence (q/k/v
+    [B, H, p], u float64 [B]) and returns o [B, H, p]; ``prefill`` appends a
+    prompt (k/v [B, n, H, p], u [B, n]) without attending."""
+
+    def __init__(self, batch, heads, head_dim, cfg: AttnConfig, max_len, dtype=torch.bfloat16,
+                 device=None):
+        import ctypes
+
+        self.B, self.H, self.p = int(batch), int(heads), int(head_dim)
+        self.cfg, self.dtype, self.max_len = cfg, dtype, int(max_len)
+        self.device = torch.device(device) if device is not None else torch.device(
+            "cuda", torch.cuda.current_device())
+        self._desc = make_desc(self.B, self.max_len, self.H, self.p, cfg, dtype)
+        self._h = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            check(_lib.load().skb_cache_create(self._desc, ctypes.byref(self._h)))
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                _lib.load().skb_cache_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    def _chk(self, t, shape, dtype, name):
+        if tuple(t.shape) != tuple(shape):
+            raise _lib.ShapeError(f"cache: {name} must be {tuple(shape)}, got {tuple(t.shape)}")
+        if t.dtype != dtype or not t.is_cuda:
+            raise _lib.ArgumentError(f"cache: {name} must be a CUDA {dtype} tensor")
+        return t.contiguous()
+
+    def step(self, q, k, v, u, out=None):
+        shp = (self.B, self.H, self.p)
+        q, k, v = (self._chk(t, shp, self.dtype, n) for t, n in ((q, "q"), (k, "k"), (v, "v")))
+        u = self._chk(u, (self.B,), torch.float64, "u")
+        o = torch.empty_like(q) if out is None else out
+        check(_lib.load().skb_cache_step(self._h, q.data_ptr(), k.data_ptr(), v.data_ptr(),
+                                         u.data_ptr(), o.data_ptr(), _stream()))
+        return o
+
+    def prefill(self, k, v, u):
+        n = k.shape[1]
+        shp = (self.B, n, self.H, self.p)
+        k, v = (self._chk(t, shp, self.dtype, nm) for t, nm in ((k, "k"), (v, "v")))
+        u = self._chk(u, (self.B, n), torch.float64, "u")
+        check(_lib.load().skb_cache_prefill(self._h, k.data_ptr(), v.data_ptr(), u.data_ptr(), n,
+                                            _stream()))
+
+    def state(self, b=0):
+        """{positions (selected asc, then window asc), tau, seen, peak}."""
+        import ctypes
+
+        import numpy as np
+
+        pos = np.zeros(max(1, int(math.floor(self.cfg.k)) + self.cfg.window + 1), np.int32)
+        cnt, seen, peak = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        tau = ctypes.c_double()
+        check(_lib.load().skb_cache_state(self._h, int(b), pos.ctypes.data, ctypes.byref(cnt),
+                                          ctypes.byref(tau), ctypes.byref(seen), ctypes.byref(peak),
+                                          _stream()))
+        return {"positions": pos[: cnt.value].astype(np.int64), "tau": tau.value,
+                "seen": seen.value, "peak": peak.value}

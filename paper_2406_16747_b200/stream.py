@@ -53,12 +53,16 @@ class Stream:
                                            self._ins.data_ptr(),
                                            torch.cuda.current_stream().cuda_stream))
         tau = float(self._tau.item())
+        inserted = bool(self._ins.item())
         _, _, ev = self._survivors()
-        evicted = [i for i in range(before.t + 1) if ev[i] and not self._ev_prev[i]] \
-            if hasattr(self, "_ev_prev") else [i for i in range(before.t + 1) if ev[i]]
+        prev = getattr(self, "_ev_prev", np.zeros(0, bool))
+        new = ev.copy()
+        new[: len(prev)] &= ~prev
+        if not inserted:  # a rejected arrival is flagged but not reported (stream.cpp:83-88)
+            new[before.t] = False
         self._ev_prev = ev
         return {"tau": tau if math.isfinite(tau) else None, "t": before.t + 1,
-                "inserted": bool(self._ins.item()), "evicted": evicted}
+                "inserted": inserted, "evicted": [int(i) for i in np.nonzero(new)[0]]}
 
     def _survivors(self):
         info = self._info()

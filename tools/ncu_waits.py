@@ -1,28 +1,37 @@
-"""Attribute stall samples of mbarrier wait loops to barrier offsets (ncu report)."""
-import collections
+"""Stall samples per mbarrier wait site of an ncu report (sm_100 SASS source page).
+usage: python tools/ncu_waits.py report.ncu-rep kernel_regex bar_base_offset name,name,..."""
 import csv
 import io
 import re
 import subprocess
 import sys
 
-rep = sys.argv[1]
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv"], capture_output=True, text=True).stdout
+rep, kern = sys.argv[1], sys.argv[2]
+base = int(sys.argv[3]) if len(sys.argv) > 3 else None
+names = sys.argv[4].split(",") if len(sys.argv) > 4 else []
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "-k", f"regex:{kern}"],
+                     capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 h = rows[1]
-si, st, ie = h.index("Source"), h.index("Warp Stall Sampling (All Samples)"), h.index("Instructions Executed")
-body = rows[2:]
-tot = sum(int(r[st] or 0) for r in body if len(r) > st and (r[st] or "0").isdigit())
-by = collections.Counter()
-cnt = collections.Counter()
-for k, r in enumerate(body):
-    if "TRYWAIT" in r[si]:
-        m = re.search(r"\[(R\d+)\+URZ\+(0x[0-9a-f]+)\]|\[(UR\d+)\+(0x[0-9a-f]+)\]", r[si])
-        off = (m.group(2) or m.group(4)) if m else "?"
-        # the sleep/poll instructions that follow belong to the same wait
-        s = sum(int(body[k + d][st] or 0) for d in range(0, 4) if k + d < len(body))
-        by[(k, off)] += s
-        cnt[(k, off)] += int(r[ie] or 0)
+data = rows[2:]
+si, st = h.index("Source"), h.index("Warp Stall Sampling (All Samples)")
+ie = h.index("Instructions Executed")
+tot = sum(int(r[st] or 0) for r in data)
+acc = {}
+i = 0
+while i < len(data):
+    s = data[i][si]
+    if "SYNCS.PHASECHK" in s and "TRYWAIT" in s:
+        m = re.search(r"\+(0x[0-9a-f]+)\]", s)
+        off = int(m.group(1), 16) if m else -1
+        samples = sum(int(data[j][st] or 0) for j in range(i, min(i + 4, len(data))))
+        tag = hex(off)
+        if base is not None and off >= base and (off - base) % 8 == 0 and (off - base) // 8 < len(names):
+            tag = names[(off - base) // 8]
+        acc.setdefault(tag, [0, 0])
+        acc[tag][0] += samples
+        acc[tag][1] += int(data[i][ie] or 0)
+    i += 1
 print("total samples", tot)
-for (k, off), s in by.most_common(20):
-    print(f"  #{k:5d} bar+{off:>8s}  samples {s:7d} ({100 * s / tot:4.1f}%)  polls {cnt[(k, off)]}")
+for k, (s, n) in sorted(acc.items(), key=lambda x: -x[1][0]):
+    print(f"{k:12s} {s:8d} {100 * s / tot:5.1f}%  waits={n}")
