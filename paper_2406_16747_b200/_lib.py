@@ -64,6 +64,7 @@ class SelectLayout(C.Structure):
                 ("nfrac", C.c_uint64), ("qb_count", C.c_uint64), ("qb_list", C.c_uint64),
                 ("ever_count", C.c_uint64), ("ever_list", C.c_uint64), ("misc", C.c_uint64),
                 ("scratch", C.c_uint64), ("uf", C.c_uint64), ("tauf", C.c_uint64),
+                ("qb_leave", C.c_uint64), ("qb_uf", C.c_uint64), ("qb_flags", C.c_uint64),
                 ("total_bytes", C.c_uint64), ("qblock", C.c_int64),
                 ("nqb", C.c_int64), ("qb_cap", C.c_int64)]
 

@@ -4,18 +4,21 @@
 //   [selected-union tiles: gathered rows, per-key interval mask
 //    j <= t_i < leave_j, value gates g = sat(u_j - tau_i)]
 //   ++ [window tiles: the contiguous band [i0-w+1, i0+127], band mask].
-// Per tile: S = Q K^T (tcgen05, M=N=128, K=d, fp32 in TMEM, double-buffered)
-// -> two math warpgroups, each owning 64 of the 128 columns of every row:
-// mask, row max (exchanged through smem), lazy rescale (the exponent base
-// moves only when the max grows by > 2^8), P = exp2(.), gated P~ = P*g ->
-// bf16 P~ in 128B-swizzled smem -> O += P~ V (tcgen05, accumulator in TMEM).
-// Softmax statistics use the ungated P: proj/src/cache.cpp:358-393 (softmax
-// over Sel U W, value gates applied after, no renormalisation).
+// Per tile: S = Q K^T (tcgen05, M=N=128, K=d, fp32 in TMEM, double-buffered).
+// Two math warpgroups each own one half of every tile's keys (64 columns) and
+// run an independent online softmax over them with their own accumulator
+// O_h += P~_h V_h (TS-MMA: P~ = P*g packed to bf16 in TMEM over the consumed
+// S columns) — no per-tile exchange between the halves; the two partial
+// softmaxes are merged once in the epilogue. Softmax statistics use the
+// ungated P: proj/src/cache.cpp:358-393 (softmax over Sel U W, value gates
+// applied after, no renormalisation).
 //
-// Producers fill K/V stages with cp.async row gathers (completion tracked by
-// mbarriers) and publish two per-tile flags so most tiles skip the mask and
-// the gates entirely: bit0 = every key valid for every query of the block,
-// bit1 = every gate saturated (u_j >= tau(t_hi) + 1).
+// Producers (3 warps) fill K/V stages with cp.async row gathers whose keys
+// were fetched one tile ahead, and copy the block's precomputed per-tile
+// metadata (keys, leave, u, fast-path flags from skb_select) — no dependent
+// global loads on the pipeline. The O rescale of the lazy softmax (exponent
+// base moves only when the max grows by > 2^8) is the only place the math
+// waits for a PV MMA.
 #include "skb_common.cuh"
 #include "skb_internal.h"
 #include "skb_tc.cuh"
@@ -39,18 +42,19 @@ struct FwdArgs {
     const __nv_bfloat16* v;
     __nv_bfloat16* o;
     double* lse;
-    const float* uf;
     const float* tauf;
-    const int* leave;
     const int* qb_count;
     const int* qb_list;
+    const int* qb_leave;
+    const float* qb_uf;
+    const int* qb_flags;
     int nqb, qb_cap;
     int B, L, H, w, T, R1;
     float scale_log2;
     int mask_st;
 };
 
-constexpr int kKS = 3;  // K ring depth (V ring: 2). P~ lives in TMEM, not smem.
+constexpr int kKS = 3;  // K + metadata ring depth (V ring: 2)
 
 template <int D>
 struct FwdSmem {
@@ -59,22 +63,26 @@ struct FwdSmem {
     static constexpr int kK = kQ + kTile;          // [kKS]
     static constexpr int kV = kK + kKS * kTile;    // [2]
     static constexpr int kMeta = kV + 2 * kTile;   // [kKS][key|leave|uf][128] x 4 B
-    static constexpr int kFlags = kMeta + kKS * 3 * 128 * 4;  // [kKS][4]
-    static constexpr int kRed = kFlags + kKS * 4 * 4;   // [2 parity][2 halves][128] f32
+    static constexpr int kFlags = kMeta + kKS * 3 * 128 * 4;  // [kKS] (16 B apart)
+    static constexpr int kRed = kFlags + kKS * 16;            // [2 halves][m|l][128] f32
     static constexpr int kBar = kRed + 2 * 2 * 128 * 4;
-    static constexpr int kTmemSlot = kBar + 24 * 8;  // 23 barriers
+    static constexpr int kNumBars = 28;
+    static constexpr int kTmemSlot = kBar + kNumBars * 8;
     static constexpr int kBytes = kTmemSlot + 16;
     static constexpr int kAlloc = kBytes + 1024;  // room to align the base to 1024
 };
 
-enum { B_QFULL = 0, B_KFULL = 1, B_KEMPTY = 4, B_SFULL = 7, B_SEMPTY = 9, B_PFULL = 11, B_PVDONE = 12,
-       B_VFULL = 13, B_VEMPTY = 15, B_MFULL = 17, B_MEMPTY = 20 };  // 23 barriers
+// PFULL is per (S stage, half): a warpgroup may finish tile j+1 before the MMA
+// warp consumes tile j's P~, so one barrier per half could run two phases ahead.
+enum { B_QFULL = 0, B_KFULL = 1, B_KEMPTY = 4, B_MFULL = 7, B_MEMPTY = 10, B_VFULL = 13, B_VEMPTY = 15,
+       B_SFULL = 17, B_SEMPTY = 19, B_PFULL = 21, B_PVDONE = 25, B_ODONE = 27 };  // 28 barriers
 
 template <int D, bool KEY_SOFT>
 __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
     using SM = FwdSmem<D>;
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    // keep the shared address space visible to the compiler (LDS/STS, not generic)
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const uint32_t sbase = smem_u32(smem);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SM::kBar);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + SM::kTmemSlot);
@@ -85,21 +93,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
     const int qb = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t bl = (int64_t)b * a.L;
+    const int64_t qrow = (int64_t)b * a.nqb + qb;
     const int i0 = qb * 128;
-    const int cnt = (a.R1 > 0) ? a.qb_count[(int64_t)b * a.nqb + qb] : 0;
+    const int cnt = (a.R1 > 0) ? a.qb_count[qrow] : 0;
     const int n_sel = (cnt + 127) / 128;
     const int n_win = (a.w + 127 + 127) / 128;
     const int n = n_sel + n_win;
     const int jw0 = i0 - a.w + 1;  // first key of the window band
-    const int* list = a.qb_list + ((int64_t)b * a.nqb + qb) * a.qb_cap;
 
     if (threadIdx.x == 0) {
         mbar_init(&bars[B_QFULL], kProducers);
         for (int s = 0; s < kKS; ++s) {
             mbar_init(&bars[B_KFULL + s], kProducers);
             mbar_init(&bars[B_KEMPTY + s], 1);
-            // metadata: 96 cp.async completions + 96 plain arrivals (which release the flags)
-            mbar_init(&bars[B_MFULL + s], 2 * kProducers);
+            mbar_init(&bars[B_MFULL + s], kProducers);
             mbar_init(&bars[B_MEMPTY + s], kMath);
         }
         for (int s = 0; s < 2; ++s) {
@@ -107,9 +114,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
             mbar_init(&bars[B_VEMPTY + s], 1);
             mbar_init(&bars[B_SFULL + s], 1);
             mbar_init(&bars[B_SEMPTY + s], kMath);
+            mbar_init(&bars[B_PFULL + 2 * s], kMath / 2);
+            mbar_init(&bars[B_PFULL + 2 * s + 1], kMath / 2);
+            mbar_init(&bars[B_PVDONE + s], 1);
         }
-        mbar_init(&bars[B_PFULL], kMath);
-        mbar_init(&bars[B_PVDONE], 1);
+        mbar_init(&bars[B_ODONE], 1);
         mbar_fence_init();
     }
     if (warp == kMmaWarp) tmem_alloc<512>(tmem_slot);
@@ -117,65 +126,52 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
     __syncthreads();
     tc_after_sync();
     const uint32_t tmem = *tmem_slot;
-    const uint32_t tS = tmem, tO = tmem + 256;
+    const uint32_t tS = tmem, tO = tmem + 256;  // O half h at tO + h * 128
 
     if (warp >= kProdWarp0 && warp < kMmaWarp) {
         // ------------------------------------------------------------ producers
         const int pw = warp - kProdWarp0, ptid = threadIdx.x - kProdWarp0 * 32;
-        load_tile<D, 128>(sbase + SM::kQ, a.q, b, h, a.L, a.H, pw, lane,
-                          [&](int r) { return i0 + r < a.L ? i0 + r : -1; });
+        {
+            RowKeys<D, 128> qk;
+            qk.fetch(pw, lane, [&](int r) { return i0 + r < a.L ? i0 + r : -1; });
+            qk.issue(sbase + SM::kQ, a.q, b, h, a.L, a.H, pw, lane);
+        }
         cp_async_arrive_noinc(&bars[B_QFULL]);
-        const int t_lo = i0 - a.w;
-        const int t_hi = min(i0 + 127, a.L - 1) - a.w;
-        const float tau_hi = (t_hi >= 0 && a.R1 > 0) ? __ldg(a.tauf + bl + t_hi) : -INFINITY;
-        // K is released by the QK^T commit, the metadata by the math warps once
-        // they are done with the tile, V by the PV commit. K + metadata run one
-        // tile ahead of V so a softmax never waits for a V gather.
+        const int* list = a.qb_list + qrow * a.qb_cap;
         auto keyfn = [&](int jt, int r) {
-            if (jt < n_sel) {
-                const int idx = jt * 128 + r;
-                return idx < cnt ? __ldg(list + idx) : -1;
-            }
+            if (jt < n_sel) return __ldg(list + jt * 128 + r);  // padded with -1
             return jw0 + (jt - n_sel) * 128 + r;
         };
+        RowKeys<D, 128> kcur, kprev;
+        kcur.fetch(pw, lane, [&](int r) { return keyfn(0, r); });
+        const int ma = ptid >> 5, mc = ptid & 31;  // metadata: array, 16-byte chunk
+        const int* msrc = ma == 0 ? a.qb_list : ma == 1 ? a.qb_leave : reinterpret_cast<const int*>(a.qb_uf);
+        // K + metadata run one tile ahead of V so a softmax never waits for a V gather
         for (int jt = 0; jt <= n; ++jt) {
+            RowKeys<D, 128> knext;
             if (jt < n) {
                 const int ks = jt % kKS;
-                if (jt >= kKS) mbar_wait(&bars[B_KEMPTY + ks], ((jt - kKS) / kKS) & 1);
-                load_tile<D, 128>(sbase + SM::kK + ks * SM::kTile, a.k, b, h, a.L, a.H, pw, lane,
-                                  [&](int r) { return keyfn(jt, r); });
-                cp_async_arrive_noinc(&bars[B_KFULL + ks]);
                 if (jt >= kKS) mbar_wait(&bars[B_MEMPTY + ks], ((jt - kKS) / kKS) & 1);
                 if (jt < n_sel) {
-                    bool all_ok = true, all_sat = true;
-                    for (int c = ptid; c < 128; c += kProducers) {
-                        const int idx = jt * 128 + c;
-                        const int key = idx < cnt ? __ldg(list + idx) : -1;
-                        const uint32_t mb = smem_u32(meta + (ks * 3) * 128 + c);
-                        cp_async4(mb, list + (idx < cnt ? idx : 0), idx < cnt);
-                        cp_async4(mb + 128 * 4, a.leave + bl + (key >= 0 ? key : 0), key >= 0);
-                        cp_async4(mb + 256 * 4, a.uf + bl + (key >= 0 ? key : 0), key >= 0);
-                        if (key >= 0) {
-                            all_ok = all_ok && key <= t_lo && __ldg(a.leave + bl + key) > t_hi;
-                            all_sat = all_sat && __ldg(a.uf + bl + key) >= tau_hi + 1.f;
-                        } else {
-                            all_ok = false;
-                        }
-                    }
-                    all_ok = __all_sync(0xffffffffu, all_ok);
-                    all_sat = __all_sync(0xffffffffu, all_sat);
-                    if (lane == 0) tflags[ks * 4 + pw] = (all_ok ? 1 : 0) | (all_sat ? 2 : 0);
+                    cp_async16(smem_u32(meta + (ks * 3 + ma) * 128 + mc * 4),
+                               msrc + qrow * a.qb_cap + jt * 128 + mc * 4, true);
+                    if (ptid == 0)
+                        cp_async4(smem_u32(tflags + ks * 4), a.qb_flags + qrow * (a.qb_cap / 128) + jt, true);
                 }
-                mbar_arrive(&bars[B_MFULL + ks]);
                 cp_async_arrive_noinc(&bars[B_MFULL + ks]);
+                if (jt >= kKS) mbar_wait(&bars[B_KEMPTY + ks], ((jt - kKS) / kKS) & 1);
+                kcur.issue(sbase + SM::kK + ks * SM::kTile, a.k, b, h, a.L, a.H, pw, lane);
+                cp_async_arrive_noinc(&bars[B_KFULL + ks]);
+                if (jt + 1 < n) knext.fetch(pw, lane, [&](int r) { return keyfn(jt + 1, r); });
             }
             if (jt >= 1) {
                 const int j = jt - 1, vs = j & 1;
                 if (j >= 2) mbar_wait(&bars[B_VEMPTY + vs], ((j - 2) >> 1) & 1);
-                load_tile<D, 128>(sbase + SM::kV + vs * SM::kTile, a.v, b, h, a.L, a.H, pw, lane,
-                                  [&](int r) { return keyfn(j, r); });
+                kprev.issue(sbase + SM::kV + vs * SM::kTile, a.v, b, h, a.L, a.H, pw, lane);
                 cp_async_arrive_noinc(&bars[B_VFULL + vs]);
             }
+            kprev = kcur;
+            kcur = knext;
         }
     } else if (warp == kMmaWarp) {
         // ------------------------------------------------------------ MMA issuer
@@ -186,15 +182,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
             fence_proxy_async();
             auto pv = [&](int j) {
                 mbar_wait(&bars[B_VFULL + (j & 1)], (j >> 1) & 1);
-                mbar_wait(&bars[B_PFULL], j & 1);
                 fence_proxy_async();
-                tc_after_sync();
                 const uint32_t vb = sbase + SM::kV + (j & 1) * SM::kTile;
-                const uint32_t pa = tS + (j & 1) * 128;  // P~ packed over this tile's S columns
 #pragma unroll
-                for (int kk = 0; kk < 8; ++kk)
-                    umma_f16_ts(tO, pa + kk * 8, desc_mnmajor(vb, 128, kk), idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
-                umma_commit(&bars[B_PVDONE]);
+                for (int hf = 0; hf < 2; ++hf) {
+                    mbar_wait(&bars[B_PFULL + 2 * (j & 1) + hf], (j >> 1) & 1);
+                    tc_after_sync();
+                    // P~ of this half: 64 keys packed over the first 32 of its own S columns
+                    const uint32_t pa = tS + (j & 1) * 128 + hf * 64;
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk)
+                        umma_f16_ts(tO + hf * 128, pa + kk * 8, desc_mnmajor(vb, 128, hf * 4 + kk), idesc_pv,
+                                    (j > 0 || kk > 0) ? 1u : 0u);
+                    umma_commit(&bars[B_PVDONE + hf]);
+                }
                 umma_commit(&bars[B_VEMPTY + (j & 1)]);
             };
             for (int jt = 0; jt < n; ++jt) {
@@ -214,11 +215,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
                 if (jt >= 1) pv(jt - 1);
             }
             pv(n - 1);
+            umma_commit(&bars[B_ODONE]);  // every MMA of the CTA complete
         }
         __syncwarp();
     } else {
         // ------------------------------------------------------------ math (warps 0-7)
-        const int hf = warp >> 2;                // column half: 0 -> cols 0..63, 1 -> 64..127
+        const int hf = warp >> 2;                // key half: 0 -> tile cols 0..63, 1 -> 64..127
         const int r = ((warp & 3) << 5) | lane;  // tile row = TMEM lane
         const int c0 = hf * 64;
         const int i = i0 + r;
@@ -226,15 +228,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
         const float tau_i = (t >= 0 && a.R1 > 0) ? a.tauf[bl + t] : -INFINITY;
         const int lo_win = max(i - a.w + 1, 0);
         const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+        const uint32_t tOh = tO + hf * 128;
         const float sl2 = a.scale_log2;
-        float m = -INFINITY, l = 0.f;  // l: this half's partial row sum
+        float m = -INFINITY, l = 0.f;  // this half's running max (log2 units) and sum
         float sv[64];
         for (int jt = 0; jt < n; ++jt) {
             const int s = jt & 1;
             const bool is_sel = jt < n_sel;
-            mbar_wait(&bars[B_SFULL + s], (jt >> 1) & 1);
             const int ks = jt % kKS;
-            mbar_wait(&bars[B_MFULL + ks], (jt / kKS) & 1);  // metadata + flags visibility
+            mbar_wait(&bars[B_SFULL + s], (jt >> 1) & 1);
+            if (is_sel) mbar_wait(&bars[B_MFULL + ks], (jt / kKS) & 1);
             tc_after_sync();
             tmem_ld32(tS + lane_off + s * 128 + c0, sv);
             tmem_ld32(tS + lane_off + s * 128 + c0 + 32, sv + 32);
@@ -242,24 +245,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
             tc_before_sync();
             mbar_arrive(&bars[B_SEMPTY + s]);
 
-#if SKB_EXP == 1
-            if (true) {  // experiment: no softmax work
-                if (jt >= 1) {
-                    mbar_wait(&bars[B_PVDONE], (jt - 1) & 1);
-                    tc_after_sync();
-                }
-                tc_before_sync();
-                mbar_arrive(&bars[B_MEMPTY + ks]);
-                mbar_arrive(&bars[B_PFULL]);
-                continue;
-            }
-#endif
             const int* mk = meta + (ks * 3) * 128 + c0;
             const int* ml = mk + 128;
             const float* mu = reinterpret_cast<const float*>(mk + 256);
             int fl = 3;
             if (is_sel) {
-                fl = tflags[ks * 4] & tflags[ks * 4 + 1] & tflags[ks * 4 + 2];
+                fl = tflags[ks * 4];
                 if (KEY_SOFT) {  // gated logits (proj/src/cache.cpp:368-369)
 #pragma unroll
                     for (int c = 0; c < 64; c += 4) {
@@ -270,15 +261,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
                         sv[c + 3] *= __saturatef(uu.w - tau_i);
                     }
                 }
-                if (!(fl & 1)) {  // per-key interval mask j <= t < leave_j
+                if (!(fl & 1)) {  // per-key interval mask j <= t < leave_j (padding: key -1)
 #pragma unroll
                     for (int c = 0; c < 64; c += 4) {
                         const int4 kj = *reinterpret_cast<const int4*>(mk + c);
                         const int4 lv = *reinterpret_cast<const int4*>(ml + c);
-                        sv[c + 0] = (kj.x <= t && lv.x > t) ? sv[c + 0] : -INFINITY;
-                        sv[c + 1] = (kj.y <= t && lv.y > t) ? sv[c + 1] : -INFINITY;
-                        sv[c + 2] = (kj.z <= t && lv.z > t) ? sv[c + 2] : -INFINITY;
-                        sv[c + 3] = (kj.w <= t && lv.w > t) ? sv[c + 3] : -INFINITY;
+                        sv[c + 0] = (kj.x >= 0 && kj.x <= t && lv.x > t) ? sv[c + 0] : -INFINITY;
+                        sv[c + 1] = (kj.y >= 0 && kj.y <= t && lv.y > t) ? sv[c + 1] : -INFINITY;
+                        sv[c + 2] = (kj.z >= 0 && kj.z <= t && lv.z > t) ? sv[c + 2] : -INFINITY;
+                        sv[c + 3] = (kj.w >= 0 && kj.w <= t && lv.w > t) ? sv[c + 3] : -INFINITY;
                     }
                 }
             } else {
@@ -291,14 +282,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
                     for (int c = 0; c < 64; ++c) sv[c] = (c >= cmin && c <= cmax) ? sv[c] : -INFINITY;
                 }
             }
-            // row max over both halves
             float mr = sv[0];
 #pragma unroll
             for (int c = 1; c < 64; ++c) mr = fmaxf(mr, sv[c]);
-            float* rb = red + (jt & 1) * 256;
-            rb[hf * 128 + r] = mr;
-            math_bar();
-            mr = fmaxf(mr, rb[(hf ^ 1) * 128 + r]);
             const float mt = mr * sl2;  // scale > 0: max commutes with scaling
             float fac = 1.f;
             bool need = false;
@@ -332,66 +318,73 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
                     sv[c + 3] *= __saturatef(uu.w - tau_i);
                 }
             }
-            if (jt >= 1) {
-                mbar_wait(&bars[B_PVDONE], (jt - 1) & 1);
+            if (__any_sync(0xffffffffu, need)) {
+                // O_h must hold PV(jt-1) before it is rescaled; PV(jt-2) is
+                // already complete (S(jt) was committed after it)
+                mbar_wait(&bars[B_PVDONE + hf], (jt - 1) & 1);
                 tc_after_sync();
-            }
-            if (__any_sync(0xffffffffu, need)) {  // rescale this half's O columns
                 float ov[32];
 #pragma unroll
-                for (int c = 0; c < D / 64; ++c) {
-                    const uint32_t ta = tO + lane_off + hf * (D / 2) + c * 32;
+                for (int c = 0; c < D / 32; ++c) {
+                    const uint32_t ta = tOh + lane_off + c * 32;
                     tmem_ld32(ta, ov);
                     tmem_wait_ld();
 #pragma unroll
                     for (int e = 0; e < 32; ++e) ov[e] *= fac;
                     tmem_st32(ta, ov);
                 }
-                tmem_wait_st();
             }
-            // P~ (this half's 64 keys) -> TMEM over this tile's consumed S columns,
-            // packed bf16x2: the A operand of the PV MMA
+            // P~ (this half's 64 keys) -> TMEM over the tile's consumed S
+            // columns, packed bf16x2: the A operand of this half's PV MMA
             {
                 uint32_t pk[16];
 #pragma unroll
                 for (int e = 0; e < 16; ++e) pk[e] = pack_bf16(sv[2 * e], sv[2 * e + 1]);
-                tmem_st16u(tS + lane_off + s * 128 + hf * 32, pk);
+                tmem_st16u(tS + lane_off + s * 128 + c0, pk);
 #pragma unroll
                 for (int e = 0; e < 16; ++e) pk[e] = pack_bf16(sv[32 + 2 * e], sv[33 + 2 * e]);
-                tmem_st16u(tS + lane_off + s * 128 + hf * 32 + 16, pk);
+                tmem_st16u(tS + lane_off + s * 128 + c0 + 16, pk);
                 tmem_wait_st();
             }
             tc_before_sync();
-            mbar_arrive(&bars[B_MEMPTY + ks]);
-            mbar_arrive(&bars[B_PFULL]);
+            mbar_arrive(&bars[B_MEMPTY + ks]);  // every tile (the producer waits on each stage)
+            mbar_arrive(&bars[B_PFULL + 2 * s + hf]);
         }
-        // epilogue: O / l, lse. The row's l is the sum of both halves' partials.
-        float* rb = red + (n & 1) * 256;
-        rb[hf * 128 + r] = l;
+        // epilogue: merge the two halves' softmaxes; half h writes O columns
+        // [h*D/2, (h+1)*D/2) = (O_0 f_0 + O_1 f_1) / (l_0 f_0 + l_1 f_1)
+        red[(hf * 2 + 0) * 128 + r] = m;
+        red[(hf * 2 + 1) * 128 + r] = l;
         math_bar();
-        const float lrow = l + rb[(hf ^ 1) * 128 + r];
-        mbar_wait(&bars[B_PVDONE], (n - 1) & 1);
+        const float mo = red[((hf ^ 1) * 2 + 0) * 128 + r];
+        const float lo = red[((hf ^ 1) * 2 + 1) * 128 + r];
+        const float M = fmaxf(m, mo);
+        const float fs = (m == -INFINITY) ? 0.f : ex2(m - M);
+        const float fo = (mo == -INFINITY) ? 0.f : ex2(mo - M);
+        const float lrow = l * fs + lo * fo;
+        const float f0 = hf == 0 ? fs : fo, f1 = hf == 0 ? fo : fs;
+        mbar_wait(&bars[B_ODONE], 0);
         tc_after_sync();
         const float inv = lrow > 0.f ? 1.f / lrow : 0.f;
         __nv_bfloat16* orow = a.o + ((bl + (i < a.L ? i : 0)) * a.H + h) * D + hf * (D / 2);
 #pragma unroll
         for (int c = 0; c < D / 64; ++c) {
-            float ov[32];
-            tmem_ld32(tO + lane_off + hf * (D / 2) + c * 32, ov);
+            float o0[32], o1[32];
+            tmem_ld32(tO + lane_off + hf * (D / 2) + c * 32, o0);
+            tmem_ld32(tO + 128 + lane_off + hf * (D / 2) + c * 32, o1);
             tmem_wait_ld();
             if (i < a.L) {
 #pragma unroll
                 for (int e = 0; e < 32; e += 8) {
                     uint4 pk;
-                    pk.x = pack_bf16(ov[e] * inv, ov[e + 1] * inv);
-                    pk.y = pack_bf16(ov[e + 2] * inv, ov[e + 3] * inv);
-                    pk.z = pack_bf16(ov[e + 4] * inv, ov[e + 5] * inv);
-                    pk.w = pack_bf16(ov[e + 6] * inv, ov[e + 7] * inv);
+                    pk.x = pack_bf16((o0[e] * f0 + o1[e] * f1) * inv, (o0[e + 1] * f0 + o1[e + 1] * f1) * inv);
+                    pk.y = pack_bf16((o0[e + 2] * f0 + o1[e + 2] * f1) * inv, (o0[e + 3] * f0 + o1[e + 3] * f1) * inv);
+                    pk.z = pack_bf16((o0[e + 4] * f0 + o1[e + 4] * f1) * inv, (o0[e + 5] * f0 + o1[e + 5] * f1) * inv);
+                    pk.w = pack_bf16((o0[e + 6] * f0 + o1[e + 6] * f1) * inv, (o0[e + 7] * f0 + o1[e + 7] * f1) * inv);
                     *reinterpret_cast<uint4*>(orow + c * 32 + e) = pk;
                 }
             }
         }
-        if (hf == 0 && i < a.L) a.lse[((int64_t)b * a.H + h) * a.L + i] = (double)((m + __log2f(lrow)) * kLn2);
+        if (hf == 0 && i < a.L) a.lse[((int64_t)b * a.H + h) * a.L + i] = (double)((M + __log2f(lrow)) * kLn2);
     }
     tc_before_sync();
     __syncthreads();
@@ -430,11 +423,12 @@ void run_attn_fwd_tc(const skb_attn_desc& d, const void* q, const void* k, const
     a.v = static_cast<const __nv_bfloat16*>(v);
     a.o = static_cast<__nv_bfloat16*>(o);
     a.lse = lse;
-    a.uf = s.uf;
     a.tauf = s.tauf;
-    a.leave = s.leave;
     a.qb_count = s.qb_count;
     a.qb_list = s.qb_list;
+    a.qb_leave = s.qb_leave;
+    a.qb_uf = s.qb_uf;
+    a.qb_flags = s.qb_flags;
     a.nqb = s.nqb;
     a.qb_cap = s.qb_cap;
     a.B = (int)d.batch;

@@ -24,6 +24,9 @@ struct SelView {
     const int* ever_list;
     const float* uf;    // u as fp32 [B, L]
     const float* tauf;  // tau as fp32 [B, L] (push time)
+    const int* qb_leave;    // [B, NQB, qb_cap] leave of each union entry
+    const float* qb_uf;     // [B, NQB, qb_cap] u of each union entry
+    const int* qb_flags;    // [B, NQB, qb_cap / 128]
     int nqb, qb_cap;
 };
 SelView sel_view(const skb_attn_desc& d, const void* ws);

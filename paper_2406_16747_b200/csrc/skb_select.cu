@@ -407,6 +407,42 @@ k_ever_list(const int* __restrict__ leave1, int L, int T, int* __restrict__ ever
     if (threadIdx.x == 0) ever_count[b] = base_s;
 }
 
+// Per-block metadata for the tensor-core kernels, so their producers issue no
+// dependent loads: for every union entry (padded to whole 128-entry tiles with
+// key -1) its leave and u, and per tile the fast-path flags.
+__global__ void __launch_bounds__(128)
+k_union_meta(const int* __restrict__ leave1, const float* __restrict__ uf, const float* __restrict__ tauf,
+             int L, int T, int window, int nqb, int cap, const int* __restrict__ qb_count, int* __restrict__ qb_list,
+             int* __restrict__ qb_leave, float* __restrict__ qb_uf, int* __restrict__ qb_flags) {
+    const int b = blockIdx.y, qb = blockIdx.x;
+    const int64_t bl = (int64_t)b * L;
+    const int64_t row = (int64_t)b * nqb + qb;
+    const int cnt = qb_count[row];
+    const int t_lo = qb * kQBlock - window;
+    const int t_hi = min(qb * kQBlock + kQBlock - 1 - window, T - 1);
+    const float tau_hi = t_hi >= 0 ? tauf[bl + t_hi] : -INFINITY;
+    const int ntiles = (cnt + 127) / 128;
+    for (int t = 0; t < ntiles; ++t) {
+        const int idx = t * 128 + threadIdx.x;
+        int key = -1, lv = 0;
+        float u = 0.f;
+        if (idx < cnt) {
+            key = qb_list[row * cap + idx];
+            lv = leave1[bl + key];
+            u = uf[bl + key];
+        } else {
+            qb_list[row * cap + idx] = -1;
+        }
+        qb_leave[row * cap + idx] = lv;
+        qb_uf[row * cap + idx] = u;
+        const bool ok = key >= 0 && key <= t_lo && lv > t_hi;
+        const bool sat = key < 0 || u >= tau_hi + 1.f;
+        const int all_ok = __syncthreads_and(ok);
+        const int all_sat = __syncthreads_and(sat);
+        if (threadIdx.x == 0) qb_flags[row * (cap / 128) + t] = (all_ok ? 1 : 0) | (all_sat ? 2 : 0);
+    }
+}
+
 __global__ void k_to_float(const double* __restrict__ u, const double* __restrict__ tau,
                            float* __restrict__ uf, float* __restrict__ tauf, int64_t n) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -477,7 +513,7 @@ static uint64_t align256(uint64_t x) { return (x + 255) & ~uint64_t(255); }
 void select_layout(const skb_attn_desc& d, skb_select_layout& o) {
     const int64_t B = d.batch, L = d.seq_len;
     const int64_t nqb = cdiv(L, kQBlock);
-    const int64_t cap = floor_k(d.k) + kQBlock;
+    const int64_t cap = cdiv(floor_k(d.k) + kQBlock, 128) * 128;
     const int64_t nch = cdiv(L, kChunk);
     uint64_t off = 0;
     auto take = [&](uint64_t bytes) {
@@ -498,6 +534,9 @@ void select_layout(const skb_attn_desc& d, skb_select_layout& o) {
     o.scratch = take((uint64_t)kOverflowSlots * (cap2 + L + 1) * 8);
     o.uf = take(B * L * 4);
     o.tauf = take(B * L * 4);
+    o.qb_leave = take(B * nqb * cap * 4);
+    o.qb_uf = take(B * nqb * cap * 4);
+    o.qb_flags = take(B * nqb * (cap / 128) * 4);
     o.total_bytes = off;
     o.qblock = kQBlock;
     o.nqb = nqb;
@@ -596,6 +635,12 @@ void run_select(const skb_attn_desc& d, const double* u, void* ws, cudaStream_t 
         k_union_lists<<<g, 256, 0, st>>>(leave1, L, T, w, nqb, (int)lay.qb_cap, qb_count, qb_list);
         k_ever_list<<<B, 256, 0, st>>>(leave1, L, T, ever_count, ever_list);
         SKB_CHECK_LAUNCH();
+        k_union_meta<<<g, 128, 0, st>>>(leave1, reinterpret_cast<const float*>(base + lay.uf),
+                                        reinterpret_cast<const float*>(base + lay.tauf), L, T, w, nqb,
+                                        (int)lay.qb_cap, qb_count, qb_list, reinterpret_cast<int*>(base + lay.qb_leave),
+                                        reinterpret_cast<float*>(base + lay.qb_uf),
+                                        reinterpret_cast<int*>(base + lay.qb_flags));
+        SKB_CHECK_LAUNCH();
     } else {
         const int64_t n = (int64_t)B * nqb;
         k_fill_int<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(qb_count, n, 0);
@@ -618,6 +663,9 @@ SelView sel_view(const skb_attn_desc& d, const void* ws) {
     s.ever_list = reinterpret_cast<const int*>(base + lay.ever_list);
     s.uf = reinterpret_cast<const float*>(base + lay.uf);
     s.tauf = reinterpret_cast<const float*>(base + lay.tauf);
+    s.qb_leave = reinterpret_cast<const int*>(base + lay.qb_leave);
+    s.qb_uf = reinterpret_cast<const float*>(base + lay.qb_uf);
+    s.qb_flags = reinterpret_cast<const int*>(base + lay.qb_flags);
     s.nqb = (int)lay.nqb;
     s.qb_cap = (int)lay.qb_cap;
     return s;

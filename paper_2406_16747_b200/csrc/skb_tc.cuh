@@ -259,6 +259,43 @@ __device__ __forceinline__ void load_tile(uint32_t dst, const __nv_bfloat16* bas
     }
 }
 
+// Row keys of one R-row tile for this producer thread, fetched ahead of the
+// copies so a gathered key is never on a copy's critical path.
+template <int D, int R>
+struct RowKeys {
+    static constexpr int kChunks = D / 8;
+    static constexpr int kRowsPerIter = 32 / kChunks;
+    static constexpr int kGroups = R / kRowsPerIter;
+    static constexpr int kPW = kProducers / 32;
+    static constexpr int kIters = (kGroups + kPW - 1) / kPW;
+    int k[kIters];
+
+    template <class KeyFn>
+    __device__ __forceinline__ void fetch(int pw, int lane, KeyFn keyfn) {
+        const int sub = lane / kChunks;
+#pragma unroll
+        for (int it = 0; it < kIters; ++it) {
+            const int g = pw + kPW * it;
+            k[it] = g < kGroups ? keyfn(g * kRowsPerIter + sub) : -1;
+        }
+    }
+    // cp.async the rows (key < 0 or >= L: zero-filled) into the swizzled tile
+    __device__ __forceinline__ void issue(uint32_t dst, const __nv_bfloat16* base, int b, int h, int L, int H, int pw,
+                                          int lane) const {
+        const int sub = lane / kChunks, ch = lane % kChunks;
+#pragma unroll
+        for (int it = 0; it < kIters; ++it) {
+            const int g = pw + kPW * it;
+            if (g < kGroups) {
+                const int r = g * kRowsPerIter + sub;
+                const bool ok = k[it] >= 0 && k[it] < L;
+                const __nv_bfloat16* src = base + (((int64_t)b * L + (ok ? k[it] : 0)) * H + h) * D + ch * 8;
+                cp_async16(dst + sw_off(r, ch, R), src, ok);
+            }
+        }
+    }
+};
+
 __device__ __forceinline__ int warp_max_i(int v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));

@@ -58,7 +58,7 @@ def test_config_errors_map_to_reference_taxonomy():
         _lib.check(lib.skb_select_layout_of(bad2, lay))
     ok = make_desc(2, 300, 2, 8, AttnConfig(k=8.5, window=8), torch.float32)
     _lib.check(lib.skb_select_layout_of(ok, lay))
-    assert lay.qb_cap == 8 + 128 and lay.nqb == 3 and lay.total_bytes > 0
+    assert lay.qb_cap == 256 and lay.nqb == 3 and lay.total_bytes > 0  # floor(k)+128 rounded to 128
 
 
 def test_error_classes_follow_pybind_mapping():

@@ -102,6 +102,9 @@ CASES = [
     (90, 2, 32, 0.5, 6, "soft", "soft", "iid"),             # floor(k) = 0 with a stream
     (40, 1, 32, 8.0, 64, "hard", "soft", "iid"),            # L < w: no pushes
     (257, 2, 128, 32.0, 31, "hard", "soft", "recency"),
+    # many tiles per query block: K/V/metadata rings wrap several times
+    (2048, 2, 128, 300.0, 300, "hard", "soft", "recency"),
+    (1536, 1, 64, 420.5, 200, "soft", "soft", "iid"),
 ]
 
 
