@@ -99,9 +99,9 @@ typedef struct skb_select_layout {
     uint64_t scratch;     /* double scratch (overflow chunks) */
     uint64_t uf;          /* float  [B, L]  u as fp32 (tensor-core gates)    */
     uint64_t tauf;        /* float  [B, L]  tau as fp32 (push time)          */
-    uint64_t qb_leave;    /* int32  [B, NQB, qb_cap] leave of each union entry (0 = padding) */
+    uint64_t qb_leave;    /* int32  [B, NQB, qb_cap] leave - key of each union entry (0 = padding) */
     uint64_t qb_uf;       /* float  [B, NQB, qb_cap] u of each union entry     */
-    uint64_t qb_flags;    /* int32  [B, NQB, qb_cap/128] per 128-entry tile:
+    uint64_t qb_flags;    /* int32x4 [B, NQB, qb_cap/128] per 128-entry tile (.x used):
                              bit0 every key valid for every query of the block,
                              bit1 every gate saturated (u >= tau(t_hi) + 1)   */
     uint64_t total_bytes;

@@ -22,9 +22,28 @@
 #include "skb_common.cuh"
 #include "skb_internal.h"
 #include "skb_tc.cuh"
+#include "skb_tmap.h"
 
 #ifndef SKB_EXP
 #define SKB_EXP 0
+#endif
+
+#ifdef SKB_TRACE
+// Timeline probe (experiment builds only): clock64 stamps of one CTA's
+// pipeline events, read back with skb_debug_trace().
+__device__ unsigned long long g_skb_trace[4096];
+#define SKB_TR(role, jt, ev)                                                                         \
+    do {                                                                                              \
+        if (blockIdx.x == 100 && blockIdx.y == 0 && blockIdx.z == 0 && (jt) < 16)                  \
+            g_skb_trace[(role) * 256 + (jt) * 16 + (ev)] = clock64();                                \
+    } while (0)
+extern "C" int skb_debug_trace(unsigned long long* out, int n) {
+    return (int)cudaMemcpyFromSymbol(out, g_skb_trace, sizeof(unsigned long long) * (n < 4096 ? n : 4096));
+}
+#else
+#define SKB_TR(role, jt, ev) \
+    do {                     \
+    } while (0)
 #endif
 
 namespace skb {
@@ -37,6 +56,11 @@ constexpr float kLn2 = 0.6931471805599453f;
 constexpr float kRescaleSlack = 8.0f;  // lazy rescale threshold (log2 units)
 
 struct FwdArgs {
+    CUtensorMap tm_q;   // 3-D row tiles (box 64 x 128)
+    CUtensorMap tm_k;
+    CUtensorMap tm_v;
+    CUtensorMap tg_k;   // 2-D row gathers (box 64 x 1)
+    CUtensorMap tg_v;
     const __nv_bfloat16* q;
     const __nv_bfloat16* k;
     const __nv_bfloat16* v;
@@ -78,7 +102,7 @@ enum { B_QFULL = 0, B_KFULL = 1, B_KEMPTY = 4, B_MFULL = 7, B_MEMPTY = 10, B_VFU
        B_SFULL = 17, B_SEMPTY = 19, B_PFULL = 21, B_PVDONE = 25, B_ODONE = 27 };  // 28 barriers
 
 template <int D, bool KEY_SOFT>
-__global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
+__global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(const __grid_constant__ FwdArgs a) {
     using SM = FwdSmem<D>;
     extern __shared__ __align__(16) uint8_t smem_raw[];
     // keep the shared address space visible to the compiler (LDS/STS, not generic)
@@ -102,15 +126,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
     const int jw0 = i0 - a.w + 1;  // first key of the window band
 
     if (threadIdx.x == 0) {
-        mbar_init(&bars[B_QFULL], kProducers);
+        mbar_init(&bars[B_QFULL], 1);
         for (int s = 0; s < kKS; ++s) {
-            mbar_init(&bars[B_KFULL + s], kProducers);
+            mbar_init(&bars[B_KFULL + s], kProducers + 1);
             mbar_init(&bars[B_KEMPTY + s], 1);
             mbar_init(&bars[B_MFULL + s], kProducers);
             mbar_init(&bars[B_MEMPTY + s], kMath);
         }
         for (int s = 0; s < 2; ++s) {
-            mbar_init(&bars[B_VFULL + s], kProducers);
+            mbar_init(&bars[B_VFULL + s], kProducers + 1);
             mbar_init(&bars[B_VEMPTY + s], 1);
             mbar_init(&bars[B_SFULL + s], 1);
             mbar_init(&bars[B_SEMPTY + s], kMath);
@@ -130,25 +154,48 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
 
     if (warp >= kProdWarp0 && warp < kMmaWarp) {
         // ------------------------------------------------------------ producers
+        // Selected-union tiles: cp.async row gathers (keys fetched one tile
+        // ahead; TMA tile::gather4 moves only 512 B per op and measured slower).
+        // Q and the window band: 3-D TMA row tiles (OOB rows -> 0), issued by
+        // one thread. Every FULL barrier counts 96 thread arrivals + 1 (the TMA
+        // expect_tx on band tiles, a plain arrival on gathered ones).
+        constexpr int kAtoms = D / 64;
+        constexpr uint32_t kTileBytes = 128 * D * 2;
         const int pw = warp - kProdWarp0, ptid = threadIdx.x - kProdWarp0 * 32;
-        {
-            RowKeys<D, 128> qk;
-            qk.fetch(pw, lane, [&](int r) { return i0 + r < a.L ? i0 + r : -1; });
-            qk.issue(sbase + SM::kQ, a.q, b, h, a.L, a.H, pw, lane);
+        if (ptid == 0) {
+            mbar_expect_tx(&bars[B_QFULL], kTileBytes);
+#pragma unroll
+            for (int at = 0; at < kAtoms; ++at)
+                tma_load_3d(sbase + SM::kQ + at * 128 * 128, &a.tm_q, h * D + at * 64, i0, b, &bars[B_QFULL]);
         }
-        cp_async_arrive_noinc(&bars[B_QFULL]);
         const int* list = a.qb_list + qrow * a.qb_cap;
-        auto keyfn = [&](int jt, int r) {
-            if (jt < n_sel) return __ldg(list + jt * 128 + r);  // padded with -1
-            return jw0 + (jt - n_sel) * 128 + r;
-        };
         RowKeys<D, 128> kcur, kprev;
-        kcur.fetch(pw, lane, [&](int r) { return keyfn(0, r); });
+        if (n_sel > 0) kcur.fetch(pw, lane, [&](int r) { return __ldg(list + r); }, b, h, a.L, a.H);
         const int ma = ptid >> 5, mc = ptid & 31;  // metadata: array, 16-byte chunk
         const int* msrc = ma == 0 ? a.qb_list : ma == 1 ? a.qb_leave : reinterpret_cast<const int*>(a.qb_uf);
+        auto load_rows = [&](int jt, uint32_t dst, const RowKeys<D, 128>& keys, const __nv_bfloat16* src,
+                             const CUtensorMap* tm3, uint64_t* bar) {
+            if (SKB_EXP == 5) {  // experiment: no loads at all
+                mbar_arrive(bar);
+                if (ptid == 0) mbar_arrive(bar);
+            } else if (jt < n_sel) {
+                keys.issue(dst, src, pw, lane);
+                cp_async_arrive_noinc(bar);
+                if (ptid == 0) mbar_arrive(bar);
+            } else {
+                if (ptid == 0) {
+                    mbar_expect_tx(bar, kTileBytes);
+#pragma unroll
+                    for (int at = 0; at < kAtoms; ++at)
+                        tma_load_3d(dst + at * 128 * 128, tm3, h * D + at * 64, jw0 + (jt - n_sel) * 128, b, bar);
+                }
+                mbar_arrive(bar);
+            }
+        };
         // K + metadata run one tile ahead of V so a softmax never waits for a V gather
         for (int jt = 0; jt <= n; ++jt) {
             RowKeys<D, 128> knext;
+            if (ptid == 0) SKB_TR(2, jt, 0);
             if (jt < n) {
                 const int ks = jt % kKS;
                 if (jt >= kKS) mbar_wait(&bars[B_MEMPTY + ks], ((jt - kKS) / kKS) & 1);
@@ -156,19 +203,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
                     cp_async16(smem_u32(meta + (ks * 3 + ma) * 128 + mc * 4),
                                msrc + qrow * a.qb_cap + jt * 128 + mc * 4, true);
                     if (ptid == 0)
-                        cp_async4(smem_u32(tflags + ks * 4), a.qb_flags + qrow * (a.qb_cap / 128) + jt, true);
+                        cp_async16(smem_u32(tflags + ks * 4), a.qb_flags + (qrow * (a.qb_cap / 128) + jt) * 4, true);
                 }
                 cp_async_arrive_noinc(&bars[B_MFULL + ks]);
                 if (jt >= kKS) mbar_wait(&bars[B_KEMPTY + ks], ((jt - kKS) / kKS) & 1);
-                kcur.issue(sbase + SM::kK + ks * SM::kTile, a.k, b, h, a.L, a.H, pw, lane);
-                cp_async_arrive_noinc(&bars[B_KFULL + ks]);
-                if (jt + 1 < n) knext.fetch(pw, lane, [&](int r) { return keyfn(jt + 1, r); });
+                if (ptid == 0) SKB_TR(2, jt, 1);
+                load_rows(jt, sbase + SM::kK + ks * SM::kTile, kcur, a.k, &a.tm_k, &bars[B_KFULL + ks]);
+                if (ptid == 0) SKB_TR(2, jt, 2);
+                if (jt + 1 < n_sel)
+                    knext.fetch(pw, lane, [&](int r) { return __ldg(list + (jt + 1) * 128 + r); }, b, h, a.L, a.H);
             }
             if (jt >= 1) {
                 const int j = jt - 1, vs = j & 1;
                 if (j >= 2) mbar_wait(&bars[B_VEMPTY + vs], ((j - 2) >> 1) & 1);
-                kprev.issue(sbase + SM::kV + vs * SM::kTile, a.v, b, h, a.L, a.H, pw, lane);
-                cp_async_arrive_noinc(&bars[B_VFULL + vs]);
+                if (ptid == 0) SKB_TR(2, j, 3);
+                load_rows(j, sbase + SM::kV + vs * SM::kTile, kprev, a.v, &a.tm_v, &bars[B_VFULL + vs]);
+                if (ptid == 0) SKB_TR(2, j, 4);
             }
             kprev = kcur;
             kcur = knext;
@@ -187,11 +237,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
 #pragma unroll
                 for (int hf = 0; hf < 2; ++hf) {
                     mbar_wait(&bars[B_PFULL + 2 * (j & 1) + hf], (j >> 1) & 1);
+                    SKB_TR(3, j, 2 + hf);
                     tc_after_sync();
                     // P~ of this half: 64 keys packed over the first 32 of its own S columns
                     const uint32_t pa = tS + (j & 1) * 128 + hf * 64;
 #pragma unroll
-                    for (int kk = 0; kk < 4; ++kk)
+                    for (int kk = 0; kk < (SKB_EXP == 4 ? 0 : 4); ++kk)
                         umma_f16_ts(tO + hf * 128, pa + kk * 8, desc_mnmajor(vb, 128, hf * 4 + kk), idesc_pv,
                                     (j > 0 || kk > 0) ? 1u : 0u);
                     umma_commit(&bars[B_PVDONE + hf]);
@@ -201,16 +252,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
             for (int jt = 0; jt < n; ++jt) {
                 const int s = jt & 1;
                 const int ks = jt % kKS;
+                SKB_TR(3, jt, 8);
                 mbar_wait(&bars[B_KFULL + ks], (jt / kKS) & 1);
+                SKB_TR(3, jt, 0);
                 fence_proxy_async();
                 if (jt >= 2) mbar_wait(&bars[B_SEMPTY + s], ((jt - 2) >> 1) & 1);
                 tc_after_sync();
                 const uint32_t kb = sbase + SM::kK + ks * SM::kTile;
 #pragma unroll
-                for (int kk = 0; kk < D / 16; ++kk)
+                for (int kk = 0; kk < (SKB_EXP == 4 ? 0 : D / 16); ++kk)
                     umma_f16(tS + s * 128, desc_kmajor(sbase + SM::kQ, 128, kk), desc_kmajor(kb, 128, kk),
                              idesc_qk, kk > 0 ? 1u : 0u);
                 umma_commit(&bars[B_SFULL + s]);
+                SKB_TR(3, jt, 1);
                 umma_commit(&bars[B_KEMPTY + ks]);
                 if (jt >= 1) pv(jt - 1);
             }
@@ -218,7 +272,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
             umma_commit(&bars[B_ODONE]);  // every MMA of the CTA complete
         }
         __syncwarp();
-    } else {
+    } else if (warp < kProdWarp0) {
         // ------------------------------------------------------------ math (warps 0-7)
         const int hf = warp >> 2;                // key half: 0 -> tile cols 0..63, 1 -> 64..127
         const int r = ((warp & 3) << 5) | lane;  // tile row = TMEM lane
@@ -236,20 +290,31 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
             const int s = jt & 1;
             const bool is_sel = jt < n_sel;
             const int ks = jt % kKS;
+            if (lane == 0) SKB_TR(hf, jt, 9);
             mbar_wait(&bars[B_SFULL + s], (jt >> 1) & 1);
+            if (lane == 0) SKB_TR(hf, jt, 0);
             if (is_sel) mbar_wait(&bars[B_MFULL + ks], (jt / kKS) & 1);
             tc_after_sync();
             tmem_ld32(tS + lane_off + s * 128 + c0, sv);
             tmem_ld32(tS + lane_off + s * 128 + c0 + 32, sv + 32);
             tmem_wait_ld();
+            if (lane == 0 && (warp & 3) == 0) SKB_TR(hf, jt, 1);
             tc_before_sync();
             mbar_arrive(&bars[B_SEMPTY + s]);
 
+#if SKB_EXP == 1 || SKB_EXP == 4
+            if (true) {  // experiment: no softmax work (pipeline without the math)
+                tc_before_sync();
+                mbar_arrive(&bars[B_MEMPTY + ks]);
+                mbar_arrive(&bars[B_PFULL + 2 * s + hf]);
+                continue;
+            }
+#endif
             const int* mk = meta + (ks * 3) * 128 + c0;
             const int* ml = mk + 128;
             const float* mu = reinterpret_cast<const float*>(mk + 256);
             int fl = 3;
-            if (is_sel) {
+            if (is_sel && SKB_EXP != 3) {
                 fl = tflags[ks * 4];
                 if (KEY_SOFT) {  // gated logits (proj/src/cache.cpp:368-369)
 #pragma unroll
@@ -261,15 +326,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
                         sv[c + 3] *= __saturatef(uu.w - tau_i);
                     }
                 }
-                if (!(fl & 1)) {  // per-key interval mask j <= t < leave_j (padding: key -1)
+                if (!(fl & 1)) {  // per-key interval mask j <= t < leave_j: (unsigned)(t - j) < leave_j - j
 #pragma unroll
                     for (int c = 0; c < 64; c += 4) {
                         const int4 kj = *reinterpret_cast<const int4*>(mk + c);
-                        const int4 lv = *reinterpret_cast<const int4*>(ml + c);
-                        sv[c + 0] = (kj.x >= 0 && kj.x <= t && lv.x > t) ? sv[c + 0] : -INFINITY;
-                        sv[c + 1] = (kj.y >= 0 && kj.y <= t && lv.y > t) ? sv[c + 1] : -INFINITY;
-                        sv[c + 2] = (kj.z >= 0 && kj.z <= t && lv.z > t) ? sv[c + 2] : -INFINITY;
-                        sv[c + 3] = (kj.w >= 0 && kj.w <= t && lv.w > t) ? sv[c + 3] : -INFINITY;
+                        const int4 ex = *reinterpret_cast<const int4*>(ml + c);
+                        sv[c + 0] = ((unsigned)(t - kj.x) < (unsigned)ex.x) ? sv[c + 0] : -INFINITY;
+                        sv[c + 1] = ((unsigned)(t - kj.y) < (unsigned)ex.y) ? sv[c + 1] : -INFINITY;
+                        sv[c + 2] = ((unsigned)(t - kj.z) < (unsigned)ex.z) ? sv[c + 2] : -INFINITY;
+                        sv[c + 3] = ((unsigned)(t - kj.w) < (unsigned)ex.w) ? sv[c + 3] : -INFINITY;
                     }
                 }
             } else {
@@ -277,14 +342,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
                 const int kb = jw0 + (jt - n_sel) * 128 + c0;
                 const int cmin = lo_win - kb;
                 const int cmax = i - kb;
-                if (__any_sync(0xffffffffu, cmin > 0 || cmax < 63)) {
+                if (SKB_EXP != 3 && __any_sync(0xffffffffu, cmin > 0 || cmax < 63)) {
 #pragma unroll
                     for (int c = 0; c < 64; ++c) sv[c] = (c >= cmin && c <= cmax) ? sv[c] : -INFINITY;
                 }
             }
-            float mr = sv[0];
+            float mx[8];  // 8 independent chains: the row max is not a 64-deep dependency
 #pragma unroll
-            for (int c = 1; c < 64; ++c) mr = fmaxf(mr, sv[c]);
+            for (int e = 0; e < 8; ++e) mx[e] = fmaxf(sv[e], sv[8 + e]);
+#pragma unroll
+            for (int c = 16; c < 64; c += 8)
+#pragma unroll
+                for (int e = 0; e < 8; ++e) mx[e] = fmaxf(mx[e], sv[c + e]);
+            const float mr = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                                   fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+            if (lane == 0 && (warp & 3) == 0) SKB_TR(hf, jt, 2);
             const float mt = mr * sl2;  // scale > 0: max commutes with scaling
             float fac = 1.f;
             bool need = false;
@@ -297,17 +369,24 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
                 m = mt;
             }
             const float nmb = m == -INFINITY ? 0.f : -m;  // fully masked so far: avoid -inf - -inf
-            float ps0 = 0.f, ps1 = 0.f;
+            // packed fp32x2 arithmetic: one FFMA2 / FADD2 per two keys
+            const float2 sl22 = make_float2(sl2, sl2), nmb2 = make_float2(nmb, nmb);
+            float2 ps[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                            make_float2(0.f, 0.f)};
 #pragma unroll
-            for (int c = 0; c < 64; c += 2) {
-                const float p0 = ex2(fmaf(sv[c], sl2, nmb));  // masked: exp2(-inf) = 0
-                const float p1 = ex2(fmaf(sv[c + 1], sl2, nmb));
-                ps0 += p0;
-                ps1 += p1;
-                sv[c] = p0;
-                sv[c + 1] = p1;
-            }
-            l += ps0 + ps1;
+            for (int c = 0; c < 64; c += 8)
+#pragma unroll
+                for (int e = 0; e < 8; e += 2) {
+                    float2 x = __ffma2_rn(make_float2(sv[c + e], sv[c + e + 1]), sl22, nmb2);
+                    x.x = ex2(x.x);  // masked: exp2(-inf) = 0
+                    x.y = ex2(x.y);
+                    ps[e >> 1] = __fadd2_rn(ps[e >> 1], x);
+                    sv[c + e] = x.x;
+                    sv[c + e + 1] = x.y;
+                }
+            const float2 pq = __fadd2_rn(__fadd2_rn(ps[0], ps[1]), __fadd2_rn(ps[2], ps[3]));
+            l += pq.x + pq.y;
+            if (lane == 0 && (warp & 3) == 0) SKB_TR(hf, jt, 3);
             if (is_sel && !a.mask_st && !(fl & 2)) {  // value gates (cache.cpp:381-382)
 #pragma unroll
                 for (int c = 0; c < 64; c += 4) {
@@ -347,6 +426,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(FwdArgs a) {
                 tmem_wait_st();
             }
             tc_before_sync();
+            if (lane == 0 && (warp & 3) == 0) SKB_TR(hf, jt, 4);
             mbar_arrive(&bars[B_MEMPTY + ks]);  // every tile (the producer waits on each stage)
             mbar_arrive(&bars[B_PFULL + 2 * s + hf]);
         }
@@ -418,6 +498,14 @@ void run_attn_fwd_tc(const skb_attn_desc& d, const void* q, const void* k, const
     (void)u;
     (void)ws;
     FwdArgs a{};
+    {
+        const int64_t HD = d.heads * d.head_dim;
+        a.tm_q = tmap_rows3d(q, d.batch, d.seq_len, HD, 128);
+        a.tm_k = tmap_rows3d(k, d.batch, d.seq_len, HD, 128);
+        a.tm_v = tmap_rows3d(v, d.batch, d.seq_len, HD, 128);
+        a.tg_k = tmap_gather2d(k, d.batch * d.seq_len, HD);
+        a.tg_v = tmap_gather2d(v, d.batch * d.seq_len, HD);
+    }
     a.q = static_cast<const __nv_bfloat16*>(q);
     a.k = static_cast<const __nv_bfloat16*>(k);
     a.v = static_cast<const __nv_bfloat16*>(v);

@@ -24,9 +24,9 @@ struct SelView {
     const int* ever_list;
     const float* uf;    // u as fp32 [B, L]
     const float* tauf;  // tau as fp32 [B, L] (push time)
-    const int* qb_leave;    // [B, NQB, qb_cap] leave of each union entry
+    const int* qb_leave;    // [B, NQB, qb_cap] leave - key of each union entry (0 = padding)
     const float* qb_uf;     // [B, NQB, qb_cap] u of each union entry
-    const int* qb_flags;    // [B, NQB, qb_cap / 128]
+    const int* qb_flags;    // [B, NQB, qb_cap / 128] x 4 ints (16-byte records, .x = flags)
     int nqb, qb_cap;
 };
 SelView sel_view(const skb_attn_desc& d, const void* ws);

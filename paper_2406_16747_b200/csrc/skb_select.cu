@@ -433,13 +433,15 @@ k_union_meta(const int* __restrict__ leave1, const float* __restrict__ uf, const
         } else {
             qb_list[row * cap + idx] = -1;
         }
-        qb_leave[row * cap + idx] = lv;
+        // the forward's interval mask in one unsigned compare:
+        // valid(t) <=> (unsigned)(t - key) < (unsigned)(leave - key); padding: 0
+        qb_leave[row * cap + idx] = key >= 0 ? lv - key : 0;
         qb_uf[row * cap + idx] = u;
         const bool ok = key >= 0 && key <= t_lo && lv > t_hi;
         const bool sat = key < 0 || u >= tau_hi + 1.f;
         const int all_ok = __syncthreads_and(ok);
         const int all_sat = __syncthreads_and(sat);
-        if (threadIdx.x == 0) qb_flags[row * (cap / 128) + t] = (all_ok ? 1 : 0) | (all_sat ? 2 : 0);
+        if (threadIdx.x == 0) qb_flags[(row * (cap / 128) + t) * 4] = (all_ok ? 1 : 0) | (all_sat ? 2 : 0);
     }
 }
 
@@ -536,7 +538,7 @@ void select_layout(const skb_attn_desc& d, skb_select_layout& o) {
     o.tauf = take(B * L * 4);
     o.qb_leave = take(B * nqb * cap * 4);
     o.qb_uf = take(B * nqb * cap * 4);
-    o.qb_flags = take(B * nqb * (cap / 128) * 4);
+    o.qb_flags = take(B * nqb * (cap / 128) * 16);  // one 16-byte record per tile (bulk-copyable)
     o.total_bytes = off;
     o.qblock = kQBlock;
     o.nqb = nqb;

@@ -11,6 +11,7 @@
 // columns = M/N).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
 
@@ -31,10 +32,15 @@ __device__ __forceinline__ void mbar_fence_init() {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-// try_wait with a suspend-time hint: a waiting warp sleeps in hardware instead
-// of spinning through issue slots the math warps need.
+// Barrier waits. SKB_WAIT_MODE selects the polling primitive (experiment
+// hook): 0 try_wait with a suspend-time hint, 1 plain try_wait (the hardware
+// picks the suspend window), 2 test_wait with an explicit nanosleep backoff.
+#ifndef SKB_WAIT_MODE
+#define SKB_WAIT_MODE 1
+#endif
 __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
     uint32_t ok;
+#if SKB_WAIT_MODE == 0
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
@@ -42,6 +48,24 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
         : "=r"(ok)
         : "r"(addr), "r"(parity), "r"(1000000u)
         : "memory");
+#elif SKB_WAIT_MODE == 1
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity)
+        : "memory");
+#else
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity)
+        : "memory");
+    if (!ok) __nanosleep(64);
+#endif
     return ok != 0;
 }
 // Wait for the phase with the given parity to complete. A wait that never
@@ -50,12 +74,43 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     const uint32_t addr = smem_u32(bar);
     uint32_t spins = 0;
     while (!mbar_try_wait(addr, parity)) {
-        if (++spins > (1u << 24)) __trap();
+        if (++spins > (1u << 26)) __trap();
     }
 }
 // cp.async completion of this thread's prior copies arrives on the barrier.
 __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// ------------------------------------------------------------------ TMA
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+// 3-D tiled box load {c0 = column, c1 = row, c2 = sequence} (OOB -> zeros)
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cta.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+            dst),
+        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+// four gathered rows of one 64-column box (2-D map, box {64, 1}); lands as
+// four consecutive 128-byte rows, swizzled by their shared-memory address
+__device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap* map, int col, int r0, int r1, int r2,
+                                            int r3, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
+        "l"(map), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
+        : "memory");
+}
+// plain bulk copy global -> shared (bytes % 16 == 0, both 16-byte aligned)
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
 }
 
 // ------------------------------------------------------------------ cp.async
@@ -270,27 +325,34 @@ struct RowKeys {
     static constexpr int kIters = (kGroups + kPW - 1) / kPW;
     int k[kIters];
 
+    // k[it] holds the source row index (b*L + key)*H + h, or -1 (zero fill)
     template <class KeyFn>
-    __device__ __forceinline__ void fetch(int pw, int lane, KeyFn keyfn) {
+    __device__ __forceinline__ void fetch(int pw, int lane, KeyFn keyfn, int b, int h, int L, int H) {
         const int sub = lane / kChunks;
 #pragma unroll
         for (int it = 0; it < kIters; ++it) {
             const int g = pw + kPW * it;
-            k[it] = g < kGroups ? keyfn(g * kRowsPerIter + sub) : -1;
+            const int key = g < kGroups ? keyfn(g * kRowsPerIter + sub) : -1;
+            k[it] = (key >= 0 && key < L) ? (b * L + key) * H + h : -1;
         }
     }
-    // cp.async the rows (key < 0 or >= L: zero-filled) into the swizzled tile
-    __device__ __forceinline__ void issue(uint32_t dst, const __nv_bfloat16* base, int b, int h, int L, int H, int pw,
-                                          int lane) const {
+    // cp.async the rows into the 128B-swizzled tile
+    __device__ __forceinline__ void issue(uint32_t dst, const __nv_bfloat16* base, int pw, int lane) const {
         const int sub = lane / kChunks, ch = lane % kChunks;
+        const __nv_bfloat16* basec = base + ch * 8;
+        const uint32_t dcol = (uint32_t)((ch >> 3) * (R * 128));
 #pragma unroll
         for (int it = 0; it < kIters; ++it) {
             const int g = pw + kPW * it;
             if (g < kGroups) {
                 const int r = g * kRowsPerIter + sub;
-                const bool ok = k[it] >= 0 && k[it] < L;
-                const __nv_bfloat16* src = base + (((int64_t)b * L + (ok ? k[it] : 0)) * H + h) * D + ch * 8;
-                cp_async16(dst + sw_off(r, ch, R), src, ok);
+#if defined(SKB_EXP) && SKB_EXP == 2
+                const bool ok = false;  // experiment: no gathers (zero fill)
+#else
+                const bool ok = k[it] >= 0;
+#endif
+                cp_async16(dst + dcol + r * 128 + (((ch & 7) ^ (r & 7)) << 4),
+                           basec + (int64_t)(ok ? k[it] : 0) * D, ok);
             }
         }
     }
