@@ -54,6 +54,10 @@ using namespace tc;
 
 constexpr float kLn2 = 0.6931471805599453f;
 constexpr float kRescaleSlack = 8.0f;  // lazy rescale threshold (log2 units)
+#ifndef SKB_POLY_PAIR
+#define SKB_POLY_PAIR -1
+#endif
+constexpr int kPolyPair = SKB_POLY_PAIR;  // which key pair of every 8 uses the polynomial exp2 (-1: none)
 
 struct FwdArgs {
     CUtensorMap tm_q;   // 3-D row tiles (box 64 x 128)
@@ -170,16 +174,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(const __grid_constant__ 
         }
         const int* list = a.qb_list + qrow * a.qb_cap;
         RowKeys<D, 128> kcur, kprev;
-        if (n_sel > 0) kcur.fetch(pw, lane, [&](int r) { return __ldg(list + r); }, b, h, a.L, a.H);
+        if (n_sel > 0) kcur.fetch(pw, lane, [&](int r) { return __ldg(list + r); });
         const int ma = ptid >> 5, mc = ptid & 31;  // metadata: array, 16-byte chunk
         const int* msrc = ma == 0 ? a.qb_list : ma == 1 ? a.qb_leave : reinterpret_cast<const int*>(a.qb_uf);
         auto load_rows = [&](int jt, uint32_t dst, const RowKeys<D, 128>& keys, const __nv_bfloat16* src,
                              const CUtensorMap* tm3, uint64_t* bar) {
-            if (SKB_EXP == 5) {  // experiment: no loads at all
+            if (SKB_EXP == 5 || SKB_EXP == 7 || SKB_EXP == 8) {  // experiment: no loads at all
                 mbar_arrive(bar);
                 if (ptid == 0) mbar_arrive(bar);
             } else if (jt < n_sel) {
-                keys.issue(dst, src, pw, lane);
+                keys.issue(dst, src, b, h, a.L, a.H, pw, lane);
                 cp_async_arrive_noinc(bar);
                 if (ptid == 0) mbar_arrive(bar);
             } else {
@@ -210,8 +214,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(const __grid_constant__ 
                 if (ptid == 0) SKB_TR(2, jt, 1);
                 load_rows(jt, sbase + SM::kK + ks * SM::kTile, kcur, a.k, &a.tm_k, &bars[B_KFULL + ks]);
                 if (ptid == 0) SKB_TR(2, jt, 2);
-                if (jt + 1 < n_sel)
-                    knext.fetch(pw, lane, [&](int r) { return __ldg(list + (jt + 1) * 128 + r); }, b, h, a.L, a.H);
+                if (jt + 1 < n_sel) knext.fetch(pw, lane, [&](int r) { return __ldg(list + (jt + 1) * 128 + r); });
             }
             if (jt >= 1) {
                 const int j = jt - 1, vs = j & 1;
@@ -242,7 +245,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(const __grid_constant__ 
                     // P~ of this half: 64 keys packed over the first 32 of its own S columns
                     const uint32_t pa = tS + (j & 1) * 128 + hf * 64;
 #pragma unroll
-                    for (int kk = 0; kk < (SKB_EXP == 4 ? 0 : 4); ++kk)
+                    for (int kk = 0; kk < ((SKB_EXP == 4 || SKB_EXP == 7) ? 0 : 4); ++kk)
                         umma_f16_ts(tO + hf * 128, pa + kk * 8, desc_mnmajor(vb, 128, hf * 4 + kk), idesc_pv,
                                     (j > 0 || kk > 0) ? 1u : 0u);
                     umma_commit(&bars[B_PVDONE + hf]);
@@ -260,7 +263,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(const __grid_constant__ 
                 tc_after_sync();
                 const uint32_t kb = sbase + SM::kK + ks * SM::kTile;
 #pragma unroll
-                for (int kk = 0; kk < (SKB_EXP == 4 ? 0 : D / 16); ++kk)
+                for (int kk = 0; kk < ((SKB_EXP == 4 || SKB_EXP == 7) ? 0 : D / 16); ++kk)
                     umma_f16(tS + s * 128, desc_kmajor(sbase + SM::kQ, 128, kk), desc_kmajor(kb, 128, kk),
                              idesc_qk, kk > 0 ? 1u : 0u);
                 umma_commit(&bars[B_SFULL + s]);
@@ -302,7 +305,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(const __grid_constant__ 
             tc_before_sync();
             mbar_arrive(&bars[B_SEMPTY + s]);
 
-#if SKB_EXP == 1 || SKB_EXP == 4
+#if SKB_EXP == 1 || SKB_EXP == 4 || SKB_EXP == 8
             if (true) {  // experiment: no softmax work (pipeline without the math)
                 tc_before_sync();
                 mbar_arrive(&bars[B_MEMPTY + ks]);
@@ -378,8 +381,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(const __grid_constant__ 
 #pragma unroll
                 for (int e = 0; e < 8; e += 2) {
                     float2 x = __ffma2_rn(make_float2(sv[c + e], sv[c + e + 1]), sl22, nmb2);
-                    x.x = ex2(x.x);  // masked: exp2(-inf) = 0
-                    x.y = ex2(x.y);
+                    if (SKB_EXP == 6) {  // experiment: no exponentials at all
+                    } else if (e == kPolyPair) {  // 1 pair in 4 on the FMA pipe, the rest on MUFU
+                        x = ex2_poly2(x);
+                    } else {
+                        x.x = ex2(x.x);  // masked: exp2(-inf) = 0
+                        x.y = ex2(x.y);
+                    }
                     ps[e >> 1] = __fadd2_rn(ps[e >> 1], x);
                     sv[c + e] = x.x;
                     sv[c + e + 1] = x.y;

@@ -258,6 +258,24 @@ __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t
     asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d)
                  : "memory");
 }
+// exp2 of two values on the FMA/ALU pipes (the MUFU unit is the softmax
+// bottleneck: 16 ex2/clk/SM): Cody-Waite split x = n + f with the 1.5*2^23
+// rounding trick, 2^f by a degree-3 minimax polynomial on [-1/2, 1/2]
+// (max relative error 7.5e-5, far below the bf16 P~ it feeds), 2^n added
+// into the exponent bits. Inputs below -126 (masked: -inf) give ~1e-38.
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+    x.x = fmaxf(x.x, -126.f);  // n >= -126 keeps the exponent field non-negative
+    x.y = fmaxf(x.y, -126.f);
+    const float2 magic = make_float2(12582912.f, 12582912.f);
+    const float2 t = __fadd2_rn(x, magic);
+    const float2 j = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));
+    const float2 f = __fadd2_rn(x, make_float2(-j.x, -j.y));
+    float2 p = __ffma2_rn(make_float2(0.05517098f, 0.05517098f), f, make_float2(0.2426097f, 0.2426097f));
+    p = __ffma2_rn(p, f, make_float2(0.69326097f, 0.69326097f));
+    p = __ffma2_rn(p, f, make_float2(0.99992816f, 0.99992816f));
+    return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                       __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
+}
 __device__ __forceinline__ float ex2(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -325,21 +343,22 @@ struct RowKeys {
     static constexpr int kIters = (kGroups + kPW - 1) / kPW;
     int k[kIters];
 
-    // k[it] holds the source row index (b*L + key)*H + h, or -1 (zero fill)
+    // k[it] holds the raw key (no arithmetic on it here, so a prefetch never
+    // waits for its loads); issue() turns it into the row index
     template <class KeyFn>
-    __device__ __forceinline__ void fetch(int pw, int lane, KeyFn keyfn, int b, int h, int L, int H) {
+    __device__ __forceinline__ void fetch(int pw, int lane, KeyFn keyfn) {
         const int sub = lane / kChunks;
 #pragma unroll
         for (int it = 0; it < kIters; ++it) {
             const int g = pw + kPW * it;
-            const int key = g < kGroups ? keyfn(g * kRowsPerIter + sub) : -1;
-            k[it] = (key >= 0 && key < L) ? (b * L + key) * H + h : -1;
+            k[it] = g < kGroups ? keyfn(g * kRowsPerIter + sub) : -1;
         }
     }
-    // cp.async the rows into the 128B-swizzled tile
-    __device__ __forceinline__ void issue(uint32_t dst, const __nv_bfloat16* base, int pw, int lane) const {
+    // cp.async the rows (key < 0 or >= L: zero fill) into the 128B-swizzled tile
+    __device__ __forceinline__ void issue(uint32_t dst, const __nv_bfloat16* base, int b, int h, int L, int H, int pw,
+                                          int lane) const {
         const int sub = lane / kChunks, ch = lane % kChunks;
-        const __nv_bfloat16* basec = base + ch * 8;
+        const __nv_bfloat16* basec = base + ((int64_t)b * L * H + h) * D + ch * 8;
         const uint32_t dcol = (uint32_t)((ch >> 3) * (R * 128));
 #pragma unroll
         for (int it = 0; it < kIters; ++it) {
@@ -349,10 +368,10 @@ struct RowKeys {
 #if defined(SKB_EXP) && SKB_EXP == 2
                 const bool ok = false;  // experiment: no gathers (zero fill)
 #else
-                const bool ok = k[it] >= 0;
+                const bool ok = (unsigned)k[it] < (unsigned)L;
 #endif
                 cp_async16(dst + dcol + r * 128 + (((ch & 7) ^ (r & 7)) << 4),
-                           basec + (int64_t)(ok ? k[it] : 0) * D, ok);
+                           basec + (int64_t)(ok ? k[it] : 0) * (H * D), ok);
             }
         }
     }
