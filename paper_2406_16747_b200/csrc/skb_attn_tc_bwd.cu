@@ -19,6 +19,7 @@
 #include "skb_common.cuh"
 #include "skb_internal.h"
 #include "skb_tc.cuh"
+#include "skb_tmap.h"
 
 namespace skb {
 
@@ -27,6 +28,10 @@ namespace {
 using namespace tc;
 
 struct BwdArgs {
+    CUtensorMap tm_q128, tm_do128;  // 3-D row tiles (box 64 x rows)
+    CUtensorMap tm_k64, tm_v64;
+    CUtensorMap tm_q64, tm_do64;
+    CUtensorMap tm_k128, tm_v128;
     const __nv_bfloat16 *q, *k, *v, *dout;
     __nv_bfloat16 *dq, *dk, *dv;
     float *dk_acc, *dv_acc;  // fp32 partials of the selected pass, [B, L, H, D]
@@ -37,6 +42,9 @@ struct BwdArgs {
     const int* leave;
     const int* qb_count;
     const int* qb_list;
+    const int* qb_leave;  // leave - key per union entry (0 = padding)
+    const float* qb_uf;
+    const int* qb_flags;  // 16-byte record per 128-entry tile
     const int* ever_count;
     const int* ever_list;
     double *rowsum, *colsum;
@@ -73,30 +81,37 @@ __global__ void k_bwd_prep(const __nv_bfloat16* __restrict__ o, const __nv_bfloa
 }
 
 // ------------------------------------------------------------------ dK / dV
+// Key-major: a CTA owns 128 keys (a contiguous window tile, or 128 entries of
+// the ever-selected list) and walks the 64-query tiles that read them. Per
+// tile: S^T = K Q^T and dP^T = V dO^T (M=128, N=64) in TMEM; two math
+// warpgroups (32 queries each) write P~^T and dS^T back into TMEM as bf16
+// over their consumed columns — the A operands of the TS-MMAs dV += P~^T dO
+// and dK += dS^T Q. Q/dO tiles arrive by 3-D TMA (contiguous queries), the
+// per-query lse/delta/tau by cp.async; a stage is released by the MMA commit.
+constexpr int kQS = 3;  // Q/dO ring depth
+
 template <int D>
 struct KSmem {
     static constexpr int kKV = 128 * D * 2;  // 128-key tile
     static constexpr int kQT = 64 * D * 2;   // 64-query tile
-    static constexpr int kPD = 128 * 64 * 2; // 128 x 64 bf16 (P~^T or dS^T)
     static constexpr int kK = 0;
     static constexpr int kV = kK + kKV;
-    static constexpr int kQ = kV + kKV;       // [2]
-    static constexpr int kDO = kQ + 2 * kQT;  // [2]
-    static constexpr int kPT = kDO + 2 * kQT; // [2]
-    static constexpr int kDS = kPT + 2 * kPD; // [2]
-    static constexpr int kMeta = kDS + 2 * kPD;  // [2][3][64] f32
-    static constexpr int kBar = kMeta + 2 * 3 * 64 * 4;
-    static constexpr int kTmemSlot = kBar + 16 * 8;
+    static constexpr int kQ = kV + kKV;          // [kQS]
+    static constexpr int kDO = kQ + kQS * kQT;   // [kQS]
+    static constexpr int kMeta = kDO + kQS * kQT;  // [kQS][lse2|delta|tau][64] f32
+    static constexpr int kBar = kMeta + kQS * 3 * 64 * 4;
+    static constexpr int kNumBars = 16;
+    static constexpr int kTmemSlot = kBar + kNumBars * 8;
     static constexpr int kAlloc = kTmemSlot + 16 + 1024;
 };
-enum { KB_KVFULL = 0, KB_QDFULL = 1, KB_QDEMPTY = 3, KB_SFULL = 5, KB_SEMPTY = 7, KB_PDSFULL = 9,
-       KB_PDSEMPTY = 10, KB_ACCDONE = 12 };
+enum { KB_KVFULL = 0, KB_QDFULL = 1, KB_QDEMPTY = 4, KB_SFULL = 7, KB_SEMPTY = 9, KB_PDSFULL = 11,
+       KB_ACCDONE = 13 };  // 14 barriers
 
 template <int D, bool SEL, bool KEY_SOFT>
-__global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_tc(BwdArgs a) {
+__global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_tc(const __grid_constant__ BwdArgs a) {
     using SM = KSmem<D>;
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const uint32_t sbase = smem_u32(smem);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SM::kBar);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + SM::kTmemSlot);
@@ -134,15 +149,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_tc(BwdArgs a) {
         if (lane == 0) atomicMax(&s_range[1], hi);
     }
     if (threadIdx.x == 0) {
-        mbar_init(&bars[KB_KVFULL], kProducers);
-        for (int s = 0; s < 2; ++s) {
-            mbar_init(&bars[KB_QDFULL + s], kProducers);
+        mbar_init(&bars[KB_KVFULL], kProducers + 1);
+        for (int s = 0; s < kQS; ++s) {
+            mbar_init(&bars[KB_QDFULL + s], kProducers + 1);
             mbar_init(&bars[KB_QDEMPTY + s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
             mbar_init(&bars[KB_SFULL + s], 1);
             mbar_init(&bars[KB_SEMPTY + s], kMath);
-            mbar_init(&bars[KB_PDSEMPTY + s], 1);
+            mbar_init(&bars[KB_PDSFULL + s], kMath);
         }
-        mbar_init(&bars[KB_PDSFULL], kMath);
         mbar_init(&bars[KB_ACCDONE], 1);
         mbar_fence_init();
     }
@@ -157,19 +173,32 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_tc(BwdArgs a) {
     const int nq = q_hi > q_lo ? (q_hi - q_lo + 63) / 64 : 0;
 
     if (warp >= kProdWarp0 && warp < kMmaWarp) {
+        constexpr int kAtoms = D / 64;
         const int pw = warp - kProdWarp0, ptid = threadIdx.x - kProdWarp0 * 32;
-        load_tile<D, 128>(sbase + SM::kK, a.k, b, h, a.L, a.H, pw, lane, key_of);
-        load_tile<D, 128>(sbase + SM::kV, a.v, b, h, a.L, a.H, pw, lane, key_of);
-        cp_async_arrive_noinc(&bars[KB_KVFULL]);
+        if (SEL) {  // the ever-selected rows: one gather per CTA
+            RowKeys<D, 128> kk;
+            kk.fetch(pw, lane, key_of);
+            kk.issue(sbase + SM::kK, a.k, b, h, a.L, a.H, pw, lane);
+            kk.issue(sbase + SM::kV, a.v, b, h, a.L, a.H, pw, lane);
+            cp_async_arrive_noinc(&bars[KB_KVFULL]);
+            if (ptid == 0) mbar_arrive(&bars[KB_KVFULL]);
+        } else {
+            if (ptid == 0) {
+                mbar_expect_tx(&bars[KB_KVFULL], 2 * 128 * D * 2);
+#pragma unroll
+                for (int at = 0; at < kAtoms; ++at) {
+                    tma_load_3d(sbase + SM::kK + at * 128 * 128, &a.tm_k128, h * D + at * 64, j0, b, &bars[KB_KVFULL]);
+                    tma_load_3d(sbase + SM::kV + at * 128 * 128, &a.tm_v128, h * D + at * 64, j0, b, &bars[KB_KVFULL]);
+                }
+            }
+            mbar_arrive(&bars[KB_KVFULL]);
+        }
         const float* lse2 = a.lse2 + ((int64_t)b * a.H + h) * a.L;
         const float* dlt = a.delta + ((int64_t)b * a.H + h) * a.L;
         for (int qt = 0; qt < nq; ++qt) {
-            const int s = qt & 1;
-            if (qt >= 2) mbar_wait(&bars[KB_QDEMPTY + s], ((qt - 2) >> 1) & 1);
+            const int s = qt % kQS;
+            if (qt >= kQS) mbar_wait(&bars[KB_QDEMPTY + s], ((qt - kQS) / kQS) & 1);
             const int qs = q_lo + qt * 64;
-            auto qf = [&](int r) { return qs + r < a.L ? qs + r : -1; };
-            load_tile<D, 64>(sbase + SM::kQ + s * SM::kQT, a.q, b, h, a.L, a.H, pw, lane, qf);
-            load_tile<D, 64>(sbase + SM::kDO + s * SM::kQT, a.dout, b, h, a.L, a.H, pw, lane, qf);
             for (int c = ptid; c < 64; c += kProducers) {
                 const int i = qs + c;
                 const bool ok = i < a.L;
@@ -180,6 +209,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_tc(BwdArgs a) {
                 cp_async4(mb + 128 * 4, a.tauf + bl + (ok && t >= 0 ? t : 0), ok && t >= 0);
             }
             cp_async_arrive_noinc(&bars[KB_QDFULL + s]);
+            if (ptid == 0) {
+                mbar_expect_tx(&bars[KB_QDFULL + s], 2 * 64 * D * 2);
+#pragma unroll
+                for (int at = 0; at < kAtoms; ++at) {
+                    tma_load_3d(sbase + SM::kQ + s * SM::kQT + at * 64 * 128, &a.tm_q64, h * D + at * 64, qs, b,
+                                &bars[KB_QDFULL + s]);
+                    tma_load_3d(sbase + SM::kDO + s * SM::kQT + at * 64 * 128, &a.tm_do64, h * D + at * 64, qs, b,
+                                &bars[KB_QDFULL + s]);
+                }
+            }
         }
     } else if (warp == kMmaWarp) {
         if (lane == 0 && nq > 0) {
@@ -188,28 +227,25 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_tc(BwdArgs a) {
             mbar_wait(&bars[KB_KVFULL], 0);
             fence_proxy_async();
             auto acc = [&](int j) {
-                const int s = j & 1;
-                mbar_wait(&bars[KB_PDSFULL], j & 1);
+                const int s = j & 1, qs = j % kQS;
+                mbar_wait(&bars[KB_PDSFULL + s], (j >> 1) & 1);
                 tc_after_sync();
-                const uint32_t dob = sbase + SM::kDO + s * SM::kQT, qb = sbase + SM::kQ + s * SM::kQT;
-                const uint32_t ptb = sbase + SM::kPT + s * SM::kPD, dsb = sbase + SM::kDS + s * SM::kPD;
+                const uint32_t dob = sbase + SM::kDO + qs * SM::kQT, qb = sbase + SM::kQ + qs * SM::kQT;
+                // P~^T / dS^T of query half hf (32 queries) sit in TMEM columns [hf*32, hf*32+16)
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk) {
-                    umma_f16(tDV, desc_kmajor(ptb, 128, kk), desc_mnmajor(dob, 64, kk), id_acc,
-                             (j > 0 || kk > 0) ? 1u : 0u);
-                    umma_f16(tDK, desc_kmajor(dsb, 128, kk), desc_mnmajor(qb, 64, kk), id_acc,
-                             (j > 0 || kk > 0) ? 1u : 0u);
+                    const uint32_t co = s * 64 + (kk >> 1) * 32 + (kk & 1) * 8;
+                    umma_f16_ts(tDV, tS + co, desc_mnmajor(dob, 64, kk), id_acc, (j > 0 || kk > 0) ? 1u : 0u);
+                    umma_f16_ts(tDK, tP + co, desc_mnmajor(qb, 64, kk), id_acc, (j > 0 || kk > 0) ? 1u : 0u);
                 }
-                umma_commit(&bars[KB_QDEMPTY + s]);
-                umma_commit(&bars[KB_PDSEMPTY + s]);
+                umma_commit(&bars[KB_QDEMPTY + qs]);
             };
             for (int qt = 0; qt < nq; ++qt) {
-                const int s = qt & 1;
-                mbar_wait(&bars[KB_QDFULL + s], (qt >> 1) & 1);
-                fence_proxy_async();
+                const int s = qt & 1, qs = qt % kQS;
+                mbar_wait(&bars[KB_QDFULL + qs], (qt / kQS) & 1);
                 if (qt >= 2) mbar_wait(&bars[KB_SEMPTY + s], ((qt - 2) >> 1) & 1);
                 tc_after_sync();
-                const uint32_t qb = sbase + SM::kQ + s * SM::kQT, dob = sbase + SM::kDO + s * SM::kQT;
+                const uint32_t qb = sbase + SM::kQ + qs * SM::kQT, dob = sbase + SM::kDO + qs * SM::kQT;
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk) {
                     umma_f16(tS + s * 64, desc_kmajor(sbase + SM::kK, 128, kk), desc_kmajor(qb, 64, kk), id_s,
@@ -224,7 +260,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_tc(BwdArgs a) {
             umma_commit(&bars[KB_ACCDONE]);
         }
         __syncwarp();
-    } else {
+    } else if (warp < kProdWarp0) {
         // key rows: two math warpgroups, each owning 32 of the 64 query columns
         const int hf = warp >> 2;
         const int r = ((warp & 3) << 5) | lane;
@@ -233,16 +269,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_tc(BwdArgs a) {
         const float uj = (SEL && key >= 0) ? __ldg(a.uf + bl + key) : 0.f;
         const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
         const float sl2 = a.scale_log2;
+        const float2 sl22 = make_float2(sl2, sl2);
         // queries reading this key form one interval: window [j, j+w), selected
         // [j+w, leave_j+w) (proj/src/cache.cpp:259-311)
         const int lo_i = SEL ? key + a.w : key;
         const int hi_i = min(a.L, SEL ? leave + a.w : key + a.w);  // exclusive
         float colsum = 0.f;
         for (int qt = 0; qt < nq; ++qt) {
-            const int s = qt & 1;
+            const int s = qt & 1, qs3 = qt % kQS;
             const int qs = q_lo + qt * 64 + hf * 32;  // first query of this thread's columns
             mbar_wait(&bars[KB_SFULL + s], (qt >> 1) & 1);
-            mbar_wait(&bars[KB_QDFULL + s], (qt >> 1) & 1);
+            mbar_wait(&bars[KB_QDFULL + qs3], (qt / kQS) & 1);
             tc_after_sync();
             float sv[32], dp[32];
             tmem_ld32(tS + lane_off + s * 64 + hf * 32, sv);
@@ -250,7 +287,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_tc(BwdArgs a) {
             tmem_wait_ld();
             tc_before_sync();
             mbar_arrive(&bars[KB_SEMPTY + s]);
-            const float* ml = qmeta + (s * 3) * 64 + hf * 32;
+            const float* ml = qmeta + (qs3 * 3) * 64 + hf * 32;
             const float* md = ml + 64;
             const float* mt = ml + 128;
             const int cmin = key >= 0 ? lo_i - qs : 32;
@@ -261,55 +298,67 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_tc(BwdArgs a) {
                 const int clast = max(0, min(31, a.L - 1 - qs));
                 sat = __all_sync(0xffffffffu, key < 0 || uj >= mt[clast] + 1.f);
             }
-            float csum = 0.f;
+            if (!full) {
 #pragma unroll
-            for (int c = 0; c < 32; c += 4) {
-                const float4 l4 = *reinterpret_cast<const float4*>(ml + c);
-                const float4 d4 = *reinterpret_cast<const float4*>(md + c);
-                const float la[4] = {l4.x, l4.y, l4.z, l4.w};
-                const float da[4] = {d4.x, d4.y, d4.z, d4.w};
-                float ta[4] = {0.f, 0.f, 0.f, 0.f};
-                if (SEL && !sat) {
+                for (int c = 0; c < 32; ++c) sv[c] = (c >= cmin && c <= cmax) ? sv[c] : -INFINITY;
+            }
+            if (!SEL || sat) {  // all gates 1 on these columns: plain softmax backward, packed fp32x2
+#pragma unroll
+                for (int c = 0; c < 32; c += 4) {
+                    const float4 l4 = *reinterpret_cast<const float4*>(ml + c);
+                    const float4 d4 = *reinterpret_cast<const float4*>(md + c);
+                    float2 x0 = __ffma2_rn(make_float2(sv[c], sv[c + 1]), sl22, make_float2(-l4.x, -l4.y));
+                    float2 x1 = __ffma2_rn(make_float2(sv[c + 2], sv[c + 3]), sl22, make_float2(-l4.z, -l4.w));
+                    x0.x = ex2(x0.x);
+                    x0.y = ex2(x0.y);
+                    x1.x = ex2(x1.x);
+                    x1.y = ex2(x1.y);
+                    const float2 c0 = __fmul2_rn(x0, __fadd2_rn(make_float2(dp[c], dp[c + 1]), make_float2(-d4.x, -d4.y)));
+                    const float2 c1 = __fmul2_rn(x1, __fadd2_rn(make_float2(dp[c + 2], dp[c + 3]), make_float2(-d4.z, -d4.w)));
+                    sv[c] = x0.x, sv[c + 1] = x0.y, sv[c + 2] = x1.x, sv[c + 3] = x1.y;  // P~^T
+                    dp[c] = c0.x, dp[c + 1] = c0.y, dp[c + 2] = c1.x, dp[c + 3] = c1.y;  // dS^T (unscaled)
+                }
+            } else {
+                float csum = 0.f;
+#pragma unroll
+                for (int c = 0; c < 32; c += 4) {
+                    const float4 l4 = *reinterpret_cast<const float4*>(ml + c);
+                    const float4 d4 = *reinterpret_cast<const float4*>(md + c);
                     const float4 t4 = *reinterpret_cast<const float4*>(mt + c);
-                    ta[0] = t4.x;
-                    ta[1] = t4.y;
-                    ta[2] = t4.z;
-                    ta[3] = t4.w;
-                }
+                    const float la[4] = {l4.x, l4.y, l4.z, l4.w};
+                    const float da[4] = {d4.x, d4.y, d4.z, d4.w};
+                    const float ta[4] = {t4.x, t4.y, t4.z, t4.w};
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const int cc_ = c + e;
-                    const float g = (SEL && !sat) ? __saturatef(uj - ta[e]) : 1.f;
-                    const float kap = (KEY_SOFT && SEL) ? g : 1.f;
-                    const float x = (full || (cc_ >= cmin && cc_ <= cmax)) ? sv[cc_] * kap : -INFINITY;
-                    const float p = ex2(fmaf(x, sl2, -la[e]));  // masked: 0
-                    const float wv = (SEL && !a.mask_st) ? g : 1.f;
-                    const float cc = p * fmaf(wv, dp[cc_], -da[e]);
-                    if (SEL && !sat) {
+                    for (int e = 0; e < 4; ++e) {
+                        const int cc_ = c + e;
+                        const float g = __saturatef(uj - ta[e]);
+                        const float kap = KEY_SOFT ? g : 1.f;
+                        const float raw = sv[cc_];
+                        const float x = (KEY_SOFT && raw == -INFINITY) ? raw : raw * kap;
+                        const float p = ex2(fmaf(x, sl2, -la[e]));  // masked: 0
+                        const float wv = a.mask_st ? 1.f : g;
+                        const float cc = p * fmaf(wv, dp[cc_], -da[e]);
                         float gm = p * dp[cc_];
-                        if (KEY_SOFT) gm += a.scale * cc * sv[cc_];
+                        if (KEY_SOFT) gm += a.scale * cc * (raw == -INFINITY ? 0.f : raw);
                         csum += (g > 0.f && g < 1.f) ? gm : 0.f;
+                        sv[cc_] = p * wv;    // P~^T
+                        dp[cc_] = cc * kap;  // dS^T (scale applied in the epilogue)
                     }
-                    sv[cc_] = p * wv;    // P~^T
-                    dp[cc_] = cc * kap;  // dS^T (scale applied in the epilogue)
                 }
+                colsum += csum;
             }
-            colsum += csum;
-            if (qt >= 2) mbar_wait(&bars[KB_PDSEMPTY + s], ((qt - 2) >> 1) & 1);
-            const uint32_t ptb = sbase + SM::kPT + s * SM::kPD, dsb = sbase + SM::kDS + s * SM::kPD;
+            {  // P~^T and dS^T -> TMEM over this half's consumed columns (packed bf16x2)
+                uint32_t pk[16];
 #pragma unroll
-            for (int ch = 0; ch < 4; ++ch) {
-                const int pc = ((hf * 4 + ch) ^ (r & 7)) << 4;
-                const float* x = sv + ch * 8;
-                st_shared_v4(ptb + r * 128 + pc, pack_bf16(x[0], x[1]), pack_bf16(x[2], x[3]),
-                             pack_bf16(x[4], x[5]), pack_bf16(x[6], x[7]));
-                const float* y = dp + ch * 8;
-                st_shared_v4(dsb + r * 128 + pc, pack_bf16(y[0], y[1]), pack_bf16(y[2], y[3]),
-                             pack_bf16(y[4], y[5]), pack_bf16(y[6], y[7]));
+                for (int e = 0; e < 16; ++e) pk[e] = pack_bf16(sv[2 * e], sv[2 * e + 1]);
+                tmem_st16u(tS + lane_off + s * 64 + hf * 32, pk);
+#pragma unroll
+                for (int e = 0; e < 16; ++e) pk[e] = pack_bf16(dp[2 * e], dp[2 * e + 1]);
+                tmem_st16u(tP + lane_off + s * 64 + hf * 32, pk);
+                tmem_wait_st();
             }
-            fence_proxy_async();
             tc_before_sync();
-            mbar_arrive(&bars[KB_PDSFULL]);
+            mbar_arrive(&bars[KB_PDSFULL + s]);
         }
         if (SEL && key >= 0 && colsum != 0.f) atomicAdd(a.colsum + bl + key, (double)colsum);
         if (nq > 0) {
@@ -385,61 +434,69 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_tc(BwdArgs a) {
 }
 
 // ------------------------------------------------------------------ dQ
+// Query-major over 64-key tiles [selected union | window band]. Per tile:
+// S = Q K^T and dP = dO V^T (tcgen05, M=128, N=64) in TMEM; two math
+// warpgroups (32 keys each) form dS = P (wv dP - delta) * kappa and write it
+// back into TMEM as bf16 over their consumed dP columns: the A operand of the
+// TS-MMA dQ += dS K. Producers: Q/dO and the window band by 3-D TMA, the
+// selected rows by cp.async gathers with keys fetched one tile ahead, the
+// per-key metadata by cp.async from skb_select's precomputed block arrays.
 constexpr int kNS = 3;  // K/V ring depth of the dQ kernel
 
 template <int D>
 struct QSmem {
     static constexpr int kQT = 128 * D * 2;  // 128-query tile
     static constexpr int kKT = 64 * D * 2;   // 64-key tile
-    static constexpr int kDSB = 128 * 64 * 2;
     static constexpr int kQ = 0;
     static constexpr int kDO = kQ + kQT;
     static constexpr int kK = kDO + kQT;            // [kNS]
     static constexpr int kV = kK + kNS * kKT;       // [kNS]
-    static constexpr int kDS = kV + kNS * kKT;      // [2]
-    static constexpr int kMeta = kDS + 2 * kDSB;    // [kNS][3][64] x 4 B
-    static constexpr int kFlags = kMeta + kNS * 3 * 64 * 4;  // [kNS][4] int
-    static constexpr int kBar = kFlags + kNS * 4 * 4;
-    static constexpr int kTmemSlot = kBar + 24 * 8;
+    static constexpr int kMeta = kV + kNS * kKT;    // [kNS][key|ext|uf][64] x 4 B
+    static constexpr int kFlags = kMeta + kNS * 3 * 64 * 4;  // [kNS] x 16 B
+    static constexpr int kBar = kFlags + kNS * 16;
+    static constexpr int kNumBars = 20;
+    static constexpr int kTmemSlot = kBar + kNumBars * 8;
     static constexpr int kAlloc = kTmemSlot + 16 + 1024;
 };
-enum { QB_QFULL = 0, QB_KVFULL = 1, QB_KVEMPTY = 4, QB_SFULL = 7, QB_SEMPTY = 9, QB_DSFULL = 11,
-       QB_DSEMPTY = 12, QB_DQDONE = 14 };
+enum { QB_QFULL = 0, QB_KVFULL = 1, QB_KVEMPTY = 4, QB_MFULL = 7, QB_MEMPTY = 10, QB_SFULL = 13,
+       QB_SEMPTY = 15, QB_DSFULL = 17, QB_DQDONE = 19 };  // 20 barriers
 
 template <int D, bool KEY_SOFT>
-__global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(BwdArgs a) {
+__global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(const __grid_constant__ BwdArgs a) {
     using SM = QSmem<D>;
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const uint32_t sbase = smem_u32(smem);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SM::kBar);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + SM::kTmemSlot);
-    int* meta = reinterpret_cast<int*>(smem + SM::kMeta);  // [stage][key|leave|uf][64]
-    int* tflags = reinterpret_cast<int*>(smem + SM::kFlags);  // [stage][producer warp]
+    int* meta = reinterpret_cast<int*>(smem + SM::kMeta);
+    int* tflags = reinterpret_cast<int*>(smem + SM::kFlags);
 
     const int qb = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t bl = (int64_t)b * a.L;
+    const int64_t qrow = (int64_t)b * a.nqb + qb;
     const int i0 = qb * 128;
-    const int cnt = (a.R1 > 0) ? a.qb_count[(int64_t)b * a.nqb + qb] : 0;
+    const int cnt = (a.R1 > 0) ? a.qb_count[qrow] : 0;
     const int n_sel = (cnt + 63) / 64;
     const int n_win = (a.w + 127 + 63) / 64;
     const int n = n_sel + n_win;
     const int jw0 = i0 - a.w + 1;
-    const int* list = a.qb_list + ((int64_t)b * a.nqb + qb) * a.qb_cap;
+    const int* list = a.qb_list + qrow * a.qb_cap;
 
     if (threadIdx.x == 0) {
-        mbar_init(&bars[QB_QFULL], kProducers);
+        mbar_init(&bars[QB_QFULL], 1);
         for (int s = 0; s < kNS; ++s) {
-            mbar_init(&bars[QB_KVFULL + s], 2 * kProducers);  // cp.async + flag release
+            mbar_init(&bars[QB_KVFULL + s], kProducers + 1);
             mbar_init(&bars[QB_KVEMPTY + s], 1);
+            mbar_init(&bars[QB_MFULL + s], kProducers);
+            mbar_init(&bars[QB_MEMPTY + s], kMath);
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(&bars[QB_SFULL + s], 1);
             mbar_init(&bars[QB_SEMPTY + s], kMath);
-            mbar_init(&bars[QB_DSEMPTY + s], 1);
+            mbar_init(&bars[QB_DSFULL + s], kMath);
         }
-        mbar_init(&bars[QB_DSFULL], kMath);
         mbar_init(&bars[QB_DQDONE], 1);
         mbar_fence_init();
     }
@@ -448,77 +505,78 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(BwdArgs a) {
     __syncthreads();
     tc_after_sync();
     const uint32_t tmem = *tmem_slot;
-    const uint32_t tS = tmem, tP = tmem + 128, tDQ = tmem + 256;
+    const uint32_t tS = tmem, tP = tmem + 128, tDQ = tmem + 256;  // S[2], dP/dS[2] (64 cols each), dQ
 
     if (warp >= kProdWarp0 && warp < kMmaWarp) {
+        constexpr int kAtoms = D / 64;
         const int pw = warp - kProdWarp0, ptid = threadIdx.x - kProdWarp0 * 32;
-        auto qf = [&](int r) { return i0 + r < a.L ? i0 + r : -1; };
-        load_tile<D, 128>(sbase + SM::kQ, a.q, b, h, a.L, a.H, pw, lane, qf);
-        load_tile<D, 128>(sbase + SM::kDO, a.dout, b, h, a.L, a.H, pw, lane, qf);
-        cp_async_arrive_noinc(&bars[QB_QFULL]);
+        if (ptid == 0) {
+            mbar_expect_tx(&bars[QB_QFULL], 2 * 128 * D * 2);
+#pragma unroll
+            for (int at = 0; at < kAtoms; ++at) {
+                tma_load_3d(sbase + SM::kQ + at * 128 * 128, &a.tm_q128, h * D + at * 64, i0, b, &bars[QB_QFULL]);
+                tma_load_3d(sbase + SM::kDO + at * 128 * 128, &a.tm_do128, h * D + at * 64, i0, b,
+                            &bars[QB_QFULL]);
+            }
+        }
+        RowKeys<D, 64> kcur;
+        if (n_sel > 0) kcur.fetch(pw, lane, [&](int r) { return __ldg(list + r); });
+        const int ma = ptid >> 4, mc = ptid & 15;  // metadata: 48 threads, array x 16-byte chunk
+        const int* msrc = ma == 0 ? a.qb_list : ma == 1 ? a.qb_leave : reinterpret_cast<const int*>(a.qb_uf);
         for (int jt = 0; jt < n; ++jt) {
-            const int s = jt % kNS;  // K/V stage
+            const int s = jt % kNS;
+            if (jt >= kNS) mbar_wait(&bars[QB_MEMPTY + s], ((jt - kNS) / kNS) & 1);
+            if (jt < n_sel) {
+                if (ptid < 48)
+                    cp_async16(smem_u32(meta + (s * 3 + ma) * 64 + mc * 4), msrc + qrow * a.qb_cap + jt * 64 + mc * 4,
+                               true);
+                if (ptid == 48)
+                    cp_async16(smem_u32(tflags + s * 4), a.qb_flags + (qrow * (a.qb_cap / 128) + (jt >> 1)) * 4, true);
+            }
+            cp_async_arrive_noinc(&bars[QB_MFULL + s]);
             if (jt >= kNS) mbar_wait(&bars[QB_KVEMPTY + s], ((jt - kNS) / kNS) & 1);
             if (jt < n_sel) {
-                // the row gathers first: they are the long pole
-                auto kf = [&](int r) {
-                    const int idx = jt * 64 + r;
-                    return idx < cnt ? __ldg(list + idx) : -1;
-                };
-                load_tile<D, 64>(sbase + SM::kK + s * SM::kKT, a.k, b, h, a.L, a.H, pw, lane, kf);
-                load_tile<D, 64>(sbase + SM::kV + s * SM::kKT, a.v, b, h, a.L, a.H, pw, lane, kf);
-                const int t_lo = i0 - a.w;
-                const int t_hi = min(i0 + 127, a.L - 1) - a.w;
-                const float tau_hi = t_hi >= 0 ? __ldg(a.tauf + bl + t_hi) : -INFINITY;
-                bool all_ok = true, all_sat = true;
-                for (int c = ptid; c < 64; c += kProducers) {
-                    const int idx = jt * 64 + c;
-                    const int key = idx < cnt ? __ldg(list + idx) : -1;
-                    const uint32_t mb = smem_u32(meta + (s * 3) * 64 + c);
-                    cp_async4(mb, list + (idx < cnt ? idx : 0), idx < cnt);
-                    cp_async4(mb + 64 * 4, a.leave + bl + (key >= 0 ? key : 0), key >= 0);
-                    cp_async4(mb + 128 * 4, a.uf + bl + (key >= 0 ? key : 0), key >= 0);
-                    if (key >= 0) {
-                        all_ok = all_ok && key <= t_lo && __ldg(a.leave + bl + key) > t_hi;
-                        all_sat = all_sat && __ldg(a.uf + bl + key) >= tau_hi + 1.f;
-                    } else {
-                        all_ok = false;
+                kcur.issue(sbase + SM::kK + s * SM::kKT, a.k, b, h, a.L, a.H, pw, lane);
+                kcur.issue(sbase + SM::kV + s * SM::kKT, a.v, b, h, a.L, a.H, pw, lane);
+                cp_async_arrive_noinc(&bars[QB_KVFULL + s]);
+                if (ptid == 0) mbar_arrive(&bars[QB_KVFULL + s]);
+                if (jt + 1 < n_sel) kcur.fetch(pw, lane, [&](int r) { return __ldg(list + (jt + 1) * 64 + r); });
+            } else {
+                if (ptid == 0) {
+                    const int kb0 = jw0 + (jt - n_sel) * 64;
+                    mbar_expect_tx(&bars[QB_KVFULL + s], 2 * 64 * D * 2);
+#pragma unroll
+                    for (int at = 0; at < kAtoms; ++at) {
+                        tma_load_3d(sbase + SM::kK + s * SM::kKT + at * 64 * 128, &a.tm_k64, h * D + at * 64, kb0, b,
+                                    &bars[QB_KVFULL + s]);
+                        tma_load_3d(sbase + SM::kV + s * SM::kKT + at * 64 * 128, &a.tm_v64, h * D + at * 64, kb0, b,
+                                    &bars[QB_KVFULL + s]);
                     }
                 }
-                all_ok = __all_sync(0xffffffffu, all_ok);
-                all_sat = __all_sync(0xffffffffu, all_sat);
-                if (lane == 0) tflags[s * 4 + pw] = (all_ok ? 1 : 0) | (all_sat ? 2 : 0);
-            } else {
-                const int kb0 = jw0 + (jt - n_sel) * 64;
-                auto kf = [&](int r) { return kb0 + r; };
-                load_tile<D, 64>(sbase + SM::kK + s * SM::kKT, a.k, b, h, a.L, a.H, pw, lane, kf);
-                load_tile<D, 64>(sbase + SM::kV + s * SM::kKT, a.v, b, h, a.L, a.H, pw, lane, kf);
+                mbar_arrive(&bars[QB_KVFULL + s]);
             }
-            mbar_arrive(&bars[QB_KVFULL + s]);
-            cp_async_arrive_noinc(&bars[QB_KVFULL + s]);
         }
     } else if (warp == kMmaWarp) {
         if (lane == 0) {
             constexpr uint32_t id_s = umma_idesc(128, 64, false, false);
             constexpr uint32_t id_dq = umma_idesc(128, D, false, true);
             mbar_wait(&bars[QB_QFULL], 0);
-            fence_proxy_async();
             auto dq = [&](int j) {
                 const int s = j & 1, ks = j % kNS;
-                mbar_wait(&bars[QB_DSFULL], j & 1);
+                mbar_wait(&bars[QB_DSFULL + s], (j >> 1) & 1);
                 tc_after_sync();
-                const uint32_t dsb = sbase + SM::kDS + s * SM::kDSB, kb = sbase + SM::kK + ks * SM::kKT;
+                const uint32_t kb = sbase + SM::kK + ks * SM::kKT;
+                // dS of key half hf (32 keys) lives in TMEM columns [hf*32, hf*32+16) of dP(s)
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk)
-                    umma_f16(tDQ, desc_kmajor(dsb, 128, kk), desc_mnmajor(kb, 64, kk), id_dq,
-                             (j > 0 || kk > 0) ? 1u : 0u);
+                    umma_f16_ts(tDQ, tP + s * 64 + (kk >> 1) * 32 + (kk & 1) * 8, desc_mnmajor(kb, 64, kk), id_dq,
+                                (j > 0 || kk > 0) ? 1u : 0u);
                 umma_commit(&bars[QB_KVEMPTY + ks]);
-                umma_commit(&bars[QB_DSEMPTY + s]);
             };
             for (int jt = 0; jt < n; ++jt) {
                 const int s = jt & 1, ks = jt % kNS;
                 mbar_wait(&bars[QB_KVFULL + ks], (jt / kNS) & 1);
-                fence_proxy_async();
+                fence_proxy_async();  // cp.async (generic proxy) rows -> tensor core reads
                 if (jt >= 2) mbar_wait(&bars[QB_SEMPTY + s], ((jt - 2) >> 1) & 1);
                 tc_after_sync();
                 const uint32_t kb = sbase + SM::kK + ks * SM::kKT, vb = sbase + SM::kV + ks * SM::kKT;
@@ -536,7 +594,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(BwdArgs a) {
             umma_commit(&bars[QB_DQDONE]);
         }
         __syncwarp();
-    } else {
+    } else if (warp < kProdWarp0) {
         // query rows: two math warpgroups, each owning 32 of the 64 key columns
         const int hf = warp >> 2;
         const int r = ((warp & 3) << 5) | lane;
@@ -549,13 +607,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(BwdArgs a) {
         const float dlt = i < a.L ? a.delta[hl + i] : 0.f;
         const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
         const float sl2 = a.scale_log2;
+        const float2 sl22 = make_float2(sl2, sl2), nl2 = make_float2(nlse2, nlse2), ndl = make_float2(-dlt, -dlt);
         float rsum = 0.f;
         for (int jt = 0; jt < n; ++jt) {
             const int s = jt & 1;
             const bool is_sel = jt < n_sel;
             const int ks = jt % kNS;
             mbar_wait(&bars[QB_SFULL + s], (jt >> 1) & 1);
-            mbar_wait(&bars[QB_KVFULL + ks], (jt / kNS) & 1);
+            if (is_sel) mbar_wait(&bars[QB_MFULL + ks], (jt / kNS) & 1);
             tc_after_sync();
             float sv[32], dp[32];
             tmem_ld32(tS + lane_off + s * 64 + hf * 32, sv);
@@ -563,23 +622,25 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(BwdArgs a) {
             tmem_wait_ld();
             tc_before_sync();
             mbar_arrive(&bars[QB_SEMPTY + s]);
+            bool plain = true;
             if (is_sel) {
                 const int* mk = meta + (ks * 3) * 64 + hf * 32;
                 const int* ml = mk + 64;
                 const float* mu = reinterpret_cast<const float*>(mk + 128);
-                const int fl = tflags[ks * 4] & tflags[ks * 4 + 1] & tflags[ks * 4 + 2];
-                if (!(fl & 1)) {  // per-key interval mask j <= t < leave_j
+                const int fl = tflags[ks * 4];
+                if (!(fl & 1)) {  // per-key interval mask j <= t < leave_j: (unsigned)(t - j) < leave_j - j
 #pragma unroll
                     for (int c = 0; c < 32; c += 4) {
                         const int4 kj = *reinterpret_cast<const int4*>(mk + c);
-                        const int4 lv = *reinterpret_cast<const int4*>(ml + c);
-                        sv[c + 0] = (kj.x <= t && lv.x > t) ? sv[c + 0] : -INFINITY;
-                        sv[c + 1] = (kj.y <= t && lv.y > t) ? sv[c + 1] : -INFINITY;
-                        sv[c + 2] = (kj.z <= t && lv.z > t) ? sv[c + 2] : -INFINITY;
-                        sv[c + 3] = (kj.w <= t && lv.w > t) ? sv[c + 3] : -INFINITY;
+                        const int4 ex = *reinterpret_cast<const int4*>(ml + c);
+                        sv[c + 0] = ((unsigned)(t - kj.x) < (unsigned)ex.x) ? sv[c + 0] : -INFINITY;
+                        sv[c + 1] = ((unsigned)(t - kj.y) < (unsigned)ex.y) ? sv[c + 1] : -INFINITY;
+                        sv[c + 2] = ((unsigned)(t - kj.z) < (unsigned)ex.z) ? sv[c + 2] : -INFINITY;
+                        sv[c + 3] = ((unsigned)(t - kj.w) < (unsigned)ex.w) ? sv[c + 3] : -INFINITY;
                     }
                 }
                 if (!(fl & 2)) {  // fractional gates present
+                    plain = false;
 #pragma unroll
                     for (int c = 0; c < 32; c += 4) {
                         const float4 uu = *reinterpret_cast<const float4*>(mu + c);
@@ -600,12 +661,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(BwdArgs a) {
                             dp[c + e] = cc * kap;
                         }
                     }
-                } else {  // all gates 1: plain softmax backward
-#pragma unroll
-                    for (int c = 0; c < 32; ++c) {
-                        const float p = ex2(fmaf(sv[c], sl2, nlse2));
-                        dp[c] = p * (dp[c] - dlt);
-                    }
                 }
             } else {
                 const int kb = jw0 + (jt - n_sel) * 64 + hf * 32;
@@ -615,23 +670,29 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(BwdArgs a) {
 #pragma unroll
                     for (int c = 0; c < 32; ++c) sv[c] = (c >= cmin && c <= cmax) ? sv[c] : -INFINITY;
                 }
+            }
+            if (plain) {  // all gates 1: plain softmax backward, packed fp32x2
 #pragma unroll
-                for (int c = 0; c < 32; ++c) {
-                    const float p = ex2(fmaf(sv[c], sl2, nlse2));
-                    dp[c] = p * (dp[c] - dlt);
+                for (int c = 0; c < 32; c += 2) {
+                    float2 x = __ffma2_rn(make_float2(sv[c], sv[c + 1]), sl22, nl2);
+                    x.x = ex2(x.x);
+                    x.y = ex2(x.y);
+                    const float2 d = __fmul2_rn(x, __fadd2_rn(make_float2(dp[c], dp[c + 1]), ndl));
+                    dp[c] = d.x;
+                    dp[c + 1] = d.y;
                 }
             }
-            if (jt >= 2) mbar_wait(&bars[QB_DSEMPTY + s], ((jt - 2) >> 1) & 1);
-            const uint32_t dsb = sbase + SM::kDS + s * SM::kDSB;
+            // dS -> TMEM over this half's consumed dP columns (packed bf16x2)
+            {
+                uint32_t pk[16];
 #pragma unroll
-            for (int ch = 0; ch < 4; ++ch) {
-                const float* y = dp + ch * 8;
-                st_shared_v4(dsb + r * 128 + (((hf * 4 + ch) ^ (r & 7)) << 4), pack_bf16(y[0], y[1]),
-                             pack_bf16(y[2], y[3]), pack_bf16(y[4], y[5]), pack_bf16(y[6], y[7]));
+                for (int e = 0; e < 16; ++e) pk[e] = pack_bf16(dp[2 * e], dp[2 * e + 1]);
+                tmem_st16u(tP + lane_off + s * 64 + hf * 32, pk);
+                tmem_wait_st();
             }
-            fence_proxy_async();
             tc_before_sync();
-            mbar_arrive(&bars[QB_DSFULL]);
+            mbar_arrive(&bars[QB_MEMPTY + ks]);
+            mbar_arrive(&bars[QB_DSFULL + s]);
         }
         mbar_wait(&bars[QB_DQDONE], 0);
         tc_after_sync();
@@ -697,6 +758,17 @@ void run_attn_bwd_tc(const skb_attn_desc& d, const void* q, const void* k, const
     (void)u;
     char* base = static_cast<char*>(ws);
     BwdArgs a{};
+    {
+        const int64_t HD = d.heads * d.head_dim;
+        a.tm_q128 = tmap_rows3d(q, d.batch, d.seq_len, HD, 128);
+        a.tm_do128 = tmap_rows3d(dout, d.batch, d.seq_len, HD, 128);
+        a.tm_k64 = tmap_rows3d(k, d.batch, d.seq_len, HD, 64);
+        a.tm_v64 = tmap_rows3d(v, d.batch, d.seq_len, HD, 64);
+        a.tm_q64 = tmap_rows3d(q, d.batch, d.seq_len, HD, 64);
+        a.tm_do64 = tmap_rows3d(dout, d.batch, d.seq_len, HD, 64);
+        a.tm_k128 = tmap_rows3d(k, d.batch, d.seq_len, HD, 128);
+        a.tm_v128 = tmap_rows3d(v, d.batch, d.seq_len, HD, 128);
+    }
     a.q = static_cast<const __nv_bfloat16*>(q);
     a.k = static_cast<const __nv_bfloat16*>(k);
     a.v = static_cast<const __nv_bfloat16*>(v);
@@ -715,6 +787,9 @@ void run_attn_bwd_tc(const skb_attn_desc& d, const void* q, const void* k, const
     a.leave = s.leave;
     a.qb_count = s.qb_count;
     a.qb_list = s.qb_list;
+    a.qb_leave = s.qb_leave;
+    a.qb_uf = s.qb_uf;
+    a.qb_flags = s.qb_flags;
     a.ever_count = s.ever_count;
     a.ever_list = s.ever_list;
     a.rowsum = rowsum;
