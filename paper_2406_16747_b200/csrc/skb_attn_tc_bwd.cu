@@ -54,23 +54,33 @@ struct BwdArgs {
     int mask_st;
 };
 
+// One (b, i, h) row per D/8 threads: 16-byte loads of O and dO, a
+// shuffle-reduced dot product, lse converted to log2 units. HBM-bound.
 template <int D>
-__global__ void k_bwd_prep(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
-                           const double* __restrict__ lse, float* __restrict__ lse2,
-                           float* __restrict__ delta, int B, int L, int H) {
-    const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;  // (b, i, h)
-    const int lane = threadIdx.x & 31;
-    if (row >= (int64_t)B * L * H) return;
-    const __nv_bfloat16* orow = o + row * D;
-    const __nv_bfloat16* grow = dout + row * D;
+__global__ void __launch_bounds__(256) k_bwd_prep(const __nv_bfloat16* __restrict__ o,
+                                                  const __nv_bfloat16* __restrict__ dout,
+                                                  const double* __restrict__ lse, float* __restrict__ lse2,
+                                                  float* __restrict__ delta, int B, int L, int H) {
+    constexpr int kTpr = D / 8;  // threads per row
+    const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t row = gt / kTpr;  // (b, i, h)
+    const int sub = (int)(gt % kTpr);
+    const bool ok = row < (int64_t)B * L * H;
     float acc = 0.f;
-    for (int c = lane * 2; c < D; c += 64) {
-        const float2 x = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(orow + c));
-        const float2 g = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(grow + c));
-        acc += x.x * g.x + x.y * g.y;
+    if (ok) {
+        const uint4 x = *reinterpret_cast<const uint4*>(o + row * D + sub * 8);
+        const uint4 g = *reinterpret_cast<const uint4*>(dout + row * D + sub * 8);
+        const uint32_t xs[4] = {x.x, x.y, x.z, x.w}, gs[4] = {g.x, g.y, g.z, g.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const float2 a2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xs[e]));
+            const float2 b2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&gs[e]));
+            acc = fmaf(a2.x, b2.x, fmaf(a2.y, b2.y, acc));
+        }
     }
-    acc = warp_sum(acc);
-    if (lane == 0) {
+#pragma unroll
+    for (int off = kTpr / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if (ok && sub == 0) {
         const int h = (int)(row % H);
         const int64_t bi = row / H;
         const int i = (int)(bi % L), b = (int)(bi / L);
@@ -807,7 +817,7 @@ void run_attn_bwd_tc(const skb_attn_desc& d, const void* q, const void* k, const
     a.scale_log2 = (float)(scale * 1.4426950408889634);
     a.mask_st = d.mask_mode;
     const int64_t rows = d.batch * d.seq_len * d.heads;
-    const unsigned pg = (unsigned)cdiv(rows * 32, 256);
+    const unsigned pg = (unsigned)cdiv(rows * (d.head_dim / 8), 256);
     if (d.head_dim == 128)
         k_bwd_prep<128><<<pg, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(o), a.dout, lse, lse2, delta,
                                             a.B, a.L, a.H);

@@ -322,6 +322,22 @@ __global__ void __launch_bounds__(kTauThreads) k_tau_chunks(TauArgs a) {
     }
 }
 
+// Second pass over the chunks whose band exceeded the first pass's small
+// shared-memory cap, with the large cap; its own overflows go to queue 2.
+__global__ void __launch_bounds__(kTauThreads) k_tau_chunks_big(TauArgs a, int nchunks, int* q2_count, int* q2_items) {
+    extern __shared__ double smem[];
+    const int n = *a.ovf_count;
+    double* bz = smem;
+    double* P = smem + a.cap;
+    for (int it = blockIdx.x; it < n; it += gridDim.x) {
+        const int item = a.ovf_items[it];
+        if (!tau_chunk(a, item / nchunks, item % nchunks, bz, P, a.cap, false)) {
+            if (threadIdx.x == 0) q2_items[atomicAdd(q2_count, 1)] = item;
+        }
+        __syncthreads();
+    }
+}
+
 __global__ void __launch_bounds__(kTauThreads) k_tau_overflow(TauArgs a, int nchunks, int cap2) {
     const int n = *a.ovf_count;
     double* bz = a.scratch + (int64_t)blockIdx.x * a.scratch_stride;
@@ -531,7 +547,7 @@ void select_layout(const skb_attn_desc& d, skb_select_layout& o) {
     o.qb_list = take(B * nqb * cap * 4);
     o.ever_count = take(B * 4);
     o.ever_list = take(B * L * 4);
-    o.misc = take((1 + B * nch) * 4);
+    o.misc = take((2 + 2 * B * nch) * 4);  // two overflow queues: [count, items...] x 2
     const int64_t cap2 = next_pow2((int)std::max<int64_t>(L, 1));
     o.scratch = take((uint64_t)kOverflowSlots * (cap2 + L + 1) * 8);
     o.uf = take(B * L * 4);
@@ -597,7 +613,8 @@ void run_select(const skb_attn_desc& d, const double* u, void* ws, cudaStream_t 
     }
     if (d.k > 0.0 && T > 0) {
         const int nch = (int)cdiv(T, kChunk);
-        SKB_CHECK_CUDA(cudaMemsetAsync(misc, 0, 4, st));
+        SKB_CHECK_CUDA(cudaMemsetAsync(misc, 0, (2 + 2 * (size_t)B * nch) * 4, st));
+        int* q2 = misc + 1 + B * nch;  // second queue: [count, items...]
         TauArgs a;
         a.u = u;
         a.leave2 = leave2;
@@ -609,20 +626,33 @@ void run_select(const skb_attn_desc& d, const double* u, void* ws, cudaStream_t 
         a.T = T;
         a.R2 = R2;
         a.k = d.k;
-        a.cap = std::min(8192, next_pow2(std::max(T, 32)));
+        const int cap_big = std::min(8192, next_pow2(std::max(T, 32)));
+        // pass 1: a small band cap (many CTAs per SM) serves slope-dominated
+        // scores, whose band is ~ceil(k) wide; wider bands spill to pass 2
+        a.cap = std::min(cap_big, std::max(256, next_pow2(2 * R2)));
         const int cap2 = next_pow2(std::max(L, 1));
         a.scratch = scratch;
         a.scratch_stride = cap2 + L + 1;
-        const size_t smem = (size_t)a.cap * 2 * sizeof(double) + 16;
         static bool attr_set = false;
         if (!attr_set) {
             SKB_CHECK_CUDA(cudaFuncSetAttribute(k_tau_chunks, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                 (int)(8192 * 2 * sizeof(double) + 16)));
+            SKB_CHECK_CUDA(cudaFuncSetAttribute(k_tau_chunks_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)(8192 * 2 * sizeof(double) + 16)));
             attr_set = true;
         }
         dim3 g(nch, B);
-        k_tau_chunks<<<g, kTauThreads, smem, st>>>(a);
+        k_tau_chunks<<<g, kTauThreads, (size_t)a.cap * 2 * sizeof(double) + 16, st>>>(a);
         SKB_CHECK_LAUNCH();
+        if (cap_big > a.cap) {
+            TauArgs a2 = a;
+            a2.cap = cap_big;
+            k_tau_chunks_big<<<std::min(B * nch, 4 * 148), kTauThreads, (size_t)cap_big * 2 * sizeof(double) + 16, st>>>(
+                a2, nch, q2, q2 + 1);
+            SKB_CHECK_LAUNCH();
+            a.ovf_count = q2;  // the global-scratch pass serves what is left
+            a.ovf_items = q2 + 1;
+        }
         k_tau_overflow<<<kOverflowSlots, kTauThreads, 0, st>>>(a, nch, cap2);
         SKB_CHECK_LAUNCH();
         k_tau_monotone<<<B, 1024, 0, st>>>(tau, L, T);
