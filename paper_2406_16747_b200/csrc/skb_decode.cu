@@ -34,6 +34,7 @@
 // reference by rounding (never the selected set).
 #include <algorithm>
 #include <cfloat>
+#include <type_traits>
 #include <vector>
 
 #include "skb_common.cuh"
@@ -77,21 +78,31 @@ __device__ int warp_count_ge(const double* v, int n, double z) {
     return warp_sum_i(c);
 }
 
+// Shift [pos, n) up by one and put (z, zi) at pos. Blocks of 32 x 8 elements
+// from the top: all loads of a block are issued before any store, so a block
+// costs two memory round trips instead of one per 32 elements.
 __device__ void warp_insert(double* v, int* ix, int n, int pos, double z, int zi) {
     const int lane = threadIdx.x & 31;
-    for (int base = n - 1; base >= pos; base -= 32) {
-        const int i = base - lane;
-        const bool act = i >= pos;
-        double a = 0.0;
-        int b = 0;
-        if (act) {
-            a = v[i];
-            b = ix[i];
+    constexpr int U = 8;
+    for (int top = n - 1; top >= pos; top -= 32 * U) {
+        double a[U];
+        int c[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int i = top - u * 32 - lane;
+            if (i >= pos) {
+                a[u] = v[i];
+                c[u] = ix[i];
+            }
         }
         __syncwarp();
-        if (act) {
-            v[i + 1] = a;
-            ix[i + 1] = b;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int i = top - u * 32 - lane;
+            if (i >= pos) {
+                v[i + 1] = a[u];
+                ix[i + 1] = c[u];
+            }
         }
         __syncwarp();
     }
@@ -577,6 +588,133 @@ k_cache_attn(CacheArgs A, const T* __restrict__ q, int H, int p, float scale, fl
     }
 }
 
+// bf16 fast path (head_dim 64/128, H a multiple of 32/(D/8)): every load is a
+// 16-byte chunk and a warp instruction covers 512 contiguous bytes of a slot
+// row (HPL heads); warp w owns head groups j = w, w+8, ... for all entries of
+// the chunk, so the K and V streams are fully coalesced with many loads in
+// flight per lane.
+template <int D>
+__global__ void __launch_bounds__(kAttnThreads)
+k_cache_attn_bf16(CacheArgs A, const __nv_bfloat16* __restrict__ q, int H, float scale, float* __restrict__ po,
+                  float* __restrict__ pm, float* __restrict__ pl, int nsplit) {
+    constexpr int LPH = D / 8;     // lanes per head row (16 B each)
+    constexpr int HPL = 32 / LPH;  // heads per warp load
+    constexpr int JMAX = 4;        // head groups per warp (H <= 32 * HPL / 8 * JMAX)
+    extern __shared__ float sm[];
+    float* sp = sm;                                          // [H][kSlotsPerCta]
+    int* ss = reinterpret_cast<int*>(sp + H * kSlotsPerCta);  // [kSlotsPerCta]
+    float* svg = reinterpret_cast<float*>(ss + kSlotsPerCta);
+    float* skg = svg + kSlotsPerCta;
+    const int b = blockIdx.y, chunk = blockIdx.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = kAttnThreads / 32;
+    const int n = A.att_n[b];
+    const int e0 = chunk * kSlotsPerCta;
+    const int ne = max(0, min(kSlotsPerCta, n - e0));
+    const int64_t bS = (int64_t)b * A.S;
+    for (int e = threadIdx.x; e < ne; e += kAttnThreads) {
+        ss[e] = A.att_slot[bS + e0 + e];
+        svg[e] = A.att_vg[bS + e0 + e];
+        skg[e] = A.att_kg[bS + e0 + e] * scale;
+    }
+    const int nj = H / HPL;
+    const int hsub = lane / LPH, dch = (lane % LPH) * 8;
+    float qv[JMAX][8];
+#pragma unroll
+    for (int jj = 0; jj < JMAX; ++jj) {
+        const int j = warp + jj * nw;
+        if (j < nj) {
+            const uint4 r = *reinterpret_cast<const uint4*>(q + ((int64_t)b * H + j * HPL + hsub) * D + dch);
+            const uint32_t w4[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+            for (int x = 0; x < 4; ++x) {
+                const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w4[x]));
+                qv[jj][2 * x] = f.x;
+                qv[jj][2 * x + 1] = f.y;
+            }
+        }
+    }
+    __syncthreads();
+    const __nv_bfloat16* kp = reinterpret_cast<const __nv_bfloat16*>(A.kpool);
+    const __nv_bfloat16* vp = reinterpret_cast<const __nv_bfloat16*>(A.vpool);
+    auto dot8 = [](const uint4& r, const float* qq) {
+        const uint32_t w4[4] = {r.x, r.y, r.z, r.w};
+        float acc = 0.f;
+#pragma unroll
+        for (int x = 0; x < 4; ++x) {
+            const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w4[x]));
+            acc = fmaf(qq[2 * x], f.x, fmaf(qq[2 * x + 1], f.y, acc));
+        }
+        return acc;
+    };
+    // logits
+#pragma unroll
+    for (int jj = 0; jj < JMAX; ++jj) {
+        const int j = warp + jj * nw;
+        if (j >= nj) break;
+        const int h = j * HPL + hsub;
+        for (int eb = 0; eb < ne; eb += 8) {
+            uint4 r[8];
+#pragma unroll
+            for (int x = 0; x < 8; ++x)
+                if (eb + x < ne) r[x] = *reinterpret_cast<const uint4*>(kp + ((bS + ss[eb + x]) * H + h) * D + dch);
+#pragma unroll
+            for (int x = 0; x < 8; ++x) {
+                float d = eb + x < ne ? dot8(r[x], qv[jj]) : 0.f;
+#pragma unroll
+                for (int o = LPH / 2; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+                if ((lane % LPH) == 0 && eb + x < ne) sp[h * kSlotsPerCta + eb + x] = d * skg[eb + x];
+            }
+        }
+    }
+    __syncthreads();
+    for (int h = warp; h < H; h += nw) {
+        float m = -INFINITY;
+        for (int e = lane; e < ne; e += 32) m = fmaxf(m, sp[h * kSlotsPerCta + e]);
+        m = warp_max(m);
+        float l = 0.f;
+        for (int e = lane; e < ne; e += 32) {
+            const float pe = expf(sp[h * kSlotsPerCta + e] - m);
+            sp[h * kSlotsPerCta + e] = pe * svg[e];  // value-gated weight; l keeps the ungated sum
+            l += pe;
+        }
+        l = warp_sum(l);
+        if (lane == 0) {
+            const int64_t o = ((int64_t)b * nsplit + chunk) * H + h;
+            pm[o] = ne > 0 ? m : -INFINITY;
+            pl[o] = l;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int jj = 0; jj < JMAX; ++jj) {
+        const int j = warp + jj * nw;
+        if (j >= nj) break;
+        const int h = j * HPL + hsub;
+        float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        for (int eb = 0; eb < ne; eb += 8) {
+            uint4 r[8];
+#pragma unroll
+            for (int x = 0; x < 8; ++x)
+                if (eb + x < ne) r[x] = *reinterpret_cast<const uint4*>(vp + ((bS + ss[eb + x]) * H + h) * D + dch);
+#pragma unroll
+            for (int x = 0; x < 8; ++x) {
+                if (eb + x >= ne) break;
+                const float w = sp[h * kSlotsPerCta + eb + x];
+                const uint32_t w4[4] = {r[x].x, r[x].y, r[x].z, r[x].w};
+#pragma unroll
+                for (int y = 0; y < 4; ++y) {
+                    const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w4[y]));
+                    acc[2 * y] = fmaf(w, f.x, acc[2 * y]);
+                    acc[2 * y + 1] = fmaf(w, f.y, acc[2 * y + 1]);
+                }
+            }
+        }
+        float* out = po + (((int64_t)b * nsplit + chunk) * H + h) * D + dch;
+        *reinterpret_cast<float4*>(out) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+        *reinterpret_cast<float4*>(out + 4) = make_float4(acc[4], acc[5], acc[6], acc[7]);
+    }
+}
+
 template <class T>
 __global__ void k_cache_combine(const float* __restrict__ po, const float* __restrict__ pm,
                                 const float* __restrict__ pl, const int* __restrict__ att_n, int H, int p,
@@ -835,7 +973,19 @@ static void cache_attend(skb_cache* c, const void* q, void* o, cudaStream_t st) 
         kern<<<g, kAttnThreads, smem, st>>>(c->A, static_cast<const T*>(q), H, p, scale, c->po, c->pm, c->pl,
                                             c->nsplit);
     };
-    if (c->vec == 4) launch(k_cache_attn<T, 4>);
+    constexpr bool kBf16 = std::is_same<T, __nv_bfloat16>::value;
+    const bool fast = kBf16 && (p == 128 || p == 64) && (H % (256 / p)) == 0 && H / (256 / p) <= 4 * 8;
+    if (fast) {
+        const size_t fsmem = (size_t)H * kSlotsPerCta * 4 + kSlotsPerCta * 12;
+        auto run = [&](auto kern) {
+            if (fsmem > 48 * 1024)
+                SKB_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem));
+            kern<<<g, kAttnThreads, fsmem, st>>>(c->A, reinterpret_cast<const __nv_bfloat16*>(q), H, scale, c->po,
+                                                 c->pm, c->pl, c->nsplit);
+        };
+        if (p == 128) run(k_cache_attn_bf16<128>);
+        else run(k_cache_attn_bf16<64>);
+    } else if (c->vec == 4) launch(k_cache_attn<T, 4>);
     else if (c->vec == 2) launch(k_cache_attn<T, 2>);
     else launch(k_cache_attn<T, 1>);
     SKB_CHECK_LAUNCH();
