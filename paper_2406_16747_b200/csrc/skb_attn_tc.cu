@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(const __grid_constant__ 
                 mbar_arrive(bar);
                 if (ptid == 0) mbar_arrive(bar);
             } else if (jt < n_sel) {
-                keys.issue(dst, src, b, h, a.L, a.H, pw, lane);
+                keys.template issue<false>(dst, src, b, h, a.L, a.H, pw, lane);  // union keys are valid
                 cp_async_arrive_noinc(bar);
                 if (ptid == 0) mbar_arrive(bar);
             } else {

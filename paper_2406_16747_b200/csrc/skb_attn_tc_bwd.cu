@@ -546,8 +546,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(const __grid_constant
             cp_async_arrive_noinc(&bars[QB_MFULL + s]);
             if (jt >= kNS) mbar_wait(&bars[QB_KVEMPTY + s], ((jt - kNS) / kNS) & 1);
             if (jt < n_sel) {
-                kcur.issue(sbase + SM::kK + s * SM::kKT, a.k, b, h, a.L, a.H, pw, lane);
-                kcur.issue(sbase + SM::kV + s * SM::kKT, a.v, b, h, a.L, a.H, pw, lane);
+                kcur.issue<false>(sbase + SM::kK + s * SM::kKT, a.k, b, h, a.L, a.H, pw, lane);
+                kcur.issue<false>(sbase + SM::kV + s * SM::kKT, a.v, b, h, a.L, a.H, pw, lane);
                 cp_async_arrive_noinc(&bars[QB_KVFULL + s]);
                 if (ptid == 0) mbar_arrive(&bars[QB_KVFULL + s]);
                 if (jt + 1 < n_sel) kcur.fetch(pw, lane, [&](int r) { return __ldg(list + (jt + 1) * 64 + r); });

@@ -442,19 +442,22 @@ k_union_meta(const int* __restrict__ leave1, const float* __restrict__ uf, const
         const int idx = t * 128 + threadIdx.x;
         int key = -1, lv = 0;
         float u = 0.f;
-        if (idx < cnt) {
+        const bool real = idx < cnt;
+        if (real) {
             key = qb_list[row * cap + idx];
             lv = leave1[bl + key];
             u = uf[bl + key];
         } else {
-            qb_list[row * cap + idx] = -1;
+            // padding re-reads the block's first key (a valid row, so the
+            // gathers need no bounds check); ext = 0 masks it everywhere
+            qb_list[row * cap + idx] = qb_list[row * cap];
         }
-        // the forward's interval mask in one unsigned compare:
+        // the interval mask in one unsigned compare:
         // valid(t) <=> (unsigned)(t - key) < (unsigned)(leave - key); padding: 0
-        qb_leave[row * cap + idx] = key >= 0 ? lv - key : 0;
+        qb_leave[row * cap + idx] = real ? lv - key : 0;
         qb_uf[row * cap + idx] = u;
-        const bool ok = key >= 0 && key <= t_lo && lv > t_hi;
-        const bool sat = key < 0 || u >= tau_hi + 1.f;
+        const bool ok = real && key <= t_lo && lv > t_hi;
+        const bool sat = !real || u >= tau_hi + 1.f;
         const int all_ok = __syncthreads_and(ok);
         const int all_sat = __syncthreads_and(sat);
         if (threadIdx.x == 0) qb_flags[(row * (cap / 128) + t) * 4] = (all_ok ? 1 : 0) | (all_sat ? 2 : 0);

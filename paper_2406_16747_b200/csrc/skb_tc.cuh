@@ -354,11 +354,15 @@ struct RowKeys {
             k[it] = g < kGroups ? keyfn(g * kRowsPerIter + sub) : -1;
         }
     }
-    // cp.async the rows (key < 0 or >= L: zero fill) into the 128B-swizzled tile
+    // cp.async the rows into the 128B-swizzled tile. CHECKED: keys < 0 or
+    // >= L are zero-filled; unchecked callers guarantee valid keys.
+    template <bool CHECKED = true>
     __device__ __forceinline__ void issue(uint32_t dst, const __nv_bfloat16* base, int b, int h, int L, int H, int pw,
                                           int lane) const {
         const int sub = lane / kChunks, ch = lane % kChunks;
-        const __nv_bfloat16* basec = base + ((int64_t)b * L * H + h) * D + ch * 8;
+        // one IMAD.WIDE per row: src = basec + key * row_bytes
+        const uint64_t basec = reinterpret_cast<uint64_t>(base + ((int64_t)b * L * H + h) * D) + (uint64_t)(ch * 16);
+        const uint32_t row_bytes = (uint32_t)(H * D * 2);
         const uint32_t dcol = (uint32_t)((ch >> 3) * (R * 128));
 #pragma unroll
         for (int it = 0; it < kIters; ++it) {
@@ -368,10 +372,11 @@ struct RowKeys {
 #if defined(SKB_EXP) && SKB_EXP == 2
                 const bool ok = false;  // experiment: no gathers (zero fill)
 #else
-                const bool ok = (unsigned)k[it] < (unsigned)L;
+                const bool ok = !CHECKED || (unsigned)k[it] < (unsigned)L;
 #endif
+                const uint32_t key = (CHECKED && !ok) ? 0u : (uint32_t)k[it];
                 cp_async16(dst + dcol + r * 128 + (((ch & 7) ^ (r & 7)) << 4),
-                           basec + (int64_t)(ok ? k[it] : 0) * (H * D), ok);
+                           reinterpret_cast<const void*>(basec + (uint64_t)key * row_bytes), ok);
             }
         }
     }
