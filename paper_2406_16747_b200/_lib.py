@@ -118,8 +118,9 @@ def load():
                     f"{LIB_PATH} is missing: build it with `make -C {HERE}` "
                     "(or __graft_entry__.build()); the SparseK path has no CPU fallback")
             lib = C.CDLL(LIB_PATH)
-            if hasattr(lib, "skb_debug_trace"):  # -DSKB_TRACE experiment builds
-                lib.skb_debug_trace.argtypes = [C.c_void_p, C.c_int]
+            for dbg in ("skb_debug_trace", "skb_debug_trace_bwd"):  # -DSKB_TRACE experiment builds
+                if hasattr(lib, dbg):
+                    getattr(lib, dbg).argtypes = [C.c_void_p, C.c_int]
             for name, (args, res) in _SIGS.items():
                 fn = getattr(lib, name)
                 fn.argtypes = args

@@ -21,6 +21,22 @@
 #include "skb_tc.cuh"
 #include "skb_tmap.h"
 
+#ifdef SKB_TRACE
+__device__ unsigned long long g_skb_trace_bwd[4096];
+#define SKB_TRB(role, jt, ev)                                                                        \
+    do {                                                                                              \
+        if (blockIdx.x == 100 && blockIdx.y == 0 && blockIdx.z == 0 && (jt) < 32)                  \
+            g_skb_trace_bwd[(role) * 512 + (jt) * 16 + (ev)] = clock64();                            \
+    } while (0)
+extern "C" int skb_debug_trace_bwd(unsigned long long* out, int n) {
+    return (int)cudaMemcpyFromSymbol(out, g_skb_trace_bwd, sizeof(unsigned long long) * (n < 4096 ? n : 4096));
+}
+#else
+#define SKB_TRB(role, jt, ev) \
+    do {                      \
+    } while (0)
+#endif
+
 namespace skb {
 
 namespace {
@@ -464,12 +480,14 @@ struct QSmem {
     static constexpr int kMeta = kV + kNS * kKT;    // [kNS][key|ext|uf][64] x 4 B
     static constexpr int kFlags = kMeta + kNS * 3 * 64 * 4;  // [kNS] x 16 B
     static constexpr int kBar = kFlags + kNS * 16;
-    static constexpr int kNumBars = 20;
+    static constexpr int kNumBars = 23;
     static constexpr int kTmemSlot = kBar + kNumBars * 8;
     static constexpr int kAlloc = kTmemSlot + 16 + 1024;
 };
+// S/dP live in a 3-deep TMEM ring (S: columns 0-191, dP: 192-383, dQ: 384-511)
+constexpr int kSS = 3;
 enum { QB_QFULL = 0, QB_KVFULL = 1, QB_KVEMPTY = 4, QB_MFULL = 7, QB_MEMPTY = 10, QB_SFULL = 13,
-       QB_SEMPTY = 15, QB_DSFULL = 17, QB_DQDONE = 19 };  // 20 barriers
+       QB_SEMPTY = 16, QB_DSFULL = 19, QB_DQDONE = 22 };  // 23 barriers
 
 template <int D, bool KEY_SOFT>
 __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(const __grid_constant__ BwdArgs a) {
@@ -502,7 +520,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(const __grid_constant
             mbar_init(&bars[QB_MFULL + s], kProducers);
             mbar_init(&bars[QB_MEMPTY + s], kMath);
         }
-        for (int s = 0; s < 2; ++s) {
+        for (int s = 0; s < kSS; ++s) {
             mbar_init(&bars[QB_SFULL + s], 1);
             mbar_init(&bars[QB_SEMPTY + s], kMath);
             mbar_init(&bars[QB_DSFULL + s], kMath);
@@ -515,7 +533,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(const __grid_constant
     __syncthreads();
     tc_after_sync();
     const uint32_t tmem = *tmem_slot;
-    const uint32_t tS = tmem, tP = tmem + 128, tDQ = tmem + 256;  // S[2], dP/dS[2] (64 cols each), dQ
+    const uint32_t tS = tmem, tP = tmem + 64 * kSS, tDQ = tmem + 128 * kSS;  // S[3], dP/dS[3] (64 cols each), dQ
 
     if (warp >= kProdWarp0 && warp < kMmaWarp) {
         constexpr int kAtoms = D / 64;
@@ -535,6 +553,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(const __grid_constant
         const int* msrc = ma == 0 ? a.qb_list : ma == 1 ? a.qb_leave : reinterpret_cast<const int*>(a.qb_uf);
         for (int jt = 0; jt < n; ++jt) {
             const int s = jt % kNS;
+            if (ptid == 0) SKB_TRB(2, jt, 0);
             if (jt >= kNS) mbar_wait(&bars[QB_MEMPTY + s], ((jt - kNS) / kNS) & 1);
             if (jt < n_sel) {
                 if (ptid < 48)
@@ -544,7 +563,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(const __grid_constant
                     cp_async16(smem_u32(tflags + s * 4), a.qb_flags + (qrow * (a.qb_cap / 128) + (jt >> 1)) * 4, true);
             }
             cp_async_arrive_noinc(&bars[QB_MFULL + s]);
+            if (ptid == 0) SKB_TRB(2, jt, 1);
             if (jt >= kNS) mbar_wait(&bars[QB_KVEMPTY + s], ((jt - kNS) / kNS) & 1);
+            if (ptid == 0) SKB_TRB(2, jt, 2);
             if (jt < n_sel) {
                 kcur.issue<false>(sbase + SM::kK + s * SM::kKT, a.k, b, h, a.L, a.H, pw, lane);
                 kcur.issue<false>(sbase + SM::kV + s * SM::kKT, a.v, b, h, a.L, a.H, pw, lane);
@@ -572,8 +593,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(const __grid_constant
             constexpr uint32_t id_dq = umma_idesc(128, D, false, true);
             mbar_wait(&bars[QB_QFULL], 0);
             auto dq = [&](int j) {
-                const int s = j & 1, ks = j % kNS;
-                mbar_wait(&bars[QB_DSFULL + s], (j >> 1) & 1);
+                const int s = j % kSS, ks = j % kNS;
+                mbar_wait(&bars[QB_DSFULL + s], (j / kSS) & 1);
+                SKB_TRB(3, j, 2);
                 tc_after_sync();
                 const uint32_t kb = sbase + SM::kK + ks * SM::kKT;
                 // dS of key half hf (32 keys) lives in TMEM columns [hf*32, hf*32+16) of dP(s)
@@ -584,10 +606,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(const __grid_constant
                 umma_commit(&bars[QB_KVEMPTY + ks]);
             };
             for (int jt = 0; jt < n; ++jt) {
-                const int s = jt & 1, ks = jt % kNS;
+                const int s = jt % kSS, ks = jt % kNS;
+                SKB_TRB(3, jt, 8);
                 mbar_wait(&bars[QB_KVFULL + ks], (jt / kNS) & 1);
+                SKB_TRB(3, jt, 0);
                 fence_proxy_async();  // cp.async (generic proxy) rows -> tensor core reads
-                if (jt >= 2) mbar_wait(&bars[QB_SEMPTY + s], ((jt - 2) >> 1) & 1);
+                if (jt >= kSS) mbar_wait(&bars[QB_SEMPTY + s], ((jt - kSS) / kSS) & 1);
                 tc_after_sync();
                 const uint32_t kb = sbase + SM::kK + ks * SM::kKT, vb = sbase + SM::kV + ks * SM::kKT;
 #pragma unroll
@@ -598,6 +622,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(const __grid_constant
                              kk > 0 ? 1u : 0u);
                 }
                 umma_commit(&bars[QB_SFULL + s]);
+                SKB_TRB(3, jt, 1);
                 if (jt >= 1) dq(jt - 1);
             }
             dq(n - 1);
@@ -620,11 +645,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(const __grid_constant
         const float2 sl22 = make_float2(sl2, sl2), nl2 = make_float2(nlse2, nlse2), ndl = make_float2(-dlt, -dlt);
         float rsum = 0.f;
         for (int jt = 0; jt < n; ++jt) {
-            const int s = jt & 1;
+            const int s = jt % kSS;
             const bool is_sel = jt < n_sel;
             const int ks = jt % kNS;
-            mbar_wait(&bars[QB_SFULL + s], (jt >> 1) & 1);
+            if (lane == 0 && (warp & 3) == 0) SKB_TRB(hf, jt, 9);
+            mbar_wait(&bars[QB_SFULL + s], (jt / kSS) & 1);
             if (is_sel) mbar_wait(&bars[QB_MFULL + ks], (jt / kNS) & 1);
+            if (lane == 0 && (warp & 3) == 0) SKB_TRB(hf, jt, 0);
             tc_after_sync();
             float sv[32], dp[32];
             tmem_ld32(tS + lane_off + s * 64 + hf * 32, sv);
@@ -701,6 +728,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(const __grid_constant
                 tmem_wait_st();
             }
             tc_before_sync();
+            if (lane == 0 && (warp & 3) == 0) SKB_TRB(hf, jt, 4);
             mbar_arrive(&bars[QB_MEMPTY + ks]);
             mbar_arrive(&bars[QB_DSFULL + s]);
         }
