@@ -460,34 +460,33 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_tc(const __grid_consta
 }
 
 // ------------------------------------------------------------------ dQ
-// Query-major over 64-key tiles [selected union | window band]. Per tile:
-// S = Q K^T and dP = dO V^T (tcgen05, M=128, N=64) in TMEM; two math
+// Query-major over 64-key tiles [selected union | window band]. Q and dO
+// live in TMEM for the whole CTA (loaded once by the math warps), so all
+// three MMAs are TS-MMAs that read only the K/V tile from shared memory:
+// S = Q K^T and dP = dO V^T (M=128, N=64) into a TMEM ring; two math
 // warpgroups (32 keys each) form dS = P (wv dP - delta) * kappa and write it
-// back into TMEM as bf16 over their consumed dP columns: the A operand of the
-// TS-MMA dQ += dS K. Producers: Q/dO and the window band by 3-D TMA, the
-// selected rows by cp.async gathers with keys fetched one tile ahead, the
-// per-key metadata by cp.async from skb_select's precomputed block arrays.
-constexpr int kNS = 3;  // K/V ring depth of the dQ kernel
+// back into TMEM as bf16 over their consumed dP columns: the A operand of
+// dQ += dS K. Producers: the window band by 3-D TMA, the selected rows by
+// cp.async gathers with keys fetched one tile ahead, the per-key metadata by
+// cp.async from skb_select's precomputed block arrays.
+constexpr int kNS = 4;  // K/V ring depth of the dQ kernel
 
 template <int D>
 struct QSmem {
-    static constexpr int kQT = 128 * D * 2;  // 128-query tile
     static constexpr int kKT = 64 * D * 2;   // 64-key tile
-    static constexpr int kQ = 0;
-    static constexpr int kDO = kQ + kQT;
-    static constexpr int kK = kDO + kQT;            // [kNS]
+    static constexpr int kK = 0;                    // [kNS]
     static constexpr int kV = kK + kNS * kKT;       // [kNS]
     static constexpr int kMeta = kV + kNS * kKT;    // [kNS][key|ext|uf][64] x 4 B
     static constexpr int kFlags = kMeta + kNS * 3 * 64 * 4;  // [kNS] x 16 B
     static constexpr int kBar = kFlags + kNS * 16;
-    static constexpr int kNumBars = 23;
+    static constexpr int kNumBars = 26;
     static constexpr int kTmemSlot = kBar + kNumBars * 8;
     static constexpr int kAlloc = kTmemSlot + 16 + 1024;
 };
-// S/dP live in a 3-deep TMEM ring (S: columns 0-191, dP: 192-383, dQ: 384-511)
-constexpr int kSS = 3;
-enum { QB_QFULL = 0, QB_KVFULL = 1, QB_KVEMPTY = 4, QB_MFULL = 7, QB_MEMPTY = 10, QB_SFULL = 13,
-       QB_SEMPTY = 16, QB_DSFULL = 19, QB_DQDONE = 22 };  // 23 barriers
+// TMEM: Q (bf16, 64 columns), dO (64), S[2] (64 each), dP/dS[2], dQ (128)
+constexpr int kSS = 2;
+enum { QB_QFULL = 0, QB_KVFULL = 1, QB_KVEMPTY = 5, QB_MFULL = 9, QB_MEMPTY = 13, QB_SFULL = 17,
+       QB_SEMPTY = 19, QB_DSFULL = 21, QB_DQDONE = 23 };  // 24 barriers
 
 template <int D, bool KEY_SOFT>
 __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(const __grid_constant__ BwdArgs a) {
@@ -513,7 +512,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(const __grid_constant
     const int* list = a.qb_list + qrow * a.qb_cap;
 
     if (threadIdx.x == 0) {
-        mbar_init(&bars[QB_QFULL], 1);
+        mbar_init(&bars[QB_QFULL], kMath);
         for (int s = 0; s < kNS; ++s) {
             mbar_init(&bars[QB_KVFULL + s], kProducers + 1);
             mbar_init(&bars[QB_KVEMPTY + s], 1);
@@ -533,20 +532,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(const __grid_constant
     __syncthreads();
     tc_after_sync();
     const uint32_t tmem = *tmem_slot;
-    const uint32_t tS = tmem, tP = tmem + 64 * kSS, tDQ = tmem + 128 * kSS;  // S[3], dP/dS[3] (64 cols each), dQ
+    const uint32_t tQ = tmem, tDO = tmem + 64, tS = tmem + 128, tP = tmem + 128 + 64 * kSS, tDQ = tmem + 384;
 
     if (warp >= kProdWarp0 && warp < kMmaWarp) {
         constexpr int kAtoms = D / 64;
         const int pw = warp - kProdWarp0, ptid = threadIdx.x - kProdWarp0 * 32;
-        if (ptid == 0) {
-            mbar_expect_tx(&bars[QB_QFULL], 2 * 128 * D * 2);
-#pragma unroll
-            for (int at = 0; at < kAtoms; ++at) {
-                tma_load_3d(sbase + SM::kQ + at * 128 * 128, &a.tm_q128, h * D + at * 64, i0, b, &bars[QB_QFULL]);
-                tma_load_3d(sbase + SM::kDO + at * 128 * 128, &a.tm_do128, h * D + at * 64, i0, b,
-                            &bars[QB_QFULL]);
-            }
-        }
         RowKeys<D, 64> kcur;
         if (n_sel > 0) kcur.fetch(pw, lane, [&](int r) { return __ldg(list + r); });
         const int ma = ptid >> 4, mc = ptid & 15;  // metadata: 48 threads, array x 16-byte chunk
@@ -592,6 +582,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(const __grid_constant
             constexpr uint32_t id_s = umma_idesc(128, 64, false, false);
             constexpr uint32_t id_dq = umma_idesc(128, D, false, true);
             mbar_wait(&bars[QB_QFULL], 0);
+            tc_after_sync();
             auto dq = [&](int j) {
                 const int s = j % kSS, ks = j % kNS;
                 mbar_wait(&bars[QB_DSFULL + s], (j / kSS) & 1);
@@ -616,10 +607,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(const __grid_constant
                 const uint32_t kb = sbase + SM::kK + ks * SM::kKT, vb = sbase + SM::kV + ks * SM::kKT;
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk) {
-                    umma_f16(tS + s * 64, desc_kmajor(sbase + SM::kQ, 128, kk), desc_kmajor(kb, 64, kk), id_s,
-                             kk > 0 ? 1u : 0u);
-                    umma_f16(tP + s * 64, desc_kmajor(sbase + SM::kDO, 128, kk), desc_kmajor(vb, 64, kk), id_s,
-                             kk > 0 ? 1u : 0u);
+                    umma_f16_ts(tS + s * 64, tQ + kk * 8, desc_kmajor(kb, 64, kk), id_s, kk > 0 ? 1u : 0u);
+                    umma_f16_ts(tP + s * 64, tDO + kk * 8, desc_kmajor(vb, 64, kk), id_s, kk > 0 ? 1u : 0u);
                 }
                 umma_commit(&bars[QB_SFULL + s]);
                 SKB_TRB(3, jt, 1);
@@ -643,6 +632,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(const __grid_constant
         const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
         const float sl2 = a.scale_log2;
         const float2 sl22 = make_float2(sl2, sl2), nl2 = make_float2(nlse2, nlse2), ndl = make_float2(-dlt, -dlt);
+        {  // this row of Q (warpgroup 0) or dO (warpgroup 1) -> TMEM: the A operand of S / dP
+            const __nv_bfloat16* src = (hf == 0 ? a.q : a.dout) + ((bl + (i < a.L ? i : 0)) * a.H + h) * D;
+            uint32_t w[D / 2];
+#pragma unroll
+            for (int c = 0; c < D / 8; ++c) {
+                uint4 x = make_uint4(0u, 0u, 0u, 0u);
+                if (i < a.L) x = *reinterpret_cast<const uint4*>(src + c * 8);
+                w[4 * c] = x.x, w[4 * c + 1] = x.y, w[4 * c + 2] = x.z, w[4 * c + 3] = x.w;
+            }
+            const uint32_t dst = (hf == 0 ? tQ : tDO) + lane_off;
+#pragma unroll
+            for (int c = 0; c < D / 64; ++c) tmem_st32u(dst + c * 32, w + c * 32);
+            tmem_wait_st();
+            tc_before_sync();
+            mbar_arrive(&bars[QB_QFULL]);
+        }
         float rsum = 0.f;
         for (int jt = 0; jt < n; ++jt) {
             const int s = jt % kSS;

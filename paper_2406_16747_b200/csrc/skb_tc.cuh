@@ -223,6 +223,17 @@ __device__ __forceinline__ void umma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, ui
         "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, {%5, %6, %7, %8}, p;\n\t}" ::"r"(d_tmem),
         "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(0u), "r"(0u), "r"(0u), "r"(0u));
 }
+// 32 lanes x 32 columns of raw 32-bit words (e.g. a bf16 row as an A operand).
+__device__ __forceinline__ void tmem_st32u(uint32_t taddr, const uint32_t* v) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+        "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+        "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]),
+        "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]),
+        "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31]));
+}
 // 32 lanes x 16 columns of packed bf16x2 (the A-operand layout above).
 __device__ __forceinline__ void tmem_st16u(uint32_t taddr, const uint32_t* v) {
     asm volatile(
@@ -239,15 +250,19 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
                  : "memory");
 }
 
+// The start-address field of a descriptor is (addr >> 4) & 0x3FFF and shared
+// memory stays below 2^18 bytes, so desc(base + off) = desc(base) + off / 16:
+// the descriptor of a tile is built once and each K slice adds an immediate
+// (keeps the single-thread MMA issue loop short).
 // K-major operand with R rows (M or N) and K = 64*katoms columns: descriptor for
 // the 16-wide K slice kk (0 .. 4*katoms-1).
 __device__ __forceinline__ uint64_t desc_kmajor(uint32_t base, int R, int kk) {
-    return umma_desc(base + (uint32_t)((kk >> 2) * R * 128 + (kk & 3) * 32), 16, 1024);
+    return umma_desc(base, 16, 1024) + (uint64_t)(((kk >> 2) * R * 128 + (kk & 3) * 32) >> 4);
 }
 // MN-major operand stored as K rows x (64*natoms) columns (R = number of K
 // rows in the tile): descriptor for the 16-deep K slice kk.
 __device__ __forceinline__ uint64_t desc_mnmajor(uint32_t base, int R, int kk) {
-    return umma_desc(base + (uint32_t)(kk * 16 * 128), (uint32_t)(R * 128), 1024);
+    return umma_desc(base, (uint32_t)(R * 128), 1024) + (uint64_t)((kk * 16 * 128) >> 4);
 }
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
