@@ -460,33 +460,31 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_tc(const __grid_consta
 }
 
 // ------------------------------------------------------------------ dQ
-// Query-major over 64-key tiles [selected union | window band]. Q and dO
-// live in TMEM for the whole CTA (loaded once by the math warps), so all
-// three MMAs are TS-MMAs that read only the K/V tile from shared memory:
-// S = Q K^T and dP = dO V^T (M=128, N=64) into a TMEM ring; two math
-// warpgroups (32 keys each) form dS = P (wv dP - delta) * kappa and write it
-// back into TMEM as bf16 over their consumed dP columns: the A operand of
-// dQ += dS K. Producers: the window band by 3-D TMA, the selected rows by
-// cp.async gathers with keys fetched one tile ahead, the per-key metadata by
-// cp.async from skb_select's precomputed block arrays.
-constexpr int kNS = 4;  // K/V ring depth of the dQ kernel
+// Query-major over 128-key tiles [selected union | window band] (N=128 MMAs:
+// narrow tiles pay a high per-instruction cost). TMEM: Q (bf16 A operand,
+// loaded once by the math warps), dS (bf16), S and dP (fp32, 128 columns
+// each), dQ. Per tile: S = Q K^T (TS) and dP = dO V^T (SS, dO resident in
+// shared memory); the S/dP of tile j+1 run while the math warpgroups (64 keys
+// each) form dS_j = P (wv dP - delta) * kappa; dQ += dS_j K (TS). Producers:
+// dO and the window band by 3-D TMA, selected rows by cp.async gathers with
+// keys fetched one tile ahead, per-key metadata from skb_select's block arrays.
+constexpr int kNS = 2;  // K/V ring depth of the dQ kernel
 
 template <int D>
 struct QSmem {
-    static constexpr int kKT = 64 * D * 2;   // 64-key tile
-    static constexpr int kK = 0;                    // [kNS]
-    static constexpr int kV = kK + kNS * kKT;       // [kNS]
-    static constexpr int kMeta = kV + kNS * kKT;    // [kNS][key|ext|uf][64] x 4 B
-    static constexpr int kFlags = kMeta + kNS * 3 * 64 * 4;  // [kNS] x 16 B
+    static constexpr int kKT = 128 * D * 2;  // 128-key tile
+    static constexpr int kDO = 0;            // dO tile (128 queries)
+    static constexpr int kK = kDO + kKT;     // [kNS]
+    static constexpr int kV = kK + kNS * kKT;  // [kNS]
+    static constexpr int kMeta = kV + kNS * kKT;  // [kNS][key|ext|uf][128] x 4 B
+    static constexpr int kFlags = kMeta + kNS * 3 * 128 * 4;  // [kNS] x 16 B
     static constexpr int kBar = kFlags + kNS * 16;
-    static constexpr int kNumBars = 26;
+    static constexpr int kNumBars = 16;
     static constexpr int kTmemSlot = kBar + kNumBars * 8;
     static constexpr int kAlloc = kTmemSlot + 16 + 1024;
 };
-// TMEM: Q (bf16, 64 columns), dO (64), S[2] (64 each), dP/dS[2], dQ (128)
-constexpr int kSS = 2;
-enum { QB_QFULL = 0, QB_KVFULL = 1, QB_KVEMPTY = 5, QB_MFULL = 9, QB_MEMPTY = 13, QB_SFULL = 17,
-       QB_SEMPTY = 19, QB_DSFULL = 21, QB_DQDONE = 23 };  // 24 barriers
+enum { QB_QFULL = 0, QB_DOFULL = 1, QB_KVFULL = 2, QB_KVEMPTY = 4, QB_MFULL = 6, QB_MEMPTY = 8, QB_SFULL = 10,
+       QB_SEMPTY = 11, QB_DSFULL = 12, QB_DSEMPTY = 13, QB_DQDONE = 14 };  // 15 barriers
 
 template <int D, bool KEY_SOFT>
 __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(const __grid_constant__ BwdArgs a) {
@@ -505,25 +503,25 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(const __grid_constant
     const int64_t qrow = (int64_t)b * a.nqb + qb;
     const int i0 = qb * 128;
     const int cnt = (a.R1 > 0) ? a.qb_count[qrow] : 0;
-    const int n_sel = (cnt + 63) / 64;
-    const int n_win = (a.w + 127 + 63) / 64;
+    const int n_sel = (cnt + 127) / 128;
+    const int n_win = (a.w + 127 + 127) / 128;
     const int n = n_sel + n_win;
     const int jw0 = i0 - a.w + 1;
     const int* list = a.qb_list + qrow * a.qb_cap;
 
     if (threadIdx.x == 0) {
-        mbar_init(&bars[QB_QFULL], kMath);
+        mbar_init(&bars[QB_QFULL], kMath / 2);
+        mbar_init(&bars[QB_DOFULL], 1);
         for (int s = 0; s < kNS; ++s) {
             mbar_init(&bars[QB_KVFULL + s], kProducers + 1);
             mbar_init(&bars[QB_KVEMPTY + s], 1);
             mbar_init(&bars[QB_MFULL + s], kProducers);
             mbar_init(&bars[QB_MEMPTY + s], kMath);
         }
-        for (int s = 0; s < kSS; ++s) {
-            mbar_init(&bars[QB_SFULL + s], 1);
-            mbar_init(&bars[QB_SEMPTY + s], kMath);
-            mbar_init(&bars[QB_DSFULL + s], kMath);
-        }
+        mbar_init(&bars[QB_SFULL], 1);
+        mbar_init(&bars[QB_SEMPTY], kMath);
+        mbar_init(&bars[QB_DSFULL], kMath);
+        mbar_init(&bars[QB_DSEMPTY], 1);
         mbar_init(&bars[QB_DQDONE], 1);
         mbar_fence_init();
     }
@@ -532,25 +530,30 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(const __grid_constant
     __syncthreads();
     tc_after_sync();
     const uint32_t tmem = *tmem_slot;
-    const uint32_t tQ = tmem, tDO = tmem + 64, tS = tmem + 128, tP = tmem + 128 + 64 * kSS, tDQ = tmem + 384;
+    const uint32_t tQ = tmem, tDS = tmem + 64, tS = tmem + 128, tP = tmem + 256, tDQ = tmem + 384;
 
     if (warp >= kProdWarp0 && warp < kMmaWarp) {
         constexpr int kAtoms = D / 64;
         const int pw = warp - kProdWarp0, ptid = threadIdx.x - kProdWarp0 * 32;
-        RowKeys<D, 64> kcur;
+        if (ptid == 0) {
+            mbar_expect_tx(&bars[QB_DOFULL], 128 * D * 2);
+#pragma unroll
+            for (int at = 0; at < kAtoms; ++at)
+                tma_load_3d(sbase + SM::kDO + at * 128 * 128, &a.tm_do128, h * D + at * 64, i0, b, &bars[QB_DOFULL]);
+        }
+        RowKeys<D, 128> kcur;
         if (n_sel > 0) kcur.fetch(pw, lane, [&](int r) { return __ldg(list + r); });
-        const int ma = ptid >> 4, mc = ptid & 15;  // metadata: 48 threads, array x 16-byte chunk
+        const int ma = ptid >> 5, mc = ptid & 31;  // metadata: array x 16-byte chunk (96 threads)
         const int* msrc = ma == 0 ? a.qb_list : ma == 1 ? a.qb_leave : reinterpret_cast<const int*>(a.qb_uf);
         for (int jt = 0; jt < n; ++jt) {
             const int s = jt % kNS;
             if (ptid == 0) SKB_TRB(2, jt, 0);
             if (jt >= kNS) mbar_wait(&bars[QB_MEMPTY + s], ((jt - kNS) / kNS) & 1);
             if (jt < n_sel) {
-                if (ptid < 48)
-                    cp_async16(smem_u32(meta + (s * 3 + ma) * 64 + mc * 4), msrc + qrow * a.qb_cap + jt * 64 + mc * 4,
-                               true);
-                if (ptid == 48)
-                    cp_async16(smem_u32(tflags + s * 4), a.qb_flags + (qrow * (a.qb_cap / 128) + (jt >> 1)) * 4, true);
+                cp_async16(smem_u32(meta + (s * 3 + ma) * 128 + mc * 4), msrc + qrow * a.qb_cap + jt * 128 + mc * 4,
+                           true);
+                if (ptid == 0)
+                    cp_async16(smem_u32(tflags + s * 4), a.qb_flags + (qrow * (a.qb_cap / 128) + jt) * 4, true);
             }
             cp_async_arrive_noinc(&bars[QB_MFULL + s]);
             if (ptid == 0) SKB_TRB(2, jt, 1);
@@ -561,17 +564,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(const __grid_constant
                 kcur.issue<false>(sbase + SM::kV + s * SM::kKT, a.v, b, h, a.L, a.H, pw, lane);
                 cp_async_arrive_noinc(&bars[QB_KVFULL + s]);
                 if (ptid == 0) mbar_arrive(&bars[QB_KVFULL + s]);
-                if (jt + 1 < n_sel) kcur.fetch(pw, lane, [&](int r) { return __ldg(list + (jt + 1) * 64 + r); });
+                if (jt + 1 < n_sel) kcur.fetch(pw, lane, [&](int r) { return __ldg(list + (jt + 1) * 128 + r); });
             } else {
                 if (ptid == 0) {
-                    const int kb0 = jw0 + (jt - n_sel) * 64;
-                    mbar_expect_tx(&bars[QB_KVFULL + s], 2 * 64 * D * 2);
+                    const int kb0 = jw0 + (jt - n_sel) * 128;
+                    mbar_expect_tx(&bars[QB_KVFULL + s], 2 * 128 * D * 2);
 #pragma unroll
                     for (int at = 0; at < kAtoms; ++at) {
-                        tma_load_3d(sbase + SM::kK + s * SM::kKT + at * 64 * 128, &a.tm_k64, h * D + at * 64, kb0, b,
+                        tma_load_3d(sbase + SM::kK + s * SM::kKT + at * 128 * 128, &a.tm_k128, h * D + at * 64, kb0, b,
                                     &bars[QB_KVFULL + s]);
-                        tma_load_3d(sbase + SM::kV + s * SM::kKT + at * 64 * 128, &a.tm_v64, h * D + at * 64, kb0, b,
-                                    &bars[QB_KVFULL + s]);
+                        tma_load_3d(sbase + SM::kV + s * SM::kKT + at * 128 * 128, &a.tm_v128, h * D + at * 64, kb0,
+                                    b, &bars[QB_KVFULL + s]);
                     }
                 }
                 mbar_arrive(&bars[QB_KVFULL + s]);
@@ -579,47 +582,51 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(const __grid_constant
         }
     } else if (warp == kMmaWarp) {
         if (lane == 0) {
-            constexpr uint32_t id_s = umma_idesc(128, 64, false, false);
+            constexpr uint32_t id_s = umma_idesc(128, 128, false, false);
             constexpr uint32_t id_dq = umma_idesc(128, D, false, true);
             mbar_wait(&bars[QB_QFULL], 0);
+            mbar_wait(&bars[QB_DOFULL], 0);
             tc_after_sync();
-            auto dq = [&](int j) {
-                const int s = j % kSS, ks = j % kNS;
-                mbar_wait(&bars[QB_DSFULL + s], (j / kSS) & 1);
-                SKB_TRB(3, j, 2);
-                tc_after_sync();
-                const uint32_t kb = sbase + SM::kK + ks * SM::kKT;
-                // dS of key half hf (32 keys) lives in TMEM columns [hf*32, hf*32+16) of dP(s)
-#pragma unroll
-                for (int kk = 0; kk < 4; ++kk)
-                    umma_f16_ts(tDQ, tP + s * 64 + (kk >> 1) * 32 + (kk & 1) * 8, desc_mnmajor(kb, 64, kk), id_dq,
-                                (j > 0 || kk > 0) ? 1u : 0u);
-                umma_commit(&bars[QB_KVEMPTY + ks]);
-            };
-            for (int jt = 0; jt < n; ++jt) {
-                const int s = jt % kSS, ks = jt % kNS;
-                SKB_TRB(3, jt, 8);
-                mbar_wait(&bars[QB_KVFULL + ks], (jt / kNS) & 1);
-                SKB_TRB(3, jt, 0);
+            auto sdp = [&](int j) {  // S_j = Q K_j^T (TS), dP_j = dO V_j^T (SS)
+                const int ks = j % kNS;
+                SKB_TRB(3, j, 8);
+                mbar_wait(&bars[QB_KVFULL + ks], (j / kNS) & 1);
+                SKB_TRB(3, j, 0);
                 fence_proxy_async();  // cp.async (generic proxy) rows -> tensor core reads
-                if (jt >= kSS) mbar_wait(&bars[QB_SEMPTY + s], ((jt - kSS) / kSS) & 1);
+                if (j >= 1) mbar_wait(&bars[QB_SEMPTY], (j - 1) & 1);
                 tc_after_sync();
                 const uint32_t kb = sbase + SM::kK + ks * SM::kKT, vb = sbase + SM::kV + ks * SM::kKT;
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk) {
-                    umma_f16_ts(tS + s * 64, tQ + kk * 8, desc_kmajor(kb, 64, kk), id_s, kk > 0 ? 1u : 0u);
-                    umma_f16_ts(tP + s * 64, tDO + kk * 8, desc_kmajor(vb, 64, kk), id_s, kk > 0 ? 1u : 0u);
+                    umma_f16_ts(tS, tQ + kk * 8, desc_kmajor(kb, 128, kk), id_s, kk > 0 ? 1u : 0u);
+                    umma_f16(tP, desc_kmajor(sbase + SM::kDO, 128, kk), desc_kmajor(vb, 128, kk), id_s,
+                             kk > 0 ? 1u : 0u);
                 }
-                umma_commit(&bars[QB_SFULL + s]);
-                SKB_TRB(3, jt, 1);
-                if (jt >= 1) dq(jt - 1);
+                umma_commit(&bars[QB_SFULL]);
+                SKB_TRB(3, j, 1);
+            };
+            auto dq = [&](int j) {  // dQ += dS_j K_j (TS)
+                const int ks = j % kNS;
+                mbar_wait(&bars[QB_DSFULL], j & 1);
+                SKB_TRB(3, j, 2);
+                tc_after_sync();
+                const uint32_t kb = sbase + SM::kK + ks * SM::kKT;
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk)
+                    umma_f16_ts(tDQ, tDS + kk * 8, desc_mnmajor(kb, 128, kk), id_dq, (j > 0 || kk > 0) ? 1u : 0u);
+                umma_commit(&bars[QB_DSEMPTY]);
+                umma_commit(&bars[QB_KVEMPTY + ks]);
+            };
+            sdp(0);
+            for (int jt = 0; jt < n; ++jt) {
+                if (jt + 1 < n) sdp(jt + 1);  // overlaps the math on tile jt
+                dq(jt);
             }
-            dq(n - 1);
             umma_commit(&bars[QB_DQDONE]);
         }
         __syncwarp();
     } else if (warp < kProdWarp0) {
-        // query rows: two math warpgroups, each owning 32 of the 64 key columns
+        // query rows: two math warpgroups, each owning 64 of the 128 key columns
         const int hf = warp >> 2;
         const int r = ((warp & 3) << 5) | lane;
         const int i = i0 + r;
@@ -632,47 +639,48 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(const __grid_constant
         const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
         const float sl2 = a.scale_log2;
         const float2 sl22 = make_float2(sl2, sl2), nl2 = make_float2(nlse2, nlse2), ndl = make_float2(-dlt, -dlt);
-        {  // this row of Q (warpgroup 0) or dO (warpgroup 1) -> TMEM: the A operand of S / dP
-            const __nv_bfloat16* src = (hf == 0 ? a.q : a.dout) + ((bl + (i < a.L ? i : 0)) * a.H + h) * D;
-            uint32_t w[D / 2];
+        const int c0 = hf * 64;
+        if (hf == 0) {  // this row of Q -> TMEM: the A operand of S
+            const __nv_bfloat16* src = a.q + ((bl + (i < a.L ? i : 0)) * a.H + h) * D;
+            uint32_t wq[D / 2];
 #pragma unroll
             for (int c = 0; c < D / 8; ++c) {
                 uint4 x = make_uint4(0u, 0u, 0u, 0u);
                 if (i < a.L) x = *reinterpret_cast<const uint4*>(src + c * 8);
-                w[4 * c] = x.x, w[4 * c + 1] = x.y, w[4 * c + 2] = x.z, w[4 * c + 3] = x.w;
+                wq[4 * c] = x.x, wq[4 * c + 1] = x.y, wq[4 * c + 2] = x.z, wq[4 * c + 3] = x.w;
             }
-            const uint32_t dst = (hf == 0 ? tQ : tDO) + lane_off;
 #pragma unroll
-            for (int c = 0; c < D / 64; ++c) tmem_st32u(dst + c * 32, w + c * 32);
+            for (int c = 0; c < D / 64; ++c) tmem_st32u(tQ + lane_off + c * 32, wq + c * 32);
             tmem_wait_st();
             tc_before_sync();
             mbar_arrive(&bars[QB_QFULL]);
         }
         float rsum = 0.f;
         for (int jt = 0; jt < n; ++jt) {
-            const int s = jt % kSS;
             const bool is_sel = jt < n_sel;
             const int ks = jt % kNS;
             if (lane == 0 && (warp & 3) == 0) SKB_TRB(hf, jt, 9);
-            mbar_wait(&bars[QB_SFULL + s], (jt / kSS) & 1);
+            mbar_wait(&bars[QB_SFULL], jt & 1);
             if (is_sel) mbar_wait(&bars[QB_MFULL + ks], (jt / kNS) & 1);
             if (lane == 0 && (warp & 3) == 0) SKB_TRB(hf, jt, 0);
             tc_after_sync();
-            float sv[32], dp[32];
-            tmem_ld32(tS + lane_off + s * 64 + hf * 32, sv);
-            tmem_ld32(tP + lane_off + s * 64 + hf * 32, dp);
+            float sv[64], dp[64];
+            tmem_ld32(tS + lane_off + c0, sv);
+            tmem_ld32(tS + lane_off + c0 + 32, sv + 32);
+            tmem_ld32(tP + lane_off + c0, dp);
+            tmem_ld32(tP + lane_off + c0 + 32, dp + 32);
             tmem_wait_ld();
             tc_before_sync();
-            mbar_arrive(&bars[QB_SEMPTY + s]);
+            mbar_arrive(&bars[QB_SEMPTY]);  // S/dP of the next tile may overwrite now
             bool plain = true;
             if (is_sel) {
-                const int* mk = meta + (ks * 3) * 64 + hf * 32;
-                const int* ml = mk + 64;
-                const float* mu = reinterpret_cast<const float*>(mk + 128);
+                const int* mk = meta + (ks * 3) * 128 + c0;
+                const int* ml = mk + 128;
+                const float* mu = reinterpret_cast<const float*>(mk + 256);
                 const int fl = tflags[ks * 4];
                 if (!(fl & 1)) {  // per-key interval mask j <= t < leave_j: (unsigned)(t - j) < leave_j - j
 #pragma unroll
-                    for (int c = 0; c < 32; c += 4) {
+                    for (int c = 0; c < 64; c += 4) {
                         const int4 kj = *reinterpret_cast<const int4*>(mk + c);
                         const int4 ex = *reinterpret_cast<const int4*>(ml + c);
                         sv[c + 0] = ((unsigned)(t - kj.x) < (unsigned)ex.x) ? sv[c + 0] : -INFINITY;
@@ -684,7 +692,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(const __grid_constant
                 if (!(fl & 2)) {  // fractional gates present
                     plain = false;
 #pragma unroll
-                    for (int c = 0; c < 32; c += 4) {
+                    for (int c = 0; c < 64; c += 4) {
                         const float4 uu = *reinterpret_cast<const float4*>(mu + c);
                         const float ua[4] = {uu.x, uu.y, uu.z, uu.w};
 #pragma unroll
@@ -705,17 +713,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(const __grid_constant
                     }
                 }
             } else {
-                const int kb = jw0 + (jt - n_sel) * 64 + hf * 32;
+                const int kb = jw0 + (jt - n_sel) * 128 + c0;
                 const int cmin = lo_win - kb;
                 const int cmax = i - kb;
-                if (__any_sync(0xffffffffu, cmin > 0 || cmax < 31)) {
+                if (__any_sync(0xffffffffu, cmin > 0 || cmax < 63)) {
 #pragma unroll
-                    for (int c = 0; c < 32; ++c) sv[c] = (c >= cmin && c <= cmax) ? sv[c] : -INFINITY;
+                    for (int c = 0; c < 64; ++c) sv[c] = (c >= cmin && c <= cmax) ? sv[c] : -INFINITY;
                 }
             }
             if (plain) {  // all gates 1: plain softmax backward, packed fp32x2
 #pragma unroll
-                for (int c = 0; c < 32; c += 2) {
+                for (int c = 0; c < 64; c += 2) {
                     float2 x = __ffma2_rn(make_float2(sv[c], sv[c + 1]), sl22, nl2);
                     x.x = ex2(x.x);
                     x.y = ex2(x.y);
@@ -724,18 +732,23 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(const __grid_constant
                     dp[c + 1] = d.y;
                 }
             }
-            // dS -> TMEM over this half's consumed dP columns (packed bf16x2)
+            // dS -> TMEM (packed bf16x2), once dQ of the previous tile has read the buffer
+            if (jt >= 1) mbar_wait(&bars[QB_DSEMPTY], (jt - 1) & 1);
+            tc_after_sync();
             {
                 uint32_t pk[16];
 #pragma unroll
                 for (int e = 0; e < 16; ++e) pk[e] = pack_bf16(dp[2 * e], dp[2 * e + 1]);
-                tmem_st16u(tP + lane_off + s * 64 + hf * 32, pk);
+                tmem_st16u(tDS + lane_off + hf * 32, pk);
+#pragma unroll
+                for (int e = 0; e < 16; ++e) pk[e] = pack_bf16(dp[32 + 2 * e], dp[33 + 2 * e]);
+                tmem_st16u(tDS + lane_off + hf * 32 + 16, pk);
                 tmem_wait_st();
             }
             tc_before_sync();
             if (lane == 0 && (warp & 3) == 0) SKB_TRB(hf, jt, 4);
             mbar_arrive(&bars[QB_MEMPTY + ks]);
-            mbar_arrive(&bars[QB_DSFULL + s]);
+            mbar_arrive(&bars[QB_DSFULL]);
         }
         mbar_wait(&bars[QB_DQDONE], 0);
         tc_after_sync();

@@ -9,4 +9,4 @@ for f in ('gpurun_out/bench.log',):
     d=json.loads(open(f).read().strip().splitlines()[-1]); r=d['roofline']
     print(f, round(d['value']), round(d['ms_per_step'],3), {k:round(r[k],3) for k in ('select_ms','attn_fwd_ms','attn_bwd_ms','frac','step_frac')})
 "
-SKB_LIB_PATH=paper_2406_16747_b200/_build/tr/libsparsek_b200.so timeout 300 python tools/trace_dq.py | sed -n 12,16p
+SKB_LIB_PATH=paper_2406_16747_b200/_build/tr/libsparsek_b200.so timeout 300 python tools/trace_dq.py | sed -n 6,9p
