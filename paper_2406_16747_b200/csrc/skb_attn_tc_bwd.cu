@@ -468,23 +468,24 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_tc(const __grid_consta
 // each) form dS_j = P (wv dP - delta) * kappa; dQ += dS_j K (TS). Producers:
 // dO and the window band by 3-D TMA, selected rows by cp.async gathers with
 // keys fetched one tile ahead, per-key metadata from skb_select's block arrays.
-constexpr int kNS = 2;  // K/V ring depth of the dQ kernel
+constexpr int kNS = 3;  // K (+ metadata) ring depth of the dQ kernel
+constexpr int kNV = 2;  // V ring depth (V is released as soon as dP is computed)
 
 template <int D>
 struct QSmem {
     static constexpr int kKT = 128 * D * 2;  // 128-key tile
     static constexpr int kDO = 0;            // dO tile (128 queries)
     static constexpr int kK = kDO + kKT;     // [kNS]
-    static constexpr int kV = kK + kNS * kKT;  // [kNS]
-    static constexpr int kMeta = kV + kNS * kKT;  // [kNS][key|ext|uf][128] x 4 B
+    static constexpr int kV = kK + kNS * kKT;  // [kNV]
+    static constexpr int kMeta = kV + kNV * kKT;  // [kNS][key|ext|uf][128] x 4 B
     static constexpr int kFlags = kMeta + kNS * 3 * 128 * 4;  // [kNS] x 16 B
     static constexpr int kBar = kFlags + kNS * 16;
-    static constexpr int kNumBars = 16;
+    static constexpr int kNumBars = 20;
     static constexpr int kTmemSlot = kBar + kNumBars * 8;
     static constexpr int kAlloc = kTmemSlot + 16 + 1024;
 };
-enum { QB_QFULL = 0, QB_DOFULL = 1, QB_KVFULL = 2, QB_KVEMPTY = 4, QB_MFULL = 6, QB_MEMPTY = 8, QB_SFULL = 10,
-       QB_SEMPTY = 11, QB_DSFULL = 12, QB_DSEMPTY = 13, QB_DQDONE = 14 };  // 15 barriers
+enum { QB_QFULL = 0, QB_DOFULL = 1, QB_KVFULL = 2, QB_KVEMPTY = 5, QB_MFULL = 8, QB_MEMPTY = 11, QB_VFULL = 14,
+       QB_VEMPTY = 16, QB_SFULL = 18, QB_SEMPTY = 19, QB_DSFULL = 20, QB_DSEMPTY = 21, QB_DQDONE = 22 };  // 23
 
 template <int D, bool KEY_SOFT>
 __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(const __grid_constant__ BwdArgs a) {
@@ -517,6 +518,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(const __grid_constant
             mbar_init(&bars[QB_KVEMPTY + s], 1);
             mbar_init(&bars[QB_MFULL + s], kProducers);
             mbar_init(&bars[QB_MEMPTY + s], kMath);
+        }
+        for (int s = 0; s < kNV; ++s) {
+            mbar_init(&bars[QB_VFULL + s], kProducers + 1);
+            mbar_init(&bars[QB_VEMPTY + s], 1);
         }
         mbar_init(&bars[QB_SFULL], 1);
         mbar_init(&bars[QB_SEMPTY], kMath);
@@ -557,28 +562,29 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(const __grid_constant
             }
             cp_async_arrive_noinc(&bars[QB_MFULL + s]);
             if (ptid == 0) SKB_TRB(2, jt, 1);
+            // rows of tile jt of one tensor into dst, completing on bar (97 arrivals)
+            auto rows = [&](uint32_t dst, const __nv_bfloat16* src, const CUtensorMap* tm, uint64_t* bar) {
+                if (jt < n_sel) {
+                    kcur.issue<false>(dst, src, b, h, a.L, a.H, pw, lane);
+                    cp_async_arrive_noinc(bar);
+                    if (ptid == 0) mbar_arrive(bar);
+                } else {
+                    if (ptid == 0) {
+                        mbar_expect_tx(bar, 128 * D * 2);
+#pragma unroll
+                        for (int at = 0; at < kAtoms; ++at)
+                            tma_load_3d(dst + at * 128 * 128, tm, h * D + at * 64, jw0 + (jt - n_sel) * 128, b, bar);
+                    }
+                    mbar_arrive(bar);
+                }
+            };
             if (jt >= kNS) mbar_wait(&bars[QB_KVEMPTY + s], ((jt - kNS) / kNS) & 1);
             if (ptid == 0) SKB_TRB(2, jt, 2);
-            if (jt < n_sel) {
-                kcur.issue<false>(sbase + SM::kK + s * SM::kKT, a.k, b, h, a.L, a.H, pw, lane);
-                kcur.issue<false>(sbase + SM::kV + s * SM::kKT, a.v, b, h, a.L, a.H, pw, lane);
-                cp_async_arrive_noinc(&bars[QB_KVFULL + s]);
-                if (ptid == 0) mbar_arrive(&bars[QB_KVFULL + s]);
-                if (jt + 1 < n_sel) kcur.fetch(pw, lane, [&](int r) { return __ldg(list + (jt + 1) * 128 + r); });
-            } else {
-                if (ptid == 0) {
-                    const int kb0 = jw0 + (jt - n_sel) * 128;
-                    mbar_expect_tx(&bars[QB_KVFULL + s], 2 * 128 * D * 2);
-#pragma unroll
-                    for (int at = 0; at < kAtoms; ++at) {
-                        tma_load_3d(sbase + SM::kK + s * SM::kKT + at * 128 * 128, &a.tm_k128, h * D + at * 64, kb0, b,
-                                    &bars[QB_KVFULL + s]);
-                        tma_load_3d(sbase + SM::kV + s * SM::kKT + at * 128 * 128, &a.tm_v128, h * D + at * 64, kb0,
-                                    b, &bars[QB_KVFULL + s]);
-                    }
-                }
-                mbar_arrive(&bars[QB_KVFULL + s]);
-            }
+            rows(sbase + SM::kK + s * SM::kKT, a.k, &a.tm_k128, &bars[QB_KVFULL + s]);
+            const int vs = jt % kNV;
+            if (jt >= kNV) mbar_wait(&bars[QB_VEMPTY + vs], ((jt - kNV) / kNV) & 1);
+            rows(sbase + SM::kV + vs * SM::kKT, a.v, &a.tm_v128, &bars[QB_VFULL + vs]);
+            if (jt + 1 < n_sel) kcur.fetch(pw, lane, [&](int r) { return __ldg(list + (jt + 1) * 128 + r); });
         }
     } else if (warp == kMmaWarp) {
         if (lane == 0) {
@@ -591,11 +597,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(const __grid_constant
                 const int ks = j % kNS;
                 SKB_TRB(3, j, 8);
                 mbar_wait(&bars[QB_KVFULL + ks], (j / kNS) & 1);
+                mbar_wait(&bars[QB_VFULL + (j % kNV)], (j / kNV) & 1);
                 SKB_TRB(3, j, 0);
                 fence_proxy_async();  // cp.async (generic proxy) rows -> tensor core reads
                 if (j >= 1) mbar_wait(&bars[QB_SEMPTY], (j - 1) & 1);
                 tc_after_sync();
-                const uint32_t kb = sbase + SM::kK + ks * SM::kKT, vb = sbase + SM::kV + ks * SM::kKT;
+                const uint32_t kb = sbase + SM::kK + ks * SM::kKT, vb = sbase + SM::kV + (j % kNV) * SM::kKT;
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk) {
                     umma_f16_ts(tS, tQ + kk * 8, desc_kmajor(kb, 128, kk), id_s, kk > 0 ? 1u : 0u);
@@ -603,6 +610,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(const __grid_constant
                              kk > 0 ? 1u : 0u);
                 }
                 umma_commit(&bars[QB_SFULL]);
+                umma_commit(&bars[QB_VEMPTY + (j % kNV)]);
                 SKB_TRB(3, j, 1);
             };
             auto dq = [&](int j) {  // dQ += dS_j K_j (TS)
