@@ -468,6 +468,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_tc(const __grid_consta
 // each) form dS_j = P (wv dP - delta) * kappa; dQ += dS_j K (TS). Producers:
 // dO and the window band by 3-D TMA, selected rows by cp.async gathers with
 // keys fetched one tile ahead, per-key metadata from skb_select's block arrays.
+#ifndef SKB_DQ_POLY
+#define SKB_DQ_POLY 1
+#endif
+constexpr bool kDqPoly = SKB_DQ_POLY != 0;
 constexpr int kNS = 3;  // K (+ metadata) ring depth of the dQ kernel
 constexpr int kNV = 2;  // V ring depth (V is released as soon as dP is computed)
 
@@ -733,8 +737,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(const __grid_constant
 #pragma unroll
                 for (int c = 0; c < 64; c += 2) {
                     float2 x = __ffma2_rn(make_float2(sv[c], sv[c + 1]), sl22, nl2);
-                    x.x = ex2(x.x);
-                    x.y = ex2(x.y);
+                    if ((c & 7) == 6 && kDqPoly) {  // one pair in four on the FMA pipe (MUFU relief)
+                        x = ex2_poly2(x);
+                    } else {
+                        x.x = ex2(x.x);
+                        x.y = ex2(x.y);
+                    }
                     const float2 d = __fmul2_rn(x, __fadd2_rn(make_float2(dp[c], dp[c + 1]), ndl));
                     dp[c] = d.x;
                     dp[c + 1] = d.y;
