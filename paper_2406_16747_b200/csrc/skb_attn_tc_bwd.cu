@@ -25,8 +25,8 @@
 __device__ unsigned long long g_skb_trace_bwd[4096];
 #define SKB_TRB(role, jt, ev)                                                                        \
     do {                                                                                              \
-        if (blockIdx.x == 100 && blockIdx.y == 0 && blockIdx.z == 0 && (jt) < 32)                  \
-            g_skb_trace_bwd[(role) * 512 + (jt) * 16 + (ev)] = clock64();                            \
+        if (blockIdx.x == 100 && blockIdx.y == 0 && blockIdx.z == 0 && (jt) < 32 && (role) < 8)     \
+            g_skb_trace_bwd[((role) * 512 + (jt) * 16 + (ev)) & 4095] = clock64();                   \
     } while (0)
 extern "C" int skb_debug_trace_bwd(unsigned long long* out, int n) {
     return (int)cudaMemcpyFromSymbol(out, g_skb_trace_bwd, sizeof(unsigned long long) * (n < 4096 ? n : 4096));
@@ -223,7 +223,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_tc(const __grid_consta
         const float* dlt = a.delta + ((int64_t)b * a.H + h) * a.L;
         for (int qt = 0; qt < nq; ++qt) {
             const int s = qt % kQS;
+            if (ptid == 0 && !SEL) SKB_TRB(4 + 2, qt, 0);
             if (qt >= kQS) mbar_wait(&bars[KB_QDEMPTY + s], ((qt - kQS) / kQS) & 1);
+            if (ptid == 0 && !SEL) SKB_TRB(4 + 2, qt, 1);
             const int qs = q_lo + qt * 64;
             for (int c = ptid; c < 64; c += kProducers) {
                 const int i = qs + c;
@@ -255,6 +257,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_tc(const __grid_consta
             auto acc = [&](int j) {
                 const int s = j & 1, qs = j % kQS;
                 mbar_wait(&bars[KB_PDSFULL + s], (j >> 1) & 1);
+                if (!SEL) SKB_TRB(4 + 3, j, 2);
                 tc_after_sync();
                 const uint32_t dob = sbase + SM::kDO + qs * SM::kQT, qb = sbase + SM::kQ + qs * SM::kQT;
                 // P~^T / dS^T of query half hf (32 queries) sit in TMEM columns [hf*32, hf*32+16)
@@ -268,7 +271,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_tc(const __grid_consta
             };
             for (int qt = 0; qt < nq; ++qt) {
                 const int s = qt & 1, qs = qt % kQS;
+                if (!SEL) SKB_TRB(4 + 3, qt, 8);
                 mbar_wait(&bars[KB_QDFULL + qs], (qt / kQS) & 1);
+                if (!SEL) SKB_TRB(4 + 3, qt, 0);
                 if (qt >= 2) mbar_wait(&bars[KB_SEMPTY + s], ((qt - 2) >> 1) & 1);
                 tc_after_sync();
                 const uint32_t qb = sbase + SM::kQ + qs * SM::kQT, dob = sbase + SM::kDO + qs * SM::kQT;
@@ -280,6 +285,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_tc(const __grid_consta
                              kk > 0 ? 1u : 0u);
                 }
                 umma_commit(&bars[KB_SFULL + s]);
+                if (!SEL) SKB_TRB(4 + 3, qt, 1);
                 if (qt >= 1) acc(qt - 1);
             }
             acc(nq - 1);
@@ -304,8 +310,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_tc(const __grid_consta
         for (int qt = 0; qt < nq; ++qt) {
             const int s = qt & 1, qs3 = qt % kQS;
             const int qs = q_lo + qt * 64 + hf * 32;  // first query of this thread's columns
+            if (!SEL && lane == 0 && (warp & 3) == 0) SKB_TRB(4 + hf, qt, 9);
             mbar_wait(&bars[KB_SFULL + s], (qt >> 1) & 1);
             mbar_wait(&bars[KB_QDFULL + qs3], (qt / kQS) & 1);
+            if (!SEL && lane == 0 && (warp & 3) == 0) SKB_TRB(4 + hf, qt, 0);
             tc_after_sync();
             float sv[32], dp[32];
             tmem_ld32(tS + lane_off + s * 64 + hf * 32, sv);
@@ -384,6 +392,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_tc(const __grid_consta
                 tmem_wait_st();
             }
             tc_before_sync();
+            if (!SEL && lane == 0 && (warp & 3) == 0) SKB_TRB(4 + hf, qt, 4);
             mbar_arrive(&bars[KB_PDSFULL + s]);
         }
         if (SEL && key >= 0 && colsum != 0.f) atomicAdd(a.colsum + bl + key, (double)colsum);

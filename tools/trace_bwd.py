@@ -1,0 +1,39 @@
+"""Per-tile timeline of one dQ CTA (needs a -DSKB_TRACE build)."""
+import ctypes
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+from paper_2406_16747_b200 import _lib, ops  # noqa: E402
+
+dev = torch.device("cuda", 0)
+C = bench.CFG
+cfg = ops.AttnConfig(k=C["k"], window=C["w"])
+q, k, v, do, u = bench.make_inputs(torch, dev, 1234, "recency")
+sys.argv = sys.argv[:2]
+sel = ops.select(u, cfg, heads=C["H"], head_dim=C["d"], dtype=torch.bfloat16)
+o, lse, _ = ops.attn_fwd(q, k, v, u, cfg, sel=sel)
+for _ in range(2):
+    ops.attn_bwd(q, k, v, o, do, lse, u, sel, cfg)
+torch.cuda.synchronize()
+buf = (ctypes.c_ulonglong * 4096)()
+_lib.load().skb_debug_trace_bwd(buf, 4096)
+t = np.array(buf, dtype=np.int64)
+names = {0: {9: "wS", 0: "S", 4: "dS"}, 1: {9: "wS", 0: "S", 4: "dS"}, 2: {0: "it", 1: "meta", 2: "kvgo"},
+         3: {8: "wKV", 0: "KV", 1: "SdP", 2: "DS"}}
+roles = {0: "WG0", 1: "WG1", 2: "PROD", 3: "MMA"}
+base = 4  # 0: dq roles, 4: dK/dV (window pass) roles
+t0 = min(x for x in t[base * 512:(base + 4) * 512] if x > 0)
+for jt in range(32):
+    row = []
+    for r in range(4):
+        for ev, nm in names[r].items():
+            x = t[((r + base) * 512 + jt * 16 + ev) & 4095]
+            if x > 0:
+                row.append(f"{roles[r]}.{nm}={x - t0}")
+    if row:
+        print(f"tile {jt:2d}: " + " ".join(row))
