@@ -226,3 +226,70 @@ def test_tensor_core_path_vs_oracle(cuda, oracle, case):
     np.testing.assert_allclose(tc["lse"], lse.T, rtol=0, atol=2e-2)
     if np.abs(gu).max() > 0:
         assert rel_err(tc["du"], gu) < 5e-2, rel_err(tc["du"], gu)
+
+
+FULL_CASES = [
+    # BASELINE.json configs at full size, one sequence each: (L, H, p, k, w)
+    ("cfg3", 16384, 32, 128, 1024.0, 512),
+    ("cfg2", 4096, 12, 64, 256.0, 256),
+]
+
+
+@pytest.mark.parametrize("case", FULL_CASES, ids=[c[0] for c in FULL_CASES])
+@pytest.mark.parametrize("kind", ["recency", "iid"])
+def test_full_size_tensor_core_path(cuda, oracle, case, kind):
+    """Full BASELINE shapes, bf16 tcgen05 path, two independent checks:
+    (1) sampled query rows recomputed in float64 from the C oracle's selection
+        (Sel_i, tau_i) — o_i and dq_i within 2e-2;
+    (2) every output against the f32 CUDA-core gather path on the same
+        (bf16-rounded) inputs — o, dq, dk, dv within 2e-2, du within 5e-2."""
+    import torch
+
+    from paper_2406_16747_b200 import ops
+
+    name, L, H, p, k, w = case
+    rng = np.random.default_rng(L + H)
+    g = torch.Generator(device=cuda)
+    g.manual_seed(L)
+    shape = (1, L, H, p)
+    q, kk, v, do = (torch.randn(shape, generator=g, device=cuda).to(torch.bfloat16) for _ in range(4))
+    u_np = _scores(rng, L, kind)
+    u = torch.from_numpy(u_np)[None].to(cuda)
+    cfg = ops.AttnConfig(k=k, window=w)
+    o, lse, sel = ops.attn_fwd(q, kk, v, u, cfg)
+    dq, dk, dv, du = ops.attn_bwd(q, kk, v, o, do, lse, u, sel, cfg)
+    gcfg = ops.AttnConfig(k=k, window=w, force_gather=True)
+    f = lambda t: t.float().contiguous()
+    og, lseg, selg = ops.attn_fwd(f(q), f(kk), f(v), u, gcfg)
+    dqg, dkg, dvg, dug = ops.attn_bwd(f(q), f(kk), f(v), og, f(do), lseg, u, selg, gcfg)
+    torch.cuda.synchronize()
+    rel = lambda a, b: float((a.double() - b.double()).norm() / b.double().norm().clamp_min(1e-30))
+    for nm, a, b_ in (("o", o, og), ("dq", dq, dqg), ("dk", dk, dkg), ("dv", dv, dvg)):
+        assert rel(a, b_) < 2e-2, (nm, rel(a, b_))
+    assert rel(du, dug) < 5e-2, rel(du, dug)
+    # (1) sampled rows against the oracle's selection
+    osel = oracle.select(u_np, k, w)
+    Qn, Kn, Vn, dOn = (t[0].double().cpu().numpy() for t in (q, kk, v, do))
+    on, dqn = o[0].double().cpu().numpy(), dq[0].double().cpu().numpy()
+    scale = 1.0 / np.sqrt(p)
+    rows = np.unique(np.concatenate([[0, w - 1, w, w + int(k), L - 1], rng.integers(0, L, size=40)]))
+    num_o = den_o = num_q = den_q = 0.0
+    for i in rows:
+        att = osel.att_of(i)
+        ns = osel.n_sel[i]
+        gates = np.ones(len(att))
+        gates[:ns] = np.clip(u_np[att[:ns]] - osel.tau_q[i], 0, 1)
+        for h in range(H):
+            a = scale * Kn[att, h] @ Qn[i, h]
+            P = np.exp(a - a.max())
+            P /= P.sum()
+            oo = (P * gates) @ Vn[att, h]
+            dP = Vn[att, h] @ dOn[i, h]
+            dlt = np.sum(P * gates * dP)
+            dqq = scale * ((P * (gates * dP - dlt)) @ Kn[att, h])
+            num_o += np.sum((on[i, h] - oo) ** 2)
+            den_o += np.sum(oo ** 2)
+            num_q += np.sum((dqn[i, h] - dqq) ** 2)
+            den_q += np.sum(dqq ** 2)
+    assert np.sqrt(num_o / den_o) < 2e-2, np.sqrt(num_o / den_o)
+    assert np.sqrt(num_q / den_q) < 2e-2, np.sqrt(num_q / den_q)
