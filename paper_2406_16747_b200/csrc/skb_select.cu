@@ -351,10 +351,10 @@ __global__ void __launch_bounds__(kTauThreads) k_tau_overflow(TauArgs a, int nch
 
 // ---------------------------------------------------------------- unions
 // Ordered block compaction of keys j in [0, t_hi] with leave_j > max(j, t_lo).
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(1024)
 k_union_lists(const int* __restrict__ leave1, int L, int T, int window, int nqb, int cap,
               int* __restrict__ qb_count, int* __restrict__ qb_list) {
-    __shared__ int wsum[8];
+    __shared__ int wsum[32];
     __shared__ int base_s;
     const int b = blockIdx.y, qb = blockIdx.x;
     const int t_lo = qb * kQBlock - window;
@@ -364,7 +364,7 @@ k_union_lists(const int* __restrict__ leave1, int L, int T, int window, int nqb,
     if (threadIdx.x == 0) base_s = 0;
     __syncthreads();
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    for (int j0 = 0; j0 <= t_hi; j0 += 256) {
+    for (int j0 = 0; j0 <= t_hi; j0 += blockDim.x) {
         const int j = j0 + threadIdx.x;
         bool keep = false;
         if (j <= t_hi) {
@@ -383,7 +383,7 @@ k_union_lists(const int* __restrict__ leave1, int L, int T, int window, int nqb,
         __syncthreads();
         if (threadIdx.x == 0) {
             int tot = 0;
-            for (int w = 0; w < 8; ++w) tot += wsum[w];
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += wsum[w];
             base_s += tot;
         }
         __syncthreads();
@@ -392,10 +392,10 @@ k_union_lists(const int* __restrict__ leave1, int L, int T, int window, int nqb,
 }
 
 // Ever-selected keys per sequence, ascending.
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(1024)
 k_ever_list(const int* __restrict__ leave1, int L, int T, int* __restrict__ ever_count,
             int* __restrict__ ever_list) {
-    __shared__ int wsum[8];
+    __shared__ int wsum[32];
     __shared__ int base_s;
     const int b = blockIdx.x;
     const int* lv = leave1 + (int64_t)b * L;
@@ -403,7 +403,7 @@ k_ever_list(const int* __restrict__ leave1, int L, int T, int* __restrict__ ever
     if (threadIdx.x == 0) base_s = 0;
     __syncthreads();
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    for (int j0 = 0; j0 < T; j0 += 256) {
+    for (int j0 = 0; j0 < T; j0 += blockDim.x) {
         const int j = j0 + threadIdx.x;
         const bool keep = j < T && lv[j] > j;
         const unsigned bal = __ballot_sync(0xffffffffu, keep);
@@ -415,7 +415,7 @@ k_ever_list(const int* __restrict__ leave1, int L, int T, int* __restrict__ ever
         __syncthreads();
         if (threadIdx.x == 0) {
             int tot = 0;
-            for (int w = 0; w < 8; ++w) tot += wsum[w];
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += wsum[w];
             base_s += tot;
         }
         __syncthreads();
@@ -667,8 +667,8 @@ void run_select(const skb_attn_desc& d, const double* u, void* ws, cudaStream_t 
     const int nqb = (int)lay.nqb;
     if (R1 > 0 && T > 0) {
         dim3 g(nqb, B);
-        k_union_lists<<<g, 256, 0, st>>>(leave1, L, T, w, nqb, (int)lay.qb_cap, qb_count, qb_list);
-        k_ever_list<<<B, 256, 0, st>>>(leave1, L, T, ever_count, ever_list);
+        k_union_lists<<<g, 512, 0, st>>>(leave1, L, T, w, nqb, (int)lay.qb_cap, qb_count, qb_list);
+        k_ever_list<<<B, 1024, 0, st>>>(leave1, L, T, ever_count, ever_list);
         SKB_CHECK_LAUNCH();
         k_union_meta<<<g, 128, 0, st>>>(leave1, reinterpret_cast<const float*>(base + lay.uf),
                                         reinterpret_cast<const float*>(base + lay.tauf), L, T, w, nqb,
