@@ -73,7 +73,7 @@ def main(tag, launches_csv, rep):
                 out.append(f"   {nm:24s} {r[i]} {u[i]}")
         rd = float(r[h.index('dram__bytes_read.sum')]) * SCALE[u[h.index('dram__bytes_read.sum')]]
         wr = float(r[h.index('dram__bytes_write.sum')]) * SCALE[u[h.index('dram__bytes_write.sum')]]
-        name = r[ki].split("::")[-1].split("(")[0]
+        name = r[ki].split("(")[0].split("::")[-1]
         traffic[name] = rd + wr
     open(os.path.join(ROOT, "profiles", f"{tag}_ncu_attn.txt"), "w").write("\n".join(out) + "\n")
     fwd = sum(v for k, v in traffic.items() if k.startswith("k_fwd_tc"))
