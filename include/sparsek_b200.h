@@ -69,6 +69,10 @@ typedef struct skb_attn_desc {
     int32_t mask_mode; /* 0 MaskApply::soft, 1 MaskApply::straight_through */
     int32_t dtype;     /* skb_dtype of Q/K/V/O/dO/dQ/dK/dV             */
     uint32_t flags;    /* SKB_FLAG_*                                    */
+    int64_t chunk_len; /* 0: one chunk; > 0: chunk-wise recurrent training
+                          (chunked_forward, Algorithm 3): the forward is
+                          unchanged, gradients never cross to the left of a
+                          chunk start (proj/src/attention.cpp:228-234)     */
 } skb_attn_desc;
 
 /* ScoringParams (proj/include/sparsek/selection.hpp:19-27) minus w_score. */
@@ -76,7 +80,8 @@ typedef struct skb_scoring {
     int32_t norm_mode;     /* 0 none, 1 timestep_norm                   */
     int32_t slope_order;   /* 0 slope_then_norm, 1 norm_then_slope      */
     int32_t slope_enabled; /* 0/1                                       */
-    int32_t reserved;
+    int32_t chunk_len;     /* backward only: the norm pullback stays inside
+                              each chunk (proj/src/attention.cpp:482-502); 0 = one chunk */
     double slope_eps;      /* > 0                                       */
 } skb_scoring;
 

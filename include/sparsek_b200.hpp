@@ -111,6 +111,7 @@ struct AttnConfig {  // attention.hpp:18-32 (group_size / linear_mix are CPU-onl
     double scale = 0.0;  // 0 -> 1/sqrt(head_dim)
     KeyMode key_mode = KeyMode::hard;
     MaskApply mask_mode = MaskApply::soft;
+    size_t chunk_len = 0;  // chunked_forward (cache.hpp:93-96): backward stop-grad at chunk starts
 };
 
 inline skb_attn_desc make_desc(int64_t batch, int64_t seq_len, int64_t head_dim, const AttnConfig& c, DType dt,
@@ -127,6 +128,7 @@ inline skb_attn_desc make_desc(int64_t batch, int64_t seq_len, int64_t head_dim,
     d.mask_mode = c.mask_mode == MaskApply::straight_through ? 1 : 0;
     d.dtype = (int32_t)dt;
     d.flags = flags;
+    d.chunk_len = (int64_t)c.chunk_len;
     return d;
 }
 

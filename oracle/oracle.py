@@ -290,15 +290,18 @@ class Reference:
                                          surv.ctypes.data_as(C.POINTER(C.c_uint64)), _d(p_last)))
         return tau, ins.astype(bool), surv.astype(np.int64), p_last
 
-    def attention(self, x, wq, wk, wv, wo, w_score, cfg, use_float=False, grad_out=None):
-        """Forward with tape (+ backward when grad_out is given)."""
+    def attention(self, x, wq, wk, wv, wo, w_score, cfg, use_float=False, grad_out=None,
+                  chunk_len=0):
+        """Forward with tape (+ backward when grad_out is given); chunk_len > 0
+        runs the reference's chunked_forward (Algorithm 3)."""
         x, wq, wk, wv, wo = (np.ascontiguousarray(a, np.float64) for a in (x, wq, wk, wv, wo))
         w_score = np.ascontiguousarray(w_score, np.float64)
         L, D = x.shape
         h = C.c_void_p()
-        self._rc(self.lib.ref_attention_fwd(C.c_int32(int(use_float)), C.c_uint64(L),
-                                            C.c_uint64(D), _d(x), _d(wq), _d(wk), _d(wv),
-                                            _d(wo), _d(w_score), C.byref(cfg), C.byref(h)))
+        self._rc(self.lib.ref_attention_fwd_chunked(C.c_int32(int(use_float)), C.c_uint64(L),
+                                                    C.c_uint64(D), _d(x), _d(wq), _d(wk), _d(wv),
+                                                    _d(wo), _d(w_score), C.byref(cfg),
+                                                    C.c_uint64(int(chunk_len)), C.byref(h)))
         try:
             n, ta, ts, nt = (C.c_uint64() for _ in range(4))
             self._rc(self.lib.ref_tape_sizes(h, C.byref(n), C.byref(ta), C.byref(ts),

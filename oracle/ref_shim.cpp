@@ -189,9 +189,21 @@ struct TapeRun : TapeBase {
 extern "C" {
 
 // Forward with tape. Returns an opaque handle in *out (free with ref_tape_free).
+int ref_attention_fwd_chunked(int32_t use_float, uint64_t L, uint64_t D, const double* x,
+                              const double* wq, const double* wk, const double* wv, const double* wo,
+                              const double* w_score, const ref_cfg* c, uint64_t chunk_len, void** out);
+
 int ref_attention_fwd(int32_t use_float, uint64_t L, uint64_t D, const double* x, const double* wq,
                       const double* wk, const double* wv, const double* wo,
                       const double* w_score, const ref_cfg* c, void** out) {
+    return ref_attention_fwd_chunked(use_float, L, D, x, wq, wk, wv, wo, w_score, c, 0, out);
+}
+
+// chunk_len 0: sparsek_attention (attention.hpp:81-85); > 0: chunked_forward
+// (cache.hpp:93-96, Algorithm 3) — same outputs, tape.chunk_starts set.
+int ref_attention_fwd_chunked(int32_t use_float, uint64_t L, uint64_t D, const double* x,
+                              const double* wq, const double* wk, const double* wv, const double* wo,
+                              const double* w_score, const ref_cfg* c, uint64_t chunk_len, void** out) {
     REF_GUARD_BEGIN
     auto run_t = [&](auto tag) -> TapeBase* {
         using T = decltype(tag);
@@ -200,8 +212,11 @@ int ref_attention_fwd(int32_t use_float, uint64_t L, uint64_t D, const double* x
                                   mat_in<T>(wo, D, D)};
         r->scoring = to_scoring(c, w_score, D);
         try {
-            r->y = sparsek_attention(mat_in<T>(x, L, D), r->params, r->scoring, to_cfg(c),
-                                     &r->tape);
+            if (chunk_len == 0)
+                r->y = sparsek_attention(mat_in<T>(x, L, D), r->params, r->scoring, to_cfg(c), &r->tape);
+            else
+                r->y = chunked_forward(mat_in<T>(x, L, D), chunk_len, r->params, r->scoring, to_cfg(c),
+                                       &r->tape);
         } catch (...) {
             delete r;
             throw;

@@ -12,6 +12,7 @@ from .api import (  # noqa: F401
     __version__,
     attention,
     attention_grads,
+    chunked_forward,
     dense_attention,
     sparsek,
     sparsek_jvp,
@@ -21,6 +22,6 @@ from . import ops  # noqa: F401
 
 __all__ = [
     "ArgumentError", "ConfigError", "NumericError", "ShapeError", "IoError", "Stream",
-    "__version__", "attention", "attention_grads", "dense_attention", "sparsek", "sparsek_jvp",
+    "__version__", "attention", "attention_grads", "chunked_forward", "dense_attention", "sparsek", "sparsek_jvp",
     "topk_hard", "ops",
 ]

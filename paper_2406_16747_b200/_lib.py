@@ -50,12 +50,12 @@ class AttnDesc(C.Structure):
     _fields_ = [("batch", C.c_int64), ("seq_len", C.c_int64), ("heads", C.c_int64),
                 ("head_dim", C.c_int64), ("k", C.c_double), ("window", C.c_int64),
                 ("scale", C.c_double), ("key_mode", C.c_int32), ("mask_mode", C.c_int32),
-                ("dtype", C.c_int32), ("flags", C.c_uint32)]
+                ("dtype", C.c_int32), ("flags", C.c_uint32), ("chunk_len", C.c_int64)]
 
 
 class Scoring(C.Structure):
     _fields_ = [("norm_mode", C.c_int32), ("slope_order", C.c_int32),
-                ("slope_enabled", C.c_int32), ("reserved", C.c_int32),
+                ("slope_enabled", C.c_int32), ("chunk_len", C.c_int32),
                 ("slope_eps", C.c_double)]
 
 

@@ -167,23 +167,42 @@ def attention(x, wq, wk, wv, wo, w_score, k, window, heads=1, key_mode="hard", m
 
 def attention_grads(x, wq, wk, wv, wo, w_score, k, window, grad_out, heads=1, key_mode="hard",
                     mask_mode="soft", slope_eps=0.01, slope_enabled=True,
-                    norm_mode="timestep_norm", slope_order="norm_then_slope"):
+                    norm_mode="timestep_norm", slope_order="norm_then_slope", chunk_len=0):
     """Forward + sparsek_attention_backward (proj/src/attention.cpp:214-575):
-    returns (y, {dx, dwq, dwk, dwv, dwo, dw_score}) as float64 numpy arrays."""
+    returns (y, {dx, dwq, dwk, dwv, dwo, dw_score}) as float64 numpy arrays.
+    chunk_len > 0 is chunked_forward's training (Algorithm 3,
+    proj/src/cache.cpp:548-563): the same outputs, and gradients that never
+    cross to the left of a chunk start (proj/src/attention.cpp:228-234)."""
     x, (wq, wk, wv, wo) = _attention_inputs(x, wq, wk, wv, wo, heads)
+    if int(chunk_len) < 0:
+        raise ArgumentError("chunked_forward: chunk_len must be positive")
     cfg = _core_cfg(float(k), int(window), key_mode, mask_mode)
+    if chunk_len:
+        cfg = ops.AttnConfig(k=cfg.k, window=cfg.window, key_mode=cfg.key_mode,
+                             mask_mode=cfg.mask_mode, chunk_len=int(chunk_len))
     L, D = x.shape
     wsc = _vec(w_score, "w_score")
     d = _dev()
     leaf = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(d).requires_grad_(True)
     xt, wqt, wkt, wvt, wot, wst = (leaf(a) for a in (x, wq, wk, wv, wo, wsc))
     sc = ops.ScoringConfig(slope_eps=float(slope_eps), slope_enabled=bool(slope_enabled),
-                           norm_mode=norm_mode, slope_order=slope_order)
+                           norm_mode=norm_mode, slope_order=slope_order, chunk_len=int(chunk_len))
     y, _ = attention_torch(xt.view(1, L, D), wqt, wkt, wvt, wot, wst, cfg, heads, sc)
     y.backward(torch.from_numpy(np.ascontiguousarray(grad_out, np.float64)).to(d).view(1, L, D))
     g = lambda t: (t.grad.cpu().numpy() if t.grad is not None else np.zeros(tuple(t.shape)))
     return y[0].detach().cpu().numpy(), dict(dx=g(xt), dwq=g(wqt), dwk=g(wkt), dwv=g(wvt),
                                              dwo=g(wot), dw_score=g(wst))
+
+
+def chunked_forward(x, chunk_len, wq, wk, wv, wo, w_score, k, window, heads=1, key_mode="hard",
+                    mask_mode="soft", slope_eps=0.01, slope_enabled=True):
+    """chunked_forward (proj/include/sparsek/cache.hpp:93-96): feeding the
+    sequence chunk by chunk reproduces the unchunked forward exactly
+    (proj/tests/test_cache.cpp:34-64), which the batch kernels compute."""
+    if int(chunk_len) <= 0:
+        raise ArgumentError("chunked_forward: chunk_len must be positive")
+    return attention(x, wq, wk, wv, wo, w_score, k, window, heads=heads, key_mode=key_mode,
+                     mask_mode=mask_mode, slope_eps=slope_eps, slope_enabled=slope_enabled)
 
 
 def dense_attention(x, wq, wk, wv, wo, heads=1):

@@ -59,6 +59,7 @@ struct Args {
     int B, L, H, p, w, T, R1;
     double scale;
     int key_soft, mask_st;
+    int chunk_len;  // 0 = one chunk
 };
 
 __device__ __forceinline__ double gate_of(double uj, double tau) {
@@ -217,6 +218,9 @@ __global__ void __launch_bounds__(kWarps * 32) k_bwd_gather(Args a) {
         }
     };
 
+    // chunk-wise training: keys left of this query's chunk start receive no
+    // gradient (proj/src/attention.cpp:228-234, 284-300, 472)
+    const int cs = a.chunk_len > 0 ? (i / a.chunk_len) * a.chunk_len : 0;
     // pass 1: s = sum p wv b; dv; gm (value path)
     double s = 0.0, gsum = 0.0;
     for_keys([&](int j, double g, bool sel) {
@@ -224,6 +228,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_bwd_gather(Args a) {
         eval(j, g, sel, pj, bj, dotj);
         const double wv = (sel && !a.mask_st) ? g : 1.0;
         s += pj * wv * bj;
+        if (j < cs) return;
         const double c0 = pj * wv;
         double* dvr = a.dv_acc + (bl + j) * rs + (int64_t)h * a.p;
 #pragma unroll
@@ -247,7 +252,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_bwd_gather(Args a) {
             const int c = lane + 32 * m;
             if (m < np && c < a.p) {
                 dqa[m] += coef * (double)ldv<S>(K + ko + c);
-                atomicAdd(dkr + c, coef * (double)qv[m]);
+                if (j >= cs) atomicAdd(dkr + c, coef * (double)qv[m]);
             }
         }
         if (sel) {
@@ -256,7 +261,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_bwd_gather(Args a) {
             const double f = a.u[bl + j] - tau;
             if (f > 0.0 && f < 1.0) {
                 gsum += gm;
-                if (lane == 0) atomicAdd(a.colsum + bl + j, gm);
+                if (lane == 0 && j >= cs) atomicAdd(a.colsum + bl + j, gm);
             }
         }
     });
@@ -293,6 +298,7 @@ Args make_args(const skb_attn_desc& d, const SelView& s) {
     a.scale = d.scale > 0.0 ? d.scale : 1.0 / std::sqrt((double)d.head_dim);
     a.key_soft = d.key_mode;
     a.mask_st = d.mask_mode;
+    a.chunk_len = (int)d.chunk_len;
     return a;
 }
 

@@ -68,6 +68,7 @@ struct BwdArgs {
     int B, L, H, w, T, R1;
     float scale, scale_log2;
     int mask_st;
+    int chunk_len;  // 0 = one chunk
 };
 
 // One (b, i, h) row per D/8 threads: 16-byte loads of O and dO, a
@@ -170,7 +171,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_tc(const __grid_consta
     if (threadIdx.x < 128) {  // warps 0-3 cover the 128 keys
         const int key = key_of(threadIdx.x);
         int hi = 0;
-        if (key >= 0) hi = SEL ? __ldg(a.leave + bl + key) + a.w : key + a.w;  // exclusive
+        if (key >= 0) {
+            hi = SEL ? __ldg(a.leave + bl + key) + a.w : key + a.w;  // exclusive
+            if (a.chunk_len > 0) hi = min(hi, (key / a.chunk_len + 1) * a.chunk_len);
+        }
         hi = warp_max_i(hi);
         if (lane == 0) atomicMax(&s_range[1], hi);
     }
@@ -305,7 +309,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_tc(const __grid_consta
         // queries reading this key form one interval: window [j, j+w), selected
         // [j+w, leave_j+w) (proj/src/cache.cpp:259-311)
         const int lo_i = SEL ? key + a.w : key;
-        const int hi_i = min(a.L, SEL ? leave + a.w : key + a.w);  // exclusive
+        int hi_i = min(a.L, SEL ? leave + a.w : key + a.w);  // exclusive
+        // chunk-wise training: gradients never cross to the left of a chunk
+        // start, so a key only hears from queries of its own chunk
+        // (proj/src/attention.cpp:228-234, 284-300)
+        if (a.chunk_len > 0 && key >= 0) hi_i = min(hi_i, (key / a.chunk_len + 1) * a.chunk_len);
         float colsum = 0.f;
         for (int qt = 0; qt < nq; ++qt) {
             const int s = qt & 1, qs3 = qt % kQS;
@@ -887,6 +895,7 @@ void run_attn_bwd_tc(const skb_attn_desc& d, const void* q, const void* k, const
     a.scale = (float)scale;
     a.scale_log2 = (float)(scale * 1.4426950408889634);
     a.mask_st = d.mask_mode;
+    a.chunk_len = (int)d.chunk_len;
     const int64_t rows = d.batch * d.seq_len * d.heads;
     const unsigned pg = (unsigned)cdiv(rows * (d.head_dim / 8), 256);
     if (d.head_dim == 128)

@@ -56,7 +56,7 @@ k_mean_prefix(const double* __restrict__ rowsum, const int* __restrict__ nfrac,
 
 __global__ void k_jvp(const double* __restrict__ u, const double* __restrict__ tau,
                       const double* __restrict__ colsum, const double* __restrict__ M, int L, int T,
-                      double* __restrict__ du) {
+                      int w, int chunk_len, double* __restrict__ du) {
     const int b = blockIdx.y;
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= L) return;
@@ -83,7 +83,10 @@ __global__ void k_jvp(const double* __restrict__ u, const double* __restrict__ t
         if (!(uj - tb[mid] > 0.0)) hi = mid;
         else lo = mid + 1;
     }
-    const int ta = lo;
+    int ta = lo;
+    // chunk-wise training: only queries of j's own chunk (i < chunk end, i.e.
+    // t < chunk end - w) spread gradient to j (proj/src/attention.cpp:472)
+    if (chunk_len > 0) ta = min(ta, max(j, (j / chunk_len + 1) * chunk_len - w));
     const double* Mb = M + (int64_t)b * (L + 1);
     const double sub = tc < ta ? Mb[ta] - Mb[tc] : 0.0;
     du[bl + j] = colsum[bl + j] - sub;
@@ -123,7 +126,7 @@ void run_jvp(const skb_attn_desc& d, const double* u, const SelView& s, const do
     k_mean_prefix<<<B, 1024, 0, st>>>(rowsum, s.nfrac, s.tau, L, T, mean_prefix);
     SKB_CHECK_LAUNCH();
     dim3 g((unsigned)cdiv(L, 256), B);
-    k_jvp<<<g, 256, 0, st>>>(u, s.tau, colsum, mean_prefix, L, T, du);
+    k_jvp<<<g, 256, 0, st>>>(u, s.tau, colsum, mean_prefix, L, T, (int)d.window, (int)d.chunk_len, du);
     SKB_CHECK_LAUNCH();
 }
 

@@ -159,6 +159,31 @@ k_score_pullback(const double* __restrict__ gu, const double* __restrict__ raw,
     }
 }
 
+// Chunk-wise training: graw[j2] only collects from j >= j2 in j2's own chunk
+// (proj/src/attention.cpp:491, `for j2 = cs_of[j] ..`): one thread per
+// (sequence, chunk) runs the suffix sums backwards over its chunk.
+__global__ void k_score_pullback_chunked(const double* __restrict__ gu, const double* __restrict__ raw,
+                                         const double* __restrict__ mean, const double* __restrict__ sdev, int L,
+                                         int chunk_len, int nchunks, double* __restrict__ graw) {
+    const int b = blockIdx.y;
+    const int ch = blockIdx.x * blockDim.x + threadIdx.x;
+    if (ch >= nchunks) return;
+    const int64_t bl = (int64_t)b * L;
+    const int lo = ch * chunk_len, hi = min(L, lo + chunk_len);
+    double rA = 0.0, rB = 0.0, rC = 0.0;
+    for (int j = hi - 1; j >= lo; --j) {
+        const double g = gu[bl + j];
+        const double s = sdev[bl + j], mu = mean[bl + j];
+        const double cnt = (double)(j + 1);
+        const double coef = g / s;
+        const double y = (raw[bl + j] - mu) / s;
+        rA += coef / cnt;
+        rB += coef * y / (cnt * s);
+        rC += coef * y / (cnt * s) * mu;
+        graw[bl + j] = coef - rA - raw[bl + j] * rB + rC;
+    }
+}
+
 // dw_score[c] = sum_{b,j} graw[b,j] * x[b,j,c]: column blocks x row slabs, atomics across slabs.
 template <class S>
 __global__ void k_dw_score(const S* __restrict__ x, const double* __restrict__ graw, int64_t rows,
@@ -240,7 +265,14 @@ void run_score_bwd(int64_t B, int64_t L, int64_t D, int32_t xdt, const void* x, 
                    const skb_scoring& sc, const double* gu, const double* raw, const double* mean,
                    const double* sdev, double* graw, double* dw, void* dx, cudaStream_t st) {
     const int64_t rows = B * L;
-    k_score_pullback<<<(unsigned)B, 1024, 0, st>>>(gu, raw, mean, sdev, (int)L, sc.norm_mode, graw);
+    SKB_REQUIRE(sc.chunk_len >= 0, SKB_EARG, "chunked_forward: chunk_len must be positive");
+    if (sc.norm_mode != 0 && sc.chunk_len > 0 && sc.chunk_len < L) {
+        const int nch = (int)cdiv(L, sc.chunk_len);
+        k_score_pullback_chunked<<<dim3((unsigned)cdiv(nch, 128), (unsigned)B), 128, 0, st>>>(
+            gu, raw, mean, sdev, (int)L, sc.chunk_len, nch, graw);
+    } else {
+        k_score_pullback<<<(unsigned)B, 1024, 0, st>>>(gu, raw, mean, sdev, (int)L, sc.norm_mode, graw);
+    }
     SKB_CHECK_LAUNCH();
     if (dw) {
         SKB_CHECK_CUDA(cudaMemsetAsync(dw, 0, D * sizeof(double), st));

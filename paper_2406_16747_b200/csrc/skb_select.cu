@@ -578,6 +578,7 @@ void validate_desc(const skb_attn_desc& d) {
                 "mask_mode must be 'soft' or 'straight_through'");
     SKB_REQUIRE(d.dtype == SKB_F32 || d.dtype == SKB_BF16 || d.dtype == SKB_F64, SKB_EARG,
                 "attention: unsupported dtype");
+    SKB_REQUIRE(d.chunk_len >= 0, SKB_EARG, "chunked_forward: chunk_len must be positive");
 }
 
 void run_select(const skb_attn_desc& d, const double* u, void* ws, cudaStream_t st) {

@@ -35,6 +35,7 @@ class AttnConfig:
     key_mode: str = "hard"       # "hard" | "soft"
     mask_mode: str = "soft"      # "soft" | "straight_through"
     force_gather: bool = False   # BF16 on the CUDA-core gather kernels
+    chunk_len: int = 0           # chunked_forward (Algorithm 3): backward stop-grad at chunk starts
 
     def key_code(self):
         if self.key_mode not in ("hard", "soft"):
@@ -51,8 +52,11 @@ def make_desc(B, L, H, p, cfg: AttnConfig, dtype: torch.dtype) -> AttnDesc:
     if dtype not in _DT:
         raise _lib.ArgumentError(f"unsupported dtype {dtype}")
     flags = _lib.SKB_FLAG_FORCE_GATHER if cfg.force_gather else 0
+    if cfg.chunk_len < 0:
+        raise _lib.ArgumentError("chunked_forward: chunk_len must be positive")
     return AttnDesc(int(B), int(L), int(H), int(p), float(cfg.k), int(cfg.window),
-                    float(cfg.scale), cfg.key_code(), cfg.mask_code(), _DT[dtype], flags)
+                    float(cfg.scale), cfg.key_code(), cfg.mask_code(), _DT[dtype], flags,
+                    int(cfg.chunk_len))
 
 
 def _check_qkv(q, k, v):
@@ -213,11 +217,12 @@ class ScoringConfig:
     slope_enabled: bool = True
     norm_mode: str = "timestep_norm"      # "timestep_norm" | "none"
     slope_order: str = "norm_then_slope"  # "norm_then_slope" | "slope_then_norm"
+    chunk_len: int = 0                    # backward: norm pullback kept inside each chunk
 
     def c(self):
         return Scoring(int(self.norm_mode == "timestep_norm"),
                        int(self.slope_order == "norm_then_slope"), int(bool(self.slope_enabled)),
-                       0, float(self.slope_eps))
+                       int(self.chunk_len), float(self.slope_eps))
 
 
 def score_fwd(x: torch.Tensor, w: torch.Tensor, sc: ScoringConfig):
