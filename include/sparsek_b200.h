@@ -201,6 +201,15 @@ int skb_stream_push(skb_stream* s, const double* z, int64_t n, double* tau_out,
 int skb_stream_query(skb_stream* s, skb_stream_info* out, void* stream);
 /* Host copies: survivor values/indices in ascending index order (|survivors|
  * entries) and the evicted flag of every pushed index (t entries). */
+/* The reference's stream wire format (StreamState::serialize/deserialize,
+ * proj/src/stream.cpp:224-289; little-endian k, heap_cap, tau, t, sum_s,
+ * sum_f, cap_drops, heap_ops, pushes_since_refresh, heap S, heap F, evicted
+ * bits). serialize: out == NULL returns the size in *bytes; the heaps are
+ * written in (value asc, index desc) order, a valid heap for the reference's
+ * HeapCmp. deserialize: a blob of either origin -> a new device stream with
+ * room for `capacity` pushes in total. */
+int skb_stream_serialize(skb_stream* s, uint8_t* out, size_t* bytes, void* stream);
+int skb_stream_deserialize(const uint8_t* data, size_t bytes, int64_t capacity, skb_stream** out);
 int skb_stream_survivors(skb_stream* s, double* values, int64_t* indices, uint8_t* evicted,
                          void* stream);
 

@@ -290,6 +290,27 @@ class Reference:
                                          surv.ctypes.data_as(C.POINTER(C.c_uint64)), _d(p_last)))
         return tau, ins.astype(bool), surv.astype(np.int64), p_last
 
+    def stream_blob(self, z, k, heap_cap=0):
+        """StreamState::serialize after pushing z (proj/src/stream.cpp:224-252)."""
+        z = np.ascontiguousarray(z, np.float64)
+        used = C.c_uint64()
+        self._rc(self.lib.ref_stream_blob(_d(z), C.c_uint64(len(z)), C.c_double(k),
+                                          C.c_uint64(heap_cap), None, C.c_uint64(0), C.byref(used)))
+        buf = (C.c_uint8 * used.value)()
+        self._rc(self.lib.ref_stream_blob(_d(z), C.c_uint64(len(z)), C.c_double(k),
+                                          C.c_uint64(heap_cap), buf, C.c_uint64(used.value),
+                                          C.byref(used)))
+        return bytes(buf)
+
+    def stream_resume(self, blob, z):
+        """StreamState::deserialize(blob), push z; per-push tau."""
+        z = np.ascontiguousarray(z, np.float64)
+        tau = np.zeros(len(z))
+        buf = (C.c_uint8 * len(blob)).from_buffer_copy(blob)
+        self._rc(self.lib.ref_stream_resume(buf, C.c_uint64(len(blob)), _d(z), C.c_uint64(len(z)),
+                                            _d(tau)))
+        return tau
+
     def attention(self, x, wq, wk, wv, wo, w_score, cfg, use_float=False, grad_out=None,
                   chunk_len=0):
         """Forward with tape (+ backward when grad_out is given); chunk_len > 0

@@ -132,6 +132,32 @@ int ref_stream_run(const double* z, uint64_t n, double k, uint64_t heap_cap, dou
     REF_GUARD_END
 }
 
+// StreamState::serialize after pushing z[0..n): *used = blob size (out may be
+// null to query it; cap = out capacity).
+int ref_stream_blob(const double* z, uint64_t n, double k, uint64_t heap_cap, uint8_t* out,
+                    uint64_t cap, uint64_t* used) {
+    REF_GUARD_BEGIN
+    StreamState st{KBudget(k), heap_cap};
+    for (uint64_t t = 0; t < n; ++t) st.push(z[t]);
+    std::vector<std::uint8_t> blob;
+    st.serialize(blob);
+    *used = blob.size();
+    if (out) {
+        if (cap < blob.size()) throw ArgumentError("ref_stream_blob: buffer too small");
+        std::memcpy(out, blob.data(), blob.size());
+    }
+    REF_GUARD_END
+}
+
+// StreamState::deserialize(blob), then push z[0..n) and report each tau.
+int ref_stream_resume(const uint8_t* blob, uint64_t len, const double* z, uint64_t n,
+                      double* tau_out) {
+    REF_GUARD_BEGIN
+    StreamState st = StreamState::deserialize(blob, len, nullptr);
+    for (uint64_t t = 0; t < n; ++t) tau_out[t] = st.push(z[t]).tau;
+    REF_GUARD_END
+}
+
 }  // extern "C"
 
 namespace {

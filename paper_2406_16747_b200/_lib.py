@@ -102,6 +102,8 @@ _SIGS = {
     "skb_stream_push": ([_vp, _vp, C.c_int64, _vp, _vp, _vp], C.c_int),
     "skb_stream_query": ([_vp, C.POINTER(StreamInfo), _vp], C.c_int),
     "skb_stream_survivors": ([_vp, _vp, _vp, _vp, _vp], C.c_int),
+    "skb_stream_serialize": ([_vp, _vp, C.POINTER(C.c_size_t), _vp], C.c_int),
+    "skb_stream_deserialize": ([_vp, C.c_size_t, C.c_int64, C.POINTER(_vp)], C.c_int),
 }
 
 _lock = threading.Lock()

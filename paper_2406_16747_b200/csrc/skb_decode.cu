@@ -34,6 +34,7 @@
 // reference by rounding (never the selected set).
 #include <algorithm>
 #include <cfloat>
+#include <cstring>
 #include <type_traits>
 #include <vector>
 
@@ -870,6 +871,154 @@ int skb_stream_query(skb_stream* s, skb_stream_info* out, void* stream) {
     out->cap_drops = c.cap_drops;
     out->heap_ops = c.heap_ops;
     out->k = c.k;
+    K5_END
+}
+
+int skb_stream_serialize(skb_stream* s, uint8_t* out, size_t* bytes, void* stream) {
+    K5_BEGIN
+    SKB_REQUIRE(s != nullptr && bytes != nullptr, SKB_EARG, "stream_serialize: null argument");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    StreamCtl c;
+    SKB_CHECK_CUDA(cudaMemcpyAsync(&c, s->ctl, sizeof(c), cudaMemcpyDeviceToHost, st));
+    SKB_CHECK_CUDA(cudaStreamSynchronize(st));
+    const size_t need = 8 * 9 + 8 + (size_t)c.nS * 16 + 8 + (size_t)c.nF * 16 + 8 + (size_t)(c.t + 7) / 8;
+    if (!out) {
+        *bytes = need;
+        return SKB_OK;
+    }
+    SKB_REQUIRE(*bytes >= need, SKB_EARG, "stream_serialize: buffer too small");
+    std::vector<double> sv(c.nS), fv(c.nF);
+    std::vector<int> si(c.nS), fi(c.nF);
+    std::vector<uint8_t> ev(c.t);
+    if (c.nS) {
+        SKB_CHECK_CUDA(cudaMemcpyAsync(sv.data(), s->arr.sv, c.nS * 8, cudaMemcpyDeviceToHost, st));
+        SKB_CHECK_CUDA(cudaMemcpyAsync(si.data(), s->arr.si, c.nS * 4, cudaMemcpyDeviceToHost, st));
+    }
+    if (c.nF) {
+        SKB_CHECK_CUDA(cudaMemcpyAsync(fv.data(), s->arr.fv, c.nF * 8, cudaMemcpyDeviceToHost, st));
+        SKB_CHECK_CUDA(cudaMemcpyAsync(fi.data(), s->arr.fi, c.nF * 4, cudaMemcpyDeviceToHost, st));
+    }
+    if (c.t) SKB_CHECK_CUDA(cudaMemcpyAsync(ev.data(), s->arr.evicted, c.t, cudaMemcpyDeviceToHost, st));
+    SKB_CHECK_CUDA(cudaStreamSynchronize(st));
+    size_t off = 0;
+    auto put = [&](const void* p, size_t n) {
+        std::memcpy(out + off, p, n);
+        off += n;
+    };
+    const uint64_t hc = (uint64_t)c.heap_cap, tt = (uint64_t)c.t, psr = (uint64_t)c.since_refresh;
+    put(&c.k, 8);
+    put(&hc, 8);
+    put(&c.tau, 8);
+    put(&tt, 8);
+    put(&c.sum_s, 8);
+    put(&c.sum_f, 8);
+    put(&c.cap_drops, 8);
+    put(&c.heap_ops, 8);
+    put(&psr, 8);
+    auto put_heap = [&](const std::vector<double>& v, const std::vector<int>& ix) {
+        const uint64_t n = v.size();
+        put(&n, 8);
+        for (size_t r = v.size(); r-- > 0;) {  // (value asc, index desc): a valid HeapCmp heap
+            const uint64_t i64 = (uint64_t)ix[r];
+            put(&v[r], 8);
+            put(&i64, 8);
+        }
+    };
+    put_heap(sv, si);
+    put_heap(fv, fi);
+    put(&tt, 8);
+    for (int64_t i = 0; i < c.t; i += 8) {
+        uint8_t byte = 0;
+        for (int b = 0; b < 8 && i + b < c.t; ++b)
+            if (ev[i + b]) byte |= (uint8_t)(1u << b);
+        put(&byte, 1);
+    }
+    *bytes = off;
+    K5_END
+}
+
+int skb_stream_deserialize(const uint8_t* data, size_t bytes, int64_t capacity, skb_stream** out) {
+    K5_BEGIN
+    SKB_REQUIRE(data != nullptr && out != nullptr, SKB_EARG, "stream_deserialize: null argument");
+    size_t off = 0;
+    auto get = [&](void* p, size_t n) {
+        SKB_REQUIRE(off + n <= bytes, SKB_EIO, "stream state: truncated buffer");
+        std::memcpy(p, data + off, n);
+        off += n;
+    };
+    double k, tau, sum_s, sum_f;
+    uint64_t heap_cap, t, cap_drops, heap_ops, psr;
+    get(&k, 8);
+    get(&heap_cap, 8);
+    get(&tau, 8);
+    get(&t, 8);
+    get(&sum_s, 8);
+    get(&sum_f, 8);
+    get(&cap_drops, 8);
+    get(&heap_ops, 8);
+    get(&psr, 8);
+    auto get_heap = [&](std::vector<std::pair<double, int64_t>>& h) {
+        uint64_t n;
+        get(&n, 8);
+        SKB_REQUIRE(n <= bytes / 16, SKB_EIO, "stream state: truncated buffer");
+        h.resize(n);
+        for (auto& e : h) {
+            uint64_t ix;
+            get(&e.first, 8);
+            get(&ix, 8);
+            e.second = (int64_t)ix;
+        }
+        // device layout: (value desc, index asc)
+        std::sort(h.begin(), h.end(), [](const auto& a, const auto& b) {
+            return a.first > b.first || (a.first == b.first && a.second < b.second);
+        });
+    };
+    std::vector<std::pair<double, int64_t>> hs, hf;
+    get_heap(hs);
+    get_heap(hf);
+    uint64_t nbits;
+    get(&nbits, 8);
+    SKB_REQUIRE(nbits == t, SKB_EIO, "stream state: evicted bits do not cover the pushes");
+    std::vector<uint8_t> ev(nbits);
+    for (uint64_t i = 0; i < nbits; i += 8) {
+        uint8_t byte;
+        get(&byte, 1);
+        for (uint64_t b = 0; b < 8 && i + b < nbits; ++b) ev[i + b] = (byte >> b) & 1u;
+    }
+    SKB_REQUIRE(capacity >= (int64_t)t, SKB_EARG, "stream_deserialize: capacity below the pushes so far");
+    skb_stream* s = nullptr;
+    int rc = skb_stream_create(k, (int64_t)heap_cap, std::max<int64_t>(capacity, 1), &s);
+    if (rc != SKB_OK) return rc;
+    StreamCtl c{};
+    c.k = k;
+    c.tau = tau;
+    c.sum_s = sum_s;
+    c.sum_f = sum_f;
+    c.t = (long long)t;
+    c.heap_cap = (long long)heap_cap;
+    c.heap_ops = heap_ops;
+    c.cap_drops = cap_drops;
+    c.nS = (int)hs.size();
+    c.nF = (int)hf.size();
+    c.since_refresh = (int)psr;
+    c.cap = (int)s->capacity;
+    std::vector<double> v(std::max(hs.size(), hf.size()));
+    std::vector<int> ix(v.size());
+    auto upload = [&](const std::vector<std::pair<double, int64_t>>& h, double* dv, int* di) {
+        for (size_t i = 0; i < h.size(); ++i) {
+            v[i] = h[i].first;
+            ix[i] = (int)h[i].second;
+        }
+        if (!h.empty()) {
+            SKB_CHECK_CUDA(cudaMemcpy(dv, v.data(), h.size() * 8, cudaMemcpyHostToDevice));
+            SKB_CHECK_CUDA(cudaMemcpy(di, ix.data(), h.size() * 4, cudaMemcpyHostToDevice));
+        }
+    };
+    upload(hs, s->arr.sv, s->arr.si);
+    upload(hf, s->arr.fv, s->arr.fi);
+    if (t) SKB_CHECK_CUDA(cudaMemcpy(s->arr.evicted, ev.data(), t, cudaMemcpyHostToDevice));
+    SKB_CHECK_CUDA(cudaMemcpy(s->ctl, &c, sizeof(c), cudaMemcpyHostToDevice));
+    *out = s;
     K5_END
 }
 

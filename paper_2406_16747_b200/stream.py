@@ -37,6 +37,31 @@ class Stream:
             except Exception:
                 pass
 
+    def serialize(self) -> bytes:
+        """The reference's wire format (StreamState::serialize,
+        proj/src/stream.cpp:224-252): readable by StreamState::deserialize."""
+        n = C.c_size_t()
+        lib = _lib.load()
+        st = torch.cuda.current_stream().cuda_stream
+        check(lib.skb_stream_serialize(self._h, None, C.byref(n), st))
+        buf = (C.c_uint8 * n.value)()
+        check(lib.skb_stream_serialize(self._h, buf, C.byref(n), st))
+        return bytes(buf)[: n.value]
+
+    @classmethod
+    def deserialize(cls, blob: bytes, capacity=1 << 16):
+        """A stream from a blob of the reference's format (either origin)."""
+        self = cls.__new__(cls)
+        self._cap = int(capacity)
+        self._h = C.c_void_p()
+        buf = (C.c_uint8 * len(blob)).from_buffer_copy(blob)
+        check(_lib.load().skb_stream_deserialize(buf, len(blob), self._cap, C.byref(self._h)))
+        self._k = self._info().k
+        self._dev = torch.device("cuda", torch.cuda.current_device())
+        self._tau = torch.empty(1, dtype=torch.float64, device=self._dev)
+        self._ins = torch.empty(1, dtype=torch.uint8, device=self._dev)
+        return self
+
     def _info(self):
         info = _lib.StreamInfo()
         check(_lib.load().skb_stream_query(self._h, C.byref(info),

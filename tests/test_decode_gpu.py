@@ -210,3 +210,34 @@ def test_stream_rejection_is_permanent(cuda):
     assert not r["inserted"] and st.is_evicted(st.t - 1)
     sol = st.solution()
     assert sol["p"][st.t - 1] == 0.0
+
+
+@pytest.mark.parametrize("kind", ["iid", "ties", "recency"])
+def test_stream_wire_format_interop(cuda, reference, kind):
+    """The device stream speaks the reference's StreamState wire format
+    (proj/src/stream.cpp:224-289) both ways, and resuming from a blob gives the
+    same taus as never stopping (bit for bit)."""
+    import paper_2406_16747_b200 as sparsek
+
+    rng = np.random.default_rng(21)
+    z = _scores(rng, 300, kind)
+    k, n1 = 7.5, 180
+    tau_all, _, _, _ = reference.stream(z, k)
+    # ours -> reference
+    st = sparsek.Stream(k)
+    for x in z[:n1]:
+        st.push(x)
+    blob = st.serialize()
+    tau_ref_resumed = reference.stream_resume(blob, z[n1:])
+    np.testing.assert_array_equal(tau_ref_resumed, tau_all[n1:])
+    # reference -> ours
+    st2 = sparsek.Stream.deserialize(reference.stream_blob(z[:n1], k))
+    got = []
+    for x in z[n1:]:
+        r = st2.push(x)
+        got.append(r["tau"] if r["tau"] is not None else -np.inf)
+    np.testing.assert_array_equal(np.asarray(got), tau_all[n1:])
+    # ours -> ours
+    st3 = sparsek.Stream.deserialize(blob)
+    got3 = [st3.push(x)["tau"] for x in z[n1:]]
+    np.testing.assert_array_equal(np.asarray(got3, dtype=float), tau_all[n1:])
