@@ -125,6 +125,14 @@ int skb_version(void);
 int skb_score_fwd(int64_t B, int64_t L, int64_t D, int32_t x_dtype, const void* x,
                   const double* w, const skb_scoring* sc, double* raw, double* u, double* mean,
                   double* sdev, void* stream);
+/* Incremental scoring (score_tokens with base_pos: the TimestepNormState is
+ * carried across calls, proj/include/sparsek/selection.hpp:55-56,
+ * proj/src/selection.cpp:13-31): x [B, n, D] continues each sequence's
+ * float64 state [B, 3] = {count, mean, m2} (zeros for a fresh sequence);
+ * raw/u float64 [B, n]. Bit-identical to the reference for identical x and w. */
+int skb_score_continue(int64_t B, int64_t n, int64_t D, int32_t x_dtype, const void* x,
+                       const double* w, const skb_scoring* sc, double* state, double* raw,
+                       double* u, void* stream);
 /* gu: float64 [B, L] -> graw [B, L]; dw_score float64 [D] (= sum over B and
  * positions of graw * x); dx (optional, x_dtype [B, L, D]) += graw * w. */
 int skb_score_bwd(int64_t B, int64_t L, int64_t D, int32_t x_dtype, const void* x,

@@ -8,6 +8,7 @@ API and Python bindings over hand-written sm_100a kernels.
 """
 from ._lib import ArgumentError, ConfigError, IoError, NumericError, ShapeError  # noqa: F401
 from .api import (  # noqa: F401
+    DecodeSession,
     Stream,
     __version__,
     attention,
@@ -21,7 +22,7 @@ from .api import (  # noqa: F401
 from . import ops  # noqa: F401
 
 __all__ = [
-    "ArgumentError", "ConfigError", "NumericError", "ShapeError", "IoError", "Stream",
+    "ArgumentError", "ConfigError", "DecodeSession", "NumericError", "ShapeError", "IoError", "Stream",
     "__version__", "attention", "attention_grads", "chunked_forward", "dense_attention", "sparsek", "sparsek_jvp",
     "topk_hard", "ops",
 ]

@@ -81,6 +81,8 @@ _SIGS = {
     "skb_version": ([], C.c_int),
     "skb_score_fwd": ([C.c_int64, C.c_int64, C.c_int64, C.c_int32, _vp, _vp, C.POINTER(Scoring),
                        _vp, _vp, _vp, _vp, _vp], C.c_int),
+    "skb_score_continue": ([C.c_int64, C.c_int64, C.c_int64, C.c_int32, _vp, _vp, C.POINTER(Scoring),
+                            _vp, _vp, _vp, _vp], C.c_int),
     "skb_score_bwd": ([C.c_int64, C.c_int64, C.c_int64, C.c_int32, _vp, _vp, C.POINTER(Scoring),
                        _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp], C.c_int),
     "skb_select_layout_of": ([C.POINTER(AttnDesc), C.POINTER(SelectLayout)], C.c_int),

@@ -205,6 +205,68 @@ def chunked_forward(x, chunk_len, wq, wk, wv, wo, w_score, k, window, heads=1, k
                      mask_mode=mask_mode, slope_eps=slope_eps, slope_enabled=slope_enabled)
 
 
+class DecodeSession:
+    """x-level generation over a batch of B sequences: SparseKvCache::forward_chunk
+    on a prompt followed by generate_step per new row (proj/src/cache.cpp:195-230,
+    570-577). Device tensors throughout: projections are cuBLAS GEMMs, the score
+    continues a per-sequence TimestepNormState on the device (skb_score_continue),
+    the prompt's outputs come from the batch kernels (K2/K3; the same outputs
+    forward_chunk gives, proj/tests/test_cache.cpp:34-64) and every step is one
+    skb_cache_step (K5) over the constant-(floor(k)+w) pool.
+
+    x rows are [B, D] (step) or [B, n, D] (prefill) in the session dtype; w* are
+    [D, D], w_score [D]."""
+
+    def __init__(self, wq, wk, wv, wo, w_score, cfg: ops.AttnConfig, heads: int, batch: int,
+                 max_len: int, scoring: ops.ScoringConfig = ops.ScoringConfig(), dtype=None):
+        self.wq, self.wk, self.wv, self.wo = wq, wk, wv, wo
+        D = wq.shape[0]
+        if D % heads:
+            raise ConfigError("attention: d_model must be a positive multiple of heads")
+        self.D, self.H, self.p, self.B = D, int(heads), D // int(heads), int(batch)
+        self.cfg, self.sc = cfg, scoring
+        self.dtype = dtype or wq.dtype
+        self.w_score = w_score
+        if cfg.k > 0.0 and (w_score is None or w_score.shape != (D,)):
+            raise ConfigError("attention: w_score length must equal d_model")
+        self.state = torch.zeros((self.B, 3), dtype=torch.float64, device=wq.device)
+        self.cache = ops.DecodeCache(self.B, self.H, self.p, cfg, max_len, dtype=self.dtype,
+                                     device=wq.device)
+        self.t = 0
+
+    def _proj_score(self, x):
+        B, n, D = x.shape
+        q, k, v = ((x @ w).view(B, n, self.H, self.p) for w in (self.wq, self.wk, self.wv))
+        if self.cfg.k > 0.0:
+            _, u = ops.score_continue(x, self.w_score, self.sc, self.state)
+        else:
+            u = torch.zeros((B, n), dtype=torch.float64, device=x.device)
+        return q, k, v, u
+
+    @torch.no_grad()
+    def prefill(self, x):
+        """forward_chunk on a prompt x [B, n, D] (only valid as the first call);
+        returns y [B, n, D]."""
+        if self.t:
+            raise ArgumentError("DecodeSession: prefill must precede generation")
+        B, n, D = x.shape
+        q, k, v, u = self._proj_score(x)
+        hc = ops.sparsek_attention_core(q.contiguous(), k.contiguous(), v.contiguous(),
+                                        u.contiguous(), self.cfg)
+        self.cache.prefill(k.contiguous(), v.contiguous(), u.contiguous())
+        self.t = n
+        return hc.reshape(B, n, D) @ self.wo
+
+    @torch.no_grad()
+    def step(self, x_row):
+        """generate_step: x_row [B, D] -> y [B, D]."""
+        q, k, v, u = self._proj_score(x_row.view(self.B, 1, self.D))
+        o = self.cache.step(q[:, 0].contiguous(), k[:, 0].contiguous(), v[:, 0].contiguous(),
+                            u[:, 0].contiguous())
+        self.t += 1
+        return o.reshape(self.B, self.D) @ self.wo
+
+
 def dense_attention(x, wq, wk, wv, wo, heads=1):
     """Quadratic causal softmax attention (proj/src/attention.cpp:76-111): the
     SparseK kernels with a budget covering every position (all gates 1)."""

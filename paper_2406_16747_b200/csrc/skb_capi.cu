@@ -10,6 +10,8 @@ namespace skb {
 void run_score_fwd(int64_t B, int64_t L, int64_t D, int32_t xdt, const void* x, const double* w,
                    const skb_scoring& sc, double* raw, double* u, double* mean, double* sdev,
                    cudaStream_t st);
+void run_score_continue(int64_t B, int64_t n, int64_t D, int32_t xdt, const void* x, const double* w,
+                        const skb_scoring& sc, double* state, double* raw, double* u, cudaStream_t st);
 void run_score_bwd(int64_t B, int64_t L, int64_t D, int32_t xdt, const void* x, const double* w,
                    const skb_scoring& sc, const double* gu, const double* raw, const double* mean,
                    const double* sdev, double* graw, double* dw, void* dx, cudaStream_t st);
@@ -61,6 +63,19 @@ int skb_score_fwd(int64_t B, int64_t L, int64_t D, int32_t x_dtype, const void* 
     NONNULL(mean, "score_fwd mean");
     NONNULL(sdev, "score_fwd sdev");
     skb::run_score_fwd(B, L, D, x_dtype, x, w, *sc, raw, u, mean, sdev, S(stream));
+    SKB_API_END
+}
+
+int skb_score_continue(int64_t B, int64_t n, int64_t D, int32_t x_dtype, const void* x, const double* w,
+                       const skb_scoring* sc, double* state, double* raw, double* u, void* stream) {
+    SKB_API_BEGIN
+    NONNULL(x, "score_continue x");
+    NONNULL(w, "score_continue w");
+    NONNULL(sc, "score_continue scoring");
+    NONNULL(state, "score_continue state");
+    NONNULL(raw, "score_continue raw");
+    NONNULL(u, "score_continue u");
+    skb::run_score_continue(B, n, D, x_dtype, x, w, *sc, state, raw, u, S(stream));
     SKB_API_END
 }
 

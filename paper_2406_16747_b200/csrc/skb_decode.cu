@@ -255,8 +255,8 @@ struct CacheArgs {
     int* pos_of;        // [B, S]    slot -> position (-1 = free)
     int* free_stack;    // [B, S]
     int* att_slot;      // [B, S]    attended slots of the current step
-    float* att_kg;      // [B, S]    logit multiplier (gate under soft keys, else 1)
-    float* att_vg;      // [B, S]    value weight (gate under soft mask, else 1)
+    double* att_kg;     // [B, S]    logit multiplier (gate under soft keys, else 1)
+    double* att_vg;     // [B, S]    value weight (gate under soft mask, else 1)
     int* att_n;         // [B]
     uint8_t* kpool;     // [B, S, H, p] dtype
     uint8_t* vpool;
@@ -336,10 +336,10 @@ __device__ void warp_cache_advance(const CacheArgs& A, int b, CacheCtl& c, doubl
         const int ns = c.nsel;
         for (int r = lane; r < ns; r += 32) {
             const int jp = sa.si[r];
-            const float g = (float)fmin(1.0, fmax(0.0, sa.sv[r] - tau));
+            const double g = fmin(1.0, fmax(0.0, sa.sv[r] - tau));
             A.att_slot[bS + r] = A.slot_of[bL + jp];
-            A.att_kg[bS + r] = A.key_soft ? g : 1.f;
-            A.att_vg[bS + r] = A.mask_st ? 1.f : g;
+            A.att_kg[bS + r] = A.key_soft ? g : 1.0;
+            A.att_vg[bS + r] = A.mask_st ? 1.0 : g;
         }
         int n = ns;
         if (A.w > 0) {
@@ -347,8 +347,8 @@ __device__ void warp_cache_advance(const CacheArgs& A, int b, CacheCtl& c, doubl
             for (int jp = r0 + lane; jp <= pos; jp += 32) {
                 const int r = ns + (jp - r0);
                 A.att_slot[bS + r] = A.slot_of[bL + jp];
-                A.att_kg[bS + r] = 1.f;
-                A.att_vg[bS + r] = 1.f;
+                A.att_kg[bS + r] = 1.0;
+                A.att_vg[bS + r] = 1.0;
             }
             n += pos - r0 + 1;
         }
@@ -360,8 +360,8 @@ __device__ void warp_cache_advance(const CacheArgs& A, int b, CacheCtl& c, doubl
             if (!selected) {
                 if (lane == 0) {
                     A.att_slot[bS + n] = slot;
-                    A.att_kg[bS + n] = 1.f;
-                    A.att_vg[bS + n] = 1.f;
+                    A.att_kg[bS + n] = 1.0;
+                    A.att_vg[bS + n] = 1.0;
                 }
                 n += 1;
             }
@@ -473,23 +473,34 @@ __device__ __forceinline__ void ldv(const float* p, float* o) {
     }
 }
 template <int VEC>
-__device__ __forceinline__ void ldv(const double* p, float* o) {
+__device__ __forceinline__ void ldv(const double* p, double* o) {
 #pragma unroll
-    for (int e = 0; e < VEC; ++e) o[e] = (float)p[e];
+    for (int e = 0; e < VEC; ++e) o[e] = p[e];
 }
+// float64 pools accumulate in float64 (the reference's double build), the
+// others in float32
+template <class T>
+using AccOf = typename std::conditional<std::is_same<T, double>::value, double, float>::type;
+__device__ __forceinline__ float exp_acc(float x) { return expf(x); }
+__device__ __forceinline__ double exp_acc(double x) { return exp(x); }
 
 // CTA = (chunk of kSlotsPerCta attended entries, sequence), all heads. Each
 // (entry, head) row is p contiguous elements; a warp covers it with lanes
 // owning VEC consecutive elements per 32*VEC stride.
 template <class T, int VEC>
 __global__ void __launch_bounds__(kAttnThreads)
-k_cache_attn(CacheArgs A, const T* __restrict__ q, int H, int p, float scale, float* __restrict__ po,
-             float* __restrict__ pm, float* __restrict__ pl, int nsplit) {
-    extern __shared__ float sm[];
-    float* sq = sm;                       // [H * p] query
-    float* sp = sq + H * p;               // [H][kSlotsPerCta] logits -> probabilities
-    int* ss = reinterpret_cast<int*>(sp + H * kSlotsPerCta);  // [kSlotsPerCta] slots
-    float* svg = reinterpret_cast<float*>(ss + kSlotsPerCta);  // value weights
+k_cache_attn(CacheArgs A, const T* __restrict__ q, int H, int p, double scale_d, void* po_,
+             void* pm_, void* pl_, int nsplit) {
+    using Acc = AccOf<T>;
+    Acc* po = static_cast<Acc*>(po_);
+    Acc* pm = static_cast<Acc*>(pm_);
+    Acc* pl = static_cast<Acc*>(pl_);
+    const Acc scale = (Acc)scale_d;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    Acc* sq = reinterpret_cast<Acc*>(smraw);  // [H * p] query
+    Acc* sp = sq + H * p;                     // [H][kSlotsPerCta] logits -> probabilities
+    Acc* svg = sp + H * kSlotsPerCta;         // [kSlotsPerCta] value weights
+    int* ss = reinterpret_cast<int*>(svg + kSlotsPerCta);  // [kSlotsPerCta] slots
     const int b = blockIdx.y, chunk = blockIdx.x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = kAttnThreads / 32;
     const int n = A.att_n[b];
@@ -497,10 +508,10 @@ k_cache_attn(CacheArgs A, const T* __restrict__ q, int H, int p, float scale, fl
     const int ne = max(0, min(kSlotsPerCta, n - e0));
     const int64_t bS = (int64_t)b * A.S;
     const int hp = H * p;
-    for (int i = threadIdx.x; i < hp; i += kAttnThreads) sq[i] = tof(q[(int64_t)b * hp + i]);
+    for (int i = threadIdx.x; i < hp; i += kAttnThreads) sq[i] = (Acc)q[(int64_t)b * hp + i];
     for (int e = threadIdx.x; e < ne; e += kAttnThreads) {
         ss[e] = A.att_slot[bS + e0 + e];
-        svg[e] = A.att_vg[bS + e0 + e];
+        svg[e] = (Acc)A.att_vg[bS + e0 + e];
     }
     __syncthreads();
     const T* kp = reinterpret_cast<const T*>(A.kpool);
@@ -509,43 +520,43 @@ k_cache_attn(CacheArgs A, const T* __restrict__ q, int H, int p, float scale, fl
     const int units = ne * H;
     constexpr int U = 4;
     for (int u0 = warp * U; u0 < units; u0 += nw * U) {
-        float acc[U];
+        Acc acc[U];
 #pragma unroll
-        for (int x = 0; x < U; ++x) acc[x] = 0.f;
+        for (int x = 0; x < U; ++x) acc[x] = 0;
 #pragma unroll
         for (int x = 0; x < U; ++x) {
             const int un = u0 + x;
             if (un < units) {
                 const int e = un / H, h = un % H;
                 const T* kr = kp + ((bS + ss[e]) * H + h) * (int64_t)p;
-                const float* qr = sq + h * p;
+                const Acc* qr = sq + h * p;
                 for (int c = lane * VEC; c < p; c += 32 * VEC) {
-                    float kv[VEC];
+                    Acc kv[VEC];
                     ldv<VEC>(kr + c, kv);
 #pragma unroll
-                    for (int v = 0; v < VEC; ++v) acc[x] = fmaf(qr[c + v], kv[v], acc[x]);
+                    for (int v = 0; v < VEC; ++v) acc[x] = fma(qr[c + v], kv[v], acc[x]);
                 }
             }
         }
 #pragma unroll
         for (int x = 0; x < U; ++x) {
-            const float s = warp_sum(acc[x]);
+            const Acc s = warp_sum(acc[x]);
             const int un = u0 + x;
             if (lane == 0 && un < units) {
                 const int e = un / H, h = un % H;
-                sp[h * kSlotsPerCta + e] = s * scale * A.att_kg[bS + e0 + e];
+                sp[h * kSlotsPerCta + e] = s * scale * (Acc)A.att_kg[bS + e0 + e];
             }
         }
     }
     __syncthreads();
     // per-head softmax over this chunk (partial: max m, sum l of exp(a - m))
     for (int h = warp; h < H; h += nw) {
-        float m = -INFINITY;
-        for (int e = lane; e < ne; e += 32) m = fmaxf(m, sp[h * kSlotsPerCta + e]);
+        Acc m = -INFINITY;
+        for (int e = lane; e < ne; e += 32) m = fmax(m, sp[h * kSlotsPerCta + e]);
         m = warp_max(m);
-        float l = 0.f;
+        Acc l = 0;
         for (int e = lane; e < ne; e += 32) {
-            const float pe = ne > 0 ? expf(sp[h * kSlotsPerCta + e] - m) : 0.f;
+            const Acc pe = ne > 0 ? exp_acc(sp[h * kSlotsPerCta + e] - m) : Acc(0);
             sp[h * kSlotsPerCta + e] = pe;
             l += pe;
         }
@@ -560,29 +571,29 @@ k_cache_attn(CacheArgs A, const T* __restrict__ q, int H, int p, float scale, fl
     // o_partial[h] = sum_e p_e * vg_e * v_e
     for (int h = warp; h < H; h += nw) {
         for (int c0 = lane * VEC; c0 < p; c0 += 32 * VEC) {
-            float acc[VEC];
+            Acc acc[VEC];
 #pragma unroll
-            for (int v = 0; v < VEC; ++v) acc[v] = 0.f;
+            for (int v = 0; v < VEC; ++v) acc[v] = 0;
             int e = 0;
             for (; e + 4 <= ne; e += 4) {
-                float vv[4][VEC];
+                Acc vv[4][VEC];
 #pragma unroll
                 for (int x = 0; x < 4; ++x) ldv<VEC>(vp + ((bS + ss[e + x]) * H + h) * (int64_t)p + c0, vv[x]);
 #pragma unroll
                 for (int x = 0; x < 4; ++x) {
-                    const float w = sp[h * kSlotsPerCta + e + x] * svg[e + x];
+                    const Acc w = sp[h * kSlotsPerCta + e + x] * svg[e + x];
 #pragma unroll
-                    for (int v = 0; v < VEC; ++v) acc[v] = fmaf(w, vv[x][v], acc[v]);
+                    for (int v = 0; v < VEC; ++v) acc[v] = fma(w, vv[x][v], acc[v]);
                 }
             }
             for (; e < ne; ++e) {
-                float vv[VEC];
+                Acc vv[VEC];
                 ldv<VEC>(vp + ((bS + ss[e]) * H + h) * (int64_t)p + c0, vv);
-                const float w = sp[h * kSlotsPerCta + e] * svg[e];
+                const Acc w = sp[h * kSlotsPerCta + e] * svg[e];
 #pragma unroll
-                for (int v = 0; v < VEC; ++v) acc[v] = fmaf(w, vv[v], acc[v]);
+                for (int v = 0; v < VEC; ++v) acc[v] = fma(w, vv[v], acc[v]);
             }
-            float* out = po + (((int64_t)b * nsplit + chunk) * H + h) * p + c0;
+            Acc* out = po + (((int64_t)b * nsplit + chunk) * H + h) * p + c0;
 #pragma unroll
             for (int v = 0; v < VEC; ++v) out[v] = acc[v];
         }
@@ -614,8 +625,8 @@ k_cache_attn_bf16(CacheArgs A, const __nv_bfloat16* __restrict__ q, int H, float
     const int64_t bS = (int64_t)b * A.S;
     for (int e = threadIdx.x; e < ne; e += kAttnThreads) {
         ss[e] = A.att_slot[bS + e0 + e];
-        svg[e] = A.att_vg[bS + e0 + e];
-        skg[e] = A.att_kg[bS + e0 + e] * scale;
+        svg[e] = (float)A.att_vg[bS + e0 + e];
+        skg[e] = (float)A.att_kg[bS + e0 + e] * scale;
     }
     const int nj = H / HPL;
     const int hsub = lane / LPH, dch = (lane % LPH) * 8;
@@ -717,26 +728,29 @@ k_cache_attn_bf16(CacheArgs A, const __nv_bfloat16* __restrict__ q, int H, float
 }
 
 template <class T>
-__global__ void k_cache_combine(const float* __restrict__ po, const float* __restrict__ pm,
-                                const float* __restrict__ pl, const int* __restrict__ att_n, int H, int p,
-                                int nsplit, T* __restrict__ o) {
+__global__ void k_cache_combine(const void* po_, const void* pm_, const void* pl_,
+                                const int* __restrict__ att_n, int H, int p, int nsplit, T* __restrict__ o) {
+    using Acc = AccOf<T>;
+    const Acc* po = static_cast<const Acc*>(po_);
+    const Acc* pm = static_cast<const Acc*>(pm_);
+    const Acc* pl = static_cast<const Acc*>(pl_);
     const int h = blockIdx.x, b = blockIdx.y;
     const int used = min(nsplit, (att_n[b] + kSlotsPerCta - 1) / kSlotsPerCta);
-    float M = -INFINITY;
-    for (int s = 0; s < used; ++s) M = fmaxf(M, pm[((int64_t)b * nsplit + s) * H + h]);
-    float Lsum = 0.f;
+    Acc M = -INFINITY;
+    for (int s = 0; s < used; ++s) M = fmax(M, pm[((int64_t)b * nsplit + s) * H + h]);
+    Acc Lsum = 0;
     for (int s = 0; s < used; ++s) {
         const int64_t i = ((int64_t)b * nsplit + s) * H + h;
-        if (pm[i] > -INFINITY) Lsum += pl[i] * expf(pm[i] - M);
+        if (pm[i] > -INFINITY) Lsum += pl[i] * exp_acc(pm[i] - M);
     }
-    const float inv = Lsum > 0.f ? 1.f / Lsum : 0.f;
+    const Acc inv = Lsum > 0 ? Acc(1) / Lsum : Acc(0);
     for (int c = threadIdx.x; c < p; c += blockDim.x) {
-        float acc = 0.f;
+        Acc acc = 0;
         for (int s = 0; s < used; ++s) {
             const int64_t i = ((int64_t)b * nsplit + s) * H + h;
-            if (pm[i] > -INFINITY) acc += po[i * p + c] * expf(pm[i] - M);
+            if (pm[i] > -INFINITY) acc += po[i * p + c] * exp_acc(pm[i] - M);
         }
-        store_from_f(o + ((int64_t)b * H + h) * p + c, acc * inv);
+        o[((int64_t)b * H + h) * p + c] = (T)(acc * inv);
     }
 }
 
@@ -757,9 +771,9 @@ struct skb_cache {
     CacheArgs A{};
     int nsplit = 0;
     int vec = 1;
-    float* po = nullptr;
-    float* pm = nullptr;
-    float* pl = nullptr;
+    double* po = nullptr;  // split partials: float64 for float64 pools, else float32
+    double* pm = nullptr;
+    double* pl = nullptr;
     std::vector<void*> allocs;
     ~skb_cache() {
         for (void* p : allocs) cudaFree(p);
@@ -1078,17 +1092,17 @@ int skb_cache_create(const skb_attn_desc* d, skb_cache** out) {
         A.pos_of = c->alloc<int>(B * S);
         A.free_stack = c->alloc<int>(B * S);
         A.att_slot = c->alloc<int>(B * S);
-        A.att_kg = c->alloc<float>(B * S);
-        A.att_vg = c->alloc<float>(B * S);
+        A.att_kg = c->alloc<double>(B * S);
+        A.att_vg = c->alloc<double>(B * S);
         A.att_n = c->alloc<int>(B);
         A.kpool = c->alloc<uint8_t>((size_t)(B * S) * A.row_bytes);
         A.vpool = c->alloc<uint8_t>((size_t)(B * S) * A.row_bytes);
         SKB_CHECK_CUDA(cudaMemset(A.kpool, 0, (size_t)(B * S) * A.row_bytes));
         SKB_CHECK_CUDA(cudaMemset(A.vpool, 0, (size_t)(B * S) * A.row_bytes));
         c->nsplit = (int)cdiv(S, kSlotsPerCta);
-        c->po = c->alloc<float>(B * c->nsplit * H * p);
-        c->pm = c->alloc<float>(B * c->nsplit * H);
-        c->pl = c->alloc<float>(B * c->nsplit * H);
+        c->po = c->alloc<double>(B * c->nsplit * H * p);  // sized for float64 partials
+        c->pm = c->alloc<double>(B * c->nsplit * H);
+        c->pl = c->alloc<double>(B * c->nsplit * H);
         c->vec = (p % 128 == 0) ? 4 : (p % 64 == 0) ? 2 : 1;
         k_cache_init<<<(unsigned)B, 256>>>(A, d->k);
         SKB_CHECK_LAUNCH();
@@ -1112,14 +1126,16 @@ template <class T>
 static void cache_attend(skb_cache* c, const void* q, void* o, cudaStream_t st) {
     const skb_attn_desc& d = c->d;
     const int H = (int)d.heads, p = (int)d.head_dim;
-    const float scale = (float)(d.scale > 0.0 ? d.scale : 1.0 / std::sqrt((double)p));
-    const size_t smem = (size_t)H * p * 4 + (size_t)H * kSlotsPerCta * 4 + kSlotsPerCta * 8;
+    const double scale_d = d.scale > 0.0 ? d.scale : 1.0 / std::sqrt((double)p);
+    const float scale = (float)scale_d;
+    const size_t asz = sizeof(AccOf<T>);
+    const size_t smem = (size_t)H * p * asz + (size_t)H * kSlotsPerCta * asz + kSlotsPerCta * (asz + 4);
     SKB_REQUIRE(smem <= 200 * 1024, SKB_ECONFIG, "cache: heads * head_dim too large for the decode kernel");
     dim3 g((unsigned)c->nsplit, (unsigned)d.batch);
     auto launch = [&](auto kern) {
         if (smem > 48 * 1024)
             SKB_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        kern<<<g, kAttnThreads, smem, st>>>(c->A, static_cast<const T*>(q), H, p, scale, c->po, c->pm, c->pl,
+        kern<<<g, kAttnThreads, smem, st>>>(c->A, static_cast<const T*>(q), H, p, scale_d, c->po, c->pm, c->pl,
                                             c->nsplit);
     };
     constexpr bool kBf16 = std::is_same<T, __nv_bfloat16>::value;
@@ -1129,8 +1145,9 @@ static void cache_attend(skb_cache* c, const void* q, void* o, cudaStream_t st) 
         auto run = [&](auto kern) {
             if (fsmem > 48 * 1024)
                 SKB_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem));
-            kern<<<g, kAttnThreads, fsmem, st>>>(c->A, reinterpret_cast<const __nv_bfloat16*>(q), H, scale, c->po,
-                                                 c->pm, c->pl, c->nsplit);
+            kern<<<g, kAttnThreads, fsmem, st>>>(c->A, reinterpret_cast<const __nv_bfloat16*>(q), H, scale,
+                                                 reinterpret_cast<float*>(c->po), reinterpret_cast<float*>(c->pm),
+                                                 reinterpret_cast<float*>(c->pl), c->nsplit);
         };
         if (p == 128) run(k_cache_attn_bf16<128>);
         else run(k_cache_attn_bf16<64>);

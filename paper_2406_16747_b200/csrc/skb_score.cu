@@ -60,6 +60,43 @@ __global__ void k_score_welford(const double* __restrict__ raw, int L, skb_scori
     }
 }
 
+// Incremental scoring for decoding (score_tokens with base_pos, TimestepNormState
+// carried across calls; proj/src/selection.cpp:13-31): n new rows per sequence
+// continue the Welford state [count, mean, m2] exactly as the reference's
+// push does, operation for operation.
+__global__ void k_score_continue(const double* __restrict__ rawv, int n, skb_scoring sc,
+                                 double* __restrict__ state, double* __restrict__ raw_out,
+                                 double* __restrict__ u_out, int* __restrict__ bad) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= gridDim.x * blockDim.x) return;
+    double* stt = state + (int64_t)b * 3;
+    double cnt = stt[0], mu = stt[1], m2 = stt[2];
+    for (int i = 0; i < n; ++i) {
+        const int64_t r = (int64_t)b * n + i;
+        const double rw = rawv[r];
+        if (!isfinite(rw)) *bad = 1;
+        const double slope = sc.slope_enabled ? __dmul_rn(__dadd_rn(cnt, 1.0), sc.slope_eps) : 0.0;
+        if (sc.norm_mode == 0) {
+            raw_out[r] = rw;
+            u_out[r] = __dadd_rn(rw, slope);
+            cnt = __dadd_rn(cnt, 1.0);
+            continue;
+        }
+        const double rin = sc.slope_order == 0 ? __dadd_rn(rw, slope) : rw;
+        cnt = __dadd_rn(cnt, 1.0);
+        const double delta = __dsub_rn(rin, mu);
+        mu = __dadd_rn(mu, __ddiv_rn(delta, cnt));
+        m2 = __dadd_rn(m2, __dmul_rn(delta, __dsub_rn(rin, mu)));
+        const double sd = __dsqrt_rn(__dadd_rn(__ddiv_rn(m2, cnt), 1e-5));
+        const double z = __ddiv_rn(__dsub_rn(rin, mu), sd);
+        raw_out[r] = rin;
+        u_out[r] = sc.slope_order == 0 ? z : __dadd_rn(z, slope);
+    }
+    stt[0] = cnt;
+    stt[1] = mu;
+    stt[2] = m2;
+}
+
 __global__ void k_score_finish(const double* __restrict__ raw_in, int64_t n, int L, skb_scoring sc,
                                double* __restrict__ raw, double* __restrict__ u,
                                double* __restrict__ mean, double* __restrict__ sdev_var,
@@ -253,6 +290,29 @@ void run_score_fwd(int64_t B, int64_t L, int64_t D, int32_t xdt, const void* x, 
     SKB_CHECK_CUDA(cudaMemcpyAsync(raw, u, rows * sizeof(double), cudaMemcpyDeviceToDevice, st));
     k_score_finish<<<(unsigned)cdiv(rows, 256), 256, 0, st>>>(raw, rows, (int)L, sc, raw, u, mean,
                                                              sdev, bad);
+    SKB_CHECK_LAUNCH();
+    int hbad = 0;
+    SKB_CHECK_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+    SKB_CHECK_CUDA(cudaFreeAsync(bad, st));
+    SKB_CHECK_CUDA(cudaStreamSynchronize(st));
+    SKB_REQUIRE(!hbad, SKB_ENUMERIC, "score: non-finite value");
+}
+
+void run_score_continue(int64_t B, int64_t n, int64_t D, int32_t xdt, const void* x, const double* w,
+                        const skb_scoring& sc, double* state, double* raw, double* u, cudaStream_t st) {
+    SKB_REQUIRE(B >= 1 && n >= 1 && D >= 1, SKB_ESHAPE, "score_tokens: empty input");
+    SKB_REQUIRE(sc.slope_eps > 0.0, SKB_EARG, "ScoringParams: slope_eps must be positive");
+    const int64_t rows = B * n;
+    int* bad = nullptr;
+    SKB_CHECK_CUDA(cudaMallocAsync(&bad, sizeof(int), st));
+    SKB_CHECK_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), st));
+    dispatch_x(xdt, [&](auto tag) {
+        using S = std::remove_const_t<std::remove_pointer_t<decltype(tag)>>;
+        k_score_raw<S><<<(unsigned)cdiv(rows, 128), 128, 0, st>>>(static_cast<const S*>(x), w, rows, (int)D, raw);
+    });
+    SKB_CHECK_LAUNCH();
+    // raw holds the dot products; the continuation rewrites raw/u in place
+    k_score_continue<<<(unsigned)B, 1, 0, st>>>(raw, (int)n, sc, state, raw, u, bad);
     SKB_CHECK_LAUNCH();
     int hbad = 0;
     SKB_CHECK_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st));

@@ -242,6 +242,26 @@ def score_fwd(x: torch.Tensor, w: torch.Tensor, sc: ScoringConfig):
     return raw, u, mean, sdev
 
 
+def score_continue(x: torch.Tensor, w: torch.Tensor, sc: ScoringConfig, state: torch.Tensor):
+    """Incremental scoring (score_tokens with a carried TimestepNormState,
+    proj/src/selection.cpp:22-31): x [B, n, D] continues ``state`` (float64
+    [B, 3] = count, mean, m2; updated in place). Returns (raw, u) [B, n]."""
+    if x.dim() != 3:
+        raise _lib.ShapeError("score: x must be [B, L, D]")
+    B, n, D = x.shape
+    if w.shape != (D,):
+        raise _lib.ShapeError("score_tokens: x.cols != w_score length")
+    if state.shape != (B, 3) or state.dtype != torch.float64 or not state.is_contiguous():
+        raise _lib.ArgumentError("score_continue: state must be a contiguous float64 [B, 3]")
+    x = x.contiguous()
+    w = w.to(torch.float64).contiguous()
+    raw, u = (torch.empty((B, n), dtype=torch.float64, device=x.device) for _ in range(2))
+    check(_lib.load().skb_score_continue(B, n, D, _DT[x.dtype], x.data_ptr(), w.data_ptr(), sc.c(),
+                                         state.data_ptr(), raw.data_ptr(), u.data_ptr(),
+                                         _stream()))
+    return raw, u
+
+
 def score_bwd(x, w, sc: ScoringConfig, gu, raw, mean, sdev, dx=None, want_dw=True):
     B, L, D = x.shape
     graw = torch.empty((B, L), dtype=torch.float64, device=x.device)
