@@ -50,7 +50,7 @@ struct BwdArgs {
     CUtensorMap tm_k128, tm_v128;
     const __nv_bfloat16 *q, *k, *v, *dout;
     __nv_bfloat16 *dq, *dk, *dv;
-    float *dk_acc, *dv_acc;  // fp32 partials of the selected pass, [B, L, H, D]
+    float *dk_acc, *dv_acc;  // fp32 partials of the selected pass, 32-key groups (part_off)
     const float* lse2;       // [B, H, L] lse * log2(e)
     const float* delta;      // [B, H, L] rowsum(dO * O)
     const float* uf;
@@ -70,6 +70,15 @@ struct BwdArgs {
     int mask_st;
     int chunk_len;  // 0 = one chunk
 };
+
+// fp32 dK/dV partials of the selected pass, [B][H][ceil(L/32)][D/4][32 keys][4]:
+// the 32 consecutive keys of a warp read or write one 4-column group as 512
+// contiguous bytes (a row-major [L, D] tile would cost one line per thread).
+template <int D>
+__device__ __forceinline__ int64_t part_off(const BwdArgs& a, int b, int h, int key, int c4) {
+    const int ng = (a.L + 31) >> 5;
+    return ((((int64_t)(b * a.H + h) * ng + (key >> 5)) * (D / 4) + c4) * 32 + (key & 31)) * 4;
+}
 
 // One (b, i, h) row per D/8 threads: 16-byte loads of O and dO, a
 // shuffle-reduced dot product, lse converted to log2 units. HBM-bound.
@@ -426,21 +435,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_tc(const __grid_consta
 #pragma unroll
             for (int e = 0; e < 32; ++e) dk[e] *= a.scale;
             if (SEL) {
-                float* pk = a.dk_acc + rowoff + c * 32;
-                float* pv = a.dv_acc + rowoff + c * 32;
 #pragma unroll
                 for (int e = 0; e < 32; e += 4) {
-                    *reinterpret_cast<float4*>(pk + e) = make_float4(dk[e], dk[e + 1], dk[e + 2], dk[e + 3]);
-                    *reinterpret_cast<float4*>(pv + e) = make_float4(dv[e], dv[e + 1], dv[e + 2], dv[e + 3]);
+                    const int64_t po = part_off<D>(a, b, h, key, (col + e) >> 2);
+                    *reinterpret_cast<float4*>(a.dk_acc + po) = make_float4(dk[e], dk[e + 1], dk[e + 2], dk[e + 3]);
+                    *reinterpret_cast<float4*>(a.dv_acc + po) = make_float4(dv[e], dv[e + 1], dv[e + 2], dv[e + 3]);
                 }
             } else {
                 if (has_sel) {
-                    const float* pk = a.dk_acc + rowoff + c * 32;
-                    const float* pv = a.dv_acc + rowoff + c * 32;
 #pragma unroll
                     for (int e = 0; e < 32; e += 4) {
-                        const float4 x = *reinterpret_cast<const float4*>(pk + e);
-                        const float4 y = *reinterpret_cast<const float4*>(pv + e);
+                        const int64_t po = part_off<D>(a, b, h, key, (col + e) >> 2);
+                        const float4 x = *reinterpret_cast<const float4*>(a.dk_acc + po);
+                        const float4 y = *reinterpret_cast<const float4*>(a.dv_acc + po);
                         dk[e] += x.x;
                         dk[e + 1] += x.y;
                         dk[e + 2] += x.z;
@@ -474,6 +481,326 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_tc(const __grid_consta
     __syncthreads();
     tc_after_sync();
     if (warp == kMmaWarp) tmem_dealloc<512>(tmem);
+}
+
+// Window pass, persistent: one CTA per SM walks key tiles wi = blockIdx.x,
+// blockIdx.x + gridDim.x, ... (key tile fastest, so the CTAs in flight share
+// their query tiles in L2). Every ring (Q/dO stages, S buffers) runs on a
+// global counter across work items, so the next item's K/V and first query
+// tiles load while the current item finishes its last dV/dK MMAs and its
+// epilogue; K/V are released by the commit of an item's last S/dP MMA, the
+// dV/dK accumulators by the math warps once they are read out.
+template <int D>
+struct KWSmem {  // KSmem + per-warpgroup staging rows for the coalesced dK/dV stores
+    using K = KSmem<D>;
+    static constexpr int kK = K::kK, kV = K::kV, kQ = K::kQ, kDO = K::kDO, kMeta = K::kMeta, kQT = K::kQT;
+    static constexpr int kPitch = D + 16;          // bytes per staged half row (D/2 bf16) + pad
+    static constexpr int kStgWG = 128 * kPitch;
+    static constexpr int kStg = kMeta + kQS * 3 * 64 * 4;
+    static constexpr int kBar = kStg + 2 * kStgWG;
+    static constexpr int kTmemSlot = kBar + 16 * 8;
+    static constexpr int kAlloc = kTmemSlot + 16 + 1024;
+};
+enum { KW_KVFULL = 0, KW_KVEMPTY = 1, KW_QDFULL = 2, KW_QDEMPTY = 5, KW_SFULL = 8, KW_SEMPTY = 10,
+       KW_PDSFULL = 12, KW_ACCDONE = 14, KW_ACCEMPTY = 15 };  // 16 barriers
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_win_tc(const __grid_constant__ BwdArgs a) {
+    using SM = KWSmem<D>;
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    const uint32_t sbase = smem_u32(smem);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SM::kBar);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + SM::kTmemSlot);
+    float* qmeta = reinterpret_cast<float*>(smem + SM::kMeta);  // [stage][lse2|delta][64]
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#define TRW(role, gg, ev) SKB_TRB(role, (gg) - tr0, ev)
+    const int ntk = (a.L + 127) / 128;
+    const int nitems = ntk * a.H * a.B;
+    // the queries reading key tile kt: [j0, hi) with hi = max over its keys of
+    // min(key + w, chunk end) — both nondecreasing in key, so the last key's
+    auto item = [&](int wi, int& b, int& h, int& j0, int& nkeys, int& nq) {
+        const int kt = wi % ntk;
+        const int bh = wi / ntk;
+        h = bh % a.H;
+        b = bh / a.H;
+        j0 = kt * 128;
+        nkeys = min(128, a.L - j0);
+        const int jl = j0 + nkeys - 1;
+        int hi = jl + a.w;
+        if (a.chunk_len > 0) hi = min(hi, (jl / a.chunk_len + 1) * a.chunk_len);
+        hi = min(a.L, max(hi, jl + 1));
+        nq = (hi - j0 + 63) / 64;
+    };
+    if (threadIdx.x == 0) {
+        mbar_init(&bars[KW_KVFULL], 1);
+        mbar_init(&bars[KW_KVEMPTY], 1);
+        for (int s = 0; s < kQS; ++s) {
+            mbar_init(&bars[KW_QDFULL + s], kProducers + 1);
+            mbar_init(&bars[KW_QDEMPTY + s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&bars[KW_SFULL + s], 1);
+            mbar_init(&bars[KW_SEMPTY + s], kMath);
+            mbar_init(&bars[KW_PDSFULL + s], kMath);
+        }
+        mbar_init(&bars[KW_ACCDONE], 1);
+        mbar_init(&bars[KW_ACCEMPTY], kMath);
+        mbar_fence_init();
+    }
+    if (warp == kMmaWarp) tmem_alloc<512>(tmem_slot);
+    tc_before_sync();
+    __syncthreads();
+    tc_after_sync();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t tS = tmem, tP = tmem + 128, tDV = tmem + 256, tDK = tmem + 384;
+
+    if (warp >= kProdWarp0 && warp < kMmaWarp) {
+        constexpr int kAtoms = D / 64;
+        const int ptid = threadIdx.x - kProdWarp0 * 32;
+        int g = 0, it = 0, tr0 = 1 << 20;
+        for (int wi = blockIdx.x; wi < nitems; wi += gridDim.x, ++it) {
+            int b, h, j0, nkeys, nq;
+            item(wi, b, h, j0, nkeys, nq);
+            if (it == 20) tr0 = g;
+            if (ptid == 0) {
+                if (it > 0) mbar_wait(&bars[KW_KVEMPTY], (it - 1) & 1);
+                TRW(6, g, 2);
+                mbar_expect_tx(&bars[KW_KVFULL], 2 * 128 * D * 2);
+#pragma unroll
+                for (int at = 0; at < kAtoms; ++at) {
+                    tma_load_3d(sbase + SM::kK + at * 128 * 128, &a.tm_k128, h * D + at * 64, j0, b, &bars[KW_KVFULL]);
+                    tma_load_3d(sbase + SM::kV + at * 128 * 128, &a.tm_v128, h * D + at * 64, j0, b, &bars[KW_KVFULL]);
+                }
+            }
+            const float* lse2 = a.lse2 + ((int64_t)b * a.H + h) * a.L;
+            const float* dlt = a.delta + ((int64_t)b * a.H + h) * a.L;
+            for (int qt = 0; qt < nq; ++qt, ++g) {
+                const int s = g % kQS;
+                if (ptid == 0) TRW(6, g, 0);
+                if (g >= kQS) mbar_wait(&bars[KW_QDEMPTY + s], ((g - kQS) / kQS) & 1);
+                if (ptid == 0) TRW(6, g, 1);
+                const int qs = j0 + qt * 64;
+                for (int c = ptid; c < 64; c += kProducers) {
+                    const int i = qs + c;
+                    const bool ok = i < a.L;
+                    const uint32_t mb = smem_u32(qmeta + (s * 3) * 64 + c);
+                    cp_async4(mb, lse2 + (ok ? i : 0), ok);
+                    cp_async4(mb + 64 * 4, dlt + (ok ? i : 0), ok);
+                }
+                cp_async_arrive_noinc(&bars[KW_QDFULL + s]);
+                if (ptid == 0) {
+                    mbar_expect_tx(&bars[KW_QDFULL + s], 2 * 64 * D * 2);
+#pragma unroll
+                    for (int at = 0; at < kAtoms; ++at) {
+                        tma_load_3d(sbase + SM::kQ + s * SM::kQT + at * 64 * 128, &a.tm_q64, h * D + at * 64, qs, b,
+                                    &bars[KW_QDFULL + s]);
+                        tma_load_3d(sbase + SM::kDO + s * SM::kQT + at * 64 * 128, &a.tm_do64, h * D + at * 64, qs, b,
+                                    &bars[KW_QDFULL + s]);
+                    }
+                }
+            }
+        }
+    } else if (warp == kMmaWarp) {
+        if (lane == 0) {
+            constexpr uint32_t id_s = umma_idesc(128, 64, false, false);
+            constexpr uint32_t id_acc = umma_idesc(128, D, false, true);
+            int g = 0, it = 0, tr0 = 1 << 20;
+            // dV += P~^T dO, dK += dS^T Q for the tile at global index gj (item
+            // tile qt); the first tile of an item waits for the accumulators
+            auto acc = [&](int gj, int qt, int itn) {
+                const int s = gj & 1, qs = gj % kQS;
+                mbar_wait(&bars[KW_PDSFULL + s], (gj >> 1) & 1);
+                TRW(7, gj, 2);
+                if (qt == 0 && itn > 0) mbar_wait(&bars[KW_ACCEMPTY], (itn - 1) & 1);
+                TRW(7, gj, 3);
+                tc_after_sync();
+                const uint32_t dob = sbase + SM::kDO + qs * SM::kQT, qb = sbase + SM::kQ + qs * SM::kQT;
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) {
+                    const uint32_t co = s * 64 + (kk >> 1) * 32 + (kk & 1) * 8;
+                    umma_f16_ts(tDV, tS + co, desc_mnmajor(dob, 64, kk), id_acc, (qt > 0 || kk > 0) ? 1u : 0u);
+                    umma_f16_ts(tDK, tP + co, desc_mnmajor(qb, 64, kk), id_acc, (qt > 0 || kk > 0) ? 1u : 0u);
+                }
+                umma_commit(&bars[KW_QDEMPTY + qs]);
+            };
+            for (int wi = blockIdx.x; wi < nitems; wi += gridDim.x, ++it) {
+                int b, h, j0, nkeys, nq;
+                item(wi, b, h, j0, nkeys, nq);
+                if (it == 20) tr0 = g;
+                mbar_wait(&bars[KW_KVFULL], it & 1);
+                TRW(7, g, 4);
+                tc_after_sync();
+                for (int qt = 0; qt < nq; ++qt, ++g) {
+                    const int s = g & 1, qs = g % kQS;
+                    TRW(7, g, 8);
+                    mbar_wait(&bars[KW_QDFULL + qs], (g / kQS) & 1);
+                    TRW(7, g, 0);
+                    if (g >= 2) mbar_wait(&bars[KW_SEMPTY + s], ((g - 2) >> 1) & 1);
+                    TRW(7, g, 5);
+                    tc_after_sync();
+                    const uint32_t qb = sbase + SM::kQ + qs * SM::kQT, dob = sbase + SM::kDO + qs * SM::kQT;
+#pragma unroll
+                    for (int kk = 0; kk < D / 16; ++kk) {
+                        umma_f16(tS + s * 64, desc_kmajor(sbase + SM::kK, 128, kk), desc_kmajor(qb, 64, kk), id_s,
+                                 kk > 0 ? 1u : 0u);
+                        umma_f16(tP + s * 64, desc_kmajor(sbase + SM::kV, 128, kk), desc_kmajor(dob, 64, kk), id_s,
+                                 kk > 0 ? 1u : 0u);
+                    }
+                    umma_commit(&bars[KW_SFULL + s]);
+                    TRW(7, g, 1);
+                    if (qt == nq - 1) umma_commit(&bars[KW_KVEMPTY]);
+                    if (qt >= 1) acc(g - 1, qt - 1, it);
+                }
+                acc(g - 1, nq - 1, it);
+                umma_commit(&bars[KW_ACCDONE]);
+            }
+        }
+        __syncwarp();
+    } else if (warp < kProdWarp0) {
+        const int hf = warp >> 2;
+        const int r = ((warp & 3) << 5) | lane;
+        const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+        const float sl2 = a.scale_log2;
+        const float2 sl22 = make_float2(sl2, sl2);
+        int g = 0, it = 0, tr0 = 1 << 20;
+        const bool trl = lane == 0 && (warp & 3) == 0;
+        for (int wi = blockIdx.x; wi < nitems; wi += gridDim.x, ++it) {
+            int b, h, j0, nkeys, nq;
+            item(wi, b, h, j0, nkeys, nq);
+            if (it == 20) tr0 = g;
+            const int64_t bl = (int64_t)b * a.L;
+            const int key = r < nkeys ? j0 + r : -1;
+            // queries [key, key + w) read this key from the window
+            // (proj/src/cache.cpp:259-311); chunk-wise training clips them to
+            // the key's chunk (proj/src/attention.cpp:228-234, 284-300)
+            int hi_i = min(a.L, key + a.w);
+            if (a.chunk_len > 0 && key >= 0) hi_i = min(hi_i, (key / a.chunk_len + 1) * a.chunk_len);
+            const bool has_sel = key >= 0 && a.R1 > 0 && key < a.T && __ldg(a.leave + bl + key) > key;
+            if (has_sel) {  // warm L2 (and the TLB) for the epilogue's partial reads
+#pragma unroll
+                for (int e = 0; e < D / 2; e += 8) {
+                    prefetch_l2(a.dk_acc + part_off<D>(a, b, h, key, (hf * (D / 2) + e) >> 2));
+                    prefetch_l2(a.dv_acc + part_off<D>(a, b, h, key, (hf * (D / 2) + e) >> 2));
+                }
+            }
+            for (int qt = 0; qt < nq; ++qt, ++g) {
+                const int s = g & 1, qs3 = g % kQS;
+                const int qs = j0 + qt * 64 + hf * 32;
+                if (trl) TRW(4 + hf, g, 9);
+                mbar_wait(&bars[KW_SFULL + s], (g >> 1) & 1);
+                mbar_wait(&bars[KW_QDFULL + qs3], (g / kQS) & 1);
+                if (trl) TRW(4 + hf, g, 0);
+                tc_after_sync();
+                float sv[32], dp[32];
+                tmem_ld32(tS + lane_off + s * 64 + hf * 32, sv);
+                tmem_ld32(tP + lane_off + s * 64 + hf * 32, dp);
+                tmem_wait_ld();
+                tc_before_sync();
+                mbar_arrive(&bars[KW_SEMPTY + s]);
+                const float* ml = qmeta + (qs3 * 3) * 64 + hf * 32;
+                const float* md = ml + 64;
+                const int cmin = key >= 0 ? key - qs : 32;
+                const int cmax = key >= 0 ? hi_i - 1 - qs : -1;
+                if (!__all_sync(0xffffffffu, cmin <= 0 && cmax >= 31)) {
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) sv[c] = (c >= cmin && c <= cmax) ? sv[c] : -INFINITY;
+                }
+#pragma unroll
+                for (int c = 0; c < 32; c += 4) {  // gates 1: plain softmax backward, packed fp32x2
+                    const float4 l4 = *reinterpret_cast<const float4*>(ml + c);
+                    const float4 d4 = *reinterpret_cast<const float4*>(md + c);
+                    float2 x0 = __ffma2_rn(make_float2(sv[c], sv[c + 1]), sl22, make_float2(-l4.x, -l4.y));
+                    float2 x1 = __ffma2_rn(make_float2(sv[c + 2], sv[c + 3]), sl22, make_float2(-l4.z, -l4.w));
+                    x0.x = ex2(x0.x);
+                    x0.y = ex2(x0.y);
+                    x1.x = ex2(x1.x);
+                    x1.y = ex2(x1.y);
+                    const float2 c0 = __fmul2_rn(x0, __fadd2_rn(make_float2(dp[c], dp[c + 1]), make_float2(-d4.x, -d4.y)));
+                    const float2 c1 = __fmul2_rn(x1, __fadd2_rn(make_float2(dp[c + 2], dp[c + 3]), make_float2(-d4.z, -d4.w)));
+                    sv[c] = x0.x, sv[c + 1] = x0.y, sv[c + 2] = x1.x, sv[c + 3] = x1.y;
+                    dp[c] = c0.x, dp[c + 1] = c0.y, dp[c + 2] = c1.x, dp[c + 3] = c1.y;
+                }
+                {
+                    uint32_t pk[16];
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) pk[e] = pack_bf16(sv[2 * e], sv[2 * e + 1]);
+                    tmem_st16u(tS + lane_off + s * 64 + hf * 32, pk);
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) pk[e] = pack_bf16(dp[2 * e], dp[2 * e + 1]);
+                    tmem_st16u(tP + lane_off + s * 64 + hf * 32, pk);
+                    tmem_wait_st();
+                }
+                tc_before_sync();
+                if (trl) TRW(4 + hf, g, 4);
+                mbar_arrive(&bars[KW_PDSFULL + s]);
+            }
+            mbar_wait(&bars[KW_ACCDONE], it & 1);
+            if (trl) TRW(4 + hf, g, 5);
+            tc_after_sync();
+            float dv[D / 2], dk[D / 2];
+#pragma unroll
+            for (int c = 0; c < D / 64; ++c) {
+                tmem_ld32(tDV + lane_off + hf * (D / 2) + c * 32, dv + c * 32);
+                tmem_ld32(tDK + lane_off + hf * (D / 2) + c * 32, dk + c * 32);
+            }
+            tmem_wait_ld();
+            tc_before_sync();
+            if (trl) TRW(4 + hf, g, 6);
+            mbar_arrive(&bars[KW_ACCEMPTY]);
+#pragma unroll
+            for (int e = 0; e < D / 2; ++e) dk[e] *= a.scale;
+            // + the selected pass's partials, then bf16 rows staged in smem and
+            // stored by the warpgroup as contiguous 16-byte chunks
+            uint8_t* stg = smem + SM::kStg + hf * SM::kStgWG;
+            const int wt = threadIdx.x & 127;
+#pragma unroll
+            for (int t2 = 0; t2 < 2; ++t2) {
+                float* x = t2 == 0 ? dk : dv;
+                const float* part = t2 == 0 ? a.dk_acc : a.dv_acc;
+                if (has_sel) {
+#pragma unroll
+                    for (int e = 0; e < D / 2; e += 4) {
+                        const float4 pp =
+                            *reinterpret_cast<const float4*>(part + part_off<D>(a, b, h, key, (hf * (D / 2) + e) >> 2));
+                        x[e] += pp.x, x[e + 1] += pp.y, x[e + 2] += pp.z, x[e + 3] += pp.w;
+                    }
+                }
+                if (trl) TRW(4 + hf, g, 10 + 3 * t2);
+#pragma unroll
+                for (int e = 0; e < D / 2; e += 8) {
+                    uint4 v4;
+                    v4.x = pack_bf16(x[e], x[e + 1]);
+                    v4.y = pack_bf16(x[e + 2], x[e + 3]);
+                    v4.z = pack_bf16(x[e + 4], x[e + 5]);
+                    v4.w = pack_bf16(x[e + 6], x[e + 7]);
+                    *reinterpret_cast<uint4*>(stg + r * SM::kPitch + e * 2) = v4;
+                }
+                wg_bar(hf);
+                if (trl) TRW(4 + hf, g, 11 + 3 * t2);
+                __nv_bfloat16* out = t2 == 0 ? a.dk : a.dv;
+                constexpr int kCh = D / 16;  // 16-byte chunks per staged half row
+#pragma unroll
+                for (int i = 0; i < kCh; ++i) {
+                    const int idx = wt + i * 128;
+                    const int row = idx / kCh, ch = idx % kCh;
+                    if (row < nkeys) {
+                        const uint4 v4 = *reinterpret_cast<const uint4*>(stg + row * SM::kPitch + ch * 16);
+                        *reinterpret_cast<uint4*>(out + ((bl + j0 + row) * a.H + h) * D + hf * (D / 2) + ch * 8) = v4;
+                    }
+                }
+                wg_bar(hf);
+                if (trl) TRW(4 + hf, g, 12 + 3 * t2);
+            }
+            if (trl) TRW(4 + hf, g, 7);
+        }
+    }
+    tc_before_sync();
+    __syncthreads();
+    tc_after_sync();
+    if (warp == kMmaWarp) tmem_dealloc<512>(tmem);
+#undef TRW
 }
 
 // ------------------------------------------------------------------ dQ
@@ -822,6 +1149,7 @@ void launch_bwd(const BwdArgs& a, const skb_attn_desc& d, cudaStream_t st) {
     if (!attr) {
         set_smem(k_bwd_dkdv_tc<D, true, KS>, KSmem<D>::kAlloc);
         set_smem(k_bwd_dkdv_tc<D, false, KS>, KSmem<D>::kAlloc);
+        set_smem(k_bwd_dkdv_win_tc<D>, KWSmem<D>::kAlloc);
         set_smem(k_bwd_dq_tc<D, KS>, QSmem<D>::kAlloc);
         attr = true;
     }
@@ -830,8 +1158,15 @@ void launch_bwd(const BwdArgs& a, const skb_attn_desc& d, cudaStream_t st) {
         k_bwd_dkdv_tc<D, true, KS><<<gs, kThreads, KSmem<D>::kAlloc, st>>>(a);
         SKB_CHECK_LAUNCH();
     }
-    dim3 gw((unsigned)cdiv(a.L, 128), (unsigned)d.heads, (unsigned)d.batch);
-    k_bwd_dkdv_tc<D, false, KS><<<gw, kThreads, KSmem<D>::kAlloc, st>>>(a);
+    static const int persist = getenv("SKB_WIN_PERSIST") ? atoi(getenv("SKB_WIN_PERSIST")) : 1;
+    if (persist) {
+        const int64_t items = cdiv(a.L, 128) * d.heads * d.batch;
+        const int grid = (int)std::min<int64_t>(items, num_sms());
+        k_bwd_dkdv_win_tc<D><<<grid, kThreads, KWSmem<D>::kAlloc, st>>>(a);
+    } else {
+        dim3 gw((unsigned)cdiv(a.L, 128), (unsigned)d.heads, (unsigned)d.batch);
+        k_bwd_dkdv_tc<D, false, KS><<<gw, kThreads, KSmem<D>::kAlloc, st>>>(a);
+    }
     SKB_CHECK_LAUNCH();
     dim3 gq((unsigned)a.nqb, (unsigned)d.heads, (unsigned)d.batch);
     k_bwd_dq_tc<D, KS><<<gq, kThreads, QSmem<D>::kAlloc, st>>>(a);

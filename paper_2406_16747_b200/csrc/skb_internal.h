@@ -9,6 +9,15 @@
 
 namespace skb {
 
+// SM count of the current device (persistent grids)
+inline int num_sms() {
+    static int cached[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (!cached[dev]) cudaDeviceGetAttribute(&cached[dev], cudaDevAttrMultiProcessorCount, dev);
+    return cached[dev] > 0 ? cached[dev] : 148;
+}
 void validate_desc(const skb_attn_desc& d);
 void select_layout(const skb_attn_desc& d, skb_select_layout& o);
 void run_select(const skb_attn_desc& d, const double* u, void* ws, cudaStream_t st);

@@ -82,6 +82,14 @@ __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+__device__ __forceinline__ void prefetch_l2(const void* addr) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(addr));
+}
+// bulk L2 prefetch of [addr, addr + bytes) (16-byte aligned, multiple of 16)
+__device__ __forceinline__ void prefetch_l2_bulk(const void* addr, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(addr), "r"(bytes) : "memory");
+}
+
 // ------------------------------------------------------------------ TMA
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
@@ -310,6 +318,8 @@ constexpr int kMmaWarp = 11;
 
 // Named barrier over the 256 math threads (id 1; 0 is __syncthreads).
 __device__ __forceinline__ void math_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+// one math warpgroup (128 threads); ids 2 and 3
+__device__ __forceinline__ void wg_bar(int hf) { asm volatile("bar.sync %0, 128;" ::"r"(2 + hf) : "memory"); }
 
 // Load an R-row tile of a [B, L, H, D] bf16 tensor into the swizzled layout.
 // keyfn(row) gives the source row (< 0 or >= L: zero-filled). The producer
