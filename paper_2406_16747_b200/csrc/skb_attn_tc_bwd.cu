@@ -48,9 +48,10 @@ struct BwdArgs {
     CUtensorMap tm_k64, tm_v64;
     CUtensorMap tm_q64, tm_do64;
     CUtensorMap tm_k128, tm_v128;
+    CUtensorMap tm_dk_st, tm_dv_st;  // 32-key group stores (tmap_groups4d)
     const __nv_bfloat16 *q, *k, *v, *dout;
     __nv_bfloat16 *dq, *dk, *dv;
-    float *dk_acc, *dv_acc;  // fp32 partials of the selected pass, 32-key groups (part_off)
+    __nv_bfloat16 *dk_acc, *dv_acc;  // partials of the selected pass, 32-key groups (part_off)
     const float* lse2;       // [B, H, L] lse * log2(e)
     const float* delta;      // [B, H, L] rowsum(dO * O)
     const float* uf;
@@ -71,13 +72,14 @@ struct BwdArgs {
     int chunk_len;  // 0 = one chunk
 };
 
-// fp32 dK/dV partials of the selected pass, [B][H][ceil(L/32)][D/4][32 keys][4]:
-// the 32 consecutive keys of a warp read or write one 4-column group as 512
-// contiguous bytes (a row-major [L, D] tile would cost one line per thread).
+// dK/dV partials of the selected pass (bf16; the window pass adds them to its
+// fp32 accumulators), [B][H][ceil(L/32)][D/8][32 keys][8]: the 32 consecutive
+// keys of a warp write one 8-column group as 512 contiguous bytes, and a
+// 128-key window tile's partials are one contiguous block (one bulk copy).
 template <int D>
-__device__ __forceinline__ int64_t part_off(const BwdArgs& a, int b, int h, int key, int c4) {
+__device__ __forceinline__ int64_t part_off(const BwdArgs& a, int b, int h, int key, int c8) {
     const int ng = (a.L + 31) >> 5;
-    return ((((int64_t)(b * a.H + h) * ng + (key >> 5)) * (D / 4) + c4) * 32 + (key & 31)) * 4;
+    return ((((int64_t)(b * a.H + h) * ng + (key >> 5)) * (D / 8) + c8) * 32 + (key & 31)) * 8;
 }
 
 // One (b, i, h) row per D/8 threads: 16-byte loads of O and dO, a
@@ -436,28 +438,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_tc(const __grid_consta
             for (int e = 0; e < 32; ++e) dk[e] *= a.scale;
             if (SEL) {
 #pragma unroll
-                for (int e = 0; e < 32; e += 4) {
-                    const int64_t po = part_off<D>(a, b, h, key, (col + e) >> 2);
-                    *reinterpret_cast<float4*>(a.dk_acc + po) = make_float4(dk[e], dk[e + 1], dk[e + 2], dk[e + 3]);
-                    *reinterpret_cast<float4*>(a.dv_acc + po) = make_float4(dv[e], dv[e + 1], dv[e + 2], dv[e + 3]);
+                for (int e = 0; e < 32; e += 8) {
+                    const int64_t po = part_off<D>(a, b, h, key, (col + e) >> 3);
+                    uint4 x, y;
+                    x.x = pack_bf16(dk[e], dk[e + 1]);
+                    x.y = pack_bf16(dk[e + 2], dk[e + 3]);
+                    x.z = pack_bf16(dk[e + 4], dk[e + 5]);
+                    x.w = pack_bf16(dk[e + 6], dk[e + 7]);
+                    y.x = pack_bf16(dv[e], dv[e + 1]);
+                    y.y = pack_bf16(dv[e + 2], dv[e + 3]);
+                    y.z = pack_bf16(dv[e + 4], dv[e + 5]);
+                    y.w = pack_bf16(dv[e + 6], dv[e + 7]);
+                    *reinterpret_cast<uint4*>(a.dk_acc + po) = x;
+                    *reinterpret_cast<uint4*>(a.dv_acc + po) = y;
                 }
             } else {
-                if (has_sel) {
-#pragma unroll
-                    for (int e = 0; e < 32; e += 4) {
-                        const int64_t po = part_off<D>(a, b, h, key, (col + e) >> 2);
-                        const float4 x = *reinterpret_cast<const float4*>(a.dk_acc + po);
-                        const float4 y = *reinterpret_cast<const float4*>(a.dv_acc + po);
-                        dk[e] += x.x;
-                        dk[e + 1] += x.y;
-                        dk[e + 2] += x.z;
-                        dk[e + 3] += x.w;
-                        dv[e] += y.x;
-                        dv[e + 1] += y.y;
-                        dv[e + 2] += y.z;
-                        dv[e + 3] += y.w;
-                    }
-                }
+                static_assert(SEL, "the window pass is k_bwd_dkdv_win_tc");
                 __nv_bfloat16* gk = a.dk + rowoff + c * 32;
                 __nv_bfloat16* gv = a.dv + rowoff + c * 32;
 #pragma unroll
@@ -491,18 +487,26 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_tc(const __grid_consta
 // epilogue; K/V are released by the commit of an item's last S/dP MMA, the
 // dV/dK accumulators by the math warps once they are read out.
 template <int D>
-struct KWSmem {  // KSmem + per-warpgroup staging rows for the coalesced dK/dV stores
-    using K = KSmem<D>;
-    static constexpr int kK = K::kK, kV = K::kV, kQ = K::kQ, kDO = K::kDO, kMeta = K::kMeta, kQT = K::kQT;
-    static constexpr int kPitch = D + 16;          // bytes per staged half row (D/2 bf16) + pad
-    static constexpr int kStgWG = 128 * kPitch;
-    static constexpr int kStg = kMeta + kQS * 3 * 64 * 4;
-    static constexpr int kBar = kStg + 2 * kStgWG;
-    static constexpr int kTmemSlot = kBar + 16 * 8;
+struct KWSmem {
+    static constexpr int kKV = 128 * D * 2;
+    static constexpr int kQT = 64 * D * 2;
+    static constexpr int kK = 0;
+    static constexpr int kV = kK + kKV;
+    static constexpr int kQ = kV + kKV;            // [kQS]
+    static constexpr int kDO = kQ + kQS * kQT;     // [kQS]
+    static constexpr int kPart = kDO + kQS * kQT;  // dK then dV partials of the tile (part_off order);
+    static constexpr int kPartB = 128 * D * 2;     //   the epilogue stages its bf16 rows in place
+    static constexpr int kMeta = kPart + 2 * kPartB;  // [kQS][lse2|delta][64] f32
+    static constexpr int kBar = kMeta + kQS * 2 * 64 * 4;
+    static constexpr int kTmemSlot = kBar + 18 * 8;
     static constexpr int kAlloc = kTmemSlot + 16 + 1024;
+    static_assert(kAlloc <= 232448, "smem");
 };
 enum { KW_KVFULL = 0, KW_KVEMPTY = 1, KW_QDFULL = 2, KW_QDEMPTY = 5, KW_SFULL = 8, KW_SEMPTY = 10,
-       KW_PDSFULL = 12, KW_ACCDONE = 14, KW_ACCEMPTY = 15 };  // 16 barriers
+       KW_PDSFULL = 12, KW_ACCDONE = 14, KW_ACCEMPTY = 15, KW_PARTFULL = 16, KW_STGFULL = 17 };  // 18 barriers
+// producer threads (warps 8-9) on the Q/dO ring; warp 10 moves the partials in
+// and the finished dK/dV rows out
+constexpr int kWinQProd = 64;
 
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_win_tc(const __grid_constant__ BwdArgs a) {
@@ -513,6 +517,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_win_tc(const __grid_co
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SM::kBar);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + SM::kTmemSlot);
     float* qmeta = reinterpret_cast<float*>(smem + SM::kMeta);  // [stage][lse2|delta][64]
+    // the selected pass touched keys of this tile (its partials must be added)
+    auto tile_sel = [&](int j0) { return a.R1 > 0 && j0 < a.T; };
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #define TRW(role, gg, ev) SKB_TRB(role, (gg) - tr0, ev)
@@ -537,7 +543,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_win_tc(const __grid_co
         mbar_init(&bars[KW_KVFULL], 1);
         mbar_init(&bars[KW_KVEMPTY], 1);
         for (int s = 0; s < kQS; ++s) {
-            mbar_init(&bars[KW_QDFULL + s], kProducers + 1);
+            mbar_init(&bars[KW_QDFULL + s], kWinQProd + 1);
             mbar_init(&bars[KW_QDEMPTY + s], 1);
         }
         for (int s = 0; s < 2; ++s) {
@@ -547,6 +553,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_win_tc(const __grid_co
         }
         mbar_init(&bars[KW_ACCDONE], 1);
         mbar_init(&bars[KW_ACCEMPTY], kMath);
+        mbar_init(&bars[KW_PARTFULL], 1);
+        mbar_init(&bars[KW_STGFULL], kMath);
         mbar_fence_init();
     }
     if (warp == kMmaWarp) tmem_alloc<512>(tmem_slot);
@@ -556,7 +564,46 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_win_tc(const __grid_co
     const uint32_t tmem = *tmem_slot;
     const uint32_t tS = tmem, tP = tmem + 128, tDV = tmem + 256, tDK = tmem + 384;
 
-    if (warp >= kProdWarp0 && warp < kMmaWarp) {
+    if (warp == kMmaWarp - 1) {
+        // the math warps stage tile n's bf16 rows (part_off order) in the
+        // partial buffer; this lane stores them (one TMA store per 32-key
+        // group and half), waits for the reads, then loads tile n+1's partials
+        // — all while tile n+1 computes
+        if (lane == 0) {
+            int it = 0, pb_ = 0, pj0 = 0, pnk = 0, ph = 0;
+            auto store_prev = [&](int itp) {
+                mbar_wait(&bars[KW_STGFULL], itp & 1);
+                for (int t2 = 0; t2 < 2; ++t2) {
+                    const CUtensorMap* tm = t2 == 0 ? &a.tm_dk_st : &a.tm_dv_st;
+                    const uint32_t pbuf = sbase + SM::kPart + t2 * SM::kPartB;
+                    for (int gq = 0; gq < (pnk + 31) / 32; ++gq)
+                        for (int hf = 0; hf < 2; ++hf)
+                            tma_store_4d(tm, pbuf + gq * (32 * D * 2) + hf * (D / 16) * 512, 0, pj0 + gq * 32,
+                                         ph * (D / 8) + hf * (D / 16), pb_);
+                }
+                bulk_commit();
+                bulk_wait_read0();
+            };
+            for (int wi = blockIdx.x; wi < nitems; wi += gridDim.x, ++it) {
+                int b, h, j0, nkeys, nq;
+                item(wi, b, h, j0, nkeys, nq);
+                if (it > 0) store_prev(it - 1);
+                pb_ = b, pj0 = j0, pnk = nkeys, ph = h;
+                if (tile_sel(j0)) {
+                    const uint32_t pb = (uint32_t)(((nkeys + 31) >> 5) * 32 * D * 2);
+                    mbar_expect_tx(&bars[KW_PARTFULL], 2 * pb);
+                    bulk_load(sbase + SM::kPart, a.dk_acc + part_off<D>(a, b, h, j0, 0), pb, &bars[KW_PARTFULL]);
+                    bulk_load(sbase + SM::kPart + SM::kPartB, a.dv_acc + part_off<D>(a, b, h, j0, 0), pb,
+                              &bars[KW_PARTFULL]);
+                } else {
+                    mbar_arrive(&bars[KW_PARTFULL]);
+                }
+            }
+            if (it > 0) store_prev(it - 1);
+            asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // writes complete before exit
+        }
+        __syncwarp();
+    } else if (warp >= kProdWarp0 && warp < kMmaWarp - 1) {
         constexpr int kAtoms = D / 64;
         const int ptid = threadIdx.x - kProdWarp0 * 32;
         int g = 0, it = 0, tr0 = 1 << 20;
@@ -582,10 +629,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_win_tc(const __grid_co
                 if (g >= kQS) mbar_wait(&bars[KW_QDEMPTY + s], ((g - kQS) / kQS) & 1);
                 if (ptid == 0) TRW(6, g, 1);
                 const int qs = j0 + qt * 64;
-                for (int c = ptid; c < 64; c += kProducers) {
+                {
+                    const int c = ptid;
                     const int i = qs + c;
                     const bool ok = i < a.L;
-                    const uint32_t mb = smem_u32(qmeta + (s * 3) * 64 + c);
+                    const uint32_t mb = smem_u32(qmeta + (s * 2) * 64 + c);
                     cp_async4(mb, lse2 + (ok ? i : 0), ok);
                     cp_async4(mb + 64 * 4, dlt + (ok ? i : 0), ok);
                 }
@@ -677,14 +725,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_win_tc(const __grid_co
             // the key's chunk (proj/src/attention.cpp:228-234, 284-300)
             int hi_i = min(a.L, key + a.w);
             if (a.chunk_len > 0 && key >= 0) hi_i = min(hi_i, (key / a.chunk_len + 1) * a.chunk_len);
-            const bool has_sel = key >= 0 && a.R1 > 0 && key < a.T && __ldg(a.leave + bl + key) > key;
-            if (has_sel) {  // warm L2 (and the TLB) for the epilogue's partial reads
-#pragma unroll
-                for (int e = 0; e < D / 2; e += 8) {
-                    prefetch_l2(a.dk_acc + part_off<D>(a, b, h, key, (hf * (D / 2) + e) >> 2));
-                    prefetch_l2(a.dv_acc + part_off<D>(a, b, h, key, (hf * (D / 2) + e) >> 2));
-                }
-            }
+            const bool has_sel = key >= 0 && key < a.T && tile_sel(j0) && __ldg(a.leave + bl + key) > key;
             for (int qt = 0; qt < nq; ++qt, ++g) {
                 const int s = g & 1, qs3 = g % kQS;
                 const int qs = j0 + qt * 64 + hf * 32;
@@ -699,7 +740,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_win_tc(const __grid_co
                 tmem_wait_ld();
                 tc_before_sync();
                 mbar_arrive(&bars[KW_SEMPTY + s]);
-                const float* ml = qmeta + (qs3 * 3) * 64 + hf * 32;
+                const float* ml = qmeta + (qs3 * 2) * 64 + hf * 32;
                 const float* md = ml + 64;
                 const int cmin = key >= 0 ? key - qs : 32;
                 const int cmax = key >= 0 ? hi_i - 1 - qs : -1;
@@ -751,48 +792,40 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_win_tc(const __grid_co
             mbar_arrive(&bars[KW_ACCEMPTY]);
 #pragma unroll
             for (int e = 0; e < D / 2; ++e) dk[e] *= a.scale;
-            // + the selected pass's partials, then bf16 rows staged in smem and
-            // stored by the warpgroup as contiguous 16-byte chunks
-            uint8_t* stg = smem + SM::kStg + hf * SM::kStgWG;
-            const int wt = threadIdx.x & 127;
+            // + the selected pass's partials (bulk-copied to smem in part_off
+            // order: 32-key groups of [D/8][32][8]); the bf16 result is staged in
+            // place and stored by the warpgroup as contiguous 16-byte row chunks
+            mbar_wait(&bars[KW_PARTFULL], it & 1);
+            constexpr int kGrp = 32 * D * 2;  // bytes per 32-key group
 #pragma unroll
             for (int t2 = 0; t2 < 2; ++t2) {
                 float* x = t2 == 0 ? dk : dv;
-                const float* part = t2 == 0 ? a.dk_acc : a.dv_acc;
-                if (has_sel) {
-#pragma unroll
-                    for (int e = 0; e < D / 2; e += 4) {
-                        const float4 pp =
-                            *reinterpret_cast<const float4*>(part + part_off<D>(a, b, h, key, (hf * (D / 2) + e) >> 2));
-                        x[e] += pp.x, x[e + 1] += pp.y, x[e + 2] += pp.z, x[e + 3] += pp.w;
-                    }
-                }
-                if (trl) TRW(4 + hf, g, 10 + 3 * t2);
+                uint8_t* pbuf = smem + SM::kPart + t2 * SM::kPartB;
+                uint8_t* prow = pbuf + (r >> 5) * kGrp + (r & 31) * 16;  // + c8 * 512
 #pragma unroll
                 for (int e = 0; e < D / 2; e += 8) {
+                    uint4* cell = reinterpret_cast<uint4*>(prow + ((hf * (D / 2) + e) >> 3) * 512);
+                    if (has_sel) {
+                        const uint4 pp = *cell;
+                        const uint32_t pw[4] = {pp.x, pp.y, pp.z, pp.w};
+#pragma unroll
+                        for (int q2 = 0; q2 < 4; ++q2) {
+                            const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&pw[q2]));
+                            x[e + 2 * q2] += f.x;
+                            x[e + 2 * q2 + 1] += f.y;
+                        }
+                    }
                     uint4 v4;
                     v4.x = pack_bf16(x[e], x[e + 1]);
                     v4.y = pack_bf16(x[e + 2], x[e + 3]);
                     v4.z = pack_bf16(x[e + 4], x[e + 5]);
                     v4.w = pack_bf16(x[e + 6], x[e + 7]);
-                    *reinterpret_cast<uint4*>(stg + r * SM::kPitch + e * 2) = v4;
+                    *cell = v4;
                 }
-                wg_bar(hf);
-                if (trl) TRW(4 + hf, g, 11 + 3 * t2);
-                __nv_bfloat16* out = t2 == 0 ? a.dk : a.dv;
-                constexpr int kCh = D / 16;  // 16-byte chunks per staged half row
-#pragma unroll
-                for (int i = 0; i < kCh; ++i) {
-                    const int idx = wt + i * 128;
-                    const int row = idx / kCh, ch = idx % kCh;
-                    if (row < nkeys) {
-                        const uint4 v4 = *reinterpret_cast<const uint4*>(stg + row * SM::kPitch + ch * 16);
-                        *reinterpret_cast<uint4*>(out + ((bl + j0 + row) * a.H + h) * D + hf * (D / 2) + ch * 8) = v4;
-                    }
-                }
-                wg_bar(hf);
-                if (trl) TRW(4 + hf, g, 12 + 3 * t2);
+                if (trl) TRW(4 + hf, g, 10 + 3 * t2);
             }
+            fence_async_smem();  // the staged rows -> the TMA stores (async proxy)
+            mbar_arrive(&bars[KW_STGFULL]);
             if (trl) TRW(4 + hf, g, 7);
         }
     }
@@ -1148,7 +1181,6 @@ void launch_bwd(const BwdArgs& a, const skb_attn_desc& d, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
         set_smem(k_bwd_dkdv_tc<D, true, KS>, KSmem<D>::kAlloc);
-        set_smem(k_bwd_dkdv_tc<D, false, KS>, KSmem<D>::kAlloc);
         set_smem(k_bwd_dkdv_win_tc<D>, KWSmem<D>::kAlloc);
         set_smem(k_bwd_dq_tc<D, KS>, QSmem<D>::kAlloc);
         attr = true;
@@ -1158,16 +1190,12 @@ void launch_bwd(const BwdArgs& a, const skb_attn_desc& d, cudaStream_t st) {
         k_bwd_dkdv_tc<D, true, KS><<<gs, kThreads, KSmem<D>::kAlloc, st>>>(a);
         SKB_CHECK_LAUNCH();
     }
-    static const int persist = getenv("SKB_WIN_PERSIST") ? atoi(getenv("SKB_WIN_PERSIST")) : 1;
-    if (persist) {
+    {
         const int64_t items = cdiv(a.L, 128) * d.heads * d.batch;
         const int grid = (int)std::min<int64_t>(items, num_sms());
         k_bwd_dkdv_win_tc<D><<<grid, kThreads, KWSmem<D>::kAlloc, st>>>(a);
-    } else {
-        dim3 gw((unsigned)cdiv(a.L, 128), (unsigned)d.heads, (unsigned)d.batch);
-        k_bwd_dkdv_tc<D, false, KS><<<gw, kThreads, KSmem<D>::kAlloc, st>>>(a);
+        SKB_CHECK_LAUNCH();
     }
-    SKB_CHECK_LAUNCH();
     dim3 gq((unsigned)a.nqb, (unsigned)d.heads, (unsigned)d.batch);
     k_bwd_dq_tc<D, KS><<<gq, kThreads, QSmem<D>::kAlloc, st>>>(a);
     SKB_CHECK_LAUNCH();
@@ -1192,6 +1220,8 @@ void run_attn_bwd_tc(const skb_attn_desc& d, const void* q, const void* k, const
         a.tm_do64 = tmap_rows3d(dout, d.batch, d.seq_len, HD, 64);
         a.tm_k128 = tmap_rows3d(k, d.batch, d.seq_len, HD, 128);
         a.tm_v128 = tmap_rows3d(v, d.batch, d.seq_len, HD, 128);
+        a.tm_dk_st = tmap_groups4d(dk, d.batch, d.seq_len, HD, (int)d.head_dim / 16);
+        a.tm_dv_st = tmap_groups4d(dv, d.batch, d.seq_len, HD, (int)d.head_dim / 16);
     }
     a.q = static_cast<const __nv_bfloat16*>(q);
     a.k = static_cast<const __nv_bfloat16*>(k);
@@ -1200,8 +1230,8 @@ void run_attn_bwd_tc(const skb_attn_desc& d, const void* q, const void* k, const
     a.dq = static_cast<__nv_bfloat16*>(dq);
     a.dk = static_cast<__nv_bfloat16*>(dk);
     a.dv = static_cast<__nv_bfloat16*>(dv);
-    a.dk_acc = reinterpret_cast<float*>(base + bl.dk_acc);
-    a.dv_acc = reinterpret_cast<float*>(base + bl.dv_acc);
+    a.dk_acc = reinterpret_cast<__nv_bfloat16*>(base + bl.dk_acc);
+    a.dv_acc = reinterpret_cast<__nv_bfloat16*>(base + bl.dv_acc);
     float* lse2 = reinterpret_cast<float*>(base + bl.dq_acc);
     float* delta = lse2 + d.batch * d.heads * d.seq_len;
     a.lse2 = lse2;

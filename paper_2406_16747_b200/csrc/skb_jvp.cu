@@ -109,10 +109,10 @@ void bwd_layout(const skb_attn_desc& d, BwdLayout& o) {
     const bool tc = d.dtype == SKB_BF16 && tc_supported(d) && !(d.flags & SKB_FLAG_FORCE_GATHER);
     // gather backward: fp64 dK/dV accumulators; tensor-core backward: fp32
     // partials of the selected pass + lse2/delta rows in the dq_acc region
-    // (the fp32 partials are stored in 32-key groups, skb_attn_tc_bwd.cu part_off)
+    // (the bf16 partials are stored in 32-key groups, skb_attn_tc_bwd.cu part_off)
     const uint64_t N32 = (uint64_t)d.batch * ((d.seq_len + 31) / 32 * 32) * d.heads * d.head_dim;
-    o.dk_acc = take(tc ? N32 * 4 : N * 8);
-    o.dv_acc = take(tc ? N32 * 4 : N * 8);
+    o.dk_acc = take(tc ? N32 * 2 : N * 8);
+    o.dv_acc = take(tc ? N32 * 2 : N * 8);
     o.dq_acc = take(tc ? BL * d.heads * 8 : 0);
     o.total = off;
 }

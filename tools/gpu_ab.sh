@@ -1,6 +1,6 @@
 # A/B: parity tests, bench with an env toggle (AB_VAR, default SKB_WIN_PERSIST) off/on, launch table.
 V=${AB_VAR:-SKB_WIN_PERSIST}
-python -m pytest tests/test_core_gpu.py tests/test_chunked_gpu.py -x -q 2>&1 | tail -4
+python -m pytest tests/test_core_gpu.py tests/test_chunked_gpu.py tests/test_api_gpu.py -x -q 2>&1 | tail -1 | sed "s/^/TESTS: /"
 for v in 0 1; do
   env $V=$v python bench.py --steps 20 --warmup 5 --no-e2e 2>/dev/null | tail -1 | python -c "
 import json,sys; d=json.loads(sys.stdin.read()); r=d['roofline']
