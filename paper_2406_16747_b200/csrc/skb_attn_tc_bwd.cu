@@ -65,6 +65,7 @@ struct BwdArgs {
     const int* ever_count;
     const int* ever_list;
     double *rowsum, *colsum;
+    int2* sel_items;  // [B][cdiv(L,128)] {q_lo, nq} of the selected pass's key tiles
     int nqb, qb_cap;
     int B, L, H, w, T, R1;
     float scale, scale_log2;
@@ -174,6 +175,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_tc(const __grid_consta
         if (r >= nkeys) return -1;
         return SEL ? __ldg(elist + kt * 128 + r) : j0 + r;
     };
+    if (threadIdx.x == 0) SKB_TRB(6, 31, 7);
     if (threadIdx.x == 0) {
         s_range[0] = SEL ? __ldg(elist + kt * 128) + a.w : j0;  // the list is ascending
         s_range[1] = 0;
@@ -238,9 +240,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_tc(const __grid_consta
         const float* dlt = a.delta + ((int64_t)b * a.H + h) * a.L;
         for (int qt = 0; qt < nq; ++qt) {
             const int s = qt % kQS;
-            if (ptid == 0 && !SEL) SKB_TRB(4 + 2, qt, 0);
+            if (ptid == 0) SKB_TRB(4 + 2, qt, 0);
             if (qt >= kQS) mbar_wait(&bars[KB_QDEMPTY + s], ((qt - kQS) / kQS) & 1);
-            if (ptid == 0 && !SEL) SKB_TRB(4 + 2, qt, 1);
+            if (ptid == 0) SKB_TRB(4 + 2, qt, 1);
             const int qs = q_lo + qt * 64;
             for (int c = ptid; c < 64; c += kProducers) {
                 const int i = qs + c;
@@ -272,7 +274,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_tc(const __grid_consta
             auto acc = [&](int j) {
                 const int s = j & 1, qs = j % kQS;
                 mbar_wait(&bars[KB_PDSFULL + s], (j >> 1) & 1);
-                if (!SEL) SKB_TRB(4 + 3, j, 2);
+                SKB_TRB(4 + 3, j, 2);
                 tc_after_sync();
                 const uint32_t dob = sbase + SM::kDO + qs * SM::kQT, qb = sbase + SM::kQ + qs * SM::kQT;
                 // P~^T / dS^T of query half hf (32 queries) sit in TMEM columns [hf*32, hf*32+16)
@@ -286,9 +288,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_tc(const __grid_consta
             };
             for (int qt = 0; qt < nq; ++qt) {
                 const int s = qt & 1, qs = qt % kQS;
-                if (!SEL) SKB_TRB(4 + 3, qt, 8);
+                SKB_TRB(4 + 3, qt, 8);
                 mbar_wait(&bars[KB_QDFULL + qs], (qt / kQS) & 1);
-                if (!SEL) SKB_TRB(4 + 3, qt, 0);
+                SKB_TRB(4 + 3, qt, 0);
                 if (qt >= 2) mbar_wait(&bars[KB_SEMPTY + s], ((qt - 2) >> 1) & 1);
                 tc_after_sync();
                 const uint32_t qb = sbase + SM::kQ + qs * SM::kQT, dob = sbase + SM::kDO + qs * SM::kQT;
@@ -300,7 +302,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_tc(const __grid_consta
                              kk > 0 ? 1u : 0u);
                 }
                 umma_commit(&bars[KB_SFULL + s]);
-                if (!SEL) SKB_TRB(4 + 3, qt, 1);
+                SKB_TRB(4 + 3, qt, 1);
                 if (qt >= 1) acc(qt - 1);
             }
             acc(nq - 1);
@@ -329,10 +331,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_tc(const __grid_consta
         for (int qt = 0; qt < nq; ++qt) {
             const int s = qt & 1, qs3 = qt % kQS;
             const int qs = q_lo + qt * 64 + hf * 32;  // first query of this thread's columns
-            if (!SEL && lane == 0 && (warp & 3) == 0) SKB_TRB(4 + hf, qt, 9);
+            if (lane == 0 && (warp & 3) == 0) SKB_TRB(4 + hf, qt, 9);
             mbar_wait(&bars[KB_SFULL + s], (qt >> 1) & 1);
             mbar_wait(&bars[KB_QDFULL + qs3], (qt / kQS) & 1);
-            if (!SEL && lane == 0 && (warp & 3) == 0) SKB_TRB(4 + hf, qt, 0);
+            if (lane == 0 && (warp & 3) == 0) SKB_TRB(4 + hf, qt, 0);
             tc_after_sync();
             float sv[32], dp[32];
             tmem_ld32(tS + lane_off + s * 64 + hf * 32, sv);
@@ -411,7 +413,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_tc(const __grid_consta
                 tmem_wait_st();
             }
             tc_before_sync();
-            if (!SEL && lane == 0 && (warp & 3) == 0) SKB_TRB(4 + hf, qt, 4);
+            if (lane == 0 && (warp & 3) == 0) SKB_TRB(4 + hf, qt, 4);
             mbar_arrive(&bars[KB_PDSFULL + s]);
         }
         if (SEL && key >= 0 && colsum != 0.f) atomicAdd(a.colsum + bl + key, (double)colsum);
@@ -419,6 +421,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_tc(const __grid_consta
             mbar_wait(&bars[KB_ACCDONE], 0);
             tc_after_sync();
         }
+        if (lane == 0 && (warp & 3) == 0) SKB_TRB(4 + hf, 31, 5);
         const bool has_sel = !SEL && key >= 0 && a.R1 > 0 && key < a.T && __ldg(a.leave + bl + key) > key;
         const int64_t rowoff = ((bl + (key >= 0 ? key : 0)) * a.H + h) * D + hf * (D / 2);
 #pragma unroll
@@ -473,6 +476,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_tc(const __grid_consta
             }
         }
     }
+    if (lane == 0 && (warp & 3) == 0 && warp < kProdWarp0) SKB_TRB(4 + (warp >> 2), 31, 6);
     tc_before_sync();
     __syncthreads();
     tc_after_sync();
@@ -521,7 +525,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_win_tc(const __grid_co
     auto tile_sel = [&](int j0) { return a.R1 > 0 && j0 < a.T; };
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-#define TRW(role, gg, ev) SKB_TRB(role, (gg) - tr0, ev)
+#ifdef SKB_TRACE_WIN  // items 20.. of the CTA (tools/trace_win.py)
+#define TRW(role, gg, ev) \
+    if ((gg) >= tr0) SKB_TRB(role, (gg) - tr0, ev)
+#else
+#define TRW(role, gg, ev) \
+    do {                  \
+    } while (0)
+#endif
     const int ntk = (a.L + 127) / 128;
     const int nitems = ntk * a.H * a.B;
     // the queries reading key tile kt: [j0, hi) with hi = max over its keys of
@@ -834,6 +845,378 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_win_tc(const __grid_co
     tc_after_sync();
     if (warp == kMmaWarp) tmem_dealloc<512>(tmem);
 #undef TRW
+}
+
+// The query range of each 128-entry tile of the ever-selected list (shared by
+// all heads): one warp per tile, [first key + w, max(leave + w)) clipped to the
+// keys' chunks, in 64-query tiles.
+__global__ void k_sel_items(BwdArgs a, int ntk) {
+    const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (wid >= a.B * ntk) return;
+    const int b = wid / ntk, kt = wid % ntk;
+    const int ec = a.ever_count[b];
+    int2 res = make_int2(0, 0);
+    if (kt * 128 < ec) {
+        const int* el = a.ever_list + (int64_t)b * a.L + kt * 128;
+        const int n = min(128, ec - kt * 128);
+        int hi = 0;
+        for (int r = lane; r < n; r += 32) {
+            const int key = el[r];
+            int x = a.leave[(int64_t)b * a.L + key] + a.w;
+            if (a.chunk_len > 0) x = min(x, (key / a.chunk_len + 1) * a.chunk_len);
+            hi = max(hi, x);
+        }
+        hi = min(a.L, warp_max_i(hi));
+        const int q_lo = ((el[0] + a.w) / 64) * 64;
+        res = make_int2(q_lo, hi > q_lo ? (hi - q_lo + 63) / 64 : 0);
+    }
+    if (lane == 0) a.sel_items[wid] = res;
+}
+
+// Selected pass, persistent: work item = (128-entry tile of the ever-selected
+// list, head); the rings run across items as in the window pass, so the next
+// tile's row gathers and first query tiles load under the current tile's last
+// MMAs and epilogue. K/V rows are gathered (cp.async) after the commit of the
+// item's last S/dP MMA releases the buffer.
+template <int D, bool KEY_SOFT>
+__global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_sel_tc(const __grid_constant__ BwdArgs a) {
+    using SM = KSmem<D>;
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    const uint32_t sbase = smem_u32(smem);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SM::kBar);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + SM::kTmemSlot);
+    float* qmeta = reinterpret_cast<float*>(smem + SM::kMeta);  // [stage][lse2|delta|tau][64]
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef SKB_TRACE_SEL  // items 6.. of the CTA (tools/trace_selp.py)
+#define TRS(role, gg, ev) \
+    if ((gg) >= tr0) SKB_TRB(role, (gg) - tr0, ev)
+#else
+#define TRS(role, gg, ev) \
+    do {                  \
+    } while (0)
+#endif
+    const int ntk = (a.L + 127) / 128;
+    const int nitems = ntk * a.H * a.B;
+    // item wi -> (kt fastest, h, b); invalid tiles (beyond the list) are skipped
+    // by every role alike; nq == 0 tiles only write zero partials
+    auto item = [&](int wi, int& b, int& h, int& kt, int& nkeys, int& q_lo, int& nq) -> bool {
+        kt = wi % ntk;
+        const int bh = wi / ntk;
+        h = bh % a.H;
+        b = bh / a.H;
+        const int ec = __ldg(a.ever_count + b);
+        if (kt * 128 >= ec) return false;
+        nkeys = min(128, ec - kt * 128);
+        const int2 info = a.sel_items[b * ntk + kt];
+        q_lo = info.x;
+        nq = info.y;
+        return true;
+    };
+    if (threadIdx.x == 0) {
+        mbar_init(&bars[KW_KVFULL], kProducers + 1);
+        mbar_init(&bars[KW_KVEMPTY], 1);
+        for (int s = 0; s < kQS; ++s) {
+            mbar_init(&bars[KW_QDFULL + s], kProducers + 1);
+            mbar_init(&bars[KW_QDEMPTY + s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&bars[KW_SFULL + s], 1);
+            mbar_init(&bars[KW_SEMPTY + s], kMath);
+            mbar_init(&bars[KW_PDSFULL + s], kMath);
+        }
+        mbar_init(&bars[KW_ACCDONE], 1);
+        mbar_init(&bars[KW_ACCEMPTY], kMath);
+        mbar_fence_init();
+    }
+    if (warp == kMmaWarp) tmem_alloc<512>(tmem_slot);
+    tc_before_sync();
+    __syncthreads();
+    tc_after_sync();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t tS = tmem, tP = tmem + 128, tDV = tmem + 256, tDK = tmem + 384;
+
+    if (warp >= kProdWarp0 && warp < kMmaWarp) {
+        constexpr int kAtoms = D / 64;
+        const int pw = warp - kProdWarp0, ptid = threadIdx.x - kProdWarp0 * 32;
+        int g = 0, kit = 0, tr0 = 1 << 28;
+        for (int wi = blockIdx.x; wi < nitems; wi += gridDim.x) {
+            int b, h, kt, nkeys, q_lo, nq;
+            if (!item(wi, b, h, kt, nkeys, q_lo, nq) || nq == 0) continue;
+            if (kit == 6) tr0 = g;
+            const int64_t bl = (int64_t)b * a.L;
+            const int* elist = a.ever_list + bl + kt * 128;
+            RowKeys<D, 128> kk;
+            kk.fetch(pw, lane, [&](int r) { return r < nkeys ? __ldg(elist + r) : -1; });
+            if (ptid == 0) TRS(6, g, 3);
+            if (kit > 0) mbar_wait(&bars[KW_KVEMPTY], (kit - 1) & 1);
+            if (ptid == 0) TRS(6, g, 2);
+            kk.issue(sbase + SM::kK, a.k, b, h, a.L, a.H, pw, lane);
+            kk.issue(sbase + SM::kV, a.v, b, h, a.L, a.H, pw, lane);
+            cp_async_arrive_noinc(&bars[KW_KVFULL]);
+            if (ptid == 0) mbar_arrive(&bars[KW_KVFULL]);
+            ++kit;
+            const float* lse2 = a.lse2 + ((int64_t)b * a.H + h) * a.L;
+            const float* dlt = a.delta + ((int64_t)b * a.H + h) * a.L;
+            for (int qt = 0; qt < nq; ++qt, ++g) {
+                const int s = g % kQS;
+                if (g >= kQS) mbar_wait(&bars[KW_QDEMPTY + s], ((g - kQS) / kQS) & 1);
+                if (ptid == 0) TRS(6, g, 1);
+                const int qs = q_lo + qt * 64;
+                for (int c = ptid; c < 64; c += kProducers) {
+                    const int i = qs + c;
+                    const bool ok = i < a.L;
+                    const int t = i - a.w;
+                    const uint32_t mb = smem_u32(qmeta + (s * 3) * 64 + c);
+                    cp_async4(mb, lse2 + (ok ? i : 0), ok);
+                    cp_async4(mb + 64 * 4, dlt + (ok ? i : 0), ok);
+                    cp_async4(mb + 128 * 4, a.tauf + bl + (ok && t >= 0 ? t : 0), ok && t >= 0);
+                }
+                cp_async_arrive_noinc(&bars[KW_QDFULL + s]);
+                if (ptid == 0) {
+                    mbar_expect_tx(&bars[KW_QDFULL + s], 2 * 64 * D * 2);
+#pragma unroll
+                    for (int at = 0; at < kAtoms; ++at) {
+                        tma_load_3d(sbase + SM::kQ + s * SM::kQT + at * 64 * 128, &a.tm_q64, h * D + at * 64, qs, b,
+                                    &bars[KW_QDFULL + s]);
+                        tma_load_3d(sbase + SM::kDO + s * SM::kQT + at * 64 * 128, &a.tm_do64, h * D + at * 64, qs, b,
+                                    &bars[KW_QDFULL + s]);
+                    }
+                }
+            }
+        }
+    } else if (warp == kMmaWarp) {
+        if (lane == 0) {
+            constexpr uint32_t id_s = umma_idesc(128, 64, false, false);
+            constexpr uint32_t id_acc = umma_idesc(128, D, false, true);
+            int g = 0, kit = 0, tr0 = 1 << 28;
+            auto acc = [&](int gj, int qt, int kitn) {
+                const int s = gj & 1, qs = gj % kQS;
+                mbar_wait(&bars[KW_PDSFULL + s], (gj >> 1) & 1);
+                TRS(7, gj, 2);
+                if (qt == 0 && kitn > 0) mbar_wait(&bars[KW_ACCEMPTY], (kitn - 1) & 1);
+                tc_after_sync();
+                const uint32_t dob = sbase + SM::kDO + qs * SM::kQT, qb = sbase + SM::kQ + qs * SM::kQT;
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) {
+                    const uint32_t co = s * 64 + (kk >> 1) * 32 + (kk & 1) * 8;
+                    umma_f16_ts(tDV, tS + co, desc_mnmajor(dob, 64, kk), id_acc, (qt > 0 || kk > 0) ? 1u : 0u);
+                    umma_f16_ts(tDK, tP + co, desc_mnmajor(qb, 64, kk), id_acc, (qt > 0 || kk > 0) ? 1u : 0u);
+                }
+                umma_commit(&bars[KW_QDEMPTY + qs]);
+            };
+            for (int wi = blockIdx.x; wi < nitems; wi += gridDim.x) {
+                int b, h, kt, nkeys, q_lo, nq;
+                if (!item(wi, b, h, kt, nkeys, q_lo, nq) || nq == 0) continue;
+                if (kit == 6) tr0 = g;
+                mbar_wait(&bars[KW_KVFULL], kit & 1);
+                TRS(7, g, 4);
+                fence_proxy_async();  // cp.async rows -> the MMA (async proxy)
+                tc_after_sync();
+                for (int qt = 0; qt < nq; ++qt, ++g) {
+                    const int s = g & 1, qs = g % kQS;
+                    mbar_wait(&bars[KW_QDFULL + qs], (g / kQS) & 1);
+                    TRS(7, g, 0);
+                    if (g >= 2) mbar_wait(&bars[KW_SEMPTY + s], ((g - 2) >> 1) & 1);
+                    tc_after_sync();
+                    const uint32_t qb = sbase + SM::kQ + qs * SM::kQT, dob = sbase + SM::kDO + qs * SM::kQT;
+#pragma unroll
+                    for (int kk = 0; kk < D / 16; ++kk) {
+                        umma_f16(tS + s * 64, desc_kmajor(sbase + SM::kK, 128, kk), desc_kmajor(qb, 64, kk), id_s,
+                                 kk > 0 ? 1u : 0u);
+                        umma_f16(tP + s * 64, desc_kmajor(sbase + SM::kV, 128, kk), desc_kmajor(dob, 64, kk), id_s,
+                                 kk > 0 ? 1u : 0u);
+                    }
+                    umma_commit(&bars[KW_SFULL + s]);
+                    TRS(7, g, 1);
+                    if (qt == nq - 1) umma_commit(&bars[KW_KVEMPTY]);
+                    if (qt >= 1) acc(g - 1, qt - 1, kit);
+                }
+                acc(g - 1, nq - 1, kit);
+                umma_commit(&bars[KW_ACCDONE]);
+                ++kit;
+            }
+        }
+        __syncwarp();
+    } else if (warp < kProdWarp0) {
+        const int hf = warp >> 2;
+        const int r = ((warp & 3) << 5) | lane;
+        const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+        const float sl2 = a.scale_log2;
+        const float2 sl22 = make_float2(sl2, sl2);
+        int g = 0, kit = 0, tr0 = 1 << 28;
+        const bool trl = lane == 0 && (warp & 3) == 0;
+        for (int wi = blockIdx.x; wi < nitems; wi += gridDim.x) {
+            int b, h, kt, nkeys, q_lo, nq;
+            if (!item(wi, b, h, kt, nkeys, q_lo, nq)) continue;
+            if (kit == 6 && nq > 0) tr0 = g;
+            const int64_t bl = (int64_t)b * a.L;
+            const int key = r < nkeys ? __ldg(a.ever_list + bl + kt * 128 + r) : -1;
+            const int leave = key >= 0 ? __ldg(a.leave + bl + key) : 0;
+            const float uj = key >= 0 ? __ldg(a.uf + bl + key) : 0.f;
+            // queries [key + w, leave + w) read this key from the selection
+            // (proj/src/cache.cpp:259-311), clipped to the key's chunk
+            const int lo_i = key + a.w;
+            int hi_i = min(a.L, leave + a.w);
+            if (a.chunk_len > 0 && key >= 0) hi_i = min(hi_i, (key / a.chunk_len + 1) * a.chunk_len);
+            float colsum = 0.f;
+            for (int qt = 0; qt < nq; ++qt, ++g) {
+                const int s = g & 1, qs3 = g % kQS;
+                const int qs = q_lo + qt * 64 + hf * 32;
+                if (trl) TRS(4 + hf, g, 9);
+                mbar_wait(&bars[KW_SFULL + s], (g >> 1) & 1);
+                mbar_wait(&bars[KW_QDFULL + qs3], (g / kQS) & 1);
+                if (trl) TRS(4 + hf, g, 0);
+                tc_after_sync();
+                float sv[32], dp[32];
+                tmem_ld32(tS + lane_off + s * 64 + hf * 32, sv);
+                tmem_ld32(tP + lane_off + s * 64 + hf * 32, dp);
+                tmem_wait_ld();
+                tc_before_sync();
+                mbar_arrive(&bars[KW_SEMPTY + s]);
+                const float* ml = qmeta + (qs3 * 3) * 64 + hf * 32;
+                const float* md = ml + 64;
+                const float* mt = ml + 128;
+                const int cmin = key >= 0 ? lo_i - qs : 32;
+                const int cmax = key >= 0 ? hi_i - 1 - qs : -1;
+                const bool full = __all_sync(0xffffffffu, cmin <= 0 && cmax >= 31);
+                // all gates of this key saturated over these columns (tau nondecreasing)
+                const int clast = max(0, min(31, a.L - 1 - qs));
+                const bool sat = __all_sync(0xffffffffu, key < 0 || uj >= mt[clast] + 1.f);
+                if (!full) {
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) sv[c] = (c >= cmin && c <= cmax) ? sv[c] : -INFINITY;
+                }
+                if (sat) {  // gates 1 on these columns: plain softmax backward, packed fp32x2
+#pragma unroll
+                    for (int c = 0; c < 32; c += 4) {
+                        const float4 l4 = *reinterpret_cast<const float4*>(ml + c);
+                        const float4 d4 = *reinterpret_cast<const float4*>(md + c);
+                        float2 x0 = __ffma2_rn(make_float2(sv[c], sv[c + 1]), sl22, make_float2(-l4.x, -l4.y));
+                        float2 x1 = __ffma2_rn(make_float2(sv[c + 2], sv[c + 3]), sl22, make_float2(-l4.z, -l4.w));
+                        x0.x = ex2(x0.x);
+                        x0.y = ex2(x0.y);
+                        x1.x = ex2(x1.x);
+                        x1.y = ex2(x1.y);
+                        const float2 c0 =
+                            __fmul2_rn(x0, __fadd2_rn(make_float2(dp[c], dp[c + 1]), make_float2(-d4.x, -d4.y)));
+                        const float2 c1 =
+                            __fmul2_rn(x1, __fadd2_rn(make_float2(dp[c + 2], dp[c + 3]), make_float2(-d4.z, -d4.w)));
+                        sv[c] = x0.x, sv[c + 1] = x0.y, sv[c + 2] = x1.x, sv[c + 3] = x1.y;
+                        dp[c] = c0.x, dp[c + 1] = c0.y, dp[c + 2] = c1.x, dp[c + 3] = c1.y;
+                    }
+                } else if constexpr (!KEY_SOFT) {
+                    // hard keys, fractional gates: packed fp32x2 except the gate
+                    // saturation and the fractional-support test
+                    float2 csum2 = make_float2(0.f, 0.f);
+                    const bool mst = a.mask_st != 0;
+#pragma unroll
+                    for (int c = 0; c < 32; c += 2) {
+                        const float2 l2 = *reinterpret_cast<const float2*>(ml + c);
+                        const float2 d2 = *reinterpret_cast<const float2*>(md + c);
+                        const float2 t2 = *reinterpret_cast<const float2*>(mt + c);
+                        const float g0 = __saturatef(uj - t2.x), g1 = __saturatef(uj - t2.y);
+                        float2 p2 = __ffma2_rn(make_float2(sv[c], sv[c + 1]), sl22, make_float2(-l2.x, -l2.y));
+                        p2.x = ex2(p2.x);  // masked: 0
+                        p2.y = ex2(p2.y);
+                        const float2 dp2 = make_float2(dp[c], dp[c + 1]);
+                        const float2 wv2 = mst ? make_float2(1.f, 1.f) : make_float2(g0, g1);
+                        const float2 cc2 = __fmul2_rn(p2, __ffma2_rn(wv2, dp2, make_float2(-d2.x, -d2.y)));
+                        const float2 fr2 = make_float2((g0 > 0.f && g0 < 1.f) ? 1.f : 0.f,
+                                                       (g1 > 0.f && g1 < 1.f) ? 1.f : 0.f);
+                        csum2 = __ffma2_rn(__fmul2_rn(p2, dp2), fr2, csum2);
+                        const float2 pw2 = __fmul2_rn(p2, wv2);
+                        sv[c] = pw2.x, sv[c + 1] = pw2.y;  // P~^T
+                        dp[c] = cc2.x, dp[c + 1] = cc2.y;  // dS^T (scale applied in the epilogue)
+                    }
+                    colsum += csum2.x + csum2.y;
+                } else {
+                    float csum = 0.f;
+#pragma unroll
+                    for (int c = 0; c < 32; c += 4) {
+                        const float4 l4 = *reinterpret_cast<const float4*>(ml + c);
+                        const float4 d4 = *reinterpret_cast<const float4*>(md + c);
+                        const float4 t4 = *reinterpret_cast<const float4*>(mt + c);
+                        const float la[4] = {l4.x, l4.y, l4.z, l4.w};
+                        const float da[4] = {d4.x, d4.y, d4.z, d4.w};
+                        const float ta[4] = {t4.x, t4.y, t4.z, t4.w};
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const int cc_ = c + e;
+                            const float gt = __saturatef(uj - ta[e]);
+                            const float kap = KEY_SOFT ? gt : 1.f;
+                            const float raw = sv[cc_];
+                            const float x = (KEY_SOFT && raw == -INFINITY) ? raw : raw * kap;
+                            const float p = ex2(fmaf(x, sl2, -la[e]));  // masked: 0
+                            const float wv = a.mask_st ? 1.f : gt;
+                            const float cc = p * fmaf(wv, dp[cc_], -da[e]);
+                            float gm = p * dp[cc_];
+                            if (KEY_SOFT) gm += a.scale * cc * (raw == -INFINITY ? 0.f : raw);
+                            csum += (gt > 0.f && gt < 1.f) ? gm : 0.f;
+                            sv[cc_] = p * wv;    // P~^T
+                            dp[cc_] = cc * kap;  // dS^T (scale applied in the epilogue)
+                        }
+                    }
+                    colsum += csum;
+                }
+                {
+                    uint32_t pk[16];
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) pk[e] = pack_bf16(sv[2 * e], sv[2 * e + 1]);
+                    tmem_st16u(tS + lane_off + s * 64 + hf * 32, pk);
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) pk[e] = pack_bf16(dp[2 * e], dp[2 * e + 1]);
+                    tmem_st16u(tP + lane_off + s * 64 + hf * 32, pk);
+                    tmem_wait_st();
+                }
+                tc_before_sync();
+                if (trl) TRS(4 + hf, g, 4);
+                mbar_arrive(&bars[KW_PDSFULL + s]);
+            }
+            if (key >= 0 && colsum != 0.f) atomicAdd(a.colsum + bl + key, (double)colsum);
+            float dv[D / 2], dk[D / 2];
+            if (nq > 0) {
+                mbar_wait(&bars[KW_ACCDONE], kit & 1);
+                if (trl) TRS(4 + hf, g, 5);
+                tc_after_sync();
+#pragma unroll
+                for (int c = 0; c < D / 64; ++c) {
+                    tmem_ld32(tDV + lane_off + hf * (D / 2) + c * 32, dv + c * 32);
+                    tmem_ld32(tDK + lane_off + hf * (D / 2) + c * 32, dk + c * 32);
+                }
+                tmem_wait_ld();
+                tc_before_sync();
+                mbar_arrive(&bars[KW_ACCEMPTY]);
+                ++kit;
+            } else {
+#pragma unroll
+                for (int e = 0; e < D / 2; ++e) dv[e] = dk[e] = 0.f;
+            }
+            if (key < 0) continue;
+#pragma unroll
+            for (int e = 0; e < D / 2; e += 8) {
+                const int64_t po = part_off<D>(a, b, h, key, (hf * (D / 2) + e) >> 3);
+                uint4 x, y;
+                x.x = pack_bf16(dk[e] * a.scale, dk[e + 1] * a.scale);
+                x.y = pack_bf16(dk[e + 2] * a.scale, dk[e + 3] * a.scale);
+                x.z = pack_bf16(dk[e + 4] * a.scale, dk[e + 5] * a.scale);
+                x.w = pack_bf16(dk[e + 6] * a.scale, dk[e + 7] * a.scale);
+                y.x = pack_bf16(dv[e], dv[e + 1]);
+                y.y = pack_bf16(dv[e + 2], dv[e + 3]);
+                y.z = pack_bf16(dv[e + 4], dv[e + 5]);
+                y.w = pack_bf16(dv[e + 6], dv[e + 7]);
+                *reinterpret_cast<uint4*>(a.dk_acc + po) = x;
+                *reinterpret_cast<uint4*>(a.dv_acc + po) = y;
+            }
+            if (trl) TRS(4 + hf, g, 6);
+        }
+    }
+    tc_before_sync();
+    __syncthreads();
+    tc_after_sync();
+    if (warp == kMmaWarp) tmem_dealloc<512>(tmem);
+#undef TRS
 }
 
 // ------------------------------------------------------------------ dQ
@@ -1181,13 +1564,24 @@ void launch_bwd(const BwdArgs& a, const skb_attn_desc& d, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
         set_smem(k_bwd_dkdv_tc<D, true, KS>, KSmem<D>::kAlloc);
+        set_smem(k_bwd_dkdv_sel_tc<D, KS>, KSmem<D>::kAlloc);
         set_smem(k_bwd_dkdv_win_tc<D>, KWSmem<D>::kAlloc);
         set_smem(k_bwd_dq_tc<D, KS>, QSmem<D>::kAlloc);
         attr = true;
     }
     if (a.R1 > 0 && a.T > 0) {
-        dim3 gs((unsigned)cdiv(a.T, 128), (unsigned)d.heads, (unsigned)d.batch);
-        k_bwd_dkdv_tc<D, true, KS><<<gs, kThreads, KSmem<D>::kAlloc, st>>>(a);
+        static const int persist = getenv("SKB_SEL_PERSIST") ? atoi(getenv("SKB_SEL_PERSIST")) : 1;
+        if (persist) {
+            const int ntk = (int)cdiv(a.L, 128);
+            k_sel_items<<<(unsigned)cdiv((int64_t)a.B * ntk * 32, 256), 256, 0, st>>>(a, ntk);
+            SKB_CHECK_LAUNCH();
+            const int64_t items = (int64_t)ntk * d.heads * d.batch;
+            const int grid = (int)std::min<int64_t>(items, num_sms());
+            k_bwd_dkdv_sel_tc<D, KS><<<grid, kThreads, KSmem<D>::kAlloc, st>>>(a);
+        } else {
+            dim3 gs((unsigned)cdiv(a.T, 128), (unsigned)d.heads, (unsigned)d.batch);
+            k_bwd_dkdv_tc<D, true, KS><<<gs, kThreads, KSmem<D>::kAlloc, st>>>(a);
+        }
         SKB_CHECK_LAUNCH();
     }
     {
@@ -1248,6 +1642,7 @@ void run_attn_bwd_tc(const skb_attn_desc& d, const void* q, const void* k, const
     a.ever_list = s.ever_list;
     a.rowsum = rowsum;
     a.colsum = colsum;
+    a.sel_items = reinterpret_cast<int2*>(base + bl.sel_items);
     a.nqb = s.nqb;
     a.qb_cap = s.qb_cap;
     a.B = (int)d.batch;

@@ -114,6 +114,8 @@ void bwd_layout(const skb_attn_desc& d, BwdLayout& o) {
     o.dk_acc = take(tc ? N32 * 2 : N * 8);
     o.dv_acc = take(tc ? N32 * 2 : N * 8);
     o.dq_acc = take(tc ? BL * d.heads * 8 : 0);
+    // per 128-entry tile of the ever-selected list: {first query tile, query tiles}
+    o.sel_items = take(tc ? (uint64_t)d.batch * ((d.seq_len + 127) / 128) * 8 : 0);
     o.total = off;
 }
 
