@@ -881,6 +881,7 @@ __global__ void k_sel_items(BwdArgs a, int ntk) {
 template <int D, bool KEY_SOFT>
 __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_sel_tc(const __grid_constant__ BwdArgs a) {
     using SM = KSmem<D>;
+    static_assert(KW_ACCEMPTY < SM::kNumBars, "barrier slots");
     extern __shared__ __align__(16) uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const uint32_t sbase = smem_u32(smem);
@@ -1244,16 +1245,18 @@ struct QSmem {
     static constexpr int kMeta = kV + kNV * kKT;  // [kNS][key|ext|uf][128] x 4 B
     static constexpr int kFlags = kMeta + kNS * 3 * 128 * 4;  // [kNS] x 16 B
     static constexpr int kBar = kFlags + kNS * 16;
-    static constexpr int kNumBars = 20;
+    static constexpr int kNumBars = 26;  // QB_* (25)
     static constexpr int kTmemSlot = kBar + kNumBars * 8;
     static constexpr int kAlloc = kTmemSlot + 16 + 1024;
 };
 enum { QB_QFULL = 0, QB_DOFULL = 1, QB_KVFULL = 2, QB_KVEMPTY = 5, QB_MFULL = 8, QB_MEMPTY = 11, QB_VFULL = 14,
-       QB_VEMPTY = 16, QB_SFULL = 18, QB_SEMPTY = 19, QB_DSFULL = 20, QB_DSEMPTY = 21, QB_DQDONE = 22 };  // 23
+       QB_VEMPTY = 16, QB_SFULL = 18, QB_SEMPTY = 19, QB_DSFULL = 20, QB_DSEMPTY = 21, QB_DQDONE = 22,
+       QB_QDOEMPTY = 23, QB_DQEMPTY = 24 };  // 25
 
 template <int D, bool KEY_SOFT>
 __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(const __grid_constant__ BwdArgs a) {
     using SM = QSmem<D>;
+    static_assert(QB_DQDONE < SM::kNumBars, "barrier slots");
     extern __shared__ __align__(16) uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const uint32_t sbase = smem_u32(smem);
@@ -1274,6 +1277,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(const __grid_constant
     const int jw0 = i0 - a.w + 1;
     const int* list = a.qb_list + qrow * a.qb_cap;
 
+    if (threadIdx.x == 0) SKB_TRB(2, 31, 7);
     if (threadIdx.x == 0) {
         mbar_init(&bars[QB_QFULL], kMath / 2);
         mbar_init(&bars[QB_DOFULL], 1);
@@ -1527,6 +1531,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(const __grid_constant
             mbar_arrive(&bars[QB_DSFULL]);
         }
         mbar_wait(&bars[QB_DQDONE], 0);
+        if (lane == 0 && (warp & 3) == 0) SKB_TRB(hf, 31, 5);
         tc_after_sync();
         if (i < a.L && t >= 0 && a.R1 > 0 && rsum != 0.f) atomicAdd(a.rowsum + bl + t, (double)rsum);
         __nv_bfloat16* orow = a.dq + ((bl + (i < a.L ? i : 0)) * a.H + h) * D + hf * (D / 2);
@@ -1547,11 +1552,412 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(const __grid_constant
                 }
             }
         }
+        if (lane == 0 && (warp & 3) == 0) SKB_TRB(hf, 31, 6);
     }
     tc_before_sync();
     __syncthreads();
     tc_after_sync();
     if (warp == kMmaWarp) tmem_dealloc<512>(tmem);
+}
+
+template <int D, bool KEY_SOFT>
+__global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_p(const __grid_constant__ BwdArgs a) {
+    using SM = QSmem<D>;
+    static_assert(QB_DQEMPTY < SM::kNumBars, "barrier slots");
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    const uint32_t sbase = smem_u32(smem);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SM::kBar);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + SM::kTmemSlot);
+    int* meta = reinterpret_cast<int*>(smem + SM::kMeta);
+    int* tflags = reinterpret_cast<int*>(smem + SM::kFlags);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef SKB_TRACE_DQP  // tiles of items 6.. of the CTA (tools/trace_dqp.py)
+#define TRQ(role, jj, ev) \
+    if ((jj) >= tr0) SKB_TRB(role, (jj) - tr0, ev)
+#else
+#define TRQ(role, jj, ev) \
+    do {                  \
+    } while (0)
+#endif
+    const int n_win = (a.w + 127 + 127) / 128;
+    const int nitems = a.nqb * a.H * a.B;
+    // work item wi -> (query tile fastest, head, sequence)
+    struct Item {
+        int b, h, i0, n_sel, n, jw0;
+        int64_t bl, qrow;
+    };
+    auto item = [&](int wi) {
+        Item t;
+        const int qb = wi % a.nqb, bh = wi / a.nqb;
+        t.h = bh % a.H;
+        t.b = bh / a.H;
+        t.bl = (int64_t)t.b * a.L;
+        t.qrow = (int64_t)t.b * a.nqb + qb;
+        t.i0 = qb * 128;
+        const int cnt = (a.R1 > 0) ? __ldg(a.qb_count + t.qrow) : 0;
+        t.n_sel = (cnt + 127) / 128;
+        t.n = t.n_sel + n_win;
+        t.jw0 = t.i0 - a.w + 1;
+        return t;
+    };
+
+    if (threadIdx.x == 0) {
+        mbar_init(&bars[QB_QFULL], kMath / 2);
+        mbar_init(&bars[QB_DOFULL], 1);
+        for (int s = 0; s < kNS; ++s) {
+            mbar_init(&bars[QB_KVFULL + s], kProducers + 1);
+            mbar_init(&bars[QB_KVEMPTY + s], 1);
+            mbar_init(&bars[QB_MFULL + s], kProducers);
+            mbar_init(&bars[QB_MEMPTY + s], kMath);
+        }
+        for (int s = 0; s < kNV; ++s) {
+            mbar_init(&bars[QB_VFULL + s], kProducers + 1);
+            mbar_init(&bars[QB_VEMPTY + s], 1);
+        }
+        mbar_init(&bars[QB_SFULL], 1);
+        mbar_init(&bars[QB_SEMPTY], kMath);
+        mbar_init(&bars[QB_DSFULL], kMath);
+        mbar_init(&bars[QB_DSEMPTY], 1);
+        mbar_init(&bars[QB_DQDONE], 1);
+        mbar_init(&bars[QB_QDOEMPTY], 1);
+        mbar_init(&bars[QB_DQEMPTY], kMath);
+        mbar_fence_init();
+    }
+    if (warp == kMmaWarp) tmem_alloc<512>(tmem_slot);
+    tc_before_sync();
+    __syncthreads();
+    tc_after_sync();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t tQ = tmem, tDS = tmem + 64, tS = tmem + 128, tP = tmem + 256, tDQ = tmem + 384;
+
+    if (warp >= kProdWarp0 && warp < kMmaWarp) {
+        constexpr int kAtoms = D / 64;
+        const int pw = warp - kProdWarp0, ptid = threadIdx.x - kProdWarp0 * 32;
+        const int ma = ptid >> 5, mc = ptid & 31;  // metadata: array x 16-byte chunk (96 threads)
+        const int* msrc = ma == 0 ? a.qb_list : ma == 1 ? a.qb_leave : reinterpret_cast<const int*>(a.qb_uf);
+        int J = 0, it = 0, tr0 = 1 << 28;
+        for (int wi = blockIdx.x; wi < nitems; wi += gridDim.x, ++it) {
+            const Item I = item(wi);
+            if (it == 6) tr0 = J;
+            const int b = I.b, h = I.h, n_sel = I.n_sel, n = I.n;
+            const int* list = a.qb_list + I.qrow * a.qb_cap;
+            RowKeys<D, 128> kcur;
+            if (n_sel > 0) kcur.fetch(pw, lane, [&](int r) { return __ldg(list + r); });
+            for (int jt = 0; jt < n; ++jt, ++J) {
+                const int s = J % kNS;
+                if (jt == min(1, n - 1) && ptid == 0) {
+                    // dO of this item once the previous item's last dP is done
+                    if (it > 0) mbar_wait(&bars[QB_QDOEMPTY], (it - 1) & 1);
+                    mbar_expect_tx(&bars[QB_DOFULL], 128 * D * 2);
+#pragma unroll
+                    for (int at = 0; at < kAtoms; ++at)
+                        tma_load_3d(sbase + SM::kDO + at * 128 * 128, &a.tm_do128, h * D + at * 64, I.i0, b,
+                                    &bars[QB_DOFULL]);
+                }
+                if (J >= kNS) mbar_wait(&bars[QB_MEMPTY + s], ((J - kNS) / kNS) & 1);
+                if (jt < n_sel) {
+                    cp_async16(smem_u32(meta + (s * 3 + ma) * 128 + mc * 4),
+                               msrc + I.qrow * a.qb_cap + jt * 128 + mc * 4, true);
+                    if (ptid == 0)
+                        cp_async16(smem_u32(tflags + s * 4), a.qb_flags + (I.qrow * (a.qb_cap / 128) + jt) * 4, true);
+                }
+                cp_async_arrive_noinc(&bars[QB_MFULL + s]);
+                auto rows = [&](uint32_t dst, const __nv_bfloat16* src, const CUtensorMap* tm, uint64_t* bar) {
+                    if (jt < n_sel) {
+                        kcur.issue<false>(dst, src, b, h, a.L, a.H, pw, lane);
+                        cp_async_arrive_noinc(bar);
+                        if (ptid == 0) mbar_arrive(bar);
+                    } else {
+                        if (ptid == 0) {
+                            mbar_expect_tx(bar, 128 * D * 2);
+#pragma unroll
+                            for (int at = 0; at < kAtoms; ++at)
+                                tma_load_3d(dst + at * 128 * 128, tm, h * D + at * 64, I.jw0 + (jt - n_sel) * 128, b,
+                                            bar);
+                        }
+                        mbar_arrive(bar);
+                    }
+                };
+                if (J >= kNS) mbar_wait(&bars[QB_KVEMPTY + s], ((J - kNS) / kNS) & 1);
+                if (ptid == 0) TRQ(2, J, 2);
+                rows(sbase + SM::kK + s * SM::kKT, a.k, &a.tm_k128, &bars[QB_KVFULL + s]);
+                const int vs = J % kNV;
+                if (J >= kNV) mbar_wait(&bars[QB_VEMPTY + vs], ((J - kNV) / kNV) & 1);
+                rows(sbase + SM::kV + vs * SM::kKT, a.v, &a.tm_v128, &bars[QB_VFULL + vs]);
+                if (jt + 1 < n_sel) kcur.fetch(pw, lane, [&](int r) { return __ldg(list + (jt + 1) * 128 + r); });
+            }
+        }
+    } else if (warp == kMmaWarp) {
+        if (lane == 0) {
+            constexpr uint32_t id_s = umma_idesc(128, 128, false, false);
+            constexpr uint32_t id_dq = umma_idesc(128, D, false, true);
+            int tr0 = 1 << 28;
+            (void)tr0;
+            auto sdp = [&](int J) {  // S_J = Q K_J^T (TS), dP_J = dO V_J^T (SS)
+                const int ks = J % kNS;
+                mbar_wait(&bars[QB_KVFULL + ks], (J / kNS) & 1);
+                mbar_wait(&bars[QB_VFULL + (J % kNV)], (J / kNV) & 1);
+                TRQ(3, J, 0);
+                fence_proxy_async();  // cp.async (generic proxy) rows -> tensor core reads
+                if (J >= 1) mbar_wait(&bars[QB_SEMPTY], (J - 1) & 1);
+                tc_after_sync();
+                const uint32_t kb = sbase + SM::kK + ks * SM::kKT, vb = sbase + SM::kV + (J % kNV) * SM::kKT;
+#pragma unroll
+                for (int kk = 0; kk < D / 16; ++kk) {
+                    umma_f16_ts(tS, tQ + kk * 8, desc_kmajor(kb, 128, kk), id_s, kk > 0 ? 1u : 0u);
+                    umma_f16(tP, desc_kmajor(sbase + SM::kDO, 128, kk), desc_kmajor(vb, 128, kk), id_s,
+                             kk > 0 ? 1u : 0u);
+                }
+                umma_commit(&bars[QB_SFULL]);
+                umma_commit(&bars[QB_VEMPTY + (J % kNV)]);
+                TRQ(3, J, 1);
+            };
+            auto dq = [&](int J, int jt, int itn) {  // dQ += dS_J K_J (TS)
+                const int ks = J % kNS;
+                mbar_wait(&bars[QB_DSFULL], J & 1);
+                TRQ(3, J, 2);
+                if (jt == 0 && itn > 0) mbar_wait(&bars[QB_DQEMPTY], (itn - 1) & 1);
+                tc_after_sync();
+                const uint32_t kb = sbase + SM::kK + ks * SM::kKT;
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk)
+                    umma_f16_ts(tDQ, tDS + kk * 8, desc_mnmajor(kb, 128, kk), id_dq, (jt > 0 || kk > 0) ? 1u : 0u);
+                umma_commit(&bars[QB_DSEMPTY]);
+                umma_commit(&bars[QB_KVEMPTY + ks]);
+            };
+            int J = 0, it = 0;
+            for (int wi = blockIdx.x; wi < nitems; wi += gridDim.x, ++it) {
+                const Item I = item(wi);
+                if (it == 6) tr0 = J;
+                const int n = I.n;
+                mbar_wait(&bars[QB_QFULL], it & 1);
+                TRQ(3, J, 3);
+                mbar_wait(&bars[QB_DOFULL], it & 1);
+                TRQ(3, J, 4);
+                tc_after_sync();
+                sdp(J);
+                if (n == 1) umma_commit(&bars[QB_QDOEMPTY]);
+                for (int jt = 0; jt < n; ++jt) {
+                    if (jt + 1 < n) {
+                        sdp(J + jt + 1);  // overlaps the math on tile jt
+                        if (jt + 2 == n) umma_commit(&bars[QB_QDOEMPTY]);  // Q / dO read for the last time
+                    }
+                    dq(J + jt, jt, it);
+                }
+                umma_commit(&bars[QB_DQDONE]);
+                J += n;
+            }
+        }
+        __syncwarp();
+    } else if (warp < kProdWarp0) {
+        // query rows: two math warpgroups, each owning 64 of the 128 key columns
+        const int hf = warp >> 2;
+        const int r = ((warp & 3) << 5) | lane;
+        const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+        // this row of Q -> TMEM (the A operand of S), warpgroup 0
+        auto load_q = [&](const Item& I) {
+            const int i = I.i0 + r;
+            const __nv_bfloat16* src = a.q + ((I.bl + (i < a.L ? i : 0)) * a.H + I.h) * D;
+            uint32_t wq[D / 2];
+#pragma unroll
+            for (int c = 0; c < D / 8; ++c) {
+                uint4 x = make_uint4(0u, 0u, 0u, 0u);
+                if (i < a.L) x = *reinterpret_cast<const uint4*>(src + c * 8);
+                wq[4 * c] = x.x, wq[4 * c + 1] = x.y, wq[4 * c + 2] = x.z, wq[4 * c + 3] = x.w;
+            }
+#pragma unroll
+            for (int c = 0; c < D / 64; ++c) tmem_st32u(tQ + lane_off + c * 32, wq + c * 32);
+            tmem_wait_st();
+            tc_before_sync();
+            mbar_arrive(&bars[QB_QFULL]);
+        };
+        if (hf == 0 && (int)blockIdx.x < nitems) load_q(item(blockIdx.x));
+        int J = 0, it = 0, tr0 = 1 << 28;
+        const bool trl = lane == 0 && (warp & 3) == 0;
+        for (int wi = blockIdx.x; wi < nitems; wi += gridDim.x, ++it) {
+        const Item I = item(wi);
+        if (it == 6) tr0 = J;
+        const int b = I.b, h = I.h, n_sel = I.n_sel, n = I.n, jw0 = I.jw0;
+        const int64_t bl = I.bl;
+        const int i = I.i0 + r;
+        if (hf == 0 && wi + (int)gridDim.x < nitems) {  // the next item's Q row, for load_q
+            const Item N = item(wi + gridDim.x);
+            const int ni = N.i0 + r;
+            if (ni < a.L) {
+                const char* src = reinterpret_cast<const char*>(a.q + ((N.bl + ni) * a.H + N.h) * D);
+#pragma unroll
+                for (int c = 0; c < D * 2; c += 128) prefetch_l2(src + c);
+            }
+        }
+        const int t = i - a.w;
+        const float tau_i = (t >= 0 && a.R1 > 0) ? a.tauf[bl + t] : -INFINITY;
+        const int lo_win = max(i - a.w + 1, 0);
+        const int64_t hl = ((int64_t)b * a.H + h) * a.L;
+        const float nlse2 = i < a.L ? -a.lse2[hl + i] : -INFINITY;  // i >= L: every p = 0
+        const float dlt = i < a.L ? a.delta[hl + i] : 0.f;
+        const float sl2 = a.scale_log2;
+        const float2 sl22 = make_float2(sl2, sl2), nl2 = make_float2(nlse2, nlse2), ndl = make_float2(-dlt, -dlt);
+        const int c0 = hf * 64;
+        float rsum = 0.f;
+        for (int jt = 0; jt < n; ++jt, ++J) {
+            const bool is_sel = jt < n_sel;
+            const int ks = J % kNS;
+            if (trl) TRQ(hf, J, 9);
+            mbar_wait(&bars[QB_SFULL], J & 1);
+            if (is_sel) mbar_wait(&bars[QB_MFULL + ks], (J / kNS) & 1);
+            if (trl) TRQ(hf, J, 0);
+            tc_after_sync();
+            float sv[64], dp[64];
+            tmem_ld32(tS + lane_off + c0, sv);
+            tmem_ld32(tS + lane_off + c0 + 32, sv + 32);
+            tmem_ld32(tP + lane_off + c0, dp);
+            tmem_ld32(tP + lane_off + c0 + 32, dp + 32);
+            tmem_wait_ld();
+            tc_before_sync();
+            mbar_arrive(&bars[QB_SEMPTY]);  // S/dP of the next tile may overwrite now
+            bool plain = true;
+            if (is_sel) {
+                const int* mk = meta + (ks * 3) * 128 + c0;
+                const int* ml = mk + 128;
+                const float* mu = reinterpret_cast<const float*>(mk + 256);
+                const int fl = tflags[ks * 4];
+                if (!(fl & 1)) {  // per-key interval mask j <= t < leave_j: (unsigned)(t - j) < leave_j - j
+#pragma unroll
+                    for (int c = 0; c < 64; c += 4) {
+                        const int4 kj = *reinterpret_cast<const int4*>(mk + c);
+                        const int4 ex = *reinterpret_cast<const int4*>(ml + c);
+                        sv[c + 0] = ((unsigned)(t - kj.x) < (unsigned)ex.x) ? sv[c + 0] : -INFINITY;
+                        sv[c + 1] = ((unsigned)(t - kj.y) < (unsigned)ex.y) ? sv[c + 1] : -INFINITY;
+                        sv[c + 2] = ((unsigned)(t - kj.z) < (unsigned)ex.z) ? sv[c + 2] : -INFINITY;
+                        sv[c + 3] = ((unsigned)(t - kj.w) < (unsigned)ex.w) ? sv[c + 3] : -INFINITY;
+                    }
+                }
+                if (!(fl & 2)) {  // fractional gates present
+                    plain = false;
+                    if constexpr (!KEY_SOFT) {  // packed fp32x2 except gate saturation / support test
+                        float2 rs2 = make_float2(0.f, 0.f);
+                        const bool mst = a.mask_st != 0;
+#pragma unroll
+                        for (int c = 0; c < 64; c += 2) {
+                            const float2 uu = *reinterpret_cast<const float2*>(mu + c);
+                            const float g0 = __saturatef(uu.x - tau_i), g1 = __saturatef(uu.y - tau_i);
+                            float2 p2 = __ffma2_rn(make_float2(sv[c], sv[c + 1]), sl22, nl2);
+                            p2.x = ex2(p2.x);
+                            p2.y = ex2(p2.y);
+                            const float2 dp2 = make_float2(dp[c], dp[c + 1]);
+                            const float2 wv2 = mst ? make_float2(1.f, 1.f) : make_float2(g0, g1);
+                            const float2 cc2 = __fmul2_rn(p2, __ffma2_rn(wv2, dp2, ndl));
+                            const float2 fr2 = make_float2((g0 > 0.f && g0 < 1.f) ? 1.f : 0.f,
+                                                           (g1 > 0.f && g1 < 1.f) ? 1.f : 0.f);
+                            rs2 = __ffma2_rn(__fmul2_rn(p2, dp2), fr2, rs2);
+                            dp[c] = cc2.x;
+                            dp[c + 1] = cc2.y;
+                        }
+                        rsum += rs2.x + rs2.y;
+                    } else {
+#pragma unroll
+                    for (int c = 0; c < 64; c += 4) {
+                        const float4 uu = *reinterpret_cast<const float4*>(mu + c);
+                        const float ua[4] = {uu.x, uu.y, uu.z, uu.w};
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const float g = __saturatef(ua[e] - tau_i);
+                            const float raw = sv[c + e];
+                            const float kap = KEY_SOFT ? g : 1.f;
+                            // masked logits are -inf: keep them -inf under a zero gate
+                            const float x = (KEY_SOFT && raw == -INFINITY) ? raw : raw * kap;
+                            const float p = ex2(fmaf(x, sl2, nlse2));
+                            const float wv = a.mask_st ? 1.f : g;
+                            const float cc = p * fmaf(wv, dp[c + e], -dlt);
+                            float gm = p * dp[c + e];
+                            if (KEY_SOFT) gm += a.scale * cc * (raw == -INFINITY ? 0.f : raw);
+                            rsum += (g > 0.f && g < 1.f) ? gm : 0.f;
+                            dp[c + e] = cc * kap;
+                        }
+                    }
+                    }
+                }
+            } else {
+                const int kb = jw0 + (jt - n_sel) * 128 + c0;
+                const int cmin = lo_win - kb;
+                const int cmax = i - kb;
+                if (__any_sync(0xffffffffu, cmin > 0 || cmax < 63)) {
+#pragma unroll
+                    for (int c = 0; c < 64; ++c) sv[c] = (c >= cmin && c <= cmax) ? sv[c] : -INFINITY;
+                }
+            }
+            if (plain) {  // all gates 1: plain softmax backward, packed fp32x2
+#pragma unroll
+                for (int c = 0; c < 64; c += 2) {
+                    float2 x = __ffma2_rn(make_float2(sv[c], sv[c + 1]), sl22, nl2);
+                    if ((c & 7) == 6 && kDqPoly) {  // one pair in four on the FMA pipe (MUFU relief)
+                        x = ex2_poly2(x);
+                    } else {
+                        x.x = ex2(x.x);
+                        x.y = ex2(x.y);
+                    }
+                    const float2 d = __fmul2_rn(x, __fadd2_rn(make_float2(dp[c], dp[c + 1]), ndl));
+                    dp[c] = d.x;
+                    dp[c + 1] = d.y;
+                }
+            }
+            // dS -> TMEM (packed bf16x2), once dQ of the previous tile has read the buffer
+            if (J >= 1) mbar_wait(&bars[QB_DSEMPTY], (J - 1) & 1);
+            tc_after_sync();
+            {
+                uint32_t pk[16];
+#pragma unroll
+                for (int e = 0; e < 16; ++e) pk[e] = pack_bf16(dp[2 * e], dp[2 * e + 1]);
+                tmem_st16u(tDS + lane_off + hf * 32, pk);
+#pragma unroll
+                for (int e = 0; e < 16; ++e) pk[e] = pack_bf16(dp[32 + 2 * e], dp[33 + 2 * e]);
+                tmem_st16u(tDS + lane_off + hf * 32 + 16, pk);
+                tmem_wait_st();
+            }
+            tc_before_sync();
+            if (trl) TRQ(hf, J, 4);
+            mbar_arrive(&bars[QB_MEMPTY + ks]);
+            mbar_arrive(&bars[QB_DSFULL]);
+        }
+        // the next item's Q: the S MMAs of this item are complete (consumed above)
+        if (hf == 0 && wi + (int)gridDim.x < nitems) load_q(item(wi + gridDim.x));
+        if (trl) TRQ(hf, J - 1, 5);
+        mbar_wait(&bars[QB_DQDONE], it & 1);
+        if (trl) TRQ(hf, J - 1, 6);
+        tc_after_sync();
+        if (i < a.L && t >= 0 && a.R1 > 0 && rsum != 0.f) atomicAdd(a.rowsum + bl + t, (double)rsum);
+        __nv_bfloat16* orow = a.dq + ((bl + (i < a.L ? i : 0)) * a.H + h) * D + hf * (D / 2);
+        float xq[D / 2];
+#pragma unroll
+        for (int c = 0; c < D / 64; ++c) tmem_ld32(tDQ + lane_off + hf * (D / 2) + c * 32, xq + c * 32);
+        tmem_wait_ld();
+        tc_before_sync();
+        mbar_arrive(&bars[QB_DQEMPTY]);
+        if (trl) TRQ(hf, J - 1, 7);
+#pragma unroll
+        for (int c = 0; c < D / 64; ++c) {
+            const float* x = xq + c * 32;
+            if (i < a.L) {
+#pragma unroll
+                for (int e = 0; e < 32; e += 8) {
+                    uint4 pk;
+                    pk.x = pack_bf16(x[e] * a.scale, x[e + 1] * a.scale);
+                    pk.y = pack_bf16(x[e + 2] * a.scale, x[e + 3] * a.scale);
+                    pk.z = pack_bf16(x[e + 4] * a.scale, x[e + 5] * a.scale);
+                    pk.w = pack_bf16(x[e + 6] * a.scale, x[e + 7] * a.scale);
+                    *reinterpret_cast<uint4*>(orow + c * 32 + e) = pk;
+                }
+            }
+        }
+        }
+    }
+    tc_before_sync();
+    __syncthreads();
+    tc_after_sync();
+    if (warp == kMmaWarp) tmem_dealloc<512>(tmem);
+#undef TRQ
 }
 
 template <class K>
@@ -1567,6 +1973,7 @@ void launch_bwd(const BwdArgs& a, const skb_attn_desc& d, cudaStream_t st) {
         set_smem(k_bwd_dkdv_sel_tc<D, KS>, KSmem<D>::kAlloc);
         set_smem(k_bwd_dkdv_win_tc<D>, KWSmem<D>::kAlloc);
         set_smem(k_bwd_dq_tc<D, KS>, QSmem<D>::kAlloc);
+        set_smem(k_bwd_dq_p<D, KS>, QSmem<D>::kAlloc);
         attr = true;
     }
     if (a.R1 > 0 && a.T > 0) {
@@ -1590,8 +1997,15 @@ void launch_bwd(const BwdArgs& a, const skb_attn_desc& d, cudaStream_t st) {
         k_bwd_dkdv_win_tc<D><<<grid, kThreads, KWSmem<D>::kAlloc, st>>>(a);
         SKB_CHECK_LAUNCH();
     }
-    dim3 gq((unsigned)a.nqb, (unsigned)d.heads, (unsigned)d.batch);
-    k_bwd_dq_tc<D, KS><<<gq, kThreads, QSmem<D>::kAlloc, st>>>(a);
+    static const int dq_persist = getenv("SKB_DQ_PERSIST") ? atoi(getenv("SKB_DQ_PERSIST")) : 1;
+    if (dq_persist) {
+        const int64_t items = (int64_t)a.nqb * d.heads * d.batch;
+        const int grid = (int)std::min<int64_t>(items, num_sms());
+        k_bwd_dq_p<D, KS><<<grid, kThreads, QSmem<D>::kAlloc, st>>>(a);
+    } else {
+        dim3 gq((unsigned)a.nqb, (unsigned)d.heads, (unsigned)d.batch);
+        k_bwd_dq_tc<D, KS><<<gq, kThreads, QSmem<D>::kAlloc, st>>>(a);
+    }
     SKB_CHECK_LAUNCH();
 }
 
