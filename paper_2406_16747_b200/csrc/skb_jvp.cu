@@ -17,41 +17,52 @@ namespace skb {
 
 namespace {
 
+// M[t] = sum_{t' < t} mean_t' per sequence (M[T] = total): one CTA, coalesced
+// 1024-element chunks, a block scan per chunk carried across chunks.
 __global__ void __launch_bounds__(1024)
 k_mean_prefix(const double* __restrict__ rowsum, const int* __restrict__ nfrac,
               const double* __restrict__ tau, int L, int T, double* __restrict__ M) {
     __shared__ double wsum[32];
+    __shared__ double carry_s;
     const int b = blockIdx.x;
     const double* rs = rowsum + (int64_t)b * L;
     const int* nf = nfrac + (int64_t)b * L;
     const double* tb = tau + (int64_t)b * L;
     double* Mb = M + (int64_t)b * (L + 1);
-    const int per = (T + blockDim.x - 1) / blockDim.x;
-    const int lo = min(T, (int)threadIdx.x * per), hi = min(T, lo + per);
-    auto mean_at = [&](int t) {
-        const int n = nf[t];
-        return (n > 0 && tb[t] > -INFINITY) ? rs[t] / (double)n : 0.0;
-    };
-    double s = 0.0;
-    for (int t = lo; t < hi; ++t) s += mean_at(t);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    double incl = s;
+    double carry = 0.0;
+    for (int c0 = 0; c0 < T; c0 += 1024) {
+        const int t = c0 + threadIdx.x;
+        double x = 0.0;
+        if (t < T) {
+            const int n = nf[t];
+            x = (n > 0 && tb[t] > -INFINITY) ? rs[t] / (double)n : 0.0;
+        }
+        double incl = x;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const double y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
+        for (int o = 1; o < 32; o <<= 1) {
+            const double y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane == 31) wsum[wid] = incl;
+        __syncthreads();
+        if (wid == 0) {
+            double ws = wsum[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const double y = __shfl_up_sync(0xffffffffu, ws, o);
+                if (lane >= o) ws += y;
+            }
+            wsum[lane] = ws;  // inclusive over warps
+        }
+        __syncthreads();
+        const double pre = carry + (wid > 0 ? wsum[wid - 1] : 0.0);
+        if (t < T) Mb[t] = pre + incl - x;
+        if (threadIdx.x == 1023) carry_s = pre + incl;
+        __syncthreads();
+        carry = carry_s;
     }
-    if (lane == 31) wsum[wid] = incl;
-    __syncthreads();
-    double pre = 0.0;
-    for (int w = 0; w < wid; ++w) pre += wsum[w];
-    double run = pre + incl - s;
-    for (int t = lo; t < hi; ++t) {
-        Mb[t] = run;
-        run += mean_at(t);
-    }
-    if (lo < hi && hi == T) Mb[T] = run;
-    if (T == 0 && threadIdx.x == 0) Mb[0] = 0.0;
+    if (threadIdx.x == 0) Mb[T] = carry;
 }
 
 __global__ void k_jvp(const double* __restrict__ u, const double* __restrict__ tau,

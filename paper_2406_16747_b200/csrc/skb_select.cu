@@ -30,7 +30,7 @@ namespace skb {
 
 namespace {
 
-constexpr int kRankThreads = 256;
+constexpr int kRankThreads = 64;
 constexpr int kRankStage = 1024;
 constexpr int kTauThreads = 256;
 constexpr int kOverflowSlots = 16;
