@@ -76,7 +76,7 @@ def main(tag, launches_csv, rep):
         name = r[ki].split("(")[0].split("::")[-1]
         traffic[name] = rd + wr
     open(os.path.join(ROOT, "profiles", f"{tag}_ncu_attn.txt"), "w").write("\n".join(out) + "\n")
-    fwd = sum(v for k, v in traffic.items() if k.startswith("k_fwd_tc"))
+    fwd = sum(v for k, v in traffic.items() if k.startswith("k_fwd_"))
     bwd = sum(v for k, v in traffic.items() if k.startswith("k_bwd"))
     json.dump({"attn_fwd": fwd or None, "attn_bwd": bwd or None, "per_kernel": traffic, "source": tag},
               open(os.path.join(ROOT, "profiles", "traffic.json"), "w"), indent=1)
