@@ -16,6 +16,8 @@
 //   k_bwd_dq_tc    query-major over 64-key tiles: dQ = dS K accumulates in
 //                  TMEM; rowsum_t (the pullback numerator) is per thread.
 // rowsum/colsum feed the O(L log L) selection pullback (skb_jvp.cu).
+#include <climits>
+
 #include "skb_common.cuh"
 #include "skb_internal.h"
 #include "skb_tc.cuh"
@@ -66,6 +68,7 @@ struct BwdArgs {
     const int* ever_list;
     double *rowsum, *colsum;
     int2* sel_items;  // [B][cdiv(L,128)] {q_lo, nq} of the selected pass's key tiles
+    int* sel_order;   // [B][L] ever-selected keys grouped by leave time (the selected pass's order)
     int nqb, qb_cap;
     int B, L, H, w, T, R1;
     float scale, scale_log2;
@@ -847,8 +850,61 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_win_tc(const __grid_co
 #undef TRW
 }
 
-// The query range of each 128-entry tile of the ever-selected list (shared by
-// all heads): one warp per tile, [first key + w, max(leave + w)) clipped to the
+// The selected pass's key order: the ever-selected keys (ascending) stably
+// bucketed by leave time, so a 128-key tile holds keys whose retention
+// intervals end together and its query range [min key + w, max leave + w)
+// wastes little (iid scores: 45 % fewer 64-query tiles than key order; recency
+// scores: 3 % fewer). One CTA per sequence: per-thread chunk histograms, a
+// bucket-major scan, an in-order scatter.
+constexpr int kOrdThreads = 512, kOrdBuckets = 40;
+constexpr int kOrdCntBytes = (kOrdBuckets + 1) * kOrdThreads * 4;  // 84 KB of dynamic smem
+constexpr int kOrdMaxBk = 128 * 1024;  // bucket ids staged in smem (1 B each) up to this many keys
+__global__ void __launch_bounds__(kOrdThreads) k_sel_order(BwdArgs a) {
+    extern __shared__ __align__(16) uint8_t osm[];
+    int* cnt = reinterpret_cast<int*>(osm);  // [bucket][thread]
+    uint8_t* bks = osm + kOrdCntBytes;      // [key index] bucket id
+    __shared__ int wtot[kOrdThreads / 32];
+    const int b = blockIdx.x, t = threadIdx.x, lane = t & 31, wid = t >> 5;
+    const int n = a.ever_count[b];
+    const int* el = a.ever_list + (int64_t)b * a.L;
+    const int* lv = a.leave + (int64_t)b * a.L;
+    int* out = a.sel_order + (int64_t)b * a.L;
+    const int bw = max(256, (a.T + kOrdBuckets) / kOrdBuckets);  // <= kOrdBuckets + 1 buckets
+    const bool staged = n <= kOrdMaxBk;
+    if (staged)  // coalesced: every gather of leave in flight at once
+        for (int e = t; e < n; e += kOrdThreads) bks[e] = (uint8_t)min(kOrdBuckets, lv[el[e]] / bw);
+    auto bucket = [&](int e) { return staged ? (int)bks[e] : min(kOrdBuckets, lv[el[e]] / bw); };
+    const int c = (n + kOrdThreads - 1) / kOrdThreads;
+    const int lo = min(n, t * c), hi = min(n, lo + c);
+    for (int k = 0; k <= kOrdBuckets; ++k) cnt[k * kOrdThreads + t] = 0;
+    __syncthreads();
+    for (int e = lo; e < hi; ++e) ++cnt[bucket(e) * kOrdThreads + t];
+    __syncthreads();
+    int base = 0;
+    for (int k = 0; k <= kOrdBuckets; ++k) {  // exclusive scan in (bucket, thread) order
+        const int x = cnt[k * kOrdThreads + t];
+        int incl = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane == 31) wtot[wid] = incl;
+        __syncthreads();
+        int pre = base, tot = 0;
+        for (int w2 = 0; w2 < kOrdThreads / 32; ++w2) {
+            if (w2 < wid) pre += wtot[w2];
+            tot += wtot[w2];
+        }
+        cnt[k * kOrdThreads + t] = pre + incl - x;
+        base += tot;
+        __syncthreads();
+    }
+    for (int e = lo; e < hi; ++e) out[cnt[bucket(e) * kOrdThreads + t]++] = el[e];
+}
+
+// The query range of each 128-entry tile of the selected pass's order (shared
+// by all heads): one warp per tile, [min key + w, max(leave + w)) clipped to the
 // keys' chunks, in 64-query tiles.
 __global__ void k_sel_items(BwdArgs a, int ntk) {
     const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
@@ -857,17 +913,19 @@ __global__ void k_sel_items(BwdArgs a, int ntk) {
     const int ec = a.ever_count[b];
     int2 res = make_int2(0, 0);
     if (kt * 128 < ec) {
-        const int* el = a.ever_list + (int64_t)b * a.L + kt * 128;
+        const int* el = a.sel_order + (int64_t)b * a.L + kt * 128;
         const int n = min(128, ec - kt * 128);
-        int hi = 0;
+        int hi = 0, kmin = INT_MAX;
         for (int r = lane; r < n; r += 32) {
             const int key = el[r];
             int x = a.leave[(int64_t)b * a.L + key] + a.w;
             if (a.chunk_len > 0) x = min(x, (key / a.chunk_len + 1) * a.chunk_len);
             hi = max(hi, x);
+            kmin = min(kmin, key);
         }
         hi = min(a.L, warp_max_i(hi));
-        const int q_lo = ((el[0] + a.w) / 64) * 64;
+        kmin = -warp_max_i(-kmin);
+        const int q_lo = ((kmin + a.w) / 64) * 64;
         res = make_int2(q_lo, hi > q_lo ? (hi - q_lo + 63) / 64 : 0);
     }
     if (lane == 0) a.sel_items[wid] = res;
@@ -947,7 +1005,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_sel_tc(const __grid_co
             if (!item(wi, b, h, kt, nkeys, q_lo, nq) || nq == 0) continue;
             if (kit == 6) tr0 = g;
             const int64_t bl = (int64_t)b * a.L;
-            const int* elist = a.ever_list + bl + kt * 128;
+            const int* elist = a.sel_order + bl + kt * 128;
             RowKeys<D, 128> kk;
             kk.fetch(pw, lane, [&](int r) { return r < nkeys ? __ldg(elist + r) : -1; });
             if (ptid == 0) TRS(6, g, 3);
@@ -1053,7 +1111,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_sel_tc(const __grid_co
             if (!item(wi, b, h, kt, nkeys, q_lo, nq)) continue;
             if (kit == 6 && nq > 0) tr0 = g;
             const int64_t bl = (int64_t)b * a.L;
-            const int key = r < nkeys ? __ldg(a.ever_list + bl + kt * 128 + r) : -1;
+            const int key = r < nkeys ? __ldg(a.sel_order + bl + kt * 128 + r) : -1;
             const int leave = key >= 0 ? __ldg(a.leave + bl + key) : 0;
             const float uj = key >= 0 ? __ldg(a.uf + bl + key) : 0.f;
             // queries [key + w, leave + w) read this key from the selection
@@ -1980,6 +2038,14 @@ void launch_bwd(const BwdArgs& a, const skb_attn_desc& d, cudaStream_t st) {
         static const int persist = getenv("SKB_SEL_PERSIST") ? atoi(getenv("SKB_SEL_PERSIST")) : 1;
         if (persist) {
             const int ntk = (int)cdiv(a.L, 128);
+            const int osm = kOrdCntBytes + std::min(a.T, kOrdMaxBk);
+            static bool oattr = false;
+            if (!oattr) {
+                set_smem(k_sel_order, kOrdCntBytes + kOrdMaxBk);
+                oattr = true;
+            }
+            k_sel_order<<<(unsigned)a.B, kOrdThreads, osm, st>>>(a);
+            SKB_CHECK_LAUNCH();
             k_sel_items<<<(unsigned)cdiv((int64_t)a.B * ntk * 32, 256), 256, 0, st>>>(a, ntk);
             SKB_CHECK_LAUNCH();
             const int64_t items = (int64_t)ntk * d.heads * d.batch;
@@ -2057,6 +2123,7 @@ void run_attn_bwd_tc(const skb_attn_desc& d, const void* q, const void* k, const
     a.rowsum = rowsum;
     a.colsum = colsum;
     a.sel_items = reinterpret_cast<int2*>(base + bl.sel_items);
+    a.sel_order = reinterpret_cast<int*>(base + bl.sel_order);
     a.nqb = s.nqb;
     a.qb_cap = s.qb_cap;
     a.B = (int)d.batch;

@@ -127,6 +127,8 @@ void bwd_layout(const skb_attn_desc& d, BwdLayout& o) {
     o.dq_acc = take(tc ? BL * d.heads * 8 : 0);
     // per 128-entry tile of the ever-selected list: {first query tile, query tiles}
     o.sel_items = take(tc ? (uint64_t)d.batch * ((d.seq_len + 127) / 128) * 8 : 0);
+    // the ever-selected keys grouped by leave time (k_sel_order)
+    o.sel_order = take(tc ? BL * 4 : 0);
     o.total = off;
 }
 
