@@ -34,6 +34,9 @@ constexpr int kRankThreads = 64;
 constexpr int kRankStage = 1024;
 constexpr int kTauThreads = 256;
 constexpr int kOverflowSlots = 16;
+#ifndef SKB_TAU_EXP
+#define SKB_TAU_EXP 0
+#endif
 
 // ---------------------------------------------------------------- ranks
 // One thread per position j. The sequence streams through shared memory in
@@ -150,6 +153,7 @@ struct TauArgs {
     int* nfrac;
     int* ovf_count;  // [1]
     int* ovf_items;  // [B * nchunks]
+    int* ovf_flag;   // [B * nchunks] pass-1 overflow marks (segmented pass 2)
     double* scratch;
     int64_t scratch_stride;
     int L, T, R2;
@@ -157,13 +161,13 @@ struct TauArgs {
     int cap;  // power of two, smem capacity for the band
 };
 
-// One chunk: band collection, sort, exact solve at the chunk start, stream replay.
-// Returns false (without writing outputs) when the band exceeds `cap`.
-__device__ bool tau_chunk(const TauArgs& a, int b, int chunk, double* bz, double* P, int cap,
-                          bool probe_only_if_overflow) {
-    __shared__ double red_d[32];
+__device__ void tau_chunk_tail(const TauArgs& a, int b, int chunk, const double* bz, double* P, int mcount,
+                               double* red_d);
+
+// The band of push time t0: every prefix score above theta(t0) - 1, sorted
+// descending into bz. Returns its size, or -1 (nothing written) above `cap`.
+__device__ int tau_band(const TauArgs& a, int b, int t0, double* bz, int cap, double* red_d) {
     __shared__ int s_m;
-    const int t0 = chunk * kChunk;
     const double* ub = a.u + (int64_t)b * a.L;
     const int* lv = a.leave2 + (int64_t)b * a.L;
 
@@ -184,9 +188,8 @@ __device__ bool tau_chunk(const TauArgs& a, int b, int chunk, double* bz, double
     if (mine) atomicAdd(&s_m, mine);
     __syncthreads();
     const int mcount = s_m;
-    (void)probe_only_if_overflow;
     __syncthreads();
-    if (mcount > cap) return false;
+    if (mcount > cap) return -1;
     if (threadIdx.x == 0) s_m = 0;
     __syncthreads();
     for (int j = threadIdx.x; j < t0; j += blockDim.x) {
@@ -199,6 +202,27 @@ __device__ bool tau_chunk(const TauArgs& a, int b, int chunk, double* bz, double
     for (int i = mcount + threadIdx.x; i < n2; i += blockDim.x) bz[i] = -CUDART_INF;
     __syncthreads();
     bitonic_desc(bz, n2);
+    return mcount;
+}
+
+// One chunk: band collection, sort, exact solve at the chunk start, stream replay.
+// Returns false (without writing outputs) when the band exceeds `cap`.
+__device__ bool tau_chunk(const TauArgs& a, int b, int chunk, double* bz, double* P, int cap,
+                          bool probe_only_if_overflow) {
+    __shared__ double red_d[32];
+    (void)probe_only_if_overflow;
+    const int mcount = tau_band(a, b, chunk * kChunk, bz, cap, red_d);
+    if (mcount < 0) return false;
+    tau_chunk_tail(a, b, chunk, bz, P, mcount, red_d);
+    return true;
+}
+
+// Exact state at the chunk start from the sorted band bz[0, mcount), then the
+// stream's own push/scan for the chunk's arrivals.
+__device__ void tau_chunk_tail(const TauArgs& a, int b, int chunk, const double* bz, double* P, int mcount,
+                               double* red_d) {
+    const int t0 = chunk * kChunk;
+    const double* ub = a.u + (int64_t)b * a.L;
     excl_prefix(bz, P, mcount, red_d);
 
     // exact state after pushes [0, t0)
@@ -206,7 +230,12 @@ __device__ bool tau_chunk(const TauArgs& a, int b, int chunk, double* bz, double
     int ws = mcount, uf = mcount;
     if ((double)t0 >= a.k && mcount > 0) {
         int frac0;
-        tau0 = solve_sorted(bz, P, mcount, a.k, red_d, &frac0);
+#if SKB_TAU_EXP == 2
+        tau0 = bz[0] - 1.0;  // experiment: no exact solve
+        frac0 = 0;
+#else
+        tau0 = solve_sorted_fast(bz, P, mcount, a.k, red_d, &frac0);
+#endif
         ws = n_gt(bz, mcount, tau0);
         uf = n_ge(bz, mcount, tau0 + 1.0);
     }
@@ -233,7 +262,7 @@ __device__ bool tau_chunk(const TauArgs& a, int b, int chunk, double* bz, double
         }
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && SKB_TAU_EXP != 1) {  // (experiment 1: no replay)
         uint32_t smask = 0, fmask = 0;
         double tau = tau0;
         double sum_s = P[ws], sum_f = P[uf];
@@ -306,7 +335,7 @@ __device__ bool tau_chunk(const TauArgs& a, int b, int chunk, double* bz, double
             a.nfrac[(int64_t)b * a.L + t] = frac;
         }
     }
-    return true;
+    __syncthreads();
 }
 
 __global__ void __launch_bounds__(kTauThreads) k_tau_chunks(TauArgs a) {
@@ -318,7 +347,81 @@ __global__ void __launch_bounds__(kTauThreads) k_tau_chunks(TauArgs a) {
         if (threadIdx.x == 0) {
             const int slot = atomicAdd(a.ovf_count, 1);
             a.ovf_items[slot] = b * gridDim.x + chunk;
+            a.ovf_flag[b * gridDim.x + chunk] = 1;
         }
+    }
+}
+
+// Pass 2, segmented: a CTA owns kSegChunks consecutive chunks and handles its
+// flagged ones from the first to the last. The band is sorted once, at the
+// first; each later chunk start merges the previous chunk's <= 32 arrivals in
+// (ranked on one warp, placed by binary search), takes theta = the R2-th band
+// entry (every top-R2 score exceeds the previous cut, theta never decreases)
+// and trims at theta - 1: the same band, hence the same tau, as a fresh sort.
+constexpr int kSegChunks = 8;
+__global__ void __launch_bounds__(kTauThreads) k_tau_segments(TauArgs a, int nchunks, int* q2_count, int* q2_items) {
+    extern __shared__ double smem[];
+    __shared__ double red_d[32];
+    __shared__ double s_new[kChunk];
+    __shared__ int s_lim[2];
+    const int b = blockIdx.y, seg = blockIdx.x;
+    const int c_lo = seg * kSegChunks, c_hi = min(nchunks, c_lo + kSegChunks);
+    const int* fl = a.ovf_flag + (int64_t)b * nchunks;
+    if (threadIdx.x == 0) {
+        int f = -1, l = -1;
+        for (int c = c_lo; c < c_hi; ++c)
+            if (fl[c]) {
+                if (f < 0) f = c;
+                l = c;
+            }
+        s_lim[0] = f;
+        s_lim[1] = l;
+    }
+    __syncthreads();
+    const int cf = s_lim[0], cl = s_lim[1];
+    if (cf < 0) return;
+    double* bz = smem;
+    double* bz2 = smem + a.cap;
+    double* P = smem + 2 * a.cap;
+    const double* ub = a.u + (int64_t)b * a.L;
+    int m = tau_band(a, b, cf * kChunk, bz, a.cap, red_d);
+    for (int c = cf; c <= cl; ++c) {
+        if (c > cf) {
+            const int tp = (c - 1) * kChunk;
+            const int nv = min(kChunk, a.T - tp);
+            if (m < 0 || m + nv > a.cap) {
+                m = -1;
+            } else {
+                if (threadIdx.x < 32) {  // the previous chunk's arrivals, descending
+                    const int lane = threadIdx.x;
+                    const double cz = lane < nv ? ub[tp + lane] : -CUDART_INF;
+                    int rank = 0;
+                    for (int e = 0; e < nv; ++e) {
+                        const double y = __shfl_sync(0xffffffffu, cz, e);
+                        rank += (y > cz) || (y == cz && e < lane);
+                    }
+                    if (lane < nv) s_new[rank] = cz;
+                }
+                __syncthreads();
+                for (int i = threadIdx.x; i < m; i += blockDim.x) bz2[i + n_gt(s_new, nv, bz[i])] = bz[i];
+                for (int e = threadIdx.x; e < nv; e += blockDim.x) bz2[e + n_ge(bz, m, s_new[e])] = s_new[e];
+                __syncthreads();
+                double* t = bz;
+                bz = bz2;
+                bz2 = t;
+                m += nv;
+                const int t0 = c * kChunk;
+                const double theta = (t0 >= a.R2 && a.R2 > 0) ? bz[a.R2 - 1] : -CUDART_INF;
+                m = n_gt(bz, m, theta - 1.0);
+            }
+        }
+        if (m < 0) {  // beyond the large cap: the global-scratch pass takes the rest
+            if (threadIdx.x == 0)
+                for (int cc = c; cc <= cl; ++cc)
+                    if (fl[cc]) q2_items[atomicAdd(q2_count, 1)] = b * nchunks + cc;
+            return;
+        }
+        if (fl[c]) tau_chunk_tail(a, b, c, bz, P, m, red_d);
     }
 }
 
@@ -550,7 +653,7 @@ void select_layout(const skb_attn_desc& d, skb_select_layout& o) {
     o.qb_list = take(B * nqb * cap * 4);
     o.ever_count = take(B * 4);
     o.ever_list = take(B * L * 4);
-    o.misc = take((2 + 2 * B * nch) * 4);  // two overflow queues: [count, items...] x 2
+    o.misc = take((2 + 3 * B * nch) * 4);  // two overflow queues [count, items...] + pass-1 flags
     const int64_t cap2 = next_pow2((int)std::max<int64_t>(L, 1));
     o.scratch = take((uint64_t)kOverflowSlots * (cap2 + L + 1) * 8);
     o.uf = take(B * L * 4);
@@ -617,7 +720,7 @@ void run_select(const skb_attn_desc& d, const double* u, void* ws, cudaStream_t 
     }
     if (d.k > 0.0 && T > 0) {
         const int nch = (int)cdiv(T, kChunk);
-        SKB_CHECK_CUDA(cudaMemsetAsync(misc, 0, (2 + 2 * (size_t)B * nch) * 4, st));
+        SKB_CHECK_CUDA(cudaMemsetAsync(misc, 0, (2 + 3 * (size_t)B * nch) * 4, st));
         int* q2 = misc + 1 + B * nch;  // second queue: [count, items...]
         TauArgs a;
         a.u = u;
@@ -626,6 +729,7 @@ void run_select(const skb_attn_desc& d, const double* u, void* ws, cudaStream_t 
         a.nfrac = nfrac;
         a.ovf_count = misc;
         a.ovf_items = misc + 1;
+        a.ovf_flag = misc + 2 + 2 * B * nch;
         a.L = L;
         a.T = T;
         a.R2 = R2;
@@ -643,6 +747,8 @@ void run_select(const skb_attn_desc& d, const double* u, void* ws, cudaStream_t 
                                                 (int)(8192 * 2 * sizeof(double) + 16)));
             SKB_CHECK_CUDA(cudaFuncSetAttribute(k_tau_chunks_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                 (int)(8192 * 2 * sizeof(double) + 16)));
+            SKB_CHECK_CUDA(cudaFuncSetAttribute(k_tau_segments, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)(8192 * 3 * sizeof(double) + 16)));
             attr_set = true;
         }
         dim3 g(nch, B);
@@ -651,8 +757,8 @@ void run_select(const skb_attn_desc& d, const double* u, void* ws, cudaStream_t 
         if (cap_big > a.cap) {
             TauArgs a2 = a;
             a2.cap = cap_big;
-            k_tau_chunks_big<<<std::min(B * nch, 4 * 148), kTauThreads, (size_t)cap_big * 2 * sizeof(double) + 16, st>>>(
-                a2, nch, q2, q2 + 1);
+            dim3 gs((unsigned)cdiv(nch, kSegChunks), (unsigned)B);
+            k_tau_segments<<<gs, kTauThreads, (size_t)cap_big * 3 * sizeof(double) + 16, st>>>(a2, nch, q2, q2 + 1);
             SKB_CHECK_LAUNCH();
             a.ovf_count = q2;  // the global-scratch pass serves what is left
             a.ovf_items = q2 + 1;

@@ -148,4 +148,74 @@ __device__ inline double solve_sorted(const double* z, const double* P, int m, d
     return 0.5 * (lo + hi);
 }
 
+// solve_sorted with the bracketing breakpoints found by a warp-wide 32-ary
+// search instead of evaluating F at all 2m breakpoints: F is non-increasing in
+// b, so over each descending breakpoint list ({z_i}, {z_i - 1}) the set where
+// F >= k is a suffix. Warp 0 searches; the block shares the result.
+__device__ inline double solve_sorted_fast(const double* z, const double* P, int m, double k, double* sbuf32,
+                                           int* frac) {
+    {
+        const double kr = rint(k);
+        if (fabs(kr - k) <= 1e-9 && kr >= 1.0 && kr <= (double)m) {
+            const int u = (int)kr;
+            const double hi = z[u - 1] - 1.0;
+            const double lo = u < m ? z[u] : hi - 1.0;
+            if (lo <= hi) {
+                *frac = 0;
+                return 0.5 * (lo + hi);
+            }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        double blo = -INFINITY, bhi = INFINITY;
+        for (int list = 0; list < 2; ++list) {
+            const double off = list == 0 ? 0.0 : -1.0;
+            int lo = 0, hi = m;  // first index in [lo, hi] with F(bp) >= k (m: none)
+            while (hi > lo) {
+                const int span = hi - lo;
+                // span <= 32: lane j probes lo + j; else evenly spaced probes (lane 0: lo)
+                const int p = span <= 32 ? lo + min(lane, span - 1) : lo + (int)(((int64_t)span * lane) / 32);
+                const bool ge = f_at(z, P, m, z[p] + off) >= k;
+                const unsigned bal = __ballot_sync(0xffffffffu, ge);
+                if (span <= 32) {
+                    const unsigned below = bal & ((span >= 32) ? 0xffffffffu : ((1u << span) - 1u));
+                    hi = below ? lo + (__ffs(below) - 1) : hi;
+                    lo = hi;
+                } else {
+                    if (bal & 1u) {
+                        hi = lo;
+                    } else {
+                        const int f = bal ? __ffs(bal) - 1 : 32;  // first probe with F >= k
+                        const int plo = lo + (int)(((int64_t)span * (f - 1)) / 32);
+                        const int phi = f < 32 ? lo + (int)(((int64_t)span * f) / 32) : hi;
+                        lo = plo + 1;
+                        hi = phi;
+                    }
+                }
+            }
+            if (hi < m) blo = fmax(blo, z[hi] + off);
+            if (hi > 0) bhi = fmin(bhi, z[hi - 1] + off);
+        }
+        if (lane == 0) {
+            sbuf32[0] = blo;
+            sbuf32[1] = bhi;
+        }
+    }
+    __syncthreads();
+    const double blo = sbuf32[0], bhi = sbuf32[1];
+    __syncthreads();
+    const double mid = 0.5 * (blo + bhi);
+    const int us = n_ge(z, m, mid + 1.0), wsx = n_gt(z, m, mid);
+    if (wsx > us) {
+        *frac = wsx - us;
+        return (P[wsx] - P[us] + (double)us - k) / (double)(wsx - us);
+    }
+    *frac = 0;
+    const double hi = z[us - 1] - 1.0;
+    const double lo = us < m ? z[us] : hi - 1.0;
+    return 0.5 * (lo + hi);
+}
+
 }  // namespace skb
