@@ -358,19 +358,23 @@ __global__ void __launch_bounds__(kTauThreads) k_tau_chunks(TauArgs a) {
 // (ranked on one warp, placed by binary search), takes theta = the R2-th band
 // entry (every top-R2 score exceeds the previous cut, theta never decreases)
 // and trims at theta - 1: the same band, hence the same tau, as a fresh sort.
+// P1 (the first pass, small cap): every chunk of the segment; past the cap the
+// remaining chunks are flagged for pass 2 (large cap, flagged chunks only).
 constexpr int kSegChunks = 8;
-__global__ void __launch_bounds__(kTauThreads) k_tau_segments(TauArgs a, int nchunks, int* q2_count, int* q2_items) {
+template <bool P1>
+__global__ void __launch_bounds__(kTauThreads) k_tau_segments(TauArgs a, int nchunks, int seg_chunks, int* q2_count,
+                                                              int* q2_items) {
     extern __shared__ double smem[];
     __shared__ double red_d[32];
     __shared__ double s_new[kChunk];
     __shared__ int s_lim[2];
     const int b = blockIdx.y, seg = blockIdx.x;
-    const int c_lo = seg * kSegChunks, c_hi = min(nchunks, c_lo + kSegChunks);
-    const int* fl = a.ovf_flag + (int64_t)b * nchunks;
+    const int c_lo = seg * seg_chunks, c_hi = min(nchunks, c_lo + seg_chunks);
+    int* fl = a.ovf_flag + (int64_t)b * nchunks;
     if (threadIdx.x == 0) {
         int f = -1, l = -1;
         for (int c = c_lo; c < c_hi; ++c)
-            if (fl[c]) {
+            if (P1 || fl[c]) {
                 if (f < 0) f = c;
                 l = c;
             }
@@ -415,13 +419,19 @@ __global__ void __launch_bounds__(kTauThreads) k_tau_segments(TauArgs a, int nch
                 m = n_gt(bz, m, theta - 1.0);
             }
         }
-        if (m < 0) {  // beyond the large cap: the global-scratch pass takes the rest
+        if (m < 0) {  // beyond the cap: the next pass takes the rest
             if (threadIdx.x == 0)
-                for (int cc = c; cc <= cl; ++cc)
-                    if (fl[cc]) q2_items[atomicAdd(q2_count, 1)] = b * nchunks + cc;
+                for (int cc = c; cc <= cl; ++cc) {
+                    if (P1) {  // flag (segmented pass 2) and queue (the global-scratch pass)
+                        fl[cc] = 1;
+                        a.ovf_items[atomicAdd(a.ovf_count, 1)] = b * nchunks + cc;
+                    } else if (fl[cc]) {
+                        q2_items[atomicAdd(q2_count, 1)] = b * nchunks + cc;
+                    }
+                }
             return;
         }
-        if (fl[c]) tau_chunk_tail(a, b, c, bz, P, m, red_d);
+        if (P1 || fl[c]) tau_chunk_tail(a, b, c, bz, P, m, red_d);
     }
 }
 
@@ -747,18 +757,28 @@ void run_select(const skb_attn_desc& d, const double* u, void* ws, cudaStream_t 
                                                 (int)(8192 * 2 * sizeof(double) + 16)));
             SKB_CHECK_CUDA(cudaFuncSetAttribute(k_tau_chunks_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                 (int)(8192 * 2 * sizeof(double) + 16)));
-            SKB_CHECK_CUDA(cudaFuncSetAttribute(k_tau_segments, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            SKB_CHECK_CUDA(cudaFuncSetAttribute(k_tau_segments<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)(8192 * 3 * sizeof(double) + 16)));
+            SKB_CHECK_CUDA(cudaFuncSetAttribute(k_tau_segments<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                 (int)(8192 * 3 * sizeof(double) + 16)));
             attr_set = true;
         }
-        dim3 g(nch, B);
-        k_tau_chunks<<<g, kTauThreads, (size_t)a.cap * 2 * sizeof(double) + 16, st>>>(a);
+        static const int p1seg = getenv("SKB_TAU_P1SEG") ? atoi(getenv("SKB_TAU_P1SEG")) : 0;  // per-chunk pass 1 measured faster
+        if (p1seg > 0) {
+            dim3 g1((unsigned)cdiv(nch, p1seg), (unsigned)B);
+            k_tau_segments<true><<<g1, kTauThreads, (size_t)a.cap * 3 * sizeof(double) + 16, st>>>(a, nch, p1seg,
+                                                                                                   nullptr, nullptr);
+        } else {
+            dim3 g(nch, B);
+            k_tau_chunks<<<g, kTauThreads, (size_t)a.cap * 2 * sizeof(double) + 16, st>>>(a);
+        }
         SKB_CHECK_LAUNCH();
         if (cap_big > a.cap) {
             TauArgs a2 = a;
             a2.cap = cap_big;
             dim3 gs((unsigned)cdiv(nch, kSegChunks), (unsigned)B);
-            k_tau_segments<<<gs, kTauThreads, (size_t)cap_big * 3 * sizeof(double) + 16, st>>>(a2, nch, q2, q2 + 1);
+            k_tau_segments<false><<<gs, kTauThreads, (size_t)cap_big * 3 * sizeof(double) + 16, st>>>(a2, nch, kSegChunks,
+                                                                                                    q2, q2 + 1);
             SKB_CHECK_LAUNCH();
             a.ovf_count = q2;  // the global-scratch pass serves what is left
             a.ovf_items = q2 + 1;
