@@ -150,15 +150,21 @@ def test_batched_sequences_are_independent(cuda, oracle):
         assert rel_err(res["du"][b], gu) < 1e-8
 
 
-@pytest.mark.parametrize("kind", ["recency", "iid", "ties", "constant"])
-def test_selection_long_sequence(cuda, oracle, kind):
+SEL_LONG = [(kind, 16384, 1024.0, 512) for kind in ("recency", "iid", "ties", "constant")] + [
+    # wide tau bands: the segmented large-cap pass and its global-scratch overflow
+    ("iid", 32768, 4096.0, 64),
+    ("iid", 12000, 300.5, 700),
+]
+
+
+@pytest.mark.parametrize("kind,L,k,w", SEL_LONG, ids=[f"{c[0]}-{c[1]}-{c[2]}" for c in SEL_LONG])
+def test_selection_long_sequence(cuda, oracle, kind, L, k, w):
     """cfg3-length sequence: retention intervals and tau against the oracle's
     heap restatement (bit-exact sets; tau 1e-9 on non-degenerate steps)."""
     import torch
 
     from paper_2406_16747_b200 import ops
 
-    L, k, w = 16384, 1024.0, 512
     rng = np.random.default_rng(99)
     u = _scores(rng, L, kind)
     cfg = ops.AttnConfig(k=k, window=w)
@@ -169,7 +175,7 @@ def test_selection_long_sequence(cuda, oracle, kind):
     # reference tau from the heap stream restatement
     tau_ref, _ = oracle.stream_taus(u[:T], k)
     # retention: size min(t+1, floor k) and membership = top-floor(k) of the prefix
-    kf = int(k)
+    kf = int(np.floor(k))
     order = np.lexsort((np.arange(T), -u[:T]))  # value desc, index asc
     rank_pos = np.empty(T, np.int64)
     rank_pos[order] = np.arange(T)
