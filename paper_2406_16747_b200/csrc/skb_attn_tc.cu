@@ -694,7 +694,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_p(const __grid_constant__ F
             const bool is_sel = jt < n_sel;
             const int ks = J % kKS;
             mbar_wait(&bars[B_SFULL + s], (J >> 1) & 1);
-            if (is_sel) mbar_wait(&bars[B_MFULL + ks], (J / kKS) & 1);
+            mbar_wait(&bars[B_MFULL + ks], (J / kKS) & 1);  // every phase observed (window tiles too)
             tc_after_sync();
             tmem_ld32(tS + lane_off + s * 128 + c0, sv);
             tmem_ld32(tS + lane_off + s * 128 + c0 + 32, sv + 32);
@@ -892,7 +892,7 @@ void launch_fwd(const FwdArgs& a, dim3 grid, cudaStream_t st) {
     static const int persist = getenv("SKB_FWD_PERSIST") ? atoi(getenv("SKB_FWD_PERSIST")) : 1;
     if (persist) {
         const int64_t items = (int64_t)grid.x * grid.y * grid.z;
-        const int g = (int)std::min<int64_t>(items, num_sms());
+        const int g = persist_grid(items);
         k_fwd_p<D, KS><<<g, kThreads, SM::kAlloc, st>>>(a);
     } else {
         k_fwd_tc<D, KS><<<grid, kThreads, SM::kAlloc, st>>>(a);

@@ -1864,7 +1864,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_p(const __grid_constant_
             const int ks = J % kNS;
             if (trl) TRQ(hf, J, 9);
             mbar_wait(&bars[QB_SFULL], J & 1);
-            if (is_sel) mbar_wait(&bars[QB_MFULL + ks], (J / kNS) & 1);
+            mbar_wait(&bars[QB_MFULL + ks], (J / kNS) & 1);  // every phase observed (window tiles too)
             if (trl) TRQ(hf, J, 0);
             tc_after_sync();
             float sv[64], dp[64];
@@ -2049,7 +2049,7 @@ void launch_bwd(const BwdArgs& a, const skb_attn_desc& d, cudaStream_t st) {
             k_sel_items<<<(unsigned)cdiv((int64_t)a.B * ntk * 32, 256), 256, 0, st>>>(a, ntk);
             SKB_CHECK_LAUNCH();
             const int64_t items = (int64_t)ntk * d.heads * d.batch;
-            const int grid = (int)std::min<int64_t>(items, num_sms());
+            const int grid = persist_grid(items);
             k_bwd_dkdv_sel_tc<D, KS><<<grid, kThreads, KSmem<D>::kAlloc, st>>>(a);
         } else {
             dim3 gs((unsigned)cdiv(a.T, 128), (unsigned)d.heads, (unsigned)d.batch);
@@ -2059,14 +2059,14 @@ void launch_bwd(const BwdArgs& a, const skb_attn_desc& d, cudaStream_t st) {
     }
     {
         const int64_t items = cdiv(a.L, 128) * d.heads * d.batch;
-        const int grid = (int)std::min<int64_t>(items, num_sms());
+        const int grid = persist_grid(items);
         k_bwd_dkdv_win_tc<D><<<grid, kThreads, KWSmem<D>::kAlloc, st>>>(a);
         SKB_CHECK_LAUNCH();
     }
     static const int dq_persist = getenv("SKB_DQ_PERSIST") ? atoi(getenv("SKB_DQ_PERSIST")) : 1;
     if (dq_persist) {
         const int64_t items = (int64_t)a.nqb * d.heads * d.batch;
-        const int grid = (int)std::min<int64_t>(items, num_sms());
+        const int grid = persist_grid(items);
         k_bwd_dq_p<D, KS><<<grid, kThreads, QSmem<D>::kAlloc, st>>>(a);
     } else {
         dim3 gq((unsigned)a.nqb, (unsigned)d.heads, (unsigned)d.batch);

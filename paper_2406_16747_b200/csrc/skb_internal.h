@@ -1,6 +1,8 @@
 // Internal interfaces shared by the CUDA translation units (not part of the C ABI).
 #pragma once
 
+#include <cstdlib>
+
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -8,6 +10,17 @@
 #include "sparsek_b200.h"
 
 namespace skb {
+
+// CTAs of a persistent grid over `items` work items: one per SM; the
+// SKB_MAX_CTAS environment variable caps it (tests and the sanitizer use it
+// to put many items, and ring wrap-arounds, on every CTA).
+int num_sms();
+inline int persist_grid(int64_t items) {
+    static const int cap = getenv("SKB_MAX_CTAS") ? atoi(getenv("SKB_MAX_CTAS")) : 0;
+    int64_t g = items < num_sms() ? items : num_sms();
+    if (cap > 0 && g > cap) g = cap;
+    return (int)(g > 0 ? g : 1);
+}
 
 // SM count of the current device (persistent grids)
 inline int num_sms() {

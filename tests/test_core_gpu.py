@@ -299,3 +299,45 @@ def test_full_size_tensor_core_path(cuda, oracle, case, kind):
             den_q += np.sum(dqq ** 2)
     assert np.sqrt(num_o / den_o) < 2e-2, np.sqrt(num_o / den_o)
     assert np.sqrt(num_q / den_q) < 2e-2, np.sqrt(num_q / den_q)
+
+
+@pytest.mark.parametrize("cap", ["2", "7"])
+def test_persistent_grids_many_items_per_cta(cuda, cap):
+    """The persistent kernels with their grid capped (SKB_MAX_CTAS): each CTA
+    walks dozens of work items, so every cross-item ring (K/V, Q/dO, S, the
+    accumulators, the partial and staging buffers) wraps many times; results
+    must match the gather path as with one item per CTA."""
+    import os
+    import subprocess
+    import sys
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    env = dict(os.environ, SKB_MAX_CTAS=cap)
+    r = subprocess.run([sys.executable, os.path.join(here, "scripts", "persist_check.py")], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
+def test_persistent_grid_size_never_changes_a_bit(cuda, tmp_path):
+    """Forward and backward outputs (o, lse, dq, dk, dv) are bit-identical with
+    one CTA, three CTAs and the full persistent grid: no cross-item ring state
+    leaks between work items."""
+    import os
+    import subprocess
+    import sys
+
+    import torch
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    outs = []
+    for cap in ("0", "1", "3"):
+        f = tmp_path / f"out{cap}.pt"
+        env = dict(os.environ, SKB_MAX_CTAS=cap)
+        r = subprocess.run([sys.executable, os.path.join(here, "scripts", "fwd_det.py"), str(f)], env=env,
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stdout + r.stderr
+        outs.append(torch.load(f))
+    for other in outs[1:]:
+        for kind in outs[0]:
+            for nm, x, y in zip(("o", "lse", "dq", "dk", "dv"), outs[0][kind], other[kind]):
+                assert torch.equal(x, y), (kind, nm)
