@@ -856,8 +856,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_win_tc(const __grid_co
 // wastes little (iid scores: 45 % fewer 64-query tiles than key order; recency
 // scores: 3 % fewer). One CTA per sequence: per-thread chunk histograms, a
 // bucket-major scan, an in-order scatter.
-constexpr int kOrdThreads = 512, kOrdBuckets = 40;
-constexpr int kOrdCntBytes = (kOrdBuckets + 1) * kOrdThreads * 4;  // 84 KB of dynamic smem
+constexpr int kOrdThreads = 256, kOrdBuckets = 64;  // bucket width 256 at cfg3 (measured best of 64..512)
+constexpr int kOrdCntBytes = (kOrdBuckets + 1) * kOrdThreads * 4;  // 65 KB of dynamic smem
 constexpr int kOrdMaxBk = 128 * 1024;  // bucket ids staged in smem (1 B each) up to this many keys
 __global__ void __launch_bounds__(kOrdThreads) k_sel_order(BwdArgs a) {
     extern __shared__ __align__(16) uint8_t osm[];
