@@ -133,6 +133,170 @@ k_rank_leave(const double* __restrict__ u, int L, int T, int R1, int R2, int* __
     }
 }
 
+// Two-kernel variant: (1) A_j = #{i < j : u_i >= u_j} with one CTA per
+// (64-key block, 1024-score chunk) — the triangle of pairs spread over the whole
+// GPU, partial counts added atomically into A; (2) one thread per key finishes
+// from A_j: A_j >= R2 leaves at entry, else the later scan for the
+// (R1-A_j)-th / (R2-A_j)-th strictly larger score, as in k_rank_leave.
+constexpr int kRankChunk = 1024;
+__global__ void __launch_bounds__(kRankThreads)
+k_rank_before(const double* __restrict__ u, int L, int T, int* __restrict__ A) {
+    __shared__ __align__(16) double su[kRankChunk];
+    const int b = blockIdx.z;
+    const int j0 = blockIdx.x * kRankThreads, c0 = blockIdx.y * kRankChunk;
+    if (c0 >= min(T, j0 + kRankThreads)) return;  // chunk entirely after the block's keys
+    const double* ub = u + (int64_t)b * L;
+    const int n = min(kRankChunk, T - c0);
+    for (int i = threadIdx.x; i < kRankChunk; i += kRankThreads) su[i] = i < n ? ub[c0 + i] : 0.0;
+    __syncthreads();
+    const int j = j0 + threadIdx.x;
+    if (j >= T) return;
+    const double uj = ub[j];
+    const int stop = min(n, j - c0);
+    int cnt = 0, ii = 0;
+    for (; ii + 8 <= stop; ii += 8) {
+        const double2 x0 = *reinterpret_cast<const double2*>(su + ii);
+        const double2 x1 = *reinterpret_cast<const double2*>(su + ii + 2);
+        const double2 x2 = *reinterpret_cast<const double2*>(su + ii + 4);
+        const double2 x3 = *reinterpret_cast<const double2*>(su + ii + 6);
+        cnt += (x0.x >= uj) + (x0.y >= uj) + (x1.x >= uj) + (x1.y >= uj) + (x2.x >= uj) + (x2.y >= uj) +
+               (x3.x >= uj) + (x3.y >= uj);
+    }
+    for (; ii < stop; ++ii) cnt += su[ii] >= uj;
+    if (cnt) atomicAdd(A + (int64_t)b * L + j, cnt);
+}
+
+__global__ void __launch_bounds__(kRankThreads)
+k_rank_after(const double* __restrict__ u, int L, int T, int R1, int R2, int* __restrict__ leave1,
+             int* __restrict__ leave2) {
+    __shared__ __align__(16) double su[kRankStage];
+    const int b = blockIdx.y;
+    const int j = blockIdx.x * kRankThreads + threadIdx.x;
+    const double* ub = u + (int64_t)b * L;
+    const bool active = j < T;
+    const double uj = active ? ub[j] : 0.0;
+    const int A = active ? leave1[(int64_t)b * L + j] : 0;  // k_rank_before's counts
+    int cnt = 0;
+    const int need1 = R1 - A, need2 = R2 - A;
+    int l1 = T, l2 = T;
+    bool done = !active;
+    if (active && A >= R2) {  // R2 earlier winners: never in the top R2 (nor the top R1)
+        l1 = j;
+        l2 = j;
+        done = true;
+    } else if (active && need1 <= 0) {
+        l1 = j;
+    }
+    const int jmin = blockIdx.x * kRankThreads;  // the block's first key: later scores start after it
+    for (int c0 = (jmin + 1) / 8 * 8; c0 < T; c0 += kRankStage) {
+        if (__syncthreads_and(done)) break;
+        for (int i = threadIdx.x; i < kRankStage; i += kRankThreads) su[i] = c0 + i < T ? ub[c0 + i] : 0.0;
+        __syncthreads();
+        if (done) continue;
+        const int n = min(kRankStage, T - c0);
+        int ii = max(0, j + 1 - c0);
+        if (ii >= n) continue;
+        auto hit = [&](double x, int i) {
+            if (x > uj) {
+                ++cnt;
+                if (cnt == need1) l1 = i;
+                if (cnt == need2) {
+                    l2 = i;
+                    done = true;
+                }
+            }
+        };
+        for (; ii < n && (ii & 7); ++ii) {
+            hit(su[ii], c0 + ii);
+            if (done) break;
+        }
+        if (done) continue;
+        for (; ii + 8 <= n; ii += 8) {
+            const double2 x0 = *reinterpret_cast<const double2*>(su + ii);
+            const double2 x1 = *reinterpret_cast<const double2*>(su + ii + 2);
+            const double2 x2 = *reinterpret_cast<const double2*>(su + ii + 4);
+            const double2 x3 = *reinterpret_cast<const double2*>(su + ii + 6);
+            const int g = (x0.x > uj) + (x0.y > uj) + (x1.x > uj) + (x1.y > uj) + (x2.x > uj) + (x2.y > uj) +
+                          (x3.x > uj) + (x3.y > uj);
+            const int nxt = cnt < need1 ? need1 : need2;
+            if (cnt + g >= nxt) {  // a target falls in this group: walk it
+                for (int e = 0; e < 8 && !done; ++e) hit(su[ii + e], c0 + ii + e);
+                if (done) break;
+            } else {
+                cnt += g;
+            }
+        }
+        if (done) continue;
+        for (; ii < n; ++ii) {
+            hit(su[ii], c0 + ii);
+            if (done) break;
+        }
+    }
+    if (active) {
+        leave1[(int64_t)b * L + j] = l1;
+        leave2[(int64_t)b * L + j] = l2;
+    }
+}
+
+// (2) as a warp per key: 128 later scores per step (4 coalesced loads per
+// lane), ballots and popcounts for the running count of strictly larger
+// scores, the target position by a rank search in the crossing ballot.
+__global__ void __launch_bounds__(256)
+k_rank_after_warp(const double* __restrict__ u, int L, int T, int R1, int R2, int* __restrict__ leave1,
+                  int* __restrict__ leave2) {
+    const int b = blockIdx.y;
+    const int lane = threadIdx.x & 31;
+    const int j = blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (j >= T) return;
+    const double* ub = u + (int64_t)b * L;
+    const double uj = ub[j];
+    const int A = leave1[(int64_t)b * L + j];  // k_rank_before's counts
+    int l1 = T, l2 = T;
+    if (A >= R2) {  // R2 earlier winners: never in the top R2 (nor the top R1)
+        l1 = j;
+        l2 = j;
+    } else {
+        const int need1 = R1 - A, need2 = R2 - A;
+        if (need1 <= 0) l1 = j;
+        int cnt = 0;
+        bool got1 = need1 <= 0;
+        // the position of the r-th (1-based) set bit of m
+        auto nth = [](unsigned m, int r) {
+            for (int k = 1; k < r; ++k) m &= m - 1;
+            return __ffs(m) - 1;
+        };
+        for (int i0 = j + 1; i0 < T; i0 += 128) {
+            double x[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int i = i0 + q * 32 + lane;
+                x[q] = i < T ? __ldg(ub + i) : -CUDART_INF;
+            }
+            bool fin = false;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const unsigned m = __ballot_sync(0xffffffffu, x[q] > uj);
+                const int c = __popc(m);
+                if (!got1 && cnt + c >= need1) {
+                    l1 = i0 + q * 32 + nth(m, need1 - cnt);
+                    got1 = true;
+                }
+                if (cnt + c >= need2) {
+                    l2 = i0 + q * 32 + nth(m, need2 - cnt);
+                    fin = true;
+                    break;
+                }
+                cnt += c;
+            }
+            if (fin) break;
+        }
+    }
+    if (lane == 0) {
+        leave1[(int64_t)b * L + j] = l1;
+        leave2[(int64_t)b * L + j] = l2;
+    }
+}
+
 // ---------------------------------------------------------------- tau
 __device__ __forceinline__ void argmin_hi(double& v, int& lane) {
 #pragma unroll
@@ -724,8 +888,17 @@ void run_select(const skb_attn_desc& d, const double* u, void* ws, cudaStream_t 
         k_leave_identity<<<g, 256, 0, st>>>(leave2, L);
         SKB_CHECK_LAUNCH();
     } else {
+        static const int rank2 = getenv("SKB_RANK2") ? atoi(getenv("SKB_RANK2")) : 1;
         dim3 g((unsigned)cdiv(T, kRankThreads), B);
-        k_rank_leave<<<g, kRankThreads, 0, st>>>(u, L, T, R1, R2, leave1, leave2);
+        if (rank2) {
+            SKB_CHECK_CUDA(cudaMemsetAsync(leave1, 0, (size_t)B * L * sizeof(int), st));
+            dim3 g1((unsigned)cdiv(T, kRankThreads), (unsigned)cdiv(T, kRankChunk), B);
+            k_rank_before<<<g1, kRankThreads, 0, st>>>(u, L, T, leave1);
+            SKB_CHECK_LAUNCH();
+            k_rank_after_warp<<<dim3((unsigned)cdiv(T, 8), B), 256, 0, st>>>(u, L, T, R1, R2, leave1, leave2);
+        } else {
+            k_rank_leave<<<g, kRankThreads, 0, st>>>(u, L, T, R1, R2, leave1, leave2);
+        }
         SKB_CHECK_LAUNCH();
     }
     if (d.k > 0.0 && T > 0) {
