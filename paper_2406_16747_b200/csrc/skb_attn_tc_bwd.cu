@@ -850,12 +850,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_win_tc(const __grid_co
 #undef TRW
 }
 
-// The selected pass's key order: the ever-selected keys (ascending) stably
-// bucketed by leave time, so a 128-key tile holds keys whose retention
-// intervals end together and its query range [min key + w, max leave + w)
-// wastes little (iid scores: 45 % fewer 64-query tiles than key order; recency
-// scores: 3 % fewer). One CTA per sequence: per-thread chunk histograms, a
-// bucket-major scan, an in-order scatter.
+// The selected pass's key order. Sparse ever-selected sets (e.g. iid scores,
+// ~25 % of the keys): the keys (ascending) stably bucketed by leave time, so a
+// 128-key tile holds keys whose retention intervals end together and its query
+// range [min key + w, max leave + w) wastes little (45 % fewer 64-query tiles
+// than key order, bwd 6.8 -> 4.7 ms at cfg3). Dense sets (recency scores: every
+// key is selected once): key order — the bucketed order saves only ~3 % of the
+// tiles there but scatters the row gathers and the partial stores (+8 % time).
+// One CTA per sequence: per-thread chunk histograms, a bucket-major scan, an
+// in-order scatter.
 constexpr int kOrdThreads = 256, kOrdBuckets = 64;  // bucket width 256 at cfg3 (measured best of 64..512)
 constexpr int kOrdCntBytes = (kOrdBuckets + 1) * kOrdThreads * 4;  // 65 KB of dynamic smem
 constexpr int kOrdMaxBk = 128 * 1024;  // bucket ids staged in smem (1 B each) up to this many keys
@@ -869,6 +872,11 @@ __global__ void __launch_bounds__(kOrdThreads) k_sel_order(BwdArgs a) {
     const int* el = a.ever_list + (int64_t)b * a.L;
     const int* lv = a.leave + (int64_t)b * a.L;
     int* out = a.sel_order + (int64_t)b * a.L;
+    if (2 * n > a.T) {  // dense (most keys are selected at some point): key order keeps the
+        // gathers and the 32-key partial groups contiguous, which measured faster
+        for (int e = t; e < n; e += kOrdThreads) out[e] = el[e];
+        return;
+    }
     const int bw = max(256, (a.T + kOrdBuckets) / kOrdBuckets);  // <= kOrdBuckets + 1 buckets
     const bool staged = n <= kOrdMaxBk;
     if (staged)  // coalesced: every gather of leave in flight at once
