@@ -270,6 +270,47 @@ class SparseKAttention {
     DeviceBuffer sel_, bws_;
 };
 
+// ------------------------------------------------------------------ scoring
+// ScoringParams minus w_score (selection.hpp:19-27).
+struct ScoringConfig {
+    bool timestep_norm = true;
+    bool norm_then_slope = true;
+    bool slope_enabled = true;
+    double slope_eps = 0.01;
+    skb_scoring c(int32_t chunk_len = 0) const {
+        skb_scoring s{};
+        s.norm_mode = timestep_norm ? 1 : 0;
+        s.slope_order = norm_then_slope ? 1 : 0;
+        s.slope_enabled = slope_enabled ? 1 : 0;
+        s.chunk_len = chunk_len;
+        s.slope_eps = slope_eps;
+        return s;
+    }
+};
+
+// score_tokens with a carried TimestepNormState (selection.hpp:55-56,
+// selection.cpp:13-31) for B sequences: the float64 state {count, mean, m2}
+// per sequence lives on the device and advances with every call.
+class ScoreState {
+  public:
+    ScoreState(int64_t batch, int64_t d_model, const ScoringConfig& sc)
+        : B_(batch), D_(d_model), sc_(sc), state_(batch * 3 * sizeof(double)) {
+        cuda_check(cudaMemset(state_.get(), 0, batch * 3 * sizeof(double)), "cudaMemset");
+    }
+    // x [B, n, D] of `dtype`, w_score float64 [D] -> raw/u float64 [B, n] (device buffers)
+    void score(const void* x, DType dtype, int64_t n, const double* w_score, double* raw, double* u,
+               cudaStream_t st = nullptr) {
+        const skb_scoring c = sc_.c();
+        check(skb_score_continue(B_, n, D_, (int32_t)dtype, x, w_score, &c, static_cast<double*>(state_.get()), raw,
+                                 u, st));
+    }
+
+  private:
+    int64_t B_, D_;
+    ScoringConfig sc_;
+    DeviceBuffer state_;
+};
+
 // ------------------------------------------------------------------ decode cache
 class SparseKvCache {  // cache.hpp:21-87 + generate_step (cache.cpp:570-577)
   public:

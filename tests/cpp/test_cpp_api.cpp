@@ -108,6 +108,37 @@ static int gpu_checks() {
             }
         }
     EXPECT(maxerr < 1e-5);
+    // incremental scoring: 1 + 5 + 10 rows through ScoreState == one 16-row call (bit for bit)
+    {
+        const int SB = 2, SN = 16, SD = 8;
+        std::vector<double> x(SB * SN * SD), w(SD);
+        for (auto& e : x) e = rnd();
+        for (auto& e : w) e = rnd();
+        DeviceBuffer dx(x.size() * 8), dw(w.size() * 8), r1(SB * SN * 8), u1(SB * SN * 8), r2(SB * SN * 8),
+            u2(SB * SN * 8);
+        cuda_check(cudaMemcpy(dw.get(), w.data(), w.size() * 8, cudaMemcpyHostToDevice), "H2D");
+        ScoringConfig sc;
+        ScoreState one(SB, SD, sc), parts(SB, SD, sc);
+        cuda_check(cudaMemcpy(dx.get(), x.data(), x.size() * 8, cudaMemcpyHostToDevice), "H2D");
+        one.score(dx.get(), DType::f64, SN, (const double*)dw.get(), (double*)r1.get(), (double*)u1.get());
+        std::vector<double> ua(SB * SN), ub(SB * SN);
+        cuda_check(cudaMemcpy(ua.data(), u1.get(), ua.size() * 8, cudaMemcpyDeviceToHost), "D2H");
+        int off = 0;
+        for (int n : {1, 5, 10}) {  // rows [off, off + n) of every sequence, packed [B, n, D]
+            std::vector<double> xs(SB * n * SD);
+            for (int b2 = 0; b2 < SB; ++b2)
+                for (int i = 0; i < n * SD; ++i) xs[(b2 * n) * SD + i] = x[(b2 * SN + off) * SD + i];
+            DeviceBuffer dxs(xs.size() * 8), rs(SB * n * 8), us(SB * n * 8);
+            cuda_check(cudaMemcpy(dxs.get(), xs.data(), xs.size() * 8, cudaMemcpyHostToDevice), "H2D");
+            parts.score(dxs.get(), DType::f64, n, (const double*)dw.get(), (double*)rs.get(), (double*)us.get());
+            std::vector<double> uh(SB * n);
+            cuda_check(cudaMemcpy(uh.data(), us.get(), uh.size() * 8, cudaMemcpyDeviceToHost), "D2H");
+            for (int b2 = 0; b2 < SB; ++b2)
+                for (int i = 0; i < n; ++i) ub[b2 * SN + off + i] = uh[b2 * n + i];
+            off += n;
+        }
+        for (int i = 0; i < SB * SN; ++i) EXPECT(ua[i] == ub[i]);
+    }
     std::printf("gpu ok (dense-limit max err %.3g)\n", maxerr);
     return 0;
 }
