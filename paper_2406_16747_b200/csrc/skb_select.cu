@@ -339,27 +339,51 @@ __device__ int tau_band(const TauArgs& a, int b, int t0, double* bz, int cap, do
     double theta = -CUDART_INF;
     if (t0 >= a.R2 && a.R2 > 0) {
         double mn = CUDART_INF;
-        for (int j = threadIdx.x; j < t0; j += blockDim.x)
-            if (lv[j] >= t0) mn = fmin(mn, ub[j]);
+        // 4 independent load pairs in flight per thread (the pass is latency-bound)
+        for (int j0 = threadIdx.x; j0 < t0; j0 += 4 * blockDim.x) {
+            int lvv[4];
+            double uv[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int j = j0 + q * blockDim.x;
+                lvv[q] = j < t0 ? lv[j] : -1;
+                uv[q] = j < t0 ? ub[j] : CUDART_INF;
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (lvv[q] >= t0) mn = fmin(mn, uv[q]);
+        }
         theta = block_reduce<double>(mn, red_d, false);
     }
     const double cut = theta - 1.0;
     if (threadIdx.x == 0) s_m = 0;
     __syncthreads();
-    // count first, so an oversized band is detected before anything is written
-    int mine = 0;
-    for (int j = threadIdx.x; j < t0; j += blockDim.x) mine += ub[j] > cut;
-    if (mine) atomicAdd(&s_m, mine);
+    // one pass: warp-aggregated slots, stores only below the cap (an oversized
+    // band is reported after the pass; the order is irrelevant, bz is sorted next)
+    const int lane = threadIdx.x & 31;
+    for (int j0 = 0; j0 < t0; j0 += 4 * blockDim.x) {
+        double xv[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int j = j0 + q * blockDim.x + threadIdx.x;
+            xv[q] = j < t0 ? ub[j] : -CUDART_INF;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const double x = xv[q];
+            const bool p = x > cut;
+            const unsigned m = __ballot_sync(0xffffffffu, p);
+            int base = 0;
+            if (lane == 0 && m) base = atomicAdd(&s_m, __popc(m));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            const int slot = base + __popc(m & ((1u << lane) - 1u));
+            if (p && slot < cap) bz[slot] = x;
+        }
+    }
     __syncthreads();
     const int mcount = s_m;
     __syncthreads();
     if (mcount > cap) return -1;
-    if (threadIdx.x == 0) s_m = 0;
-    __syncthreads();
-    for (int j = threadIdx.x; j < t0; j += blockDim.x) {
-        const double x = ub[j];
-        if (x > cut) bz[atomicAdd(&s_m, 1)] = x;
-    }
     int n2 = 1;
     while (n2 < mcount) n2 <<= 1;
     __syncthreads();
