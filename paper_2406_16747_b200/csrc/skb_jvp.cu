@@ -31,13 +31,16 @@ k_mean_prefix(const double* __restrict__ rowsum, const int* __restrict__ nfrac,
     double* Mb = M + (int64_t)b * (L + 1);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     double carry = 0.0;
+    auto mean_at = [&](int t) {
+        if (t >= T) return 0.0;
+        const int n = nf[t];
+        return (n > 0 && tb[t] > -INFINITY) ? rs[t] / (double)n : 0.0;
+    };
+    double xn = mean_at(threadIdx.x);  // chunk c + 1 is loaded while chunk c scans
     for (int c0 = 0; c0 < T; c0 += 1024) {
         const int t = c0 + threadIdx.x;
-        double x = 0.0;
-        if (t < T) {
-            const int n = nf[t];
-            x = (n > 0 && tb[t] > -INFINITY) ? rs[t] / (double)n : 0.0;
-        }
+        const double x = xn;
+        xn = mean_at(t + 1024);
         double incl = x;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {

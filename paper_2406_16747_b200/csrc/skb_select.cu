@@ -801,7 +801,13 @@ __global__ void __launch_bounds__(1024) k_tau_monotone(double* tau, int L, int T
     const int per = (T + blockDim.x - 1) / blockDim.x;
     const int lo = min(T, (int)threadIdx.x * per), hi = min(T, lo + per);
     double m = -CUDART_INF;
-    for (int i = lo; i < hi; ++i) m = fmax(m, tb[i]);
+    for (int i0 = lo; i0 < hi; i0 += 8) {  // 8 independent loads in flight
+        double x[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) x[q] = i0 + q < hi ? tb[i0 + q] : -CUDART_INF;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) m = fmax(m, x[q]);
+    }
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     double incl = m;
 #pragma unroll
@@ -816,9 +822,15 @@ __global__ void __launch_bounds__(1024) k_tau_monotone(double* tau, int L, int T
     double excl = __shfl_up_sync(0xffffffffu, incl, 1);
     if (lane == 0) excl = -CUDART_INF;
     double run = fmax(pre, excl);
-    for (int i = lo; i < hi; ++i) {
-        run = fmax(run, tb[i]);
-        tb[i] = run;
+    for (int i0 = lo; i0 < hi; i0 += 8) {
+        double x[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) x[q] = i0 + q < hi ? tb[i0 + q] : -CUDART_INF;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            run = fmax(run, x[q]);
+            if (i0 + q < hi) tb[i0 + q] = run;
+        }
     }
 }
 
