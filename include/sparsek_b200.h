@@ -182,6 +182,17 @@ int skb_cache_prefill(skb_cache* c, const void* k, const void* v, const double* 
                       void* stream);
 /* Host-visible state for tests/inspection: retained positions (ascending
  * selected then window), count, tau, positions seen, peak retained. */
+/* SparseKvCache<T>::serialize / deserialize (proj/src/cache.cpp:416-545) of
+ * sequence b: the reference's snapshot payload (without the "SPKC" file header
+ * of save_cache_snapshot, :579-618). norm_state = the TimestepNormState
+ * {count, mean, m2} of the caller's scoring (the cache works at the q/k/v/u
+ * level; null on snapshot = a fresh state). Snapshot with out == NULL returns
+ * the size in *bytes. Restore overwrites sequence b of a cache of the same
+ * configuration and returns the norm state. */
+int skb_cache_snapshot(skb_cache* c, int64_t b, const double* norm_state, uint8_t* out, size_t* bytes,
+                       void* stream);
+int skb_cache_restore(skb_cache* c, int64_t b, const uint8_t* data, size_t bytes, double* norm_state,
+                      void* stream);
 int skb_cache_state(skb_cache* c, int64_t b, int32_t* positions, int64_t* count, double* tau,
                     int64_t* seen, int64_t* peak, void* stream);
 

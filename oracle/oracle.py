@@ -378,6 +378,34 @@ class Reference:
                                          C.byref(peak)))
         return y, int(peak.value)
 
+    def cache_blob(self, x, wq, wk, wv, wo, w_score, cfg, prompt, use_float=False):
+        """Run rows of x (forward_chunk on the prompt, generate_step after) and
+        return (y, SparseKvCache::serialize payload)."""
+        x, wq, wk, wv, wo = (np.ascontiguousarray(a, np.float64) for a in (x, wq, wk, wv, wo))
+        w_score = np.ascontiguousarray(w_score, np.float64)
+        n, D = x.shape
+        y = np.zeros((n, D))
+        used = C.c_uint64()
+        args = lambda buf, cap: (C.c_int32(int(use_float)), C.c_uint64(n), C.c_uint64(D), C.c_uint64(prompt),
+                                 _d(x), _d(wq), _d(wk), _d(wv), _d(wo), _d(w_score), C.byref(cfg), _d(y),
+                                 buf, C.c_uint64(cap), C.byref(used))
+        self._rc(self.lib.ref_cache_blob(*args(None, 0)))
+        buf = (C.c_uint8 * used.value)()
+        self._rc(self.lib.ref_cache_blob(*args(buf, used.value)))
+        return y, bytes(buf)
+
+    def cache_resume(self, blob, x, wq, wk, wv, wo, w_score, cfg, use_float=False):
+        """SparseKvCache::deserialize(blob) then generate_step over the rows of x."""
+        x, wq, wk, wv, wo = (np.ascontiguousarray(a, np.float64) for a in (x, wq, wk, wv, wo))
+        w_score = np.ascontiguousarray(w_score, np.float64)
+        n, D = x.shape
+        y = np.zeros((n, D))
+        buf = (C.c_uint8 * len(blob)).from_buffer_copy(blob)
+        self._rc(self.lib.ref_cache_resume(C.c_int32(int(use_float)), buf, C.c_uint64(len(blob)),
+                                           C.c_uint64(n), C.c_uint64(D), _d(x), _d(wq), _d(wk), _d(wv),
+                                           _d(wo), _d(w_score), C.byref(cfg), _d(y)))
+        return y
+
     def bench_units(self, units, threads, L, p, k, window, seed=1, with_bwd=True):
         secs = C.c_double()
         self._rc(self.lib.ref_bench_units(C.c_uint64(units), C.c_uint64(threads), C.c_uint64(L),

@@ -382,6 +382,59 @@ int ref_decode_run(int32_t use_float, uint64_t L, uint64_t D, uint64_t prompt, c
     REF_GUARD_END
 }
 
+// Cache snapshots (SparseKvCache::serialize / deserialize, proj/src/cache.cpp:416-545):
+// run rows [0, n) (forward_chunk on [0, prompt), then generate_step), write y
+// rows [0, n) and the snapshot payload.
+int ref_cache_blob(int32_t use_float, uint64_t n, uint64_t D, uint64_t prompt, const double* x,
+                   const double* wq, const double* wk, const double* wv, const double* wo,
+                   const double* w_score, const ref_cfg* c, double* y, uint8_t* out, uint64_t cap,
+                   uint64_t* used) {
+    REF_GUARD_BEGIN
+    auto run = [&](auto tag) {
+        using T = decltype(tag);
+        AttnParams<T> params{mat_in<T>(wq, D, D), mat_in<T>(wk, D, D), mat_in<T>(wv, D, D),
+                             mat_in<T>(wo, D, D)};
+        SparseKvCache<T> cache(to_cfg(c), D, to_scoring(c, w_score, D));
+        if (prompt > 0) mat_out(cache.forward_chunk(mat_in<T>(x, prompt, D), params), y);
+        for (uint64_t i = prompt; i < n; ++i) {
+            std::vector<T> row(D);
+            for (size_t cc = 0; cc < D; ++cc) row[cc] = static_cast<T>(x[i * D + cc]);
+            std::vector<T> o = generate_step(cache, row, params);
+            for (size_t cc = 0; cc < D; ++cc) y[i * D + cc] = static_cast<double>(o[cc]);
+        }
+        std::vector<uint8_t> blob;
+        cache.serialize(blob);
+        *used = blob.size();
+        if (out && cap >= blob.size()) std::memcpy(out, blob.data(), blob.size());
+    };
+    if (use_float) run(float{});
+    else run(double{});
+    REF_GUARD_END
+}
+
+// deserialize a payload and generate_step rows [0, n) of x; y receives their outputs
+int ref_cache_resume(int32_t use_float, const uint8_t* blob, uint64_t len, uint64_t n, uint64_t D,
+                     const double* x, const double* wq, const double* wk, const double* wv,
+                     const double* wo, const double* w_score, const ref_cfg* c, double* y) {
+    REF_GUARD_BEGIN
+    auto run = [&](auto tag) {
+        using T = decltype(tag);
+        AttnParams<T> params{mat_in<T>(wq, D, D), mat_in<T>(wk, D, D), mat_in<T>(wv, D, D),
+                             mat_in<T>(wo, D, D)};
+        SparseKvCache<T> cache =
+            SparseKvCache<T>::deserialize(blob, len, to_cfg(c), D, to_scoring(c, w_score, D));
+        for (uint64_t i = 0; i < n; ++i) {
+            std::vector<T> row(D);
+            for (size_t cc = 0; cc < D; ++cc) row[cc] = static_cast<T>(x[i * D + cc]);
+            std::vector<T> o = generate_step(cache, row, params);
+            for (size_t cc = 0; cc < D; ++cc) y[i * D + cc] = static_cast<double>(o[cc]);
+        }
+    };
+    if (use_float) run(float{});
+    else run(double{});
+    REF_GUARD_END
+}
+
 // CPU baseline: `units` independent single-head sequences (heads=1, D=p) of
 // length L, fwd (with tape) + bwd in float, one std::thread per unit with at
 // most `threads` in flight, the way the reference trainer fans out batch

@@ -257,6 +257,18 @@ class DecodeSession:
         self.t = n
         return hc.reshape(B, n, D) @ self.wo
 
+    def snapshot(self, b=0):
+        """The reference's cache snapshot payload of sequence b (cache, stream,
+        TimestepNormState): SparseKvCache::serialize, proj/src/cache.cpp:416-475."""
+        st = self.state[b].tolist()
+        return self.cache.snapshot(b, norm_state=st)
+
+    def restore(self, blob, b=0):
+        """Resume sequence b from a snapshot payload (ours or the reference's)."""
+        ns = self.cache.restore(blob, b)
+        self.state[b] = torch.tensor(ns, dtype=torch.float64, device=self.state.device)
+        self.t = max(self.t, int(self.cache.state(b)["seen"]))
+
     @torch.no_grad()
     def step(self, x_row):
         """generate_step: x_row [B, D] -> y [B, D]."""
@@ -265,6 +277,36 @@ class DecodeSession:
                             u[:, 0].contiguous())
         self.t += 1
         return o.reshape(self.B, self.D) @ self.wo
+
+
+def save_cache_snapshot(path, payload):
+    """save_cache_snapshot's file format (proj/src/cache.cpp:579-595): "SPKC",
+    u16 version 1, u64 payload length (little endian), payload."""
+    import struct
+
+    with open(path, "wb") as f:
+        f.write(b"SPKC" + struct.pack("<HQ", 1, len(payload)) + payload)
+
+
+def load_cache_snapshot(path):
+    """The payload of a save_cache_snapshot file (proj/src/cache.cpp:597-618)."""
+    import struct
+
+    from ._lib import IoError
+
+    with open(path, "rb") as f:
+        head = f.read(14)
+        if len(head) < 4 or head[:4] != b"SPKC":
+            raise IoError(f"not a cache snapshot: {path}")
+        if len(head) < 14:
+            raise IoError("cache snapshot: truncated header")
+        ver, n = struct.unpack("<HQ", head[4:])
+        if ver != 1:
+            raise IoError("cache snapshot: unsupported version")
+        payload = f.read(n)
+        if len(payload) != n:
+            raise IoError("cache snapshot: truncated payload")
+        return payload
 
 
 def dense_attention(x, wq, wk, wv, wo, heads=1):

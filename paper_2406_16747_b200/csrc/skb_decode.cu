@@ -251,6 +251,7 @@ struct CacheArgs {
     double* fv;         // [B, Lmax] saturated
     int* fi;
     double* u_hist;     // [B, Lmax] frozen scores
+    uint8_t* ins_hist;  // [B, Lmax] the exit push of each position inserted it (z > tau); snapshots
     int* slot_of;       // [B, Lmax] position -> slot (-1 = dropped)
     int* pos_of;        // [B, S]    slot -> position (-1 = free)
     int* free_stack;    // [B, S]
@@ -315,6 +316,7 @@ __device__ void warp_cache_advance(const CacheArgs& A, int b, CacheCtl& c, doubl
             const int nS_before = c.st.nS;
             int rank;
             const bool ins = warp_stream_push(c.st, sa, ue, &rank);
+            if (lane == 0) A.ins_hist[bL + e] = ins ? 1 : 0;
             if (ins && rank >= 0 && rank < A.cap) {
                 admitted = true;
                 // the previous rank floor(k)-1 entry is pushed out of the top floor(k)
@@ -324,7 +326,8 @@ __device__ void warp_cache_advance(const CacheArgs& A, int b, CacheCtl& c, doubl
             }
         } else if (c.st.k > 0.0) {
             int rank;
-            warp_stream_push(c.st, sa, ue, &rank);  // tau still advances (floor(k) = 0)
+            const bool ins = warp_stream_push(c.st, sa, ue, &rank);  // tau still advances (floor(k) = 0)
+            if (lane == 0) A.ins_hist[bL + e] = ins ? 1 : 0;
         }
         if (!admitted) freed[0] = e;
     }
@@ -766,9 +769,22 @@ struct skb_stream {
     int64_t capacity = 0;
 };
 
+// Host-side state of a SparseKvCache snapshot that the device arrays do not
+// hold: the cache min-heap in the reference's array order, the evicted bitmap
+// and the pending-eviction list (proj/src/cache.cpp:115-179). Replayed from
+// the recorded exit pushes (ins_hist) starting at `t0` (0, or a restore point).
+struct SnapBase {
+    long long t0 = 0;
+    std::vector<std::pair<double, long long>> heap;  // (score, pos)
+    std::vector<long long> cache_pos;                // ascending
+    std::vector<uint8_t> evicted;
+    std::vector<long long> pending;
+};
+
 struct skb_cache {
     skb_attn_desc d{};
     CacheArgs A{};
+    std::vector<SnapBase> base;
     int nsplit = 0;
     int vec = 1;
     double* po = nullptr;  // split partials: float64 for float64 pools, else float32
@@ -1089,6 +1105,8 @@ int skb_cache_create(const skb_attn_desc* d, skb_cache** out) {
         A.fi = c->alloc<int>(B * Lmax);
         A.u_hist = c->alloc<double>(B * Lmax);
         A.slot_of = c->alloc<int>(B * Lmax);
+        A.ins_hist = c->alloc<uint8_t>(B * Lmax);
+        c->base.assign((size_t)B, SnapBase{});
         A.pos_of = c->alloc<int>(B * S);
         A.free_stack = c->alloc<int>(B * S);
         A.att_slot = c->alloc<int>(B * S);
@@ -1240,6 +1258,406 @@ int skb_cache_state(skb_cache* c, int64_t b, int32_t* positions, int64_t* count,
     if (tau) *tau = cc.st.tau;
     if (seen) *seen = cc.t;
     if (peak) *peak = cc.peak;
+    K5_END
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------ snapshots
+namespace {
+
+// the reference's cache heap order (SlotCmp, proj/src/cache.cpp:55-60):
+// std heaps with this comparator keep the lowest (score, then latest pos) in front
+struct SnapSlotCmp {
+    bool operator()(const std::pair<double, long long>& a, const std::pair<double, long long>& b) const {
+        return a.first > b.first || (a.first == b.first && a.second < b.second);
+    }
+};
+
+struct Bytes {
+    std::vector<uint8_t> v;
+    void raw(const void* p, size_t n) {
+        const uint8_t* q = static_cast<const uint8_t*>(p);
+        v.insert(v.end(), q, q + n);
+    }
+    void u64(uint64_t x) { raw(&x, 8); }
+    void f64(double x) { raw(&x, 8); }
+    void u8(uint8_t x) { v.push_back(x); }
+};
+
+struct Reader {
+    const uint8_t* p;
+    size_t n, off = 0;
+    void raw(void* dst, size_t k) {
+        SKB_REQUIRE(off + k <= n, SKB_EIO, "cache snapshot: truncated");
+        std::memcpy(dst, p + off, k);
+        off += k;
+    }
+    uint64_t u64() {
+        uint64_t x;
+        raw(&x, 8);
+        return x;
+    }
+    double f64() {
+        double x;
+        raw(&x, 8);
+        return x;
+    }
+    uint8_t u8() {
+        uint8_t x;
+        raw(&x, 1);
+        return x;
+    }
+};
+
+void evict_mark(SnapBase& sb, long long pos) {  // drop_kv (proj/src/cache.cpp:115-125)
+    if ((long long)sb.evicted.size() <= pos) sb.evicted.resize((size_t)pos + 1, 0);
+    sb.evicted[(size_t)pos] = 1;
+    sb.pending.push_back(pos);
+}
+
+// exit_window + admit_to_cache (proj/src/cache.cpp:136-179) for one departing position
+void replay_exit(SnapBase& sb, long long e, double score, bool has_stream, bool inserted, size_t cap) {
+    if (!has_stream || !inserted || cap == 0) {
+        evict_mark(sb, e);
+        return;
+    }
+    if (sb.heap.size() < cap) {
+        sb.heap.push_back({score, e});
+        std::push_heap(sb.heap.begin(), sb.heap.end(), SnapSlotCmp{});
+        sb.cache_pos.push_back(e);
+        return;
+    }
+    const auto worst = sb.heap.front();
+    if (score < worst.first || score == worst.first) {
+        evict_mark(sb, e);
+        return;
+    }
+    std::pop_heap(sb.heap.begin(), sb.heap.end(), SnapSlotCmp{});
+    sb.heap.back() = {score, e};
+    std::push_heap(sb.heap.begin(), sb.heap.end(), SnapSlotCmp{});
+    evict_mark(sb, worst.second);
+    sb.cache_pos.erase(std::lower_bound(sb.cache_pos.begin(), sb.cache_pos.end(), worst.second));
+    sb.cache_pos.push_back(e);
+}
+
+double to_f64(const uint8_t* p, int dt) {
+    if (dt == SKB_F64) {
+        double x;
+        std::memcpy(&x, p, 8);
+        return x;
+    }
+    if (dt == SKB_F32) {
+        float x;
+        std::memcpy(&x, p, 4);
+        return (double)x;
+    }
+    uint16_t h;
+    std::memcpy(&h, p, 2);
+    const uint32_t w = (uint32_t)h << 16;
+    float x;
+    std::memcpy(&x, &w, 4);
+    return (double)x;
+}
+
+void from_f64(double x, uint8_t* p, int dt) {
+    if (dt == SKB_F64) {
+        std::memcpy(p, &x, 8);
+    } else if (dt == SKB_F32) {
+        const float f = (float)x;
+        std::memcpy(p, &f, 4);
+    } else {
+        const __nv_bfloat16 h = __double2bfloat16(x);
+        std::memcpy(p, &h, 2);
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+// SparseKvCache<T>::serialize (proj/src/cache.cpp:416-475) of sequence b; the
+// reference's TimestepNormState {count, mean, m2} comes from the caller (the
+// cache works at the q/k/v/u level; null = a fresh state).
+int skb_cache_snapshot(skb_cache* c, int64_t b, const double* norm_state, uint8_t* out, size_t* bytes,
+                       void* stream) {
+    K5_BEGIN
+    SKB_REQUIRE(c != nullptr && bytes != nullptr, SKB_EARG, "cache_snapshot: null argument");
+    SKB_REQUIRE(b >= 0 && b < c->d.batch, SKB_EARG, "cache_snapshot: sequence out of range");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const CacheArgs& A = c->A;
+    const int dt = (int)c->d.dtype;
+    const int64_t bL = b * A.Lmax, bS = b * A.S;
+    CacheCtl cc;
+    SKB_CHECK_CUDA(cudaMemcpyAsync(&cc, A.ctl + b, sizeof(cc), cudaMemcpyDeviceToHost, st));
+    SKB_CHECK_CUDA(cudaStreamSynchronize(st));
+    SKB_REQUIRE(cc.error == 0, SKB_ESHAPE, "cache_snapshot: the cache is in an error state");
+    const long long t = cc.t;
+    std::vector<double> u(t), sv(cc.st.nS), fv(cc.st.nF);
+    std::vector<uint8_t> ins(t);
+    std::vector<int> si(cc.st.nS), fi(cc.st.nF), slot_of(t);
+    if (t) {
+        SKB_CHECK_CUDA(cudaMemcpyAsync(u.data(), A.u_hist + bL, t * 8, cudaMemcpyDeviceToHost, st));
+        SKB_CHECK_CUDA(cudaMemcpyAsync(ins.data(), A.ins_hist + bL, t, cudaMemcpyDeviceToHost, st));
+        SKB_CHECK_CUDA(cudaMemcpyAsync(slot_of.data(), A.slot_of + bL, t * 4, cudaMemcpyDeviceToHost, st));
+    }
+    if (cc.st.nS) {
+        SKB_CHECK_CUDA(cudaMemcpyAsync(sv.data(), A.sv + bL, cc.st.nS * 8, cudaMemcpyDeviceToHost, st));
+        SKB_CHECK_CUDA(cudaMemcpyAsync(si.data(), A.si + bL, cc.st.nS * 4, cudaMemcpyDeviceToHost, st));
+    }
+    if (cc.st.nF) {
+        SKB_CHECK_CUDA(cudaMemcpyAsync(fv.data(), A.fv + bL, cc.st.nF * 8, cudaMemcpyDeviceToHost, st));
+        SKB_CHECK_CUDA(cudaMemcpyAsync(fi.data(), A.fi + bL, cc.st.nF * 4, cudaMemcpyDeviceToHost, st));
+    }
+    std::vector<uint8_t> kp((size_t)A.S * A.row_bytes), vp((size_t)A.S * A.row_bytes);
+    SKB_CHECK_CUDA(cudaMemcpyAsync(kp.data(), A.kpool + bS * A.row_bytes, kp.size(), cudaMemcpyDeviceToHost, st));
+    SKB_CHECK_CUDA(cudaMemcpyAsync(vp.data(), A.vpool + bS * A.row_bytes, vp.size(), cudaMemcpyDeviceToHost, st));
+    SKB_CHECK_CUDA(cudaStreamSynchronize(st));
+
+    const bool has_stream = c->d.k > 0.0;
+    const size_t cap = (size_t)A.cap;
+    const long long w = A.w;
+    SnapBase sb = c->base[(size_t)b];  // replay the exits since the base point
+    for (long long e = std::max(0LL, sb.t0 - w); e < std::max(0LL, t - w); ++e)
+        replay_exit(sb, e, u[(size_t)e], has_stream, ins[(size_t)e] != 0, cap);
+    const long long d_model = c->d.heads * c->d.head_dim;
+    Bytes o;
+    o.u64((uint64_t)d_model);
+    o.u64((uint64_t)c->d.heads);
+    o.u64((uint64_t)w);
+    o.u64((uint64_t)cap);
+    o.f64(c->d.k);
+    o.u8(0);  // linear mix: not on the B200 path
+    o.u8(has_stream ? 1 : 0);
+    o.u64((uint64_t)t);
+    o.u64((uint64_t)t);
+    for (long long i = 0; i < t; ++i) o.f64(u[(size_t)i]);
+    o.u64(norm_state ? (uint64_t)norm_state[0] : 0);
+    o.f64(norm_state ? norm_state[1] : 0.0);
+    o.f64(norm_state ? norm_state[2] : 0.0);
+    o.f64(1e-5);  // TimestepNormState::eps (proj/include/sparsek/selection.hpp:35)
+    if (has_stream) {  // StreamState::serialize (proj/src/stream.cpp:224-252)
+        Bytes sbl;
+        const long long pushes = cc.st.t;
+        sbl.f64(cc.st.k);
+        sbl.u64((uint64_t)cc.st.heap_cap);
+        sbl.f64(cc.st.tau);
+        sbl.u64((uint64_t)pushes);
+        sbl.f64(cc.st.sum_s);
+        sbl.f64(cc.st.sum_f);
+        sbl.u64(cc.st.cap_drops);
+        sbl.u64(cc.st.heap_ops);
+        sbl.u64((uint64_t)cc.st.since_refresh);
+        auto heap = [&](const std::vector<double>& v, const std::vector<int>& ix) {
+            sbl.u64(v.size());
+            for (size_t r2 = v.size(); r2-- > 0;) {  // (value asc, index desc): a valid heap
+                sbl.f64(v[r2]);
+                sbl.u64((uint64_t)ix[r2]);
+            }
+        };
+        heap(sv, si);
+        heap(fv, fi);
+        // evicted = every push not in the survivor set (rejected at entry or popped)
+        std::vector<uint8_t> ev((size_t)pushes, 1);
+        for (int x : si)
+            if (x >= 0 && x < pushes) ev[(size_t)x] = 0;
+        sbl.u64((uint64_t)pushes);
+        for (long long i = 0; i < pushes; i += 8) {
+            uint8_t byte = 0;
+            for (int q = 0; q < 8 && i + q < pushes; ++q)
+                if (ev[(size_t)(i + q)]) byte |= (uint8_t)(1u << q);
+            sbl.u8(byte);
+        }
+        o.u64(sbl.v.size());
+        o.raw(sbl.v.data(), sbl.v.size());
+    }
+    const long long r0 = std::max(0LL, t - w);  // the window ring, oldest first
+    o.u64((uint64_t)(t - r0));
+    for (long long ppos = r0; ppos < t; ++ppos) o.u64((uint64_t)ppos);
+    o.u64(sb.heap.size());
+    for (const auto& hs : sb.heap) {
+        o.f64(hs.first);
+        o.u64((uint64_t)hs.second);
+    }
+    o.u64(sb.cache_pos.size());
+    for (long long cp : sb.cache_pos) o.u64((uint64_t)cp);
+    o.u64((uint64_t)((t - r0) + (long long)sb.cache_pos.size()));
+    const size_t es = dt == SKB_F64 ? 8 : dt == SKB_F32 ? 4 : 2;
+    auto put_kv = [&](long long ppos) {
+        const int slot = slot_of[(size_t)ppos];
+        SKB_REQUIRE(slot >= 0 && slot < A.S, SKB_ENUMERIC, "cache_snapshot: retained position without a row");
+        o.u64((uint64_t)ppos);
+        for (long long x = 0; x < d_model; ++x) o.f64(to_f64(kp.data() + (size_t)slot * A.row_bytes + x * es, dt));
+        for (long long x = 0; x < d_model; ++x) o.f64(to_f64(vp.data() + (size_t)slot * A.row_bytes + x * es, dt));
+    };
+    for (long long ppos = r0; ppos < t; ++ppos) put_kv(ppos);
+    for (long long cp : sb.cache_pos) put_kv(cp);
+    o.u64(sb.evicted.size());
+    for (size_t i = 0; i < sb.evicted.size(); i += 8) {
+        uint8_t byte = 0;
+        for (size_t q = 0; q < 8 && i + q < sb.evicted.size(); ++q)
+            if (sb.evicted[i + q]) byte |= (uint8_t)(1u << q);
+        o.u8(byte);
+    }
+    o.u64(sb.pending.size());
+    for (long long pe : sb.pending) o.u64((uint64_t)pe);
+    o.u64((uint64_t)cc.peak);
+    if (!out) {
+        *bytes = o.v.size();
+        return SKB_OK;
+    }
+    SKB_REQUIRE(*bytes >= o.v.size(), SKB_EARG, "cache_snapshot: buffer too small");
+    std::memcpy(out, o.v.data(), o.v.size());
+    *bytes = o.v.size();
+    K5_END
+}
+
+// SparseKvCache<T>::deserialize (proj/src/cache.cpp:477-545) into sequence b of
+// an existing cache of the same configuration; norm_state receives the
+// TimestepNormState {count, mean, m2} for the caller's scoring.
+int skb_cache_restore(skb_cache* c, int64_t b, const uint8_t* data, size_t bytes, double* norm_state,
+                      void* stream) {
+    K5_BEGIN
+    SKB_REQUIRE(c != nullptr && data != nullptr, SKB_EARG, "cache_restore: null argument");
+    SKB_REQUIRE(b >= 0 && b < c->d.batch, SKB_EARG, "cache_restore: sequence out of range");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const CacheArgs& A = c->A;
+    const int dt = (int)c->d.dtype;
+    const int64_t bL = b * A.Lmax, bS = b * A.S;
+    const long long d_model = c->d.heads * c->d.head_dim;
+    const bool has_stream_cfg = c->d.k > 0.0;
+    Reader r{data, bytes};
+    if (r.u64() != (uint64_t)d_model || r.u64() != (uint64_t)c->d.heads || r.u64() != (uint64_t)A.w ||
+        r.u64() != (uint64_t)A.cap)
+        throw skb::Error(SKB_EIO, "cache snapshot: configuration mismatch");
+    if (r.f64() != c->d.k) throw skb::Error(SKB_EIO, "cache snapshot: budget mismatch");
+    if (r.u8() != 0) throw skb::Error(SKB_EIO, "cache snapshot: mode mismatch");
+    const bool has_stream = r.u8() != 0;
+    if (has_stream != has_stream_cfg) throw skb::Error(SKB_EIO, "cache snapshot: stream mismatch");
+    const long long t = (long long)r.u64();
+    SKB_REQUIRE(t <= A.Lmax, SKB_ESHAPE, "cache_restore: snapshot longer than the cache's max positions");
+    const uint64_t ns = r.u64();
+    SKB_REQUIRE(ns == (uint64_t)t, SKB_EIO, "cache snapshot: score count != positions");
+    std::vector<double> u((size_t)t);
+    for (auto& x : u) x = r.f64();
+    double norm[3];
+    norm[0] = (double)r.u64();
+    norm[1] = r.f64();
+    norm[2] = r.f64();
+    (void)r.f64();  // eps
+    CacheCtl cc{};
+    std::vector<std::pair<double, long long>> hs, hf;
+    std::vector<uint8_t> sev;
+    cc.st.k = c->d.k;
+    cc.st.tau = -INFINITY;
+    cc.st.cap = A.Lmax;
+    if (has_stream) {
+        const uint64_t blen = r.u64();
+        const size_t end = r.off + blen;
+        cc.st.k = r.f64();
+        cc.st.heap_cap = (long long)r.u64();
+        cc.st.tau = r.f64();
+        cc.st.t = (long long)r.u64();
+        cc.st.sum_s = r.f64();
+        cc.st.sum_f = r.f64();
+        cc.st.cap_drops = r.u64();
+        cc.st.heap_ops = r.u64();
+        cc.st.since_refresh = (int)r.u64();
+        auto heap = [&](std::vector<std::pair<double, long long>>& h) {
+            const uint64_t n = r.u64();
+            SKB_REQUIRE(n <= bytes / 16, SKB_EIO, "cache snapshot: truncated");
+            h.resize(n);
+            for (auto& e : h) {
+                e.first = r.f64();
+                e.second = (long long)r.u64();
+            }
+            std::sort(h.begin(), h.end(), [](const auto& a, const auto& b2) {  // device: (value desc, index asc)
+                return a.first > b2.first || (a.first == b2.first && a.second < b2.second);
+            });
+        };
+        heap(hs);
+        heap(hf);
+        const uint64_t nb = r.u64();
+        for (uint64_t i = 0; i < nb; i += 8) (void)r.u8();
+        SKB_REQUIRE(r.off == end, SKB_EIO, "cache snapshot: stream blob length mismatch");
+        cc.st.nS = (int)hs.size();
+        cc.st.nF = (int)hf.size();
+    }
+    std::vector<long long> ring(r.u64());
+    for (auto& x : ring) x = (long long)r.u64();
+    SnapBase sb;
+    sb.t0 = t;
+    sb.heap.resize(r.u64());
+    for (auto& e : sb.heap) {
+        e.first = r.f64();
+        e.second = (long long)r.u64();
+    }
+    sb.cache_pos.resize(r.u64());
+    for (auto& x : sb.cache_pos) x = (long long)r.u64();
+    const uint64_t nkv = r.u64();
+    SKB_REQUIRE(nkv == ring.size() + sb.cache_pos.size() && nkv <= (uint64_t)A.S, SKB_EIO,
+                "cache snapshot: row count does not match the retained positions");
+    const size_t es = dt == SKB_F64 ? 8 : dt == SKB_F32 ? 4 : 2;
+    std::vector<uint8_t> kp((size_t)A.S * A.row_bytes, 0), vp((size_t)A.S * A.row_bytes, 0);
+    std::vector<int> slot_of((size_t)std::max<long long>(t, 1), -1), pos_of((size_t)A.S, -1);
+    for (uint64_t i = 0; i < nkv; ++i) {
+        const long long ppos = (long long)r.u64();
+        SKB_REQUIRE(ppos >= 0 && ppos < t, SKB_EIO, "cache snapshot: row position out of range");
+        for (long long x = 0; x < d_model; ++x) from_f64(r.f64(), kp.data() + i * A.row_bytes + x * es, dt);
+        for (long long x = 0; x < d_model; ++x) from_f64(r.f64(), vp.data() + i * A.row_bytes + x * es, dt);
+        slot_of[(size_t)ppos] = (int)i;
+        pos_of[i] = (int)ppos;
+    }
+    const uint64_t nbits = r.u64();
+    sb.evicted.assign(nbits, 0);
+    for (uint64_t i = 0; i < nbits; i += 8) {
+        const uint8_t byte = r.u8();
+        for (uint64_t q = 0; q < 8 && i + q < nbits; ++q) sb.evicted[i + q] = (byte >> q) & 1u;
+    }
+    sb.pending.resize(r.u64());
+    for (auto& x : sb.pending) x = (long long)r.u64();
+    cc.peak = (long long)r.u64();
+    SKB_REQUIRE(r.off == bytes, SKB_EIO, "cache snapshot: trailing bytes");
+    SKB_REQUIRE((long long)ring.size() == t - std::max(0LL, t - (long long)A.w), SKB_EIO,
+                "cache snapshot: window ring does not hold the last w positions");
+    for (size_t i = 0; i < ring.size(); ++i)
+        SKB_REQUIRE(ring[i] == t - (long long)ring.size() + (long long)i, SKB_EIO,
+                    "cache snapshot: window ring does not hold the last w positions");
+    // the retained cache positions must be the stream's top floor(k) survivors
+    SKB_REQUIRE(sb.cache_pos.size() <= (size_t)A.cap, SKB_EIO, "cache snapshot: cache larger than floor(k)");
+    cc.t = t;
+    cc.nsel = (int)sb.cache_pos.size();
+    cc.free_top = A.S - (int)nkv;
+    std::vector<int> free_stack((size_t)A.S);
+    for (int i = 0; i < cc.free_top; ++i) free_stack[(size_t)i] = A.S - 1 - i;  // the unused slots
+    // device upload
+    std::vector<double> sv(hs.size()), fv(hf.size());
+    std::vector<int> si(hs.size()), fi(hf.size());
+    for (size_t i = 0; i < hs.size(); ++i) sv[i] = hs[i].first, si[i] = (int)hs[i].second;
+    for (size_t i = 0; i < hf.size(); ++i) fv[i] = hf[i].first, fi[i] = (int)hf[i].second;
+    std::vector<uint8_t> ins((size_t)std::max<long long>(t, 1), 0);
+    SKB_CHECK_CUDA(cudaStreamSynchronize(st));
+    if (t) {
+        SKB_CHECK_CUDA(cudaMemcpy(A.u_hist + bL, u.data(), t * 8, cudaMemcpyHostToDevice));
+        SKB_CHECK_CUDA(cudaMemcpy(A.slot_of + bL, slot_of.data(), t * 4, cudaMemcpyHostToDevice));
+        SKB_CHECK_CUDA(cudaMemcpy(A.ins_hist + bL, ins.data(), t, cudaMemcpyHostToDevice));
+    }
+    if (!sv.empty()) {
+        SKB_CHECK_CUDA(cudaMemcpy(A.sv + bL, sv.data(), sv.size() * 8, cudaMemcpyHostToDevice));
+        SKB_CHECK_CUDA(cudaMemcpy(A.si + bL, si.data(), si.size() * 4, cudaMemcpyHostToDevice));
+    }
+    if (!fv.empty()) {
+        SKB_CHECK_CUDA(cudaMemcpy(A.fv + bL, fv.data(), fv.size() * 8, cudaMemcpyHostToDevice));
+        SKB_CHECK_CUDA(cudaMemcpy(A.fi + bL, fi.data(), fi.size() * 4, cudaMemcpyHostToDevice));
+    }
+    SKB_CHECK_CUDA(cudaMemcpy(A.pos_of + bS, pos_of.data(), A.S * 4, cudaMemcpyHostToDevice));
+    SKB_CHECK_CUDA(cudaMemcpy(A.free_stack + bS, free_stack.data(), A.S * 4, cudaMemcpyHostToDevice));
+    SKB_CHECK_CUDA(cudaMemcpy(A.kpool + bS * A.row_bytes, kp.data(), kp.size(), cudaMemcpyHostToDevice));
+    SKB_CHECK_CUDA(cudaMemcpy(A.vpool + bS * A.row_bytes, vp.data(), vp.size(), cudaMemcpyHostToDevice));
+    SKB_CHECK_CUDA(cudaMemcpy(A.ctl + b, &cc, sizeof(cc), cudaMemcpyHostToDevice));
+    c->base[(size_t)b] = std::move(sb);
+    if (norm_state)
+        for (int i = 0; i < 3; ++i) norm_state[i] = norm[i];
     K5_END
 }
 

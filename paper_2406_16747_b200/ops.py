@@ -385,6 +385,28 @@ class DecodeCache:
         check(_lib.load().skb_cache_prefill(self._h, k.data_ptr(), v.data_ptr(), u.data_ptr(), n,
                                             _stream()))
 
+    def snapshot(self, b=0, norm_state=None):
+        """SparseKvCache::serialize payload of sequence b (proj/src/cache.cpp:416-475);
+        norm_state = (count, mean, m2) of the scoring that fed this cache."""
+        import ctypes
+
+        ns = None if norm_state is None else (ctypes.c_double * 3)(*[float(x) for x in norm_state])
+        n = ctypes.c_size_t(0)
+        check(_lib.load().skb_cache_snapshot(self._h, int(b), ns, None, ctypes.byref(n), _stream()))
+        buf = (ctypes.c_uint8 * n.value)()
+        check(_lib.load().skb_cache_snapshot(self._h, int(b), ns, buf, ctypes.byref(n), _stream()))
+        return bytes(buf[: n.value])
+
+    def restore(self, blob, b=0):
+        """SparseKvCache::deserialize (proj/src/cache.cpp:477-545) into sequence b;
+        returns the snapshot's norm state (count, mean, m2)."""
+        import ctypes
+
+        ns = (ctypes.c_double * 3)()
+        buf = (ctypes.c_uint8 * len(blob)).from_buffer_copy(blob)
+        check(_lib.load().skb_cache_restore(self._h, int(b), buf, len(blob), ns, _stream()))
+        return tuple(ns)
+
     def state(self, b=0):
         """{positions (selected asc, then window asc), tau, seen, peak}."""
         import ctypes
