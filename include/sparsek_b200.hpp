@@ -341,6 +341,20 @@ class SparseKvCache {  // cache.hpp:21-87 + generate_step (cache.cpp:570-577)
         return pos;
     }
     size_t capacity() const { return cap_; }
+    // SparseKvCache<T>::serialize / deserialize (cache.cpp:416-545) of sequence b;
+    // norm = the TimestepNormState {count, mean, m2} of the scoring feeding this cache
+    std::vector<uint8_t> serialize(int64_t b, const double* norm = nullptr, cudaStream_t st = nullptr) const {
+        size_t n = 0;
+        check(skb_cache_snapshot(c_, b, norm, nullptr, &n, st));
+        std::vector<uint8_t> out(n);
+        check(skb_cache_snapshot(c_, b, norm, out.data(), &n, st));
+        out.resize(n);
+        return out;
+    }
+    void deserialize(int64_t b, const std::vector<uint8_t>& blob, double* norm_out = nullptr,
+                     cudaStream_t st = nullptr) {
+        check(skb_cache_restore(c_, b, blob.data(), blob.size(), norm_out, st));
+    }
 
   private:
     skb_cache* c_ = nullptr;

@@ -139,6 +139,41 @@ static int gpu_checks() {
         }
         for (int i = 0; i < SB * SN; ++i) EXPECT(ua[i] == ub[i]);
     }
+    // cache snapshot round trip: a restored cache continues bit-identically
+    {
+        const int CL = 64, CH = 2, CP = 32;
+        AttnConfig cc;
+        cc.k = 6.5;
+        cc.window = 5;
+        cc.heads = CH;
+        SparseKvCache a(1, CL, CP, cc, DType::f32), b2(1, CL, CP, cc, DType::f32);
+        std::vector<float> row(CH * CP);
+        DeviceBuffer dq2(row.size() * 4), dk2(row.size() * 4), dv2(row.size() * 4), du2(8), do1(row.size() * 4),
+            do2(row.size() * 4);
+        auto feed = [&](SparseKvCache& c, int i, void* o) {
+            seed = 1234u + 7u * (unsigned)i;
+            for (auto& e : row) e = rnd();
+            cuda_check(cudaMemcpy(dq2.get(), row.data(), row.size() * 4, cudaMemcpyHostToDevice), "H2D");
+            for (auto& e : row) e = rnd();
+            cuda_check(cudaMemcpy(dk2.get(), row.data(), row.size() * 4, cudaMemcpyHostToDevice), "H2D");
+            for (auto& e : row) e = rnd();
+            cuda_check(cudaMemcpy(dv2.get(), row.data(), row.size() * 4, cudaMemcpyHostToDevice), "H2D");
+            const double uu = rnd() + 0.01 * i;
+            cuda_check(cudaMemcpy(du2.get(), &uu, 8, cudaMemcpyHostToDevice), "H2D");
+            c.step(dq2.get(), dk2.get(), dv2.get(), (const double*)du2.get(), o);
+        };
+        for (int i = 0; i < 40; ++i) feed(a, i, do1.get());
+        b2.deserialize(0, a.serialize(0));
+        std::vector<float> o1(row.size()), o2(row.size());
+        for (int i = 40; i < CL; ++i) {
+            feed(a, i, do1.get());
+            feed(b2, i, do2.get());
+            cuda_check(cudaMemcpy(o1.data(), do1.get(), o1.size() * 4, cudaMemcpyDeviceToHost), "D2H");
+            cuda_check(cudaMemcpy(o2.data(), do2.get(), o2.size() * 4, cudaMemcpyDeviceToHost), "D2H");
+            EXPECT(std::memcmp(o1.data(), o2.data(), o1.size() * 4) == 0);
+        }
+        EXPECT(a.serialize(0) == b2.serialize(0));
+    }
     std::printf("gpu ok (dense-limit max err %.3g)\n", maxerr);
     return 0;
 }
