@@ -1399,7 +1399,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(const __grid_constant
             // rows of tile jt of one tensor into dst, completing on bar (97 arrivals)
             auto rows = [&](uint32_t dst, const __nv_bfloat16* src, const CUtensorMap* tm, uint64_t* bar) {
                 if (jt < n_sel) {
-                    kcur.issue<false>(dst, src, b, h, a.L, a.H, pw, lane);
+                    kcur.template issue<false>(dst, src, b, h, a.L, a.H, pw, lane);
                     cp_async_arrive_noinc(bar);
                     if (ptid == 0) mbar_arrive(bar);
                 } else {
@@ -1732,7 +1732,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_p(const __grid_constant_
                 cp_async_arrive_noinc(&bars[QB_MFULL + s]);
                 auto rows = [&](uint32_t dst, const __nv_bfloat16* src, const CUtensorMap* tm, uint64_t* bar) {
                     if (jt < n_sel) {
-                        kcur.issue<false>(dst, src, b, h, a.L, a.H, pw, lane);
+                        kcur.template issue<false>(dst, src, b, h, a.L, a.H, pw, lane);
                         cp_async_arrive_noinc(bar);
                         if (ptid == 0) mbar_arrive(bar);
                     } else {

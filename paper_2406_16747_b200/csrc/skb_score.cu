@@ -64,9 +64,9 @@ __global__ void k_score_welford(const double* __restrict__ raw, int L, skb_scori
 // carried across calls; proj/src/selection.cpp:13-31): n new rows per sequence
 // continue the Welford state [count, mean, m2] exactly as the reference's
 // push does, operation for operation.
-__global__ void k_score_continue(const double* __restrict__ rawv, int n, skb_scoring sc,
-                                 double* __restrict__ state, double* __restrict__ raw_out,
-                                 double* __restrict__ u_out, int* __restrict__ bad) {
+// (rawv and raw_out may alias: the continuation rewrites raw in place)
+__global__ void k_score_continue(const double* rawv, int n, skb_scoring sc, double* __restrict__ state,
+                                 double* raw_out, double* __restrict__ u_out, int* __restrict__ bad) {
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= gridDim.x * blockDim.x) return;
     double* stt = state + (int64_t)b * 3;
@@ -97,8 +97,9 @@ __global__ void k_score_continue(const double* __restrict__ rawv, int n, skb_sco
     stt[2] = m2;
 }
 
-__global__ void k_score_finish(const double* __restrict__ raw_in, int64_t n, int L, skb_scoring sc,
-                               double* __restrict__ raw, double* __restrict__ u,
+// (raw_in and raw may alias: the caller stages the dot products in raw)
+__global__ void k_score_finish(const double* raw_in, int64_t n, int L, skb_scoring sc, double* raw,
+                               double* __restrict__ u,
                                double* __restrict__ mean, double* __restrict__ sdev_var,
                                int* __restrict__ bad) {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;

@@ -166,79 +166,7 @@ k_rank_before(const double* __restrict__ u, int L, int T, int* __restrict__ A) {
     if (cnt) atomicAdd(A + (int64_t)b * L + j, cnt);
 }
 
-__global__ void __launch_bounds__(kRankThreads)
-k_rank_after(const double* __restrict__ u, int L, int T, int R1, int R2, int* __restrict__ leave1,
-             int* __restrict__ leave2) {
-    __shared__ __align__(16) double su[kRankStage];
-    const int b = blockIdx.y;
-    const int j = blockIdx.x * kRankThreads + threadIdx.x;
-    const double* ub = u + (int64_t)b * L;
-    const bool active = j < T;
-    const double uj = active ? ub[j] : 0.0;
-    const int A = active ? leave1[(int64_t)b * L + j] : 0;  // k_rank_before's counts
-    int cnt = 0;
-    const int need1 = R1 - A, need2 = R2 - A;
-    int l1 = T, l2 = T;
-    bool done = !active;
-    if (active && A >= R2) {  // R2 earlier winners: never in the top R2 (nor the top R1)
-        l1 = j;
-        l2 = j;
-        done = true;
-    } else if (active && need1 <= 0) {
-        l1 = j;
-    }
-    const int jmin = blockIdx.x * kRankThreads;  // the block's first key: later scores start after it
-    for (int c0 = (jmin + 1) / 8 * 8; c0 < T; c0 += kRankStage) {
-        if (__syncthreads_and(done)) break;
-        for (int i = threadIdx.x; i < kRankStage; i += kRankThreads) su[i] = c0 + i < T ? ub[c0 + i] : 0.0;
-        __syncthreads();
-        if (done) continue;
-        const int n = min(kRankStage, T - c0);
-        int ii = max(0, j + 1 - c0);
-        if (ii >= n) continue;
-        auto hit = [&](double x, int i) {
-            if (x > uj) {
-                ++cnt;
-                if (cnt == need1) l1 = i;
-                if (cnt == need2) {
-                    l2 = i;
-                    done = true;
-                }
-            }
-        };
-        for (; ii < n && (ii & 7); ++ii) {
-            hit(su[ii], c0 + ii);
-            if (done) break;
-        }
-        if (done) continue;
-        for (; ii + 8 <= n; ii += 8) {
-            const double2 x0 = *reinterpret_cast<const double2*>(su + ii);
-            const double2 x1 = *reinterpret_cast<const double2*>(su + ii + 2);
-            const double2 x2 = *reinterpret_cast<const double2*>(su + ii + 4);
-            const double2 x3 = *reinterpret_cast<const double2*>(su + ii + 6);
-            const int g = (x0.x > uj) + (x0.y > uj) + (x1.x > uj) + (x1.y > uj) + (x2.x > uj) + (x2.y > uj) +
-                          (x3.x > uj) + (x3.y > uj);
-            const int nxt = cnt < need1 ? need1 : need2;
-            if (cnt + g >= nxt) {  // a target falls in this group: walk it
-                for (int e = 0; e < 8 && !done; ++e) hit(su[ii + e], c0 + ii + e);
-                if (done) break;
-            } else {
-                cnt += g;
-            }
-        }
-        if (done) continue;
-        for (; ii < n; ++ii) {
-            hit(su[ii], c0 + ii);
-            if (done) break;
-        }
-    }
-    if (active) {
-        leave1[(int64_t)b * L + j] = l1;
-        leave2[(int64_t)b * L + j] = l2;
-    }
-}
-
-// (2) as a warp per key: 128 later scores per step (4 coalesced loads per
+// (2) a warp per key: 128 later scores per step (4 coalesced loads per
 // lane), ballots and popcounts for the running count of strictly larger
 // scores, the target position by a rank search in the crossing ballot.
 __global__ void __launch_bounds__(256)
@@ -298,18 +226,6 @@ k_rank_after_warp(const double* __restrict__ u, int L, int T, int R1, int R2, in
 }
 
 // ---------------------------------------------------------------- tau
-__device__ __forceinline__ void argmin_hi(double& v, int& lane) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        const double ov = __shfl_xor_sync(0xffffffffu, v, o);
-        const int ol = __shfl_xor_sync(0xffffffffu, lane, o);
-        if (ov < v || (ov == v && ol > lane)) {
-            v = ov;
-            lane = ol;
-        }
-    }
-}
-
 struct TauArgs {
     const double* u;
     const int* leave2;
