@@ -17,6 +17,7 @@
 //                  TMEM; rowsum_t (the pullback numerator) is per thread.
 // rowsum/colsum feed the O(L log L) selection pullback (skb_jvp.cu).
 #include <climits>
+#include <type_traits>
 
 #include "skb_common.cuh"
 #include "skb_internal.h"
@@ -1175,29 +1176,37 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_sel_tc(const __grid_co
                     }
                 } else if constexpr (!KEY_SOFT) {
                     // hard keys, fractional gates: packed fp32x2 except the gate
-                    // saturation and the fractional-support test
-                    float2 csum2 = make_float2(0.f, 0.f);
-                    const bool mst = a.mask_st != 0;
+                    // saturation and the fractional-support test; one loop per
+                    // (uniform) mask mode
+                    auto frac_loop = [&](auto mst_c) {
+                        constexpr bool kMst = decltype(mst_c)::value;
+                        float2 csum2 = make_float2(0.f, 0.f);
 #pragma unroll
-                    for (int c = 0; c < 32; c += 2) {
-                        const float2 l2 = *reinterpret_cast<const float2*>(ml + c);
-                        const float2 d2 = *reinterpret_cast<const float2*>(md + c);
-                        const float2 t2 = *reinterpret_cast<const float2*>(mt + c);
-                        const float g0 = __saturatef(uj - t2.x), g1 = __saturatef(uj - t2.y);
-                        float2 p2 = __ffma2_rn(make_float2(sv[c], sv[c + 1]), sl22, make_float2(-l2.x, -l2.y));
-                        p2.x = ex2(p2.x);  // masked: 0
-                        p2.y = ex2(p2.y);
-                        const float2 dp2 = make_float2(dp[c], dp[c + 1]);
-                        const float2 wv2 = mst ? make_float2(1.f, 1.f) : make_float2(g0, g1);
-                        const float2 cc2 = __fmul2_rn(p2, __ffma2_rn(wv2, dp2, make_float2(-d2.x, -d2.y)));
-                        const float2 fr2 = make_float2((g0 > 0.f && g0 < 1.f) ? 1.f : 0.f,
-                                                       (g1 > 0.f && g1 < 1.f) ? 1.f : 0.f);
-                        csum2 = __ffma2_rn(__fmul2_rn(p2, dp2), fr2, csum2);
-                        const float2 pw2 = __fmul2_rn(p2, wv2);
-                        sv[c] = pw2.x, sv[c + 1] = pw2.y;  // P~^T
-                        dp[c] = cc2.x, dp[c + 1] = cc2.y;  // dS^T (scale applied in the epilogue)
-                    }
-                    colsum += csum2.x + csum2.y;
+                        for (int c = 0; c < 32; c += 2) {
+                            const float2 l2 = *reinterpret_cast<const float2*>(ml + c);
+                            const float2 d2 = *reinterpret_cast<const float2*>(md + c);
+                            const float2 t2 = *reinterpret_cast<const float2*>(mt + c);
+                            const float g0 = __saturatef(uj - t2.x), g1 = __saturatef(uj - t2.y);
+                            float2 p2 = __ffma2_rn(make_float2(sv[c], sv[c + 1]), sl22, make_float2(-l2.x, -l2.y));
+                            p2.x = ex2(p2.x);  // masked: 0
+                            p2.y = ex2(p2.y);
+                            const float2 dp2 = make_float2(dp[c], dp[c + 1]);
+                            const float2 nd2 = make_float2(-d2.x, -d2.y);
+                            const float2 g2 = make_float2(g0, g1);
+                            const float2 cc2 = kMst ? __fmul2_rn(p2, __fadd2_rn(dp2, nd2))
+                                                    : __fmul2_rn(p2, __ffma2_rn(g2, dp2, nd2));
+                            // 0 < g < 1 <=> (bits(g) - 1) < bits(1.0) - 1 (g in [0, 1])
+                            const float2 fr2 = make_float2((__float_as_uint(g0) - 1u) < 0x3F7FFFFFu ? 1.f : 0.f,
+                                                           (__float_as_uint(g1) - 1u) < 0x3F7FFFFFu ? 1.f : 0.f);
+                            csum2 = __ffma2_rn(__fmul2_rn(p2, dp2), fr2, csum2);
+                            const float2 pw2 = kMst ? p2 : __fmul2_rn(p2, g2);
+                            sv[c] = pw2.x, sv[c + 1] = pw2.y;  // P~^T
+                            dp[c] = cc2.x, dp[c + 1] = cc2.y;  // dS^T (scale applied in the epilogue)
+                        }
+                        colsum += csum2.x + csum2.y;
+                    };
+                    if (a.mask_st) frac_loop(std::true_type{});
+                    else frac_loop(std::false_type{});
                 } else {
                     float csum = 0.f;
 #pragma unroll
@@ -1903,25 +1912,32 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_p(const __grid_constant_
                 if (!(fl & 2)) {  // fractional gates present
                     plain = false;
                     if constexpr (!KEY_SOFT) {  // packed fp32x2 except gate saturation / support test
-                        float2 rs2 = make_float2(0.f, 0.f);
-                        const bool mst = a.mask_st != 0;
+                        // the mask mode is uniform: one loop per mode (no per-element selects)
+                        auto frac_loop = [&](auto mst_c) {
+                            constexpr bool kMst = decltype(mst_c)::value;
+                            float2 rs2 = make_float2(0.f, 0.f);
 #pragma unroll
-                        for (int c = 0; c < 64; c += 2) {
-                            const float2 uu = *reinterpret_cast<const float2*>(mu + c);
-                            const float g0 = __saturatef(uu.x - tau_i), g1 = __saturatef(uu.y - tau_i);
-                            float2 p2 = __ffma2_rn(make_float2(sv[c], sv[c + 1]), sl22, nl2);
-                            p2.x = ex2(p2.x);
-                            p2.y = ex2(p2.y);
-                            const float2 dp2 = make_float2(dp[c], dp[c + 1]);
-                            const float2 wv2 = mst ? make_float2(1.f, 1.f) : make_float2(g0, g1);
-                            const float2 cc2 = __fmul2_rn(p2, __ffma2_rn(wv2, dp2, ndl));
-                            const float2 fr2 = make_float2((g0 > 0.f && g0 < 1.f) ? 1.f : 0.f,
-                                                           (g1 > 0.f && g1 < 1.f) ? 1.f : 0.f);
-                            rs2 = __ffma2_rn(__fmul2_rn(p2, dp2), fr2, rs2);
-                            dp[c] = cc2.x;
-                            dp[c + 1] = cc2.y;
-                        }
-                        rsum += rs2.x + rs2.y;
+                            for (int c = 0; c < 64; c += 2) {
+                                const float2 uu = *reinterpret_cast<const float2*>(mu + c);
+                                const float g0 = __saturatef(uu.x - tau_i), g1 = __saturatef(uu.y - tau_i);
+                                float2 p2 = __ffma2_rn(make_float2(sv[c], sv[c + 1]), sl22, nl2);
+                                p2.x = ex2(p2.x);
+                                p2.y = ex2(p2.y);
+                                const float2 dp2 = make_float2(dp[c], dp[c + 1]);
+                                const float2 cc2 = kMst ? __fmul2_rn(p2, __fadd2_rn(dp2, ndl))
+                                                        : __fmul2_rn(p2, __ffma2_rn(make_float2(g0, g1), dp2, ndl));
+                                // 0 < g < 1 <=> (bits(g) - 1) < bits(1.0) - 1 (g in [0, 1])
+                                const float2 fr2 =
+                                    make_float2((__float_as_uint(g0) - 1u) < 0x3F7FFFFFu ? 1.f : 0.f,
+                                                (__float_as_uint(g1) - 1u) < 0x3F7FFFFFu ? 1.f : 0.f);
+                                rs2 = __ffma2_rn(__fmul2_rn(p2, dp2), fr2, rs2);
+                                dp[c] = cc2.x;
+                                dp[c + 1] = cc2.y;
+                            }
+                            rsum += rs2.x + rs2.y;
+                        };
+                        if (a.mask_st) frac_loop(std::true_type{});
+                        else frac_loop(std::false_type{});
                     } else {
 #pragma unroll
                     for (int c = 0; c < 64; c += 4) {
