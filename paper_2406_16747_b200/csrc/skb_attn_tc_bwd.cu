@@ -1679,7 +1679,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_p(const __grid_constant_
     };
 
     if (threadIdx.x == 0) {
-        mbar_init(&bars[QB_QFULL], kMath / 2);
+        mbar_init(&bars[QB_QFULL], kMath);
         mbar_init(&bars[QB_DOFULL], 1);
         for (int s = 0; s < kNS; ++s) {
             mbar_init(&bars[QB_KVFULL + s], kProducers + 1);
@@ -1831,24 +1831,25 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_p(const __grid_constant_
         const int hf = warp >> 2;
         const int r = ((warp & 3) << 5) | lane;
         const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
-        // this row of Q -> TMEM (the A operand of S), warpgroup 0
+        // this row of Q -> TMEM (the A operand of S): warpgroup hf writes the
+        // packed columns of its half of the row
         auto load_q = [&](const Item& I) {
             const int i = I.i0 + r;
-            const __nv_bfloat16* src = a.q + ((I.bl + (i < a.L ? i : 0)) * a.H + I.h) * D;
-            uint32_t wq[D / 2];
+            const __nv_bfloat16* src = a.q + ((I.bl + (i < a.L ? i : 0)) * a.H + I.h) * D + hf * (D / 2);
+            uint32_t wq[D / 4];
 #pragma unroll
-            for (int c = 0; c < D / 8; ++c) {
+            for (int c = 0; c < D / 16; ++c) {
                 uint4 x = make_uint4(0u, 0u, 0u, 0u);
                 if (i < a.L) x = *reinterpret_cast<const uint4*>(src + c * 8);
                 wq[4 * c] = x.x, wq[4 * c + 1] = x.y, wq[4 * c + 2] = x.z, wq[4 * c + 3] = x.w;
             }
-#pragma unroll
-            for (int c = 0; c < D / 64; ++c) tmem_st32u(tQ + lane_off + c * 32, wq + c * 32);
+            if constexpr (D == 128) tmem_st32u(tQ + lane_off + hf * 32, wq);
+            else tmem_st16u(tQ + lane_off + hf * 16, wq);
             tmem_wait_st();
             tc_before_sync();
             mbar_arrive(&bars[QB_QFULL]);
         };
-        if (hf == 0 && (int)blockIdx.x < nitems) load_q(item(blockIdx.x));
+        if ((int)blockIdx.x < nitems) load_q(item(blockIdx.x));
         int J = 0, it = 0, tr0 = 1 << 28;
         const bool trl = lane == 0 && (warp & 3) == 0;
         for (int wi = blockIdx.x; wi < nitems; wi += gridDim.x, ++it) {
@@ -1857,13 +1858,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_p(const __grid_constant_
         const int b = I.b, h = I.h, n_sel = I.n_sel, n = I.n, jw0 = I.jw0;
         const int64_t bl = I.bl;
         const int i = I.i0 + r;
-        if (hf == 0 && wi + (int)gridDim.x < nitems) {  // the next item's Q row, for load_q
+        if (wi + (int)gridDim.x < nitems) {  // this half of the next item's Q row, for load_q
             const Item N = item(wi + gridDim.x);
             const int ni = N.i0 + r;
             if (ni < a.L) {
-                const char* src = reinterpret_cast<const char*>(a.q + ((N.bl + ni) * a.H + N.h) * D);
+                const char* src =
+                    reinterpret_cast<const char*>(a.q + ((N.bl + ni) * a.H + N.h) * D + hf * (D / 2));
 #pragma unroll
-                for (int c = 0; c < D * 2; c += 128) prefetch_l2(src + c);
+                for (int c = 0; c < D; c += 128) prefetch_l2(src + c);
             }
         }
         const int t = i - a.w;
@@ -2004,7 +2006,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_p(const __grid_constant_
             mbar_arrive(&bars[QB_DSFULL]);
         }
         // the next item's Q: the S MMAs of this item are complete (consumed above)
-        if (hf == 0 && wi + (int)gridDim.x < nitems) load_q(item(wi + gridDim.x));
+        if (wi + (int)gridDim.x < nitems) load_q(item(wi + gridDim.x));
         if (trl) TRQ(hf, J - 1, 5);
         mbar_wait(&bars[QB_DQDONE], it & 1);
         if (trl) TRQ(hf, J - 1, 6);
