@@ -179,3 +179,28 @@ def test_snapshot_config_mismatch(cuda):
     b = ops.DecodeCache(1, 2, 32, ops.AttnConfig(k=9.0, window=4), max_len=50, dtype=torch.float32)
     with pytest.raises(IoError):
         b.restore(a.snapshot(0))
+
+
+def test_session_snapshot_per_sequence(cuda):
+    """Batched session: every sequence snapshots and restores independently
+    (its own scoring state, stream and cache) and resumes bit for bit."""
+    import torch
+
+    from paper_2406_16747_b200 import DecodeSession, ops
+
+    B, L, D, H, k, w, prompt, cut = 3, 90, 32, 2, 9.5, 6, 20, 55
+    rng = np.random.default_rng(11)
+    x = torch.from_numpy(rng.normal(size=(B, L, D))).to(cuda)
+    ws = [torch.from_numpy(rng.normal(size=(D, D)) / np.sqrt(D)).to(cuda) for _ in range(4)]
+    wsc = torch.from_numpy(rng.normal(size=D)).to(cuda)
+    cfg = ops.AttnConfig(k=k, window=w)
+    a = DecodeSession(*ws, wsc, cfg, H, batch=B, max_len=L)
+    a.prefill(x[:, :prompt])
+    for i in range(prompt, cut):
+        a.step(x[:, i])
+    b = DecodeSession(*ws, wsc, cfg, H, batch=B, max_len=L)
+    for s in (2, 0, 1):  # any order
+        b.restore(a.snapshot(s), s)
+    assert torch.equal(a.state, b.state)
+    for i in range(cut, L):
+        assert torch.equal(a.step(x[:, i]), b.step(x[:, i])), i
