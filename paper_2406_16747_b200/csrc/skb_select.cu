@@ -22,6 +22,8 @@
 //      the block's push times (<= floor(k)+127 keys by irreversibility).
 #include <cfloat>
 
+#include <cub/block/block_radix_sort.cuh>
+
 #include "skb_common.cuh"
 #include "skb_internal.h"
 #include "skb_solve.cuh"
@@ -36,6 +38,18 @@ constexpr int kTauThreads = 256;
 constexpr int kOverflowSlots = 16;
 #ifndef SKB_TAU_EXP
 #define SKB_TAU_EXP 0
+#endif
+#ifdef SKB_TRACE_TAU  // phase clocks of the last chunk of sequence 0 (tools/trace_tau.py)
+__device__ unsigned long long g_skb_trace_tau[16];
+#define TTAU(t0_, T_, ev)                                                                     \
+    do {                                                                                     \
+        if (threadIdx.x == 0 && blockIdx.y == 0 && (t0_) / kChunk == ((T_) - 1) / kChunk)    \
+            g_skb_trace_tau[ev] = clock64();                                                 \
+    } while (0)
+#else
+#define TTAU(t0_, T_, ev) \
+    do {                  \
+    } while (0)
 #endif
 
 // ---------------------------------------------------------------- ranks
@@ -246,11 +260,20 @@ __device__ void tau_chunk_tail(const TauArgs& a, int b, int chunk, const double*
 
 // The band of push time t0: every prefix score above theta(t0) - 1, sorted
 // descending into bz. Returns its size, or -1 (nothing written) above `cap`.
-__device__ int tau_band(const TauArgs& a, int b, int t0, double* bz, int cap, double* red_d) {
+// Bands of <= 2048 scores (the first pass) are sorted by a block radix sort
+// (256 threads x 8 keys) whose scratch aliases the prefix-sum array P; wider
+// bands (the large-cap passes) by the shared-memory bitonic sort.
+constexpr int kRadixItems = 8;
+using BandSort = cub::BlockRadixSort<double, kTauThreads, kRadixItems>;
+constexpr int kRadixMax = kTauThreads * kRadixItems;
+
+__device__ int tau_band(const TauArgs& a, int b, int t0, double* bz, int cap, double* red_d,
+                        void* sort_tmp = nullptr) {
     __shared__ int s_m;
     const double* ub = a.u + (int64_t)b * a.L;
     const int* lv = a.leave2 + (int64_t)b * a.L;
 
+    TTAU(t0, a.T, 0);
     // theta = R2-th largest of prefix [0, t0): min over j < t0 still in the top R2 at t0-1.
     double theta = -CUDART_INF;
     if (t0 >= a.R2 && a.R2 > 0) {
@@ -272,6 +295,7 @@ __device__ int tau_band(const TauArgs& a, int b, int t0, double* bz, int cap, do
         theta = block_reduce<double>(mn, red_d, false);
     }
     const double cut = theta - 1.0;
+    TTAU(t0, a.T, 1);
     if (threadIdx.x == 0) s_m = 0;
     __syncthreads();
     // one pass: warp-aggregated slots, stores only below the cap (an oversized
@@ -299,13 +323,33 @@ __device__ int tau_band(const TauArgs& a, int b, int t0, double* bz, int cap, do
     __syncthreads();
     const int mcount = s_m;
     __syncthreads();
+    TTAU(t0, a.T, 2);
     if (mcount > cap) return -1;
+    if (sort_tmp != nullptr && mcount <= kRadixMax && blockDim.x == kTauThreads) {
+        double keys[kRadixItems];
+#pragma unroll
+        for (int e = 0; e < kRadixItems; ++e) {
+            const int idx = threadIdx.x * kRadixItems + e;
+            keys[e] = idx < mcount ? bz[idx] : -CUDART_INF;
+        }
+        BandSort(*static_cast<typename BandSort::TempStorage*>(sort_tmp)).SortDescending(keys);
+        __syncthreads();
+#pragma unroll
+        for (int e = 0; e < kRadixItems; ++e) {
+            const int idx = threadIdx.x * kRadixItems + e;
+            if (idx < mcount) bz[idx] = keys[e];
+        }
+        __syncthreads();
+        TTAU(t0, a.T, 3);
+        return mcount;
+    }
     int n2 = 1;
     while (n2 < mcount) n2 <<= 1;
     __syncthreads();
     for (int i = mcount + threadIdx.x; i < n2; i += blockDim.x) bz[i] = -CUDART_INF;
     __syncthreads();
     bitonic_desc(bz, n2);
+    TTAU(t0, a.T, 3);
     return mcount;
 }
 
@@ -315,7 +359,8 @@ __device__ bool tau_chunk(const TauArgs& a, int b, int chunk, double* bz, double
                           bool probe_only_if_overflow) {
     __shared__ double red_d[32];
     (void)probe_only_if_overflow;
-    const int mcount = tau_band(a, b, chunk * kChunk, bz, cap, red_d);
+    // the radix sort's scratch aliases P (written only after the sort)
+    const int mcount = tau_band(a, b, chunk * kChunk, bz, cap, red_d, probe_only_if_overflow ? nullptr : P);
     if (mcount < 0) return false;
     tau_chunk_tail(a, b, chunk, bz, P, mcount, red_d);
     return true;
@@ -328,6 +373,7 @@ __device__ void tau_chunk_tail(const TauArgs& a, int b, int chunk, const double*
     const int t0 = chunk * kChunk;
     const double* ub = a.u + (int64_t)b * a.L;
     excl_prefix(bz, P, mcount, red_d);
+    TTAU(t0, a.T, 4);
 
     // exact state after pushes [0, t0)
     double tau0 = -CUDART_INF;
@@ -343,6 +389,7 @@ __device__ void tau_chunk_tail(const TauArgs& a, int b, int chunk, const double*
         ws = n_gt(bz, mcount, tau0);
         uf = n_ge(bz, mcount, tau0 + 1.0);
     }
+    TTAU(t0, a.T, 5);
 
     // stream replay (proj/src/stream.cpp:72-152) for the chunk's arrivals. The
     // survivors are the sorted band prefix bz[0, ws) plus chunk entries; the
@@ -440,6 +487,7 @@ __device__ void tau_chunk_tail(const TauArgs& a, int b, int chunk, const double*
         }
     }
     __syncthreads();
+    TTAU(t0, a.T, 6);
 }
 
 __global__ void __launch_bounds__(kTauThreads) k_tau_chunks(TauArgs a) {
@@ -879,7 +927,7 @@ void run_select(const skb_attn_desc& d, const double* u, void* ws, cudaStream_t 
         static bool attr_set = false;
         if (!attr_set) {
             SKB_CHECK_CUDA(cudaFuncSetAttribute(k_tau_chunks, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                (int)(8192 * 2 * sizeof(double) + 16)));
+                                                (int)(8192 * 2 * sizeof(double) + 8 + 16)));  // bz + P[cap + 1]
             SKB_CHECK_CUDA(cudaFuncSetAttribute(k_tau_chunks_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                 (int)(8192 * 2 * sizeof(double) + 16)));
             SKB_CHECK_CUDA(cudaFuncSetAttribute(k_tau_segments<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -895,7 +943,10 @@ void run_select(const skb_attn_desc& d, const double* u, void* ws, cudaStream_t 
                                                                                                    nullptr, nullptr);
         } else {
             dim3 g(nch, B);
-            k_tau_chunks<<<g, kTauThreads, (size_t)a.cap * 2 * sizeof(double) + 16, st>>>(a);
+            // bz + P; P also holds the block radix sort's scratch
+        const size_t p1smem = (size_t)a.cap * sizeof(double) +
+                              std::max((size_t)(a.cap + 1) * sizeof(double), sizeof(BandSort::TempStorage)) + 16;
+        k_tau_chunks<<<g, kTauThreads, p1smem, st>>>(a);
         }
         SKB_CHECK_LAUNCH();
         if (cap_big > a.cap) {
@@ -959,3 +1010,9 @@ SelView sel_view(const skb_attn_desc& d, const void* ws) {
 }
 
 }  // namespace skb
+
+#ifdef SKB_TRACE_TAU
+extern "C" int skb_debug_trace_tau(unsigned long long* out, int n) {
+    return (int)cudaMemcpyFromSymbol(out, skb::g_skb_trace_tau, sizeof(unsigned long long) * (n < 16 ? n : 16));
+}
+#endif
