@@ -492,7 +492,9 @@ __device__ void tau_chunk_tail(const TauArgs& a, int b, int chunk, const double*
 
 __global__ void __launch_bounds__(kTauThreads) k_tau_chunks(TauArgs a) {
     extern __shared__ double smem[];
-    const int b = blockIdx.y, chunk = blockIdx.x;
+    // latest chunks first: their prefixes are the longest (the scans and the
+    // band grow with t0), so they must not be left to a trailing partial wave
+    const int b = blockIdx.y, chunk = gridDim.x - 1 - blockIdx.x;
     double* bz = smem;
     double* P = smem + a.cap;
     if (!tau_chunk(a, b, chunk, bz, P, a.cap, false)) {
