@@ -759,6 +759,43 @@ __global__ void k_fill_tau(double* tau, int* nfrac, int64_t n) {
     }
 }
 
+// The same running maximum with one CTA per 1024 push times: each CTA reduces
+// the prefix before its chunk itself (<= T loads, all in flight) and scans its
+// chunk, so no CTA waits on another. Reads tau_in, writes tau_out (distinct).
+__global__ void __launch_bounds__(1024) k_tau_monotone_chunks(const double* __restrict__ tau_in,
+                                                              double* __restrict__ tau_out, int L, int T) {
+    __shared__ double wmax[32];
+    const int b = blockIdx.y, c0 = blockIdx.x * 1024;
+    const double* ti = tau_in + (int64_t)b * L;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    double pre = -CUDART_INF;
+    for (int j0 = threadIdx.x; j0 < c0; j0 += 4 * 1024) {
+        double x[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) x[q] = j0 + q * 1024 < c0 ? ti[j0 + q * 1024] : -CUDART_INF;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) pre = fmax(pre, x[q]);
+    }
+    pre = warp_max(pre);
+    if (lane == 0) wmax[wid] = pre;
+    __syncthreads();
+    double before = -CUDART_INF;
+    for (int w = 0; w < 32; ++w) before = fmax(before, wmax[w]);
+    __syncthreads();
+    const int t = c0 + threadIdx.x;
+    const double v = t < T ? ti[t] : -CUDART_INF;
+    double incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl = fmax(incl, y);
+    }
+    if (lane == 31) wmax[wid] = incl;
+    __syncthreads();
+    for (int w = 0; w < wid; ++w) before = fmax(before, wmax[w]);
+    if (t < T) tau_out[(int64_t)b * L + t] = fmax(before, incl);
+}
+
 // tau_t := max over t' <= t (the stream's tau never decreases, stream.cpp:128;
 // chunk-start solves and replays can differ from it by rounding only).
 __global__ void __launch_bounds__(1024) k_tau_monotone(double* tau, int L, int T) {
@@ -831,7 +868,8 @@ void select_layout(const skb_attn_desc& d, skb_select_layout& o) {
     o.ever_list = take(B * L * 4);
     o.misc = take((2 + 3 * B * nch) * 4);  // two overflow queues [count, items...] + pass-1 flags
     const int64_t cap2 = next_pow2((int)std::max<int64_t>(L, 1));
-    o.scratch = take((uint64_t)kOverflowSlots * (cap2 + L + 1) * 8);
+    // the overflow pass's global bands; afterwards the running-max staging of tau [B, L]
+    o.scratch = take(std::max<uint64_t>((uint64_t)kOverflowSlots * (cap2 + L + 1), (uint64_t)B * L) * 8);
     o.uf = take(B * L * 4);
     o.tauf = take(B * L * 4);
     o.qb_leave = take(B * nqb * cap * 4);
@@ -963,8 +1001,14 @@ void run_select(const skb_attn_desc& d, const double* u, void* ws, cudaStream_t 
         }
         k_tau_overflow<<<kOverflowSlots, kTauThreads, 0, st>>>(a, nch, cap2);
         SKB_CHECK_LAUNCH();
-        k_tau_monotone<<<B, 1024, 0, st>>>(tau, L, T);
-        SKB_CHECK_LAUNCH();
+        // running max into the uf/tauf scratch (rewritten by k_to_float below), then back
+        {
+            double* tmp = reinterpret_cast<double*>(base + lay.scratch);
+            k_tau_monotone_chunks<<<dim3((unsigned)cdiv(T, 1024), (unsigned)B), 1024, 0, st>>>(tau, tmp, L, T);
+            SKB_CHECK_LAUNCH();
+            SKB_CHECK_CUDA(cudaMemcpy2DAsync(tau, (size_t)L * 8, tmp, (size_t)L * 8, (size_t)T * 8, B,
+                                             cudaMemcpyDeviceToDevice, st));
+        }
     }
     k_to_float<<<(unsigned)cdiv(BL, 256), 256, 0, st>>>(u, tau, reinterpret_cast<float*>(base + lay.uf),
                                                           reinterpret_cast<float*>(base + lay.tauf), BL);
