@@ -17,55 +17,51 @@ namespace skb {
 
 namespace {
 
-// M[t] = sum_{t' < t} mean_t' per sequence (M[T] = total): one CTA, coalesced
-// 1024-element chunks, a block scan per chunk carried across chunks.
+// M[t] = sum_{t' < t} mean_t' per sequence (M[T] = total): one CTA per 1024
+// push times; each reduces the means before its chunk itself (all loads in
+// flight) and scans its chunk, so no CTA waits on another.
 __global__ void __launch_bounds__(1024)
 k_mean_prefix(const double* __restrict__ rowsum, const int* __restrict__ nfrac,
               const double* __restrict__ tau, int L, int T, double* __restrict__ M) {
     __shared__ double wsum[32];
-    __shared__ double carry_s;
-    const int b = blockIdx.x;
+    const int b = blockIdx.y, c0 = blockIdx.x * 1024;
     const double* rs = rowsum + (int64_t)b * L;
     const int* nf = nfrac + (int64_t)b * L;
     const double* tb = tau + (int64_t)b * L;
     double* Mb = M + (int64_t)b * (L + 1);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    double carry = 0.0;
     auto mean_at = [&](int t) {
-        if (t >= T) return 0.0;
         const int n = nf[t];
         return (n > 0 && tb[t] > -INFINITY) ? rs[t] / (double)n : 0.0;
     };
-    double xn = mean_at(threadIdx.x);  // chunk c + 1 is loaded while chunk c scans
-    for (int c0 = 0; c0 < T; c0 += 1024) {
-        const int t = c0 + threadIdx.x;
-        const double x = xn;
-        xn = mean_at(t + 1024);
-        double incl = x;
+    double pre = 0.0;
+    for (int j0 = threadIdx.x; j0 < c0; j0 += 4 * 1024) {
+        double x[4];
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const double y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
-        }
-        if (lane == 31) wsum[wid] = incl;
-        __syncthreads();
-        if (wid == 0) {
-            double ws = wsum[lane];
+        for (int q = 0; q < 4; ++q) x[q] = j0 + q * 1024 < c0 ? mean_at(j0 + q * 1024) : 0.0;
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const double y = __shfl_up_sync(0xffffffffu, ws, o);
-                if (lane >= o) ws += y;
-            }
-            wsum[lane] = ws;  // inclusive over warps
-        }
-        __syncthreads();
-        const double pre = carry + (wid > 0 ? wsum[wid - 1] : 0.0);
-        if (t < T) Mb[t] = pre + incl - x;
-        if (threadIdx.x == 1023) carry_s = pre + incl;
-        __syncthreads();
-        carry = carry_s;
+        for (int q = 0; q < 4; ++q) pre += x[q];
     }
-    if (threadIdx.x == 0) Mb[T] = carry;
+    pre = warp_sum(pre);
+    if (lane == 0) wsum[wid] = pre;
+    __syncthreads();
+    double before = 0.0;
+    for (int w = 0; w < 32; ++w) before += wsum[w];
+    __syncthreads();
+    const int t = c0 + threadIdx.x;
+    const double x = t < T ? mean_at(t) : 0.0;
+    double incl = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) wsum[wid] = incl;
+    __syncthreads();
+    for (int w = 0; w < wid; ++w) before += wsum[w];
+    if (t < T) Mb[t] = before + incl - x;
+    if (t == T - 1) Mb[T] = before + incl;
+    if (T == 0 && blockIdx.x == 0 && threadIdx.x == 0) Mb[0] = 0.0;
 }
 
 __global__ void k_jvp(const double* __restrict__ u, const double* __restrict__ tau,
@@ -143,7 +139,8 @@ void run_jvp(const skb_attn_desc& d, const double* u, const SelView& s, const do
         SKB_CHECK_CUDA(cudaMemsetAsync(du, 0, (size_t)B * L * sizeof(double), st));
         return;
     }
-    k_mean_prefix<<<B, 1024, 0, st>>>(rowsum, s.nfrac, s.tau, L, T, mean_prefix);
+    k_mean_prefix<<<dim3((unsigned)std::max<int64_t>(1, cdiv(T, 1024)), (unsigned)B), 1024, 0, st>>>(
+        rowsum, s.nfrac, s.tau, L, T, mean_prefix);
     SKB_CHECK_LAUNCH();
     dim3 g((unsigned)cdiv(L, 256), B);
     k_jvp<<<g, 256, 0, st>>>(u, s.tau, colsum, mean_prefix, L, T, (int)d.window, (int)d.chunk_len, du);
