@@ -617,77 +617,95 @@ __global__ void __launch_bounds__(kTauThreads) k_tau_overflow(TauArgs a, int nch
 }
 
 // ---------------------------------------------------------------- unions
-// Ordered block compaction of keys j in [0, t_hi] with leave_j > max(j, t_lo).
+// Ordered block compaction of keys j in [0, t_hi] with leave_j > max(j, t_lo),
+// 4 x blockDim keys per step (4 sub-chunks in order; two barriers per step).
 __global__ void __launch_bounds__(1024)
 k_union_lists(const int* __restrict__ leave1, int L, int T, int window, int nqb, int cap,
               int* __restrict__ qb_count, int* __restrict__ qb_list) {
-    __shared__ int wsum[32];
-    __shared__ int base_s;
+    __shared__ int wsum[4][32];
     const int b = blockIdx.y, qb = blockIdx.x;
     const int t_lo = qb * kQBlock - window;
     const int t_hi = min(qb * kQBlock + kQBlock - 1 - window, T - 1);
     const int* lv = leave1 + (int64_t)b * L;
     int* out = qb_list + ((int64_t)b * nqb + qb) * cap;
-    if (threadIdx.x == 0) base_s = 0;
-    __syncthreads();
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    for (int j0 = 0; j0 <= t_hi; j0 += blockDim.x) {
-        const int j = j0 + threadIdx.x;
-        bool keep = false;
-        if (j <= t_hi) {
-            const int l = lv[j];
-            keep = l > j && l > t_lo;
+    int base = 0;
+    const int nt = blockDim.x, nw = nt >> 5;
+    for (int j0 = 0; j0 <= t_hi; j0 += 4 * nt) {
+        unsigned bal[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int j = j0 + q * nt + threadIdx.x;
+            bool keep = false;
+            if (j <= t_hi) {
+                const int l = lv[j];
+                keep = l > j && l > t_lo;
+            }
+            bal[q] = __ballot_sync(0xffffffffu, keep);
+            if (lane == 0) wsum[q][wid] = __popc(bal[q]);
         }
-        const unsigned bal = __ballot_sync(0xffffffffu, keep);
-        if (lane == 0) wsum[wid] = __popc(bal);
         __syncthreads();
-        int off = base_s;
-        for (int w = 0; w < wid; ++w) off += wsum[w];
-        if (keep) {
-            const int pos = off + __popc(bal & ((1u << lane) - 1u));
-            if (pos < cap) out[pos] = j;
+        int off = base;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            int before = 0, tot = 0;
+            for (int w = 0; w < nw; ++w) {
+                before += w < wid ? wsum[q][w] : 0;
+                tot += wsum[q][w];
+            }
+            if ((bal[q] >> lane) & 1u) {
+                const int pos = off + before + __popc(bal[q] & ((1u << lane) - 1u));
+                if (pos < cap) out[pos] = j0 + q * nt + threadIdx.x;
+            }
+            off += tot;
         }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            int tot = 0;
-            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += wsum[w];
-            base_s += tot;
-        }
+        base = off;
         __syncthreads();
     }
-    if (threadIdx.x == 0) qb_count[(int64_t)b * nqb + qb] = min(base_s, cap);
+    if (threadIdx.x == 0) qb_count[(int64_t)b * nqb + qb] = min(base, cap);
 }
 
-// Ever-selected keys per sequence, ascending.
+// Ever-selected keys per sequence, ascending: one CTA per 1024 keys; each
+// counts the kept keys before its chunk itself (all loads in flight) and
+// compacts its chunk, so no CTA waits on another.
 __global__ void __launch_bounds__(1024)
 k_ever_list(const int* __restrict__ leave1, int L, int T, int* __restrict__ ever_count,
             int* __restrict__ ever_list) {
     __shared__ int wsum[32];
-    __shared__ int base_s;
-    const int b = blockIdx.x;
+    const int b = blockIdx.y, c0 = blockIdx.x * 1024;
     const int* lv = leave1 + (int64_t)b * L;
     int* out = ever_list + (int64_t)b * L;
-    if (threadIdx.x == 0) base_s = 0;
-    __syncthreads();
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    for (int j0 = 0; j0 < T; j0 += blockDim.x) {
-        const int j = j0 + threadIdx.x;
-        const bool keep = j < T && lv[j] > j;
-        const unsigned bal = __ballot_sync(0xffffffffu, keep);
-        if (lane == 0) wsum[wid] = __popc(bal);
-        __syncthreads();
-        int off = base_s;
-        for (int w = 0; w < wid; ++w) off += wsum[w];
-        if (keep) out[off + __popc(bal & ((1u << lane) - 1u))] = j;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            int tot = 0;
-            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += wsum[w];
-            base_s += tot;
+    int pre = 0;
+    for (int j0 = threadIdx.x; j0 < c0; j0 += 4 * 1024) {
+        int x[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int j = j0 + q * 1024;
+            x[q] = j < c0 ? (lv[j] > j) : 0;
         }
-        __syncthreads();
+        pre += x[0] + x[1] + x[2] + x[3];
     }
-    if (threadIdx.x == 0) ever_count[b] = base_s;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) pre += __shfl_xor_sync(0xffffffffu, pre, o);
+    if (lane == 0) wsum[wid] = pre;
+    __syncthreads();
+    int base = 0;
+    for (int w = 0; w < 32; ++w) base += wsum[w];
+    __syncthreads();
+    const int j = c0 + threadIdx.x;
+    const bool keep = j < T && lv[j] > j;
+    const unsigned bal = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0) wsum[wid] = __popc(bal);
+    __syncthreads();
+    int off = base;
+    for (int w = 0; w < wid; ++w) off += wsum[w];
+    if (keep) out[off + __popc(bal & ((1u << lane) - 1u))] = j;
+    if (c0 + 1024 >= T && threadIdx.x == 0) {  // the last chunk: the total
+        int tot = base;
+        for (int w = 0; w < 32; ++w) tot += wsum[w];
+        ever_count[b] = tot;
+    }
 }
 
 // Per-block metadata for the tensor-core kernels, so their producers issue no
@@ -1017,7 +1035,8 @@ void run_select(const skb_attn_desc& d, const double* u, void* ws, cudaStream_t 
     if (R1 > 0 && T > 0) {
         dim3 g(nqb, B);
         k_union_lists<<<g, 512, 0, st>>>(leave1, L, T, w, nqb, (int)lay.qb_cap, qb_count, qb_list);
-        k_ever_list<<<B, 1024, 0, st>>>(leave1, L, T, ever_count, ever_list);
+        k_ever_list<<<dim3((unsigned)cdiv(T, 1024), (unsigned)B), 1024, 0, st>>>(leave1, L, T, ever_count,
+                                                                                   ever_list);
         SKB_CHECK_LAUNCH();
         k_union_meta<<<g, 128, 0, st>>>(leave1, reinterpret_cast<const float*>(base + lay.uf),
                                         reinterpret_cast<const float*>(base + lay.tauf), L, T, w, nqb,
