@@ -153,15 +153,16 @@ k_rank_leave(const double* __restrict__ u, int L, int T, int R1, int R2, int* __
 // from A_j: A_j >= R2 leaves at entry, else the later scan for the
 // (R1-A_j)-th / (R2-A_j)-th strictly larger score, as in k_rank_leave.
 constexpr int kRankChunk = 1024;
-__global__ void __launch_bounds__(kRankThreads)
+constexpr int kRankBeforeThreads = 256;  // keys per CTA sharing one staged score chunk
+__global__ void __launch_bounds__(kRankBeforeThreads)
 k_rank_before(const double* __restrict__ u, int L, int T, int* __restrict__ A) {
     __shared__ __align__(16) double su[kRankChunk];
     const int b = blockIdx.z;
-    const int j0 = blockIdx.x * kRankThreads, c0 = blockIdx.y * kRankChunk;
-    if (c0 >= min(T, j0 + kRankThreads)) return;  // chunk entirely after the block's keys
+    const int j0 = blockIdx.x * kRankBeforeThreads, c0 = blockIdx.y * kRankChunk;
+    if (c0 >= min(T, j0 + kRankBeforeThreads)) return;  // chunk entirely after the block's keys
     const double* ub = u + (int64_t)b * L;
     const int n = min(kRankChunk, T - c0);
-    for (int i = threadIdx.x; i < kRankChunk; i += kRankThreads) su[i] = i < n ? ub[c0 + i] : 0.0;
+    for (int i = threadIdx.x; i < kRankChunk; i += kRankBeforeThreads) su[i] = i < n ? ub[c0 + i] : 0.0;
     __syncthreads();
     const int j = j0 + threadIdx.x;
     if (j >= T) return;
@@ -950,8 +951,8 @@ void run_select(const skb_attn_desc& d, const double* u, void* ws, cudaStream_t 
         dim3 g((unsigned)cdiv(T, kRankThreads), B);
         if (rank2) {
             SKB_CHECK_CUDA(cudaMemsetAsync(leave1, 0, (size_t)B * L * sizeof(int), st));
-            dim3 g1((unsigned)cdiv(T, kRankThreads), (unsigned)cdiv(T, kRankChunk), B);
-            k_rank_before<<<g1, kRankThreads, 0, st>>>(u, L, T, leave1);
+            dim3 g1((unsigned)cdiv(T, kRankBeforeThreads), (unsigned)cdiv(T, kRankChunk), B);
+            k_rank_before<<<g1, kRankBeforeThreads, 0, st>>>(u, L, T, leave1);
             SKB_CHECK_LAUNCH();
             k_rank_after_warp<<<dim3((unsigned)cdiv(T, 8), B), 256, 0, st>>>(u, L, T, R1, R2, leave1, leave2);
         } else {
