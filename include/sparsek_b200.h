@@ -218,6 +218,31 @@ int skb_stream_destroy(skb_stream* s);
 int skb_stream_push(skb_stream* s, const double* z, int64_t n, double* tau_out,
                     uint8_t* inserted_out, void* stream);
 int skb_stream_query(skb_stream* s, skb_stream_info* out, void* stream);
+/* StreamState::push(z) with its StreamStepResult (proj/include/sparsek/stream.hpp:12-18,
+ * proj/src/stream.cpp:72-152) in one device round trip: z is a host value;
+ * evicted (host, max_evicted entries) receives the indices that left the
+ * survivors during this push, in pop order; n_evicted is their total count. */
+typedef struct skb_stream_step {
+    double tau;         /* -inf while t < k                            */
+    int64_t t;          /* elements pushed so far                       */
+    int32_t inserted;   /* 0: arrived at or below tau, never survived   */
+    int32_t cap_forced; /* a bounded heap dropped a survivor            */
+    int64_t n_evicted;
+} skb_stream_step;
+int skb_stream_push_step(skb_stream* s, double z, skb_stream_step* out, int64_t* evicted, int64_t max_evicted,
+                         void* stream);
+/* StreamState::solution + stream_mask (proj/src/stream.cpp:154-222) on the
+ * device: survivors in ascending index order — p (float64), indices (int64)
+ * and, when hard != NULL, the top-floor(k) SelectionMask flag (uint8); all
+ * device buffers with room for every survivor. Counts and tau on the host. */
+typedef struct skb_stream_solution_info {
+    double tau;          /* -inf when infeasible (t < k)                */
+    int64_t t, n;        /* pushes; survivors (entries written)        */
+    int64_t u_count, w_count;
+    int32_t degenerate, infeasible;
+} skb_stream_solution_info;
+int skb_stream_solution(skb_stream* s, double* p, int64_t* indices, uint8_t* hard, skb_stream_solution_info* out,
+                        void* stream);
 /* Host copies: survivor values/indices in ascending index order (|survivors|
  * entries) and the evicted flag of every pushed index (t entries). */
 /* The reference's stream wire format (StreamState::serialize/deserialize,

@@ -358,6 +358,64 @@ class Reference:
         finally:
             self.lib.ref_tape_free(h)
 
+    def stream_events(self, z, k, heap_cap=0):
+        """Per push: (tau, inserted, cap_forced, evicted list) from StreamStepResult."""
+        z = np.ascontiguousarray(z, np.float64)
+        n = len(z)
+        tau = np.zeros(n)
+        ins, capf = np.zeros(n, np.uint8), np.zeros(n, np.uint8)
+        cnt = np.zeros(n, np.uint64)
+        flat = np.zeros(max(n, 1), np.uint64)
+        u64p = C.POINTER(C.c_uint64)
+        self._rc(self.lib.ref_stream_events(_d(z), C.c_uint64(n), C.c_double(k), C.c_uint64(heap_cap),
+                                            _d(tau), ins.ctypes.data_as(_u8p), capf.ctypes.data_as(_u8p),
+                                            cnt.ctypes.data_as(u64p), flat.ctypes.data_as(u64p),
+                                            C.c_uint64(len(flat))))
+        off = np.concatenate([[0], np.cumsum(cnt)]).astype(np.int64)
+        evs = [flat[off[t]:off[t + 1]].astype(np.int64).tolist() for t in range(n)]
+        return tau, ins.astype(bool), capf.astype(bool), evs
+
+    def stream_mask(self, z, k, heap_cap=0):
+        """stream_mask after pushing z: (positions, hard, soft, indices)."""
+        z = np.ascontiguousarray(z, np.float64)
+        n = len(z)
+        pos, idx = np.zeros(max(n, 1), np.uint64), np.zeros(max(n, 1), np.uint64)
+        hard, soft = np.zeros(max(n, 1)), np.zeros(max(n, 1))
+        nn, ni = C.c_uint64(), C.c_uint64()
+        u64p = C.POINTER(C.c_uint64)
+        self._rc(self.lib.ref_stream_mask(_d(z), C.c_uint64(n), C.c_double(k), C.c_uint64(heap_cap),
+                                          pos.ctypes.data_as(u64p), _d(hard), _d(soft), C.byref(nn),
+                                          idx.ctypes.data_as(u64p), C.byref(ni)))
+        m = nn.value
+        return (pos[:m].astype(np.int64), hard[:m], soft[:m], idx[:ni.value].astype(np.int64))
+
+    def sparsek_st(self, z, k):
+        z = np.ascontiguousarray(z, np.float64)
+        fwd, p = np.zeros_like(z), np.zeros_like(z)
+        self._rc(self.lib.ref_sparsek_st(_d(z), C.c_uint64(len(z)), C.c_double(k), _d(fwd), _d(p)))
+        return fwd, p
+
+    def sparsek_partial_stats(self, z, k, sort_cap):
+        z = np.ascontiguousarray(z, np.float64)
+        p = np.zeros_like(z)
+        tau = C.c_double()
+        calls, fb = C.c_uint64(), C.c_uint64()
+        self._rc(self.lib.ref_sparsek_partial_stats(_d(z), C.c_uint64(len(z)), C.c_double(k),
+                                                    C.c_uint64(sort_cap), _d(p), C.byref(tau),
+                                                    C.byref(calls), C.byref(fb)))
+        return p, tau.value, calls.value, fb.value
+
+    def dense_attention_grads(self, x, wq, wk, wv, wo, grad_out, heads=1):
+        """dense_causal_attention + dense_causal_attention_backward (double)."""
+        x, wq, wk, wv, wo, g = (np.ascontiguousarray(a, np.float64) for a in (x, wq, wk, wv, wo, grad_out))
+        L, D = x.shape
+        y, dx = np.zeros((L, D)), np.zeros((L, D))
+        dws = [np.zeros((D, D)) for _ in range(4)]
+        self._rc(self.lib.ref_dense_attention_grads(C.c_uint64(L), C.c_uint64(D), C.c_uint64(heads), _d(x),
+                                                    _d(wq), _d(wk), _d(wv), _d(wo), _d(g), _d(y), _d(dx),
+                                                    *[_d(a) for a in dws]))
+        return y, dict(dx=dx, dwq=dws[0], dwk=dws[1], dwv=dws[2], dwo=dws[3])
+
     def dense_attention(self, x, wq, wk, wv, wo, heads=1):
         x, wq, wk, wv, wo = (np.ascontiguousarray(a, np.float64) for a in (x, wq, wk, wv, wo))
         L, D = x.shape

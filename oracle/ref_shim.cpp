@@ -132,6 +132,73 @@ int ref_stream_run(const double* z, uint64_t n, double k, uint64_t heap_cap, dou
     REF_GUARD_END
 }
 
+// StreamState::push events: per push the StreamStepResult (tau, inserted,
+// cap_forced) and its evicted indices, flattened (ev_count[t] entries each,
+// in the order the reference reports them; ev_flat holds ev_cap entries).
+int ref_stream_events(const double* z, uint64_t n, double k, uint64_t heap_cap, double* tau_out,
+                      uint8_t* inserted_out, uint8_t* cap_forced_out, uint64_t* ev_count, uint64_t* ev_flat,
+                      uint64_t ev_cap) {
+    REF_GUARD_BEGIN
+    StreamState st{KBudget(k), heap_cap};
+    uint64_t used = 0;
+    for (uint64_t t = 0; t < n; ++t) {
+        StreamStepResult r = st.push(z[t]);
+        tau_out[t] = r.tau;
+        inserted_out[t] = r.inserted ? 1 : 0;
+        cap_forced_out[t] = r.cap_forced ? 1 : 0;
+        ev_count[t] = r.evicted.size();
+        for (size_t e : r.evicted) {
+            if (used >= ev_cap) throw ArgumentError("ref_stream_events: ev_flat too small");
+            ev_flat[used++] = e;
+        }
+    }
+    REF_GUARD_END
+}
+
+// stream_mask after pushing z[0..n) (proj/src/stream.cpp:199-222): hard/soft
+// per survivor slot (ascending index; positions in pos_out), *n_out slots and
+// the hard set's positions in idx_out (*n_idx of them).
+int ref_stream_mask(const double* z, uint64_t n, double k, uint64_t heap_cap, uint64_t* pos_out, double* hard_out,
+                    double* soft_out, uint64_t* n_out, uint64_t* idx_out, uint64_t* n_idx) {
+    REF_GUARD_BEGIN
+    StreamState st{KBudget(k), heap_cap};
+    for (uint64_t t = 0; t < n; ++t) st.push(z[t]);
+    SelectionMask m = stream_mask(st);
+    const SparseKSolution sol = st.solution();
+    *n_out = m.hard.size();
+    for (size_t i = 0; i < m.hard.size(); ++i) {
+        pos_out[i] = sol.indices[i];
+        hard_out[i] = m.hard[i];
+        soft_out[i] = m.soft[i];
+    }
+    *n_idx = m.indices.size();
+    for (size_t i = 0; i < m.indices.size(); ++i) idx_out[i] = m.indices[i];
+    REF_GUARD_END
+}
+
+// sparsek_st (proj/src/sparsek_op.cpp:167-172): hard forward + soft carrier p.
+int ref_sparsek_st(const double* z, uint64_t m, double k, double* forward, double* p) {
+    REF_GUARD_BEGIN
+    std::vector<double> zv(z, z + m);
+    StResult r = sparsek_st(zv, KBudget(k));
+    std::memcpy(forward, r.forward.data(), m * sizeof(double));
+    fill_solution(r.backward_carrier, m, p, nullptr, nullptr, nullptr, nullptr, nullptr);
+    REF_GUARD_END
+}
+
+// sparsek_partial with PartialSortStats (proj/src/sparsek_op.cpp:116-139).
+int ref_sparsek_partial_stats(const double* z, uint64_t m, double k, uint64_t sort_cap, double* p, double* tau,
+                              uint64_t* calls, uint64_t* fallbacks) {
+    REF_GUARD_BEGIN
+    std::vector<double> zv(z, z + m);
+    PartialSortStats st;
+    SparseKSolution sol = sparsek_partial(zv, KBudget(k), sort_cap, &st);
+    fill_solution(sol, m, p, tau, nullptr, nullptr, nullptr, nullptr);
+    *calls = st.calls;
+    *fallbacks = st.fallbacks;
+    REF_GUARD_END
+}
+
 // StreamState::serialize after pushing z[0..n): *used = blob size (out may be
 // null to query it; cap = out capacity).
 int ref_stream_blob(const double* z, uint64_t n, double k, uint64_t heap_cap, uint8_t* out,
@@ -351,6 +418,29 @@ int ref_dense_attention(uint64_t L, uint64_t D, uint64_t heads, const double* x,
     MatT<double> r = dense_causal_attention(mat_in<double>(x, L, D), params,
                                             cfg.effective_scale(D), heads);
     mat_out(r, y);
+    REF_GUARD_END
+}
+
+// dense_causal_attention + its backward (proj/src/attention.cpp:76-205), double.
+int ref_dense_attention_grads(uint64_t L, uint64_t D, uint64_t heads, const double* x, const double* wq,
+                              const double* wk, const double* wv, const double* wo, const double* grad_out,
+                              double* y, double* dx, double* dwq, double* dwk, double* dwv, double* dwo) {
+    REF_GUARD_BEGIN
+    AttnParams<double> params{mat_in<double>(wq, D, D), mat_in<double>(wk, D, D),
+                              mat_in<double>(wv, D, D), mat_in<double>(wo, D, D)};
+    AttnConfig cfg;
+    cfg.heads = heads;
+    const double scale = cfg.effective_scale(D);
+    MatT<double> xm = mat_in<double>(x, L, D), hc;
+    MatT<double> r = dense_causal_attention(xm, params, scale, heads, &hc);
+    mat_out(r, y);
+    AttnGrads<double> g = dense_causal_attention_backward(xm, params, scale, heads, hc,
+                                                          mat_in<double>(grad_out, L, D));
+    mat_out(g.dx, dx);
+    mat_out(g.dwq, dwq);
+    mat_out(g.dwk, dwk);
+    mat_out(g.dwv, dwv);
+    mat_out(g.dwo, dwo);
     REF_GUARD_END
 }
 

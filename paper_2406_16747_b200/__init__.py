@@ -9,20 +9,29 @@ API and Python bindings over hand-written sm_100a kernels.
 from ._lib import ArgumentError, ConfigError, IoError, NumericError, ShapeError  # noqa: F401
 from .api import (  # noqa: F401
     DecodeSession,
+    PartialSortStats,
+    SelectionMask,
     Stream,
     __version__,
     attention,
+    attention_backward,
     attention_grads,
+    attention_with_tape,
     chunked_forward,
     dense_attention,
+    dense_attention_grads,
     sparsek,
     sparsek_jvp,
+    sparsek_partial,
+    sparsek_st,
+    stream_mask,
     topk_hard,
 )
 from . import ops  # noqa: F401
 
 __all__ = [
     "ArgumentError", "ConfigError", "DecodeSession", "NumericError", "ShapeError", "IoError", "Stream",
-    "__version__", "attention", "attention_grads", "chunked_forward", "dense_attention", "sparsek", "sparsek_jvp",
-    "topk_hard", "ops",
+    "PartialSortStats", "SelectionMask", "__version__", "attention", "attention_backward", "attention_grads",
+    "attention_with_tape", "chunked_forward", "dense_attention", "dense_attention_grads", "sparsek",
+    "sparsek_jvp", "sparsek_partial", "sparsek_st", "stream_mask", "topk_hard", "ops",
 ]

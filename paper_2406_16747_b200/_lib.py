@@ -75,6 +75,16 @@ class StreamInfo(C.Structure):
                 ("k", C.c_double)]
 
 
+class StreamStep(C.Structure):
+    _fields_ = [("tau", C.c_double), ("t", C.c_int64), ("inserted", C.c_int32),
+                ("cap_forced", C.c_int32), ("n_evicted", C.c_int64)]
+
+
+class StreamSolutionInfo(C.Structure):
+    _fields_ = [("tau", C.c_double), ("t", C.c_int64), ("n", C.c_int64), ("u_count", C.c_int64),
+                ("w_count", C.c_int64), ("degenerate", C.c_int32), ("infeasible", C.c_int32)]
+
+
 _vp = C.c_void_p
 _SIGS = {
     "skb_last_error": ([], C.c_char_p),
@@ -105,6 +115,8 @@ _SIGS = {
     "skb_stream_destroy": ([_vp], C.c_int),
     "skb_stream_push": ([_vp, _vp, C.c_int64, _vp, _vp, _vp], C.c_int),
     "skb_stream_query": ([_vp, C.POINTER(StreamInfo), _vp], C.c_int),
+    "skb_stream_push_step": ([_vp, C.c_double, C.POINTER(StreamStep), _vp, C.c_int64, _vp], C.c_int),
+    "skb_stream_solution": ([_vp, _vp, _vp, _vp, C.POINTER(StreamSolutionInfo), _vp], C.c_int),
     "skb_stream_survivors": ([_vp, _vp, _vp, _vp, _vp], C.c_int),
     "skb_stream_serialize": ([_vp, _vp, C.POINTER(C.c_size_t), _vp], C.c_int),
     "skb_stream_deserialize": ([_vp, C.c_size_t, C.c_int64, C.POINTER(_vp)], C.c_int),

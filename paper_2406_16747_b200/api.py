@@ -41,22 +41,82 @@ def _check_budget(k):
         raise ArgumentError("KBudget: k must be positive and finite")
 
 
+class PartialSortStats:
+    """PartialSortStats (proj/include/sparsek/sparsek_op.hpp:42-45)."""
+
+    def __init__(self):
+        self.calls = 0
+        self.fallbacks = 0
+
+    def __repr__(self):
+        return f"PartialSortStats(calls={self.calls}, fallbacks={self.fallbacks})"
+
+
+def _solve_row(zz, k):
+    zt = torch.from_numpy(zz).to(_dev()).view(1, -1)
+    p, tau, uc, wc, fl = ops.sparsek_rows(zt, k)
+    fl = int(fl[0])
+    return {"p": p[0].cpu().numpy(), "tau": _tau_out(float(tau[0])), "u_count": int(uc[0]),
+            "w_count": int(wc[0]), "degenerate": bool(fl & 1), "infeasible": bool(fl & 2)}
+
+
+def _public(sol):
+    return {key: sol[key] for key in ("p", "tau", "u_count", "w_count", "degenerate")}
+
+
+def sparsek_partial(z, k, sort_cap, stats: PartialSortStats | None = None):
+    """sparsek_partial (proj/src/sparsek_op.cpp:116-139): the solve restricted to
+    the sort_cap largest values, falling back to the full solve when the cut
+    cannot be certified. The device solver always evaluates the exact
+    projection, which is what both branches of the reference return; ``stats``
+    counts the calls and the reference's fallbacks — its truncated scan fails
+    exactly when the accepted support reaches the cap (w_count >= sort_cap)."""
+    k = float(k)
+    zz = _vec(z, "sparsek_partial")
+    if zz.size == 0:
+        raise ArgumentError("sparsek_partial: empty input")
+    _check_budget(k)
+    if sort_cap < math.ceil(k):
+        raise ArgumentError("sparsek_partial: sort_cap below ceil(k)")
+    if stats is not None:
+        stats.calls += 1
+    if not np.all(np.isfinite(zz)):
+        raise NumericError("sparsek_partial: non-finite input")
+    sol = _solve_row(zz, k)
+    if (stats is not None and not sol["infeasible"] and sort_cap < zz.size
+            and sol["w_count"] >= sort_cap):
+        stats.fallbacks += 1
+    return _public(sol)
+
+
 def sparsek(z, k, sort_cap=0):
     """Clamped-shift projection of z onto {0 <= p <= 1, sum p = k}
     (proj/src/sparsek_op.cpp:102-139). Returns {p, tau, u_count, w_count, degenerate}."""
+    if sort_cap:
+        return sparsek_partial(z, k, sort_cap)
     k = float(k)
     zz = _vec(z, "sparsek")
     if zz.size == 0:
         raise ArgumentError("sparsek: empty input")
     _check_budget(k)
-    if sort_cap and sort_cap < math.ceil(k):
-        raise ArgumentError("sparsek_partial: sort_cap below ceil(k)")
     if not np.all(np.isfinite(zz)):
         raise NumericError("sparsek: non-finite input")
-    zt = torch.from_numpy(zz).to(_dev()).view(1, -1)
-    p, tau, uc, wc, fl = ops.sparsek_rows(zt, k)
-    return {"p": p[0].cpu().numpy(), "tau": _tau_out(float(tau[0])), "u_count": int(uc[0]),
-            "w_count": int(wc[0]), "degenerate": bool(int(fl[0]) & 1)}
+    return _public(_solve_row(zz, k))
+
+
+def sparsek_st(z, k):
+    """Straight-through pairing (proj/src/sparsek_op.cpp:167-172): the hard
+    top-floor(k) forward and the soft solution as the gradient carrier.
+    Returns {forward, backward_carrier}."""
+    k = float(k)
+    zz = _vec(z, "sparsek_st")
+    if zz.size == 0:
+        raise ArgumentError("sparsek: empty input")
+    _check_budget(k)
+    if not np.all(np.isfinite(zz)):
+        raise NumericError("sparsek: non-finite input")
+    carrier = _public(_solve_row(zz, k))
+    return {"forward": topk_hard(zz, int(math.floor(k))), "backward_carrier": carrier}
 
 
 def sparsek_jvp(z, k, v):
@@ -84,7 +144,7 @@ def topk_hard(z, k):
     return out[0].cpu().numpy()
 
 
-from .stream import Stream  # noqa: E402  (device-resident StreamState)
+from .stream import SelectionMask, Stream, stream_mask  # noqa: E402,F401  (device-resident StreamState)
 
 
 def _mat(a, name):
@@ -323,3 +383,69 @@ def dense_attention(x, wq, wk, wv, wo, heads=1):
     u = torch.zeros((1, L), dtype=torch.float64, device=d)
     o, _, _ = ops.attn_fwd(q.contiguous(), kk.contiguous(), v.contiguous(), u, cfg)
     return (o.reshape(L, D) @ t(wo)).cpu().numpy()
+
+
+def dense_attention_grads(x, wq, wk, wv, wo, grad_out, heads=1):
+    """dense_causal_attention + dense_causal_attention_backward
+    (proj/src/attention.cpp:76-205): returns (y, {dx, dwq, dwk, dwv, dwo}) as
+    float64 numpy arrays. The attention core is the SparseK kernels with a
+    budget covering every position (tau = -inf, every gate 1) and constant
+    scores, so no gradient reaches a score."""
+    x, (wq, wk, wv, wo) = _attention_inputs(x, wq, wk, wv, wo, heads)
+    L, D = x.shape
+    p = D // heads
+    d = _dev()
+    leaf = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(d).requires_grad_(True)
+    xt, wqt, wkt, wvt, wot = (leaf(a) for a in (x, wq, wk, wv, wo))
+    cfg = ops.AttnConfig(k=float(L + 1), window=1)
+    q, kk, v = ((xt @ w).view(1, L, heads, p) for w in (wqt, wkt, wvt))
+    u = torch.zeros((1, L), dtype=torch.float64, device=d)
+    hc = ops.sparsek_attention_core(q, kk, v, u, cfg)
+    y = hc.reshape(L, D) @ wot
+    y.backward(torch.from_numpy(np.ascontiguousarray(grad_out, np.float64)).to(d))
+    return y.detach().cpu().numpy(), dict(dx=xt.grad.cpu().numpy(), dwq=wqt.grad.cpu().numpy(),
+                                          dwk=wkt.grad.cpu().numpy(), dwv=wvt.grad.cpu().numpy(),
+                                          dwo=wot.grad.cpu().numpy())
+
+
+def attention_with_tape(x, wq, wk, wv, wo, w_score, k, window, heads=1, key_mode="hard",
+                        mask_mode="soft", slope_eps=0.01, slope_enabled=True,
+                        norm_mode="timestep_norm", slope_order="norm_then_slope", chunk_len=0):
+    """sparsek_attention with an AttnTape (proj/include/sparsek/attention.hpp:81-85):
+    returns (y, tape); the tape stays on the device and feeds
+    ``attention_backward``. Inputs are numpy (float64, like the bindings) or
+    device tensors (their dtype is kept)."""
+    from . import tape as tp
+
+    if isinstance(x, torch.Tensor):
+        d = x.device
+        conv = lambda a: a
+    else:
+        x, (wq, wk, wv, wo) = _attention_inputs(x, wq, wk, wv, wo, heads)
+        d = _dev()
+        conv = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.float64)).to(d)
+    cfg = _core_cfg(float(k), int(window), key_mode, mask_mode)
+    if chunk_len:
+        cfg = ops.AttnConfig(k=cfg.k, window=cfg.window, key_mode=cfg.key_mode, mask_mode=cfg.mask_mode,
+                             chunk_len=int(chunk_len))
+    params = tp.AttnParams(conv(wq), conv(wk), conv(wv), conv(wo))
+    sc = ops.ScoringConfig(slope_eps=float(slope_eps), slope_enabled=bool(slope_enabled),
+                           norm_mode=norm_mode, slope_order=slope_order, chunk_len=int(chunk_len))
+    ws = conv(w_score) if (w_score is not None and cfg.k > 0.0) else None
+    tape = tp.AttnTape()
+    y = tp.forward(conv(x), params, ws, sc, cfg, int(heads), tape)
+    tape.params, tape.w_score, tape.scoring = params, ws, sc
+    return (y if isinstance(x, torch.Tensor) else y.cpu().numpy()), tape
+
+
+def attention_backward(tape, grad_out):
+    """sparsek_attention_backward (proj/src/attention.cpp:214-575) from a tape
+    made by ``attention_with_tape``: {dx, dwq, dwk, dwv, dwo, dw_score}."""
+    from . import tape as tp
+
+    host = not isinstance(grad_out, torch.Tensor)
+    g = torch.from_numpy(np.ascontiguousarray(grad_out, np.float64)).to(tape.x.device) if host else grad_out
+    out = tp.backward(tape, g, tape.params, tape.w_score, tape.scoring)
+    if tape.x.shape[0] == 1:
+        out["dx"] = out["dx"][0]
+    return {k: v.cpu().numpy() for k, v in out.items()} if host else out

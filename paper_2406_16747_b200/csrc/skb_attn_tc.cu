@@ -881,13 +881,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_p(const __grid_constant__ F
 template <int D, bool KS>
 void launch_fwd(const FwdArgs& a, dim3 grid, cudaStream_t st) {
     using SM = FwdSmem<D>;
-    static bool attr = false;
-    if (!attr) {
+    static uint64_t attr = 0;
+    if (first_on_device(&attr)) {
         SKB_CHECK_CUDA(cudaFuncSetAttribute(k_fwd_tc<D, KS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             SM::kAlloc));
         SKB_CHECK_CUDA(cudaFuncSetAttribute(k_fwd_p<D, KS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             SM::kAlloc));
-        attr = true;
     }
     static const int persist = getenv("SKB_FWD_PERSIST") ? atoi(getenv("SKB_FWD_PERSIST")) : 1;
     if (persist) {

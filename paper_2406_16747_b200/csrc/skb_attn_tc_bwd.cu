@@ -2051,25 +2051,21 @@ void set_smem(K kern, int bytes) {
 
 template <int D, bool KS>
 void launch_bwd(const BwdArgs& a, const skb_attn_desc& d, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
+    static uint64_t attr = 0;
+    if (first_on_device(&attr)) {
         set_smem(k_bwd_dkdv_tc<D, true, KS>, KSmem<D>::kAlloc);
         set_smem(k_bwd_dkdv_sel_tc<D, KS>, KSmem<D>::kAlloc);
         set_smem(k_bwd_dkdv_win_tc<D>, KWSmem<D>::kAlloc);
         set_smem(k_bwd_dq_tc<D, KS>, QSmem<D>::kAlloc);
         set_smem(k_bwd_dq_p<D, KS>, QSmem<D>::kAlloc);
-        attr = true;
     }
     if (a.R1 > 0 && a.T > 0) {
         static const int persist = getenv("SKB_SEL_PERSIST") ? atoi(getenv("SKB_SEL_PERSIST")) : 1;
         if (persist) {
             const int ntk = (int)cdiv(a.L, 128);
             const int osm = kOrdCntBytes + std::min(a.T, kOrdMaxBk);
-            static bool oattr = false;
-            if (!oattr) {
-                set_smem(k_sel_order, kOrdCntBytes + kOrdMaxBk);
-                oattr = true;
-            }
+            static uint64_t oattr = 0;
+            if (first_on_device(&oattr)) set_smem(k_sel_order, kOrdCntBytes + kOrdMaxBk);
             k_sel_order<<<(unsigned)a.B, kOrdThreads, osm, st>>>(a);
             SKB_CHECK_LAUNCH();
             k_sel_items<<<(unsigned)cdiv((int64_t)a.B * ntk * 32, 256), 256, 0, st>>>(a, ntk);

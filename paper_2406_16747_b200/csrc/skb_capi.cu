@@ -178,7 +178,7 @@ int skb_attn_bwd(const skb_attn_desc* d, const void* q, const void* k, const voi
     } else {
         skb::run_attn_bwd_gather(*d, q, k, v, dout, lse, u, s, dq, dk, dv, rowsum, colsum, ws, bl, st);
     }
-    skb::run_jvp(*d, u, s, rowsum, colsum, mp, du, st);
+    skb::run_jvp(*d, u, s, rowsum, colsum, mp, reinterpret_cast<double*>(base + bl.chunk_sums), du, st);
     SKB_API_END
 }
 

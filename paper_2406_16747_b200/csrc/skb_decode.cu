@@ -62,6 +62,8 @@ struct StreamArr {
     double* fv;
     int* fi;
     uint8_t* evicted;  // [cap] or null
+    int* evlog;        // indices popped from the survivors, in pop order (or null)
+    int* evcount;      // entries in evlog (lane 0 owns both)
 };
 
 __device__ __forceinline__ int warp_sum_i(int v) {
@@ -157,6 +159,7 @@ __device__ bool warp_stream_push(StreamCtl& c, const StreamArr& a, double z, int
         c.nS -= 1;
         c.sum_s -= v;
         if (a.evicted && lane == 0) a.evicted[ix] = 1;
+        if (a.evlog && lane == 0) a.evlog[(*a.evcount)++] = ix;
         c.heap_ops += 1;
     };
     auto pop_f = [&]() {
@@ -233,6 +236,100 @@ __global__ void k_stream_push(StreamCtl* ctl, StreamArr a, const double* __restr
     if (lane == 0) *ctl = c;
 }
 
+// One push with the reference's StreamStepResult (proj/include/sparsek/stream.hpp:12-18):
+// tau, t, inserted, cap_forced and the survivors popped by this push (evlog).
+struct StreamStepRes {
+    double tau;
+    long long t;
+    int inserted, cap_forced, n_evicted, error;
+};
+__global__ void k_stream_push_step(StreamCtl* ctl, StreamArr a, double z, StreamStepRes* res) {
+    StreamCtl c = *ctl;
+    const int lane = threadIdx.x & 31;
+    if (lane == 0) *a.evcount = 0;
+    __syncwarp();
+    const unsigned long long drops0 = c.cap_drops;
+    int rank;
+    const bool ins = c.t < c.cap ? warp_stream_push(c, a, z, &rank) : (c.error = 2, false);
+    if (lane == 0) {
+        *ctl = c;
+        StreamStepRes r;
+        r.tau = c.tau;
+        r.t = c.t;
+        r.inserted = ins ? 1 : 0;
+        r.cap_forced = c.cap_drops != drops0 ? 1 : 0;
+        r.n_evicted = *a.evcount;
+        r.error = c.error;
+        *res = r;
+    }
+}
+
+// StreamState::solution + stream_mask (proj/src/stream.cpp:154-222) on the
+// device: survivors in ascending index order with p = clamp(z - tau, 0, 1)
+// (all ones while t < k), and the hard top-floor(k) flag — the survivors
+// array is sorted by (value desc, index asc), so its first floor(k) entries
+// are the mask's (p desc, index asc) top (saturated entries are at most k).
+// One CTA: scatter each survivor's rank to its index, compact in index order.
+struct StreamSolRes {
+    int n, u_count, w_count, pad;
+};
+__global__ void __launch_bounds__(1024) k_stream_solution(const StreamCtl* ctl, StreamArr a, int* rank_of,
+                                                          double* p_out, long long* idx_out, uint8_t* hard_out,
+                                                          StreamSolRes* res) {
+    __shared__ int wsum[32];
+    __shared__ int s_u, s_w;
+    const StreamCtl c = *ctl;
+    const int T = (int)c.t, nS = c.nS;
+    const int kk = (int)floor(c.k);
+    const bool infeasible = (double)c.t < c.k;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (threadIdx.x == 0) s_u = s_w = 0;
+    for (int j = threadIdx.x; j < T; j += 1024) rank_of[j] = -1;
+    __syncthreads();
+    for (int r = threadIdx.x; r < nS; r += 1024) rank_of[a.si[r]] = r;
+    __syncthreads();
+    int base = 0, nu = 0, nw = 0;
+    for (int j0 = 0; j0 < T; j0 += 1024) {
+        const int j = j0 + threadIdx.x;
+        const int r = j < T ? rank_of[j] : -1;
+        const bool keep = r >= 0;
+        const unsigned bal = __ballot_sync(0xffffffffu, keep);
+        if (lane == 0) wsum[wid] = __popc(bal);
+        __syncthreads();
+        int off = base, tot = 0;
+        for (int w = 0; w < 32; ++w) {
+            if (w < wid) off += wsum[w];
+            tot += wsum[w];
+        }
+        if (keep) {
+            const int o = off + __popc(bal & ((1u << lane) - 1u));
+            double pj = 1.0;
+            if (!infeasible) {
+                pj = a.sv[r] - c.tau;
+                pj = pj < 0.0 ? 0.0 : (pj > 1.0 ? 1.0 : pj);
+            }
+            p_out[o] = pj;
+            idx_out[o] = j;
+            if (hard_out) hard_out[o] = r < kk ? 1 : 0;
+            nu += pj == 1.0;
+            nw += pj > 0.0;
+        }
+        base += tot;
+        __syncthreads();
+    }
+    atomicAdd(&s_u, nu);
+    atomicAdd(&s_w, nw);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        StreamSolRes r;
+        r.n = base;
+        r.u_count = s_u;
+        r.w_count = s_w;
+        r.pad = 0;
+        *res = r;
+    }
+}
+
 // ------------------------------------------------------------------ cache
 struct CacheCtl {
     StreamCtl st;
@@ -291,7 +388,7 @@ __device__ void warp_cache_advance(const CacheArgs& A, int b, CacheCtl& c, doubl
         return;
     }
     const int pos = (int)c.t;
-    StreamArr sa{A.sv + bL, A.si + bL, A.fv + bL, A.fi + bL, nullptr};
+    StreamArr sa{A.sv + bL, A.si + bL, A.fv + bL, A.fi + bL, nullptr, nullptr, nullptr};
     if (lane == 0) A.u_hist[bL + pos] = u_new;
     // the new row enters the window ring (kv_.emplace + ring_.push_back)
     const int slot = A.free_stack[bS + c.free_top - 1];
@@ -767,6 +864,11 @@ struct skb_stream {
     StreamCtl* ctl = nullptr;
     StreamArr arr{};
     int64_t capacity = 0;
+    int* rank_of = nullptr;          // [capacity] solution scratch
+    StreamStepRes* dres = nullptr;   // device result of the last push_step
+    StreamSolRes* dsol = nullptr;
+    uint8_t* hres = nullptr;         // pinned: StreamStepRes + the first kLogInline evicted indices
+    static constexpr int kLogInline = 64;
 };
 
 // Host-side state of a SparseKvCache snapshot that the device arrays do not
@@ -790,6 +892,7 @@ struct skb_cache {
     double* po = nullptr;  // split partials: float64 for float64 pools, else float32
     double* pm = nullptr;
     double* pl = nullptr;
+    double* zeros = nullptr;  // [B] idle scores for k = 0 (on the cache's device)
     std::vector<void*> allocs;
     ~skb_cache() {
         for (void* p : allocs) cudaFree(p);
@@ -835,19 +938,34 @@ int skb_stream_create(double k, int64_t heap_cap, int64_t capacity, skb_stream**
     skb_stream* s = new skb_stream();
     s->capacity = capacity;
     void* p = nullptr;
-    cudaError_t e = cudaMalloc(&p, sizeof(StreamCtl) + (size_t)capacity * (8 + 4 + 8 + 4 + 1) + 64);
+    // ctl | sv fv | si fi | evlog rank_of | step/solution results | evcount | evicted bits
+    const size_t ctl_b = (sizeof(StreamCtl) + 15) & ~size_t(15);
+    cudaError_t e = cudaMalloc(&p, ctl_b + (size_t)capacity * (8 + 8 + 4 + 4 + 4 + 4 + 1) + 256);
     if (e != cudaSuccess) {
         delete s;
         throw skb::Error(SKB_ECUDA, std::string("stream_create: ") + cudaGetErrorString(e));
     }
     char* base = static_cast<char*>(p);
     s->ctl = reinterpret_cast<StreamCtl*>(base);
-    char* q = base + ((sizeof(StreamCtl) + 15) & ~size_t(15));
+    char* q = base + ctl_b;
     s->arr.sv = reinterpret_cast<double*>(q);
     s->arr.fv = s->arr.sv + capacity;
     s->arr.si = reinterpret_cast<int*>(s->arr.fv + capacity);
     s->arr.fi = s->arr.si + capacity;
-    s->arr.evicted = reinterpret_cast<uint8_t*>(s->arr.fi + capacity);
+    s->arr.evlog = s->arr.fi + capacity;
+    s->rank_of = s->arr.evlog + capacity;
+    char* r8 = reinterpret_cast<char*>(s->rank_of + capacity);
+    r8 = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(r8) + 15) & ~uintptr_t(15));
+    s->dres = reinterpret_cast<StreamStepRes*>(r8);
+    s->dsol = reinterpret_cast<StreamSolRes*>(r8 + 64);
+    s->arr.evcount = reinterpret_cast<int*>(r8 + 96);
+    s->arr.evicted = reinterpret_cast<uint8_t*>(r8 + 128);
+    e = cudaMallocHost(&s->hres, 64 + sizeof(int) * skb_stream::kLogInline);
+    if (e != cudaSuccess) {
+        cudaFree(p);
+        delete s;
+        throw skb::Error(SKB_ECUDA, std::string("stream_create: ") + cudaGetErrorString(e));
+    }
     StreamCtl c{};
     c.k = k;
     c.tau = -INFINITY;
@@ -861,6 +979,7 @@ int skb_stream_create(double k, int64_t heap_cap, int64_t capacity, skb_stream**
 
 int skb_stream_destroy(skb_stream* s) {
     if (s) {
+        cudaFreeHost(s->hres);
         cudaFree(s->ctl);
         delete s;
     }
@@ -879,11 +998,74 @@ int skb_stream_push(skb_stream* s, const double* z, int64_t n, double* tau_out, 
     SKB_CHECK_CUDA(cudaMemcpyAsync(&c, s->ctl, sizeof(c), cudaMemcpyDeviceToHost, st));
     SKB_CHECK_CUDA(cudaStreamSynchronize(st));
     SKB_REQUIRE(c.t + n <= s->capacity, SKB_ESHAPE, "stream_push: capacity exceeded");
-    k_stream_push<<<1, 32, 0, st>>>(s->ctl, s->arr, z, (int)n, tau_out, inserted_out);
+    StreamArr arr = s->arr;
+    arr.evlog = nullptr;  // batched pushes report through tau/inserted only
+    k_stream_push<<<1, 32, 0, st>>>(s->ctl, arr, z, (int)n, tau_out, inserted_out);
     SKB_CHECK_LAUNCH();
     SKB_CHECK_CUDA(cudaMemcpyAsync(&c, s->ctl, sizeof(c), cudaMemcpyDeviceToHost, st));
     SKB_CHECK_CUDA(cudaStreamSynchronize(st));
     SKB_REQUIRE(c.error == 0, SKB_ENUMERIC, "stream scan exhausted (internal)");
+    K5_END
+}
+
+int skb_stream_push_step(skb_stream* s, double z, skb_stream_step* out, int64_t* evicted, int64_t max_evicted,
+                         void* stream) {
+    K5_BEGIN
+    SKB_REQUIRE(s != nullptr && out != nullptr, SKB_EARG, "stream_push: null argument");
+    SKB_REQUIRE(std::isfinite(z), SKB_ENUMERIC, "stream_push: non-finite value");
+    SKB_REQUIRE(max_evicted >= 0 && (max_evicted == 0 || evicted != nullptr), SKB_EARG,
+                "stream_push: bad evicted buffer");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    k_stream_push_step<<<1, 32, 0, st>>>(s->ctl, s->arr, z, s->dres);
+    SKB_CHECK_LAUNCH();
+    // one round trip: the result and the first kLogInline popped indices
+    SKB_CHECK_CUDA(cudaMemcpyAsync(s->hres, s->dres, sizeof(StreamStepRes), cudaMemcpyDeviceToHost, st));
+    SKB_CHECK_CUDA(cudaMemcpyAsync(s->hres + 64, s->arr.evlog, sizeof(int) * skb_stream::kLogInline,
+                                   cudaMemcpyDeviceToHost, st));
+    SKB_CHECK_CUDA(cudaStreamSynchronize(st));
+    StreamStepRes r;
+    std::memcpy(&r, s->hres, sizeof(r));
+    SKB_REQUIRE(r.error != 2, SKB_ESHAPE, "stream_push: capacity exceeded");
+    SKB_REQUIRE(r.error == 0, SKB_ENUMERIC, "stream scan exhausted (internal)");
+    out->tau = r.tau;
+    out->t = r.t;
+    out->inserted = r.inserted;
+    out->cap_forced = r.cap_forced;
+    out->n_evicted = r.n_evicted;
+    const int64_t ncopy = std::min<int64_t>(r.n_evicted, max_evicted);
+    const int* inl = reinterpret_cast<const int*>(s->hres + 64);
+    std::vector<int> tail;
+    if (ncopy > skb_stream::kLogInline) {
+        tail.resize((size_t)ncopy);
+        SKB_CHECK_CUDA(cudaMemcpy(tail.data(), s->arr.evlog, sizeof(int) * ncopy, cudaMemcpyDeviceToHost));
+        inl = tail.data();
+    }
+    for (int64_t i = 0; i < ncopy; ++i) evicted[i] = inl[i];
+    K5_END
+}
+
+int skb_stream_solution(skb_stream* s, double* p, int64_t* indices, uint8_t* hard, skb_stream_solution_info* out,
+                        void* stream) {
+    K5_BEGIN
+    SKB_REQUIRE(s != nullptr && out != nullptr && p != nullptr && indices != nullptr, SKB_EARG,
+                "stream_solution: null argument");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    k_stream_solution<<<1, 1024, 0, st>>>(s->ctl, s->arr, s->rank_of, p, reinterpret_cast<long long*>(indices),
+                                          hard, s->dsol);
+    SKB_CHECK_LAUNCH();
+    StreamCtl c;
+    StreamSolRes r;
+    SKB_CHECK_CUDA(cudaMemcpyAsync(&c, s->ctl, sizeof(c), cudaMemcpyDeviceToHost, st));
+    SKB_CHECK_CUDA(cudaMemcpyAsync(&r, s->dsol, sizeof(r), cudaMemcpyDeviceToHost, st));
+    SKB_CHECK_CUDA(cudaStreamSynchronize(st));
+    const bool infeasible = (double)c.t < c.k;
+    out->tau = infeasible ? -INFINITY : c.tau;
+    out->t = c.t;
+    out->n = r.n;
+    out->u_count = r.u_count;
+    out->w_count = r.w_count;
+    out->infeasible = infeasible ? 1 : 0;
+    out->degenerate = (infeasible || r.u_count == r.w_count) ? 1 : 0;
     K5_END
 }
 
@@ -1122,6 +1304,8 @@ int skb_cache_create(const skb_attn_desc* d, skb_cache** out) {
         c->pm = c->alloc<double>(B * c->nsplit * H);
         c->pl = c->alloc<double>(B * c->nsplit * H);
         c->vec = (p % 128 == 0) ? 4 : (p % 64 == 0) ? 2 : 1;
+        c->zeros = c->alloc<double>(B);
+        SKB_CHECK_CUDA(cudaMemset(c->zeros, 0, B * sizeof(double)));
         k_cache_init<<<(unsigned)B, 256>>>(A, d->k);
         SKB_CHECK_LAUNCH();
         SKB_CHECK_CUDA(cudaDeviceSynchronize());
@@ -1189,17 +1373,7 @@ int skb_cache_step(skb_cache* c, const void* q, const void* k, const void* v, co
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int B = (int)c->d.batch;
     const double* uu = u;
-    if (!uu) {  // k = 0: scores idle (proj/src/cache.cpp:219-227)
-        static thread_local double* zeros = nullptr;
-        static thread_local int nz = 0;
-        if (nz < B) {
-            if (zeros) cudaFree(zeros);
-            SKB_CHECK_CUDA(cudaMalloc(&zeros, B * sizeof(double)));
-            SKB_CHECK_CUDA(cudaMemset(zeros, 0, B * sizeof(double)));
-            nz = B;
-        }
-        uu = zeros;
-    }
+    if (!uu) uu = c->zeros;  // k = 0: scores idle (proj/src/cache.cpp:219-227)
     k_cache_control<<<(unsigned)cdiv(B, 4), 128, 0, st>>>(c->A, B, static_cast<const uint8_t*>(k),
                                                           static_cast<const uint8_t*>(v), uu);
     SKB_CHECK_LAUNCH();
@@ -1307,6 +1481,12 @@ struct Reader {
         uint8_t x;
         raw(&x, 1);
         return x;
+    }
+    // an element count, bounded by the bytes left (each element >= elem bytes)
+    uint64_t count(size_t elem) {
+        const uint64_t c = u64();
+        SKB_REQUIRE(c <= (n - off) / elem, SKB_EIO, "cache snapshot: truncated");
+        return c;
     }
 };
 
@@ -1536,7 +1716,7 @@ int skb_cache_restore(skb_cache* c, int64_t b, const uint8_t* data, size_t bytes
     if (has_stream != has_stream_cfg) throw skb::Error(SKB_EIO, "cache snapshot: stream mismatch");
     const long long t = (long long)r.u64();
     SKB_REQUIRE(t <= A.Lmax, SKB_ESHAPE, "cache_restore: snapshot longer than the cache's max positions");
-    const uint64_t ns = r.u64();
+    const uint64_t ns = r.count(8);
     SKB_REQUIRE(ns == (uint64_t)t, SKB_EIO, "cache snapshot: score count != positions");
     std::vector<double> u((size_t)t);
     for (auto& x : u) x = r.f64();
@@ -1564,12 +1744,12 @@ int skb_cache_restore(skb_cache* c, int64_t b, const uint8_t* data, size_t bytes
         cc.st.heap_ops = r.u64();
         cc.st.since_refresh = (int)r.u64();
         auto heap = [&](std::vector<std::pair<double, long long>>& h) {
-            const uint64_t n = r.u64();
-            SKB_REQUIRE(n <= bytes / 16, SKB_EIO, "cache snapshot: truncated");
+            const uint64_t n = r.count(16);
             h.resize(n);
             for (auto& e : h) {
                 e.first = r.f64();
                 e.second = (long long)r.u64();
+                SKB_REQUIRE(e.second >= 0 && e.second < t, SKB_EIO, "cache snapshot: stream entry out of range");
             }
             std::sort(h.begin(), h.end(), [](const auto& a, const auto& b2) {  // device: (value desc, index asc)
                 return a.first > b2.first || (a.first == b2.first && a.second < b2.second);
@@ -1578,21 +1758,22 @@ int skb_cache_restore(skb_cache* c, int64_t b, const uint8_t* data, size_t bytes
         heap(hs);
         heap(hf);
         const uint64_t nb = r.u64();
+        SKB_REQUIRE(nb <= 8 * (uint64_t)(bytes - r.off), SKB_EIO, "cache snapshot: truncated");
         for (uint64_t i = 0; i < nb; i += 8) (void)r.u8();
         SKB_REQUIRE(r.off == end, SKB_EIO, "cache snapshot: stream blob length mismatch");
         cc.st.nS = (int)hs.size();
         cc.st.nF = (int)hf.size();
     }
-    std::vector<long long> ring(r.u64());
+    std::vector<long long> ring(r.count(8));
     for (auto& x : ring) x = (long long)r.u64();
     SnapBase sb;
     sb.t0 = t;
-    sb.heap.resize(r.u64());
+    sb.heap.resize(r.count(16));
     for (auto& e : sb.heap) {
         e.first = r.f64();
         e.second = (long long)r.u64();
     }
-    sb.cache_pos.resize(r.u64());
+    sb.cache_pos.resize(r.count(8));
     for (auto& x : sb.cache_pos) x = (long long)r.u64();
     const uint64_t nkv = r.u64();
     SKB_REQUIRE(nkv == ring.size() + sb.cache_pos.size() && nkv <= (uint64_t)A.S, SKB_EIO,
@@ -1609,12 +1790,13 @@ int skb_cache_restore(skb_cache* c, int64_t b, const uint8_t* data, size_t bytes
         pos_of[i] = (int)ppos;
     }
     const uint64_t nbits = r.u64();
+    SKB_REQUIRE(nbits <= 8 * (uint64_t)(bytes - r.off), SKB_EIO, "cache snapshot: truncated");
     sb.evicted.assign(nbits, 0);
     for (uint64_t i = 0; i < nbits; i += 8) {
         const uint8_t byte = r.u8();
         for (uint64_t q = 0; q < 8 && i + q < nbits; ++q) sb.evicted[i + q] = (byte >> q) & 1u;
     }
-    sb.pending.resize(r.u64());
+    sb.pending.resize(r.count(8));
     for (auto& x : sb.pending) x = (long long)r.u64();
     cc.peak = (long long)r.u64();
     SKB_REQUIRE(r.off == bytes, SKB_EIO, "cache snapshot: trailing bytes");
@@ -1625,6 +1807,26 @@ int skb_cache_restore(skb_cache* c, int64_t b, const uint8_t* data, size_t bytes
                     "cache snapshot: window ring does not hold the last w positions");
     // the retained cache positions must be the stream's top floor(k) survivors
     SKB_REQUIRE(sb.cache_pos.size() <= (size_t)A.cap, SKB_EIO, "cache snapshot: cache larger than floor(k)");
+    // the device attends slot_of[survivor] for the first nsel survivors: each
+    // must be a stored row, and together they must be exactly cache_pos
+    // (the reference throws NumericError on an attended position with no row)
+    SKB_REQUIRE(hs.size() >= sb.cache_pos.size(), SKB_EIO, "cache snapshot: fewer survivors than cached rows");
+    {
+        std::vector<long long> head;
+        for (size_t i = 0; i < sb.cache_pos.size(); ++i) {
+            const long long pp = hs[i].second;
+            SKB_REQUIRE(pp >= 0 && pp < t && slot_of[(size_t)pp] >= 0, SKB_ENUMERIC,
+                        "attended position has no stored row");
+            head.push_back(pp);
+        }
+        std::sort(head.begin(), head.end());
+        std::vector<long long> cp(sb.cache_pos);
+        std::sort(cp.begin(), cp.end());
+        SKB_REQUIRE(head == cp, SKB_EIO, "cache snapshot: cached positions are not the stream's top floor(k)");
+        for (long long pp : ring)
+            SKB_REQUIRE(pp >= 0 && pp < t && slot_of[(size_t)pp] >= 0, SKB_ENUMERIC,
+                        "attended position has no stored row");
+    }
     cc.t = t;
     cc.nsel = (int)sb.cache_pos.size();
     cc.free_top = A.S - (int)nkv;

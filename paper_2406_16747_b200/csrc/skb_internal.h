@@ -31,6 +31,16 @@ inline int num_sms() {
     if (!cached[dev]) cudaDeviceGetAttribute(&cached[dev], cudaDevAttrMultiProcessorCount, dev);
     return cached[dev] > 0 ? cached[dev] : 148;
 }
+// Function attributes (dynamic shared memory above 48 KB) are per device
+// context: true the first time a call site runs on the current device.
+inline bool first_on_device(uint64_t* seen) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t bit = 1ull << (dev & 63);
+    if (*seen & bit) return false;
+    *seen |= bit;
+    return true;
+}
 void validate_desc(const skb_attn_desc& d);
 void select_layout(const skb_attn_desc& d, skb_select_layout& o);
 void run_select(const skb_attn_desc& d, const double* u, void* ws, cudaStream_t st);
@@ -54,7 +64,7 @@ struct SelView {
 SelView sel_view(const skb_attn_desc& d, const void* ws);
 
 struct BwdLayout {
-    uint64_t rowsum, colsum, mean_prefix, dk_acc, dv_acc, dq_acc, sel_items, sel_order, total;
+    uint64_t rowsum, colsum, mean_prefix, chunk_sums, dk_acc, dv_acc, dq_acc, sel_items, sel_order, total;
 };
 void bwd_layout(const skb_attn_desc& d, BwdLayout& o);
 
@@ -75,6 +85,6 @@ void run_attn_bwd_tc(const skb_attn_desc& d, const void* q, const void* k, const
                      double* colsum, void* ws, const BwdLayout& bl, cudaStream_t st);
 // du from the gate-gradient row/column sums (selection pullback).
 void run_jvp(const skb_attn_desc& d, const double* u, const SelView& s, const double* rowsum,
-             const double* colsum, double* mean_prefix, double* du, cudaStream_t st);
+             const double* colsum, double* mean_prefix, double* chunk_sums, double* du, cudaStream_t st);
 
 }  // namespace skb

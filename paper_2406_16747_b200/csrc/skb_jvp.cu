@@ -17,12 +17,35 @@ namespace skb {
 
 namespace {
 
+__device__ __forceinline__ double mean_at(const double* rs, const int* nf, const double* tb, int t) {
+    const int n = nf[t];
+    return (n > 0 && tb[t] > -INFINITY) ? rs[t] / (double)n : 0.0;
+}
+
+// Sum of mean_t over every 1024-push chunk (the first level of k_mean_prefix).
+__global__ void __launch_bounds__(1024)
+k_mean_chunk_sums(const double* __restrict__ rowsum, const int* __restrict__ nfrac,
+                  const double* __restrict__ tau, int L, int T, double* __restrict__ csum) {
+    __shared__ double wsum[32];
+    const int b = blockIdx.y, t = blockIdx.x * 1024 + threadIdx.x;
+    const int64_t bl = (int64_t)b * L;
+    double s = warp_sum(t < T ? mean_at(rowsum + bl, nfrac + bl, tau + bl, t) : 0.0);
+    if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double tot = 0.0;
+        for (int w = 0; w < 32; ++w) tot += wsum[w];
+        csum[(int64_t)b * gridDim.x + blockIdx.x] = tot;
+    }
+}
+
 // M[t] = sum_{t' < t} mean_t' per sequence (M[T] = total): one CTA per 1024
-// push times; each reduces the means before its chunk itself (all loads in
-// flight) and scans its chunk, so no CTA waits on another.
+// push times; each adds the chunk sums before it (O(T / 1024) loads) and
+// scans its chunk, so no CTA waits on another.
 __global__ void __launch_bounds__(1024)
 k_mean_prefix(const double* __restrict__ rowsum, const int* __restrict__ nfrac,
-              const double* __restrict__ tau, int L, int T, double* __restrict__ M) {
+              const double* __restrict__ tau, int L, int T, const double* __restrict__ csum,
+              double* __restrict__ M) {
     __shared__ double wsum[32];
     const int b = blockIdx.y, c0 = blockIdx.x * 1024;
     const double* rs = rowsum + (int64_t)b * L;
@@ -30,18 +53,9 @@ k_mean_prefix(const double* __restrict__ rowsum, const int* __restrict__ nfrac,
     const double* tb = tau + (int64_t)b * L;
     double* Mb = M + (int64_t)b * (L + 1);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    auto mean_at = [&](int t) {
-        const int n = nf[t];
-        return (n > 0 && tb[t] > -INFINITY) ? rs[t] / (double)n : 0.0;
-    };
+    const double* cs = csum + (int64_t)b * gridDim.x;
     double pre = 0.0;
-    for (int j0 = threadIdx.x; j0 < c0; j0 += 4 * 1024) {
-        double x[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) x[q] = j0 + q * 1024 < c0 ? mean_at(j0 + q * 1024) : 0.0;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) pre += x[q];
-    }
+    for (int c = threadIdx.x; c < (int)blockIdx.x; c += 1024) pre += cs[c];
     pre = warp_sum(pre);
     if (lane == 0) wsum[wid] = pre;
     __syncthreads();
@@ -49,7 +63,7 @@ k_mean_prefix(const double* __restrict__ rowsum, const int* __restrict__ nfrac,
     for (int w = 0; w < 32; ++w) before += wsum[w];
     __syncthreads();
     const int t = c0 + threadIdx.x;
-    const double x = t < T ? mean_at(t) : 0.0;
+    const double x = t < T ? mean_at(rs, nf, tb, t) : 0.0;
     double incl = x;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -116,6 +130,7 @@ void bwd_layout(const skb_attn_desc& d, BwdLayout& o) {
     o.rowsum = take(BL * 8);
     o.colsum = take(BL * 8);
     o.mean_prefix = take((BL + d.batch) * 8);
+    o.chunk_sums = take((uint64_t)d.batch * ((d.seq_len + 1023) / 1024) * 8);
     const bool tc = d.dtype == SKB_BF16 && tc_supported(d) && !(d.flags & SKB_FLAG_FORCE_GATHER);
     // gather backward: fp64 dK/dV accumulators; tensor-core backward: fp32
     // partials of the selected pass + lse2/delta rows in the dq_acc region
@@ -132,15 +147,16 @@ void bwd_layout(const skb_attn_desc& d, BwdLayout& o) {
 }
 
 void run_jvp(const skb_attn_desc& d, const double* u, const SelView& s, const double* rowsum,
-             const double* colsum, double* mean_prefix, double* du, cudaStream_t st) {
+             const double* colsum, double* mean_prefix, double* chunk_sums, double* du, cudaStream_t st) {
     const int B = (int)d.batch, L = (int)d.seq_len;
     const int T = std::max(0, L - (int)d.window);
     if (floor_k(d.k) < 1 || T == 0) {
         SKB_CHECK_CUDA(cudaMemsetAsync(du, 0, (size_t)B * L * sizeof(double), st));
         return;
     }
-    k_mean_prefix<<<dim3((unsigned)std::max<int64_t>(1, cdiv(T, 1024)), (unsigned)B), 1024, 0, st>>>(
-        rowsum, s.nfrac, s.tau, L, T, mean_prefix);
+    const dim3 gc((unsigned)std::max<int64_t>(1, cdiv(T, 1024)), (unsigned)B);
+    k_mean_chunk_sums<<<gc, 1024, 0, st>>>(rowsum, s.nfrac, s.tau, L, T, chunk_sums);
+    k_mean_prefix<<<gc, 1024, 0, st>>>(rowsum, s.nfrac, s.tau, L, T, chunk_sums, mean_prefix);
     SKB_CHECK_LAUNCH();
     dim3 g((unsigned)cdiv(L, 256), B);
     k_jvp<<<g, 256, 0, st>>>(u, s.tau, colsum, mean_prefix, L, T, (int)d.window, (int)d.chunk_len, du);

@@ -147,11 +147,10 @@ void launch_rows(OpArgs a, int64_t n, cudaStream_t st) {
     double* scratch = nullptr;
     if (a.n2 <= kSmemCap) {
         smem = (size_t)(a.n2 + a.m + 1) * sizeof(double);
-        static bool attr = false;
-        if (!attr) {
+        static uint64_t attr = 0;
+        if (first_on_device(&attr)) {
             SKB_CHECK_CUDA(cudaFuncSetAttribute(k_sparsek_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                 (int)((2 * kSmemCap + 1) * sizeof(double))));
-            attr = true;
         }
     } else {
         SKB_CHECK_CUDA(cudaMallocAsync(&scratch, (size_t)n * (a.n2 + a.m + 1) * sizeof(double), st));

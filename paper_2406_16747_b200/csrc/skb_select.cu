@@ -666,27 +666,31 @@ k_union_lists(const int* __restrict__ leave1, int L, int T, int window, int nqb,
     if (threadIdx.x == 0) qb_count[(int64_t)b * nqb + qb] = min(base, cap);
 }
 
-// Ever-selected keys per sequence, ascending: one CTA per 1024 keys; each
-// counts the kept keys before its chunk itself (all loads in flight) and
-// compacts its chunk, so no CTA waits on another.
+// Kept-key count of every 1024-key chunk (the first level of k_ever_list's scan).
 __global__ void __launch_bounds__(1024)
-k_ever_list(const int* __restrict__ leave1, int L, int T, int* __restrict__ ever_count,
-            int* __restrict__ ever_list) {
+k_ever_chunk_counts(const int* __restrict__ leave1, int L, int T, int* __restrict__ cnt) {
+    __shared__ int wsum[32];
+    const int b = blockIdx.y, j = blockIdx.x * 1024 + threadIdx.x;
+    const int* lv = leave1 + (int64_t)b * L;
+    const int c = __syncthreads_count(j < T && lv[j] > j);
+    if (threadIdx.x == 0) cnt[(int64_t)b * gridDim.x + blockIdx.x] = c;
+    (void)wsum;
+}
+
+// Ever-selected keys per sequence, ascending: one CTA per 1024 keys; each
+// adds the chunk counts before it (k_ever_chunk_counts: O(T / 1024) loads,
+// so the whole scan is O(T + (T / 1024)^2)) and compacts its chunk.
+__global__ void __launch_bounds__(1024)
+k_ever_list(const int* __restrict__ leave1, int L, int T, const int* __restrict__ chunk_cnt,
+            int* __restrict__ ever_count, int* __restrict__ ever_list) {
     __shared__ int wsum[32];
     const int b = blockIdx.y, c0 = blockIdx.x * 1024;
     const int* lv = leave1 + (int64_t)b * L;
     int* out = ever_list + (int64_t)b * L;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int* cc = chunk_cnt + (int64_t)b * gridDim.x;
     int pre = 0;
-    for (int j0 = threadIdx.x; j0 < c0; j0 += 4 * 1024) {
-        int x[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int j = j0 + q * 1024;
-            x[q] = j < c0 ? (lv[j] > j) : 0;
-        }
-        pre += x[0] + x[1] + x[2] + x[3];
-    }
+    for (int c = threadIdx.x; c < (int)blockIdx.x; c += 1024) pre += cc[c];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) pre += __shfl_xor_sync(0xffffffffu, pre, o);
     if (lane == 0) wsum[wid] = pre;
@@ -778,23 +782,33 @@ __global__ void k_fill_tau(double* tau, int* nfrac, int64_t n) {
     }
 }
 
+// Maximum of every 1024-push chunk (the first level of k_tau_monotone_chunks).
+__global__ void __launch_bounds__(1024) k_tau_chunk_max(const double* __restrict__ tau_in, int L, int T,
+                                                        double* __restrict__ cmax) {
+    __shared__ double wmax[32];
+    const int b = blockIdx.y, t = blockIdx.x * 1024 + threadIdx.x;
+    double m = warp_max(t < T ? tau_in[(int64_t)b * L + t] : -CUDART_INF);
+    if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < 32; ++w) m = fmax(m, wmax[w]);
+        cmax[(int64_t)b * gridDim.x + blockIdx.x] = fmax(m, wmax[0]);
+    }
+}
+
 // The same running maximum with one CTA per 1024 push times: each CTA reduces
-// the prefix before its chunk itself (<= T loads, all in flight) and scans its
-// chunk, so no CTA waits on another. Reads tau_in, writes tau_out (distinct).
+// the chunk maxima before it (O(T / 1024) loads) and scans its chunk, so no
+// CTA waits on another. Reads tau_in, writes tau_out (distinct).
 __global__ void __launch_bounds__(1024) k_tau_monotone_chunks(const double* __restrict__ tau_in,
-                                                              double* __restrict__ tau_out, int L, int T) {
+                                                              double* __restrict__ tau_out, int L, int T,
+                                                              const double* __restrict__ cmax) {
     __shared__ double wmax[32];
     const int b = blockIdx.y, c0 = blockIdx.x * 1024;
     const double* ti = tau_in + (int64_t)b * L;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const double* cm = cmax + (int64_t)b * gridDim.x;
     double pre = -CUDART_INF;
-    for (int j0 = threadIdx.x; j0 < c0; j0 += 4 * 1024) {
-        double x[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) x[q] = j0 + q * 1024 < c0 ? ti[j0 + q * 1024] : -CUDART_INF;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) pre = fmax(pre, x[q]);
-    }
+    for (int c = threadIdx.x; c < (int)blockIdx.x; c += 1024) pre = fmax(pre, cm[c]);
     pre = warp_max(pre);
     if (lane == 0) wmax[wid] = pre;
     __syncthreads();
@@ -888,7 +902,9 @@ void select_layout(const skb_attn_desc& d, skb_select_layout& o) {
     o.misc = take((2 + 3 * B * nch) * 4);  // two overflow queues [count, items...] + pass-1 flags
     const int64_t cap2 = next_pow2((int)std::max<int64_t>(L, 1));
     // the overflow pass's global bands; afterwards the running-max staging of tau [B, L]
-    o.scratch = take(std::max<uint64_t>((uint64_t)kOverflowSlots * (cap2 + L + 1), (uint64_t)B * L) * 8);
+    // (+ per-1024 chunk aggregates of the two-level scans after the staging area)
+    o.scratch = take(std::max<uint64_t>((uint64_t)kOverflowSlots * (cap2 + L + 1),
+                                        (uint64_t)B * L + (uint64_t)B * cdiv(L, 1024)) * 8);
     o.uf = take(B * L * 4);
     o.tauf = take(B * L * 4);
     o.qb_leave = take(B * nqb * cap * 4);
@@ -983,8 +999,8 @@ void run_select(const skb_attn_desc& d, const double* u, void* ws, cudaStream_t 
         const int cap2 = next_pow2(std::max(L, 1));
         a.scratch = scratch;
         a.scratch_stride = cap2 + L + 1;
-        static bool attr_set = false;
-        if (!attr_set) {
+        static uint64_t attr_set = 0;
+        if (first_on_device(&attr_set)) {
             SKB_CHECK_CUDA(cudaFuncSetAttribute(k_tau_chunks, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                 (int)(8192 * 2 * sizeof(double) + 8 + 16)));  // bz + P[cap + 1]
             SKB_CHECK_CUDA(cudaFuncSetAttribute(k_tau_chunks_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -993,7 +1009,6 @@ void run_select(const skb_attn_desc& d, const double* u, void* ws, cudaStream_t 
                                                 (int)(8192 * 3 * sizeof(double) + 16)));
             SKB_CHECK_CUDA(cudaFuncSetAttribute(k_tau_segments<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                 (int)(8192 * 3 * sizeof(double) + 16)));
-            attr_set = true;
         }
         static const int p1seg = getenv("SKB_TAU_P1SEG") ? atoi(getenv("SKB_TAU_P1SEG")) : 0;  // per-chunk pass 1 measured faster
         if (p1seg > 0) {
@@ -1023,7 +1038,10 @@ void run_select(const skb_attn_desc& d, const double* u, void* ws, cudaStream_t 
         // running max into the uf/tauf scratch (rewritten by k_to_float below), then back
         {
             double* tmp = reinterpret_cast<double*>(base + lay.scratch);
-            k_tau_monotone_chunks<<<dim3((unsigned)cdiv(T, 1024), (unsigned)B), 1024, 0, st>>>(tau, tmp, L, T);
+            double* cmax = tmp + BL;
+            const dim3 gc((unsigned)cdiv(T, 1024), (unsigned)B);
+            k_tau_chunk_max<<<gc, 1024, 0, st>>>(tau, L, T, cmax);
+            k_tau_monotone_chunks<<<gc, 1024, 0, st>>>(tau, tmp, L, T, cmax);
             SKB_CHECK_LAUNCH();
             SKB_CHECK_CUDA(cudaMemcpy2DAsync(tau, (size_t)L * 8, tmp, (size_t)L * 8, (size_t)T * 8, B,
                                              cudaMemcpyDeviceToDevice, st));
@@ -1036,8 +1054,12 @@ void run_select(const skb_attn_desc& d, const double* u, void* ws, cudaStream_t 
     if (R1 > 0 && T > 0) {
         dim3 g(nqb, B);
         k_union_lists<<<g, 512, 0, st>>>(leave1, L, T, w, nqb, (int)lay.qb_cap, qb_count, qb_list);
-        k_ever_list<<<dim3((unsigned)cdiv(T, 1024), (unsigned)B), 1024, 0, st>>>(leave1, L, T, ever_count,
-                                                                                   ever_list);
+        {
+            int* ccnt = reinterpret_cast<int*>(reinterpret_cast<double*>(base + lay.scratch) + BL);
+            const dim3 gc((unsigned)cdiv(T, 1024), (unsigned)B);
+            k_ever_chunk_counts<<<gc, 1024, 0, st>>>(leave1, L, T, ccnt);
+            k_ever_list<<<gc, 1024, 0, st>>>(leave1, L, T, ccnt, ever_count, ever_list);
+        }
         SKB_CHECK_LAUNCH();
         k_union_meta<<<g, 128, 0, st>>>(leave1, reinterpret_cast<const float*>(base + lay.uf),
                                         reinterpret_cast<const float*>(base + lay.tauf), L, T, w, nqb,

@@ -26,6 +26,22 @@ def _stream():
     return torch.cuda.current_stream().cuda_stream
 
 
+def _on_device(fn):
+    """Run `fn` with its first CUDA tensor argument's device current, so the
+    launches and torch's current stream both belong to that device."""
+    import functools
+
+    @functools.wraps(fn)
+    def wrapped(*args, **kw):
+        for a in list(args) + list(kw.values()):
+            if isinstance(a, torch.Tensor) and a.is_cuda:
+                with torch.cuda.device(a.device):
+                    return fn(*args, **kw)
+        return fn(*args, **kw)
+
+    return wrapped
+
+
 @dataclass(frozen=True)
 class AttnConfig:
     """AttnConfig (proj/include/sparsek/attention.hpp:18-32) at the core level."""
@@ -118,6 +134,15 @@ class Selection:
         return out
 
 
+def _scores(u, B, L, device):
+    """u as a contiguous float64 [B, L] tensor on `device` (the kernels read it raw)."""
+    if u.shape != (B, L):
+        raise _lib.ShapeError("u must be [B, L]")
+    if u.dtype != torch.float64 or u.device != device:
+        raise _lib.ArgumentError("u must be a float64 tensor on the q/k/v device")
+    return u.contiguous()
+
+
 def select(u: torch.Tensor, cfg: AttnConfig, heads=1, head_dim=1, dtype=torch.float32,
            desc: AttnDesc | None = None) -> Selection:
     """K2: prefix tau and top-floor(k) retention intervals for u [B, L] float64."""
@@ -129,8 +154,9 @@ def select(u: torch.Tensor, cfg: AttnConfig, heads=1, head_dim=1, dtype=torch.fl
         desc = make_desc(B, L, heads, head_dim, cfg, dtype)
     lay = SelectLayout()
     check(_lib.load().skb_select_layout_of(desc, lay))
-    ws = torch.empty(lay.total_bytes, dtype=torch.uint8, device=u.device)
-    check(_lib.load().skb_select(desc, u.data_ptr(), ws.data_ptr(), _stream()))
+    with torch.cuda.device(u.device):
+        ws = torch.empty(lay.total_bytes, dtype=torch.uint8, device=u.device)
+        check(_lib.load().skb_select(desc, u.data_ptr(), ws.data_ptr(), _stream()))
     return Selection(desc, ws, lay)
 
 
@@ -138,16 +164,15 @@ def attn_fwd(q, k, v, u, cfg: AttnConfig, sel: Selection | None = None):
     """K3. Returns (o [B,L,H,p], lse float64 [B,H,L], selection)."""
     _check_qkv(q, k, v)
     B, L, H, p = q.shape
-    if u.shape != (B, L):
-        raise _lib.ShapeError("u must be [B, L]")
+    u = _scores(u, B, L, q.device)
     desc = make_desc(B, L, H, p, cfg, q.dtype)
-    u = u.contiguous()
-    if sel is None:
-        sel = select(u, cfg, desc=desc)
-    o = torch.empty_like(q)
-    lse = torch.empty((B, H, L), dtype=torch.float64, device=q.device)
-    check(_lib.load().skb_attn_fwd(desc, q.data_ptr(), k.data_ptr(), v.data_ptr(), u.data_ptr(),
-                                   sel.ws.data_ptr(), o.data_ptr(), lse.data_ptr(), _stream()))
+    with torch.cuda.device(q.device):
+        if sel is None:
+            sel = select(u, cfg, desc=desc)
+        o = torch.empty_like(q)
+        lse = torch.empty((B, H, L), dtype=torch.float64, device=q.device)
+        check(_lib.load().skb_attn_fwd(desc, q.data_ptr(), k.data_ptr(), v.data_ptr(), u.data_ptr(),
+                                       sel.ws.data_ptr(), o.data_ptr(), lse.data_ptr(), _stream()))
     return o, lse, sel
 
 
@@ -155,20 +180,26 @@ def attn_bwd(q, k, v, o, do, lse, u, sel: Selection, cfg: AttnConfig, ws=None):
     """K4 + selection pullback. Returns (dq, dk, dv, du float64 [B, L])."""
     _check_qkv(q, k, v)
     B, L, H, p = q.shape
+    u = _scores(u, B, L, q.device)
+    if lse.shape != (B, H, L) or lse.dtype != torch.float64 or not lse.is_contiguous():
+        raise _lib.ArgumentError("attn_bwd: lse must be a contiguous float64 [B, H, L] tensor")
+    if o is not None and (o.shape != q.shape or o.dtype != q.dtype or not o.is_contiguous()):
+        raise _lib.ArgumentError("attn_bwd: o must be contiguous with q's shape and dtype")
     desc = make_desc(B, L, H, p, cfg, q.dtype)
     do = do.contiguous()
     if do.dtype != q.dtype:
         do = do.to(q.dtype)
     lib = _lib.load()
-    if ws is None:
-        n = C_size()
-        check(lib.skb_attn_bwd_workspace_size(desc, n))
-        ws = torch.empty(n.value, dtype=torch.uint8, device=q.device)
-    dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
-    du = torch.empty((B, L), dtype=torch.float64, device=q.device)
-    check(lib.skb_attn_bwd(desc, q.data_ptr(), k.data_ptr(), v.data_ptr(), _ptr(o), do.data_ptr(),
-                           lse.data_ptr(), u.data_ptr(), sel.ws.data_ptr(), dq.data_ptr(),
-                           dk.data_ptr(), dv.data_ptr(), du.data_ptr(), ws.data_ptr(), _stream()))
+    with torch.cuda.device(q.device):
+        if ws is None:
+            n = C_size()
+            check(lib.skb_attn_bwd_workspace_size(desc, n))
+            ws = torch.empty(n.value, dtype=torch.uint8, device=q.device)
+        dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+        du = torch.empty((B, L), dtype=torch.float64, device=q.device)
+        check(lib.skb_attn_bwd(desc, q.data_ptr(), k.data_ptr(), v.data_ptr(), _ptr(o), do.data_ptr(),
+                               lse.data_ptr(), u.data_ptr(), sel.ws.data_ptr(), dq.data_ptr(),
+                               dk.data_ptr(), dv.data_ptr(), du.data_ptr(), ws.data_ptr(), _stream()))
     return dq, dk, dv, du
 
 
@@ -191,7 +222,7 @@ class SparseKAttentionFn(torch.autograd.Function):
 
     @staticmethod
     def forward(ctx, q, k, v, u, cfg: AttnConfig):
-        q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
+        q, k, v, u = q.contiguous(), k.contiguous(), v.contiguous(), u.contiguous()
         o, lse, sel = attn_fwd(q, k, v, u, cfg)
         ctx.save_for_backward(q, k, v, o, lse, u)
         ctx.sel, ctx.cfg = sel, cfg
@@ -225,6 +256,7 @@ class ScoringConfig:
                        int(self.chunk_len), float(self.slope_eps))
 
 
+@_on_device
 def score_fwd(x: torch.Tensor, w: torch.Tensor, sc: ScoringConfig):
     """x [B, L, D] -> (raw, u, mean, sdev) float64 [B, L]."""
     if x.dim() != 3:
@@ -242,6 +274,7 @@ def score_fwd(x: torch.Tensor, w: torch.Tensor, sc: ScoringConfig):
     return raw, u, mean, sdev
 
 
+@_on_device
 def score_continue(x: torch.Tensor, w: torch.Tensor, sc: ScoringConfig, state: torch.Tensor):
     """Incremental scoring (score_tokens with a carried TimestepNormState,
     proj/src/selection.cpp:22-31): x [B, n, D] continues ``state`` (float64
@@ -262,6 +295,7 @@ def score_continue(x: torch.Tensor, w: torch.Tensor, sc: ScoringConfig, state: t
     return raw, u
 
 
+@_on_device
 def score_bwd(x, w, sc: ScoringConfig, gu, raw, mean, sdev, dx=None, want_dw=True):
     B, L, D = x.shape
     graw = torch.empty((B, L), dtype=torch.float64, device=x.device)
@@ -295,6 +329,7 @@ def score_tokens(x, w, sc: ScoringConfig):
 
 # ---------------------------------------------------------------- operator
 
+@_on_device
 def sparsek_rows(z: torch.Tensor, k: float):
     """Batched SparseK projection of the rows of z [n, m] (float64, CUDA)."""
     if z.dim() != 2 or z.dtype != torch.float64 or not z.is_cuda:
@@ -311,6 +346,7 @@ def sparsek_rows(z: torch.Tensor, k: float):
     return p, tau, uc, wc, fl
 
 
+@_on_device
 def sparsek_jvp_rows(z: torch.Tensor, k: float, v: torch.Tensor):
     z = z.contiguous()
     v = v.to(torch.float64).contiguous()
@@ -321,6 +357,7 @@ def sparsek_jvp_rows(z: torch.Tensor, k: float, v: torch.Tensor):
     return out
 
 
+@_on_device
 def topk_hard_rows(z: torch.Tensor, k: int):
     z = z.contiguous()
     n, m = z.shape
@@ -330,6 +367,17 @@ def topk_hard_rows(z: torch.Tensor, k: int):
 
 
 # ---------------------------------------------------------------- decode (K5)
+
+def _cache_dev(fn):
+    import functools
+
+    @functools.wraps(fn)
+    def wrapped(self, *a, **kw):
+        with torch.cuda.device(self.device):
+            return fn(self, *a, **kw)
+
+    return wrapped
+
 
 class DecodeCache:
     """Constant-(floor(k)+w) KV cache for generation over skb_cache_*:
@@ -368,6 +416,7 @@ class DecodeCache:
             raise _lib.ArgumentError(f"cache: {name} must be a CUDA {dtype} tensor")
         return t.contiguous()
 
+    @_cache_dev
     def step(self, q, k, v, u, out=None):
         shp = (self.B, self.H, self.p)
         q, k, v = (self._chk(t, shp, self.dtype, n) for t, n in ((q, "q"), (k, "k"), (v, "v")))
@@ -377,6 +426,7 @@ class DecodeCache:
                                          u.data_ptr(), o.data_ptr(), _stream()))
         return o
 
+    @_cache_dev
     def prefill(self, k, v, u):
         n = k.shape[1]
         shp = (self.B, n, self.H, self.p)
@@ -385,6 +435,7 @@ class DecodeCache:
         check(_lib.load().skb_cache_prefill(self._h, k.data_ptr(), v.data_ptr(), u.data_ptr(), n,
                                             _stream()))
 
+    @_cache_dev
     def snapshot(self, b=0, norm_state=None):
         """SparseKvCache::serialize payload of sequence b (proj/src/cache.cpp:416-475);
         norm_state = (count, mean, m2) of the scoring that fed this cache."""
@@ -397,6 +448,7 @@ class DecodeCache:
         check(_lib.load().skb_cache_snapshot(self._h, int(b), ns, buf, ctypes.byref(n), _stream()))
         return bytes(buf[: n.value])
 
+    @_cache_dev
     def restore(self, blob, b=0):
         """SparseKvCache::deserialize (proj/src/cache.cpp:477-545) into sequence b;
         returns the snapshot's norm state (count, mean, m2)."""
@@ -407,6 +459,7 @@ class DecodeCache:
         check(_lib.load().skb_cache_restore(self._h, int(b), buf, len(blob), ns, _stream()))
         return tuple(ns)
 
+    @_cache_dev
     def state(self, b=0):
         """{positions (selected asc, then window asc), tau, seen, peak}."""
         import ctypes

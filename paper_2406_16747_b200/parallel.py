@@ -71,7 +71,7 @@ class HeadParallelSparseK(torch.autograd.Function):
     def forward(ctx, q, k, v, u, cfg, group=None):
         from . import ops
 
-        q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
+        q, k, v, u = q.contiguous(), k.contiguous(), v.contiguous(), u.contiguous()
         o, lse, sel = ops.attn_fwd(q, k, v, u, cfg)
         ctx.save_for_backward(q, k, v, o, lse, u)
         ctx.sel, ctx.cfg, ctx.group = sel, cfg, group

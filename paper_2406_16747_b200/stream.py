@@ -1,6 +1,11 @@
 """Device-resident incremental SparseK stream: the reference's ``Stream``
 (StreamState, proj/include/sparsek/stream.hpp:26-72; pybind surface
-proj/bindings/module.cpp:101-128) over skb_stream_* (include/sparsek_b200.h)."""
+proj/bindings/module.cpp:101-128) over skb_stream_* (include/sparsek_b200.h).
+
+Each ``push`` is one kernel and one device round trip (skb_stream_push_step
+returns tau, t, inserted and the survivors popped by that push);
+``solution``/``mask`` are computed on the device (skb_stream_solution).
+Batches of scores go through ``push_many`` (one launch for n pushes)."""
 from __future__ import annotations
 
 import ctypes as C
@@ -11,6 +16,24 @@ import torch
 
 from . import _lib
 from ._lib import ArgumentError, NumericError, check
+
+
+def _st():
+    return torch.cuda.current_stream().cuda_stream
+
+
+class SelectionMask:
+    """SelectionMask (proj/include/sparsek/selection.hpp:43-49) over the survivors
+    of a stream (stream_mask, proj/src/stream.cpp:199-222): ``hard`` = the
+    top-floor(k) indicator, ``soft`` = the SparseK weights, ``indices`` = the
+    positions of the hard set (ascending); hard/soft follow ``positions``."""
+
+    def __init__(self, positions, hard, soft):
+        self.positions = positions
+        self.hard = hard
+        self.soft = soft
+        self.indices = positions[hard == 1.0]
+        self.mode = "soft"
 
 
 class Stream:
@@ -25,9 +48,13 @@ class Stream:
         self._cap = int(capacity)
         self._h = C.c_void_p()
         check(_lib.load().skb_stream_create(k, int(heap_cap), self._cap, C.byref(self._h)))
+        self._init_common()
+
+    def _init_common(self):
         self._dev = torch.device("cuda", torch.cuda.current_device())
-        self._tau = torch.empty(1, dtype=torch.float64, device=self._dev)
-        self._ins = torch.empty(1, dtype=torch.uint8, device=self._dev)
+        # room for every index one push can evict (at most the capacity)
+        self._ev = (C.c_int64 * self._cap)()
+        self._step = _lib.StreamStep()
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -42,10 +69,9 @@ class Stream:
         proj/src/stream.cpp:224-252): readable by StreamState::deserialize."""
         n = C.c_size_t()
         lib = _lib.load()
-        st = torch.cuda.current_stream().cuda_stream
-        check(lib.skb_stream_serialize(self._h, None, C.byref(n), st))
+        check(lib.skb_stream_serialize(self._h, None, C.byref(n), _st()))
         buf = (C.c_uint8 * n.value)()
-        check(lib.skb_stream_serialize(self._h, buf, C.byref(n), st))
+        check(lib.skb_stream_serialize(self._h, buf, C.byref(n), _st()))
         return bytes(buf)[: n.value]
 
     @classmethod
@@ -56,65 +82,69 @@ class Stream:
         self._h = C.c_void_p()
         buf = (C.c_uint8 * len(blob)).from_buffer_copy(blob)
         check(_lib.load().skb_stream_deserialize(buf, len(blob), self._cap, C.byref(self._h)))
+        self._init_common()
         self._k = self._info().k
-        self._dev = torch.device("cuda", torch.cuda.current_device())
-        self._tau = torch.empty(1, dtype=torch.float64, device=self._dev)
-        self._ins = torch.empty(1, dtype=torch.uint8, device=self._dev)
         return self
 
     def _info(self):
         info = _lib.StreamInfo()
-        check(_lib.load().skb_stream_query(self._h, C.byref(info),
-                                            torch.cuda.current_stream().cuda_stream))
+        check(_lib.load().skb_stream_query(self._h, C.byref(info), _st()))
         return info
 
     def push(self, z):
+        """StreamState::push (proj/src/stream.cpp:72-152) -> {tau, t, inserted,
+        evicted}; ``evicted`` lists the survivors this push removed."""
         z = float(z)
         if not math.isfinite(z):
             raise NumericError("stream_push: non-finite value")
-        zt = torch.tensor([z], dtype=torch.float64, device=self._dev)
-        before = self._info()
-        check(_lib.load().skb_stream_push(self._h, zt.data_ptr(), 1, self._tau.data_ptr(),
-                                           self._ins.data_ptr(),
-                                           torch.cuda.current_stream().cuda_stream))
-        tau = float(self._tau.item())
-        inserted = bool(self._ins.item())
-        _, _, ev = self._survivors()
-        prev = getattr(self, "_ev_prev", np.zeros(0, bool))
-        new = ev.copy()
-        new[: len(prev)] &= ~prev
-        if not inserted:  # a rejected arrival is flagged but not reported (stream.cpp:83-88)
-            new[before.t] = False
-        self._ev_prev = ev
-        return {"tau": tau if math.isfinite(tau) else None, "t": before.t + 1,
-                "inserted": inserted, "evicted": [int(i) for i in np.nonzero(new)[0]]}
+        st = self._step
+        check(_lib.load().skb_stream_push_step(self._h, z, C.byref(st), self._ev, len(self._ev), _st()))
+        evicted = self._ev[: int(st.n_evicted)]
+        tau = float(st.tau)
+        return {"tau": tau if math.isfinite(tau) else None, "t": int(st.t),
+                "inserted": bool(st.inserted), "evicted": evicted}
 
-    def _survivors(self):
-        info = self._info()
-        vals = np.zeros(max(info.survivors, 1))
-        idx = np.zeros(max(info.survivors, 1), np.int64)
-        ev = np.zeros(max(info.t, 1), np.uint8)
-        check(_lib.load().skb_stream_survivors(
-            self._h, vals.ctypes.data, idx.ctypes.data, ev.ctypes.data,
-            torch.cuda.current_stream().cuda_stream))
-        return vals[: info.survivors], idx[: info.survivors], ev[: info.t].astype(bool)
+    def push_many(self, z):
+        """Push a batch of scores in one launch; returns (tau, inserted) per push."""
+        zt = torch.as_tensor(np.asarray(z, np.float64), device=self._dev).contiguous()
+        if not torch.isfinite(zt).all():
+            raise NumericError("stream_push: non-finite value")
+        n = zt.numel()
+        tau = torch.empty(n, dtype=torch.float64, device=self._dev)
+        ins = torch.empty(n, dtype=torch.uint8, device=self._dev)
+        check(_lib.load().skb_stream_push(self._h, zt.data_ptr(), n, tau.data_ptr(), ins.data_ptr(), _st()))
+        return tau, ins.bool()
+
+    def _solution_dev(self, want_hard):
+        n = max(1, self.survivors)
+        p = torch.empty(n, dtype=torch.float64, device=self._dev)
+        idx = torch.empty(n, dtype=torch.int64, device=self._dev)
+        hard = torch.empty(n, dtype=torch.uint8, device=self._dev) if want_hard else None
+        info = _lib.StreamSolutionInfo()
+        check(_lib.load().skb_stream_solution(self._h, p.data_ptr(), idx.data_ptr(),
+                                              hard.data_ptr() if want_hard else None, C.byref(info), _st()))
+        m = int(info.n)
+        return p[:m], idx[:m], (hard[:m] if want_hard else None), info
 
     def solution(self):
         """{p, tau, u_count, w_count, degenerate} over the full prefix
-        (StreamState::solution, proj/src/stream.cpp:154-192)."""
-        info = self._info()
-        vals, idx, _ = self._survivors()
-        p = np.zeros(info.t)
-        if info.t < self._k:
-            p[idx] = 1.0
-            return {"p": p, "tau": None, "u_count": len(idx), "w_count": len(idx),
-                    "degenerate": True}
-        pv = np.clip(vals - info.tau, 0.0, 1.0)
-        p[idx] = pv
-        uc = int(np.sum(pv == 1.0))
-        wc = int(np.sum(pv > 0.0))
-        return {"p": p, "tau": info.tau, "u_count": uc, "w_count": wc,
-                "degenerate": bool(wc == uc)}
+        (StreamState::solution, proj/src/stream.cpp:154-192); p is computed on
+        the device and scattered to the prefix length."""
+        p, idx, _, info = self._solution_dev(False)
+        full = torch.zeros(int(info.t), dtype=torch.float64, device=self._dev)
+        if idx.numel():
+            full[idx] = p
+        tau = float(info.tau)
+        return {"p": full.cpu().numpy(), "tau": tau if math.isfinite(tau) else None,
+                "u_count": int(info.u_count), "w_count": int(info.w_count),
+                "degenerate": bool(info.degenerate)}
+
+    def mask(self) -> SelectionMask:
+        """stream_mask (proj/src/stream.cpp:199-222); ArgumentError on an empty state."""
+        if self.t == 0:
+            raise ArgumentError("stream_mask: empty state")
+        p, idx, hard, _ = self._solution_dev(True)
+        return SelectionMask(idx.cpu().numpy(), hard.double().cpu().numpy(), p.cpu().numpy())
 
     @property
     def tau(self):
@@ -130,5 +160,14 @@ class Stream:
         return int(self._info().survivors)
 
     def is_evicted(self, index):
-        _, _, ev = self._survivors()
-        return bool(ev[int(index)])
+        info = self._info()
+        index = int(index)
+        if not (0 <= index < info.t):
+            raise IndexError("is_evicted: index out of range")
+        ev = np.zeros(max(info.t, 1), np.uint8)
+        check(_lib.load().skb_stream_survivors(self._h, None, None, ev.ctypes.data, _st()))
+        return bool(ev[index])
+
+
+def stream_mask(stream: Stream) -> SelectionMask:
+    return stream.mask()
