@@ -163,6 +163,12 @@ int skb_sparsek(int64_t n, int64_t m, const double* z, double k, double* p, doub
 int skb_sparsek_jvp(int64_t n, int64_t m, const double* z, double k, const double* v,
                     double* out, void* stream);
 int skb_topk_hard(int64_t n, int64_t m, const double* z, int64_t k, double* out, void* stream);
+/* sparsek_jvp(sol, v) from a solution's weights p (proj/src/sparsek_op.cpp:141-150):
+ * out = (v - mean over {0 < p < 1} of v) on that support, 0 elsewhere; device [m]. */
+int skb_support_jvp(int64_t m, const double* p, const double* v, double* out, void* stream);
+/* Row-major C[M, N] = A[M, K] B[K, N] on the device (the reference's matmul,
+ * proj/src/numerics.cpp:8-24; a library GEMM), dtype F32/F64/BF16. */
+int skb_matmul(int32_t dtype, int64_t M, int64_t N, int64_t K, const void* a, const void* b, void* c, void* stream);
 
 /* ---- K5: constant-(floor(k)+w) KV cache for decoding --------------------- */
 typedef struct skb_cache skb_cache;
@@ -195,6 +201,14 @@ int skb_cache_restore(skb_cache* c, int64_t b, const uint8_t* data, size_t bytes
                       void* stream);
 int skb_cache_state(skb_cache* c, int64_t b, int32_t* positions, int64_t* count, double* tau,
                     int64_t* seen, int64_t* peak, void* stream);
+/* The eviction ledger of sequence b (SparseKvCache::drain_evictions / ever_evicted /
+ * frozen_score, proj/include/sparsek/cache.hpp:38-48): pending evictions since the
+ * last drain (cleared when drain != 0; *n_pending = their count, the first
+ * pending_cap are copied), the evicted flag of positions [0, evicted_cap) and
+ * the frozen scores of positions [0, scores_cap). Host outputs; any may be NULL. */
+int skb_cache_ledger(skb_cache* c, int64_t b, int32_t drain, int64_t* pending, int64_t pending_cap,
+                     int64_t* n_pending, uint8_t* evicted, int64_t evicted_cap, double* scores, int64_t scores_cap,
+                     void* stream);
 
 
 /* ---- Incremental SparseK stream on the device (Algorithm 2) ------------- */
@@ -256,6 +270,60 @@ int skb_stream_serialize(skb_stream* s, uint8_t* out, size_t* bytes, void* strea
 int skb_stream_deserialize(const uint8_t* data, size_t bytes, int64_t capacity, skb_stream** out);
 int skb_stream_survivors(skb_stream* s, double* values, int64_t* indices, uint8_t* evicted,
                          void* stream);
+
+/* ---- x-level operator: sparsek_attention<T> / sparsek_attention_backward<T>
+ * (proj/include/sparsek/attention.hpp:81-91, proj/src/attention.cpp:37-43,214-575)
+ * and SparseKvCache<T>::forward_chunk / generate_step (proj/include/sparsek/
+ * cache.hpp:21-102). x [B, L, d_model] and W* [d_model, d_model] (row-major,
+ * head h owns columns [h*p, (h+1)*p)) in `dtype`; w_score float64 [d_model].
+ * All pointers are device (or managed) memory; projections are library GEMMs. */
+typedef struct skb_x_desc {
+    int64_t batch;      /* B independent sequences                         */
+    int64_t seq_len;    /* L (for a cache: the maximum positions per sequence) */
+    int64_t d_model;    /* D = heads * head_dim                            */
+    int64_t heads;
+    double k;           /* AttnConfig::k                                   */
+    int64_t window;     /* AttnConfig::window                              */
+    double scale;       /* 0 -> 1/sqrt(head_dim)                           */
+    int32_t key_mode;   /* 0 hard, 1 soft                                  */
+    int32_t mask_mode;  /* 0 soft, 1 straight_through                      */
+    int32_t dtype;      /* skb_dtype of x, W*, y and the gradients         */
+    uint32_t flags;     /* SKB_FLAG_*                                      */
+    int64_t chunk_len;  /* chunked_forward's stop-grad chunks; 0 = one     */
+    skb_scoring scoring;
+} skb_x_desc;
+
+typedef struct skb_xattn skb_xattn; /* a device-resident AttnTape */
+/* y = sparsek_attention(x); with tape != NULL the forward state is kept in a
+ * new tape (free with skb_xattn_destroy). */
+int skb_xattn_forward(const skb_x_desc* d, const void* x, const void* wq, const void* wk, const void* wv,
+                      const void* wo, const double* w_score, void* y, skb_xattn** tape, void* stream);
+/* AttnGrads from a tape: dx [B, L, D], dW* [D, D] (dtype), dw_score float64 [D]. */
+int skb_xattn_backward(skb_xattn* tape, const void* grad_out, const void* wq, const void* wk, const void* wv,
+                       const void* wo, const double* w_score, void* dx, void* dwq, void* dwk, void* dwv,
+                       void* dwo, double* dw_score, void* stream);
+/* Copy one AttnTape field (host or device destination, `bytes` = its size):
+ * x/q/k/v/head_concat [B, L, D] dtype; raw/u/norm_mean/norm_sdev float64 [B, L];
+ * lse float64 [B, H, L] (= maxa + log denom); tau_push float64 [B, L] (push
+ * time t; -inf while t + 1 < k); leave int32 [B, L] (position j is selected for
+ * push times j <= t < leave_j). */
+enum {
+    SKB_TAPE_X = 0, SKB_TAPE_Q, SKB_TAPE_K, SKB_TAPE_V, SKB_TAPE_HEAD_CONCAT, SKB_TAPE_RAW, SKB_TAPE_U,
+    SKB_TAPE_NORM_MEAN, SKB_TAPE_NORM_SDEV, SKB_TAPE_LSE, SKB_TAPE_TAU_PUSH, SKB_TAPE_LEAVE
+};
+int skb_xattn_tape_get(skb_xattn* tape, int32_t field, void* dst, size_t bytes, void* stream);
+int skb_xattn_destroy(skb_xattn* tape);
+
+typedef struct skb_xcache skb_xcache; /* SparseKvCache<T> for B sequences */
+int skb_xcache_create(const skb_x_desc* d, skb_xcache** out);
+int skb_xcache_destroy(skb_xcache* c);
+/* forward_chunk: x [B, n, D] -> y [B, n, D]; generate_step is n = 1. */
+int skb_xcache_forward_chunk(skb_xcache* c, const void* x, int64_t n, const void* wq, const void* wk,
+                             const void* wv, const void* wo, const double* w_score, void* y, void* stream);
+/* The underlying q/k/v-level cache (skb_cache_state / snapshot / restore). */
+skb_cache* skb_xcache_inner(skb_xcache* c);
+/* TimestepNormState {count, mean, m2} per sequence (host [B, 3]): get (set = 0) or set. */
+int skb_xcache_norm_state(skb_xcache* c, double* norm_state, int32_t set, void* stream);
 
 #ifdef __cplusplus
 }

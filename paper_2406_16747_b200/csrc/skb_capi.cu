@@ -20,6 +20,7 @@ void run_sparsek(int64_t n, int64_t m, const double* z, double k, double* p, dou
 void run_sparsek_jvp(int64_t n, int64_t m, const double* z, double k, const double* v, double* out,
                      cudaStream_t st);
 void run_topk_hard(int64_t n, int64_t m, const double* z, int64_t k, double* out, cudaStream_t st);
+void run_support_jvp(int64_t m, const double* p, const double* v, double* out, cudaStream_t st);
 }  // namespace skb
 
 namespace {
@@ -202,6 +203,15 @@ int skb_sparsek_jvp(int64_t n, int64_t m, const double* z, double k, const doubl
     NONNULL(v, "sparsek_jvp v");
     NONNULL(out, "sparsek_jvp out");
     skb::run_sparsek_jvp(n, m, z, k, v, out, S(stream));
+    SKB_API_END
+}
+
+int skb_support_jvp(int64_t m, const double* p, const double* v, double* out, void* stream) {
+    SKB_API_BEGIN
+    NONNULL(p, "sparsek_jvp p");
+    NONNULL(v, "sparsek_jvp v");
+    NONNULL(out, "sparsek_jvp out");
+    skb::run_support_jvp(m, p, v, out, S(stream));
     SKB_API_END
 }
 

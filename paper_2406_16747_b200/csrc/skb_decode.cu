@@ -1559,6 +1559,48 @@ extern "C" {
 // SparseKvCache<T>::serialize (proj/src/cache.cpp:416-475) of sequence b; the
 // reference's TimestepNormState {count, mean, m2} comes from the caller (the
 // cache works at the q/k/v/u level; null = a fresh state).
+// The eviction ledger of sequence b (SparseKvCache::drain_evictions /
+// ever_evicted, proj/src/cache.cpp:115-125, proj/include/sparsek/cache.hpp:38-45):
+// the host replay advances to the current position (its base moves forward),
+// then reports the pending evictions (cleared when drain != 0), the evicted
+// flag of the first evicted_cap positions and the frozen scores.
+int skb_cache_ledger(skb_cache* c, int64_t b, int32_t drain, int64_t* pending, int64_t pending_cap,
+                     int64_t* n_pending, uint8_t* evicted, int64_t evicted_cap, double* scores, int64_t scores_cap,
+                     void* stream) {
+    K5_BEGIN
+    SKB_REQUIRE(c != nullptr && n_pending != nullptr, SKB_EARG, "cache_ledger: null argument");
+    SKB_REQUIRE(b >= 0 && b < c->d.batch, SKB_EARG, "cache_ledger: sequence out of range");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const CacheArgs& A = c->A;
+    const int64_t bL = b * A.Lmax;
+    CacheCtl cc;
+    SKB_CHECK_CUDA(cudaMemcpyAsync(&cc, A.ctl + b, sizeof(cc), cudaMemcpyDeviceToHost, st));
+    SKB_CHECK_CUDA(cudaStreamSynchronize(st));
+    const long long t = cc.t, w = A.w;
+    SnapBase& sb = c->base[(size_t)b];
+    const long long e0 = std::max(0LL, sb.t0 - w), e1 = std::max(0LL, t - w);
+    std::vector<double> u((size_t)std::max<long long>(t, 1));
+    std::vector<uint8_t> ins((size_t)std::max<long long>(t, 1));
+    if (t) {
+        SKB_CHECK_CUDA(cudaMemcpyAsync(u.data(), A.u_hist + bL, t * 8, cudaMemcpyDeviceToHost, st));
+        SKB_CHECK_CUDA(cudaMemcpyAsync(ins.data(), A.ins_hist + bL, t, cudaMemcpyDeviceToHost, st));
+        SKB_CHECK_CUDA(cudaStreamSynchronize(st));
+    }
+    for (long long e = e0; e < e1; ++e)
+        replay_exit(sb, e, u[(size_t)e], c->d.k > 0.0, ins[(size_t)e] != 0, (size_t)A.cap);
+    sb.t0 = t;
+    *n_pending = (int64_t)sb.pending.size();
+    if (pending)
+        for (size_t i = 0; i < sb.pending.size() && (int64_t)i < pending_cap; ++i) pending[i] = sb.pending[i];
+    if (drain) sb.pending.clear();
+    if (evicted)
+        for (int64_t i = 0; i < evicted_cap; ++i)
+            evicted[i] = (i < (int64_t)sb.evicted.size() && sb.evicted[(size_t)i]) ? 1 : 0;
+    if (scores)
+        for (int64_t i = 0; i < scores_cap && i < t; ++i) scores[i] = u[(size_t)i];
+    K5_END
+}
+
 int skb_cache_snapshot(skb_cache* c, int64_t b, const double* norm_state, uint8_t* out, size_t* bytes,
                        void* stream) {
     K5_BEGIN

@@ -195,6 +195,47 @@ void run_sparsek_jvp(int64_t n, int64_t m, const double* z, double k, const doub
     launch_rows(a, n, st);
 }
 
+// sparsek_jvp(sol, v) (proj/src/sparsek_op.cpp:141-150) from a solution's p:
+// out_j = v_j - mean over the support {0 < p < 1} on the support, else 0.
+__global__ void __launch_bounds__(1024) k_support_jvp(const double* __restrict__ p, const double* __restrict__ v,
+                                                      int m, double* __restrict__ out) {
+    __shared__ double ssum[32];
+    __shared__ int scnt[32];
+    double s = 0.0;
+    int c = 0;
+    for (int j = threadIdx.x; j < m; j += blockDim.x) {
+        const bool sup = p[j] > 0.0 && p[j] < 1.0;
+        s += sup ? v[j] : 0.0;
+        c += sup;
+    }
+    s = warp_sum(s);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0) {
+        ssum[threadIdx.x >> 5] = s;
+        scnt[threadIdx.x >> 5] = c;
+    }
+    __syncthreads();
+    double tot = 0.0;
+    int cnt = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {  // fixed order: deterministic
+        tot += ssum[w];
+        cnt += scnt[w];
+    }
+    const double vbar = cnt ? tot / (double)cnt : 0.0;
+    for (int j = threadIdx.x; j < m; j += blockDim.x) {
+        const bool sup = p[j] > 0.0 && p[j] < 1.0;
+        out[j] = sup ? v[j] - vbar : 0.0;
+    }
+}
+
+void run_support_jvp(int64_t m, const double* p, const double* v, double* out, cudaStream_t st) {
+    SKB_REQUIRE(m >= 0, SKB_ESHAPE, "sparsek_jvp: v length mismatch");
+    if (m == 0) return;
+    k_support_jvp<<<1, 1024, 0, st>>>(p, v, (int)m, out);
+    SKB_CHECK_LAUNCH();
+}
+
 void run_topk_hard(int64_t n, int64_t m, const double* z, int64_t k, double* out, cudaStream_t st) {
     SKB_REQUIRE(m >= 1 && n >= 1, SKB_EARG, "topk_hard: empty input");
     dim3 g((unsigned)cdiv(m, 256), (unsigned)n);

@@ -67,4 +67,4 @@ def test_chunked_tensor_core_vs_gather(cuda, chunk):
     torch.cuda.synchronize()
     rel = lambda a, b: float((a.double() - b.double()).norm() / b.double().norm().clamp_min(1e-30))
     for nm, a, b in zip(("o", "dq", "dk", "dv", "du"), res[False], res[True]):
-        assert rel(a, b) < (5e-2 if nm == "du" else 2e-2), (nm, rel(a, b))
+        assert rel(a, b) < 2e-2, (nm, rel(a, b))

@@ -131,7 +131,7 @@ def test_core_vs_oracle(cuda, oracle, case, dtype):
     for name, a, b in (("dq", res["dq"], dq), ("dk", res["dk"], dk), ("dv", res["dv"], dv)):
         assert rel_err(a, b) < gtol, (name, rel_err(a, b))
     if np.abs(gu).max() > 0:
-        assert rel_err(res["du"], gu) < (1e-8 if dtype == "f64" else 10 * gtol), rel_err(res["du"], gu)
+        assert rel_err(res["du"], gu) < (1e-8 if dtype == "f64" else gtol), rel_err(res["du"], gu)
     else:
         assert np.abs(res["du"]).max() == 0
 
@@ -231,7 +231,7 @@ def test_tensor_core_path_vs_oracle(cuda, oracle, case):
         assert rel_err(tc[name], ga[name]) < 2e-2, (name, rel_err(tc[name], ga[name]))
     np.testing.assert_allclose(tc["lse"], lse.T, rtol=0, atol=2e-2)
     if np.abs(gu).max() > 0:
-        assert rel_err(tc["du"], gu) < 5e-2, rel_err(tc["du"], gu)
+        assert rel_err(tc["du"], gu) < 2e-2, rel_err(tc["du"], gu)
 
 
 FULL_CASES = [
@@ -248,7 +248,7 @@ def test_full_size_tensor_core_path(cuda, oracle, case, kind):
     (1) sampled query rows recomputed in float64 from the C oracle's selection
         (Sel_i, tau_i) — o_i and dq_i within 2e-2;
     (2) every output against the f32 CUDA-core gather path on the same
-        (bf16-rounded) inputs — o, dq, dk, dv within 2e-2, du within 5e-2."""
+        (bf16-rounded) inputs — o, dq, dk, dv and du within 2e-2."""
     import torch
 
     from paper_2406_16747_b200 import ops
@@ -272,7 +272,7 @@ def test_full_size_tensor_core_path(cuda, oracle, case, kind):
     rel = lambda a, b: float((a.double() - b.double()).norm() / b.double().norm().clamp_min(1e-30))
     for nm, a, b_ in (("o", o, og), ("dq", dq, dqg), ("dk", dk, dkg), ("dv", dv, dvg)):
         assert rel(a, b_) < 2e-2, (nm, rel(a, b_))
-    assert rel(du, dug) < 5e-2, rel(du, dug)
+    assert rel(du, dug) < 2e-2, rel(du, dug)
     # (1) sampled rows against the oracle's selection
     osel = oracle.select(u_np, k, w)
     Qn, Kn, Vn, dOn = (t[0].double().cpu().numpy() for t in (q, kk, v, do))
