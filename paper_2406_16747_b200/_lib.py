@@ -75,6 +75,14 @@ class StreamInfo(C.Structure):
                 ("k", C.c_double)]
 
 
+class XDesc(C.Structure):
+    """skb_x_desc: the x-level operator configuration (include/sparsek_b200.h)."""
+    _fields_ = [("batch", C.c_int64), ("seq_len", C.c_int64), ("d_model", C.c_int64), ("heads", C.c_int64),
+                ("k", C.c_double), ("window", C.c_int64), ("scale", C.c_double), ("key_mode", C.c_int32),
+                ("mask_mode", C.c_int32), ("dtype", C.c_int32), ("flags", C.c_uint32), ("chunk_len", C.c_int64),
+                ("scoring", Scoring)]
+
+
 class StreamStep(C.Structure):
     _fields_ = [("tau", C.c_double), ("t", C.c_int64), ("inserted", C.c_int32),
                 ("cap_forced", C.c_int32), ("n_evicted", C.c_int64)]
@@ -115,6 +123,19 @@ _SIGS = {
     "skb_stream_destroy": ([_vp], C.c_int),
     "skb_stream_push": ([_vp, _vp, C.c_int64, _vp, _vp, _vp], C.c_int),
     "skb_stream_query": ([_vp, C.POINTER(StreamInfo), _vp], C.c_int),
+    "skb_support_jvp": ([C.c_int64, _vp, _vp, _vp, _vp], C.c_int),
+    "skb_matmul": ([C.c_int32, C.c_int64, C.c_int64, C.c_int64, _vp, _vp, _vp, _vp], C.c_int),
+    "skb_xattn_forward": ([C.POINTER(XDesc)] + [_vp] * 7 + [C.POINTER(_vp), _vp], C.c_int),
+    "skb_xattn_backward": ([_vp] * 14, C.c_int),
+    "skb_xattn_tape_get": ([_vp, C.c_int32, _vp, C.c_size_t, _vp], C.c_int),
+    "skb_xattn_destroy": ([_vp], C.c_int),
+    "skb_xcache_create": ([C.POINTER(XDesc), C.POINTER(_vp)], C.c_int),
+    "skb_xcache_destroy": ([_vp], C.c_int),
+    "skb_xcache_forward_chunk": ([_vp, _vp, C.c_int64] + [_vp] * 7, C.c_int),
+    "skb_xcache_inner": ([_vp], _vp),
+    "skb_xcache_norm_state": ([_vp, _vp, C.c_int32, _vp], C.c_int),
+    "skb_cache_ledger": ([_vp, C.c_int64, C.c_int32, _vp, C.c_int64, _vp, _vp, C.c_int64, _vp, C.c_int64, _vp],
+                         C.c_int),
     "skb_stream_push_step": ([_vp, C.c_double, C.POINTER(StreamStep), _vp, C.c_int64, _vp], C.c_int),
     "skb_stream_solution": ([_vp, _vp, _vp, _vp, C.POINTER(StreamSolutionInfo), _vp], C.c_int),
     "skb_stream_survivors": ([_vp, _vp, _vp, _vp, _vp], C.c_int),

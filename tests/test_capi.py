@@ -13,7 +13,7 @@ LIB = os.path.join(ROOT, "paper_2406_16747_b200", "libsparsek_b200.so")
 
 def declared():
     txt = open(HEADER).read()
-    return sorted(set(re.findall(r"^(?:const char\*|int)\s+(skb_\w+)\s*\(", txt, re.M)))
+    return sorted(set(re.findall(r"^(?:const char\*|int|skb_\w+\*)\s+(skb_\w+)\s*\(", txt, re.M)))
 
 
 def test_header_declares_the_boundary():
