@@ -7,16 +7,23 @@ retention) -> K3 forward -> K4 backward + selection pullback (du).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 
-N > 1 runs under torchrun, one rank per GPU, each rank owning its own B=2
-sequences (weak scaling, no data-path collective). Timing: CUDA events on the
-launching stream, barrier + synchronize around the timed region, max over
-ranks. Inputs (1.07 GB per rank) exceed the 126 MB L2, so no flush is needed.
+N > 1 runs under torchrun, one rank per GPU: the fixed cfg3 workload (B*H = 64
+(sequence, head) units) is split over the ranks b-major (strong scaling; at
+N=8 every GPU owns 8 heads of one sequence). Each rank recomputes
+the selection of its sequence from u[b] (no collective); the one data-path
+exchange is the all-reduce of the selection pullback du[b] over the ranks
+sharing b. Timing: CUDA events on the launching stream, barrier + synchronize
+around the timed region, max over ranks. Inputs (1.07 GB) exceed the 126 MB
+L2, so no flush is needed.
 
 The JSON line also carries: `roofline` for the dominant kernel (achieved
 algorithmic TFLOP/s over its event-timed duration vs MEASURED_PEAKS.json),
 `cpu_baseline` (the compiled reference on this host's cores, bounded sample),
 `e2e` (the same step through the C ABI from pinned host buffers, copies
-included), `gpu_launches`, and SM clocks sampled during the timed region.
+included), `gpu_launches`, SM clocks sampled during the timed region, and (N=1)
+a `secondary` object: iid-score cfg3, cfg2, the per-rank shares of cfg3 at
+N=2/4/8 timed on this GPU, and cfg4 decode with the reference's generate_step
+timed on the host.
 """
 from __future__ import annotations
 
@@ -185,7 +192,7 @@ def run_reference_arm(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": secs * 1e3, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": secs * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": "cfg3 B=2 H=32 L=16384 d=128 k=1024 w=512 (CPU sample)",
                    "sample_L": L, "threads": threads},
@@ -197,28 +204,22 @@ def run_reference_arm(args):
 
 
 DECODE = dict(B=64, ctx=32768, H=32, d=128, k=1024.0, w=512)
+CFG2 = dict(B=8, H=12, L=4096, d=64, k=256.0, w=256)
 
 
-def run_decode(args):
+def decode_timing(torch, ops, dev, steps, warmup, seed=99):
     """BASELINE.json configs[3]: incremental decode with the constant-(k+w) KV
     cache, batch 64, 32k context prefilled, H=32, d=128, k=1024, w=512, bf16.
     A step = one new token for every sequence (stream push + eviction + gated
     attention over floor(k)+w+1 slots). HBM-bound: the slot pool is read once
-    per step."""
-    import torch
-
-    from paper_2406_16747_b200 import ops
-
-    rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    per step. Returns (ms_per_step, prefill_s, cache)."""
     C = DECODE
     B, H, d, ctx = C["B"], C["H"], C["d"], C["ctx"]
     cfg = ops.AttnConfig(k=C["k"], window=C["w"])
-    nsteps = args.warmup + args.steps
+    nsteps = warmup + steps
     cache = ops.DecodeCache(B, H, d, cfg, max_len=ctx + nsteps + 8, dtype=torch.bfloat16)
     g = torch.Generator(device=dev)
-    g.manual_seed(99 + rank)
+    g.manual_seed(seed)
     chunk = 4096  # prefill in chunks to bound the host-side history buffers
     t_pre = time.time()
     for c0 in range(0, ctx, chunk):
@@ -236,7 +237,7 @@ def run_decode(args):
     vs = torch.randn((nsteps, B, H, d), generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16)
     us = torch.randn((nsteps, B), generator=g, device=dev, dtype=torch.float64) + 0.01 * (ctx + 1)
     out = torch.empty((B, H, d), dtype=torch.bfloat16, device=dev)
-    for i in range(args.warmup):
+    for i in range(warmup):
         cache.step(qs[i], ks[i], vs[i], us[i], out=out)
     torch.cuda.synchronize()
     # the K timed steps as one CUDA graph (the cache state lives on the device,
@@ -246,36 +247,172 @@ def run_decode(args):
     side.wait_stream(torch.cuda.current_stream())
     with torch.cuda.stream(side):
         with torch.cuda.graph(graph, stream=side):
-            for i in range(args.warmup, nsteps):
+            for i in range(warmup, nsteps):
                 cache.step(qs[i], ks[i], vs[i], us[i], out=out)
     torch.cuda.current_stream().wait_stream(side)
     torch.cuda.synchronize()
     st = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        torch.cuda.synchronize()
-        e0.record(st)
-        graph.replay()
-        e1.record(st)
-        torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / args.steps
+    torch.cuda.synchronize()
+    e0.record(st)
+    graph.replay()
+    e1.record(st)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / steps, t_pre, cache
+
+
+def decode_summary(ms, t_pre, cache):
+    C = DECODE
+    B, H, d = C["B"], C["H"], C["d"]
     S = int(C["k"]) + C["w"] + 1
     bytes_step = B * S * H * d * 2 * 2  # K and V slot pools, read once
     hbm, _, _, src = peaks()
     ach = bytes_step / (ms / 1e3) / 1e9
     st0 = cache.state(0)
-    line = {
-        "metric": "SparseK incremental decode tokens/s (constant-(k+w) KV cache)", "value": B / (ms / 1e3),
-        "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": "cfg4: batch 64, 32k context prefilled, H=32 d=128 k=1024 w=512",
-                   "prefill_s": t_pre, "retained_rows": int(len(st0["positions"])), "peak_kv": st0["peak"]},
-        "roofline": {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
-                     "traffic": None, "bytes_per_step": bytes_step, "peak_kind": f"{src} copy bandwidth"},
-        "gpu_launches": 3 * args.steps, "clocks": clk.summary(),
-    }
+    return {"value": B / (ms / 1e3), "unit": "tokens/s", "ms_per_step": ms,
+            "config": {"workload": "cfg4: batch 64, 32k context prefilled, H=32 d=128 k=1024 w=512",
+                       "prefill_s": t_pre, "retained_rows": int(len(st0["positions"])), "peak_kv": st0["peak"]},
+            "roofline": {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                         "traffic": None, "bytes_per_step": bytes_step, "peak_kind": f"{src} copy bandwidth"}}
+
+
+def cpu_decode_sample(threads, steps=2000):
+    """The reference's generate_step on this host: `threads` single-head
+    (d=128, k=1024, w=512) caches prefilled with 2048 rows (> floor(k)+w, so a
+    step does the full O(k+w) work), `steps` steps each, float, one std::thread
+    per cache. Scaled to cfg4's 64 x 32 (sequence, head) units per token step."""
+    from oracle.oracle import Reference
+
+    C = DECODE
+    ref = Reference()
+    secs = ref.bench_decode(threads, threads, 2048, steps, C["d"], C["k"], C["w"], seed=3)
+    units_total = C["B"] * C["H"]
+    tok_per_s = C["B"] * (threads * steps / units_total) / secs
+    return {"value": tok_per_s, "unit": "tokens/s", "cores": threads, "kind": "reference",
+            "sample": f"{threads} single-head caches (d=128,k=1024,w=512, 2048-row prompt) x {steps} "
+                      f"generate_step<float>, one std::thread each, {secs:.2f}s; scaled to 64x32 units/token"}
+
+
+def run_decode(args):
+    import torch
+
+    from paper_2406_16747_b200 import ops
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    with ClockSampler(local) as clk:
+        ms, t_pre, cache = decode_timing(torch, ops, dev, args.steps, args.warmup, seed=99 + rank)
+    d = decode_summary(ms, t_pre, cache)
+    line = {"metric": "SparseK incremental decode tokens/s (constant-(k+w) KV cache)", "value": d["value"],
+            "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic", "config": d["config"], "roofline": d["roofline"],
+            "gpu_launches": 3 * args.steps, "clocks": clk.summary()}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_decode_sample(max(1, os.cpu_count() or 1))
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+class TrainBlock:
+    """One rank's share of a fwd+bwd workload: sequences [b0, b1) and heads
+    [h0, h1) of config C, resident in HBM. u[b] is seeded by the sequence, so
+    every rank holding b computes the same selection."""
+
+    def __init__(self, torch, ops, dev, C, scores, b0, b1, h0, h1, seed, du_group=None):
+        self.torch, self.ops, self.C = torch, ops, C
+        self.H = h1 - h0
+        self.nb = b1 - b0
+        L, d = C["L"], C["d"]
+        self.cfg = ops.AttnConfig(k=C["k"], window=C["w"])
+        g = torch.Generator(device=dev)
+        g.manual_seed(seed)
+        shape = (self.nb, L, self.H, d)
+        self.q, self.k, self.v, self.do = (
+            torch.randn(shape, generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16) for _ in range(4))
+        us = []
+        for b in range(b0, b1):
+            gu = torch.Generator(device=dev)
+            gu.manual_seed(4242 + b)
+            u = torch.randn((L,), generator=gu, device=dev, dtype=torch.float64)
+            if scores == "recency":  # mimics norm_then_slope output: N(0,1) + 0.01 (i+1)
+                u = u + 0.01 * torch.arange(1, L + 1, device=dev, dtype=torch.float64)
+            us.append(u)
+        self.u = torch.stack(us).contiguous()
+        self.bws = ops.bwd_workspace(self.q, self.cfg)
+        self.du_group = du_group
+
+    def step(self, st, ev=None):
+        ops, C = self.ops, self.C
+        if ev is not None:
+            ev[0].record(st)
+        sel = ops.select(self.u, self.cfg, heads=self.H, head_dim=C["d"], dtype=self.torch.bfloat16)
+        if ev is not None:
+            ev[1].record(st)
+        o, lse, _ = ops.attn_fwd(self.q, self.k, self.v, self.u, self.cfg, sel=sel)
+        if ev is not None:
+            ev[2].record(st)
+        dq, dk, dv, du = ops.attn_bwd(self.q, self.k, self.v, o, self.do, lse, self.u, sel, self.cfg, ws=self.bws)
+        if ev is not None:
+            ev[3].record(st)
+        if self.du_group is not None:  # the one data-path exchange: head-summed selection pullback
+            from paper_2406_16747_b200.parallel import allreduce_du
+
+            allreduce_du(du, self.du_group)
+        return o, dq, dk, dv, du
+
+    def time(self, steps, warmup, barrier=None):
+        torch = self.torch
+        st = torch.cuda.current_stream()
+        for _ in range(warmup):
+            self.step(st)
+        torch.cuda.synchronize()
+        if barrier:
+            barrier()
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(steps)]
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        if barrier:
+            barrier()
+        t0.record(st)
+        for i in range(steps):
+            self.step(st, evs[i])
+        t1.record(st)
+        torch.cuda.synchronize()
+        if barrier:
+            barrier()
+        ms = t0.elapsed_time(t1) / steps
+        ph = {"select_ms": sum(e[0].elapsed_time(e[1]) for e in evs) / steps,
+              "attn_fwd_ms": sum(e[1].elapsed_time(e[2]) for e in evs) / steps,
+              "attn_bwd_ms": sum(e[2].elapsed_time(e[3]) for e in evs) / steps}
+        return ms, ph
+
+
+def work_of(C, nb, nh):
+    """Algorithmic FLOPs (attended pairs) and compulsory bytes of nb x nh units."""
+    natt = n_att(C["L"], C["k"], C["w"])
+    d, L = C["d"], C["L"]
+    fl_fwd = 4.0 * d * natt * nb * nh
+    fl_bwd = 8.0 * d * natt * nb * nh
+    # fwd: Q,K,V,u in, O,LSE out; bwd: Q,K,V,O,dO,LSE in, dQ,dK,dV,du out (bf16 rows, f64 lse/u)
+    row = L * nh * d * 2 * nb
+    by_fwd = 4 * row + nb * nh * L * 8 + nb * L * 8
+    by_bwd = 8 * row + nb * nh * L * 8 + nb * L * 8 * 2
+    return natt, fl_fwd, fl_bwd, by_fwd, by_bwd
+
+
+def secondary_train(torch, ops, dev, C, scores, steps, warmup, label):
+    blk = TrainBlock(torch, ops, dev, C, scores, 0, C["B"], 0, C["H"], seed=77)
+    ms, ph = blk.time(steps, warmup)
+    hbm, tf_burst, _, _ = peaks()
+    natt, ff, fb, bf, bb = work_of(C, C["B"], C["H"])
+    t_roof = max((ff + fb) / (tf_burst * 1e12), (bf + bb) / (hbm * 1e9)) * 1e3
+    del blk
+    torch.cuda.empty_cache()
+    return {"workload": label, "value": C["B"] * C["L"] / (ms / 1e3), "unit": "tokens/s", "ms_per_step": ms,
+            **ph, "tflops": (ff + fb) / (ms / 1e3) / 1e12, "roofline_ms": t_roof, "frac": t_roof / ms}
 
 
 def main():
@@ -287,6 +424,7 @@ def main():
     ap.add_argument("--scores", default="recency", choices=["recency", "iid"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--workload", default="train", choices=["train", "decode"],
                     help="train: cfg3 fwd+bwd (the headline); decode: cfg4 constant-(k+w) cache steps")
     args = ap.parse_args()
@@ -302,69 +440,49 @@ def main():
     import torch.distributed as dist
 
     from paper_2406_16747_b200 import ops
+    from paper_2406_16747_b200 import parallel
+    from paper_2406_16747_b200.parallel import unit_shard
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    C = CFG
+    B, H, L, d, kb, w = (C[x] for x in ("B", "H", "L", "d", "k", "w"))
+    # strong scaling: the fixed cfg3 workload (B*H = 64 (sequence, head) units)
+    # split over the ranks, b-major (8 GPUs: 8 heads of one sequence each)
+    blocks = unit_shard(B, H, world, rank)
+    du_group = None
     if world > 1:
         dist.init_process_group("nccl", init_method="env://", device_id=dev)
-    B, H, L, d, kb, w = (CFG[x] for x in ("B", "H", "L", "d", "k", "w"))
-    cfg = ops.AttnConfig(k=kb, window=w)
-    q, k, v, do, u = make_inputs(torch, dev, 1234 + rank, args.scores)
-    bws = ops.bwd_workspace(q, cfg)
-    st = torch.cuda.current_stream()
-
-    def step(ev=None):
-        if ev is not None:
-            ev[0].record(st)
-        sel = ops.select(u, cfg, heads=H, head_dim=d, dtype=torch.bfloat16)
-        if ev is not None:
-            ev[1].record(st)
-        o, lse, _ = ops.attn_fwd(q, k, v, u, cfg, sel=sel)
-        if ev is not None:
-            ev[2].record(st)
-        out = ops.attn_bwd(q, k, v, o, do, lse, u, sel, cfg, ws=bws)
-        if ev is not None:
-            ev[3].record(st)
-        return out
-
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+        # ranks sharing a sequence all-reduce its du partials; every rank builds
+        # every group (torch.distributed requires all ranks to call new_group)
+        seq_ranks = parallel.seq_ranks(B, H, world)
+        groups = {b: dist.new_group(rs) for b, rs in sorted(seq_ranks.items())}
+        mine = sorted({b for b, _, _ in blocks})
+        if len(mine) == 1 and len(seq_ranks[mine[0]]) > 1:
+            du_group = groups[mine[0]]
+    if all(h0 == 0 and h1 == H for _, h0, h1 in blocks):
+        b0, b1, h0, h1 = blocks[0][0], blocks[-1][0] + 1, 0, H
+    elif len(blocks) == 1:
+        b0, h0, h1 = blocks[0]
+        b1 = b0 + 1
+    else:
+        raise SystemExit(f"bench: world size {world} splits cfg3 into ragged blocks {blocks}")
+    blk = TrainBlock(torch, ops, dev, C, args.scores, b0, b1, h0, h1, seed=1234 + rank, du_group=du_group)
+    barrier = (lambda: dist.barrier()) if world > 1 else None
     with ClockSampler(local) as clk:
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        t0 = torch.cuda.Event(enable_timing=True)
-        t1 = torch.cuda.Event(enable_timing=True)
-        t0.record(st)
-        for i in range(args.steps):
-            step(evs[i])
-        t1.record(st)
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-    ms = t0.elapsed_time(t1)
-    sel_ms = sum(e[0].elapsed_time(e[1]) for e in evs) / args.steps
-    fwd_ms = sum(e[1].elapsed_time(e[2]) for e in evs) / args.steps
-    bwd_ms = sum(e[2].elapsed_time(e[3]) for e in evs) / args.steps
+        ms_step, phases = blk.time(args.steps, args.warmup, barrier)
     if world > 1:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        t = torch.tensor([ms_step], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    ms_step = ms / args.steps
-    tokens = B * L * world
+        ms_step = float(t.item())
+    tokens = B * L  # the whole job's tokens (fixed workload)
     value = tokens / (ms_step / 1e3)
 
-    # ---- roofline (algorithmic work)
+    # ---- roofline of the dominant kernel group (algorithmic work)
     hbm, tf_burst, tf_sus, src = peaks()
-    natt = n_att(L, kb, w)
-    fl_fwd = 4.0 * d * natt * B * H
-    fl_bwd = 8.0 * d * natt * B * H
-    phases = {"select_ms": sel_ms, "attn_fwd_ms": fwd_ms, "attn_bwd_ms": bwd_ms}
+    natt, fl_fwd, fl_bwd, _, _ = work_of(C, b1 - b0, h1 - h0)
+    bwd_ms, fwd_ms = phases["attn_bwd_ms"], phases["attn_fwd_ms"]
     dom = "attn_bwd" if bwd_ms >= fwd_ms else "attn_fwd"
     dom_ms, dom_fl = (bwd_ms, fl_bwd) if dom == "attn_bwd" else (fwd_ms, fl_fwd)
     ach = dom_fl / (dom_ms / 1e3) / 1e12
@@ -372,129 +490,201 @@ def main():
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         traffic = json.load(open(tp)).get(dom)
-    roof = {"bound": "tensor", "kernel": dom, "achieved": ach, "peak": tf_sus, "unit": "TFLOP/s",
-            "frac": ach / tf_sus, "traffic": traffic, "peak_kind": f"{src} bf16 sustained",
-            "step_achieved": (fl_fwd + fl_bwd) / (ms_step / 1e3) / 1e12,
-            "step_frac": (fl_fwd + fl_bwd) / (ms_step / 1e3) / 1e12 / tf_sus,
+    rank_ms = phases["select_ms"] + fwd_ms + bwd_ms
+    roof = {"bound": "tensor", "kernel": dom, "achieved": ach, "peak": tf_burst, "unit": "TFLOP/s",
+            "frac": ach / tf_burst, "traffic": traffic,
+            "peak_kind": f"{src} bf16 burst (frac_sustained uses {tf_sus})", "frac_sustained": ach / tf_sus,
+            "step_achieved": (fl_fwd + fl_bwd) / (rank_ms / 1e3) / 1e12,
+            "step_frac": (fl_fwd + fl_bwd) / (rank_ms / 1e3) / 1e12 / tf_burst,
             "flops_per_step": fl_fwd + fl_bwd, "n_att_per_bh": natt, **phases}
 
     # ---- end to end through the C ABI from pinned host buffers
     e2e = None
     if not args.no_e2e:
-        hq, hk, hv, hdo = (t.cpu().pin_memory() for t in (q, k, v, do))
-        hu = u.cpu().pin_memory()
-        outs = [torch.empty_like(x, device="cpu").pin_memory() for x in (q, q, q, q)]
-        hdu = torch.empty_like(hu).pin_memory()
+        e2e = e2e_timing(torch, ops, blk, args.steps, world, dev, tokens)
 
-        # Three streams, double-buffered device inputs and outputs: the H2D of
-        # step i+1 and the D2H of step i-1 overlap the kernels of step i (PCIe is
-        # full duplex). Every step still moves all of its inputs in and all of
-        # its results out inside the timed region.
-        s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
-        dbuf = [[torch.empty_like(x) for x in (q, k, v, do, u)] for _ in range(2)]
-        obuf = [None, None]
-        ev_in = [torch.cuda.Event() for _ in range(2)]
-        ev_done = [torch.cuda.Event() for _ in range(2)]
-        ev_out = [torch.cuda.Event() for _ in range(2)]
+    # ---- gather-inclusive time (N > 1): O/dQ/dK/dV all-gathered over the
+    # ranks sharing a sequence after every step
+    gather = None
+    if world > 1 and du_group is not None:
+        from paper_2406_16747_b200.parallel import gather_heads
 
-        def h2d(i):
-            bi = i & 1
-            with torch.cuda.stream(s_in):
-                s_in.wait_event(ev_done[bi])  # the compute of step i-2 no longer reads this buffer
-                for dst, src in zip(dbuf[bi], (hq, hk, hv, hdo, hu)):
-                    dst.copy_(src, non_blocking=True)
-                ev_in[bi].record(s_in)
-
-        def compute(i):
-            bi = i & 1
-            st.wait_event(ev_in[bi])
-            st.wait_event(ev_out[bi])  # the D2H of step i-2 has drained this output slot
-            dq_, dk_, dv_, ddo, du_ = dbuf[bi]
-            sel = ops.select(du_, cfg, heads=H, head_dim=d, dtype=torch.bfloat16)
-            o, lse, _ = ops.attn_fwd(dq_, dk_, dv_, du_, cfg, sel=sel)
-            gq, gk, gv, gu = ops.attn_bwd(dq_, dk_, dv_, o, ddo, lse, du_, sel, cfg, ws=bws)
-            obuf[bi] = (o, gq, gk, gv, gu)
-            ev_done[bi].record(st)
-
-        def d2h(i):
-            bi = i & 1
-            with torch.cuda.stream(s_out):
-                s_out.wait_event(ev_done[bi])
-                for hst, dvt in zip(outs + [hdu], obuf[bi]):
-                    hst.copy_(dvt, non_blocking=True)
-                ev_out[bi].record(s_out)
-
-        def run(n):
-            h2d(0)
-            for i in range(n):
-                if i + 1 < n:
-                    h2d(i + 1)
-                compute(i)
-                d2h(i)
-
-        for e in ev_done + ev_out:
-            e.record(st)
-        run(2)
+        st = torch.cuda.current_stream()
+        dist.barrier()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(st)
+        for _ in range(args.steps):
+            outs = blk.step(st)
+            for x in outs[:4]:
+                gather_heads(x, du_group)
+        g1.record(st)
         torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        n_e2e = max(3, args.steps)  # pipeline fill (first H2D) and drain (last D2H) amortised over the run
-        a0 = torch.cuda.Event(enable_timing=True)
-        a1 = torch.cuda.Event(enable_timing=True)
-        a0.record(st)
-        s_in.wait_stream(st)  # no copy of the timed steps starts before a0
-        s_out.wait_stream(st)
-        run(n_e2e)
-        st.wait_stream(s_out)
-        a1.record(st)
-        torch.cuda.synchronize()
-        e_ms = a0.elapsed_time(a1) / n_e2e
-        if world > 1:
-            t = torch.tensor([e_ms], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e_ms = float(t.item())
-        h2d = sum(x.numel() * x.element_size() for x in (hq, hk, hv, hdo, hu))
-        d2h = sum(x.numel() * x.element_size() for x in outs) + hdu.numel() * 8
-        e2e = {"value": tokens / (e_ms / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "ms_per_step": e_ms,
-               "pipelining": "H2D(i+1) and D2H(i-1) overlap the kernels of step i on separate streams"}
+        gms = torch.tensor([g0.elapsed_time(g1) / args.steps], device=dev, dtype=torch.float64)
+        dist.all_reduce(gms, op=dist.ReduceOp.MAX)
+        gather = {"ms_per_step": float(gms.item()), "value": tokens / (float(gms.item()) / 1e3),
+                  "what": "step + all-gather of O, dQ, dK, dV over the ranks sharing each sequence"}
 
-    # ---- CPU baseline (rank 0, N=1 only)
+    # ---- CPU baseline and secondary configurations (rank 0, N=1 only)
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        try:
-            threads = max(1, os.cpu_count() or 1)
-            tps, secs, units = cpu_reference_sample(threads, L)
-            cpu = {"value": tps, "unit": "tokens/s", "cores": threads, "kind": "reference",
-                   "sample": f"{units} single-head units (d=128,k=1024,w=512,L={L}) fwd+bwd of the "
-                             f"reference <float> path, one std::thread each, {secs:.1f}s; scaled to "
-                             f"B*H=64 units"}
-        except Exception as e:  # the checker is optional on a box without oracle/_ref
-            cpu = {"value": None, "unit": "tokens/s", "cores": 0, "kind": "reference",
-                   "sample": f"unavailable: {e}"}
-
-    # this repo's kernels per step, counted once (CUPTI) outside the timed region
-    try:
-        launches_per_step = count_skb_launches(torch, step)
-    except Exception:  # profiler unavailable: the static count of skb_select/attn_fwd/attn_bwd
-        launches_per_step = 17
+    secondary = None
+    if rank == 0 and world == 1:
+        if not args.no_cpu_baseline:
+            try:
+                threads = max(1, os.cpu_count() or 1)
+                tps, secs, units = cpu_reference_sample(threads, L)
+                cpu = {"value": tps, "unit": "tokens/s", "cores": threads, "kind": "reference",
+                       "sample": f"{units} single-head units (d=128,k=1024,w=512,L={L}) fwd+bwd of the "
+                                 f"reference <float> path, one std::thread each, {secs:.1f}s; scaled to "
+                                 f"B*H=64 units"}
+            except Exception as e:  # the checker is optional on a box without oracle/_ref
+                cpu = {"value": None, "unit": "tokens/s", "cores": 0, "kind": "reference",
+                       "sample": f"unavailable: {e}"}
+        if not args.no_secondary:
+            secondary = run_secondary(torch, ops, dev, args, blk, ms_step)
+    launches_per_step = count_skb_launches(torch, lambda: blk.step(torch.cuda.current_stream()))
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": "cfg3: B=2 H=32 L=16384 d=128 k=1024 w=512 per GPU, bf16 fwd+bwd "
-                               "(select + attention + selection pullback)",
-                   "global_batch": B * world, "seq_len": L, "heads": H, "head_dim": d, "k": kb,
-                   "window": w, "scores": args.scores,
-                   "l2": "inputs 1.07 GB/rank > 126 MB L2 (no flush needed)",
-                   "parallelism": f"(B,H)-sharded weak scaling x{world}"},
-        "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+        "config": {"workload": "cfg3: B=2 H=32 L=16384 d=128 k=1024 w=512, bf16 fwd+bwd (select + attention "
+                               "+ selection pullback), fixed total work split over the GPUs by (b, h)",
+                   "global_batch": B, "seq_len": L, "heads": H, "head_dim": d, "k": kb,
+                   "window": w, "scores": args.scores, "rank_block": {"b": [b0, b1], "h": [h0, h1]},
+                   "l2": "inputs 1.07 GB > 126 MB L2 (no flush needed)",
+                   "parallelism": f"(B,H) head-sharded x{world}" + (", du all-reduce per sequence" if world > 1 else "")},
+        "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gather_inclusive": gather,
+        "secondary": secondary,
         "gpu_launches": launches_per_step * args.steps, "clocks": clk.summary(),
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_secondary(torch, ops, dev, args, blk, full_ms):
+    """Driver-visible secondary numbers (one JSON object): iid-score cfg3, cfg2
+    fwd+bwd, the per-rank share of cfg3 at N=2/4/8 timed on this GPU (the
+    strong-scaling projection without the du all-reduce), and cfg4 decode with
+    the reference generate_step on the host."""
+    out = {}
+    try:
+        out["cfg3_iid"] = secondary_train(torch, ops, dev, CFG, "iid", args.steps, args.warmup,
+                                          "cfg3 B=2 H=32 L=16384 d=128 k=1024 w=512, iid scores")
+        out["cfg2"] = secondary_train(torch, ops, dev, CFG2, "recency", args.steps, args.warmup,
+                                      "cfg2 B=8 H=12 L=4096 d=64 k=256 w=256, bf16 fwd+bwd")
+        proj = {}
+        for n in (2, 4, 8):
+            from paper_2406_16747_b200.parallel import unit_shard
+
+            (b, h0, h1), = unit_shard(CFG["B"], CFG["H"], n, 0)
+            sh = TrainBlock(torch, ops, dev, CFG, args.scores, b, b + 1, h0, h1, seed=5)
+            ms, ph = sh.time(args.steps, args.warmup)
+            proj[f"n{n}"] = {"share": f"b={b} heads [{h0},{h1})", "ms_per_step": ms, **ph,
+                             "projected_speedup": full_ms / ms}
+            del sh
+        out["strong_scaling_projection"] = proj
+        torch.cuda.empty_cache()
+        ms, t_pre, cache = decode_timing(torch, ops, dev, args.steps, args.warmup)
+        dec = decode_summary(ms, t_pre, cache)
+        del cache
+        torch.cuda.empty_cache()
+        if not args.no_cpu_baseline:
+            dec["cpu_baseline"] = cpu_decode_sample(max(1, os.cpu_count() or 1))
+        out["cfg4_decode"] = dec
+    except Exception as e:  # a secondary failure must not lose the headline line
+        out["error"] = repr(e)
+    return out
+
+
+def e2e_timing(torch, ops, blk, steps, world, dev, tokens):
+    """The step end to end from pinned host buffers: every step copies its
+    inputs in and all its results out inside the timed region."""
+    import torch.distributed as dist
+
+    st = torch.cuda.current_stream()
+    cfg, H, d = blk.cfg, blk.H, blk.C["d"]
+    hq, hk, hv, hdo = (t.cpu().pin_memory() for t in (blk.q, blk.k, blk.v, blk.do))
+    hu = blk.u.cpu().pin_memory()
+    outs = [torch.empty_like(x, device="cpu").pin_memory() for x in (blk.q,) * 4]
+    hdu = torch.empty_like(hu).pin_memory()
+
+    # Three streams, double-buffered device inputs and outputs: the H2D of
+    # step i+1 and the D2H of step i-1 overlap the kernels of step i (PCIe is
+    # full duplex). Every step still moves all of its inputs in and all of
+    # its results out inside the timed region.
+    s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+    dbuf = [[torch.empty_like(x) for x in (blk.q, blk.k, blk.v, blk.do, blk.u)] for _ in range(2)]
+    obuf = [None, None]
+    ev_in = [torch.cuda.Event() for _ in range(2)]
+    ev_done = [torch.cuda.Event() for _ in range(2)]
+    ev_out = [torch.cuda.Event() for _ in range(2)]
+
+    def h2d(i):
+        bi = i & 1
+        with torch.cuda.stream(s_in):
+            s_in.wait_event(ev_done[bi])  # the compute of step i-2 no longer reads this buffer
+            for dst, src in zip(dbuf[bi], (hq, hk, hv, hdo, hu)):
+                dst.copy_(src, non_blocking=True)
+            ev_in[bi].record(s_in)
+
+    def compute(i):
+        bi = i & 1
+        st.wait_event(ev_in[bi])
+        st.wait_event(ev_out[bi])  # the D2H of step i-2 has drained this output slot
+        dq_, dk_, dv_, ddo, du_ = dbuf[bi]
+        sel = ops.select(du_, cfg, heads=H, head_dim=d, dtype=torch.bfloat16)
+        o, lse, _ = ops.attn_fwd(dq_, dk_, dv_, du_, cfg, sel=sel)
+        gq, gk, gv, gu = ops.attn_bwd(dq_, dk_, dv_, o, ddo, lse, du_, sel, cfg, ws=blk.bws)
+        if blk.du_group is not None:
+            from paper_2406_16747_b200.parallel import allreduce_du
+
+            allreduce_du(gu, blk.du_group)
+        obuf[bi] = (o, gq, gk, gv, gu)
+        ev_done[bi].record(st)
+
+    def d2h(i):
+        bi = i & 1
+        with torch.cuda.stream(s_out):
+            s_out.wait_event(ev_done[bi])
+            for hst, dvt in zip(outs + [hdu], obuf[bi]):
+                hst.copy_(dvt, non_blocking=True)
+            ev_out[bi].record(s_out)
+
+    def run(n):
+        h2d(0)
+        for i in range(n):
+            if i + 1 < n:
+                h2d(i + 1)
+            compute(i)
+            d2h(i)
+
+    for e in ev_done + ev_out:
+        e.record(st)
+    run(2)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    n_e2e = max(3, steps)  # pipeline fill (first H2D) and drain (last D2H) amortised over the run
+    a0 = torch.cuda.Event(enable_timing=True)
+    a1 = torch.cuda.Event(enable_timing=True)
+    a0.record(st)
+    s_in.wait_stream(st)  # no copy of the timed steps starts before a0
+    s_out.wait_stream(st)
+    run(n_e2e)
+    st.wait_stream(s_out)
+    a1.record(st)
+    torch.cuda.synchronize()
+    e_ms = a0.elapsed_time(a1) / n_e2e
+    if world > 1:
+        t = torch.tensor([e_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e_ms = float(t.item())
+    h2d_b = sum(x.numel() * x.element_size() for x in (hq, hk, hv, hdo, hu))
+    d2h_b = sum(x.numel() * x.element_size() for x in outs) + hdu.numel() * 8
+    return {"value": tokens / (e_ms / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d_b,
+            "d2h_bytes_per_step": d2h_b, "ms_per_step": e_ms,
+            "pipelining": "H2D(i+1) and D2H(i-1) overlap the kernels of step i on separate streams"}
 
 
 if __name__ == "__main__":

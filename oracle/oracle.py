@@ -473,6 +473,15 @@ class Reference:
         return secs.value
 
 
+    def bench_decode(self, units, threads, prompt, steps, p, k, window, seed=1):
+        """Seconds for `steps` generate_step calls on each of `units` single-head
+        caches prefilled with `prompt` rows (ref_bench_decode)."""
+        secs = C.c_double()
+        self._rc(self.lib.ref_bench_decode(C.c_uint64(units), C.c_uint64(threads), C.c_uint64(prompt),
+                                           C.c_uint64(steps), C.c_uint64(p), C.c_double(k),
+                                           C.c_uint64(window), C.c_uint64(seed), C.byref(secs)))
+        return secs.value
+
 def core_problem_via_reference(ref: Reference, Q, K, V, u_or_w, dO, *, kbudget, window,
                                key_mode="hard", mask_mode="soft", norm_mode="none",
                                slope_enabled=False, slope_eps=0.01,

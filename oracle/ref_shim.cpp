@@ -585,4 +585,74 @@ int ref_bench_units(uint64_t units, uint64_t threads, uint64_t L, uint64_t p, do
     REF_GUARD_END
 }
 
+// CPU decode baseline: `units` independent single-head caches (heads=1,
+// D=p), each prefilled with forward_chunk over `prompt` rows and then timed
+// over `steps` generate_step calls (proj/src/cache.cpp:570-577), float, one
+// std::thread per unit with at most `threads` in flight. Once the prompt
+// exceeds floor(k)+w the per-step work is O(k+w) regardless of the context.
+// Returns the wall seconds of the generate_step phase in *secs.
+int ref_bench_decode(uint64_t units, uint64_t threads, uint64_t prompt, uint64_t steps, uint64_t p, double k,
+                     uint64_t window, uint64_t seed, double* secs) {
+    REF_GUARD_BEGIN
+    AttnConfig cfg;
+    cfg.k = k;
+    cfg.window = window;
+    cfg.heads = 1;
+    struct Unit {
+        AttnParams<float> params;
+        ScoringParams scoring;
+        std::unique_ptr<SparseKvCache<float>> cache;
+        std::vector<std::vector<float>> rows;
+    };
+    std::vector<Unit> us(units);
+    std::vector<std::string> errs(units);
+    auto prep = [&](uint64_t u) {
+        try {
+            Rng rng(seed + 104729 * u);
+            Unit& un = us[u];
+            const double s = 0.6 / std::sqrt(static_cast<double>(p));
+            for (MatT<float>* m : {&un.params.wq, &un.params.wk, &un.params.wv, &un.params.wo}) {
+                *m = MatT<float>(p, p);
+                for (auto& v : m->data) v = static_cast<float>(s * rng.normal());
+            }
+            un.scoring.w_score.resize(p);
+            for (auto& v : un.scoring.w_score) v = rng.normal() / std::sqrt(static_cast<double>(p));
+            MatT<float> x(prompt, p);
+            for (auto& v : x.data) v = static_cast<float>(rng.normal());
+            un.cache = std::make_unique<SparseKvCache<float>>(cfg, p, un.scoring);
+            (void)un.cache->forward_chunk(x, un.params);
+            un.rows.assign(steps, std::vector<float>(p));
+            for (auto& r : un.rows)
+                for (auto& v : r) v = static_cast<float>(rng.normal());
+        } catch (const std::exception& e) {
+            errs[u] = e.what();
+        }
+    };
+    auto work = [&](uint64_t u) {
+        try {
+            Unit& un = us[u];
+            for (uint64_t i = 0; i < steps; ++i) (void)generate_step(*un.cache, un.rows[i], un.params);
+        } catch (const std::exception& e) {
+            errs[u] = e.what();
+        }
+    };
+    auto fan = [&](auto fn) {
+        for (uint64_t base = 0; base < units; base += threads) {
+            std::vector<std::thread> pool;
+            for (uint64_t u = base; u < std::min(units, base + threads); ++u) pool.emplace_back(fn, u);
+            for (auto& th : pool) th.join();
+        }
+    };
+    fan(prep);
+    for (auto& e : errs)
+        if (!e.empty()) throw NumericError(e);
+    const auto t0 = std::chrono::steady_clock::now();
+    fan(work);
+    const auto t1 = std::chrono::steady_clock::now();
+    for (auto& e : errs)
+        if (!e.empty()) throw NumericError(e);
+    *secs = std::chrono::duration<double>(t1 - t0).count();
+    REF_GUARD_END
+}
+
 }  // extern "C"

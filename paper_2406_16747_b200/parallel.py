@@ -46,6 +46,16 @@ def unit_shard(B: int, H: int, world: int, rank: int) -> list[tuple[int, int, in
     return out
 
 
+def seq_ranks(B: int, H: int, world: int) -> dict[int, list[int]]:
+    """Sequence b -> the ranks whose unit_shard blocks hold heads of b (the
+    ranks that all-reduce du[b])."""
+    out: dict[int, list[int]] = {}
+    for r in range(world):
+        for b, _, _ in unit_shard(B, H, world, r):
+            out.setdefault(b, []).append(r)
+    return out
+
+
 def allreduce_du(du: torch.Tensor, group=None) -> torch.Tensor:
     """Sum the per-rank selection-pullback partials du[b, :] in place."""
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:

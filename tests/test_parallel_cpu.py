@@ -37,6 +37,15 @@ def test_unit_shard_cfg3_layout():
         assert units == [(b, h) for b in range(B) for h in range(H)]
 
 
+def test_seq_ranks_groups():
+    from paper_2406_16747_b200.parallel import seq_ranks
+
+    assert seq_ranks(2, 32, 1) == {0: [0], 1: [0]}
+    assert seq_ranks(2, 32, 2) == {0: [0], 1: [1]}
+    assert seq_ranks(2, 32, 4) == {0: [0, 1], 1: [2, 3]}
+    assert seq_ranks(2, 32, 8) == {0: [0, 1, 2, 3], 1: [4, 5, 6, 7]}
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
