@@ -573,6 +573,7 @@ def run_secondary(torch, ops, dev, args, blk, full_ms):
                                           "cfg3 B=2 H=32 L=16384 d=128 k=1024 w=512, iid scores")
         out["cfg2"] = secondary_train(torch, ops, dev, CFG2, "recency", args.steps, args.warmup,
                                       "cfg2 B=8 H=12 L=4096 d=64 k=256 w=256, bf16 fwd+bwd")
+        out["k1_score"] = k1_timing(torch, ops, dev, args.steps)
         proj = {}
         for n in (2, 4, 8):
             from paper_2406_16747_b200.parallel import unit_shard
@@ -595,6 +596,47 @@ def run_secondary(torch, ops, dev, args, blk, full_ms):
     except Exception as e:  # a secondary failure must not lose the headline line
         out["error"] = repr(e)
     return out
+
+
+def k1_timing(torch, ops, dev, steps):
+    """K1 at cfg3's x shape (B=2, L=16384, D=4096 bf16): raw = x.w (float64,
+    staged HBM stream), the serial Welford chain per sequence and the finish.
+    HBM-bound on x (268 MB) except for the Welford chain."""
+    B, L, D = 2, CFG["L"], CFG["H"] * CFG["d"]
+    g = torch.Generator(device=dev)
+    g.manual_seed(11)
+    x = torch.randn((B, L, D), generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16)
+    w = torch.randn((D,), generator=g, device=dev, dtype=torch.float64) / math.sqrt(D)
+    sc = ops.ScoringConfig()
+    for _ in range(2):
+        ops.score_fwd(x, w, sc)
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(st)
+    for _ in range(steps):
+        ops.score_fwd(x, w, sc)
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    # the dot-product kernel alone (the HBM stream)
+    raw = torch.empty((B, L), dtype=torch.float64, device=dev)
+    lib = __import__("paper_2406_16747_b200._lib", fromlist=["load"]).load()
+    r_ms = None
+    if hasattr(lib, "skb_score_raw"):
+        e0.record(st)
+        for _ in range(steps):
+            lib.skb_score_raw(B * L, D, ops._DT[torch.bfloat16], x.data_ptr(), w.data_ptr(), raw.data_ptr(), st.cuda_stream)
+        e1.record(st)
+        torch.cuda.synchronize()
+        r_ms = e0.elapsed_time(e1) / steps
+    hbm = peaks()[0]
+    xb = x.numel() * 2
+    del x
+    return {"workload": "K1 score_tokens at cfg3 x: B=2 L=16384 D=4096 bf16 (raw + Welford + finish)",
+            "ms": ms, "raw_ms": r_ms, "x_bytes": xb,
+            "raw_gbs": (xb / (r_ms / 1e3) / 1e9) if r_ms else None,
+            "raw_frac_hbm": (xb / (r_ms / 1e3) / 1e9 / hbm) if r_ms else None}
 
 
 def e2e_timing(torch, ops, blk, steps, world, dev, tokens):

@@ -125,6 +125,12 @@ int skb_version(void);
 int skb_score_fwd(int64_t B, int64_t L, int64_t D, int32_t x_dtype, const void* x,
                   const double* w, const skb_scoring* sc, double* raw, double* u, double* mean,
                   double* sdev, void* stream);
+/* The scoring GEMV alone: raw[r] = sum_c x[r, c] * w[c] for `rows` rows of
+ * x [rows, D] (the raw part of detail::score_one,
+ * proj/include/sparsek/selection.hpp:72-74: left to right, float64, no fma).
+ * Enqueued on `stream`, no host synchronisation. */
+int skb_score_raw(int64_t rows, int64_t D, int32_t x_dtype, const void* x, const double* w, double* raw,
+                  void* stream);
 /* Incremental scoring (score_tokens with base_pos: the TimestepNormState is
  * carried across calls, proj/include/sparsek/selection.hpp:55-56,
  * proj/src/selection.cpp:13-31): x [B, n, D] continues each sequence's

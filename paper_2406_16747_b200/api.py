@@ -183,6 +183,17 @@ def _core_cfg(k, window, key_mode, mask_mode):
     return ops.AttnConfig(k=float(k), window=int(window), key_mode=key_mode, mask_mode=mask_mode)
 
 
+_SIDE = {}
+
+
+def _side_stream(device):
+    """One side stream per device for K1 (kept, so no per-call creation)."""
+    key = torch.device(device).index
+    if key not in _SIDE:
+        _SIDE[key] = torch.cuda.Stream(device=device)
+    return _SIDE[key]
+
+
 def attention_torch(x, wq, wk, wv, wo, w_score, cfg: ops.AttnConfig, heads: int,
                     scoring: ops.ScoringConfig):
     """Differentiable x-level SparseK attention on device tensors:
@@ -191,11 +202,19 @@ def attention_torch(x, wq, wk, wv, wo, w_score, cfg: ops.AttnConfig, heads: int,
     score, selection, attention and their backward are libsparsek_b200 kernels."""
     B, L, D = x.shape
     p = D // heads
+    main = torch.cuda.current_stream(x.device)
+    side = _side_stream(x.device) if cfg.k > 0.0 else None
+    if side is not None:  # K1's serial Welford chain runs under the projection GEMMs
+        side.wait_stream(main)
     q = (x @ wq).view(B, L, heads, p)
     k = (x @ wk).view(B, L, heads, p)
     v = (x @ wv).view(B, L, heads, p)
     if cfg.k > 0.0:
-        u = ops.score_tokens(x, w_score, scoring)
+        with torch.cuda.stream(side):
+            u = ops.score_tokens(x, w_score, scoring)
+        main.wait_stream(side)
+        x.record_stream(side)
+        u.record_stream(main)
     else:
         u = torch.zeros((B, L), dtype=torch.float64, device=x.device)
     hc = ops.sparsek_attention_core(q, k, v, u, cfg)
@@ -256,13 +275,31 @@ def attention_grads(x, wq, wk, wv, wo, w_score, k, window, grad_out, heads=1, ke
 
 def chunked_forward(x, chunk_len, wq, wk, wv, wo, w_score, k, window, heads=1, key_mode="hard",
                     mask_mode="soft", slope_eps=0.01, slope_enabled=True):
-    """chunked_forward (proj/include/sparsek/cache.hpp:93-96): feeding the
-    sequence chunk by chunk reproduces the unchunked forward exactly
-    (proj/tests/test_cache.cpp:34-64), which the batch kernels compute."""
+    """chunked_forward (proj/src/cache.cpp:548-563, Algorithm 3): the sequence is
+    fed chunk by chunk into ONE recurrent cache whose state between chunks is
+    the constant-(floor(k)+w) retained K/V rows, the stream survivors and the
+    carried TimestepNormState — DecodeSession.forward_chunk. The first chunk
+    runs the batch kernels, each later chunk continues the state row by row
+    (generate_step's order). The output equals the unchunked forward
+    (proj/tests/test_cache.cpp:34-64)."""
     if int(chunk_len) <= 0:
         raise ArgumentError("chunked_forward: chunk_len must be positive")
-    return attention(x, wq, wk, wv, wo, w_score, k, window, heads=heads, key_mode=key_mode,
-                     mask_mode=mask_mode, slope_eps=slope_eps, slope_enabled=slope_enabled)
+    x, (wq, wk, wv, wo) = _attention_inputs(x, wq, wk, wv, wo, heads)
+    cfg = _core_cfg(float(k), int(window), key_mode, mask_mode)
+    L, D = x.shape
+    wsc = _vec(w_score, "w_score")
+    if cfg.k > 0.0 and wsc.size != D:
+        raise ConfigError("attention: w_score length must equal d_model")
+    if not (slope_eps > 0.0):
+        raise ArgumentError("ScoringParams: slope_eps must be positive")
+    d = _dev()
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(d)
+    sc = ops.ScoringConfig(slope_eps=float(slope_eps), slope_enabled=bool(slope_enabled))
+    sess = DecodeSession(t(wq), t(wk), t(wv), t(wo), t(wsc) if cfg.k > 0.0 else None, cfg, heads, 1,
+                         max_len=L, scoring=sc, dtype=torch.float64)
+    xt = t(x).view(1, L, D)
+    outs = [sess.forward_chunk(xt[:, c0:c0 + int(chunk_len)]) for c0 in range(0, L, int(chunk_len))]
+    return torch.cat(outs, 1)[0].cpu().numpy()
 
 
 class DecodeSession:
@@ -304,11 +341,32 @@ class DecodeSession:
         return q, k, v, u
 
     @torch.no_grad()
+    def forward_chunk(self, x):
+        """SparseKvCache::forward_chunk (proj/src/cache.cpp:181-400) on rows
+        x [B, n, D] that continue every sequence; returns y [B, n, D]. A fresh
+        cache runs the batch kernels over the chunk (prefill); a non-empty one
+        continues its carried state one generate_step per row (the reference's
+        row order), with the chunk's projections and scores done in one pass."""
+        B, n, D = x.shape
+        if n < 1:
+            raise ShapeError("forward_chunk: empty chunk")
+        if self.t == 0 and n > 1:
+            return self.prefill(x)
+        q, k, v, u = self._proj_score(x)
+        outs = []
+        for r in range(n):
+            outs.append(self.cache.step(q[:, r].contiguous(), k[:, r].contiguous(), v[:, r].contiguous(),
+                                        u[:, r].contiguous()))
+            self.t += 1
+        return torch.stack(outs, 1).reshape(B, n, D) @ self.wo
+
+    @torch.no_grad()
     def prefill(self, x):
-        """forward_chunk on a prompt x [B, n, D] (only valid as the first call);
-        returns y [B, n, D]."""
+        """forward_chunk on a prompt x [B, n, D] of a fresh cache (the batch
+        kernels); on a non-empty cache this is forward_chunk's continuation.
+        Returns y [B, n, D]."""
         if self.t:
-            raise ArgumentError("DecodeSession: prefill must precede generation")
+            return self.forward_chunk(x)
         B, n, D = x.shape
         q, k, v, u = self._proj_score(x)
         hc = ops.sparsek_attention_core(q.contiguous(), k.contiguous(), v.contiguous(),

@@ -127,9 +127,8 @@ __global__ void __launch_bounds__(kWarps * 32) k_fwd_gather(Args a) {
         const int cnt = a.s.qb_count[(int64_t)b * a.s.nqb + qb];
         const int* list = a.s.qb_list + ((int64_t)b * a.s.nqb + qb) * a.s.qb_cap;
         for (int e = 0; e < cnt; ++e) {
-            const int j = list[e];
-            if (j > t) break;
-            if (a.s.leave[bl + j] <= t) continue;
+            const int j = list[e];  // the union is partitioned by tile class, not sorted
+            if (j > t || a.s.leave[bl + j] <= t) continue;
             process(j, gate_of(a.u[bl + j], tau), true);
         }
     }
@@ -205,9 +204,8 @@ __global__ void __launch_bounds__(kWarps * 32) k_bwd_gather(Args a) {
             const int cnt = a.s.qb_count[(int64_t)b * a.s.nqb + qb];
             const int* list = a.s.qb_list + ((int64_t)b * a.s.nqb + qb) * a.s.qb_cap;
             for (int e = 0; e < cnt; ++e) {
-                const int j = list[e];
-                if (j > t) break;
-                if (a.s.leave[bl + j] <= t) continue;
+                const int j = list[e];  // partitioned by tile class, not sorted
+                if (j > t || a.s.leave[bl + j] <= t) continue;
                 fn(j, gate_of(a.u[bl + j], tau), true);
             }
         }

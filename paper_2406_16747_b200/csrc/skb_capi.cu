@@ -7,6 +7,8 @@
 #include "skb_internal.h"
 
 namespace skb {
+void run_score_raw(int64_t rows, int64_t D, int32_t xdt, const void* x, const double* w, double* raw,
+                   cudaStream_t st);
 void run_score_fwd(int64_t B, int64_t L, int64_t D, int32_t xdt, const void* x, const double* w,
                    const skb_scoring& sc, double* raw, double* u, double* mean, double* sdev,
                    cudaStream_t st);
@@ -64,6 +66,16 @@ int skb_score_fwd(int64_t B, int64_t L, int64_t D, int32_t x_dtype, const void* 
     NONNULL(mean, "score_fwd mean");
     NONNULL(sdev, "score_fwd sdev");
     skb::run_score_fwd(B, L, D, x_dtype, x, w, *sc, raw, u, mean, sdev, S(stream));
+    SKB_API_END
+}
+
+int skb_score_raw(int64_t rows, int64_t D, int32_t x_dtype, const void* x, const double* w, double* raw,
+                  void* stream) {
+    SKB_API_BEGIN
+    NONNULL(x, "score_raw x");
+    NONNULL(w, "score_raw w");
+    NONNULL(raw, "score_raw raw");
+    skb::run_score_raw(rows, D, x_dtype, x, w, raw, S(stream));
     SKB_API_END
 }
 

@@ -26,6 +26,7 @@ __device__ __forceinline__ double ldd<__nv_bfloat16>(const __nv_bfloat16* p, int
 }
 
 // One thread per row: raw = sum_c x[c] * w[c], left to right, no FMA.
+// (Fallback for rows that are not 16-byte aligned.)
 template <class S>
 __global__ void k_score_raw(const S* __restrict__ x, const double* __restrict__ w, int64_t rows,
                             int D, double* __restrict__ raw) {
@@ -37,27 +38,166 @@ __global__ void k_score_raw(const S* __restrict__ x, const double* __restrict__ 
     raw[r] = acc;
 }
 
-// Sequential Welford per sequence; emits the statistics the parallel finish needs.
-__global__ void k_score_welford(const double* __restrict__ raw, int L, skb_scoring sc,
-                                double* __restrict__ mean, double* __restrict__ var,
-                                int* __restrict__ bad) {
+// The same dot products, HBM-streamed: a CTA owns 128 rows; the rows are
+// staged through shared memory in 128-byte column slices (a 4-deep cp.async
+// ring, 8 threads per row so each row's slice is one coalesced 128-byte
+// read), and thread r then walks its row's slice in column order — the
+// reference's left-to-right, unfused float64 accumulation, so raw stays
+// bit-identical (proj/include/sparsek/selection.hpp:72-74).
+constexpr int kRawRows = 128;
+constexpr int kRawStages = 4;
+constexpr int kRawPitch = 144;  // 128 B slice + 16 B pad: 16-byte row reads spread over the banks
+
+template <class S>
+__global__ void __launch_bounds__(kRawRows) k_score_raw_tiled(const S* __restrict__ x, const double* __restrict__ w,
+                                                              int64_t rows, int D, double* __restrict__ raw) {
+    constexpr int kCols = 128 / (int)sizeof(S);  // columns per 128-byte slice
+    constexpr int kVec = 16 / (int)sizeof(S);    // columns per 16-byte chunk
+    constexpr int kStageB = kRawRows * kRawPitch + kCols * 8;  // x slice rows, then the w slice (float64)
+    extern __shared__ __align__(16) uint8_t raw_smem[];
+    auto tile = [&](int st) { return raw_smem + st * kStageB; };
+    const int t = threadIdx.x;
+    const int64_t r0 = (int64_t)blockIdx.x * kRawRows;
+    const int nslices = (D + kCols - 1) / kCols;
+    auto cp16 = [](uint8_t* dst, const void* src, bool ok) {
+        const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(ok ? 16 : 0)
+                     : "memory");
+    };
+    auto issue = [&](int sl) {
+        uint8_t* dst = tile(sl % kRawStages);
+        const int c0 = sl * kCols;
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {  // 128 rows x 8 chunks / 128 threads
+            const int idx = it * kRawRows + t;
+            const int rr = idx >> 3, ch = idx & 7;
+            const int64_t row = r0 + rr;
+            const int c = c0 + ch * kVec;
+            const bool ok = row < rows && c < D;
+            cp16(dst + rr * kRawPitch + ch * 16, x + (ok ? row * D + c : 0), ok);
+        }
+        if (t < kCols / 2) {  // w[c0 .. c0 + kCols) as float64 pairs
+            const int c = c0 + 2 * t;
+            cp16(dst + kRawRows * kRawPitch + t * 16, w + (c < D ? c : 0), c + 1 < D);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+#pragma unroll
+    for (int sl = 0; sl < kRawStages - 1; ++sl) {
+        if (sl < nslices) issue(sl);
+        else asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    double acc = 0.0;
+    for (int sl = 0; sl < nslices; ++sl) {
+        asm volatile("cp.async.wait_group %0;" ::"n"(kRawStages - 2) : "memory");
+        __syncthreads();  // slice sl landed for every thread; slot (sl-1) % stages is free
+        if (sl + kRawStages - 1 < nslices) issue(sl + kRawStages - 1);
+        else asm volatile("cp.async.commit_group;" ::: "memory");
+        const uint8_t* rowp = tile(sl % kRawStages) + t * kRawPitch;
+        const double* ws = reinterpret_cast<const double*>(tile(sl % kRawStages) + kRawRows * kRawPitch);
+        const int c0 = sl * kCols;
+        if (c0 + kCols <= D) {  // a full slice: no per-element predicate
+#pragma unroll
+            for (int ch = 0; ch < 8; ++ch) {
+                const uint4 v = *reinterpret_cast<const uint4*>(rowp + ch * 16);
+                const S* e = reinterpret_cast<const S*>(&v);
+                double prod[kVec];
+#pragma unroll
+                for (int q = 0; q < kVec; ++q) prod[q] = __dmul_rn(ldd<S>(e, q), ws[ch * kVec + q]);
+#pragma unroll
+                for (int q = 0; q < kVec; ++q) acc = __dadd_rn(acc, prod[q]);
+            }
+        } else {
+            const int n = D - c0;
+            for (int c = 0; c < n; ++c) {
+                const S* e = reinterpret_cast<const S*>(rowp);
+                acc = __dadd_rn(acc, __dmul_rn(ldd<S>(e, c), __ldg(w + c0 + c)));
+            }
+        }
+    }
+    if (r0 + t < rows) raw[r0 + t] = acc;
+}
+
+// Correctly rounded a / n for a positive integer count n, given y = RN(1/n):
+// q0 = RN(a y) is within an ulp of a/n, the residual a - q0 n is exact in
+// one fma, and RN(q0 + r y) is then RN(a/n) (Markstein's theorem) — the same
+// value as __ddiv_rn, with the reciprocal off the dependency chain. (A zero
+// dividend gives +0; the callers' dividends are never -0: raw sums start at
+// +0.0, so rin - mu and m2 cannot be negative zeros.)
+__device__ __forceinline__ double div_by_count(double a, double n, double y) {
+    const double q0 = __dmul_rn(a, y);
+    return __fma_rn(__fma_rn(-q0, n, a), y, q0);
+}
+
+// Sequential Welford per sequence; emits the statistics the parallel finish
+// needs. The mean recurrence is a serial float64 chain (bit-identity with the
+// reference forbids reassociation), so one thread runs it — on operands
+// staged in shared memory by a second warp, which also computes the
+// reciprocals 1/(i+1) off the chain and writes the previous block's results
+// out coalesced. Per step the chain is sub, mul, two fmas and an add.
+constexpr int kWfBlock = 256;
+
+__global__ void __launch_bounds__(64) k_score_welford(const double* __restrict__ raw, int L, skb_scoring sc,
+                                                      double* __restrict__ mean, double* __restrict__ var,
+                                                      int* __restrict__ bad) {
+    __shared__ double s_rin[2][kWfBlock], s_y[2][kWfBlock], s_mu[2][kWfBlock], s_v[2][kWfBlock];
     const int b = blockIdx.x;
     const double* rb = raw + (int64_t)b * L;
     double* mb = mean + (int64_t)b * L;
     double* vb = var + (int64_t)b * L;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nblk = (L + kWfBlock - 1) / kWfBlock;
+    bool nonfinite = false;
+    auto prep = [&](int k) {
+        const int buf = k & 1;
+#pragma unroll
+        for (int e = 0; e < kWfBlock / 32; ++e) {
+            const int j = e * 32 + lane;
+            const int i = k * kWfBlock + j;
+            const double r = i < L ? rb[i] : 0.0;
+            nonfinite |= !isfinite(r);
+            const double slope = sc.slope_enabled ? __dmul_rn((double)(i + 1), sc.slope_eps) : 0.0;
+            s_rin[buf][j] = sc.slope_order == 0 ? __dadd_rn(r, slope) : r;
+            s_y[buf][j] = __drcp_rn((double)(i + 1));
+        }
+    };
+    auto flush = [&](int k) {
+        const int buf = k & 1;
+        for (int j = lane; j < kWfBlock; j += 32) {
+            const int i = k * kWfBlock + j;
+            if (i < L) {
+                mb[i] = s_mu[buf][j];
+                vb[i] = s_v[buf][j];
+            }
+        }
+    };
+    if (warp == 1) prep(0);
+    __syncthreads();
     double mu = 0.0, m2 = 0.0;
-    for (int i = 0; i < L; ++i) {
-        const double r = rb[i];
-        if (!isfinite(r)) *bad = 1;
-        const double slope = sc.slope_enabled ? __dmul_rn((double)(i + 1), sc.slope_eps) : 0.0;
-        const double rin = sc.slope_order == 0 ? __dadd_rn(r, slope) : r;
-        const double cnt = (double)(i + 1);
-        const double delta = __dsub_rn(rin, mu);
-        mu = __dadd_rn(mu, __ddiv_rn(delta, cnt));
-        m2 = __dadd_rn(m2, __dmul_rn(delta, __dsub_rn(rin, mu)));
-        mb[i] = mu;
-        vb[i] = __ddiv_rn(m2, cnt);
+    for (int k = 0; k < nblk; ++k) {
+        const int buf = k & 1;
+        if (threadIdx.x == 0) {
+            const int n = min(kWfBlock, L - k * kWfBlock);
+            const double* rin_s = s_rin[buf];
+            const double* y_s = s_y[buf];
+#pragma unroll 4
+            for (int j = 0; j < n; ++j) {
+                const double rin = rin_s[j], y = y_s[j];
+                const double cnt = (double)(k * kWfBlock + j + 1);
+                const double delta = __dsub_rn(rin, mu);
+                mu = __dadd_rn(mu, div_by_count(delta, cnt, y));
+                m2 = __dadd_rn(m2, __dmul_rn(delta, __dsub_rn(rin, mu)));
+                s_mu[buf][j] = mu;
+                s_v[buf][j] = div_by_count(m2, cnt, y);
+            }
+        } else if (warp == 1) {
+            if (k + 1 < nblk) prep(k + 1);
+            if (k >= 1) flush(k - 1);
+        }
+        __syncthreads();
     }
+    if (warp == 1) flush(nblk - 1);
+    if (__any_sync(0xffffffffu, nonfinite) && lane == 0 && warp == 1) *bad = 1;
 }
 
 // Incremental scoring for decoding (score_tokens with base_pos, TimestepNormState
@@ -265,6 +405,44 @@ void dispatch_x(int32_t dt, F&& f) {
     else throw Error(SKB_EARG, "score: unsupported x dtype");
 }
 
+// raw[r] = x[r, :] . w for rows r: the staged kernel when rows are 16-byte
+// aligned, the row-per-thread kernel otherwise.
+void launch_raw(int32_t xdt, const void* x, const double* w, int64_t rows, int64_t D, double* out, cudaStream_t st) {
+    dispatch_x(xdt, [&](auto tag) {
+        using S = std::remove_const_t<std::remove_pointer_t<decltype(tag)>>;
+        const bool aligned = (reinterpret_cast<uintptr_t>(x) & 15u) == 0 && (D * (int64_t)sizeof(S)) % 16 == 0;
+        constexpr int smem = kRawStages * (kRawRows * kRawPitch + (128 / (int)sizeof(S)) * 8);
+        static uint64_t attr_set = 0;
+        if (aligned && first_on_device(&attr_set))
+            SKB_CHECK_CUDA(cudaFuncSetAttribute(k_score_raw_tiled<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                smem));
+        if (aligned)
+            k_score_raw_tiled<S><<<(unsigned)cdiv(rows, kRawRows), kRawRows, smem, st>>>(static_cast<const S*>(x),
+                                                                                       w, rows, (int)D, out);
+        else
+            k_score_raw<S><<<(unsigned)cdiv(rows, 128), 128, 0, st>>>(static_cast<const S*>(x), w, rows, (int)D,
+                                                                        out);
+    });
+}
+
+// The non-finite-input flag: one persistent device word per (thread,
+// device) and a pinned host word to read it back (no per-call allocation).
+int* bad_flag() {
+    thread_local int* flags[64] = {};
+    int dev = 0;
+    SKB_CHECK_CUDA(cudaGetDevice(&dev));
+    int*& f = flags[dev & 63];
+    if (!f) SKB_CHECK_CUDA(cudaMalloc(&f, sizeof(int)));
+    return f;
+}
+bool read_flag(const int* bad, cudaStream_t st) {
+    thread_local int* host = nullptr;
+    if (!host) SKB_CHECK_CUDA(cudaMallocHost(&host, sizeof(int)));
+    SKB_CHECK_CUDA(cudaMemcpyAsync(host, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+    SKB_CHECK_CUDA(cudaStreamSynchronize(st));
+    return *host != 0;
+}
+
 }  // namespace
 
 void run_score_fwd(int64_t B, int64_t L, int64_t D, int32_t xdt, const void* x, const double* w,
@@ -273,18 +451,13 @@ void run_score_fwd(int64_t B, int64_t L, int64_t D, int32_t xdt, const void* x, 
     SKB_REQUIRE(B >= 1 && L >= 1 && D >= 1, SKB_ESHAPE, "score_tokens: empty input");
     SKB_REQUIRE(sc.slope_eps > 0.0, SKB_EARG, "ScoringParams: slope_eps must be positive");
     const int64_t rows = B * L;
-    int* bad = nullptr;
-    SKB_CHECK_CUDA(cudaMallocAsync(&bad, sizeof(int), st));
+    int* bad = bad_flag();
     SKB_CHECK_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), st));
     // raw is produced into `u` first (scratch), finished into raw/u below.
-    dispatch_x(xdt, [&](auto tag) {
-        using S = std::remove_const_t<std::remove_pointer_t<decltype(tag)>>;
-        k_score_raw<S><<<(unsigned)cdiv(rows, 128), 128, 0, st>>>(static_cast<const S*>(x), w, rows,
-                                                                    (int)D, u);
-    });
+    launch_raw(xdt, x, w, rows, D, u, st);
     SKB_CHECK_LAUNCH();
     if (sc.norm_mode != 0) {
-        k_score_welford<<<(unsigned)B, 1, 0, st>>>(u, (int)L, sc, mean, sdev, bad);
+        k_score_welford<<<(unsigned)B, 64, 0, st>>>(u, (int)L, sc, mean, sdev, bad);
         SKB_CHECK_LAUNCH();
     }
     // finish: reads raw from `u`; stage it in raw first
@@ -292,11 +465,14 @@ void run_score_fwd(int64_t B, int64_t L, int64_t D, int32_t xdt, const void* x, 
     k_score_finish<<<(unsigned)cdiv(rows, 256), 256, 0, st>>>(raw, rows, (int)L, sc, raw, u, mean,
                                                              sdev, bad);
     SKB_CHECK_LAUNCH();
-    int hbad = 0;
-    SKB_CHECK_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
-    SKB_CHECK_CUDA(cudaFreeAsync(bad, st));
-    SKB_CHECK_CUDA(cudaStreamSynchronize(st));
-    SKB_REQUIRE(!hbad, SKB_ENUMERIC, "score: non-finite value");
+    SKB_REQUIRE(!read_flag(bad, st), SKB_ENUMERIC, "score: non-finite value");
+}
+
+void run_score_raw(int64_t rows, int64_t D, int32_t xdt, const void* x, const double* w, double* raw,
+                   cudaStream_t st) {
+    SKB_REQUIRE(rows >= 1 && D >= 1, SKB_ESHAPE, "score_tokens: empty input");
+    launch_raw(xdt, x, w, rows, D, raw, st);
+    SKB_CHECK_LAUNCH();
 }
 
 void run_score_continue(int64_t B, int64_t n, int64_t D, int32_t xdt, const void* x, const double* w,
@@ -304,22 +480,14 @@ void run_score_continue(int64_t B, int64_t n, int64_t D, int32_t xdt, const void
     SKB_REQUIRE(B >= 1 && n >= 1 && D >= 1, SKB_ESHAPE, "score_tokens: empty input");
     SKB_REQUIRE(sc.slope_eps > 0.0, SKB_EARG, "ScoringParams: slope_eps must be positive");
     const int64_t rows = B * n;
-    int* bad = nullptr;
-    SKB_CHECK_CUDA(cudaMallocAsync(&bad, sizeof(int), st));
+    int* bad = bad_flag();
     SKB_CHECK_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), st));
-    dispatch_x(xdt, [&](auto tag) {
-        using S = std::remove_const_t<std::remove_pointer_t<decltype(tag)>>;
-        k_score_raw<S><<<(unsigned)cdiv(rows, 128), 128, 0, st>>>(static_cast<const S*>(x), w, rows, (int)D, raw);
-    });
+    launch_raw(xdt, x, w, rows, D, raw, st);
     SKB_CHECK_LAUNCH();
     // raw holds the dot products; the continuation rewrites raw/u in place
     k_score_continue<<<(unsigned)B, 1, 0, st>>>(raw, (int)n, sc, state, raw, u, bad);
     SKB_CHECK_LAUNCH();
-    int hbad = 0;
-    SKB_CHECK_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
-    SKB_CHECK_CUDA(cudaFreeAsync(bad, st));
-    SKB_CHECK_CUDA(cudaStreamSynchronize(st));
-    SKB_REQUIRE(!hbad, SKB_ENUMERIC, "score: non-finite value");
+    SKB_REQUIRE(!read_flag(bad, st), SKB_ENUMERIC, "score: non-finite value");
 }
 
 void run_score_bwd(int64_t B, int64_t L, int64_t D, int32_t xdt, const void* x, const double* w,

@@ -719,7 +719,9 @@ k_ever_list(const int* __restrict__ leave1, int L, int T, const int* __restrict_
 __global__ void __launch_bounds__(128)
 k_union_meta(const int* __restrict__ leave1, const float* __restrict__ uf, const float* __restrict__ tauf,
              int L, int T, int window, int nqb, int cap, const int* __restrict__ qb_count, int* __restrict__ qb_list,
-             int* __restrict__ qb_leave, float* __restrict__ qb_uf, int* __restrict__ qb_flags) {
+             int* __restrict__ qb_leave, float* __restrict__ qb_uf, int* __restrict__ qb_flags, int part) {
+    extern __shared__ int um_keys[];  // [cap] the block's union, partitioned (dynamic; 0 = keep the order)
+    __shared__ int cls_tot[4], cls_run[4];
     const int b = blockIdx.y, qb = blockIdx.x;
     const int64_t bl = (int64_t)b * L;
     const int64_t row = (int64_t)b * nqb + qb;
@@ -728,19 +730,73 @@ k_union_meta(const int* __restrict__ leave1, const float* __restrict__ uf, const
     const int t_hi = min(qb * kQBlock + kQBlock - 1 - window, T - 1);
     const float tau_hi = t_hi >= 0 ? tauf[bl + t_hi] : -INFINITY;
     const int ntiles = (cnt + 127) / 128;
+    int* list = qb_list + row * cap;
+    // Class of an entry: bit 0 = it is valid for every push time of the
+    // block (no interval mask), bit 1 = its gate saturates for every query of
+    // the block (tau is nondecreasing, so u >= tau_hi + 1 suffices). Entries
+    // are stably partitioned by class (both, mask-free, gate-free, neither)
+    // so that as many 128-entry tiles as possible take the kernels' fast
+    // paths; attention is order-independent over the union.
+    auto cls_of = [&](int key) {
+        const int lv = leave1[bl + key];
+        const bool ok = key <= t_lo && lv > t_hi;
+        const bool sat = uf[bl + key] >= tau_hi + 1.f;
+        return ok && sat ? 0 : ok ? 1 : sat ? 2 : 3;
+    };
+    // part: launched with cap ints of dynamic shared memory
+    if (part && cnt > 0) {
+        if (threadIdx.x < 4) cls_tot[threadIdx.x] = 0, cls_run[threadIdx.x] = 0;
+        __syncthreads();
+        int mine[4] = {0, 0, 0, 0};
+        for (int idx = threadIdx.x; idx < cnt; idx += 128) ++mine[cls_of(list[idx])];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            int v = mine[c];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if ((threadIdx.x & 31) == 0 && v) atomicAdd(&cls_tot[c], v);
+        }
+        __syncthreads();
+        const int base[4] = {0, cls_tot[0], cls_tot[0] + cls_tot[1], cls_tot[0] + cls_tot[1] + cls_tot[2]};
+        __shared__ int wcnt[4][4];
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+        for (int i0 = 0; i0 < cnt; i0 += 128) {
+            const int idx = i0 + threadIdx.x;
+            const int key = idx < cnt ? list[idx] : -1;
+            const int c = key >= 0 ? cls_of(key) : -1;
+            unsigned bal[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                bal[q] = __ballot_sync(0xffffffffu, c == q);
+                if (lane == 0) wcnt[q][wid] = __popc(bal[q]);
+            }
+            __syncthreads();
+            if (c >= 0) {
+                int before = 0;
+                for (int w2 = 0; w2 < wid; ++w2) before += wcnt[c][w2];
+                um_keys[base[c] + cls_run[c] + before + __popc(bal[c] & ((1u << lane) - 1u))] = key;
+            }
+            __syncthreads();
+            if (threadIdx.x < 4) cls_run[threadIdx.x] += wcnt[threadIdx.x][0] + wcnt[threadIdx.x][1] +
+                                                         wcnt[threadIdx.x][2] + wcnt[threadIdx.x][3];
+            __syncthreads();
+        }
+        for (int idx = threadIdx.x; idx < cnt; idx += 128) list[idx] = um_keys[idx];
+        __syncthreads();
+    }
     for (int t = 0; t < ntiles; ++t) {
         const int idx = t * 128 + threadIdx.x;
         int key = -1, lv = 0;
         float u = 0.f;
         const bool real = idx < cnt;
         if (real) {
-            key = qb_list[row * cap + idx];
+            key = list[idx];
             lv = leave1[bl + key];
             u = uf[bl + key];
         } else {
             // padding re-reads the block's first key (a valid row, so the
             // gathers need no bounds check); ext = 0 masks it everywhere
-            qb_list[row * cap + idx] = qb_list[row * cap];
+            list[idx] = list[0];
         }
         // the interval mask in one unsigned compare:
         // valid(t) <=> (unsigned)(t - key) < (unsigned)(leave - key); padding: 0
@@ -1061,11 +1117,17 @@ void run_select(const skb_attn_desc& d, const double* u, void* ws, cudaStream_t 
             k_ever_list<<<gc, 1024, 0, st>>>(leave1, L, T, ccnt, ever_count, ever_list);
         }
         SKB_CHECK_LAUNCH();
-        k_union_meta<<<g, 128, 0, st>>>(leave1, reinterpret_cast<const float*>(base + lay.uf),
+        // partitioned by class when the union fits in shared memory, in key order otherwise
+        const size_t um_smem = (size_t)lay.qb_cap * sizeof(int);
+        const bool um_part = um_smem <= 160 * 1024;
+        static uint64_t um_attr = 0;
+        if (um_part && first_on_device(&um_attr))
+            SKB_CHECK_CUDA(cudaFuncSetAttribute(k_union_meta, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+        k_union_meta<<<g, 128, um_part ? um_smem : 0, st>>>(leave1, reinterpret_cast<const float*>(base + lay.uf),
                                         reinterpret_cast<const float*>(base + lay.tauf), L, T, w, nqb,
                                         (int)lay.qb_cap, qb_count, qb_list, reinterpret_cast<int*>(base + lay.qb_leave),
                                         reinterpret_cast<float*>(base + lay.qb_uf),
-                                        reinterpret_cast<int*>(base + lay.qb_flags));
+                                        reinterpret_cast<int*>(base + lay.qb_flags), um_part ? 1 : 0);
         SKB_CHECK_LAUNCH();
     } else {
         const int64_t n = (int64_t)B * nqb;

@@ -51,6 +51,43 @@ cublasHandle_t handle_for(cudaStream_t st) {
     return h[dev];
 }
 
+// A per-(thread, device) side stream forked from `st` (it sees everything
+// enqueued on st so far) and joined back with an event.
+class SideStream {
+  public:
+    SideStream(cudaStream_t st, bool on) : st_(st), on_(on) {
+        if (!on_) return;
+        struct Slot {
+            cudaStream_t s = nullptr;
+            cudaEvent_t fork = nullptr, join = nullptr;
+        };
+        thread_local Slot slots[64];
+        int dev = 0;
+        cudaGetDevice(&dev);
+        Slot& sl = slots[dev & 63];
+        if (!sl.s) {
+            SKB_CHECK_CUDA(cudaStreamCreateWithFlags(&sl.s, cudaStreamNonBlocking));
+            SKB_CHECK_CUDA(cudaEventCreateWithFlags(&sl.fork, cudaEventDisableTiming));
+            SKB_CHECK_CUDA(cudaEventCreateWithFlags(&sl.join, cudaEventDisableTiming));
+        }
+        side_ = sl.s;
+        join_ = sl.join;
+        SKB_CHECK_CUDA(cudaEventRecord(sl.fork, st_));
+        SKB_CHECK_CUDA(cudaStreamWaitEvent(side_, sl.fork, 0));
+    }
+    void* get() const { return on_ ? static_cast<void*>(side_) : static_cast<void*>(st_); }
+    void join() {
+        if (!on_) return;
+        SKB_CHECK_CUDA(cudaEventRecord(join_, side_));
+        SKB_CHECK_CUDA(cudaStreamWaitEvent(st_, join_, 0));
+    }
+
+  private:
+    cudaStream_t st_, side_ = nullptr;
+    cudaEvent_t join_ = nullptr;
+    bool on_;
+};
+
 // Row-major C[M, N] (+)= op(A) op(B) with op(A) [M, K], op(B) [K, N]; ta/tb
 // say whether the stored row-major matrix is transposed. Expressed as the
 // column-major product C^T = op(B)^T op(A)^T.
@@ -191,11 +228,15 @@ int skb_xattn_forward(const skb_x_desc* d, const void* x, const void* wq, const 
         t->sdev = static_cast<double*>(t->mem.get(M * 8));
         t->lse = static_cast<double*>(t->mem.get(M * d->heads * 8));
         SKB_CHECK_CUDA(cudaMemcpyAsync(t->x, x, M * D * es, cudaMemcpyDefault, st));
+        // K1 (a serial float64 Welford chain per sequence) runs on a side
+        // stream under the three projection GEMMs: both only read x.
+        SideStream side(st, d->k > 0.0);
         gemm(st, dt, false, false, M, D, D, x, D, wq, D, t->q, D, false);  // cache.cpp:204-206
         gemm(st, dt, false, false, M, D, D, x, D, wk, D, t->k, D, false);
         gemm(st, dt, false, false, M, D, D, x, D, wv, D, t->v, D, false);
         if (d->k > 0.0) {
-            check_rc(skb_score_fwd(B, L, D, dt, x, w_score, &d->scoring, t->raw, t->u, t->mean, t->sdev, stream));
+            check_rc(skb_score_fwd(B, L, D, dt, x, w_score, &d->scoring, t->raw, t->u, t->mean, t->sdev, side.get()));
+            side.join();
         } else {  // scores idle (cache.cpp:219-227)
             SKB_CHECK_CUDA(cudaMemsetAsync(t->raw, 0, M * 8, st));
             SKB_CHECK_CUDA(cudaMemsetAsync(t->u, 0, M * 8, st));

@@ -103,5 +103,30 @@ def test_session_batch_of_sequences(cuda, reference):
     for b in range(B):
         y_ref, _ = reference.decode(x[b], *ws, wsc, ref_cfg(k, w, heads=H), prompt)
         assert rel_err(y[b], y_ref) < 1e-9, (b, rel_err(y[b], y_ref))
-    with pytest.raises(Exception):
-        s.prefill(xt[:, :4])  # prefill only before generation
+
+
+def test_session_forward_chunk_continues_state(cuda, reference):
+    """forward_chunk onto a non-empty cache (Algorithm 3's recurrence): prompt,
+    then a multi-row chunk, then single steps = the reference's forward_chunk
+    followed by generate_step (the group size is invisible in the output,
+    proj/src/cache.cpp:315-317)."""
+    import torch
+
+    from oracle.oracle import ref_cfg
+    from paper_2406_16747_b200 import DecodeSession, ops
+
+    B, L, D, H, k, w, prompt, mid = 2, 80, 32, 2, 8.5, 6, 17, 40
+    rng = np.random.default_rng(78)
+    x = rng.normal(size=(B, L, D))
+    ws = [rng.normal(size=(D, D)) / np.sqrt(D) for _ in range(4)]
+    wsc = rng.normal(size=D)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(cuda)
+    s = DecodeSession(*(t(a) for a in ws), t(wsc), ops.AttnConfig(k=k, window=w), H, batch=B,
+                      max_len=L)
+    xt = t(x)
+    ys = [s.forward_chunk(xt[:, :prompt]), s.forward_chunk(xt[:, prompt:mid])]
+    ys += [s.step(xt[:, i])[:, None] for i in range(mid, L)]
+    y = torch.cat(ys, 1).cpu().numpy()
+    for b in range(B):
+        y_ref, _ = reference.decode(x[b], *ws, wsc, ref_cfg(k, w, heads=H), prompt)
+        assert rel_err(y[b], y_ref) < 1e-9, (b, rel_err(y[b], y_ref))
