@@ -207,22 +207,46 @@ void fill_tape(AttnTape<T>& tape, std::shared_ptr<skb_xattn> dev, std::size_t L,
     for (std::size_t s = 0; s < L; s += cl) tape.chunk_starts.push_back(s);
 }
 
+// LinearMixParams as one float64 [H, p, p] device block (the C ABI's feat).
+template <class T>
+std::vector<double> pack_feat(const LinearMixParams<T>& lin, std::size_t heads, std::size_t p) {
+    if (lin.feat.size() != heads) throw ShapeError("forward_chunk: one feature map per head");
+    std::vector<double> out;
+    out.reserve(heads * p * p);
+    for (const auto& f : lin.feat) {
+        if (f.rows != p || f.cols != p) throw ShapeError("forward_chunk: feature maps are head_dim x head_dim");
+        for (T v : f.data) out.push_back(static_cast<double>(v));
+    }
+    return out;
+}
+
 template <class T>
 MatT<T> run_forward(const MatT<T>& x, const AttnParams<T>& params, const ScoringParams& scoring,
-                    const AttnConfig& cfg, AttnTape<T>* tape, std::size_t chunk_len) {
+                    const AttnConfig& cfg, AttnTape<T>* tape, std::size_t chunk_len,
+                    const LinearMixParams<T>* lin = nullptr) {
     cfg.validate(x.cols, scoring);
-    if (cfg.linear_mix) throw ConfigError("linear mix: use linear_mix_attention");
+    if (cfg.linear_mix && !lin) throw ConfigError("forward_chunk: linear mix needs feature parameters");
     check_params(params, x.cols);
     const std::size_t L = x.rows, D = x.cols;
+    std::vector<double> feat;
+    if (cfg.linear_mix) feat = pack_feat(*lin, cfg.heads, D / cfg.heads);
     MatT<T> y(L, D);
     if (L == 0) return y;
-    const skb_x_desc d = x_desc<T>(L, D, cfg, scoring, chunk_len);
+    skb_x_desc d = x_desc<T>(L, D, cfg, scoring, chunk_len);
     DeviceParams<T> dp(params, scoring);
     Buf dx(x.data), dy(y.data.size() * sizeof(T));
     skb_xattn* t = nullptr;
-    check(skb_xattn_forward(&d, dx.get(), dp.wq.get(), dp.wk.get(), dp.wv.get(), dp.wo.get(),
-                            cfg.k > 0.0 ? dp.ws.template as<double>() : nullptr, dy.get(), tape ? &t : nullptr,
-                            nullptr));
+    if (cfg.linear_mix) {  // Appendix B.1 (proj/src/cache.cpp:322-356)
+        d.flags |= SKB_FLAG_LINEAR_MIX;
+        Buf df(feat);
+        check(skb_xattn_forward_lin(&d, dx.get(), dp.wq.get(), dp.wk.get(), dp.wv.get(), dp.wo.get(),
+                                    cfg.k > 0.0 ? dp.ws.template as<double>() : nullptr, df.template as<double>(),
+                                    dy.get(), tape ? &t : nullptr, nullptr));
+    } else {
+        check(skb_xattn_forward(&d, dx.get(), dp.wq.get(), dp.wk.get(), dp.wv.get(), dp.wo.get(),
+                                cfg.k > 0.0 ? dp.ws.template as<double>() : nullptr, dy.get(), tape ? &t : nullptr,
+                                nullptr));
+    }
     y.data = dy.to_host<T>(y.data.size());
     if (tape) fill_tape(*tape, std::shared_ptr<skb_xattn>(t, skb_xattn_destroy), L, D, cfg, chunk_len);
     return y;
@@ -233,17 +257,13 @@ MatT<T> run_forward(const MatT<T>& x, const AttnParams<T>& params, const Scoring
 template <class T>
 MatT<T> sparsek_attention(const MatT<T>& x, const AttnParams<T>& params, const ScoringParams& scoring,
                           const AttnConfig& cfg, AttnTape<T>* tape = nullptr, const LinearMixParams<T>* lin = nullptr) {
-    if (lin || cfg.linear_mix) {
-        if (!lin) throw ArgumentError("linear mix: missing feature maps");
-        throw ConfigError("linear mix (Appendix B.1) is not part of the B200 SparseK path");
-    }
-    return detail::run_forward(x, params, scoring, cfg, tape, 0);
+    return detail::run_forward(x, params, scoring, cfg, tape, 0, lin);
 }
 
 template <class T>
 AttnGrads<T> sparsek_attention_backward(const AttnTape<T>& tape, const MatT<T>& grad_out, const AttnParams<T>& params,
                                         const ScoringParams& scoring, const LinearMixParams<T>* lin = nullptr) {
-    if (lin) throw ConfigError("linear mix (Appendix B.1) is not part of the B200 SparseK path");
+    if (tape.cfg.linear_mix && !lin) throw ConfigError("backward: linear mix needs feature parameters");
     const std::size_t L = tape.x.rows, D = tape.d_model ? tape.d_model : tape.x.cols;
     if (grad_out.rows != L || grad_out.cols != D) throw ShapeError("sparsek_attention_backward: grad_out shape");
     detail::check_params(params, D);
@@ -251,7 +271,7 @@ AttnGrads<T> sparsek_attention_backward(const AttnTape<T>& tape, const MatT<T>& 
     const std::size_t chunk_len = tape.chunk_starts.size() > 1 ? tape.chunk_starts[1] - tape.chunk_starts[0] : 0;
     if (!dev) {  // a tape assembled on the host: re-run the forward from its inputs
         AttnTape<T> t2;
-        detail::run_forward(tape.x, params, scoring, tape.cfg, &t2, chunk_len);
+        detail::run_forward(tape.x, params, scoring, tape.cfg, &t2, chunk_len, tape.cfg.linear_mix ? lin : nullptr);
         dev = t2.device;
     }
     AttnGrads<T> g;
@@ -265,9 +285,22 @@ AttnGrads<T> sparsek_attention_backward(const AttnTape<T>& tape, const MatT<T>& 
     detail::DeviceParams<T> dp(params, scoring);
     detail::Buf dgo(grad_out.data), ddx(L * D * sizeof(T)), dq(D * D * sizeof(T)), dk(D * D * sizeof(T)),
         dv(D * D * sizeof(T)), dwo(D * D * sizeof(T)), dws(D * 8);
-    detail::check(skb_xattn_backward(dev.get(), dgo.get(), dp.wq.get(), dp.wk.get(), dp.wv.get(), dp.wo.get(),
-                                     tape.cfg.k > 0.0 ? dp.ws.template as<double>() : nullptr, ddx.get(), dq.get(),
-                                     dk.get(), dv.get(), dwo.get(), dws.as<double>(), nullptr));
+    const std::size_t H = tape.cfg.heads, p = D / H;
+    if (tape.cfg.linear_mix) {  // attention.cpp:317-445, 519-549 (+ dfeat)
+        detail::Buf df(detail::pack_feat(*lin, H, p)), ddf(H * p * p * 8);
+        detail::check(skb_xattn_backward_lin(dev.get(), dgo.get(), dp.wq.get(), dp.wk.get(), dp.wv.get(),
+                                             dp.wo.get(), tape.cfg.k > 0.0 ? dp.ws.template as<double>() : nullptr,
+                                             df.template as<double>(), ddx.get(), dq.get(), dk.get(), dv.get(),
+                                             dwo.get(), dws.as<double>(), ddf.as<double>(), nullptr));
+        const std::vector<double> hf = ddf.to_host<double>(H * p * p);
+        g.dfeat.assign(H, MatT<T>(p, p));
+        for (std::size_t h = 0; h < H; ++h)
+            for (std::size_t e = 0; e < p * p; ++e) g.dfeat[h].data[e] = static_cast<T>(hf[h * p * p + e]);
+    } else {
+        detail::check(skb_xattn_backward(dev.get(), dgo.get(), dp.wq.get(), dp.wk.get(), dp.wv.get(), dp.wo.get(),
+                                         tape.cfg.k > 0.0 ? dp.ws.template as<double>() : nullptr, ddx.get(),
+                                         dq.get(), dk.get(), dv.get(), dwo.get(), dws.as<double>(), nullptr));
+    }
     g.dx.data = ddx.to_host<T>(L * D);
     g.dwq.data = dq.to_host<T>(D * D);
     g.dwk.data = dk.to_host<T>(D * D);

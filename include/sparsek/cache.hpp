@@ -32,7 +32,9 @@ class SparseKvCache {
                   std::size_t max_positions = std::size_t(1) << 20)
         : cfg_(cfg), d_model_(d_model), scoring_(scoring), max_pos_(max_positions) {
         cfg.validate(d_model, scoring);
-        if (cfg.linear_mix) throw ConfigError("linear mix (Appendix B.1) is not part of the B200 SparseK path");
+        // the linear mix's recurrent prefix state (lin_m_/lin_b_) has no decode
+        // kernel here: linear_mix_attention / chunked_forward run it batched
+        if (cfg.linear_mix) throw ConfigError("linear mix: incremental decoding is not supported on this backend");
         const skb_x_desc d = detail::x_desc<T>(max_positions, d_model, cfg, scoring);
         skb_xcache* c = nullptr;
         detail::check(skb_xcache_create(&d, &c));
@@ -47,7 +49,7 @@ class SparseKvCache {
 
     MatT<T> forward_chunk(const MatT<T>& x_chunk, const AttnParams<T>& params, AttnTape<T>* tape = nullptr,
                           const LinearMixParams<T>* lin = nullptr) {
-        if (lin) throw ConfigError("linear mix (Appendix B.1) is not part of the B200 SparseK path");
+        if (lin) throw ConfigError("linear mix: incremental decoding is not supported on this backend");
         if (x_chunk.cols != d_model_) throw ShapeError("forward_chunk: x.cols != d_model");
         detail::check_params(params, d_model_);
         const std::size_t n = x_chunk.rows;
@@ -186,7 +188,12 @@ MatT<T> chunked_forward(const MatT<T>& x, std::size_t chunk_len, const AttnParam
                         const ScoringParams& scoring, const AttnConfig& cfg, AttnTape<T>* tape = nullptr,
                         const LinearMixParams<T>* lin = nullptr) {
     if (chunk_len == 0) throw ArgumentError("chunked_forward: chunk_len must be positive");
-    if (lin) throw ConfigError("linear mix (Appendix B.1) is not part of the B200 SparseK path");
+    if (lin || cfg.linear_mix) {  // Appendix B.1: the batch kernels, stop-gradients at the chunk starts
+        if (!lin) throw ConfigError("forward_chunk: linear mix needs feature parameters");
+        AttnConfig c = cfg;
+        c.linear_mix = true;
+        return detail::run_forward(x, params, scoring, c, tape, chunk_len, lin);
+    }
     if (tape) return detail::run_forward(x, params, scoring, cfg, tape, chunk_len);
     SparseKvCache<T> cache(cfg, x.cols, scoring, std::max<std::size_t>(x.rows, 1));
     MatT<T> out(x.rows, x.cols);

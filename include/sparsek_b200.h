@@ -55,6 +55,8 @@ typedef enum { SKB_F32 = 0, SKB_BF16 = 1, SKB_F64 = 2 } skb_dtype;
 /* Execution-path flags. The tensor-core (tcgen05) path is used for BF16 by
  * default; F32/F64 always run the CUDA-core gather path. */
 #define SKB_FLAG_FORCE_GATHER 1u /* run BF16 on the CUDA-core gather kernels */
+#define SKB_FLAG_LINEAR_MIX 2u   /* AttnConfig::linear_mix: window = floor(k) = 0 is allowed
+                                    (the linear branch reaches every position) */
 
 /* AttnConfig (proj/include/sparsek/attention.hpp:18-32) at the Q/K/V/u level. */
 typedef struct skb_attn_desc {
@@ -160,6 +162,26 @@ int skb_attn_bwd(const skb_attn_desc* d, const void* q, const void* k, const voi
                  const void* o, const void* dout, const double* lse, const double* u,
                  const void* sel_ws, void* dq, void* dk, void* dv, double* du, void* ws,
                  void* stream);
+
+/* ---- Linear-attention mix (Appendix B.1) --------------------------------- */
+/* linear_mix_attention (proj/include/sparsek/attention.hpp:93-99): exact
+ * attention over the SparseK snapshot (selected keys with gate m = g, window
+ * m = 1) mixed with positive-feature linear attention over every causal
+ * position, phi(z) = elu(F_h z) + 1:
+ *   o_i = sum_{j<=i} w_ij v_j / sum_{j<=i} w_ij,
+ *   w_ij = (1 - m_ij) phi(q_i).phi(k_j) + m_ij exp(scale q_i.k_j)
+ * (forward proj/src/cache.cpp:262-278,322-356; backward
+ * proj/src/attention.cpp:317-445,519-549). dtype float32 or float64 (the
+ * reference's instantiations); feat / dfeat: float64 [H, p, p]; den: float64
+ * [B, H, L] (saved by the forward for the backward); ws: the workspace of
+ * skb_linmix_workspace_size (both calls). A nonpositive denominator is
+ * SKB_ENUMERIC, as the reference's NumericError. */
+int skb_linmix_workspace_size(const skb_attn_desc* d, size_t* bytes);
+int skb_linmix_fwd(const skb_attn_desc* d, const void* q, const void* k, const void* v, const double* u,
+                   const void* sel_ws, const double* feat, void* o, double* den, void* ws, void* stream);
+int skb_linmix_bwd(const skb_attn_desc* d, const void* q, const void* k, const void* v, const double* u,
+                   const void* sel_ws, const double* feat, const double* den, const void* dout, void* dq,
+                   void* dk, void* dv, double* du, double* dfeat, void* ws, void* stream);
 
 /* ---- SparseK operator (batched rows) ------------------------------------ */
 /* z: float64 [n, m]; p: [n, m]; tau: [n] (-inf when infeasible); counts [n];
@@ -308,6 +330,16 @@ int skb_xattn_forward(const skb_x_desc* d, const void* x, const void* wq, const 
 int skb_xattn_backward(skb_xattn* tape, const void* grad_out, const void* wq, const void* wk, const void* wv,
                        const void* wo, const double* w_score, void* dx, void* dwq, void* dwk, void* dwv,
                        void* dwo, double* dw_score, void* stream);
+/* linear_mix_attention (proj/include/sparsek/attention.hpp:93-99) and its
+ * backward with LinearMixParams: d->flags carries SKB_FLAG_LINEAR_MIX (the
+ * scoring must be timestep_norm), feat / dfeat float64 [H, p, p]. The tape's
+ * lse field then holds the mixture denominators. */
+int skb_xattn_forward_lin(const skb_x_desc* d, const void* x, const void* wq, const void* wk, const void* wv,
+                          const void* wo, const double* w_score, const double* feat, void* y, skb_xattn** tape,
+                          void* stream);
+int skb_xattn_backward_lin(skb_xattn* tape, const void* grad_out, const void* wq, const void* wk, const void* wv,
+                           const void* wo, const double* w_score, const double* feat, void* dx, void* dwq,
+                           void* dwk, void* dwv, void* dwo, double* dw_score, double* dfeat, void* stream);
 /* Copy one AttnTape field (host or device destination, `bytes` = its size):
  * x/q/k/v/head_concat [B, L, D] dtype; raw/u/norm_mean/norm_sdev float64 [B, L];
  * lse float64 [B, H, L] (= maxa + log denom); tau_push float64 [B, L] (push

@@ -473,6 +473,25 @@ class Reference:
         return secs.value
 
 
+    def linear_mix(self, x, wq, wk, wv, wo, w_score, feat, cfg, use_float=False, grad_out=None,
+                   chunk_len=0):
+        """linear_mix_attention (+ its backward when grad_out is given):
+        (y, {dx, dwq, dwk, dwv, dwo, dw_score, dfeat} or None)."""
+        x, wq, wk, wv, wo = (np.ascontiguousarray(a, np.float64) for a in (x, wq, wk, wv, wo))
+        L, D = x.shape
+        ws = np.ascontiguousarray(w_score if w_score is not None else np.zeros(D), np.float64)
+        f = np.ascontiguousarray(feat, np.float64)
+        y = np.zeros((L, D))
+        out = dict(dx=np.zeros((L, D)), dwq=np.zeros((D, D)), dwk=np.zeros((D, D)), dwv=np.zeros((D, D)),
+                   dwo=np.zeros((D, D)), dw_score=np.zeros(D), dfeat=np.zeros_like(f))
+        g = None if grad_out is None else np.ascontiguousarray(grad_out, np.float64)
+        self._rc(self.lib.ref_linmix(C.c_int32(int(use_float)), C.c_uint64(L), C.c_uint64(D), _d(x), _d(wq),
+                                     _d(wk), _d(wv), _d(wo), _d(ws), _d(f), C.byref(cfg),
+                                     C.c_uint64(int(chunk_len)), None if g is None else _d(g), _d(y),
+                                     *(_d(out[n]) for n in ("dx", "dwq", "dwk", "dwv", "dwo", "dw_score",
+                                                            "dfeat"))))
+        return y, (out if g is not None else None)
+
     def bench_decode(self, units, threads, prompt, steps, p, k, window, seed=1):
         """Seconds for `steps` generate_step calls on each of `units` single-head
         caches prefilled with `prompt` rows (ref_bench_decode)."""

@@ -525,6 +525,47 @@ int ref_cache_resume(int32_t use_float, const uint8_t* blob, uint64_t len, uint6
     REF_GUARD_END
 }
 
+// Linear-attention mix: linear_mix_attention (attention.hpp:93-99) with a tape,
+// then sparsek_attention_backward with the same LinearMixParams (grad_out may
+// be null: forward only). feat: heads x p x p row-major; dfeat likewise.
+// chunk_len > 0 feeds the rows through one cache chunk by chunk (chunked_forward).
+int ref_linmix(int32_t use_float, uint64_t L, uint64_t D, const double* x, const double* wq, const double* wk,
+               const double* wv, const double* wo, const double* w_score, const double* feat, const ref_cfg* c,
+               uint64_t chunk_len, const double* grad_out, double* y, double* dx, double* dwq, double* dwk,
+               double* dwv, double* dwo, double* dws, double* dfeat) {
+    REF_GUARD_BEGIN
+    auto run = [&](auto tag) {
+        using T = decltype(tag);
+        const uint64_t H = c->heads, p = D / H;
+        AttnParams<T> params{mat_in<T>(wq, D, D), mat_in<T>(wk, D, D), mat_in<T>(wv, D, D), mat_in<T>(wo, D, D)};
+        ScoringParams scoring = to_scoring(c, w_score, D);
+        LinearMixParams<T> lin;
+        for (uint64_t h = 0; h < H; ++h) lin.feat.push_back(mat_in<T>(feat + h * p * p, p, p));
+        AttnConfig cfg = to_cfg(c);
+        cfg.linear_mix = true;
+        AttnTape<T> tape;
+        MatT<T> out;
+        if (chunk_len == 0) {
+            out = linear_mix_attention(mat_in<T>(x, L, D), params, scoring, cfg, lin, &tape);
+        } else {
+            out = chunked_forward(mat_in<T>(x, L, D), chunk_len, params, scoring, cfg, &tape, &lin);
+        }
+        mat_out(out, y);
+        if (!grad_out) return;
+        AttnGrads<T> g = sparsek_attention_backward(tape, mat_in<T>(grad_out, L, D), params, scoring, &lin);
+        mat_out(g.dx, dx);
+        mat_out(g.dwq, dwq);
+        mat_out(g.dwk, dwk);
+        mat_out(g.dwv, dwv);
+        mat_out(g.dwo, dwo);
+        for (uint64_t i = 0; i < g.dw_score.size(); ++i) dws[i] = g.dw_score[i];
+        for (uint64_t h = 0; h < H; ++h) mat_out(g.dfeat[h], dfeat + h * p * p);
+    };
+    if (use_float) run(float{});
+    else run(double{});
+    REF_GUARD_END
+}
+
 // CPU baseline: `units` independent single-head sequences (heads=1, D=p) of
 // length L, fwd (with tape) + bwd in float, one std::thread per unit with at
 // most `threads` in flight, the way the reference trainer fans out batch

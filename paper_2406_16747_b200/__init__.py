@@ -20,6 +20,8 @@ from .api import (  # noqa: F401
     chunked_forward,
     dense_attention,
     dense_attention_grads,
+    linear_mix_attention,
+    linear_mix_attention_grads,
     sparsek,
     sparsek_jvp,
     sparsek_partial,
@@ -32,6 +34,7 @@ from . import ops  # noqa: F401
 __all__ = [
     "ArgumentError", "ConfigError", "DecodeSession", "NumericError", "ShapeError", "IoError", "Stream",
     "PartialSortStats", "SelectionMask", "__version__", "attention", "attention_backward", "attention_grads",
-    "attention_with_tape", "chunked_forward", "dense_attention", "dense_attention_grads", "sparsek",
+    "attention_with_tape", "chunked_forward", "dense_attention", "dense_attention_grads", "linear_mix_attention",
+    "linear_mix_attention_grads", "sparsek",
     "sparsek_jvp", "sparsek_partial", "sparsek_st", "stream_mask", "topk_hard", "ops",
 ]

@@ -44,6 +44,7 @@ _ERRS = {1: ShapeError, 2: ArgumentError, 3: NumericError, 4: ConfigError, 5: Io
 
 SKB_F32, SKB_BF16, SKB_F64 = 0, 1, 2
 SKB_FLAG_FORCE_GATHER = 1
+SKB_FLAG_LINEAR_MIX = 2
 
 
 class AttnDesc(C.Structure):
@@ -111,6 +112,9 @@ _SIGS = {
     "skb_attn_fwd": ([C.POINTER(AttnDesc), _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp], C.c_int),
     "skb_attn_bwd_workspace_size": ([C.POINTER(AttnDesc), C.POINTER(C.c_size_t)], C.c_int),
     "skb_attn_bwd": ([C.POINTER(AttnDesc)] + [_vp] * 14, C.c_int),
+    "skb_linmix_workspace_size": ([C.POINTER(AttnDesc), C.POINTER(C.c_size_t)], C.c_int),
+    "skb_linmix_fwd": ([C.POINTER(AttnDesc)] + [_vp] * 10, C.c_int),
+    "skb_linmix_bwd": ([C.POINTER(AttnDesc)] + [_vp] * 15, C.c_int),
     "skb_sparsek": ([C.c_int64, C.c_int64, _vp, C.c_double, _vp, _vp, _vp, _vp, _vp, _vp],
                     C.c_int),
     "skb_sparsek_jvp": ([C.c_int64, C.c_int64, _vp, C.c_double, _vp, _vp, _vp], C.c_int),
@@ -128,6 +132,8 @@ _SIGS = {
     "skb_matmul": ([C.c_int32, C.c_int64, C.c_int64, C.c_int64, _vp, _vp, _vp, _vp], C.c_int),
     "skb_xattn_forward": ([C.POINTER(XDesc)] + [_vp] * 7 + [C.POINTER(_vp), _vp], C.c_int),
     "skb_xattn_backward": ([_vp] * 14, C.c_int),
+    "skb_xattn_forward_lin": ([C.POINTER(XDesc)] + [_vp] * 8 + [C.POINTER(_vp), _vp], C.c_int),
+    "skb_xattn_backward_lin": ([_vp] * 16, C.c_int),
     "skb_xattn_tape_get": ([_vp, C.c_int32, _vp, C.c_size_t, _vp], C.c_int),
     "skb_xattn_destroy": ([_vp], C.c_int),
     "skb_xcache_create": ([C.POINTER(XDesc), C.POINTER(_vp)], C.c_int),

@@ -273,6 +273,91 @@ def attention_grads(x, wq, wk, wv, wo, w_score, k, window, grad_out, heads=1, ke
                                              dwo=g(wot), dw_score=g(wst))
 
 
+def _lm_inputs(x, wq, wk, wv, wo, w_score, feat, k, window, heads, slope_eps):
+    x, ws = _attention_inputs(x, wq, wk, wv, wo, heads)
+    if not math.isfinite(k) or k < 0.0:
+        raise ConfigError("attention: k must be finite and >= 0")
+    if window < 0:
+        raise ConfigError("attention: window must be >= 0")
+    L, D = x.shape
+    p = D // heads
+    wsc = _vec(w_score, "w_score") if w_score is not None else np.zeros(0)
+    if k > 0.0 and wsc.size != D:
+        raise ConfigError("attention: w_score length must equal d_model")
+    if not (slope_eps > 0.0):
+        raise ArgumentError("ScoringParams: slope_eps must be positive")
+    f = np.asarray(feat, dtype=np.float64)
+    if f.ndim != 3 or f.shape[0] != heads:
+        raise ShapeError("forward_chunk: one feature map per head")
+    if f.shape[1:] != (p, p):
+        raise ShapeError("forward_chunk: feature maps are head_dim x head_dim")
+    cfg = ops.AttnConfig(k=float(k), window=int(window), linear_mix=True)
+    return x, ws, wsc, f, cfg
+
+
+def linear_mix_torch(x, wq, wk, wv, wo, w_score, feat, cfg: ops.AttnConfig, heads: int,
+                     scoring: ops.ScoringConfig):
+    """Differentiable x-level linear_mix_attention (proj/include/sparsek/
+    attention.hpp:93-99) on device tensors: x [B, L, D], feat [H, p, p]."""
+    B, L, D = x.shape
+    p = D // heads
+    if scoring.norm_mode != "timestep_norm":
+        raise ConfigError("linear mix requires timestep normalization; raw scores make the linear "
+                          "branch blow up")
+    q = (x @ wq).view(B, L, heads, p)
+    k = (x @ wk).view(B, L, heads, p)
+    v = (x @ wv).view(B, L, heads, p)
+    if cfg.k > 0.0:
+        u = ops.score_tokens(x, w_score, scoring)
+    else:
+        u = torch.zeros((B, L), dtype=torch.float64, device=x.device)
+    hc = ops.linear_mix_core(q, k, v, u, feat, cfg)
+    return hc.reshape(B, L, D) @ wo, hc
+
+
+def linear_mix_attention(x, wq, wk, wv, wo, w_score, feat, k, window, heads=1, slope_eps=0.01,
+                         slope_enabled=True):
+    """linear_mix_attention (proj/include/sparsek/attention.hpp:93-99; Appendix
+    B.1): the SparseK snapshot's exact attention mixed with positive-feature
+    linear attention over every causal position; feat: [H, p, p] (one feature
+    map per head). float64 in and out, like the reference's double path."""
+    x, (wq, wk, wv, wo), wsc, f, cfg = _lm_inputs(x, wq, wk, wv, wo, w_score, feat, k, window, heads,
+                                                   slope_eps)
+    L, D = x.shape
+    d = _dev()
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(d)
+    sc = ops.ScoringConfig(slope_eps=float(slope_eps), slope_enabled=bool(slope_enabled))
+    with torch.no_grad():
+        y, _ = linear_mix_torch(t(x).view(1, L, D), t(wq), t(wk), t(wv), t(wo),
+                                t(wsc) if cfg.k > 0.0 else None, t(f), cfg, heads, sc)
+    return y[0].cpu().numpy()
+
+
+def linear_mix_attention_grads(x, wq, wk, wv, wo, w_score, feat, k, window, grad_out, heads=1,
+                               slope_eps=0.01, slope_enabled=True, chunk_len=0):
+    """linear_mix_attention + sparsek_attention_backward with LinearMixParams
+    (proj/src/attention.cpp:317-445, 519-549): (y, {dx, dwq, dwk, dwv, dwo,
+    dw_score, dfeat}) as float64 numpy arrays."""
+    x, (wq, wk, wv, wo), wsc, f, cfg = _lm_inputs(x, wq, wk, wv, wo, w_score, feat, k, window, heads,
+                                                   slope_eps)
+    if chunk_len:
+        cfg = ops.AttnConfig(k=cfg.k, window=cfg.window, linear_mix=True, chunk_len=int(chunk_len))
+    L, D = x.shape
+    d = _dev()
+    leaf = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(d).requires_grad_(True)
+    xt, wqt, wkt, wvt, wot, ft = (leaf(a) for a in (x, wq, wk, wv, wo, f))
+    wst = leaf(wsc) if cfg.k > 0.0 else None
+    sc = ops.ScoringConfig(slope_eps=float(slope_eps), slope_enabled=bool(slope_enabled),
+                           chunk_len=int(chunk_len))
+    y, _ = linear_mix_torch(xt.view(1, L, D), wqt, wkt, wvt, wot, wst, ft, cfg, heads, sc)
+    y.backward(torch.from_numpy(np.ascontiguousarray(grad_out, np.float64)).to(d).view(1, L, D))
+    g = lambda t: (t.grad.cpu().numpy() if t is not None and t.grad is not None
+                   else np.zeros(tuple(t.shape) if t is not None else (D,)))
+    return y[0].detach().cpu().numpy(), dict(dx=g(xt), dwq=g(wqt), dwk=g(wkt), dwv=g(wvt), dwo=g(wot),
+                                             dw_score=g(wst) if wst is not None else np.zeros(D),
+                                             dfeat=g(ft))
+
+
 def chunked_forward(x, chunk_len, wq, wk, wv, wo, w_score, k, window, heads=1, key_mode="hard",
                     mask_mode="soft", slope_eps=0.01, slope_enabled=True):
     """chunked_forward (proj/src/cache.cpp:548-563, Algorithm 3): the sequence is

@@ -979,7 +979,7 @@ void validate_desc(const skb_attn_desc& d) {
     SKB_REQUIRE(std::isfinite(d.k) && d.k >= 0.0, SKB_ECONFIG, "attention: k must be finite and >= 0");
     SKB_REQUIRE(std::isfinite(d.scale) && d.scale >= 0.0, SKB_ECONFIG, "attention: bad scale");
     SKB_REQUIRE(d.window >= 0, SKB_ECONFIG, "attention: window must be >= 0");
-    SKB_REQUIRE(!(d.window == 0 && std::floor(d.k) < 1.0), SKB_ECONFIG,
+    SKB_REQUIRE(!(d.window == 0 && std::floor(d.k) < 1.0) || (d.flags & SKB_FLAG_LINEAR_MIX), SKB_ECONFIG,
                 "attention: window + floor(k) must be >= 1 (only the linear mix can run with neither)");
     SKB_REQUIRE(d.key_mode == 0 || d.key_mode == 1, SKB_EARG, "key_mode must be 'soft' or 'hard'");
     SKB_REQUIRE(d.mask_mode == 0 || d.mask_mode == 1, SKB_EARG,

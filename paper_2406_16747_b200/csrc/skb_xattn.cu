@@ -143,8 +143,10 @@ void validate_x(const skb_x_desc& d) {
     SKB_REQUIRE(d.heads >= 1, SKB_ECONFIG, "attention: heads must be positive");
     SKB_REQUIRE(d.d_model % d.heads == 0, SKB_ECONFIG, "attention: d_model must be a positive multiple of heads");
     SKB_REQUIRE(d.dtype == SKB_F32 || d.dtype == SKB_F64 || d.dtype == SKB_BF16, SKB_EARG, "attention: bad dtype");
-    SKB_REQUIRE(d.window > 0 || std::floor(d.k) >= 1.0, SKB_ECONFIG,
+    SKB_REQUIRE(d.window > 0 || std::floor(d.k) >= 1.0 || (d.flags & SKB_FLAG_LINEAR_MIX), SKB_ECONFIG,
                 "attention: window + floor(k) must be >= 1 (only the linear mix can run with neither)");
+    SKB_REQUIRE(!(d.flags & SKB_FLAG_LINEAR_MIX) || d.scoring.norm_mode == 1, SKB_ECONFIG,
+                "linear mix requires timestep normalization; raw scores make the linear branch blow up");
     SKB_REQUIRE(!(d.k > 0.0) || d.scoring.slope_eps > 0.0, SKB_EARG, "ScoringParams: slope_eps must be positive");
 }
 
@@ -161,6 +163,8 @@ struct skb_xattn {
     double *raw = nullptr, *u = nullptr, *mean = nullptr, *sdev = nullptr, *lse = nullptr;
     void* sel = nullptr;
     skb_select_layout lay{};
+    void* lmws = nullptr;  // linear mix: the skb_linmix workspace (lse holds the mixture denominators)
+    bool linear = false;
 };
 
 struct skb_xcache {
@@ -204,10 +208,13 @@ int skb_matmul(int32_t dtype, int64_t M, int64_t N, int64_t K, const void* a, co
     XA_END
 }
 
-int skb_xattn_forward(const skb_x_desc* d, const void* x, const void* wq, const void* wk, const void* wv,
-                      const void* wo, const double* w_score, void* y, skb_xattn** tape, void* stream) {
+static int xattn_forward(const skb_x_desc* d, const void* x, const void* wq, const void* wk, const void* wv,
+                         const void* wo, const double* w_score, const double* feat, void* y, skb_xattn** tape,
+                         void* stream) {
     XA_BEGIN
     SKB_REQUIRE(d && x && wq && wk && wv && wo && y, SKB_EARG, "sparsek_attention: null argument");
+    SKB_REQUIRE(!feat == !(d->flags & SKB_FLAG_LINEAR_MIX), SKB_EARG,
+                "linear mix: feature maps go with SKB_FLAG_LINEAR_MIX (and only with it)");
     validate_x(*d);
     SKB_REQUIRE(!(d->k > 0.0) || w_score != nullptr, SKB_ECONFIG, "attention: w_score length must equal d_model");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -247,7 +254,15 @@ int skb_xattn_forward(const skb_x_desc* d, const void* x, const void* wq, const 
         check_rc(skb_select_layout_of(&a, &t->lay));
         t->sel = t->mem.get(t->lay.total_bytes);
         check_rc(skb_select(&a, t->u, t->sel, stream));
-        check_rc(skb_attn_fwd(&a, t->q, t->k, t->v, t->u, t->sel, t->o, t->lse, stream));
+        if (feat) {  // Appendix B.1: the mixture readout (cache.cpp:322-356); lse holds its denominators
+            size_t lb = 0;
+            check_rc(skb_linmix_workspace_size(&a, &lb));
+            t->lmws = t->mem.get(lb);
+            t->linear = true;
+            check_rc(skb_linmix_fwd(&a, t->q, t->k, t->v, t->u, t->sel, feat, t->o, t->lse, t->lmws, stream));
+        } else {
+            check_rc(skb_attn_fwd(&a, t->q, t->k, t->v, t->u, t->sel, t->o, t->lse, stream));
+        }
         gemm(st, dt, false, false, M, D, D, t->o, D, wo, D, y, D, false);  // cache.cpp:398-399
     } catch (...) {
         delete t;
@@ -261,12 +276,14 @@ int skb_xattn_forward(const skb_x_desc* d, const void* x, const void* wq, const 
     XA_END
 }
 
-int skb_xattn_backward(skb_xattn* t, const void* grad_out, const void* wq, const void* wk, const void* wv,
-                       const void* wo, const double* w_score, void* dx, void* dwq, void* dwk, void* dwv, void* dwo,
-                       double* dw_score, void* stream) {
+static int xattn_backward(skb_xattn* t, const void* grad_out, const void* wq, const void* wk, const void* wv,
+                          const void* wo, const double* w_score, const double* feat, void* dx, void* dwq, void* dwk,
+                          void* dwv, void* dwo, double* dw_score, double* dfeat, void* stream) {
     XA_BEGIN
     SKB_REQUIRE(t && grad_out && wq && wk && wv && wo && dx && dwq && dwk && dwv && dwo && dw_score, SKB_EARG,
                 "sparsek_attention_backward: null argument");
+    SKB_REQUIRE(t->linear == (feat != nullptr), SKB_ECONFIG, "backward: linear mix needs feature parameters");
+    SKB_REQUIRE(!feat || dfeat, SKB_EARG, "sparsek_attention_backward: null dfeat");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const skb_x_desc& d = t->d;
     const int64_t B = d.batch, L = d.seq_len, D = d.d_model, M = B * L;
@@ -284,7 +301,11 @@ int skb_xattn_backward(skb_xattn* t, const void* grad_out, const void* wq, const
     void* ws = tmp.get(wsb);
     gemm(st, dt, true, false, D, D, M, t->o, D, grad_out, D, dwo, D, false);  // dWo = hc^T g (attention.cpp:236-247)
     gemm(st, dt, false, true, M, D, D, grad_out, D, wo, D, dhc, D, false);    // dhc = g Wo^T
-    check_rc(skb_attn_bwd(&a, t->q, t->k, t->v, t->o, dhc, t->lse, t->u, t->sel, dq, dk, dv, du, ws, stream));
+    if (feat)  // attention.cpp:317-445, 519-549
+        check_rc(skb_linmix_bwd(&a, t->q, t->k, t->v, t->u, t->sel, feat, t->lse, dhc, dq, dk, dv, du, dfeat,
+                                t->lmws, stream));
+    else
+        check_rc(skb_attn_bwd(&a, t->q, t->k, t->v, t->o, dhc, t->lse, t->u, t->sel, dq, dk, dv, du, ws, stream));
     gemm(st, dt, true, false, D, D, M, t->x, D, dq, D, dwq, D, false);  // dW = x^T d (attention.cpp:551-573)
     gemm(st, dt, true, false, D, D, M, t->x, D, dk, D, dwk, D, false);
     gemm(st, dt, true, false, D, D, M, t->x, D, dv, D, dwv, D, false);
@@ -304,6 +325,39 @@ int skb_xattn_backward(skb_xattn* t, const void* grad_out, const void* wq, const
     }
     SKB_CHECK_CUDA(cudaStreamSynchronize(st));  // the temporaries are freed on return
     XA_END
+}
+
+int skb_xattn_forward(const skb_x_desc* d, const void* x, const void* wq, const void* wk, const void* wv,
+                      const void* wo, const double* w_score, void* y, skb_xattn** tape, void* stream) {
+    return xattn_forward(d, x, wq, wk, wv, wo, w_score, nullptr, y, tape, stream);
+}
+
+int skb_xattn_forward_lin(const skb_x_desc* d, const void* x, const void* wq, const void* wk, const void* wv,
+                          const void* wo, const double* w_score, const double* feat, void* y, skb_xattn** tape,
+                          void* stream) {
+    if (!feat) {
+        skb::set_last_error("linear mix: missing feature maps");
+        return SKB_EARG;
+    }
+    return xattn_forward(d, x, wq, wk, wv, wo, w_score, feat, y, tape, stream);
+}
+
+int skb_xattn_backward(skb_xattn* t, const void* grad_out, const void* wq, const void* wk, const void* wv,
+                       const void* wo, const double* w_score, void* dx, void* dwq, void* dwk, void* dwv, void* dwo,
+                       double* dw_score, void* stream) {
+    return xattn_backward(t, grad_out, wq, wk, wv, wo, w_score, nullptr, dx, dwq, dwk, dwv, dwo, dw_score, nullptr,
+                          stream);
+}
+
+int skb_xattn_backward_lin(skb_xattn* t, const void* grad_out, const void* wq, const void* wk, const void* wv,
+                           const void* wo, const double* w_score, const double* feat, void* dx, void* dwq, void* dwk,
+                           void* dwv, void* dwo, double* dw_score, double* dfeat, void* stream) {
+    if (!feat) {
+        skb::set_last_error("backward: linear mix needs feature parameters");
+        return SKB_ECONFIG;
+    }
+    return xattn_backward(t, grad_out, wq, wk, wv, wo, w_score, feat, dx, dwq, dwk, dwv, dwo, dw_score, dfeat,
+                          stream);
 }
 
 int skb_xattn_tape_get(skb_xattn* t, int32_t field, void* dst, size_t bytes, void* stream) {

@@ -52,6 +52,7 @@ class AttnConfig:
     mask_mode: str = "soft"      # "soft" | "straight_through"
     force_gather: bool = False   # BF16 on the CUDA-core gather kernels
     chunk_len: int = 0           # chunked_forward (Algorithm 3): backward stop-grad at chunk starts
+    linear_mix: bool = False     # Appendix B.1 (linear_mix_attention): window = floor(k) = 0 allowed
 
     def key_code(self):
         if self.key_mode not in ("hard", "soft"):
@@ -67,7 +68,8 @@ class AttnConfig:
 def make_desc(B, L, H, p, cfg: AttnConfig, dtype: torch.dtype) -> AttnDesc:
     if dtype not in _DT:
         raise _lib.ArgumentError(f"unsupported dtype {dtype}")
-    flags = _lib.SKB_FLAG_FORCE_GATHER if cfg.force_gather else 0
+    flags = (_lib.SKB_FLAG_FORCE_GATHER if cfg.force_gather else 0) | \
+        (_lib.SKB_FLAG_LINEAR_MIX if cfg.linear_mix else 0)
     if cfg.chunk_len < 0:
         raise _lib.ArgumentError("chunked_forward: chunk_len must be positive")
     return AttnDesc(int(B), int(L), int(H), int(p), float(cfg.k), int(cfg.window),
@@ -237,6 +239,93 @@ class SparseKAttentionFn(torch.autograd.Function):
 
 def sparsek_attention_core(q, k, v, u, cfg: AttnConfig):
     return SparseKAttentionFn.apply(q, k, v, u, cfg)
+
+
+# ---------------------------------------------------------------- linear-attention mix
+
+def _linmix_ws(desc, device):
+    n = C_size()
+    check(_lib.load().skb_linmix_workspace_size(desc, n))
+    return torch.empty(n.value, dtype=torch.uint8, device=device)
+
+
+def _feat(feat, H, p, device):
+    if feat.shape != (H, p, p):
+        raise _lib.ShapeError("forward_chunk: feature maps are head_dim x head_dim (one per head)")
+    return feat.to(device=device, dtype=torch.float64).contiguous()
+
+
+def _lm_cfg(cfg: AttnConfig) -> AttnConfig:
+    import dataclasses
+
+    return cfg if cfg.linear_mix else dataclasses.replace(cfg, linear_mix=True)
+
+
+def linmix_fwd(q, k, v, u, feat, cfg: AttnConfig, sel: Selection | None = None):
+    """Linear-attention mix forward (skb_linmix_fwd): q/k/v [B, L, H, p] float32
+    or float64, u [B, L] float64, feat [H, p, p]. Returns (o, den [B, H, L],
+    selection)."""
+    _check_qkv(q, k, v)
+    cfg = _lm_cfg(cfg)
+    B, L, H, p = q.shape
+    u = _scores(u, B, L, q.device)
+    desc = make_desc(B, L, H, p, cfg, q.dtype)
+    f = _feat(feat, H, p, q.device)
+    with torch.cuda.device(q.device):
+        if sel is None:
+            sel = select(u, cfg, desc=desc)
+        o = torch.empty_like(q)
+        den = torch.empty((B, H, L), dtype=torch.float64, device=q.device)
+        ws = _linmix_ws(desc, q.device)
+        check(_lib.load().skb_linmix_fwd(desc, q.data_ptr(), k.data_ptr(), v.data_ptr(), u.data_ptr(),
+                                         sel.ws.data_ptr(), f.data_ptr(), o.data_ptr(), den.data_ptr(),
+                                         ws.data_ptr(), _stream()))
+    return o, den, sel
+
+
+def linmix_bwd(q, k, v, u, feat, den, do, sel: Selection, cfg: AttnConfig):
+    """Returns (dq, dk, dv, du [B, L] float64, dfeat [H, p, p] float64)."""
+    _check_qkv(q, k, v)
+    cfg = _lm_cfg(cfg)
+    B, L, H, p = q.shape
+    u = _scores(u, B, L, q.device)
+    desc = make_desc(B, L, H, p, cfg, q.dtype)
+    f = _feat(feat, H, p, q.device)
+    if den.shape != (B, H, L) or den.dtype != torch.float64 or not den.is_contiguous():
+        raise _lib.ArgumentError("linear mix backward: den must be a contiguous float64 [B, H, L] tensor")
+    do = do.contiguous().to(q.dtype)
+    with torch.cuda.device(q.device):
+        dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+        du = torch.empty((B, L), dtype=torch.float64, device=q.device)
+        dfeat = torch.empty((H, p, p), dtype=torch.float64, device=q.device)
+        ws = _linmix_ws(desc, q.device)
+        check(_lib.load().skb_linmix_bwd(desc, q.data_ptr(), k.data_ptr(), v.data_ptr(), u.data_ptr(),
+                                         sel.ws.data_ptr(), f.data_ptr(), den.data_ptr(), do.data_ptr(),
+                                         dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), du.data_ptr(),
+                                         dfeat.data_ptr(), ws.data_ptr(), _stream()))
+    return dq, dk, dv, du, dfeat
+
+
+class LinearMixFn(torch.autograd.Function):
+    """(q, k, v, u, feat) -> o for the linear-attention mix, with its backward."""
+
+    @staticmethod
+    def forward(ctx, q, k, v, u, feat, cfg: AttnConfig):
+        q, k, v, u = q.contiguous(), k.contiguous(), v.contiguous(), u.contiguous()
+        o, den, sel = linmix_fwd(q, k, v, u, feat, cfg)
+        ctx.save_for_backward(q, k, v, u, feat, den)
+        ctx.sel, ctx.cfg = sel, cfg
+        return o
+
+    @staticmethod
+    def backward(ctx, do):
+        q, k, v, u, feat, den = ctx.saved_tensors
+        dq, dk, dv, du, dfeat = linmix_bwd(q, k, v, u, feat, den, do, ctx.sel, ctx.cfg)
+        return dq, dk, dv, du, dfeat.to(feat.dtype), None
+
+
+def linear_mix_core(q, k, v, u, feat, cfg: AttnConfig):
+    return LinearMixFn.apply(q, k, v, u, feat, cfg)
 
 
 # ---------------------------------------------------------------- scoring (K1)

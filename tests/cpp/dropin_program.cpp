@@ -183,6 +183,26 @@ static void attention_section(const std::string& tag) {
     put(tag + "_dense_dwq", dg.dwq.data);
     // matmul
     put(tag + "_matmul", matmul(x, P.wq).data);
+    // linear-attention mix (Appendix B.1): forward, backward with dfeat, chunked training
+    LinearMixParams<T> lin;
+    for (size_t h = 0; h < H; ++h) lin.feat.push_back(rnd<T>(r, D / H, D / H, 0.3));
+    AttnTape<T> lt;
+    MatT<T> yl = linear_mix_attention(x, P, sc, cfg, lin, &lt);
+    put(tag + "_lin_y", yl.data);
+    AttnGrads<T> lg = sparsek_attention_backward(lt, g, P, sc, &lin);
+    put(tag + "_lin_dx", lg.dx.data);
+    put(tag + "_lin_dwk", lg.dwk.data);
+    put(tag + "_lin_dws", lg.dw_score);
+    std::vector<double> dfe;
+    for (const auto& f : lg.dfeat) dfe.insert(dfe.end(), f.data.begin(), f.data.end());
+    put(tag + "_lin_dfeat", dfe);
+    AttnConfig lc = cfg;
+    lc.linear_mix = true;
+    AttnTape<T> lct;
+    MatT<T> ylc = chunked_forward(x, 32, P, sc, lc, &lct, &lin);
+    put(tag + "_lin_chunked_y", ylc.data);
+    AttnGrads<T> lcg = sparsek_attention_backward(lct, g, P, sc, &lin);
+    put(tag + "_lin_chunked_dx", lcg.dx.data);
 }
 
 static void errors_section() {
