@@ -68,6 +68,7 @@ struct BwdArgs {
     const int* ever_count;
     const int* ever_list;
     double *rowsum, *colsum;
+    float* dq32;      // fused dQ: fp32 [B, L, H, D] accumulator of dS K (unscaled), reduced into by the key-major passes
     int2* sel_items;  // [B][cdiv(L,128)] {q_lo, nq} of the selected pass's key tiles
     int* sel_order;   // [B][L] ever-selected keys grouped by leave time (the selected pass's order)
     int nqb, qb_cap;
@@ -141,9 +142,11 @@ struct KSmem {
     static constexpr int kV = kK + kKV;
     static constexpr int kQ = kV + kKV;          // [kQS]
     static constexpr int kDO = kQ + kQS * kQT;   // [kQS]
-    static constexpr int kMeta = kDO + kQS * kQT;  // [kQS][lse2|delta|tau][64] f32
+    static constexpr int kDS = kDO + kQS * kQT;   // dS^T of the tile (fused dQ): 128 keys x 64 queries bf16
+    static constexpr int kStage = kDS + (D == 128 ? 128 * 64 * 2 : 0);  // fused dQ: per-warp 16 x 32 fp32 transpose
+    static constexpr int kMeta = kStage + (D == 128 ? 8 * 2048 : 0);      // [kQS][lse2|delta|tau][64] f32
     static constexpr int kBar = kMeta + kQS * 3 * 64 * 4;
-    static constexpr int kNumBars = 16;
+    static constexpr int kNumBars = 22;
     static constexpr int kTmemSlot = kBar + kNumBars * 8;
     static constexpr int kAlloc = kTmemSlot + 16 + 1024;
 };
@@ -494,31 +497,89 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_tc(const __grid_consta
 // tiles load while the current item finishes its last dV/dK MMAs and its
 // epilogue; K/V are released by the commit of an item's last S/dP MMA, the
 // dV/dK accumulators by the math warps once they are read out.
-template <int D>
+template <int D, int QS = kQS, bool FQ = false>
 struct KWSmem {
     static constexpr int kKV = 128 * D * 2;
     static constexpr int kQT = 64 * D * 2;
     static constexpr int kK = 0;
     static constexpr int kV = kK + kKV;
-    static constexpr int kQ = kV + kKV;            // [kQS]
-    static constexpr int kDO = kQ + kQS * kQT;     // [kQS]
-    static constexpr int kPart = kDO + kQS * kQT;  // dK then dV partials of the tile (part_off order);
-    static constexpr int kPartB = 128 * D * 2;     //   the epilogue stages its bf16 rows in place
-    static constexpr int kMeta = kPart + 2 * kPartB;  // [kQS][lse2|delta][64] f32
-    static constexpr int kBar = kMeta + kQS * 2 * 64 * 4;
-    static constexpr int kTmemSlot = kBar + 18 * 8;
+    static constexpr int kQ = kV + kKV;           // [QS]
+    static constexpr int kDO = kQ + QS * kQT;     // [QS]
+    static constexpr int kPart = kDO + QS * kQT;  // dK then dV partials of the tile (part_off order);
+    static constexpr int kPartB = 128 * D * 2;    //   the epilogue stages its bf16 rows in place
+    static constexpr int kDS = kPart + 2 * kPartB;         // fused dQ: dS^T of the tile, 128 keys x 64 queries
+    static constexpr int kStage = kDS + (FQ ? 128 * 64 * 2 : 0);  // fused dQ: per-warp 16 x 32 fp32 transpose
+    static constexpr int kMeta = kStage + (FQ ? 8 * 2048 : 0);       // [QS][lse2|delta][64] f32
+    static constexpr int kBar = kMeta + QS * 2 * 64 * 4;
+    static constexpr int kTmemSlot = kBar + 22 * 8;
     static constexpr int kAlloc = kTmemSlot + 16 + 1024;
     static_assert(kAlloc <= 232448, "smem");
 };
 enum { KW_KVFULL = 0, KW_KVEMPTY = 1, KW_QDFULL = 2, KW_QDEMPTY = 5, KW_SFULL = 8, KW_SEMPTY = 10,
-       KW_PDSFULL = 12, KW_ACCDONE = 14, KW_ACCEMPTY = 15, KW_PARTFULL = 16, KW_STGFULL = 17 };  // 18 barriers
+       KW_PDSFULL = 12, KW_ACCDONE = 14, KW_ACCEMPTY = 15, KW_PARTFULL = 16, KW_STGFULL = 17,
+       KW_DQFULL = 18, KW_DQEMPTY = 20 };  // 22 barriers (fused dQ: DQFULL x2 = a tile's dQ^T is complete
+                                           // in TMEM, DQEMPTY x2 = it has been read back)
+
+// Fused dQ (D = 128): the key-major passes also form dQ^T = K^T dS^T per
+// 64-query tile (M = 128 head dims, N = 64 queries, K = 128 keys) in the
+// consumed dP^T columns of the tile's TMEM buffer; the math warps read it
+// back during the next tile (or at the item's end) and add it into the fp32
+// accumulator with coalesced reductions (a warp covers 32 consecutive head
+// dims of one query). The separate query-major dQ pass, which recomputed S
+// and dP, disappears: 5 GEMM-units per attended pair instead of 7 (opt-in,
+// SKB_BWD_FUSEDQ=1; fused_dq below says why it is not the default).
+template <int D>
+__device__ __forceinline__ void dq_reduce(const BwdArgs& a, int b, int h, int q0, int drow, const float* v,
+                                          float* stage) {
+#if defined(SKB_FQ_EXP) && SKB_FQ_EXP == 1
+    return;  // experiment: no reductions (timing only)
+#endif
+    // this warp holds head dims [d0, d0 + 32) (one per lane) of queries
+    // [q0, q0 + 32): transposed through a 16-query shared-memory tile so each
+    // lane adds 4 consecutive head dims of one query (red.global.add.v4.f32;
+    // 8 lanes cover one query's 128 contiguous bytes)
+    const int lane = threadIdx.x & 31, d0 = drow - lane;
+    const int64_t st = (int64_t)a.H * D;
+    float* gbase = a.dq32 + (((int64_t)b * a.L + q0) * a.H + h) * D + d0 + (lane & 7) * 4;
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+        __syncwarp();
+#pragma unroll
+        for (int c = 0; c < 16; ++c) stage[c * 32 + lane] = v[half * 16 + c];
+        __syncwarp();
+#pragma unroll
+        for (int it = 0; it < 4; ++it) {
+            const int qq = it * 4 + (lane >> 3);  // query within the half
+            const int q = half * 16 + qq;
+            if (q0 + q < a.L) {
+                const float4 x = *reinterpret_cast<const float4*>(stage + qq * 32 + (lane & 7) * 4);
+                asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(gbase + q * st), "f"(x.x),
+                             "f"(x.y), "f"(x.z), "f"(x.w)
+                             : "memory");
+            }
+        }
+    }
+}
+// Row (key) r's 32 dS^T values of query half hf -> the SW128 dS^T tile
+// (row r = 128 B = 64 queries; the K-major A operand of dK += dS^T Q and the
+// MN-major B operand of dQ^T = K^T dS^T).
+__device__ __forceinline__ void ds_store(uint32_t ds_base, int r, int hf, const float* dp) {
+#pragma unroll
+    for (int cc = 0; cc < 4; ++cc) {
+        const int chunk = hf * 4 + cc;
+        st_shared_v4(ds_base + r * 128 + ((chunk ^ (r & 7)) << 4), pack_bf16(dp[8 * cc], dp[8 * cc + 1]),
+                     pack_bf16(dp[8 * cc + 2], dp[8 * cc + 3]), pack_bf16(dp[8 * cc + 4], dp[8 * cc + 5]),
+                     pack_bf16(dp[8 * cc + 6], dp[8 * cc + 7]));
+    }
+}
 // producer threads (warps 8-9) on the Q/dO ring; warp 10 moves the partials in
 // and the finished dK/dV rows out
 constexpr int kWinQProd = 64;
 
-template <int D>
+template <int D, bool FQ>
 __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_win_tc(const __grid_constant__ BwdArgs a) {
-    using SM = KWSmem<D>;
+    constexpr int QS = FQ ? 2 : kQS;  // the fused-dQ build gives one Q/dO stage to the dS^T tile
+    using SM = KWSmem<D, QS, FQ>;
     extern __shared__ __align__(16) uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const uint32_t sbase = smem_u32(smem);
@@ -557,7 +618,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_win_tc(const __grid_co
     if (threadIdx.x == 0) {
         mbar_init(&bars[KW_KVFULL], 1);
         mbar_init(&bars[KW_KVEMPTY], 1);
-        for (int s = 0; s < kQS; ++s) {
+        for (int s = 0; s < QS; ++s) {
             mbar_init(&bars[KW_QDFULL + s], kWinQProd + 1);
             mbar_init(&bars[KW_QDEMPTY + s], 1);
         }
@@ -570,6 +631,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_win_tc(const __grid_co
         mbar_init(&bars[KW_ACCEMPTY], kMath);
         mbar_init(&bars[KW_PARTFULL], 1);
         mbar_init(&bars[KW_STGFULL], kMath);
+        mbar_init(&bars[KW_DQFULL], 1);
+        mbar_init(&bars[KW_DQFULL + 1], 1);
+        mbar_init(&bars[KW_DQEMPTY], kMath);
+        mbar_init(&bars[KW_DQEMPTY + 1], kMath);
         mbar_fence_init();
     }
     if (warp == kMmaWarp) tmem_alloc<512>(tmem_slot);
@@ -639,9 +704,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_win_tc(const __grid_co
             const float* lse2 = a.lse2 + ((int64_t)b * a.H + h) * a.L;
             const float* dlt = a.delta + ((int64_t)b * a.H + h) * a.L;
             for (int qt = 0; qt < nq; ++qt, ++g) {
-                const int s = g % kQS;
+                const int s = g % QS;
                 if (ptid == 0) TRW(6, g, 0);
-                if (g >= kQS) mbar_wait(&bars[KW_QDEMPTY + s], ((g - kQS) / kQS) & 1);
+                if (g >= QS) mbar_wait(&bars[KW_QDEMPTY + s], ((g - QS) / QS) & 1);
                 if (ptid == 0) TRW(6, g, 1);
                 const int qs = j0 + qt * 64;
                 {
@@ -673,20 +738,40 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_win_tc(const __grid_co
             // dV += P~^T dO, dK += dS^T Q for the tile at global index gj (item
             // tile qt); the first tile of an item waits for the accumulators
             auto acc = [&](int gj, int qt, int itn) {
-                const int s = gj & 1, qs = gj % kQS;
+                const int s = gj & 1, qs = gj % QS;
                 mbar_wait(&bars[KW_PDSFULL + s], (gj >> 1) & 1);
                 TRW(7, gj, 2);
                 if (qt == 0 && itn > 0) mbar_wait(&bars[KW_ACCEMPTY], (itn - 1) & 1);
                 TRW(7, gj, 3);
                 tc_after_sync();
                 const uint32_t dob = sbase + SM::kDO + qs * SM::kQT, qb = sbase + SM::kQ + qs * SM::kQT;
+                if constexpr (FQ) {
+                    fence_proxy_async();  // the dS^T tile (st.shared) -> the MMAs
+                    constexpr uint32_t id_dq = umma_idesc(128, 64, true, true);
+                    const uint32_t dsb = sbase + SM::kDS;
 #pragma unroll
-                for (int kk = 0; kk < 4; ++kk) {
-                    const uint32_t co = s * 64 + (kk >> 1) * 32 + (kk & 1) * 8;
-                    umma_f16_ts(tDV, tS + co, desc_mnmajor(dob, 64, kk), id_acc, (qt > 0 || kk > 0) ? 1u : 0u);
-                    umma_f16_ts(tDK, tP + co, desc_mnmajor(qb, 64, kk), id_acc, (qt > 0 || kk > 0) ? 1u : 0u);
+                    for (int kk = 0; kk < 4; ++kk) {
+                        const uint32_t co = s * 64 + (kk >> 1) * 32 + (kk & 1) * 8;
+                        umma_f16_ts(tDV, tS + co, desc_mnmajor(dob, 64, kk), id_acc, (qt > 0 || kk > 0) ? 1u : 0u);
+                        umma_f16(tDK, desc_kmajor(dsb, 128, kk), desc_mnmajor(qb, 64, kk), id_acc,
+                                 (qt > 0 || kk > 0) ? 1u : 0u);
+                    }
+                    umma_commit(&bars[KW_QDEMPTY + qs]);
+                    // dQ^T = K^T dS^T into the tile's consumed dP^T columns
+#pragma unroll
+                    for (int kk = 0; kk < 8; ++kk)
+                        umma_f16(tP + s * 64, desc_mnmajor(sbase + SM::kK, 128, kk), desc_mnmajor(dsb, 128, kk), id_dq,
+                                 kk > 0 ? 1u : 0u);
+                    umma_commit(&bars[KW_DQFULL + s]);
+                } else {
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) {
+                        const uint32_t co = s * 64 + (kk >> 1) * 32 + (kk & 1) * 8;
+                        umma_f16_ts(tDV, tS + co, desc_mnmajor(dob, 64, kk), id_acc, (qt > 0 || kk > 0) ? 1u : 0u);
+                        umma_f16_ts(tDK, tP + co, desc_mnmajor(qb, 64, kk), id_acc, (qt > 0 || kk > 0) ? 1u : 0u);
+                    }
+                    umma_commit(&bars[KW_QDEMPTY + qs]);
                 }
-                umma_commit(&bars[KW_QDEMPTY + qs]);
             };
             for (int wi = blockIdx.x; wi < nitems; wi += gridDim.x, ++it) {
                 int b, h, j0, nkeys, nq;
@@ -696,27 +781,41 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_win_tc(const __grid_co
                 TRW(7, g, 4);
                 tc_after_sync();
                 for (int qt = 0; qt < nq; ++qt, ++g) {
-                    const int s = g & 1, qs = g % kQS;
+                    const int s = g & 1, qs = g % QS;
                     TRW(7, g, 8);
-                    mbar_wait(&bars[KW_QDFULL + qs], (g / kQS) & 1);
+                    mbar_wait(&bars[KW_QDFULL + qs], (g / QS) & 1);
                     TRW(7, g, 0);
                     if (g >= 2) mbar_wait(&bars[KW_SEMPTY + s], ((g - 2) >> 1) & 1);
                     TRW(7, g, 5);
                     tc_after_sync();
                     const uint32_t qb = sbase + SM::kQ + qs * SM::kQT, dob = sbase + SM::kDO + qs * SM::kQT;
+                    if constexpr (FQ) {  // S^T first: dP^T's columns may still hold dQ^T(g-2) being read back
 #pragma unroll
-                    for (int kk = 0; kk < D / 16; ++kk) {
-                        umma_f16(tS + s * 64, desc_kmajor(sbase + SM::kK, 128, kk), desc_kmajor(qb, 64, kk), id_s,
-                                 kk > 0 ? 1u : 0u);
-                        umma_f16(tP + s * 64, desc_kmajor(sbase + SM::kV, 128, kk), desc_kmajor(dob, 64, kk), id_s,
-                                 kk > 0 ? 1u : 0u);
+                        for (int kk = 0; kk < D / 16; ++kk)
+                            umma_f16(tS + s * 64, desc_kmajor(sbase + SM::kK, 128, kk), desc_kmajor(qb, 64, kk), id_s,
+                                     kk > 0 ? 1u : 0u);
+                        if (g >= 2) mbar_wait(&bars[KW_DQEMPTY + s], ((g - 2) >> 1) & 1);
+                        tc_after_sync();
+#pragma unroll
+                        for (int kk = 0; kk < D / 16; ++kk)
+                            umma_f16(tP + s * 64, desc_kmajor(sbase + SM::kV, 128, kk), desc_kmajor(dob, 64, kk), id_s,
+                                     kk > 0 ? 1u : 0u);
+                    } else {
+#pragma unroll
+                        for (int kk = 0; kk < D / 16; ++kk) {
+                            umma_f16(tS + s * 64, desc_kmajor(sbase + SM::kK, 128, kk), desc_kmajor(qb, 64, kk), id_s,
+                                     kk > 0 ? 1u : 0u);
+                            umma_f16(tP + s * 64, desc_kmajor(sbase + SM::kV, 128, kk), desc_kmajor(dob, 64, kk), id_s,
+                                     kk > 0 ? 1u : 0u);
+                        }
                     }
                     umma_commit(&bars[KW_SFULL + s]);
                     TRW(7, g, 1);
-                    if (qt == nq - 1) umma_commit(&bars[KW_KVEMPTY]);
+                    if (!FQ && qt == nq - 1) umma_commit(&bars[KW_KVEMPTY]);
                     if (qt >= 1) acc(g - 1, qt - 1, it);
                 }
                 acc(g - 1, nq - 1, it);
+                if (FQ) umma_commit(&bars[KW_KVEMPTY]);  // the last dQ^T MMA has read K
                 umma_commit(&bars[KW_ACCDONE]);
             }
         }
@@ -742,11 +841,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_win_tc(const __grid_co
             if (a.chunk_len > 0 && key >= 0) hi_i = min(hi_i, (key / a.chunk_len + 1) * a.chunk_len);
             const bool has_sel = key >= 0 && key < a.T && tile_sel(j0) && __ldg(a.leave + bl + key) > key;
             for (int qt = 0; qt < nq; ++qt, ++g) {
-                const int s = g & 1, qs3 = g % kQS;
+                const int s = g & 1, qs3 = g % QS;
                 const int qs = j0 + qt * 64 + hf * 32;
                 if (trl) TRW(4 + hf, g, 9);
                 mbar_wait(&bars[KW_SFULL + s], (g >> 1) & 1);
-                mbar_wait(&bars[KW_QDFULL + qs3], (g / kQS) & 1);
+                mbar_wait(&bars[KW_QDFULL + qs3], (g / QS) & 1);
                 if (trl) TRW(4 + hf, g, 0);
                 tc_after_sync();
                 float sv[32], dp[32];
@@ -754,7 +853,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_win_tc(const __grid_co
                 tmem_ld32(tP + lane_off + s * 64 + hf * 32, dp);
                 tmem_wait_ld();
                 tc_before_sync();
-                mbar_arrive(&bars[KW_SEMPTY + s]);
+                mbar_arrive(&bars[KW_SEMPTY + s]);  // fused dQ: the dP^T half is released after its dQ^T is read
                 const float* ml = qmeta + (qs3 * 2) * 64 + hf * 32;
                 const float* md = ml + 64;
                 const int cmin = key >= 0 ? key - qs : 32;
@@ -778,7 +877,32 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_win_tc(const __grid_co
                     sv[c] = x0.x, sv[c + 1] = x0.y, sv[c + 2] = x1.x, sv[c + 3] = x1.y;
                     dp[c] = c0.x, dp[c + 1] = c0.y, dp[c + 2] = c1.x, dp[c + 3] = c1.y;
                 }
-                {
+                if constexpr (FQ) {
+                    {
+                        uint32_t pk[16];
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) pk[e] = pack_bf16(sv[2 * e], sv[2 * e + 1]);
+                        tmem_st16u(tS + lane_off + s * 64 + hf * 32, pk);
+                    }
+                    const int sp = (g - 1) & 1;
+                    // the single dS^T tile is free once the previous tile's dK / dQ^T MMAs completed
+                    if (qt > 0) mbar_wait(&bars[KW_DQFULL + sp], ((g - 1) >> 1) & 1);
+                    ds_store(sbase + SM::kDS, r, hf, dp);
+                    fence_async_smem();
+                    tmem_wait_st();
+                    tc_before_sync();
+                    if (trl) TRW(4 + hf, g, 4);
+                    mbar_arrive(&bars[KW_PDSFULL + s]);
+                    if (qt > 0) {  // the previous tile's dQ^T -> the fp32 accumulator
+                        tc_after_sync();
+                        float qv[32];
+                        tmem_ld32(tP + lane_off + sp * 64 + hf * 32, qv);
+                        tmem_wait_ld();
+                        tc_before_sync();
+                        mbar_arrive(&bars[KW_DQEMPTY + sp]);
+                        dq_reduce<D>(a, b, h, qs - 64, r, qv, reinterpret_cast<float*>(smem + SM::kStage) + warp * 512);
+                    }
+                } else {
                     uint32_t pk[16];
 #pragma unroll
                     for (int e = 0; e < 16; ++e) pk[e] = pack_bf16(sv[2 * e], sv[2 * e + 1]);
@@ -787,10 +911,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_win_tc(const __grid_co
                     for (int e = 0; e < 16; ++e) pk[e] = pack_bf16(dp[2 * e], dp[2 * e + 1]);
                     tmem_st16u(tP + lane_off + s * 64 + hf * 32, pk);
                     tmem_wait_st();
+                    tc_before_sync();
+                    if (trl) TRW(4 + hf, g, 4);
+                    mbar_arrive(&bars[KW_PDSFULL + s]);
                 }
+            }
+            if constexpr (FQ) {  // the item's last tile: its dQ^T
+                const int sp = (g - 1) & 1;
+                mbar_wait(&bars[KW_DQFULL + sp], ((g - 1) >> 1) & 1);
+                tc_after_sync();
+                float qv[32];
+                tmem_ld32(tP + lane_off + sp * 64 + hf * 32, qv);
+                tmem_wait_ld();
                 tc_before_sync();
-                if (trl) TRW(4 + hf, g, 4);
-                mbar_arrive(&bars[KW_PDSFULL + s]);
+                mbar_arrive(&bars[KW_DQEMPTY + sp]);
+                dq_reduce<D>(a, b, h, j0 + (nq - 1) * 64 + hf * 32, r, qv, reinterpret_cast<float*>(smem + SM::kStage) + warp * 512);
             }
             mbar_wait(&bars[KW_ACCDONE], it & 1);
             if (trl) TRW(4 + hf, g, 5);
@@ -945,10 +1080,10 @@ __global__ void k_sel_items(BwdArgs a, int ntk) {
 // tile's row gathers and first query tiles load under the current tile's last
 // MMAs and epilogue. K/V rows are gathered (cp.async) after the commit of the
 // item's last S/dP MMA releases the buffer.
-template <int D, bool KEY_SOFT>
+template <int D, bool KEY_SOFT, bool FQ>
 __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_sel_tc(const __grid_constant__ BwdArgs a) {
     using SM = KSmem<D>;
-    static_assert(KW_ACCEMPTY < SM::kNumBars, "barrier slots");
+    static_assert(KW_DQFULL + 1 < SM::kNumBars, "barrier slots");
     extern __shared__ __align__(16) uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const uint32_t sbase = smem_u32(smem);
@@ -996,6 +1131,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_sel_tc(const __grid_co
         }
         mbar_init(&bars[KW_ACCDONE], 1);
         mbar_init(&bars[KW_ACCEMPTY], kMath);
+        mbar_init(&bars[KW_DQFULL], 1);
+        mbar_init(&bars[KW_DQFULL + 1], 1);
+        mbar_init(&bars[KW_DQEMPTY], kMath);
+        mbar_init(&bars[KW_DQEMPTY + 1], kMath);
         mbar_fence_init();
     }
     if (warp == kMmaWarp) tmem_alloc<512>(tmem_slot);
@@ -1066,13 +1205,32 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_sel_tc(const __grid_co
                 if (qt == 0 && kitn > 0) mbar_wait(&bars[KW_ACCEMPTY], (kitn - 1) & 1);
                 tc_after_sync();
                 const uint32_t dob = sbase + SM::kDO + qs * SM::kQT, qb = sbase + SM::kQ + qs * SM::kQT;
+                if constexpr (FQ) {
+                    fence_proxy_async();  // the dS^T tile (st.shared) -> the MMAs
+                    constexpr uint32_t id_dq = umma_idesc(128, 64, true, true);
+                    const uint32_t dsb = sbase + SM::kDS;
 #pragma unroll
-                for (int kk = 0; kk < 4; ++kk) {
-                    const uint32_t co = s * 64 + (kk >> 1) * 32 + (kk & 1) * 8;
-                    umma_f16_ts(tDV, tS + co, desc_mnmajor(dob, 64, kk), id_acc, (qt > 0 || kk > 0) ? 1u : 0u);
-                    umma_f16_ts(tDK, tP + co, desc_mnmajor(qb, 64, kk), id_acc, (qt > 0 || kk > 0) ? 1u : 0u);
+                    for (int kk = 0; kk < 4; ++kk) {
+                        const uint32_t co = s * 64 + (kk >> 1) * 32 + (kk & 1) * 8;
+                        umma_f16_ts(tDV, tS + co, desc_mnmajor(dob, 64, kk), id_acc, (qt > 0 || kk > 0) ? 1u : 0u);
+                        umma_f16(tDK, desc_kmajor(dsb, 128, kk), desc_mnmajor(qb, 64, kk), id_acc,
+                                 (qt > 0 || kk > 0) ? 1u : 0u);
+                    }
+                    umma_commit(&bars[KW_QDEMPTY + qs]);
+#pragma unroll
+                    for (int kk = 0; kk < 8; ++kk)
+                        umma_f16(tP + s * 64, desc_mnmajor(sbase + SM::kK, 128, kk), desc_mnmajor(dsb, 128, kk), id_dq,
+                                 kk > 0 ? 1u : 0u);
+                    umma_commit(&bars[KW_DQFULL + s]);
+                } else {
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) {
+                        const uint32_t co = s * 64 + (kk >> 1) * 32 + (kk & 1) * 8;
+                        umma_f16_ts(tDV, tS + co, desc_mnmajor(dob, 64, kk), id_acc, (qt > 0 || kk > 0) ? 1u : 0u);
+                        umma_f16_ts(tDK, tP + co, desc_mnmajor(qb, 64, kk), id_acc, (qt > 0 || kk > 0) ? 1u : 0u);
+                    }
+                    umma_commit(&bars[KW_QDEMPTY + qs]);
                 }
-                umma_commit(&bars[KW_QDEMPTY + qs]);
             };
             for (int wi = blockIdx.x; wi < nitems; wi += gridDim.x) {
                 int b, h, kt, nkeys, q_lo, nq;
@@ -1089,19 +1247,33 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_sel_tc(const __grid_co
                     if (g >= 2) mbar_wait(&bars[KW_SEMPTY + s], ((g - 2) >> 1) & 1);
                     tc_after_sync();
                     const uint32_t qb = sbase + SM::kQ + qs * SM::kQT, dob = sbase + SM::kDO + qs * SM::kQT;
+                    if constexpr (FQ) {  // S^T first: dP^T's columns may still hold dQ^T(g-2) being read back
 #pragma unroll
-                    for (int kk = 0; kk < D / 16; ++kk) {
-                        umma_f16(tS + s * 64, desc_kmajor(sbase + SM::kK, 128, kk), desc_kmajor(qb, 64, kk), id_s,
-                                 kk > 0 ? 1u : 0u);
-                        umma_f16(tP + s * 64, desc_kmajor(sbase + SM::kV, 128, kk), desc_kmajor(dob, 64, kk), id_s,
-                                 kk > 0 ? 1u : 0u);
+                        for (int kk = 0; kk < D / 16; ++kk)
+                            umma_f16(tS + s * 64, desc_kmajor(sbase + SM::kK, 128, kk), desc_kmajor(qb, 64, kk), id_s,
+                                     kk > 0 ? 1u : 0u);
+                        if (g >= 2) mbar_wait(&bars[KW_DQEMPTY + s], ((g - 2) >> 1) & 1);
+                        tc_after_sync();
+#pragma unroll
+                        for (int kk = 0; kk < D / 16; ++kk)
+                            umma_f16(tP + s * 64, desc_kmajor(sbase + SM::kV, 128, kk), desc_kmajor(dob, 64, kk), id_s,
+                                     kk > 0 ? 1u : 0u);
+                    } else {
+#pragma unroll
+                        for (int kk = 0; kk < D / 16; ++kk) {
+                            umma_f16(tS + s * 64, desc_kmajor(sbase + SM::kK, 128, kk), desc_kmajor(qb, 64, kk), id_s,
+                                     kk > 0 ? 1u : 0u);
+                            umma_f16(tP + s * 64, desc_kmajor(sbase + SM::kV, 128, kk), desc_kmajor(dob, 64, kk), id_s,
+                                     kk > 0 ? 1u : 0u);
+                        }
                     }
                     umma_commit(&bars[KW_SFULL + s]);
                     TRS(7, g, 1);
-                    if (qt == nq - 1) umma_commit(&bars[KW_KVEMPTY]);
+                    if (!FQ && qt == nq - 1) umma_commit(&bars[KW_KVEMPTY]);
                     if (qt >= 1) acc(g - 1, qt - 1, kit);
                 }
                 acc(g - 1, nq - 1, kit);
+                if (FQ) umma_commit(&bars[KW_KVEMPTY]);  // the last dQ^T MMA has read K
                 umma_commit(&bars[KW_ACCDONE]);
                 ++kit;
             }
@@ -1142,7 +1314,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_sel_tc(const __grid_co
                 tmem_ld32(tP + lane_off + s * 64 + hf * 32, dp);
                 tmem_wait_ld();
                 tc_before_sync();
-                mbar_arrive(&bars[KW_SEMPTY + s]);
+                mbar_arrive(&bars[KW_SEMPTY + s]);  // fused dQ: the dP^T half is released after its dQ^T is read
                 const float* ml = qmeta + (qs3 * 3) * 64 + hf * 32;
                 const float* md = ml + 64;
                 const float* mt = ml + 128;
@@ -1156,6 +1328,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_sel_tc(const __grid_co
 #pragma unroll
                     for (int c = 0; c < 32; ++c) sv[c] = (c >= cmin && c <= cmax) ? sv[c] : -INFINITY;
                 }
+                float rg[FQ ? 32 : 1];  // fused dQ: this key's fractional gate gradients per query (row sums)
                 if (sat) {  // gates 1 on these columns: plain softmax backward, packed fp32x2
 #pragma unroll
                     for (int c = 0; c < 32; c += 4) {
@@ -1198,7 +1371,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_sel_tc(const __grid_co
                             // 0 < g < 1 <=> (bits(g) - 1) < bits(1.0) - 1 (g in [0, 1])
                             const float2 fr2 = make_float2((__float_as_uint(g0) - 1u) < 0x3F7FFFFFu ? 1.f : 0.f,
                                                            (__float_as_uint(g1) - 1u) < 0x3F7FFFFFu ? 1.f : 0.f);
-                            csum2 = __ffma2_rn(__fmul2_rn(p2, dp2), fr2, csum2);
+                            const float2 gf2 = __fmul2_rn(__fmul2_rn(p2, dp2), fr2);
+                            csum2 = __fadd2_rn(csum2, gf2);
+                            if constexpr (FQ) rg[c] = gf2.x, rg[c + 1] = gf2.y;
                             const float2 pw2 = kMst ? p2 : __fmul2_rn(p2, g2);
                             sv[c] = pw2.x, sv[c + 1] = pw2.y;  // P~^T
                             dp[c] = cc2.x, dp[c + 1] = cc2.y;  // dS^T (scale applied in the epilogue)
@@ -1229,14 +1404,56 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_sel_tc(const __grid_co
                             const float cc = p * fmaf(wv, dp[cc_], -da[e]);
                             float gm = p * dp[cc_];
                             if (KEY_SOFT) gm += a.scale * cc * (raw == -INFINITY ? 0.f : raw);
-                            csum += (gt > 0.f && gt < 1.f) ? gm : 0.f;
+                            const float gf = (gt > 0.f && gt < 1.f) ? gm : 0.f;
+                            csum += gf;
+                            if constexpr (FQ) rg[cc_] = gf;
                             sv[cc_] = p * wv;    // P~^T
                             dp[cc_] = cc * kap;  // dS^T (scale applied in the epilogue)
                         }
                     }
                     colsum += csum;
                 }
-                {
+                if constexpr (FQ) {
+                    if (!sat) {  // the query-side sums of the gate gradients (the dQ pass's rowsum):
+                        // reduce-scatter over the warp's 32 keys, lane c ends with query column c
+#pragma unroll
+                        for (int off = 16; off >= 1; off >>= 1) {
+                            const bool up = (lane & off) != 0;
+#pragma unroll
+                            for (int q2 = 0; q2 < off; ++q2) {
+                                const float keep = up ? rg[q2 + off] : rg[q2];
+                                const float send = up ? rg[q2] : rg[q2 + off];
+                                rg[q2] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+                            }
+                        }
+                        const int i = qs + lane, t = i - a.w;
+                        if (rg[0] != 0.f && i < a.L && t >= 0) atomicAdd(a.rowsum + bl + t, (double)rg[0]);
+                    }
+                    {
+                        uint32_t pk[16];
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) pk[e] = pack_bf16(sv[2 * e], sv[2 * e + 1]);
+                        tmem_st16u(tS + lane_off + s * 64 + hf * 32, pk);
+                    }
+                    const int sp = (g - 1) & 1;
+                    // the single dS^T tile is free once the previous tile's dK / dQ^T MMAs completed
+                    if (qt > 0) mbar_wait(&bars[KW_DQFULL + sp], ((g - 1) >> 1) & 1);
+                    ds_store(sbase + SM::kDS, r, hf, dp);
+                    fence_async_smem();
+                    tmem_wait_st();
+                    tc_before_sync();
+                    if (trl) TRS(4 + hf, g, 4);
+                    mbar_arrive(&bars[KW_PDSFULL + s]);
+                    if (qt > 0) {  // the previous tile's dQ^T -> the fp32 accumulator
+                        tc_after_sync();
+                        float qv[32];
+                        tmem_ld32(tP + lane_off + sp * 64 + hf * 32, qv);
+                        tmem_wait_ld();
+                        tc_before_sync();
+                        mbar_arrive(&bars[KW_DQEMPTY + sp]);
+                        dq_reduce<D>(a, b, h, qs - 64, r, qv, reinterpret_cast<float*>(smem + SM::kStage) + warp * 512);
+                    }
+                } else {
                     uint32_t pk[16];
 #pragma unroll
                     for (int e = 0; e < 16; ++e) pk[e] = pack_bf16(sv[2 * e], sv[2 * e + 1]);
@@ -1245,10 +1462,23 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_sel_tc(const __grid_co
                     for (int e = 0; e < 16; ++e) pk[e] = pack_bf16(dp[2 * e], dp[2 * e + 1]);
                     tmem_st16u(tP + lane_off + s * 64 + hf * 32, pk);
                     tmem_wait_st();
+                    tc_before_sync();
+                    if (trl) TRS(4 + hf, g, 4);
+                    mbar_arrive(&bars[KW_PDSFULL + s]);
                 }
-                tc_before_sync();
-                if (trl) TRS(4 + hf, g, 4);
-                mbar_arrive(&bars[KW_PDSFULL + s]);
+            }
+            if constexpr (FQ) {
+                if (nq > 0) {  // the item's last tile: its dQ^T
+                    const int sp = (g - 1) & 1;
+                    mbar_wait(&bars[KW_DQFULL + sp], ((g - 1) >> 1) & 1);
+                    tc_after_sync();
+                    float qv[32];
+                    tmem_ld32(tP + lane_off + sp * 64 + hf * 32, qv);
+                    tmem_wait_ld();
+                    tc_before_sync();
+                    mbar_arrive(&bars[KW_DQEMPTY + sp]);
+                    dq_reduce<D>(a, b, h, q_lo + (nq - 1) * 64 + hf * 32, r, qv, reinterpret_cast<float*>(smem + SM::kStage) + warp * 512);
+                }
             }
             if (key >= 0 && colsum != 0.f) atomicAdd(a.colsum + bl + key, (double)colsum);
             float dv[D / 2], dk[D / 2];
@@ -2049,19 +2279,58 @@ void set_smem(K kern, int bytes) {
     SKB_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
 }
 
+// dq = bf16(scale * dq32) (the fused passes accumulate dS K unscaled)
+__global__ void __launch_bounds__(256) k_dq_convert(const float* __restrict__ acc, __nv_bfloat16* __restrict__ dq,
+                                                    int64_t n8, float scale) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n8) return;
+    const float4 x = reinterpret_cast<const float4*>(acc)[2 * i];
+    const float4 y = reinterpret_cast<const float4*>(acc)[2 * i + 1];
+    uint4 o;
+    o.x = pack_bf16(x.x * scale, x.y * scale);
+    o.y = pack_bf16(x.z * scale, x.w * scale);
+    o.z = pack_bf16(y.x * scale, y.y * scale);
+    o.w = pack_bf16(y.z * scale, y.w * scale);
+    reinterpret_cast<uint4*>(dq)[i] = o;
+}
+
+// The fused-dQ backward (D = 128, SKB_BWD_FUSEDQ=1): dQ formed by the
+// key-major passes instead of the query-major dQ pass. Measured slower at cfg3
+// (bwd 4.16 vs 4.03 ms): the dQ^T read-back gates the
+// next dP^T MMA into the same TMEM columns, the window pass loses a Q/dO ring
+// stage to the dS^T tile, and the fp32 reductions (8 red.v4 per thread per
+// tile) cost ~0.4 ms; it also makes dQ depend on the reduction order (not
+// bit-reproducible across grid sizes). Kept for A/B; the default is the dQ
+// pass. Chunk-wise training always takes the dQ pass: there the key-major
+// passes clip a key's queries to its own chunk (dK/dV never cross a chunk
+// start), while dQ and the gate-gradient row sums still collect from every
+// attended key (proj/src/attention.cpp:228-234, 284-300).
+inline bool fused_dq(int D, int chunk_len) {
+    static const int fused = getenv("SKB_BWD_FUSEDQ") ? atoi(getenv("SKB_BWD_FUSEDQ")) : 0;
+    return D == 128 && fused && chunk_len == 0;
+}
+
 template <int D, bool KS>
 void launch_bwd(const BwdArgs& a, const skb_attn_desc& d, cudaStream_t st) {
+    constexpr bool kFQ = D == 128;
+    const bool fq = fused_dq(D, a.chunk_len);
     static uint64_t attr = 0;
     if (first_on_device(&attr)) {
         set_smem(k_bwd_dkdv_tc<D, true, KS>, KSmem<D>::kAlloc);
-        set_smem(k_bwd_dkdv_sel_tc<D, KS>, KSmem<D>::kAlloc);
-        set_smem(k_bwd_dkdv_win_tc<D>, KWSmem<D>::kAlloc);
+        set_smem(k_bwd_dkdv_sel_tc<D, KS, false>, KSmem<D>::kAlloc);
+        set_smem(k_bwd_dkdv_win_tc<D, false>, KWSmem<D>::kAlloc);
+        if constexpr (kFQ) {
+            set_smem(k_bwd_dkdv_sel_tc<D, KS, true>, KSmem<D>::kAlloc);
+            set_smem(k_bwd_dkdv_win_tc<D, true>, KWSmem<D, 2, true>::kAlloc);
+        }
         set_smem(k_bwd_dq_tc<D, KS>, QSmem<D>::kAlloc);
         set_smem(k_bwd_dq_p<D, KS>, QSmem<D>::kAlloc);
     }
+    const int64_t ndq = (int64_t)a.B * a.L * a.H * D;
+    if (fq) SKB_CHECK_CUDA(cudaMemsetAsync(a.dq32, 0, (size_t)ndq * sizeof(float), st));
     if (a.R1 > 0 && a.T > 0) {
         static const int persist = getenv("SKB_SEL_PERSIST") ? atoi(getenv("SKB_SEL_PERSIST")) : 1;
-        if (persist) {
+        if (persist || fq) {
             const int ntk = (int)cdiv(a.L, 128);
             const int osm = kOrdCntBytes + std::min(a.T, kOrdMaxBk);
             static uint64_t oattr = 0;
@@ -2072,7 +2341,12 @@ void launch_bwd(const BwdArgs& a, const skb_attn_desc& d, cudaStream_t st) {
             SKB_CHECK_LAUNCH();
             const int64_t items = (int64_t)ntk * d.heads * d.batch;
             const int grid = persist_grid(items);
-            k_bwd_dkdv_sel_tc<D, KS><<<grid, kThreads, KSmem<D>::kAlloc, st>>>(a);
+            if constexpr (kFQ) {
+                if (fq) k_bwd_dkdv_sel_tc<D, KS, true><<<grid, kThreads, KSmem<D>::kAlloc, st>>>(a);
+                else k_bwd_dkdv_sel_tc<D, KS, false><<<grid, kThreads, KSmem<D>::kAlloc, st>>>(a);
+            } else {
+                k_bwd_dkdv_sel_tc<D, KS, false><<<grid, kThreads, KSmem<D>::kAlloc, st>>>(a);
+            }
         } else {
             dim3 gs((unsigned)cdiv(a.T, 128), (unsigned)d.heads, (unsigned)d.batch);
             k_bwd_dkdv_tc<D, true, KS><<<gs, kThreads, KSmem<D>::kAlloc, st>>>(a);
@@ -2082,8 +2356,18 @@ void launch_bwd(const BwdArgs& a, const skb_attn_desc& d, cudaStream_t st) {
     {
         const int64_t items = cdiv(a.L, 128) * d.heads * d.batch;
         const int grid = persist_grid(items);
-        k_bwd_dkdv_win_tc<D><<<grid, kThreads, KWSmem<D>::kAlloc, st>>>(a);
+        if constexpr (kFQ) {
+            if (fq) k_bwd_dkdv_win_tc<D, true><<<grid, kThreads, KWSmem<D, 2, true>::kAlloc, st>>>(a);
+            else k_bwd_dkdv_win_tc<D, false><<<grid, kThreads, KWSmem<D>::kAlloc, st>>>(a);
+        } else {
+            k_bwd_dkdv_win_tc<D, false><<<grid, kThreads, KWSmem<D>::kAlloc, st>>>(a);
+        }
         SKB_CHECK_LAUNCH();
+    }
+    if (fq) {
+        k_dq_convert<<<(unsigned)cdiv(ndq / 8, 256), 256, 0, st>>>(a.dq32, a.dq, ndq / 8, a.scale);
+        SKB_CHECK_LAUNCH();
+        return;
     }
     static const int dq_persist = getenv("SKB_DQ_PERSIST") ? atoi(getenv("SKB_DQ_PERSIST")) : 1;
     if (dq_persist) {
@@ -2145,6 +2429,7 @@ void run_attn_bwd_tc(const skb_attn_desc& d, const void* q, const void* k, const
     a.rowsum = rowsum;
     a.colsum = colsum;
     a.sel_items = reinterpret_cast<int2*>(base + bl.sel_items);
+    a.dq32 = reinterpret_cast<float*>(base + bl.dq32);
     a.sel_order = reinterpret_cast<int*>(base + bl.sel_order);
     a.nqb = s.nqb;
     a.qb_cap = s.qb_cap;

@@ -301,6 +301,24 @@ def test_full_size_tensor_core_path(cuda, oracle, case, kind):
     assert np.sqrt(num_q / den_q) < 2e-2, np.sqrt(num_q / den_q)
 
 
+@pytest.mark.parametrize("cap", ["", "3"])
+def test_fused_dq_backward_opt_in(cuda, cap):
+    """The opt-in fused-dQ backward (SKB_BWD_FUSEDQ=1: dQ^T = K^T dS^T in the
+    key-major passes, fp32 reductions) against the gather path, including
+    capped persistent grids (every cross-item ring and the dQ^T read-back wrap)."""
+    import os
+    import subprocess
+    import sys
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    env = dict(os.environ, SKB_BWD_FUSEDQ="1")
+    if cap:
+        env["SKB_MAX_CTAS"] = cap
+    r = subprocess.run([sys.executable, os.path.join(here, "scripts", "persist_check.py")], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
 @pytest.mark.parametrize("cap", ["2", "7"])
 def test_persistent_grids_many_items_per_cta(cuda, cap):
     """The persistent kernels with their grid capped (SKB_MAX_CTAS): each CTA
