@@ -574,6 +574,7 @@ def run_secondary(torch, ops, dev, args, blk, full_ms):
         out["cfg2"] = secondary_train(torch, ops, dev, CFG2, "recency", args.steps, args.warmup,
                                       "cfg2 B=8 H=12 L=4096 d=64 k=256 w=256, bf16 fwd+bwd")
         out["k1_score"] = k1_timing(torch, ops, dev, args.steps)
+        out["proj_front"] = proj_timing(torch, ops, dev, args.steps)
         proj = {}
         for n in (2, 4, 8):
             from paper_2406_16747_b200.parallel import unit_shard
@@ -637,6 +638,51 @@ def k1_timing(torch, ops, dev, steps):
             "ms": ms, "raw_ms": r_ms, "x_bytes": xb,
             "raw_gbs": (xb / (r_ms / 1e3) / 1e9) if r_ms else None,
             "raw_frac_hbm": (xb / (r_ms / 1e3) / 1e9 / hbm) if r_ms else None}
+
+
+def proj_timing(torch, ops, dev, steps):
+    """forward_chunk's front at cfg3's x shape (B=2, L=16384, D=4096 bf16):
+    q|k|v = x W* plus the score. Fused: the hand-written tcgen05 GEMM with the
+    score from the same x tiles and the Welford streaming under it
+    (skb_proj_score). Library: three cuBLAS GEMMs with K1 on a side stream."""
+    B, L, D = 2, CFG["L"], CFG["H"] * CFG["d"]
+    g = torch.Generator(device=dev)
+    g.manual_seed(12)
+    x = torch.randn((B, L, D), generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16)
+    ws = [(torch.randn((D, D), generator=g, device=dev, dtype=torch.float32) / math.sqrt(D)).to(torch.bfloat16)
+          for _ in range(3)]
+    wsc = torch.randn((D,), generator=g, device=dev, dtype=torch.float64) / math.sqrt(D)
+    sc = ops.ScoringConfig()
+    st = torch.cuda.current_stream()
+    side = torch.cuda.Stream()
+
+    def fused():
+        ops.proj_score(x, *ws, wsc, sc)
+
+    def library():
+        side.wait_stream(st)
+        q, k, v = (x @ w for w in ws)
+        with torch.cuda.stream(side):
+            ops.score_fwd(x, wsc, sc)
+        st.wait_stream(side)
+
+    res = {"workload": "x [2, 16384, 4096] bf16 -> q, k, v + score (raw, u, mean, sdev)"}
+    for name, fn in (("fused", fused), ("library", library)):
+        for _ in range(2):
+            fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(steps):
+            fn()
+        e1.record(st)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        res[f"{name}_ms"] = ms
+        res[f"{name}_tflops"] = 3 * 2.0 * B * L * D * D / (ms / 1e3) / 1e12
+    del x, ws
+    torch.cuda.empty_cache()
+    return res
 
 
 def e2e_timing(torch, ops, blk, steps, world, dev, tokens):

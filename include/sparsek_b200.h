@@ -133,6 +133,15 @@ int skb_score_fwd(int64_t B, int64_t L, int64_t D, int32_t x_dtype, const void* 
  * Enqueued on `stream`, no host synchronisation. */
 int skb_score_raw(int64_t rows, int64_t D, int32_t x_dtype, const void* x, const double* w, double* raw,
                   void* stream);
+/* The fused front of forward_chunk for bf16 (proj/src/cache.cpp:204-228):
+ * q|k|v = x Wq|Wk|Wv (x [B*L, D], W* [D, D], outputs [B*L, D]; D a multiple of
+ * 256) as one hand-written tcgen05 GEMM that also forms raw = x . w_score
+ * (bit-identical to skb_score_raw) from the same x tiles, and the rest of
+ * skb_score_fwd (Welford prefix norm + slope) streaming under it. w_score NULL:
+ * projections only (scores idle, k = 0). Synchronises `stream`. */
+int skb_proj_score(int64_t B, int64_t L, int64_t D, const void* x, const void* wq, const void* wk, const void* wv,
+                   const double* w_score, const skb_scoring* sc, void* q, void* k, void* v, double* raw, double* u,
+                   double* mean, double* sdev, void* stream);
 /* Incremental scoring (score_tokens with base_pos: the TimestepNormState is
  * carried across calls, proj/include/sparsek/selection.hpp:55-56,
  * proj/src/selection.cpp:13-31): x [B, n, D] continues each sequence's

@@ -102,6 +102,8 @@ _SIGS = {
                        _vp, _vp, _vp, _vp, _vp], C.c_int),
     "skb_cache_snapshot": ([_vp, C.c_int64, _vp, _vp, C.POINTER(C.c_size_t), _vp], C.c_int),
     "skb_cache_restore": ([_vp, C.c_int64, _vp, C.c_size_t, _vp, _vp], C.c_int),
+    "skb_proj_score": ([C.c_int64, C.c_int64, C.c_int64] + [_vp] * 5 + [C.POINTER(Scoring)] + [_vp] * 8,
+                       C.c_int),
     "skb_score_raw": ([C.c_int64, C.c_int64, C.c_int32, _vp, _vp, _vp, _vp], C.c_int),
     "skb_score_continue": ([C.c_int64, C.c_int64, C.c_int64, C.c_int32, _vp, _vp, C.POINTER(Scoring),
                             _vp, _vp, _vp, _vp], C.c_int),

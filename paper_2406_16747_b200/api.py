@@ -9,6 +9,7 @@ every computation runs in libsparsek_b200.so or cuBLAS (the D x D projections).
 from __future__ import annotations
 
 import math
+import os
 
 import numpy as np
 import torch
@@ -184,6 +185,7 @@ def _core_cfg(k, window, key_mode, mask_mode):
 
 
 _SIDE = {}
+_FUSED_FRONT = os.environ.get("SKB_FUSED_FRONT", "0") == "1"
 
 
 def _side_stream(device):
@@ -202,6 +204,18 @@ def attention_torch(x, wq, wk, wv, wo, w_score, cfg: ops.AttnConfig, heads: int,
     score, selection, attention and their backward are libsparsek_b200 kernels."""
     B, L, D = x.shape
     p = D // heads
+    if _FUSED_FRONT and ops.proj_supported(x, wq) and (cfg.k == 0.0 or w_score is not None):
+        # opt-in (SKB_FUSED_FRONT=1; bf16, d_model % 256 == 0): the hand-written
+        # CTA-pair tcgen05 projection GEMM with the score formed from the same x
+        # rows and its Welford streaming under it. At cfg3 it measures 3.48 ms
+        # against 3.12 ms for cuBLAS + K1 on a side stream (DESIGN.md section 4),
+        # so the library front stays the default.
+        q, k, v, u = ops.ProjScoreFn.apply(x, wq, wk, wv, w_score if cfg.k > 0.0 else None, scoring)
+        if u is None:
+            u = torch.zeros((B, L), dtype=torch.float64, device=x.device)
+        hc = ops.sparsek_attention_core(q.view(B, L, heads, p), k.view(B, L, heads, p), v.view(B, L, heads, p),
+                                        u, cfg)
+        return hc.reshape(B, L, D) @ wo, hc
     main = torch.cuda.current_stream(x.device)
     side = _side_stream(x.device) if cfg.k > 0.0 else None
     if side is not None:  # K1's serial Welford chain runs under the projection GEMMs

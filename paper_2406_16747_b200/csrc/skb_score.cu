@@ -139,7 +139,7 @@ constexpr int kWfBlock = 256;
 
 __global__ void __launch_bounds__(64) k_score_welford(const double* __restrict__ raw, int L, skb_scoring sc,
                                                       double* __restrict__ mean, double* __restrict__ var,
-                                                      int* __restrict__ bad) {
+                                                      int* __restrict__ bad, const int* ready) {
     __shared__ double s_rin[2][kWfBlock], s_y[2][kWfBlock], s_mu[2][kWfBlock], s_v[2][kWfBlock];
     const int b = blockIdx.x;
     const double* rb = raw + (int64_t)b * L;
@@ -150,6 +150,19 @@ __global__ void __launch_bounds__(64) k_score_welford(const double* __restrict__
     bool nonfinite = false;
     auto prep = [&](int k) {
         const int buf = k & 1;
+        if (ready) {  // streaming: wait until the producer has stored these rows (128-row blocks of B*L)
+            const int64_t r0 = (int64_t)b * L + (int64_t)k * kWfBlock;
+            const int64_t r1 = (int64_t)b * L + min(L, (k + 1) * kWfBlock) - 1;
+            for (int64_t blk = r0 / 128 + lane; blk <= r1 / 128; blk += 32) {
+                int f = 0;
+                while (true) {
+                    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(f) : "l"(ready + blk) : "memory");
+                    if (f) break;
+                    __nanosleep(256);
+                }
+            }
+            __syncwarp();
+        }
 #pragma unroll
         for (int e = 0; e < kWfBlock / 32; ++e) {
             const int j = e * 32 + lane;
@@ -457,7 +470,7 @@ void run_score_fwd(int64_t B, int64_t L, int64_t D, int32_t xdt, const void* x, 
     launch_raw(xdt, x, w, rows, D, u, st);
     SKB_CHECK_LAUNCH();
     if (sc.norm_mode != 0) {
-        k_score_welford<<<(unsigned)B, 64, 0, st>>>(u, (int)L, sc, mean, sdev, bad);
+        k_score_welford<<<(unsigned)B, 64, 0, st>>>(u, (int)L, sc, mean, sdev, bad, nullptr);
         SKB_CHECK_LAUNCH();
     }
     // finish: reads raw from `u`; stage it in raw first
@@ -467,6 +480,24 @@ void run_score_fwd(int64_t B, int64_t L, int64_t D, int32_t xdt, const void* x, 
     SKB_CHECK_LAUNCH();
     SKB_REQUIRE(!read_flag(bad, st), SKB_ENUMERIC, "score: non-finite value");
 }
+
+// Welford + finish on dot products already in `raw_in` (or arriving: `ready`
+// non-null = per-128-row readiness flags set by the fused projection GEMM,
+// skb_proj.cu); launches only, the caller checks *bad after synchronising.
+void run_score_finish_async(int64_t B, int64_t L, const skb_scoring& sc, const double* raw_in, const int* ready,
+                            double* raw, double* u, double* mean, double* sdev, int* bad, cudaStream_t st) {
+    const int64_t rows = B * L;
+    if (sc.norm_mode != 0) {
+        k_score_welford<<<(unsigned)B, 64, 0, st>>>(raw_in, (int)L, sc, mean, sdev, bad, ready);
+        SKB_CHECK_LAUNCH();
+    }
+    if (raw != raw_in)
+        SKB_CHECK_CUDA(cudaMemcpyAsync(raw, raw_in, rows * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    k_score_finish<<<(unsigned)cdiv(rows, 256), 256, 0, st>>>(raw, rows, (int)L, sc, raw, u, mean, sdev, bad);
+    SKB_CHECK_LAUNCH();
+}
+int* score_bad_flag() { return bad_flag(); }
+bool score_read_flag(const int* bad, cudaStream_t st) { return read_flag(bad, st); }
 
 void run_score_raw(int64_t rows, int64_t D, int32_t xdt, const void* x, const double* w, double* raw,
                    cudaStream_t st) {

@@ -416,6 +416,69 @@ def score_tokens(x, w, sc: ScoringConfig):
     return ScoreFn.apply(x, w, sc)
 
 
+def proj_supported(x, w):
+    """The fused projection GEMM (skb_proj_score) covers bf16 with d_model a multiple of 256."""
+    D = x.shape[-1]
+    return (x.dtype == torch.bfloat16 and w.dtype == torch.bfloat16 and D % 256 == 0 and x.is_cuda
+            and w.shape == (D, D))
+
+
+@_on_device
+def proj_score(x, wq, wk, wv, w_score, sc: ScoringConfig):
+    """forward_chunk's front (proj/src/cache.cpp:204-228) in one launch chain:
+    q|k|v = x W* (hand-written tcgen05 GEMM) and, when w_score is given, the
+    score (raw, u, mean, sdev) formed from the same x tiles (raw bit-identical
+    to score_fwd). x [B, L, D] bf16; W* [D, D] bf16. Returns q, k, v [B, L, D]
+    and the four float64 [B, L] score arrays (None without w_score)."""
+    B, L, D = x.shape
+    for w in (wq, wk, wv):
+        if w.shape != (D, D) or w.dtype != torch.bfloat16:
+            raise _lib.ShapeError("forward_chunk: projection shapes must be d_model x d_model")
+    x = x.contiguous()
+    wq, wk, wv = wq.contiguous(), wk.contiguous(), wv.contiguous()
+    q, k, v = (torch.empty((B, L, D), dtype=torch.bfloat16, device=x.device) for _ in range(3))
+    if w_score is not None:
+        wsd = w_score.to(torch.float64).contiguous()
+        raw, u, mean, sdev = (torch.empty((B, L), dtype=torch.float64, device=x.device) for _ in range(4))
+        check(_lib.load().skb_proj_score(B, L, D, x.data_ptr(), wq.data_ptr(), wk.data_ptr(), wv.data_ptr(),
+                                         wsd.data_ptr(), sc.c(), q.data_ptr(), k.data_ptr(), v.data_ptr(),
+                                         raw.data_ptr(), u.data_ptr(), mean.data_ptr(), sdev.data_ptr(),
+                                         _stream()))
+        return q, k, v, raw, u, mean, sdev
+    check(_lib.load().skb_proj_score(B, L, D, x.data_ptr(), wq.data_ptr(), wk.data_ptr(), wv.data_ptr(), None,
+                                     None, q.data_ptr(), k.data_ptr(), v.data_ptr(), None, None, None, None,
+                                     _stream()))
+    return q, k, v, None, None, None, None
+
+
+class ProjScoreFn(torch.autograd.Function):
+    """(x, Wq, Wk, Wv, w_score) -> (q, k, v, u) through the fused GEMM; the
+    backward is the reference's dW = x^T d*, dx = sum d* W*^T (cuBLAS,
+    proj/src/attention.cpp:551-573) plus the score pullback (skb_score_bwd)."""
+
+    @staticmethod
+    def forward(ctx, x, wq, wk, wv, w_score, sc: ScoringConfig):
+        q, k, v, raw, u, mean, sdev = proj_score(x, wq, wk, wv, w_score, sc)
+        ctx.save_for_backward(x, wq, wk, wv, w_score, raw, mean, sdev)
+        ctx.sc = sc
+        return q, k, v, u
+
+    @staticmethod
+    def backward(ctx, gq, gk, gv, gu):
+        x, wq, wk, wv, w_score, raw, mean, sdev = ctx.saved_tensors
+        B, L, D = x.shape
+        x2 = x.reshape(B * L, D)
+        gs = [torch.zeros_like(x) if g is None else g.contiguous() for g in (gq, gk, gv)]
+        dx = gs[0] @ wq.t() + gs[1] @ wk.t() + gs[2] @ wv.t()
+        dws = [x2.t() @ g.reshape(B * L, D) for g in gs]
+        dwsc = None
+        if w_score is not None and gu is not None:
+            graw, dw = score_bwd(x, w_score, ctx.sc, gu.contiguous(), raw, mean, sdev)
+            dx = dx + (graw.unsqueeze(-1) * w_score.to(torch.float64)).to(x.dtype)
+            dwsc = dw.to(w_score.dtype)
+        return dx, dws[0], dws[1], dws[2], dwsc, None
+
+
 # ---------------------------------------------------------------- operator
 
 @_on_device
