@@ -444,6 +444,11 @@ def main():
     from paper_2406_16747_b200.parallel import unit_shard
 
     rank, world, local = dist_env()
+    # SKB_BENCH_ONE_GPU=1 (validation only): every rank on cuda:0 over gloo, to
+    # exercise the N > 1 sharding / du all-reduce / gather code on one GPU
+    one_gpu = os.environ.get("SKB_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     C = CFG
@@ -453,7 +458,10 @@ def main():
     blocks = unit_shard(B, H, world, rank)
     du_group = None
     if world > 1:
-        dist.init_process_group("nccl", init_method="env://", device_id=dev)
+        if one_gpu:
+            dist.init_process_group("gloo", init_method="env://")
+        else:
+            dist.init_process_group("nccl", init_method="env://", device_id=dev)
         # ranks sharing a sequence all-reduce its du partials; every rank builds
         # every group (torch.distributed requires all ranks to call new_group)
         seq_ranks = parallel.seq_ranks(B, H, world)
