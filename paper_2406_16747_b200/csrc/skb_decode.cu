@@ -708,16 +708,22 @@ k_cache_attn(CacheArgs A, const T* __restrict__ q, int H, int p, double scale_d,
 template <int D>
 __global__ void __launch_bounds__(kAttnThreads)
 k_cache_attn_bf16(CacheArgs A, const __nv_bfloat16* __restrict__ q, int H, float scale, float* __restrict__ po,
-                  float* __restrict__ pm, float* __restrict__ pl, int nsplit) {
+                  float* __restrict__ pm, float* __restrict__ pl, int nsplit, int hs, int* __restrict__ done,
+                  __nv_bfloat16* __restrict__ o) {
+    // CTA = (chunk of kSlotsPerCta attended entries, sequence, group of hs
+    // heads): the head groups multiply the CTA count, so the grid runs in
+    // whole-ish waves. The last CTA of a (sequence, head group) to finish
+    // merges the split softmax of every chunk (no separate combine launch).
     constexpr int LPH = D / 8;     // lanes per head row (16 B each)
     constexpr int HPL = 32 / LPH;  // heads per warp load
     constexpr int JMAX = 4;        // head groups per warp (H <= 32 * HPL / 8 * JMAX)
     extern __shared__ float sm[];
-    float* sp = sm;                                          // [H][kSlotsPerCta]
-    int* ss = reinterpret_cast<int*>(sp + H * kSlotsPerCta);  // [kSlotsPerCta]
+    float* sp = sm;                                           // [hs][kSlotsPerCta]
+    int* ss = reinterpret_cast<int*>(sp + hs * kSlotsPerCta);  // [kSlotsPerCta]
     float* svg = reinterpret_cast<float*>(ss + kSlotsPerCta);
     float* skg = svg + kSlotsPerCta;
-    const int b = blockIdx.y, chunk = blockIdx.x;
+    __shared__ int s_last;
+    const int b = blockIdx.y, chunk = blockIdx.x, h0 = blockIdx.z * hs;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = kAttnThreads / 32;
     const int n = A.att_n[b];
     const int e0 = chunk * kSlotsPerCta;
@@ -728,14 +734,14 @@ k_cache_attn_bf16(CacheArgs A, const __nv_bfloat16* __restrict__ q, int H, float
         svg[e] = (float)A.att_vg[bS + e0 + e];
         skg[e] = (float)A.att_kg[bS + e0 + e] * scale;
     }
-    const int nj = H / HPL;
+    const int nj = hs / HPL;
     const int hsub = lane / LPH, dch = (lane % LPH) * 8;
     float qv[JMAX][8];
 #pragma unroll
     for (int jj = 0; jj < JMAX; ++jj) {
         const int j = warp + jj * nw;
         if (j < nj) {
-            const uint4 r = *reinterpret_cast<const uint4*>(q + ((int64_t)b * H + j * HPL + hsub) * D + dch);
+            const uint4 r = *reinterpret_cast<const uint4*>(q + ((int64_t)b * H + h0 + j * HPL + hsub) * D + dch);
             const uint32_t w4[4] = {r.x, r.y, r.z, r.w};
 #pragma unroll
             for (int x = 0; x < 4; ++x) {
@@ -763,7 +769,7 @@ k_cache_attn_bf16(CacheArgs A, const __nv_bfloat16* __restrict__ q, int H, float
     for (int jj = 0; jj < JMAX; ++jj) {
         const int j = warp + jj * nw;
         if (j >= nj) break;
-        const int h = j * HPL + hsub;
+        const int hl = j * HPL + hsub, h = h0 + hl;
         for (int eb = 0; eb < ne; eb += 8) {
             uint4 r[8];
 #pragma unroll
@@ -773,27 +779,28 @@ k_cache_attn_bf16(CacheArgs A, const __nv_bfloat16* __restrict__ q, int H, float
             for (int x = 0; x < 8; ++x) {
                 float d = eb + x < ne ? dot8(r[x], qv[jj]) : 0.f;
 #pragma unroll
-                for (int o = LPH / 2; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
-                if ((lane % LPH) == 0 && eb + x < ne) sp[h * kSlotsPerCta + eb + x] = d * skg[eb + x];
+                for (int o2 = LPH / 2; o2 > 0; o2 >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o2);
+                if ((lane % LPH) == 0 && eb + x < ne) sp[hl * kSlotsPerCta + eb + x] = d * skg[eb + x];
             }
         }
     }
     __syncthreads();
-    for (int h = warp; h < H; h += nw) {
+    for (int hl = warp; hl < hs; hl += nw) {
+        const int h = h0 + hl;
         float m = -INFINITY;
-        for (int e = lane; e < ne; e += 32) m = fmaxf(m, sp[h * kSlotsPerCta + e]);
+        for (int e = lane; e < ne; e += 32) m = fmaxf(m, sp[hl * kSlotsPerCta + e]);
         m = warp_max(m);
         float l = 0.f;
         for (int e = lane; e < ne; e += 32) {
-            const float pe = expf(sp[h * kSlotsPerCta + e] - m);
-            sp[h * kSlotsPerCta + e] = pe * svg[e];  // value-gated weight; l keeps the ungated sum
+            const float pe = expf(sp[hl * kSlotsPerCta + e] - m);
+            sp[hl * kSlotsPerCta + e] = pe * svg[e];  // value-gated weight; l keeps the ungated sum
             l += pe;
         }
         l = warp_sum(l);
         if (lane == 0) {
-            const int64_t o = ((int64_t)b * nsplit + chunk) * H + h;
-            pm[o] = ne > 0 ? m : -INFINITY;
-            pl[o] = l;
+            const int64_t oi = ((int64_t)b * nsplit + chunk) * H + h;
+            pm[oi] = ne > 0 ? m : -INFINITY;
+            pl[oi] = l;
         }
     }
     __syncthreads();
@@ -801,7 +808,7 @@ k_cache_attn_bf16(CacheArgs A, const __nv_bfloat16* __restrict__ q, int H, float
     for (int jj = 0; jj < JMAX; ++jj) {
         const int j = warp + jj * nw;
         if (j >= nj) break;
-        const int h = j * HPL + hsub;
+        const int hl = j * HPL + hsub, h = h0 + hl;
         float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         for (int eb = 0; eb < ne; eb += 8) {
             uint4 r[8];
@@ -811,7 +818,7 @@ k_cache_attn_bf16(CacheArgs A, const __nv_bfloat16* __restrict__ q, int H, float
 #pragma unroll
             for (int x = 0; x < 8; ++x) {
                 if (eb + x >= ne) break;
-                const float w = sp[h * kSlotsPerCta + eb + x];
+                const float w = sp[hl * kSlotsPerCta + eb + x];
                 const uint32_t w4[4] = {r[x].x, r[x].y, r[x].z, r[x].w};
 #pragma unroll
                 for (int y = 0; y < 4; ++y) {
@@ -824,6 +831,48 @@ k_cache_attn_bf16(CacheArgs A, const __nv_bfloat16* __restrict__ q, int H, float
         float* out = po + (((int64_t)b * nsplit + chunk) * H + h) * D + dch;
         *reinterpret_cast<float4*>(out) = make_float4(acc[0], acc[1], acc[2], acc[3]);
         *reinterpret_cast<float4*>(out + 4) = make_float4(acc[4], acc[5], acc[6], acc[7]);
+    }
+    if (o == nullptr) return;  // the separate combine kernel merges the chunks
+    // the last chunk CTA of (b, head group) merges every chunk's partials
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int* cnt = done + (int64_t)b * gridDim.z + blockIdx.z;
+        const int t = atomicAdd(cnt, 1);
+        s_last = t == (int)gridDim.x - 1;
+        if (s_last) *cnt = 0;  // every chunk of this step has arrived: rearm for the next step
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    const int used = min(nsplit, (n + kSlotsPerCta - 1) / kSlotsPerCta);
+    float* sM = sp;            // [hs] reuse the logit tile
+    float* sL = sp + hs;       // [hs]
+    for (int hl = warp; hl < hs; hl += nw) {
+        const int h = h0 + hl;
+        float M = -INFINITY;
+        for (int sidx = lane; sidx < used; sidx += 32) M = fmaxf(M, __ldcg(pm + ((int64_t)b * nsplit + sidx) * H + h));
+        M = warp_max(M);
+        float Ls = 0.f;
+        for (int sidx = lane; sidx < used; sidx += 32) {
+            const int64_t i = ((int64_t)b * nsplit + sidx) * H + h;
+            const float mi = __ldcg(pm + i);
+            if (mi > -INFINITY) Ls += __ldcg(pl + i) * __expf(mi - M);
+        }
+        Ls = warp_sum(Ls);
+        if (lane == 0) sM[hl] = M, sL[hl] = Ls;
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < hs * D; idx += kAttnThreads) {
+        const int hl = idx / D, c = idx % D, h = h0 + hl;
+        const float M = sM[hl], inv = sL[hl] > 0.f ? 1.f / sL[hl] : 0.f;
+        float acc = 0.f;
+        for (int sidx = 0; sidx < used; ++sidx) {
+            const int64_t i = ((int64_t)b * nsplit + sidx) * H + h;
+            const float mi = __ldcg(pm + i);
+            if (mi > -INFINITY) acc += __ldcg(po + i * D + c) * __expf(mi - M);
+        }
+        o[((int64_t)b * H + h) * D + c] = __float2bfloat16(acc * inv);
     }
 }
 
@@ -890,6 +939,7 @@ struct skb_cache {
     int nsplit = 0;
     int vec = 1;
     double* po = nullptr;  // split partials: float64 for float64 pools, else float32
+    int* done = nullptr;   // [B, head groups] chunk CTAs finished this step (bf16 fast path; self-rearming)
     double* pm = nullptr;
     double* pl = nullptr;
     double* zeros = nullptr;  // [B] idle scores for k = 0 (on the cache's device)
@@ -1303,6 +1353,8 @@ int skb_cache_create(const skb_attn_desc* d, skb_cache** out) {
         c->po = c->alloc<double>(B * c->nsplit * H * p);  // sized for float64 partials
         c->pm = c->alloc<double>(B * c->nsplit * H);
         c->pl = c->alloc<double>(B * c->nsplit * H);
+        c->done = c->alloc<int>(B * H);  // >= one counter per (sequence, head group)
+        SKB_CHECK_CUDA(cudaMemset(c->done, 0, (size_t)B * H * sizeof(int)));
         c->vec = (p % 128 == 0) ? 4 : (p % 64 == 0) ? 2 : 1;
         c->zeros = c->alloc<double>(B);
         SKB_CHECK_CUDA(cudaMemset(c->zeros, 0, B * sizeof(double)));
@@ -1343,16 +1395,29 @@ static void cache_attend(skb_cache* c, const void* q, void* o, cudaStream_t st) 
     constexpr bool kBf16 = std::is_same<T, __nv_bfloat16>::value;
     const bool fast = kBf16 && (p == 128 || p == 64) && (H % (256 / p)) == 0 && H / (256 / p) <= 4 * 8;
     if (fast) {
-        const size_t fsmem = (size_t)H * kSlotsPerCta * 4 + kSlotsPerCta * 12;
+        // head groups of 16 (or 8 at head_dim 64): 2-4x the CTAs of one group per
+        // (chunk, sequence), so the grid runs in several waves instead of 1.35
+        const int hpl = 256 / p;  // heads per warp load
+        static const int hs_env = getenv("SKB_DEC_HS") ? atoi(getenv("SKB_DEC_HS")) : 0;
+        static const int fuse = getenv("SKB_DEC_FUSE") ? atoi(getenv("SKB_DEC_FUSE")) : 0;
+        int hs = std::min(H, hs_env > 0 ? hs_env : H);
+        hs = std::max(hpl, hs - hs % hpl);
+        while (H % hs) hs -= hpl;  // a divisor of H, a multiple of hpl (H % hpl == 0 on this path)
+        const size_t fsmem = (size_t)hs * kSlotsPerCta * 4 + kSlotsPerCta * 12;
+        const dim3 gh((unsigned)c->nsplit, (unsigned)d.batch, (unsigned)(H / hs));
         auto run = [&](auto kern) {
             if (fsmem > 48 * 1024)
                 SKB_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem));
-            kern<<<g, kAttnThreads, fsmem, st>>>(c->A, reinterpret_cast<const __nv_bfloat16*>(q), H, scale,
-                                                 reinterpret_cast<float*>(c->po), reinterpret_cast<float*>(c->pm),
-                                                 reinterpret_cast<float*>(c->pl), c->nsplit);
+            kern<<<gh, kAttnThreads, fsmem, st>>>(c->A, reinterpret_cast<const __nv_bfloat16*>(q), H, scale,
+                                                  reinterpret_cast<float*>(c->po), reinterpret_cast<float*>(c->pm),
+                                                  reinterpret_cast<float*>(c->pl), c->nsplit, hs, c->done,
+                                                  fuse ? static_cast<__nv_bfloat16*>(o) : nullptr);
         };
+        SKB_REQUIRE(H % hs == 0, SKB_ECONFIG, "cache: heads must be a multiple of the decode head group");
         if (p == 128) run(k_cache_attn_bf16<128>);
         else run(k_cache_attn_bf16<64>);
+        SKB_CHECK_LAUNCH();
+        if (fuse) return;  // the last chunk CTA of each (sequence, head group) wrote o
     } else if (c->vec == 4) launch(k_cache_attn<T, 4>);
     else if (c->vec == 2) launch(k_cache_attn<T, 2>);
     else launch(k_cache_attn<T, 1>);
