@@ -32,10 +32,8 @@ class SparseKvCache {
                   std::size_t max_positions = std::size_t(1) << 20)
         : cfg_(cfg), d_model_(d_model), scoring_(scoring), max_pos_(max_positions) {
         cfg.validate(d_model, scoring);
-        // the linear mix's recurrent prefix state (lin_m_/lin_b_) has no decode
-        // kernel here: linear_mix_attention / chunked_forward run it batched
-        if (cfg.linear_mix) throw ConfigError("linear mix: incremental decoding is not supported on this backend");
-        const skb_x_desc d = detail::x_desc<T>(max_positions, d_model, cfg, scoring);
+        skb_x_desc d = detail::x_desc<T>(max_positions, d_model, cfg, scoring);
+        if (cfg.linear_mix) d.flags |= SKB_FLAG_LINEAR_MIX;  // the cache carries phi(k) and the prefix state
         skb_xcache* c = nullptr;
         detail::check(skb_xcache_create(&d, &c));
         h_.reset(c, skb_xcache_destroy);
@@ -49,7 +47,7 @@ class SparseKvCache {
 
     MatT<T> forward_chunk(const MatT<T>& x_chunk, const AttnParams<T>& params, AttnTape<T>* tape = nullptr,
                           const LinearMixParams<T>* lin = nullptr) {
-        if (lin) throw ConfigError("linear mix: incremental decoding is not supported on this backend");
+        if (cfg_.linear_mix && !lin) throw ConfigError("forward_chunk: linear mix needs feature parameters");
         if (x_chunk.cols != d_model_) throw ShapeError("forward_chunk: x.cols != d_model");
         detail::check_params(params, d_model_);
         const std::size_t n = x_chunk.rows;
@@ -60,13 +58,22 @@ class SparseKvCache {
             // sparsek_attention's; later chunks go through chunked_forward
             if (positions_seen() != 0)
                 throw ArgumentError("forward_chunk: a tape needs a fresh cache on this backend (use chunked_forward)");
-            detail::run_forward(x_chunk, params, scoring_, cfg_, tape, 0);
+            detail::run_forward(x_chunk, params, scoring_, cfg_, tape, 0, cfg_.linear_mix ? lin : nullptr);
         }
         detail::DeviceParams<T> dp(params, scoring_);
         detail::Buf dx(x_chunk.data), dy(y.data.size() * sizeof(T));
-        detail::check(skb_xcache_forward_chunk(h_.get(), dx.get(), (int64_t)n, dp.wq.get(), dp.wk.get(), dp.wv.get(),
-                                               dp.wo.get(), cfg_.k > 0.0 ? dp.ws.template as<double>() : nullptr,
-                                               dy.get(), nullptr));
+        if (cfg_.linear_mix) {  // Appendix B.1: the mixture readout with the carried prefix state
+            detail::Buf df(detail::pack_feat(*lin, cfg_.heads, d_model_ / cfg_.heads));
+            detail::check(skb_xcache_forward_chunk_lin(h_.get(), dx.get(), (int64_t)n, dp.wq.get(), dp.wk.get(),
+                                                       dp.wv.get(), dp.wo.get(),
+                                                       cfg_.k > 0.0 ? dp.ws.template as<double>() : nullptr,
+                                                       df.template as<double>(), dy.get(), nullptr));
+        } else {
+            detail::check(skb_xcache_forward_chunk(h_.get(), dx.get(), (int64_t)n, dp.wq.get(), dp.wk.get(),
+                                                   dp.wv.get(), dp.wo.get(),
+                                                   cfg_.k > 0.0 ? dp.ws.template as<double>() : nullptr, dy.get(),
+                                                   nullptr));
+        }
         y.data = dy.to_host<T>(y.data.size());
         return y;
     }

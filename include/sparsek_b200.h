@@ -192,6 +192,11 @@ int skb_linmix_bwd(const skb_attn_desc* d, const void* q, const void* k, const v
                    const void* sel_ws, const double* feat, const double* den, const void* dout, void* dq,
                    void* dk, void* dv, double* du, double* dfeat, void* ws, void* stream);
 
+/* phi(z) = elu(F_h z) + 1 per row of z [rows, H, p] (float32/float64), feat
+ * float64 [H, p, p] -> out float64 [rows, H, p]. */
+int skb_linmix_phi(int64_t rows, int64_t heads, int64_t head_dim, int32_t dtype, const void* z, const double* feat,
+                   double* out, void* stream);
+
 /* ---- SparseK operator (batched rows) ------------------------------------ */
 /* z: float64 [n, m]; p: [n, m]; tau: [n] (-inf when infeasible); counts [n];
  * flags[n]: bit0 degenerate, bit1 infeasible. */
@@ -216,6 +221,17 @@ int skb_cache_destroy(skb_cache* c);
  * (the new tokens' frozen scores) -> o [B, H, p]. */
 int skb_cache_step(skb_cache* c, const void* q, const void* k, const void* v, const double* u,
                    void* o, void* stream);
+/* Linear-attention mix decode (a cache created with SKB_FLAG_LINEAR_MIX,
+ * float32/float64; SparseKvCache::forward_chunk with LinearMixParams,
+ * proj/src/cache.cpp:262-278,322-356): skb_cache_linmix_prefill after
+ * skb_cache_prefill(k, v, u, n) records phi(k) of the retained rows and adds
+ * the n positions to the prefix state M = sum phi(k) v^T, b = sum phi(k);
+ * skb_cache_linmix_step = one position (stream push, eviction, state update)
+ * and the mixture readout o [B, H, p]. phq/phk: float64 phi rows
+ * (skb_linmix_phi). A nonpositive denominator is SKB_ENUMERIC. */
+int skb_cache_linmix_prefill(skb_cache* cache, const void* v, const double* phk, int64_t n, void* stream);
+int skb_cache_linmix_step(skb_cache* cache, const void* q, const void* k, const void* v, const double* u,
+                          const double* phq, const double* phk, void* o, void* stream);
 /* Append n positions per sequence without attending (a prompt prefill):
  * k/v [B, n, H, p] (dtype), u float64 [B, n]. The selection state advances
  * exactly as n decode steps would (forward_chunk pass 1,
@@ -367,6 +383,11 @@ int skb_xcache_destroy(skb_xcache* c);
 /* forward_chunk: x [B, n, D] -> y [B, n, D]; generate_step is n = 1. */
 int skb_xcache_forward_chunk(skb_xcache* c, const void* x, int64_t n, const void* wq, const void* wk,
                              const void* wv, const void* wo, const double* w_score, void* y, void* stream);
+/* The same with LinearMixParams (a cache created with SKB_FLAG_LINEAR_MIX;
+ * feat float64 [H, p, p]). */
+int skb_xcache_forward_chunk_lin(skb_xcache* c, const void* x, int64_t n, const void* wq, const void* wk,
+                                 const void* wv, const void* wo, const double* w_score, const double* feat, void* y,
+                                 void* stream);
 /* The underlying q/k/v-level cache (skb_cache_state / snapshot / restore). */
 skb_cache* skb_xcache_inner(skb_xcache* c);
 /* TimestepNormState {count, mean, m2} per sequence (host [B, 3]): get (set = 0) or set. */

@@ -492,6 +492,18 @@ class Reference:
                                                             "dfeat"))))
         return y, (out if g is not None else None)
 
+    def linear_mix_decode(self, x, wq, wk, wv, wo, w_score, feat, cfg, prompt, use_float=False):
+        """SparseKvCache with LinearMixParams: forward_chunk(prompt), then generate_step per row."""
+        x, wq, wk, wv, wo = (np.ascontiguousarray(a, np.float64) for a in (x, wq, wk, wv, wo))
+        L, D = x.shape
+        ws = np.ascontiguousarray(w_score if w_score is not None else np.zeros(D), np.float64)
+        f = np.ascontiguousarray(feat, np.float64)
+        y = np.zeros((L, D))
+        self._rc(self.lib.ref_linmix_decode(C.c_int32(int(use_float)), C.c_uint64(L), C.c_uint64(D),
+                                            C.c_uint64(prompt), _d(x), _d(wq), _d(wk), _d(wv), _d(wo), _d(ws),
+                                            _d(f), C.byref(cfg), _d(y)))
+        return y
+
     def bench_decode(self, units, threads, prompt, steps, p, k, window, seed=1):
         """Seconds for `steps` generate_step calls on each of `units` single-head
         caches prefilled with `prompt` rows (ref_bench_decode)."""

@@ -566,6 +566,34 @@ int ref_linmix(int32_t use_float, uint64_t L, uint64_t D, const double* x, const
     REF_GUARD_END
 }
 
+// Linear-mix decoding: forward_chunk(prompt) then generate_step per row, with
+// LinearMixParams (feat: heads x p x p).
+int ref_linmix_decode(int32_t use_float, uint64_t L, uint64_t D, uint64_t prompt, const double* x, const double* wq,
+                      const double* wk, const double* wv, const double* wo, const double* w_score, const double* feat,
+                      const ref_cfg* c, double* y) {
+    REF_GUARD_BEGIN
+    auto run = [&](auto tag) {
+        using T = decltype(tag);
+        const uint64_t H = c->heads, p = D / H;
+        AttnParams<T> params{mat_in<T>(wq, D, D), mat_in<T>(wk, D, D), mat_in<T>(wv, D, D), mat_in<T>(wo, D, D)};
+        LinearMixParams<T> lin;
+        for (uint64_t h = 0; h < H; ++h) lin.feat.push_back(mat_in<T>(feat + h * p * p, p, p));
+        AttnConfig cfg = to_cfg(c);
+        cfg.linear_mix = true;
+        SparseKvCache<T> cache(cfg, D, to_scoring(c, w_score, D));
+        if (prompt > 0) mat_out(cache.forward_chunk(mat_in<T>(x, prompt, D), params, nullptr, &lin), y);
+        for (uint64_t i = prompt; i < L; ++i) {
+            std::vector<T> row(D);
+            for (size_t cc = 0; cc < D; ++cc) row[cc] = static_cast<T>(x[i * D + cc]);
+            std::vector<T> o = generate_step(cache, row, params, &lin);
+            for (size_t cc = 0; cc < D; ++cc) y[i * D + cc] = static_cast<double>(o[cc]);
+        }
+    };
+    if (use_float) run(float{});
+    else run(double{});
+    REF_GUARD_END
+}
+
 // CPU baseline: `units` independent single-head sequences (heads=1, D=p) of
 // length L, fwd (with tape) + bwd in float, one std::thread per unit with at
 // most `threads` in flight, the way the reference trainer fans out batch

@@ -114,6 +114,9 @@ _SIGS = {
     "skb_attn_fwd": ([C.POINTER(AttnDesc), _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp], C.c_int),
     "skb_attn_bwd_workspace_size": ([C.POINTER(AttnDesc), C.POINTER(C.c_size_t)], C.c_int),
     "skb_attn_bwd": ([C.POINTER(AttnDesc)] + [_vp] * 14, C.c_int),
+    "skb_linmix_phi": ([C.c_int64, C.c_int64, C.c_int64, C.c_int32, _vp, _vp, _vp, _vp], C.c_int),
+    "skb_cache_linmix_prefill": ([_vp, _vp, _vp, C.c_int64, _vp], C.c_int),
+    "skb_cache_linmix_step": ([_vp] * 9, C.c_int),
     "skb_linmix_workspace_size": ([C.POINTER(AttnDesc), C.POINTER(C.c_size_t)], C.c_int),
     "skb_linmix_fwd": ([C.POINTER(AttnDesc)] + [_vp] * 10, C.c_int),
     "skb_linmix_bwd": ([C.POINTER(AttnDesc)] + [_vp] * 15, C.c_int),
@@ -141,6 +144,7 @@ _SIGS = {
     "skb_xcache_create": ([C.POINTER(XDesc), C.POINTER(_vp)], C.c_int),
     "skb_xcache_destroy": ([_vp], C.c_int),
     "skb_xcache_forward_chunk": ([_vp, _vp, C.c_int64] + [_vp] * 7, C.c_int),
+    "skb_xcache_forward_chunk_lin": ([_vp, _vp, C.c_int64] + [_vp] * 8, C.c_int),
     "skb_xcache_inner": ([_vp], _vp),
     "skb_xcache_norm_state": ([_vp, _vp, C.c_int32, _vp], C.c_int),
     "skb_cache_ledger": ([_vp, C.c_int64, C.c_int32, _vp, C.c_int64, _vp, _vp, C.c_int64, _vp, C.c_int64, _vp],

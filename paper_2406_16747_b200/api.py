@@ -414,8 +414,18 @@ class DecodeSession:
     [D, D], w_score [D]."""
 
     def __init__(self, wq, wk, wv, wo, w_score, cfg: ops.AttnConfig, heads: int, batch: int,
-                 max_len: int, scoring: ops.ScoringConfig = ops.ScoringConfig(), dtype=None):
+                 max_len: int, scoring: ops.ScoringConfig = ops.ScoringConfig(), dtype=None, feat=None):
+        """feat [H, p, p] (LinearMixParams): the linear-attention mix (Appendix B.1),
+        float32/float64 sessions; its prefix state is carried by the cache."""
         self.wq, self.wk, self.wv, self.wo = wq, wk, wv, wo
+        self.feat = feat
+        if feat is not None:
+            import dataclasses
+
+            cfg = cfg if cfg.linear_mix else dataclasses.replace(cfg, linear_mix=True)
+            if scoring.norm_mode != "timestep_norm":
+                raise ConfigError("linear mix requires timestep normalization; raw scores make the linear "
+                                  "branch blow up")
         D = wq.shape[0]
         if D % heads:
             raise ConfigError("attention: d_model must be a positive multiple of heads")
@@ -454,8 +464,12 @@ class DecodeSession:
         q, k, v, u = self._proj_score(x)
         outs = []
         for r in range(n):
-            outs.append(self.cache.step(q[:, r].contiguous(), k[:, r].contiguous(), v[:, r].contiguous(),
-                                        u[:, r].contiguous()))
+            qr, kr, vr, ur = (t[:, r].contiguous() for t in (q, k, v, u))
+            if self.feat is not None:
+                outs.append(self.cache.linmix_step(qr, kr, vr, ur, ops.linmix_phi(qr, self.feat),
+                                                   ops.linmix_phi(kr, self.feat)))
+            else:
+                outs.append(self.cache.step(qr, kr, vr, ur))
             self.t += 1
         return torch.stack(outs, 1).reshape(B, n, D) @ self.wo
 
@@ -468,9 +482,14 @@ class DecodeSession:
             return self.forward_chunk(x)
         B, n, D = x.shape
         q, k, v, u = self._proj_score(x)
-        hc = ops.sparsek_attention_core(q.contiguous(), k.contiguous(), v.contiguous(),
-                                        u.contiguous(), self.cfg)
-        self.cache.prefill(k.contiguous(), v.contiguous(), u.contiguous())
+        q, k, v, u = q.contiguous(), k.contiguous(), v.contiguous(), u.contiguous()
+        if self.feat is not None:  # the mixture readout over the prompt (batch kernels)
+            hc, _, _ = ops.linmix_fwd(q, k, v, u, self.feat, self.cfg)
+        else:
+            hc = ops.sparsek_attention_core(q, k, v, u, self.cfg)
+        self.cache.prefill(k, v, u)
+        if self.feat is not None:
+            self.cache.linmix_prefill(v, ops.linmix_phi(k, self.feat))
         self.t = n
         return hc.reshape(B, n, D) @ self.wo
 
@@ -489,11 +508,7 @@ class DecodeSession:
     @torch.no_grad()
     def step(self, x_row):
         """generate_step: x_row [B, D] -> y [B, D]."""
-        q, k, v, u = self._proj_score(x_row.view(self.B, 1, self.D))
-        o = self.cache.step(q[:, 0].contiguous(), k[:, 0].contiguous(), v[:, 0].contiguous(),
-                            u[:, 0].contiguous())
-        self.t += 1
-        return o.reshape(self.B, self.D) @ self.wo
+        return self.forward_chunk(x_row.view(self.B, 1, self.D)).reshape(self.B, self.D)
 
 
 def save_cache_snapshot(path, payload):

@@ -54,10 +54,14 @@ using namespace tc;
 
 constexpr float kLn2 = 0.6931471805599453f;
 constexpr float kRescaleSlack = 8.0f;  // lazy rescale threshold (log2 units)
+#ifndef SKB_POLY_MASK
+#define SKB_POLY_MASK 0
+#endif
 #ifndef SKB_POLY_PAIR
 #define SKB_POLY_PAIR -1
 #endif
 constexpr int kPolyPair = SKB_POLY_PAIR;  // which key pair of every 8 uses the polynomial exp2 (-1: none)
+constexpr int kPolyMask = SKB_POLY_MASK;  // bit e/2: key pair e of every 8 uses the polynomial exp2
 
 struct FwdArgs {
     CUtensorMap tm_q;   // 3-D row tiles (box 64 x 128)
@@ -383,7 +387,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(const __grid_constant__ 
                 for (int e = 0; e < 8; e += 2) {
                     float2 x = __ffma2_rn(make_float2(sv[c + e], sv[c + e + 1]), sl22, nmb2);
                     if (SKB_EXP == 6) {  // experiment: no exponentials at all
-                    } else if (e == kPolyPair) {  // 1 pair in 4 on the FMA pipe, the rest on MUFU
+                    } else if (e == kPolyPair || ((kPolyMask >> (e >> 1)) & 1)) {  // pairs on the FMA pipe, the rest on MUFU
                         x = ex2_poly2(x);
                     } else {
                         x.x = ex2(x.x);  // masked: exp2(-inf) = 0
@@ -778,7 +782,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_p(const __grid_constant__ F
                 for (int e = 0; e < 8; e += 2) {
                     float2 x = __ffma2_rn(make_float2(sv[c + e], sv[c + e + 1]), sl22, nmb2);
                     if (SKB_EXP == 6) {  // experiment: no exponentials at all
-                    } else if (e == kPolyPair) {  // 1 pair in 4 on the FMA pipe, the rest on MUFU
+                    } else if (e == kPolyPair || ((kPolyMask >> (e >> 1)) & 1)) {  // pairs on the FMA pipe, the rest on MUFU
                         x = ex2_poly2(x);
                     } else {
                         x.x = ex2(x.x);  // masked: exp2(-inf) = 0

@@ -359,6 +359,7 @@ struct CacheArgs {
     uint8_t* kpool;     // [B, S, H, p] dtype
     uint8_t* vpool;
     int Lmax, S, cap, w, key_soft, mask_st;
+    int lin;            // linear mix (Appendix B.1): no self entry when w = 0 (the linear branch covers it)
     int64_t row_bytes;  // H * p * esize
 };
 
@@ -452,7 +453,7 @@ __device__ void warp_cache_advance(const CacheArgs& A, int b, CacheCtl& c, doubl
             }
             n += pos - r0 + 1;
         }
-        if (A.w == 0) {
+        if (A.w == 0 && !A.lin) {
             // nothing window-resident: the query reads itself unless selected
             bool selected = false;
             for (int r = lane; r < ns; r += 32) selected |= sa.si[r] == pos;
@@ -903,6 +904,124 @@ __global__ void k_cache_combine(const void* po_, const void* pm_, const void* pl
     }
 }
 
+// ------------------------------------------------------------------ linear mix
+// Linear-attention mix decode (Appendix B.1; forward_chunk with linear_mix,
+// proj/src/cache.cpp:262-278,322-356): the cache keeps phi(k) of every slot
+// row and the prefix state M = sum_j phi(k_j) v_j^T, b = sum_j phi(k_j) over
+// every position seen (not only the retained ones).
+
+// M += phi(k_j) v_j^T and b += phi(k_j) over positions [0, n) of a chunk
+// (phk float64 [B, n, H, p], v [B, n, H, p]); one CTA per (sequence, head).
+template <class S>
+__global__ void k_lin_state_add(const double* __restrict__ phk, const S* __restrict__ v, int n, int H, int p,
+                                double* __restrict__ M, double* __restrict__ bv) {
+    const int b = blockIdx.y, h = blockIdx.x;
+    double* Mh = M + ((int64_t)b * H + h) * p * p;
+    for (int e = threadIdx.x; e < p * p; e += blockDim.x) {
+        const int r = e / p, c = e % p;
+        double acc = 0.0;
+        for (int j = 0; j < n; ++j) {
+            const int64_t row = (((int64_t)b * n + j) * H + h) * p;
+            acc += phk[row + r] * (double)v[row + c];
+        }
+        Mh[e] += acc;
+    }
+    for (int r = threadIdx.x; r < p; r += blockDim.x) {
+        double acc = 0.0;
+        for (int j = 0; j < n; ++j) acc += phk[(((int64_t)b * n + j) * H + h) * p + r];
+        bv[((int64_t)b * H + h) * p + r] += acc;
+    }
+}
+
+// phi(k) rows of the positions [t - n, t) that hold a slot -> the phi pool
+__global__ void k_lin_fill_phi(CacheArgs A, const double* __restrict__ phk, int n, int H, int p,
+                               double* __restrict__ pool) {
+    const int b = blockIdx.y, slot = blockIdx.x;
+    const int t = A.ctl[b].t;
+    const int pos = A.pos_of[(int64_t)b * A.S + slot];
+    if (pos < t - n || pos >= t) return;
+    const double* src = phk + ((int64_t)b * n + (pos - (t - n))) * H * p;
+    double* dst = pool + ((int64_t)b * A.S + slot) * H * p;
+    for (int e = threadIdx.x; e < H * p; e += blockDim.x) dst[e] = src[e];
+}
+
+// o_i = [sum_att m (e - lambda) v + phi(q)^T M] / [sum_att m (e - lambda) + phi(q).b]; warp per (sequence, head)
+template <class S>
+__global__ void __launch_bounds__(128) k_lin_decode(CacheArgs A, const S* __restrict__ q, const double* __restrict__ phq,
+                                                    const double* __restrict__ pool, const double* __restrict__ M,
+                                                    const double* __restrict__ bv, int B, int H, int p, double scale,
+                                                    S* __restrict__ o, int* __restrict__ bad) {
+    constexpr int kPer = 8;  // head_dim <= 256
+    __shared__ double s_pq[4][32 * kPer];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t wid = (int64_t)blockIdx.x * 4 + warp;
+    if (wid >= (int64_t)B * H) return;
+    const int b = (int)(wid / H), h = (int)(wid % H);
+    const int np = (p + 31) / 32;
+    double qv[kPer], pq[kPer], num[kPer];
+#pragma unroll
+    for (int m = 0; m < kPer; ++m) {
+        const int c = lane + 32 * m;
+        const bool ok = m < np && c < p;
+        qv[m] = ok ? (double)q[((int64_t)b * H + h) * p + c] : 0.0;
+        pq[m] = ok ? phq[((int64_t)b * H + h) * p + c] : 0.0;
+        if (ok) s_pq[warp][c] = pq[m];
+        num[m] = 0.0;
+    }
+    __syncwarp();
+    double den = 0.0;
+    const int n = A.att_n[b];
+    const int64_t bS = (int64_t)b * A.S;
+    const S* kp = reinterpret_cast<const S*>(A.kpool);
+    const S* vp = reinterpret_cast<const S*>(A.vpool);
+    for (int e = 0; e < n; ++e) {
+        const int slot = A.att_slot[bS + e];
+        const double m = A.att_vg[bS + e];  // the gate (selected) or 1 (window)
+        const int64_t ro = ((bS + slot) * H + h) * p;
+        double dot = 0.0, lam = 0.0;
+#pragma unroll
+        for (int x = 0; x < kPer; ++x) {
+            const int c = lane + 32 * x;
+            if (x < np && c < p) {
+                dot += qv[x] * (double)kp[ro + c];
+                lam += pq[x] * pool[ro + c];
+            }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            dot += __shfl_xor_sync(0xffffffffu, dot, off);
+            lam += __shfl_xor_sync(0xffffffffu, lam, off);
+        }
+        const double wexact = m * exp(scale * dot), wlin = m * lam;
+#pragma unroll
+        for (int x = 0; x < kPer; ++x) {
+            const int c = lane + 32 * x;
+            if (x < np && c < p) num[x] += (wexact - wlin) * (double)vp[ro + c];
+        }
+        den += wexact - wlin;
+    }
+    // + phi(q)^T M and phi(q) . b (the prefix accumulators)
+    const double* Mh = M + ((int64_t)b * H + h) * p * p;
+    const double* bh = bv + ((int64_t)b * H + h) * p;
+    double pb = 0.0;
+    for (int r = 0; r < p; ++r) {
+        const double pr = s_pq[warp][r];
+#pragma unroll
+        for (int x = 0; x < kPer; ++x) {
+            const int c = lane + 32 * x;
+            if (x < np && c < p) num[x] += pr * Mh[(int64_t)r * p + c];
+        }
+        pb += pr * bh[r];
+    }
+    den += pb;
+    if (!(den > 0.0) && lane == 0) *bad = 1;  // proj/src/cache.cpp:349-350
+#pragma unroll
+    for (int x = 0; x < kPer; ++x) {
+        const int c = lane + 32 * x;
+        if (x < np && c < p) o[((int64_t)b * H + h) * p + c] = (S)(num[x] / den);
+    }
+}
+
 }  // namespace
 }  // namespace skb
 
@@ -943,6 +1062,14 @@ struct skb_cache {
     double* pm = nullptr;
     double* pl = nullptr;
     double* zeros = nullptr;  // [B] idle scores for k = 0 (on the cache's device)
+    // linear mix: phi(k) of every slot row [B, S, H, p], the prefix state
+    // M = sum phi(k_j) v_j^T [B, H, p, p] and b = sum phi(k_j) [B, H, p] (float64)
+    double *lphk = nullptr, *lm = nullptr, *lb = nullptr;
+    int* flag = nullptr;  // device word for kernel-side errors (linear mix)
+    int* zeros_flag() {
+        if (!flag) flag = alloc<int>(1);
+        return flag;
+    }
     std::vector<void*> allocs;
     ~skb_cache() {
         for (void* p : allocs) cudaFree(p);
@@ -1327,8 +1454,10 @@ int skb_cache_create(const skb_attn_desc* d, skb_cache** out) {
         A.S = (int)S;
         A.cap = cap;
         A.w = (int)d->window;
-        A.key_soft = d->key_mode;
-        A.mask_st = d->mask_mode;
+        A.lin = (d->flags & SKB_FLAG_LINEAR_MIX) ? 1 : 0;
+        // the mixture weight of a selected key is its gate whatever the key/mask modes (cache.cpp:330)
+        A.key_soft = A.lin ? 0 : d->key_mode;
+        A.mask_st = A.lin ? 0 : d->mask_mode;
         A.row_bytes = H * p * (int64_t)esize_of(d->dtype);
         A.ctl = c->alloc<CacheCtl>(B);
         A.sv = c->alloc<double>(B * Lmax);
@@ -1358,6 +1487,15 @@ int skb_cache_create(const skb_attn_desc* d, skb_cache** out) {
         c->vec = (p % 128 == 0) ? 4 : (p % 64 == 0) ? 2 : 1;
         c->zeros = c->alloc<double>(B);
         SKB_CHECK_CUDA(cudaMemset(c->zeros, 0, B * sizeof(double)));
+        if (A.lin) {
+            SKB_REQUIRE(d->dtype == SKB_F32 || d->dtype == SKB_F64, SKB_EARG,
+                        "linear mix: dtype must be float32 or float64 (the reference's instantiations)");
+            c->lphk = c->alloc<double>(B * S * H * p);
+            c->lm = c->alloc<double>(B * H * p * p);
+            c->lb = c->alloc<double>(B * H * p);
+            SKB_CHECK_CUDA(cudaMemset(c->lm, 0, (size_t)B * H * p * p * 8));
+            SKB_CHECK_CUDA(cudaMemset(c->lb, 0, (size_t)B * H * p * 8));
+        }
         k_cache_init<<<(unsigned)B, 256>>>(A, d->k);
         SKB_CHECK_LAUNCH();
         SKB_CHECK_CUDA(cudaDeviceSynchronize());
@@ -1445,6 +1583,69 @@ int skb_cache_step(skb_cache* c, const void* q, const void* k, const void* v, co
     if (c->d.dtype == SKB_BF16) cache_attend<__nv_bfloat16>(c, q, o, st);
     else if (c->d.dtype == SKB_F32) cache_attend<float>(c, q, o, st);
     else cache_attend<double>(c, q, o, st);
+    K5_END
+}
+
+// Linear-attention mix (Appendix B.1) on a cache created with
+// SKB_FLAG_LINEAR_MIX (float32/float64): after skb_cache_prefill(k, v, u, n),
+// skb_cache_linmix_prefill(v, phk, n) records phi(k) of the retained rows and
+// adds the n positions to the prefix state; a step is
+// skb_cache_linmix_step(q, k, v, u, phq, phk) -> the mixture readout o.
+// phq / phk: float64 phi rows (skb_linmix_phi) [B, H, p] (step) or [B, n, H, p].
+int skb_cache_linmix_prefill(skb_cache* c, const void* v, const double* phk, int64_t n, void* stream) {
+    K5_BEGIN
+    SKB_REQUIRE(c != nullptr && v && phk, SKB_EARG, "cache_linmix_prefill: null argument");
+    SKB_REQUIRE(c->A.lin, SKB_ECONFIG, "forward_chunk: linear mix needs feature parameters");
+    if (n == 0) return SKB_OK;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int B = (int)c->d.batch, H = (int)c->d.heads, p = (int)c->d.head_dim;
+    k_lin_fill_phi<<<dim3((unsigned)c->A.S, (unsigned)B), 128, 0, st>>>(c->A, phk, (int)n, H, p, c->lphk);
+    SKB_CHECK_LAUNCH();
+    if (c->d.dtype == SKB_F64)
+        k_lin_state_add<double><<<dim3((unsigned)H, (unsigned)B), 256, 0, st>>>(
+            phk, static_cast<const double*>(v), (int)n, H, p, c->lm, c->lb);
+    else
+        k_lin_state_add<float><<<dim3((unsigned)H, (unsigned)B), 256, 0, st>>>(
+            phk, static_cast<const float*>(v), (int)n, H, p, c->lm, c->lb);
+    SKB_CHECK_LAUNCH();
+    K5_END
+}
+
+int skb_cache_linmix_step(skb_cache* c, const void* q, const void* k, const void* v, const double* u,
+                          const double* phq, const double* phk, void* o, void* stream) {
+    K5_BEGIN
+    SKB_REQUIRE(c != nullptr && q && k && v && phq && phk && o, SKB_EARG, "cache_linmix_step: null argument");
+    SKB_REQUIRE(c->A.lin, SKB_ECONFIG, "forward_chunk: linear mix needs feature parameters");
+    SKB_REQUIRE(u != nullptr || c->d.k == 0.0, SKB_EARG, "cache_step: null scores");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int B = (int)c->d.batch, H = (int)c->d.heads, p = (int)c->d.head_dim;
+    SKB_REQUIRE(p <= 256, SKB_ESHAPE, "linear mix: head_dim must be <= 256");
+    const double* uu = u ? u : c->zeros;
+    k_cache_control<<<(unsigned)cdiv(B, 4), 128, 0, st>>>(c->A, B, static_cast<const uint8_t*>(k),
+                                                          static_cast<const uint8_t*>(v), uu);
+    SKB_CHECK_LAUNCH();
+    // pass 1 of the position: its phi(k) row and the prefix state include it (cache.cpp:267-278)
+    k_lin_fill_phi<<<dim3((unsigned)c->A.S, (unsigned)B), 128, 0, st>>>(c->A, phk, 1, H, p, c->lphk);
+    const double scale = c->d.scale > 0.0 ? c->d.scale : 1.0 / std::sqrt((double)p);
+    int* bad = c->zeros_flag();
+    SKB_CHECK_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), st));
+    const unsigned g = (unsigned)cdiv((int64_t)B * H, 4);
+    if (c->d.dtype == SKB_F64) {
+        k_lin_state_add<double><<<dim3((unsigned)H, (unsigned)B), 256, 0, st>>>(
+            phk, static_cast<const double*>(v), 1, H, p, c->lm, c->lb);
+        k_lin_decode<double><<<dim3(g), 128, 0, st>>>(c->A, static_cast<const double*>(q), phq, c->lphk, c->lm, c->lb,
+                                                      B, H, p, scale, static_cast<double*>(o), bad);
+    } else {
+        k_lin_state_add<float><<<dim3((unsigned)H, (unsigned)B), 256, 0, st>>>(
+            phk, static_cast<const float*>(v), 1, H, p, c->lm, c->lb);
+        k_lin_decode<float><<<dim3(g), 128, 0, st>>>(c->A, static_cast<const float*>(q), phq, c->lphk, c->lm, c->lb,
+                                                     B, H, p, scale, static_cast<float*>(o), bad);
+    }
+    SKB_CHECK_LAUNCH();
+    int hbad = 0;
+    SKB_CHECK_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+    SKB_CHECK_CUDA(cudaStreamSynchronize(st));
+    SKB_REQUIRE(!hbad, SKB_ENUMERIC, "linear mix: nonpositive denominator");
     K5_END
 }
 
@@ -1669,6 +1870,8 @@ int skb_cache_ledger(skb_cache* c, int64_t b, int32_t drain, int64_t* pending, i
 int skb_cache_snapshot(skb_cache* c, int64_t b, const double* norm_state, uint8_t* out, size_t* bytes,
                        void* stream) {
     K5_BEGIN
+    SKB_REQUIRE(c == nullptr || !c->A.lin, SKB_ECONFIG,
+                "cache snapshot: the linear mix's prefix state is not serialised by this backend");
     SKB_REQUIRE(c != nullptr && bytes != nullptr, SKB_EARG, "cache_snapshot: null argument");
     SKB_REQUIRE(b >= 0 && b < c->d.batch, SKB_EARG, "cache_snapshot: sequence out of range");
     cudaStream_t st = static_cast<cudaStream_t>(stream);

@@ -463,6 +463,24 @@ void set_last_error(const char* msg);  // skb_capi.cu (thread-local skb_last_err
 
 extern "C" {
 
+int skb_linmix_phi(int64_t rows, int64_t heads, int64_t head_dim, int32_t dtype, const void* z, const double* feat,
+                   double* out, void* stream) {
+    LM_BEGIN
+    SKB_REQUIRE(z && feat && out, SKB_EARG, "linmix_phi: null argument");
+    SKB_REQUIRE(rows >= 0 && heads >= 1 && head_dim >= 1 && head_dim <= 32 * skb::kLmPer, SKB_ESHAPE,
+                "linmix_phi: bad shape");
+    if (rows == 0) return SKB_OK;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int64_t n = rows * heads;
+    skb::dispatch_lm(dtype, [&](auto tag) {
+        using S = std::remove_const_t<std::remove_pointer_t<decltype(tag)>>;
+        skb::k_phi<S><<<(unsigned)skb::cdiv(n, skb::kLmWarps), skb::kLmWarps * 32, 0, st>>>(
+            static_cast<const S*>(z), feat, out, n, (int)heads, (int)head_dim);
+    });
+    SKB_CHECK_LAUNCH();
+    LM_END
+}
+
 int skb_linmix_workspace_size(const skb_attn_desc* d, size_t* bytes) {
     LM_BEGIN
     SKB_REQUIRE(d && bytes, SKB_EARG, "linmix_workspace_size: null argument");

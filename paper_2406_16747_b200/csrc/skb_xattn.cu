@@ -446,10 +446,13 @@ int skb_xcache_norm_state(skb_xcache* c, double* norm_state, int32_t set, void* 
 // rows in the pool (skb_cache_prefill); later chunks run one generate_step
 // per row (skb_cache_step: exit/admit, then the attention over the retained
 // (floor(k) + w) rows), which is the reference's row order exactly.
-int skb_xcache_forward_chunk(skb_xcache* c, const void* x, int64_t n, const void* wq, const void* wk, const void* wv,
-                             const void* wo, const double* w_score, void* y, void* stream) {
+static int xcache_forward_chunk(skb_xcache* c, const void* x, int64_t n, const void* wq, const void* wk,
+                                const void* wv, const void* wo, const double* w_score, const double* feat, void* y,
+                                void* stream) {
     XA_BEGIN
     SKB_REQUIRE(c && x && wq && wk && wv && wo && y, SKB_EARG, "forward_chunk: null argument");
+    SKB_REQUIRE(!feat == !(c->d.flags & SKB_FLAG_LINEAR_MIX), SKB_ECONFIG,
+                "forward_chunk: linear mix needs feature parameters");
     SKB_REQUIRE(n >= 1, SKB_ESHAPE, "forward_chunk: empty chunk");
     const skb_x_desc& d = c->d;
     SKB_REQUIRE(c->seen + n <= d.seq_len, SKB_ESHAPE, "forward_chunk: cache capacity (max positions) exceeded");
@@ -480,8 +483,19 @@ int skb_xcache_forward_chunk(skb_xcache* c, const void* x, int64_t n, const void
         void* sel = tmp.get(lay.total_bytes);
         double* lse = static_cast<double*>(tmp.get(M * H * 8));
         check_rc(skb_select(&a, u, sel, stream));
-        check_rc(skb_attn_fwd(&a, q, k, v, u, sel, o, lse, stream));
-        check_rc(skb_cache_prefill(c->cache, k, v, u, n, stream));
+        if (feat) {  // the mixture readout over the chunk, then phi(k) + the prefix state into the cache
+            size_t lb = 0;
+            check_rc(skb_linmix_workspace_size(&a, &lb));
+            void* lws = tmp.get(lb);
+            check_rc(skb_linmix_fwd(&a, q, k, v, u, sel, feat, o, lse, lws, stream));
+            check_rc(skb_cache_prefill(c->cache, k, v, u, n, stream));
+            double* phk = static_cast<double*>(tmp.get(M * D * 8));
+            check_rc(skb_linmix_phi(M, H, p, dt, k, feat, phk, stream));
+            check_rc(skb_cache_linmix_prefill(c->cache, v, phk, n, stream));
+        } else {
+            check_rc(skb_attn_fwd(&a, q, k, v, u, sel, o, lse, stream));
+            check_rc(skb_cache_prefill(c->cache, k, v, u, n, stream));
+        }
     } else {
         const size_t row = (size_t)D * es;
         void* qr = tmp.get(B * row);
@@ -489,6 +503,7 @@ int skb_xcache_forward_chunk(skb_xcache* c, const void* x, int64_t n, const void
         void* vr = tmp.get(B * row);
         void* orow = tmp.get(B * row);
         double* ur = static_cast<double*>(tmp.get(B * 8));
+        void* phbuf = feat ? tmp.get(2 * B * D * 8) : nullptr;
         for (int64_t r = 0; r < n; ++r) {  // generate_step per row (cache.cpp:570-577)
             SKB_CHECK_CUDA(cudaMemcpy2DAsync(qr, row, static_cast<char*>(q) + r * row, n * row, row, B,
                                              cudaMemcpyDeviceToDevice, st));
@@ -497,7 +512,16 @@ int skb_xcache_forward_chunk(skb_xcache* c, const void* x, int64_t n, const void
             SKB_CHECK_CUDA(cudaMemcpy2DAsync(vr, row, static_cast<char*>(v) + r * row, n * row, row, B,
                                              cudaMemcpyDeviceToDevice, st));
             SKB_CHECK_CUDA(cudaMemcpy2DAsync(ur, 8, u + r, n * 8, 8, B, cudaMemcpyDeviceToDevice, st));
-            check_rc(skb_cache_step(c->cache, qr, kr, vr, d.k > 0.0 ? ur : nullptr, orow, stream));
+            if (feat) {
+                double* phq = static_cast<double*>(phbuf);
+                double* phk = phq + B * D;
+                check_rc(skb_linmix_phi(B, H, p, dt, qr, feat, phq, stream));
+                check_rc(skb_linmix_phi(B, H, p, dt, kr, feat, phk, stream));
+                check_rc(skb_cache_linmix_step(c->cache, qr, kr, vr, d.k > 0.0 ? ur : nullptr, phq, phk, orow,
+                                               stream));
+            } else {
+                check_rc(skb_cache_step(c->cache, qr, kr, vr, d.k > 0.0 ? ur : nullptr, orow, stream));
+            }
             SKB_CHECK_CUDA(cudaMemcpy2DAsync(static_cast<char*>(o) + r * row, n * row, orow, row, row, B,
                                              cudaMemcpyDeviceToDevice, st));
         }
@@ -507,6 +531,21 @@ int skb_xcache_forward_chunk(skb_xcache* c, const void* x, int64_t n, const void
     SKB_CHECK_CUDA(cudaStreamSynchronize(st));
     c->seen += n;
     XA_END
+}
+
+int skb_xcache_forward_chunk(skb_xcache* c, const void* x, int64_t n, const void* wq, const void* wk, const void* wv,
+                             const void* wo, const double* w_score, void* y, void* stream) {
+    return xcache_forward_chunk(c, x, n, wq, wk, wv, wo, w_score, nullptr, y, stream);
+}
+
+int skb_xcache_forward_chunk_lin(skb_xcache* c, const void* x, int64_t n, const void* wq, const void* wk,
+                                 const void* wv, const void* wo, const double* w_score, const double* feat, void* y,
+                                 void* stream) {
+    if (!feat) {
+        skb::set_last_error("forward_chunk: linear mix needs feature parameters");
+        return SKB_ECONFIG;
+    }
+    return xcache_forward_chunk(c, x, n, wq, wk, wv, wo, w_score, feat, y, stream);
 }
 
 }  // extern "C"

@@ -306,6 +306,19 @@ def linmix_bwd(q, k, v, u, feat, den, do, sel: Selection, cfg: AttnConfig):
     return dq, dk, dv, du, dfeat
 
 
+@_on_device
+def linmix_phi(z, feat):
+    """phi(z) = elu(F_h z) + 1 of rows z [..., H, p] (float32/float64) -> float64."""
+    H, p = z.shape[-2], z.shape[-1]
+    z = z.contiguous()
+    f = _feat(feat, H, p, z.device)
+    out = torch.empty(z.shape, dtype=torch.float64, device=z.device)
+    rows = z.numel() // (H * p)
+    check(_lib.load().skb_linmix_phi(rows, H, p, _DT[z.dtype], z.data_ptr(), f.data_ptr(), out.data_ptr(),
+                                     _stream()))
+    return out
+
+
 class LinearMixFn(torch.autograd.Function):
     """(q, k, v, u, feat) -> o for the linear-attention mix, with its backward."""
 
@@ -586,6 +599,27 @@ class DecodeCache:
         u = self._chk(u, (self.B, n), torch.float64, "u")
         check(_lib.load().skb_cache_prefill(self._h, k.data_ptr(), v.data_ptr(), u.data_ptr(), n,
                                             _stream()))
+
+    @_cache_dev
+    def linmix_prefill(self, v, phk):
+        """Linear mix (cfg.linear_mix): after prefill(k, v, u), record phi(k) of the
+        retained rows and add the prompt to the prefix state (phk float64 [B, n, H, p])."""
+        n = v.shape[1]
+        v = self._chk(v, (self.B, n, self.H, self.p), self.dtype, "v")
+        phk = self._chk(phk, (self.B, n, self.H, self.p), torch.float64, "phk")
+        check(_lib.load().skb_cache_linmix_prefill(self._h, v.data_ptr(), phk.data_ptr(), n, _stream()))
+
+    @_cache_dev
+    def linmix_step(self, q, k, v, u, phq, phk, out=None):
+        """One position of the linear-mix cache: returns the mixture readout o [B, H, p]."""
+        shp = (self.B, self.H, self.p)
+        q, k, v = (self._chk(t, shp, self.dtype, n) for t, n in ((q, "q"), (k, "k"), (v, "v")))
+        phq, phk = (self._chk(t, shp, torch.float64, n) for t, n in ((phq, "phq"), (phk, "phk")))
+        u = self._chk(u, (self.B,), torch.float64, "u")
+        o = torch.empty_like(q) if out is None else out
+        check(_lib.load().skb_cache_linmix_step(self._h, q.data_ptr(), k.data_ptr(), v.data_ptr(), u.data_ptr(),
+                                                phq.data_ptr(), phk.data_ptr(), o.data_ptr(), _stream()))
+        return o
 
     @_cache_dev
     def snapshot(self, b=0, norm_state=None):

@@ -203,6 +203,18 @@ static void attention_section(const std::string& tag) {
     put(tag + "_lin_chunked_y", ylc.data);
     AttnGrads<T> lcg = sparsek_attention_backward(lct, g, P, sc, &lin);
     put(tag + "_lin_chunked_dx", lcg.dx.data);
+    // linear-mix decoding: the cache carries the prefix state
+    SparseKvCache<T> lcache(lc, D, sc);
+    MatT<T> lprompt(30, D);
+    std::copy(x.data.begin(), x.data.begin() + 30 * D, lprompt.data.begin());
+    MatT<T> lyp = lcache.forward_chunk(lprompt, P, nullptr, &lin);
+    std::vector<double> ldec(lyp.data.begin(), lyp.data.end());
+    for (size_t i = 30; i < L; ++i) {
+        std::vector<T> row(x.row(i), x.row(i) + D);
+        std::vector<T> yo = generate_step(lcache, row, P, &lin);
+        ldec.insert(ldec.end(), yo.begin(), yo.end());
+    }
+    put(tag + "_lin_decode_y", ldec);
 }
 
 static void errors_section() {

@@ -106,3 +106,33 @@ def test_linear_mix_errors(cuda):
         sk.linear_mix_attention(x, *ws, wsc, feat[:, :2, :2], 4.0, 2, heads=H)
     with pytest.raises(ValueError):  # w_score length
         sk.linear_mix_attention(x, *ws, wsc[:3], feat, 4.0, 2, heads=H)
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("k,w,prompt", [(6.5, 4, 20), (9.0, 0, 1), (0.0, 5, 12)])
+def test_linear_mix_decode_vs_reference(cuda, reference, dtype, k, w, prompt):
+    """Incremental decoding with the linear mix: the cache carries phi(k) of its
+    rows and the prefix state M, b across steps (forward_chunk / generate_step
+    with LinearMixParams, proj/src/cache.cpp:262-278,322-356,570-577)."""
+    import torch
+
+    from oracle.oracle import ref_cfg
+    from paper_2406_16747_b200 import DecodeSession, ops
+
+    L, D, H = 56, 16, 2
+    x, ws, wsc, feat, _ = _problem(L, D, H, 11 + prompt)
+    tdt = {"f64": torch.float64, "f32": torch.float32}[dtype]
+    if dtype == "f32":
+        x = x.astype(np.float32).astype(np.float64)
+        ws = [a.astype(np.float32).astype(np.float64) for a in ws]
+        feat = feat.astype(np.float32).astype(np.float64)
+    y_ref = reference.linear_mix_decode(x, *ws, wsc, feat, ref_cfg(k, w, heads=H), prompt,
+                                        use_float=dtype == "f32")
+    t = lambda a, dt=tdt: torch.from_numpy(np.ascontiguousarray(a)).to(cuda).to(dt)
+    s = DecodeSession(*(t(a) for a in ws), t(wsc) if k > 0 else None, ops.AttnConfig(k=k, window=w), H,
+                      batch=1, max_len=L, dtype=tdt, feat=t(feat, torch.float64))
+    xt = t(x).view(1, L, D)
+    ys = [s.forward_chunk(xt[:, :prompt])] + [s.step(xt[:, i])[:, None] for i in range(prompt, L)]
+    y = torch.cat(ys, 1)[0].double().cpu().numpy()
+    tol = 1e-9 if dtype == "f64" else 1e-5
+    assert rel_err(y, y_ref) < tol, rel_err(y, y_ref)
