@@ -236,15 +236,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(const __grid_constant__ 
         if (lane == 0) {
             constexpr uint32_t idesc_qk = umma_idesc(128, 128, false, false);
             constexpr uint32_t idesc_pv = umma_idesc(128, D, false, true);
-            mbar_wait(&bars[B_QFULL], 0);
+            mbar_wait_fast(&bars[B_QFULL], 0);
             fence_proxy_async();
             auto pv = [&](int j) {
-                mbar_wait(&bars[B_VFULL + (j & 1)], (j >> 1) & 1);
+                mbar_wait_fast(&bars[B_VFULL + (j & 1)], (j >> 1) & 1);
                 fence_proxy_async();
                 const uint32_t vb = sbase + SM::kV + (j & 1) * SM::kTile;
 #pragma unroll
                 for (int hf = 0; hf < 2; ++hf) {
-                    mbar_wait(&bars[B_PFULL + 2 * (j & 1) + hf], (j >> 1) & 1);
+                    mbar_wait_fast(&bars[B_PFULL + 2 * (j & 1) + hf], (j >> 1) & 1);
                     SKB_TR(3, j, 2 + hf);
                     tc_after_sync();
                     // P~ of this half: 64 keys packed over the first 32 of its own S columns
@@ -261,10 +261,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_tc(const __grid_constant__ 
                 const int s = jt & 1;
                 const int ks = jt % kKS;
                 SKB_TR(3, jt, 8);
-                mbar_wait(&bars[B_KFULL + ks], (jt / kKS) & 1);
+                mbar_wait_fast(&bars[B_KFULL + ks], (jt / kKS) & 1);
                 SKB_TR(3, jt, 0);
                 fence_proxy_async();
-                if (jt >= 2) mbar_wait(&bars[B_SEMPTY + s], ((jt - 2) >> 1) & 1);
+                if (jt >= 2) mbar_wait_fast(&bars[B_SEMPTY + s], ((jt - 2) >> 1) & 1);
                 tc_after_sync();
                 const uint32_t kb = sbase + SM::kK + ks * SM::kTile;
 #pragma unroll
@@ -629,13 +629,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_p(const __grid_constant__ F
             constexpr uint32_t idesc_qk = umma_idesc(128, 128, false, false);
             constexpr uint32_t idesc_pv = umma_idesc(128, D, false, true);
             auto pv = [&](int J, int j, int itn) {
-                mbar_wait(&bars[B_VFULL + (J & 1)], (J >> 1) & 1);
+                mbar_wait_fast(&bars[B_VFULL + (J & 1)], (J >> 1) & 1);
                 fence_proxy_async();
-                if (j == 0 && itn > 0) mbar_wait(&bars[B_OEMPTY], (itn - 1) & 1);  // O read out
+                if (j == 0 && itn > 0) mbar_wait_fast(&bars[B_OEMPTY], (itn - 1) & 1);  // O read out
                 const uint32_t vb = sbase + SM::kV + (J & 1) * SM::kTile;
 #pragma unroll
                 for (int hf = 0; hf < 2; ++hf) {
-                    mbar_wait(&bars[B_PFULL + 2 * (J & 1) + hf], (J >> 1) & 1);
+                    mbar_wait_fast(&bars[B_PFULL + 2 * (J & 1) + hf], (J >> 1) & 1);
                     tc_after_sync();
                     // P~ of this half: 64 keys packed over the first 32 of its own S columns
                     const uint32_t pa = tS + (J & 1) * 128 + hf * 64;
@@ -651,12 +651,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_p(const __grid_constant__ F
             for (int wi = blockIdx.x; wi < nitems; wi += gridDim.x, ++it) {
                 const Item I = item(wi);
                 const int n = I.n;
-                mbar_wait(&bars[B_QFULL], it & 1);
+                mbar_wait_fast(&bars[B_QFULL], it & 1);
                 for (int jt = 0; jt < n; ++jt) {
                     const int JJ = J + jt, s = JJ & 1, ks = JJ % kKS;
-                    mbar_wait(&bars[B_KFULL + ks], (JJ / kKS) & 1);
+                    mbar_wait_fast(&bars[B_KFULL + ks], (JJ / kKS) & 1);
                     fence_proxy_async();
-                    if (JJ >= 2) mbar_wait(&bars[B_SEMPTY + s], ((JJ - 2) >> 1) & 1);
+                    if (JJ >= 2) mbar_wait_fast(&bars[B_SEMPTY + s], ((JJ - 2) >> 1) & 1);
                     tc_after_sync();
                     const uint32_t kb = sbase + SM::kK + ks * SM::kTile;
 #pragma unroll

@@ -24,15 +24,24 @@
 #include "skb_tc.cuh"
 #include "skb_tmap.h"
 
+// experiment builds only: 1 = the selected pass's math warps skip the
+// elementwise work (tensor pipe alone), 2 = no S/dP MMAs, 3 = no dV/dK MMAs
+#ifndef SKB_BWD_EXP
+#define SKB_BWD_EXP 0
+#endif
+
+
 #ifdef SKB_TRACE
-__device__ unsigned long long g_skb_trace_bwd[4096];
+// CTAs 100 and 101 (a pair of the pair pass) at offsets 0 and 4096
+__device__ unsigned long long g_skb_trace_bwd[8192];
 #define SKB_TRB(role, jt, ev)                                                                        \
     do {                                                                                              \
-        if (blockIdx.x == 100 && blockIdx.y == 0 && blockIdx.z == 0 && (jt) < 32 && (role) < 8)     \
-            g_skb_trace_bwd[((role) * 512 + (jt) * 16 + (ev)) & 4095] = clock64();                   \
+        if ((blockIdx.x == 100 || blockIdx.x == 101) && blockIdx.y == 0 && blockIdx.z == 0 && (jt) < 32 && \
+            (role) < 8)                                                                               \
+            g_skb_trace_bwd[(blockIdx.x - 100) * 4096 + (((role) * 512 + (jt) * 16 + (ev)) & 4095)] = clock64(); \
     } while (0)
 extern "C" int skb_debug_trace_bwd(unsigned long long* out, int n) {
-    return (int)cudaMemcpyFromSymbol(out, g_skb_trace_bwd, sizeof(unsigned long long) * (n < 4096 ? n : 4096));
+    return (int)cudaMemcpyFromSymbol(out, g_skb_trace_bwd, sizeof(unsigned long long) * (n < 8192 ? n : 8192));
 }
 #else
 #define SKB_TRB(role, jt, ev) \
@@ -50,6 +59,7 @@ struct BwdArgs {
     CUtensorMap tm_q128, tm_do128;  // 3-D row tiles (box 64 x rows)
     CUtensorMap tm_k64, tm_v64;
     CUtensorMap tm_q64, tm_do64;
+    CUtensorMap tm_q32, tm_do32;  // 32-row boxes (the pair pass's per-CTA query halves)
     CUtensorMap tm_k128, tm_v128;
     CUtensorMap tm_dk_st, tm_dv_st;  // 32-key group stores (tmap_groups4d)
     const __nv_bfloat16 *q, *k, *v, *dout;
@@ -134,19 +144,25 @@ __global__ void __launch_bounds__(256) k_bwd_prep(const __nv_bfloat16* __restric
 // per-query lse/delta/tau by cp.async; a stage is released by the MMA commit.
 constexpr int kQS = 3;  // Q/dO ring depth
 
-template <int D>
+// The selected pass without fused dQ holds 4 Q/dO stages: a stage is busy
+// from its TMA issue (~2.5k cycles to land under load) to the commit of the
+// tile's dV/dK MMAs, and with 3 stages that loop, not the tensor pipe, set the
+// tile period (tools/trace_selp.py; SKB_BWD_EXP decomposition in DESIGN.md).
+constexpr int kSelQS = 4;
+
+template <int D, int QS = kQS, bool FQ = false>
 struct KSmem {
     static constexpr int kKV = 128 * D * 2;  // 128-key tile
     static constexpr int kQT = 64 * D * 2;   // 64-query tile
     static constexpr int kK = 0;
     static constexpr int kV = kK + kKV;
-    static constexpr int kQ = kV + kKV;          // [kQS]
-    static constexpr int kDO = kQ + kQS * kQT;   // [kQS]
-    static constexpr int kDS = kDO + kQS * kQT;   // dS^T of the tile (fused dQ): 128 keys x 64 queries bf16
-    static constexpr int kStage = kDS + (D == 128 ? 128 * 64 * 2 : 0);  // fused dQ: per-warp 16 x 32 fp32 transpose
-    static constexpr int kMeta = kStage + (D == 128 ? 8 * 2048 : 0);      // [kQS][lse2|delta|tau][64] f32
-    static constexpr int kBar = kMeta + kQS * 3 * 64 * 4;
-    static constexpr int kNumBars = 22;
+    static constexpr int kQ = kV + kKV;          // [QS]
+    static constexpr int kDO = kQ + QS * kQT;    // [QS]
+    static constexpr int kDS = kDO + QS * kQT;   // dS^T of the tile (fused dQ): 128 keys x 64 queries bf16
+    static constexpr int kStage = kDS + (FQ ? 128 * 64 * 2 : 0);  // fused dQ: per-warp 16 x 32 fp32 transpose
+    static constexpr int kMeta = kStage + (FQ ? 8 * 2048 : 0);      // [QS][lse2|delta|tau][64] f32
+    static constexpr int kBar = kMeta + QS * 3 * 64 * 4;
+    static constexpr int kNumBars = 24;
     static constexpr int kTmemSlot = kBar + kNumBars * 8;
     static constexpr int kAlloc = kTmemSlot + 16 + 1024;
 };
@@ -511,13 +527,13 @@ struct KWSmem {
     static constexpr int kStage = kDS + (FQ ? 128 * 64 * 2 : 0);  // fused dQ: per-warp 16 x 32 fp32 transpose
     static constexpr int kMeta = kStage + (FQ ? 8 * 2048 : 0);       // [QS][lse2|delta][64] f32
     static constexpr int kBar = kMeta + QS * 2 * 64 * 4;
-    static constexpr int kTmemSlot = kBar + 22 * 8;
+    static constexpr int kTmemSlot = kBar + 24 * 8;
     static constexpr int kAlloc = kTmemSlot + 16 + 1024;
     static_assert(kAlloc <= 232448, "smem");
 };
-enum { KW_KVFULL = 0, KW_KVEMPTY = 1, KW_QDFULL = 2, KW_QDEMPTY = 5, KW_SFULL = 8, KW_SEMPTY = 10,
-       KW_PDSFULL = 12, KW_ACCDONE = 14, KW_ACCEMPTY = 15, KW_PARTFULL = 16, KW_STGFULL = 17,
-       KW_DQFULL = 18, KW_DQEMPTY = 20 };  // 22 barriers (fused dQ: DQFULL x2 = a tile's dQ^T is complete
+enum { KW_KVFULL = 0, KW_KVEMPTY = 1, KW_QDFULL = 2, KW_QDEMPTY = 6, KW_SFULL = 10, KW_SEMPTY = 12,
+       KW_PDSFULL = 14, KW_ACCDONE = 16, KW_ACCEMPTY = 17, KW_PARTFULL = 18, KW_STGFULL = 19,
+       KW_DQFULL = 20, KW_DQEMPTY = 22 };  // 24 barriers (Q/dO rings up to 4 stages) (fused dQ: DQFULL x2 = a tile's dQ^T is complete
                                            // in TMEM, DQEMPTY x2 = it has been read back)
 
 // Fused dQ (D = 128): the key-major passes also form dQ^T = K^T dS^T per
@@ -739,9 +755,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_win_tc(const __grid_co
             // tile qt); the first tile of an item waits for the accumulators
             auto acc = [&](int gj, int qt, int itn) {
                 const int s = gj & 1, qs = gj % QS;
-                mbar_wait(&bars[KW_PDSFULL + s], (gj >> 1) & 1);
+                mbar_wait_fast(&bars[KW_PDSFULL + s], (gj >> 1) & 1);
                 TRW(7, gj, 2);
-                if (qt == 0 && itn > 0) mbar_wait(&bars[KW_ACCEMPTY], (itn - 1) & 1);
+                if (qt == 0 && itn > 0) mbar_wait_fast(&bars[KW_ACCEMPTY], (itn - 1) & 1);
                 TRW(7, gj, 3);
                 tc_after_sync();
                 const uint32_t dob = sbase + SM::kDO + qs * SM::kQT, qb = sbase + SM::kQ + qs * SM::kQT;
@@ -777,15 +793,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_win_tc(const __grid_co
                 int b, h, j0, nkeys, nq;
                 item(wi, b, h, j0, nkeys, nq);
                 if (it == 20) tr0 = g;
-                mbar_wait(&bars[KW_KVFULL], it & 1);
+                mbar_wait_fast(&bars[KW_KVFULL], it & 1);
                 TRW(7, g, 4);
                 tc_after_sync();
                 for (int qt = 0; qt < nq; ++qt, ++g) {
                     const int s = g & 1, qs = g % QS;
                     TRW(7, g, 8);
-                    mbar_wait(&bars[KW_QDFULL + qs], (g / QS) & 1);
+                    mbar_wait_fast(&bars[KW_QDFULL + qs], (g / QS) & 1);
                     TRW(7, g, 0);
-                    if (g >= 2) mbar_wait(&bars[KW_SEMPTY + s], ((g - 2) >> 1) & 1);
+                    if (FQ && g >= 2) mbar_wait_fast(&bars[KW_SEMPTY + s], ((g - 2) >> 1) & 1);  // (non-fused: implied by PDSFULL(g - 2))
                     TRW(7, g, 5);
                     tc_after_sync();
                     const uint32_t qb = sbase + SM::kQ + qs * SM::kQT, dob = sbase + SM::kDO + qs * SM::kQT;
@@ -794,7 +810,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_win_tc(const __grid_co
                         for (int kk = 0; kk < D / 16; ++kk)
                             umma_f16(tS + s * 64, desc_kmajor(sbase + SM::kK, 128, kk), desc_kmajor(qb, 64, kk), id_s,
                                      kk > 0 ? 1u : 0u);
-                        if (g >= 2) mbar_wait(&bars[KW_DQEMPTY + s], ((g - 2) >> 1) & 1);
+                        if (g >= 2) mbar_wait_fast(&bars[KW_DQEMPTY + s], ((g - 2) >> 1) & 1);
                         tc_after_sync();
 #pragma unroll
                         for (int kk = 0; kk < D / 16; ++kk)
@@ -1082,7 +1098,8 @@ __global__ void k_sel_items(BwdArgs a, int ntk) {
 // item's last S/dP MMA releases the buffer.
 template <int D, bool KEY_SOFT, bool FQ>
 __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_sel_tc(const __grid_constant__ BwdArgs a) {
-    using SM = KSmem<D>;
+    constexpr int QS = FQ ? kQS : kSelQS;
+    using SM = KSmem<D, QS, FQ>;
     static_assert(KW_DQFULL + 1 < SM::kNumBars, "barrier slots");
     extern __shared__ __align__(16) uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -1120,7 +1137,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_sel_tc(const __grid_co
     if (threadIdx.x == 0) {
         mbar_init(&bars[KW_KVFULL], kProducers + 1);
         mbar_init(&bars[KW_KVEMPTY], 1);
-        for (int s = 0; s < kQS; ++s) {
+        for (int s = 0; s < QS; ++s) {
             mbar_init(&bars[KW_QDFULL + s], kProducers + 1);
             mbar_init(&bars[KW_QDEMPTY + s], 1);
         }
@@ -1167,8 +1184,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_sel_tc(const __grid_co
             const float* lse2 = a.lse2 + ((int64_t)b * a.H + h) * a.L;
             const float* dlt = a.delta + ((int64_t)b * a.H + h) * a.L;
             for (int qt = 0; qt < nq; ++qt, ++g) {
-                const int s = g % kQS;
-                if (g >= kQS) mbar_wait(&bars[KW_QDEMPTY + s], ((g - kQS) / kQS) & 1);
+                const int s = g % QS;
+                if (g >= QS) mbar_wait(&bars[KW_QDEMPTY + s], ((g - QS) / QS) & 1);
                 if (ptid == 0) TRS(6, g, 1);
                 const int qs = q_lo + qt * 64;
                 for (int c = ptid; c < 64; c += kProducers) {
@@ -1199,10 +1216,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_sel_tc(const __grid_co
             constexpr uint32_t id_acc = umma_idesc(128, D, false, true);
             int g = 0, kit = 0, tr0 = 1 << 28;
             auto acc = [&](int gj, int qt, int kitn) {
-                const int s = gj & 1, qs = gj % kQS;
-                mbar_wait(&bars[KW_PDSFULL + s], (gj >> 1) & 1);
+                const int s = gj & 1, qs = gj % QS;
+                mbar_wait_fast(&bars[KW_PDSFULL + s], (gj >> 1) & 1);
                 TRS(7, gj, 2);
-                if (qt == 0 && kitn > 0) mbar_wait(&bars[KW_ACCEMPTY], (kitn - 1) & 1);
+                if (qt == 0 && kitn > 0) mbar_wait_fast(&bars[KW_ACCEMPTY], (kitn - 1) & 1);
                 tc_after_sync();
                 const uint32_t dob = sbase + SM::kDO + qs * SM::kQT, qb = sbase + SM::kQ + qs * SM::kQT;
                 if constexpr (FQ) {
@@ -1225,6 +1242,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_sel_tc(const __grid_co
                 } else {
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk) {
+                        if (SKB_BWD_EXP == 3) break;
                         const uint32_t co = s * 64 + (kk >> 1) * 32 + (kk & 1) * 8;
                         umma_f16_ts(tDV, tS + co, desc_mnmajor(dob, 64, kk), id_acc, (qt > 0 || kk > 0) ? 1u : 0u);
                         umma_f16_ts(tDK, tP + co, desc_mnmajor(qb, 64, kk), id_acc, (qt > 0 || kk > 0) ? 1u : 0u);
@@ -1236,15 +1254,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_sel_tc(const __grid_co
                 int b, h, kt, nkeys, q_lo, nq;
                 if (!item(wi, b, h, kt, nkeys, q_lo, nq) || nq == 0) continue;
                 if (kit == 6) tr0 = g;
-                mbar_wait(&bars[KW_KVFULL], kit & 1);
+                mbar_wait_fast(&bars[KW_KVFULL], kit & 1);
                 TRS(7, g, 4);
                 fence_proxy_async();  // cp.async rows -> the MMA (async proxy)
                 tc_after_sync();
                 for (int qt = 0; qt < nq; ++qt, ++g) {
-                    const int s = g & 1, qs = g % kQS;
-                    mbar_wait(&bars[KW_QDFULL + qs], (g / kQS) & 1);
+                    const int s = g & 1, qs = g % QS;
+                    mbar_wait_fast(&bars[KW_QDFULL + qs], (g / QS) & 1);
                     TRS(7, g, 0);
-                    if (g >= 2) mbar_wait(&bars[KW_SEMPTY + s], ((g - 2) >> 1) & 1);
+                    if (FQ && g >= 2) mbar_wait_fast(&bars[KW_SEMPTY + s], ((g - 2) >> 1) & 1);  // (non-fused: implied by PDSFULL(g - 2))
                     tc_after_sync();
                     const uint32_t qb = sbase + SM::kQ + qs * SM::kQT, dob = sbase + SM::kDO + qs * SM::kQT;
                     if constexpr (FQ) {  // S^T first: dP^T's columns may still hold dQ^T(g-2) being read back
@@ -1252,7 +1270,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_sel_tc(const __grid_co
                         for (int kk = 0; kk < D / 16; ++kk)
                             umma_f16(tS + s * 64, desc_kmajor(sbase + SM::kK, 128, kk), desc_kmajor(qb, 64, kk), id_s,
                                      kk > 0 ? 1u : 0u);
-                        if (g >= 2) mbar_wait(&bars[KW_DQEMPTY + s], ((g - 2) >> 1) & 1);
+                        if (g >= 2) mbar_wait_fast(&bars[KW_DQEMPTY + s], ((g - 2) >> 1) & 1);
                         tc_after_sync();
 #pragma unroll
                         for (int kk = 0; kk < D / 16; ++kk)
@@ -1261,6 +1279,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_sel_tc(const __grid_co
                     } else {
 #pragma unroll
                         for (int kk = 0; kk < D / 16; ++kk) {
+                            if (SKB_BWD_EXP == 2) break;
                             umma_f16(tS + s * 64, desc_kmajor(sbase + SM::kK, 128, kk), desc_kmajor(qb, 64, kk), id_s,
                                      kk > 0 ? 1u : 0u);
                             umma_f16(tP + s * 64, desc_kmajor(sbase + SM::kV, 128, kk), desc_kmajor(dob, 64, kk), id_s,
@@ -1302,11 +1321,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_sel_tc(const __grid_co
             if (a.chunk_len > 0 && key >= 0) hi_i = min(hi_i, (key / a.chunk_len + 1) * a.chunk_len);
             float colsum = 0.f;
             for (int qt = 0; qt < nq; ++qt, ++g) {
-                const int s = g & 1, qs3 = g % kQS;
+                const int s = g & 1, qs3 = g % QS;
                 const int qs = q_lo + qt * 64 + hf * 32;
                 if (trl) TRS(4 + hf, g, 9);
                 mbar_wait(&bars[KW_SFULL + s], (g >> 1) & 1);
-                mbar_wait(&bars[KW_QDFULL + qs3], (g / kQS) & 1);
+                mbar_wait(&bars[KW_QDFULL + qs3], (g / QS) & 1);
                 if (trl) TRS(4 + hf, g, 0);
                 tc_after_sync();
                 float sv[32], dp[32];
@@ -1315,6 +1334,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_sel_tc(const __grid_co
                 tmem_wait_ld();
                 tc_before_sync();
                 mbar_arrive(&bars[KW_SEMPTY + s]);  // fused dQ: the dP^T half is released after its dQ^T is read
+                if (SKB_BWD_EXP == 1 && !FQ) {
+                    mbar_arrive(&bars[KW_PDSFULL + s]);
+                    continue;
+                }
                 const float* ml = qmeta + (qs3 * 3) * 64 + hf * 32;
                 const float* md = ml + 64;
                 const float* mt = ml + 128;
@@ -1523,6 +1546,428 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_sel_tc(const __grid_co
     tc_after_sync();
     if (warp == kMmaWarp) tmem_dealloc<512>(tmem);
 #undef TRS
+}
+
+// The selected pass's elementwise step for one thread's 32 query columns of a
+// key row (the single-CTA pass inlines the same arithmetic next to its fused-dQ
+// variant): P~^T into sv, dS^T (unscaled) into dp; returns the colsum term.
+template <bool KEY_SOFT>
+__device__ __forceinline__ float sel_tile_math(const BwdArgs& a, bool sat, float uj, const float* ml, const float* md,
+                                               const float* mt, float sl2, float2 sl22, float* sv, float* dp) {
+    float colsum = 0.f;
+    if (sat) {  // gates 1 on these columns: plain softmax backward, packed fp32x2
+#pragma unroll
+        for (int c = 0; c < 32; c += 4) {
+            const float4 l4 = *reinterpret_cast<const float4*>(ml + c);
+            const float4 d4 = *reinterpret_cast<const float4*>(md + c);
+            float2 x0 = __ffma2_rn(make_float2(sv[c], sv[c + 1]), sl22, make_float2(-l4.x, -l4.y));
+            float2 x1 = __ffma2_rn(make_float2(sv[c + 2], sv[c + 3]), sl22, make_float2(-l4.z, -l4.w));
+            x0.x = ex2(x0.x);
+            x0.y = ex2(x0.y);
+            x1.x = ex2(x1.x);
+            x1.y = ex2(x1.y);
+            const float2 c0 = __fmul2_rn(x0, __fadd2_rn(make_float2(dp[c], dp[c + 1]), make_float2(-d4.x, -d4.y)));
+            const float2 c1 = __fmul2_rn(x1, __fadd2_rn(make_float2(dp[c + 2], dp[c + 3]), make_float2(-d4.z, -d4.w)));
+            sv[c] = x0.x, sv[c + 1] = x0.y, sv[c + 2] = x1.x, sv[c + 3] = x1.y;
+            dp[c] = c0.x, dp[c + 1] = c0.y, dp[c + 2] = c1.x, dp[c + 3] = c1.y;
+        }
+    } else if constexpr (!KEY_SOFT) {
+        auto frac_loop = [&](auto mst_c) {
+            constexpr bool kMst = decltype(mst_c)::value;
+            float2 csum2 = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int c = 0; c < 32; c += 2) {
+                const float2 l2 = *reinterpret_cast<const float2*>(ml + c);
+                const float2 d2 = *reinterpret_cast<const float2*>(md + c);
+                const float2 t2 = *reinterpret_cast<const float2*>(mt + c);
+                const float g0 = __saturatef(uj - t2.x), g1 = __saturatef(uj - t2.y);
+                float2 p2 = __ffma2_rn(make_float2(sv[c], sv[c + 1]), sl22, make_float2(-l2.x, -l2.y));
+                p2.x = ex2(p2.x);  // masked: 0
+                p2.y = ex2(p2.y);
+                const float2 dp2 = make_float2(dp[c], dp[c + 1]);
+                const float2 nd2 = make_float2(-d2.x, -d2.y);
+                const float2 g2 = make_float2(g0, g1);
+                const float2 cc2 = kMst ? __fmul2_rn(p2, __fadd2_rn(dp2, nd2)) : __fmul2_rn(p2, __ffma2_rn(g2, dp2, nd2));
+                // 0 < g < 1 <=> (bits(g) - 1) < bits(1.0) - 1 (g in [0, 1])
+                const float2 fr2 = make_float2((__float_as_uint(g0) - 1u) < 0x3F7FFFFFu ? 1.f : 0.f,
+                                               (__float_as_uint(g1) - 1u) < 0x3F7FFFFFu ? 1.f : 0.f);
+                const float2 gf2 = __fmul2_rn(__fmul2_rn(p2, dp2), fr2);
+                csum2 = __fadd2_rn(csum2, gf2);
+                const float2 pw2 = kMst ? p2 : __fmul2_rn(p2, g2);
+                sv[c] = pw2.x, sv[c + 1] = pw2.y;  // P~^T
+                dp[c] = cc2.x, dp[c + 1] = cc2.y;  // dS^T (scale applied in the epilogue)
+            }
+            colsum += csum2.x + csum2.y;
+        };
+        if (a.mask_st) frac_loop(std::true_type{});
+        else frac_loop(std::false_type{});
+    } else {
+        float csum = 0.f;
+#pragma unroll
+        for (int c = 0; c < 32; c += 4) {
+            const float4 l4 = *reinterpret_cast<const float4*>(ml + c);
+            const float4 d4 = *reinterpret_cast<const float4*>(md + c);
+            const float4 t4 = *reinterpret_cast<const float4*>(mt + c);
+            const float la[4] = {l4.x, l4.y, l4.z, l4.w};
+            const float da[4] = {d4.x, d4.y, d4.z, d4.w};
+            const float ta[4] = {t4.x, t4.y, t4.z, t4.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int cc_ = c + e;
+                const float gt = __saturatef(uj - ta[e]);
+                const float kap = gt;
+                const float raw = sv[cc_];
+                const float x = raw == -INFINITY ? raw : raw * kap;
+                const float p = ex2(fmaf(x, sl2, -la[e]));  // masked: 0
+                const float wv = a.mask_st ? 1.f : gt;
+                const float cc = p * fmaf(wv, dp[cc_], -da[e]);
+                float gm = p * dp[cc_];
+                gm += a.scale * cc * (raw == -INFINITY ? 0.f : raw);
+                const float gf = (gt > 0.f && gt < 1.f) ? gm : 0.f;
+                csum += gf;
+                sv[cc_] = p * wv;    // P~^T
+                dp[cc_] = cc * kap;  // dS^T (scale applied in the epilogue)
+            }
+        }
+        colsum += csum;
+    }
+    return colsum;
+}
+
+// ------------------------------------------------------------ selected pass on CTA pairs
+// The selected pass (D = 128) as cta_group::2 MMAs on a cluster of two CTAs:
+// a work item is 256 entries of the ever-selected order (128 per CTA) and the
+// 64-query tiles that read any of them; the even CTA issues M = 256 MMAs.
+// A tcgen05.mma with M = 128 costs ~72 cycles for any N <= 128
+// (tools/probes/mma_rate.cu: N = 64 runs at half rate), and the single-CTA
+// pass's S^T / dP^T are N = 64; a pair instruction moves twice the keys in
+// the same time. Each CTA's TMEM, math warps and epilogue are those of the
+// single-CTA pass; what the pair changes is the B operands, split in halves:
+//   S^T = K Q^T, dP^T = V dO^T   (N = 64 queries): each CTA stages its 32
+//                                 query rows x 128 columns       ("X", 8 KB)
+//   dV += P~^T dO, dK += dS^T Q  (N = 128 columns): each CTA stages all 64
+//                                 query rows x its 64 columns     ("Y", 8 KB)
+// so a stage is 16 KB of Q + 16 KB of dO per CTA, as before, for twice the keys.
+// Barriers: the even CTA's QDFULL collects both CTAs' TMA bytes, its PDSFULL /
+// ACCEMPTY / KVFULL one arrival per warp (or relay) from each CTA; the MMA
+// commits multicast SFULL / QDEMPTY / KVEMPTY / ACCDONE to both CTAs.
+constexpr int kPairQS = 4;
+
+template <int D>
+struct PSmem {
+    static_assert(D == 128, "pair pass: D = 128");
+    static constexpr int kKV = 128 * D * 2;
+    static constexpr int kHalf = 32 * D * 2;  // X: 32 query rows x D (2 atom columns)
+    static constexpr int kQT = 2 * kHalf;     // X + Y (Y: 64 query rows x 64 columns)
+    static constexpr int kK = 0;
+    static constexpr int kV = kK + kKV;
+    static constexpr int kQ = kV + kKV;             // [kPairQS]
+    static constexpr int kDO = kQ + kPairQS * kQT;  // [kPairQS]
+    static constexpr int kMeta = kDO + kPairQS * kQT;  // [kPairQS][lse2|delta|tau][64] f32
+    static constexpr int kBar = kMeta + kPairQS * 3 * 64 * 4;
+    static constexpr int kNumBars = 24;
+    static constexpr int kTmemSlot = kBar + kNumBars * 8;
+    static constexpr int kAlloc = kTmemSlot + 16 + 1024;
+    static_assert(kAlloc <= 232448, "smem");
+};
+enum { PB_KVFULL = 0, PB_KVLOC = 1, PB_KVEMPTY = 2, PB_QDFULL = 3, PB_QDEMPTY = 7, PB_MFULL = 11, PB_SFULL = 15,
+       PB_PDSFULL = 17, PB_ACCDONE = 19, PB_ACCEMPTY = 20 };  // 21
+
+template <int D, bool KEY_SOFT>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    k_bwd_dkdv_sel_pair(const __grid_constant__ BwdArgs a) {
+    using SM = PSmem<D>;
+    constexpr int QS = kPairQS;
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    const uint32_t sbase = smem_u32(smem);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SM::kBar);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + SM::kTmemSlot);
+    float* qmeta = reinterpret_cast<float*>(smem + SM::kMeta);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef SKB_TRACE_SEL  // items 6.. of CTA 100 (tools/trace_selp.py)
+#define TRP(role, gg, ev) \
+    if ((gg) >= tr0) SKB_TRB(role, (gg) - tr0, ev)
+#else
+#define TRP(role, gg, ev) \
+    do {                  \
+    } while (0)
+#endif
+    const uint32_t rank = cluster_rank();
+    const bool leader = rank == 0;
+    const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+    const int ntk = (a.L + 127) / 128, ntk2 = (a.L + 255) / 256;
+    const int nitems = ntk2 * a.H * a.B;
+    // item wi -> (256-entry tile kt2 fastest, h, b); this CTA's keys are entries
+    // [kt2 * 256 + rank * 128, +128); the query range covers both halves
+    auto item = [&](int wi, int& b, int& h, int& kt2, int& nkeys, int& q_lo, int& nq) -> bool {
+        kt2 = wi % ntk2;
+        const int bh = wi / ntk2;
+        h = bh % a.H;
+        b = bh / a.H;
+        const int ec = __ldg(a.ever_count + b);
+        if (kt2 * 256 >= ec) return false;
+        const int n0 = min(128, ec - kt2 * 256), n1 = max(0, min(128, ec - kt2 * 256 - 128));
+        nkeys = rank ? n1 : n0;
+        int lo = INT_MAX, hi = 0;
+        const int2 i0 = a.sel_items[b * ntk + 2 * kt2];
+        if (i0.y > 0) lo = i0.x, hi = i0.x + 64 * i0.y;
+        if (n1 > 0) {
+            const int2 i1 = a.sel_items[b * ntk + 2 * kt2 + 1];
+            if (i1.y > 0) lo = min(lo, i1.x), hi = max(hi, i1.x + 64 * i1.y);
+        }
+        q_lo = hi > 0 ? lo : 0;
+        nq = hi > lo ? (hi - lo) / 64 : 0;
+        return true;
+    };
+    if (threadIdx.x == 0) {
+        mbar_init(&bars[PB_KVFULL], 2);
+        mbar_init(&bars[PB_KVLOC], kProducers + 1);
+        mbar_init(&bars[PB_KVEMPTY], 1);
+        for (int s = 0; s < QS; ++s) {
+            mbar_init(&bars[PB_QDFULL + s], 1);
+            mbar_init(&bars[PB_QDEMPTY + s], 1);
+            mbar_init(&bars[PB_MFULL + s], kProducers + 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&bars[PB_SFULL + s], 1);
+            mbar_init(&bars[PB_PDSFULL + s], 2 * (kMath / 32));
+        }
+        mbar_init(&bars[PB_ACCDONE], 1);
+        mbar_init(&bars[PB_ACCEMPTY], 2 * (kMath / 32));
+        mbar_fence_init();
+    }
+    if (warp == kMmaWarp) tmem_alloc_pair<512>(tmem_slot);
+    tc_before_sync();
+    cluster_sync_all();
+    tc_after_sync();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t tS = tmem, tP = tmem + 128, tDV = tmem + 256, tDK = tmem + 384;
+    auto lead = [&](int idx) { return peer_addr(smem_u32(&bars[idx]), 0); };
+
+    if (warp >= kProdWarp0 && warp < kMmaWarp) {
+        const int pw = warp - kProdWarp0, ptid = threadIdx.x - kProdWarp0 * 32;
+        int g = 0, kit = 0, tr0 = 1 << 28;
+        for (int wi = pair; wi < nitems; wi += npairs) {
+            int b, h, kt2, nkeys, q_lo, nq;
+            if (!item(wi, b, h, kt2, nkeys, q_lo, nq) || nq == 0) continue;
+            if (kit == 6) tr0 = g;
+            const int64_t bl = (int64_t)b * a.L;
+            const int* elist = a.sel_order + bl + kt2 * 256 + (int)rank * 128;
+            RowKeys<D, 128> kk;
+            kk.fetch(pw, lane, [&](int r) { return r < nkeys ? __ldg(elist + r) : -1; });
+            if (ptid == 0) TRP(6, g, 3);
+            if (kit > 0) mbar_wait(&bars[PB_KVEMPTY], (kit - 1) & 1);
+            if (ptid == 0) TRP(6, g, 2);
+            kk.issue(sbase + SM::kK, a.k, b, h, a.L, a.H, pw, lane);
+            kk.issue(sbase + SM::kV, a.v, b, h, a.L, a.H, pw, lane);
+            cp_async_arrive_noinc(&bars[PB_KVLOC]);
+            if (ptid == 0) mbar_arrive(&bars[PB_KVLOC]);
+            if (ptid == 64) {  // relay: this CTA's rows have landed -> the even CTA's MMA thread
+                mbar_wait(&bars[PB_KVLOC], kit & 1);
+                fence_proxy_async();
+                mbar_arrive_cluster(lead(PB_KVFULL));
+            }
+            ++kit;
+            const float* lse2 = a.lse2 + ((int64_t)b * a.H + h) * a.L;
+            const float* dlt = a.delta + ((int64_t)b * a.H + h) * a.L;
+            for (int qt = 0; qt < nq; ++qt, ++g) {
+                const int s = g % QS;
+                if (g >= QS) mbar_wait(&bars[PB_QDEMPTY + s], ((g - QS) / QS) & 1);
+                if (ptid == 0) TRP(6, g, 1);
+                const int qs = q_lo + qt * 64;
+                for (int c = ptid; c < 64; c += kProducers) {
+                    const int i = qs + c;
+                    const bool ok = i < a.L;
+                    const int t = i - a.w;
+                    const uint32_t mb = smem_u32(qmeta + (s * 3) * 64 + c);
+                    cp_async4(mb, lse2 + (ok ? i : 0), ok);
+                    cp_async4(mb + 64 * 4, dlt + (ok ? i : 0), ok);
+                    cp_async4(mb + 128 * 4, a.tauf + bl + (ok && t >= 0 ? t : 0), ok && t >= 0);
+                }
+                cp_async_arrive_noinc(&bars[PB_MFULL + s]);
+                if (ptid == 0) {
+                    mbar_arrive(&bars[PB_MFULL + s]);
+                    if (leader) mbar_expect_tx(&bars[PB_QDFULL + s], 2 * 2 * SM::kQT);
+                    const uint32_t full = lead(PB_QDFULL + s);
+                    const uint32_t q0 = sbase + SM::kQ + s * SM::kQT, d0 = sbase + SM::kDO + s * SM::kQT;
+#pragma unroll
+                    for (int at = 0; at < D / 64; ++at) {  // X: this CTA's 32 query rows, every column
+                        tma_load_3d_pair(q0 + at * 32 * 128, &a.tm_q32, h * D + at * 64, qs + (int)rank * 32, b, full);
+                        tma_load_3d_pair(d0 + at * 32 * 128, &a.tm_do32, h * D + at * 64, qs + (int)rank * 32, b, full);
+                    }
+                    // Y: every query row, this CTA's 64 columns
+                    tma_load_3d_pair(q0 + SM::kHalf, &a.tm_q64, h * D + (int)rank * 64, qs, b, full);
+                    tma_load_3d_pair(d0 + SM::kHalf, &a.tm_do64, h * D + (int)rank * 64, qs, b, full);
+                }
+            }
+        }
+    } else if (warp == kMmaWarp) {
+        if (leader && lane == 0) {
+            constexpr uint32_t id_s = umma_idesc(256, 64, false, false);
+            constexpr uint32_t id_acc = umma_idesc(256, D, false, true);
+            int g = 0, kit = 0, tr0 = 1 << 28;
+            auto acc = [&](int gj, int qt, int kitn) {
+                const int s = gj & 1, qs = gj % QS;
+                mbar_wait(&bars[PB_PDSFULL + s], (gj >> 1) & 1);
+                TRP(7, gj, 2);
+                if (qt == 0 && kitn > 0) mbar_wait(&bars[PB_ACCEMPTY], (kitn - 1) & 1);
+                tc_after_sync();
+                const uint32_t qy = sbase + SM::kQ + qs * SM::kQT + SM::kHalf;
+                const uint32_t dy = sbase + SM::kDO + qs * SM::kQT + SM::kHalf;
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) {
+                    const uint32_t co = s * 64 + (kk >> 1) * 32 + (kk & 1) * 8;
+                    umma_f16_ts_pair(tDV, tS + co, desc_mnmajor(dy, 64, kk), id_acc, (qt > 0 || kk > 0) ? 1u : 0u);
+                    umma_f16_ts_pair(tDK, tP + co, desc_mnmajor(qy, 64, kk), id_acc, (qt > 0 || kk > 0) ? 1u : 0u);
+                }
+                umma_commit_pair(&bars[PB_QDEMPTY + qs]);
+            };
+            for (int wi = pair; wi < nitems; wi += npairs) {
+                int b, h, kt2, nkeys, q_lo, nq;
+                if (!item(wi, b, h, kt2, nkeys, q_lo, nq) || nq == 0) continue;
+                if (kit == 6) tr0 = g;
+                mbar_wait(&bars[PB_KVFULL], kit & 1);
+                TRP(7, g, 4);
+                fence_proxy_async();
+                tc_after_sync();
+                for (int qt = 0; qt < nq; ++qt, ++g) {
+                    const int s = g & 1, qs = g % QS;
+                    mbar_wait(&bars[PB_QDFULL + qs], (g / QS) & 1);
+                    TRP(7, g, 0);
+                    tc_after_sync();
+                    const uint32_t qx = sbase + SM::kQ + qs * SM::kQT, dx = sbase + SM::kDO + qs * SM::kQT;
+#pragma unroll
+                    for (int kk = 0; kk < D / 16; ++kk) {
+                        umma_f16_pair(tS + s * 64, desc_kmajor(sbase + SM::kK, 128, kk), desc_kmajor(qx, 32, kk), id_s,
+                                      kk > 0 ? 1u : 0u);
+                        umma_f16_pair(tP + s * 64, desc_kmajor(sbase + SM::kV, 128, kk), desc_kmajor(dx, 32, kk), id_s,
+                                      kk > 0 ? 1u : 0u);
+                    }
+                    umma_commit_pair(&bars[PB_SFULL + s]);
+                    TRP(7, g, 1);
+                    if (qt == nq - 1) umma_commit_pair(&bars[PB_KVEMPTY]);
+                    // S/dP(g) are issued after dV/dK(g - 2) (in-order MMAs), which waited
+                    // for the math warps to finish with buffer s: no separate release
+                    if (qt >= 1) acc(g - 1, qt - 1, kit);
+                }
+                acc(g - 1, nq - 1, kit);
+                umma_commit_pair(&bars[PB_ACCDONE]);
+                ++kit;
+            }
+        }
+        __syncwarp();
+    } else if (warp < kProdWarp0) {
+        const int hf = warp >> 2;
+        const int r = ((warp & 3) << 5) | lane;
+        const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+        const float sl2 = a.scale_log2;
+        const float2 sl22 = make_float2(sl2, sl2);
+        int g = 0, kit = 0, tr0 = 1 << 28;
+        const bool trl = lane == 0 && (warp & 3) == 0;
+        for (int wi = pair; wi < nitems; wi += npairs) {
+            int b, h, kt2, nkeys, q_lo, nq;
+            if (!item(wi, b, h, kt2, nkeys, q_lo, nq)) continue;
+            if (kit == 6 && nq > 0) tr0 = g;
+            const int64_t bl = (int64_t)b * a.L;
+            const int e = kt2 * 256 + (int)rank * 128 + r;
+            const int key = r < nkeys ? __ldg(a.sel_order + bl + e) : -1;
+            const int leave = key >= 0 ? __ldg(a.leave + bl + key) : 0;
+            const float uj = key >= 0 ? __ldg(a.uf + bl + key) : 0.f;
+            // queries [key + w, leave + w) read this key from the selection
+            // (proj/src/cache.cpp:259-311), clipped to the key's chunk
+            const int lo_i = key + a.w;
+            int hi_i = min(a.L, leave + a.w);
+            if (a.chunk_len > 0 && key >= 0) hi_i = min(hi_i, (key / a.chunk_len + 1) * a.chunk_len);
+            float colsum = 0.f;
+            for (int qt = 0; qt < nq; ++qt, ++g) {
+                const int s = g & 1, qs3 = g % QS;
+                const int qs = q_lo + qt * 64 + hf * 32;
+                if (trl) TRP(4 + hf, g, 9);
+                mbar_wait(&bars[PB_SFULL + s], (g >> 1) & 1);
+                mbar_wait(&bars[PB_MFULL + qs3], (g / QS) & 1);
+                if (trl) TRP(4 + hf, g, 0);
+                tc_after_sync();
+                float sv[32], dp[32];
+                tmem_ld32(tS + lane_off + s * 64 + hf * 32, sv);
+                tmem_ld32(tP + lane_off + s * 64 + hf * 32, dp);
+                tmem_wait_ld();
+                if (SKB_BWD_EXP == 1) {  // experiment: no elementwise work
+                    tc_before_sync();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_cluster(lead(PB_PDSFULL + s));
+                    continue;
+                }
+                const float* ml = qmeta + (qs3 * 3) * 64 + hf * 32;
+                const float* md = ml + 64;
+                const float* mt = ml + 128;
+                const int cmin = key >= 0 ? lo_i - qs : 32;
+                const int cmax = key >= 0 ? hi_i - 1 - qs : -1;
+                const bool full = __all_sync(0xffffffffu, cmin <= 0 && cmax >= 31);
+                const int clast = max(0, min(31, a.L - 1 - qs));
+                const bool sat = __all_sync(0xffffffffu, key < 0 || uj >= mt[clast] + 1.f);
+                if (!full) {
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) sv[c] = (c >= cmin && c <= cmax) ? sv[c] : -INFINITY;
+                }
+                colsum += sel_tile_math<KEY_SOFT>(a, sat, uj, ml, md, mt, sl2, sl22, sv, dp);
+                uint32_t pk[16];
+#pragma unroll
+                for (int e2 = 0; e2 < 16; ++e2) pk[e2] = pack_bf16(sv[2 * e2], sv[2 * e2 + 1]);
+                tmem_st16u(tS + lane_off + s * 64 + hf * 32, pk);
+#pragma unroll
+                for (int e2 = 0; e2 < 16; ++e2) pk[e2] = pack_bf16(dp[2 * e2], dp[2 * e2 + 1]);
+                tmem_st16u(tP + lane_off + s * 64 + hf * 32, pk);
+                tmem_wait_st();
+                tc_before_sync();
+                __syncwarp();
+                if (trl) TRP(4 + hf, g, 4);
+                if (lane == 0) mbar_arrive_cluster(lead(PB_PDSFULL + s));
+            }
+            if (key >= 0 && colsum != 0.f) atomicAdd(a.colsum + bl + key, (double)colsum);
+            float dv[D / 2], dk[D / 2];
+            if (nq > 0) {
+                mbar_wait(&bars[PB_ACCDONE], kit & 1);
+                if (trl) TRP(4 + hf, g, 5);
+                tc_after_sync();
+#pragma unroll
+                for (int c = 0; c < D / 64; ++c) {
+                    tmem_ld32(tDV + lane_off + hf * (D / 2) + c * 32, dv + c * 32);
+                    tmem_ld32(tDK + lane_off + hf * (D / 2) + c * 32, dk + c * 32);
+                }
+                tmem_wait_ld();
+                tc_before_sync();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(lead(PB_ACCEMPTY));
+                ++kit;
+            } else {
+#pragma unroll
+                for (int e2 = 0; e2 < D / 2; ++e2) dv[e2] = dk[e2] = 0.f;
+            }
+            if (key < 0) continue;
+#pragma unroll
+            for (int e2 = 0; e2 < D / 2; e2 += 8) {
+                const int64_t po = part_off<D>(a, b, h, key, (hf * (D / 2) + e2) >> 3);
+                uint4 x, y;
+                x.x = pack_bf16(dk[e2] * a.scale, dk[e2 + 1] * a.scale);
+                x.y = pack_bf16(dk[e2 + 2] * a.scale, dk[e2 + 3] * a.scale);
+                x.z = pack_bf16(dk[e2 + 4] * a.scale, dk[e2 + 5] * a.scale);
+                x.w = pack_bf16(dk[e2 + 6] * a.scale, dk[e2 + 7] * a.scale);
+                y.x = pack_bf16(dv[e2], dv[e2 + 1]);
+                y.y = pack_bf16(dv[e2 + 2], dv[e2 + 3]);
+                y.z = pack_bf16(dv[e2 + 4], dv[e2 + 5]);
+                y.w = pack_bf16(dv[e2 + 6], dv[e2 + 7]);
+                *reinterpret_cast<uint4*>(a.dk_acc + po) = x;
+                *reinterpret_cast<uint4*>(a.dv_acc + po) = y;
+            }
+        }
+    }
+    tc_before_sync();
+    cluster_sync_all();
+    tc_after_sync();
+    if (warp == kMmaWarp) tmem_dealloc_pair<512>(tmem);
+#undef TRP
 }
 
 // ------------------------------------------------------------------ dQ
@@ -2002,11 +2447,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_p(const __grid_constant_
             (void)tr0;
             auto sdp = [&](int J) {  // S_J = Q K_J^T (TS), dP_J = dO V_J^T (SS)
                 const int ks = J % kNS;
-                mbar_wait(&bars[QB_KVFULL + ks], (J / kNS) & 1);
-                mbar_wait(&bars[QB_VFULL + (J % kNV)], (J / kNV) & 1);
+                mbar_wait_fast(&bars[QB_KVFULL + ks], (J / kNS) & 1);
+                mbar_wait_fast(&bars[QB_VFULL + (J % kNV)], (J / kNV) & 1);
                 TRQ(3, J, 0);
                 fence_proxy_async();  // cp.async (generic proxy) rows -> tensor core reads
-                if (J >= 1) mbar_wait(&bars[QB_SEMPTY], (J - 1) & 1);
+                if (J >= 1) mbar_wait_fast(&bars[QB_SEMPTY], (J - 1) & 1);
                 tc_after_sync();
                 const uint32_t kb = sbase + SM::kK + ks * SM::kKT, vb = sbase + SM::kV + (J % kNV) * SM::kKT;
 #pragma unroll
@@ -2021,9 +2466,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_p(const __grid_constant_
             };
             auto dq = [&](int J, int jt, int itn) {  // dQ += dS_J K_J (TS)
                 const int ks = J % kNS;
-                mbar_wait(&bars[QB_DSFULL], J & 1);
+                mbar_wait_fast(&bars[QB_DSFULL], J & 1);
                 TRQ(3, J, 2);
-                if (jt == 0 && itn > 0) mbar_wait(&bars[QB_DQEMPTY], (itn - 1) & 1);
+                if (jt == 0 && itn > 0) mbar_wait_fast(&bars[QB_DQEMPTY], (itn - 1) & 1);
                 tc_after_sync();
                 const uint32_t kb = sbase + SM::kK + ks * SM::kKT;
 #pragma unroll
@@ -2037,9 +2482,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_p(const __grid_constant_
                 const Item I = item(wi);
                 if (it == 6) tr0 = J;
                 const int n = I.n;
-                mbar_wait(&bars[QB_QFULL], it & 1);
+                mbar_wait_fast(&bars[QB_QFULL], it & 1);
                 TRQ(3, J, 3);
-                mbar_wait(&bars[QB_DOFULL], it & 1);
+                mbar_wait_fast(&bars[QB_DOFULL], it & 1);
                 TRQ(3, J, 4);
                 tc_after_sync();
                 sdp(J);
@@ -2305,6 +2750,12 @@ __global__ void __launch_bounds__(256) k_dq_convert(const float* __restrict__ ac
 // passes clip a key's queries to its own chunk (dK/dV never cross a chunk
 // start), while dQ and the gate-gradient row sums still collect from every
 // attended key (proj/src/attention.cpp:228-234, 284-300).
+// the selected pass on CTA pairs (D = 128), opt-in (SKB_BWD_PAIR=1): measured
+// slower than the one-CTA pass (2.28 vs 1.69 ms at cfg3), see k_bwd_dkdv_sel_pair
+inline bool sel_pair() {
+    static const int on = getenv("SKB_BWD_PAIR") ? atoi(getenv("SKB_BWD_PAIR")) : 0;
+    return on != 0;
+}
 inline bool fused_dq(int D, int chunk_len) {
     static const int fused = getenv("SKB_BWD_FUSEDQ") ? atoi(getenv("SKB_BWD_FUSEDQ")) : 0;
     return D == 128 && fused && chunk_len == 0;
@@ -2317,10 +2768,10 @@ void launch_bwd(const BwdArgs& a, const skb_attn_desc& d, cudaStream_t st) {
     static uint64_t attr = 0;
     if (first_on_device(&attr)) {
         set_smem(k_bwd_dkdv_tc<D, true, KS>, KSmem<D>::kAlloc);
-        set_smem(k_bwd_dkdv_sel_tc<D, KS, false>, KSmem<D>::kAlloc);
+        set_smem(k_bwd_dkdv_sel_tc<D, KS, false>, KSmem<D, kSelQS>::kAlloc);
         set_smem(k_bwd_dkdv_win_tc<D, false>, KWSmem<D>::kAlloc);
         if constexpr (kFQ) {
-            set_smem(k_bwd_dkdv_sel_tc<D, KS, true>, KSmem<D>::kAlloc);
+            set_smem(k_bwd_dkdv_sel_tc<D, KS, true>, KSmem<D, kQS, true>::kAlloc);
             set_smem(k_bwd_dkdv_win_tc<D, true>, KWSmem<D, 2, true>::kAlloc);
         }
         set_smem(k_bwd_dq_tc<D, KS>, QSmem<D>::kAlloc);
@@ -2342,10 +2793,19 @@ void launch_bwd(const BwdArgs& a, const skb_attn_desc& d, cudaStream_t st) {
             const int64_t items = (int64_t)ntk * d.heads * d.batch;
             const int grid = persist_grid(items);
             if constexpr (kFQ) {
-                if (fq) k_bwd_dkdv_sel_tc<D, KS, true><<<grid, kThreads, KSmem<D>::kAlloc, st>>>(a);
-                else k_bwd_dkdv_sel_tc<D, KS, false><<<grid, kThreads, KSmem<D>::kAlloc, st>>>(a);
+                if (fq) {
+                    k_bwd_dkdv_sel_tc<D, KS, true><<<grid, kThreads, KSmem<D, kQS, true>::kAlloc, st>>>(a);
+                } else if (sel_pair()) {
+                    const int64_t items2 = cdiv(a.L, 256) * d.heads * d.batch;
+                    const int npairs = (int)std::max<int64_t>(1, std::min<int64_t>(items2, persist_grid(items2 * 2) / 2));
+                    static uint64_t pattr = 0;
+                    if (first_on_device(&pattr)) set_smem(k_bwd_dkdv_sel_pair<D, KS>, PSmem<D>::kAlloc);
+                    k_bwd_dkdv_sel_pair<D, KS><<<2 * npairs, kThreads, PSmem<D>::kAlloc, st>>>(a);
+                } else {
+                    k_bwd_dkdv_sel_tc<D, KS, false><<<grid, kThreads, KSmem<D, kSelQS>::kAlloc, st>>>(a);
+                }
             } else {
-                k_bwd_dkdv_sel_tc<D, KS, false><<<grid, kThreads, KSmem<D>::kAlloc, st>>>(a);
+                k_bwd_dkdv_sel_tc<D, KS, false><<<grid, kThreads, KSmem<D, kSelQS>::kAlloc, st>>>(a);
             }
         } else {
             dim3 gs((unsigned)cdiv(a.T, 128), (unsigned)d.heads, (unsigned)d.batch);
@@ -2398,6 +2858,8 @@ void run_attn_bwd_tc(const skb_attn_desc& d, const void* q, const void* k, const
         a.tm_v64 = tmap_rows3d(v, d.batch, d.seq_len, HD, 64);
         a.tm_q64 = tmap_rows3d(q, d.batch, d.seq_len, HD, 64);
         a.tm_do64 = tmap_rows3d(dout, d.batch, d.seq_len, HD, 64);
+        a.tm_q32 = tmap_rows3d(q, d.batch, d.seq_len, HD, 32);
+        a.tm_do32 = tmap_rows3d(dout, d.batch, d.seq_len, HD, 32);
         a.tm_k128 = tmap_rows3d(k, d.batch, d.seq_len, HD, 128);
         a.tm_v128 = tmap_rows3d(v, d.batch, d.seq_len, HD, 128);
         a.tm_dk_st = tmap_groups4d(dk, d.batch, d.seq_len, HD, (int)d.head_dim / 16);

@@ -155,17 +155,17 @@ k_rank_leave(const double* __restrict__ u, int L, int T, int R1, int R2, int* __
 constexpr int kRankChunk = 1024;
 constexpr int kRankBeforeThreads = 256;  // keys per CTA sharing one staged score chunk
 __global__ void __launch_bounds__(kRankBeforeThreads)
-k_rank_before(const double* __restrict__ u, int L, int T, int* __restrict__ A) {
+k_rank_before(const double* __restrict__ u, int L, int T, int* __restrict__ A, int klo, int khi) {
     __shared__ __align__(16) double su[kRankChunk];
     const int b = blockIdx.z;
-    const int j0 = blockIdx.x * kRankBeforeThreads, c0 = blockIdx.y * kRankChunk;
-    if (c0 >= min(T, j0 + kRankBeforeThreads)) return;  // chunk entirely after the block's keys
+    const int j0 = klo + blockIdx.x * kRankBeforeThreads, c0 = blockIdx.y * kRankChunk;
+    if (c0 >= min(khi, j0 + kRankBeforeThreads)) return;  // chunk entirely after the block's keys
     const double* ub = u + (int64_t)b * L;
     const int n = min(kRankChunk, T - c0);
     for (int i = threadIdx.x; i < kRankChunk; i += kRankBeforeThreads) su[i] = i < n ? ub[c0 + i] : 0.0;
     __syncthreads();
     const int j = j0 + threadIdx.x;
-    if (j >= T) return;
+    if (j >= khi) return;
     const double uj = ub[j];
     const int stop = min(n, j - c0);
     int cnt = 0, ii = 0;
@@ -186,11 +186,11 @@ k_rank_before(const double* __restrict__ u, int L, int T, int* __restrict__ A) {
 // scores, the target position by a rank search in the crossing ballot.
 __global__ void __launch_bounds__(256)
 k_rank_after_warp(const double* __restrict__ u, int L, int T, int R1, int R2, int* __restrict__ leave1,
-                  int* __restrict__ leave2) {
+                  int* __restrict__ leave2, int klo, int khi) {
     const int b = blockIdx.y;
     const int lane = threadIdx.x & 31;
-    const int j = blockIdx.x * 8 + (threadIdx.x >> 5);
-    if (j >= T) return;
+    const int j = klo + blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (j >= khi) return;
     const double* ub = u + (int64_t)b * L;
     const double uj = ub[j];
     const int A = leave1[(int64_t)b * L + j];  // k_rank_before's counts
@@ -254,6 +254,8 @@ struct TauArgs {
     int L, T, R2;
     double k;
     int cap;  // power of two, smem capacity for the band
+    int nch;  // chunks per sequence (all of them; a launch may cover a range)
+    int c_off, c_end;  // this launch's chunk range [c_off, c_end)
 };
 
 __device__ void tau_chunk_tail(const TauArgs& a, int b, int chunk, const double* bz, double* P, int mcount,
@@ -495,14 +497,14 @@ __global__ void __launch_bounds__(kTauThreads) k_tau_chunks(TauArgs a) {
     extern __shared__ double smem[];
     // latest chunks first: their prefixes are the longest (the scans and the
     // band grow with t0), so they must not be left to a trailing partial wave
-    const int b = blockIdx.y, chunk = gridDim.x - 1 - blockIdx.x;
+    const int b = blockIdx.y, chunk = a.c_end - 1 - blockIdx.x;
     double* bz = smem;
     double* P = smem + a.cap;
     if (!tau_chunk(a, b, chunk, bz, P, a.cap, false)) {
         if (threadIdx.x == 0) {
             const int slot = atomicAdd(a.ovf_count, 1);
-            a.ovf_items[slot] = b * gridDim.x + chunk;
-            a.ovf_flag[b * gridDim.x + chunk] = 1;
+            a.ovf_items[slot] = b * a.nch + chunk;
+            a.ovf_flag[b * a.nch + chunk] = 1;
         }
     }
 }
@@ -523,8 +525,8 @@ __global__ void __launch_bounds__(kTauThreads) k_tau_segments(TauArgs a, int nch
     __shared__ double red_d[32];
     __shared__ double s_new[kChunk];
     __shared__ int s_lim[2];
-    const int b = blockIdx.y, seg = blockIdx.x;
-    const int c_lo = seg * seg_chunks, c_hi = min(nchunks, c_lo + seg_chunks);
+    const int b = blockIdx.y, seg = a.c_off / seg_chunks + blockIdx.x;
+    const int c_lo = seg * seg_chunks, c_hi = min(min(nchunks, a.c_end), c_lo + seg_chunks);
     int* fl = a.ovf_flag + (int64_t)b * nchunks;
     if (threadIdx.x == 0) {
         int f = -1, l = -1;
@@ -1024,9 +1026,9 @@ void run_select(const skb_attn_desc& d, const double* u, void* ws, cudaStream_t 
         if (rank2) {
             SKB_CHECK_CUDA(cudaMemsetAsync(leave1, 0, (size_t)B * L * sizeof(int), st));
             dim3 g1((unsigned)cdiv(T, kRankBeforeThreads), (unsigned)cdiv(T, kRankChunk), B);
-            k_rank_before<<<g1, kRankBeforeThreads, 0, st>>>(u, L, T, leave1);
+            k_rank_before<<<g1, kRankBeforeThreads, 0, st>>>(u, L, T, leave1, 0, T);
             SKB_CHECK_LAUNCH();
-            k_rank_after_warp<<<dim3((unsigned)cdiv(T, 8), B), 256, 0, st>>>(u, L, T, R1, R2, leave1, leave2);
+            k_rank_after_warp<<<dim3((unsigned)cdiv(T, 8), B), 256, 0, st>>>(u, L, T, R1, R2, leave1, leave2, 0, T);
         } else {
             k_rank_leave<<<g, kRankThreads, 0, st>>>(u, L, T, R1, R2, leave1, leave2);
         }
@@ -1048,6 +1050,9 @@ void run_select(const skb_attn_desc& d, const double* u, void* ws, cudaStream_t 
         a.T = T;
         a.R2 = R2;
         a.k = d.k;
+        a.nch = nch;
+        a.c_off = 0;
+        a.c_end = nch;
         const int cap_big = std::min(8192, next_pow2(std::max(T, 32)));
         // pass 1: a small band cap (many CTAs per SM) serves slope-dominated
         // scores, whose band is ~ceil(k) wide; wider bands spill to pass 2

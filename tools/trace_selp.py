@@ -19,21 +19,25 @@ o, lse, _ = ops.attn_fwd(q, k, v, u, cfg, sel=sel)
 for _ in range(2):
     ops.attn_bwd(q, k, v, o, do, lse, u, sel, cfg)
 torch.cuda.synchronize()
-buf = (ctypes.c_ulonglong * 4096)()
-_lib.load().skb_debug_trace_bwd(buf, 4096)
-t = np.array(buf, dtype=np.int64)
-names = {4: {9: "wS", 0: "S", 4: "PdS", 5: "accD", 6: "end"}, 6: {3: "fetched", 2: "KVgo", 1: "Qgo"},
-         7: {4: "KV", 0: "Q", 1: "SdP", 2: "PdS"}}
-names[5] = names[4]
-roles = {4: "WG0", 5: "WG1", 6: "PROD", 7: "MMA"}
-vals = [x for x in t[4 * 512:8 * 512] if x > 0]
-t0 = min(vals)
-for jt in range(32):
-    row = []
-    for r in (7, 4, 5, 6):
-        for ev, nm in names[r].items():
-            x = t[(r * 512 + jt * 16 + ev) & 4095]
-            if x > 0:
-                row.append(f"{roles[r]}.{nm}={x - t0}")
-    if row:
-        print(f"g{jt:2d}: " + " ".join(row))
+buf = (ctypes.c_ulonglong * 8192)()
+_lib.load().skb_debug_trace_bwd(buf, 8192)
+tt = np.array(buf, dtype=np.int64)
+for cta in (0, 1):
+    t = tt[cta * 4096:(cta + 1) * 4096]
+    if not (t > 0).any():
+        continue
+    print(f"== CTA {100 + cta}")
+    names = {4: {9: "wS", 0: "S", 4: "PdS", 5: "accD", 6: "end"}, 6: {3: "fetched", 2: "KVgo", 1: "Qgo"},
+             7: {4: "KV", 0: "Q", 1: "SdP", 2: "PdS"}}
+    names[5] = names[4]
+    roles = {4: "WG0", 5: "WG1", 6: "PROD", 7: "MMA"}
+    t0 = min(x for x in np.concatenate([tt[4 * 512:8 * 512], tt[4096 + 4 * 512:4096 + 8 * 512]]) if x > 0)
+    for jt in range(32):
+        row = []
+        for r in (7, 4, 5, 6):
+            for ev, nm in names[r].items():
+                x = t[(r * 512 + jt * 16 + ev) & 4095]
+                if x > 0:
+                    row.append(f"{roles[r]}.{nm}={x - t0}")
+        if row:
+            print(f"g{jt:2d}: " + " ".join(row))
