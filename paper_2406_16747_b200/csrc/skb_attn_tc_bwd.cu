@@ -1143,15 +1143,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_sel_tc(const __grid_co
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(&bars[KW_SFULL + s], 1);
-            mbar_init(&bars[KW_SEMPTY + s], kMath);
-            mbar_init(&bars[KW_PDSFULL + s], kMath);
+            mbar_init(&bars[KW_SEMPTY + s], kMathArrivals);
+            mbar_init(&bars[KW_PDSFULL + s], kMathArrivals);
         }
         mbar_init(&bars[KW_ACCDONE], 1);
-        mbar_init(&bars[KW_ACCEMPTY], kMath);
+        mbar_init(&bars[KW_ACCEMPTY], kMathArrivals);
         mbar_init(&bars[KW_DQFULL], 1);
         mbar_init(&bars[KW_DQFULL + 1], 1);
-        mbar_init(&bars[KW_DQEMPTY], kMath);
-        mbar_init(&bars[KW_DQEMPTY + 1], kMath);
+        mbar_init(&bars[KW_DQEMPTY], kMathArrivals);
+        mbar_init(&bars[KW_DQEMPTY + 1], kMathArrivals);
         mbar_fence_init();
     }
     if (warp == kMmaWarp) tmem_alloc<512>(tmem_slot);
@@ -1333,9 +1333,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_sel_tc(const __grid_co
                 tmem_ld32(tP + lane_off + s * 64 + hf * 32, dp);
                 tmem_wait_ld();
                 tc_before_sync();
-                mbar_arrive(&bars[KW_SEMPTY + s]);  // fused dQ: the dP^T half is released after its dQ^T is read
+                if (FQ) warp_arrive(&bars[KW_SEMPTY + s]);  // fused dQ: the dP^T half is released after its dQ^T is read
                 if (SKB_BWD_EXP == 1 && !FQ) {
-                    mbar_arrive(&bars[KW_PDSFULL + s]);
+                    warp_arrive(&bars[KW_PDSFULL + s]);
                     continue;
                 }
                 const float* ml = qmeta + (qs3 * 3) * 64 + hf * 32;
@@ -1466,14 +1466,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_sel_tc(const __grid_co
                     tmem_wait_st();
                     tc_before_sync();
                     if (trl) TRS(4 + hf, g, 4);
-                    mbar_arrive(&bars[KW_PDSFULL + s]);
+                    warp_arrive(&bars[KW_PDSFULL + s]);
                     if (qt > 0) {  // the previous tile's dQ^T -> the fp32 accumulator
                         tc_after_sync();
                         float qv[32];
                         tmem_ld32(tP + lane_off + sp * 64 + hf * 32, qv);
                         tmem_wait_ld();
                         tc_before_sync();
-                        mbar_arrive(&bars[KW_DQEMPTY + sp]);
+                        warp_arrive(&bars[KW_DQEMPTY + sp]);
                         dq_reduce<D>(a, b, h, qs - 64, r, qv, reinterpret_cast<float*>(smem + SM::kStage) + warp * 512);
                     }
                 } else {
@@ -1487,7 +1487,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_sel_tc(const __grid_co
                     tmem_wait_st();
                     tc_before_sync();
                     if (trl) TRS(4 + hf, g, 4);
-                    mbar_arrive(&bars[KW_PDSFULL + s]);
+                    warp_arrive(&bars[KW_PDSFULL + s]);
                 }
             }
             if constexpr (FQ) {
@@ -1499,7 +1499,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_sel_tc(const __grid_co
                     tmem_ld32(tP + lane_off + sp * 64 + hf * 32, qv);
                     tmem_wait_ld();
                     tc_before_sync();
-                    mbar_arrive(&bars[KW_DQEMPTY + sp]);
+                    warp_arrive(&bars[KW_DQEMPTY + sp]);
                     dq_reduce<D>(a, b, h, q_lo + (nq - 1) * 64 + hf * 32, r, qv, reinterpret_cast<float*>(smem + SM::kStage) + warp * 512);
                 }
             }
@@ -1516,7 +1516,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_sel_tc(const __grid_co
                 }
                 tmem_wait_ld();
                 tc_before_sync();
-                mbar_arrive(&bars[KW_ACCEMPTY]);
+                warp_arrive(&bars[KW_ACCEMPTY]);
                 ++kit;
             } else {
 #pragma unroll

@@ -70,18 +70,14 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
 }
 // Wait for the phase with the given parity to complete. A wait that never
 // completes (a pipeline bug) traps after ~seconds instead of hanging the GPU.
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+__device__ __forceinline__ void mbar_wait_slow(uint64_t* bar, uint32_t parity) {
     const uint32_t addr = smem_u32(bar);
     uint32_t spins = 0;
     while (!mbar_try_wait(addr, parity)) {
         if (++spins > (1u << 26)) __trap();
     }
 }
-// The MMA-issuing thread's wait: a non-blocking test first. A try_wait costs
-// the single issuing thread ~150 cycles even on a completed phase, ~3x a
-// test_wait (tools/probes/mma_rate.cu), and the thread's time between MMA
-// groups is tensor-pipe idle time when its queue has drained.
-__device__ __forceinline__ void mbar_wait_fast(uint64_t* bar, uint32_t parity) {
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
     uint32_t ok;
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
@@ -90,7 +86,22 @@ __device__ __forceinline__ void mbar_wait_fast(uint64_t* bar, uint32_t parity) {
         : "=r"(ok)
         : "r"(smem_u32(bar)), "r"(parity)
         : "memory");
-    if (!ok) mbar_wait(bar, parity);
+    return ok != 0;
+}
+// A try_wait costs ~150 cycles even on a completed phase, ~3x a test_wait
+// (tools/probes/mma_rate.cu): every wait tests first. On the single
+// MMA-issuing thread that time is tensor-pipe idle time once its queue drains.
+#ifndef SKB_WAIT_TEST_FIRST
+#define SKB_WAIT_TEST_FIRST 1
+#endif
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    if (SKB_WAIT_TEST_FIRST && mbar_test(bar, parity)) return;
+    mbar_wait_slow(bar, parity);
+}
+// (kept for the call sites on MMA-issuing threads)
+__device__ __forceinline__ void mbar_wait_fast(uint64_t* bar, uint32_t parity) {
+    if (SKB_WAIT_TEST_FIRST && mbar_test(bar, parity)) return;
+    mbar_wait_slow(bar, parity);
 }
 // cp.async completion of this thread's prior copies arrives on the barrier.
 __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
@@ -339,6 +350,20 @@ constexpr int kMath = 256;
 constexpr int kProducers = 96;
 constexpr int kProdWarp0 = 8;
 constexpr int kMmaWarp = 11;
+// One arrival per warp (barrier count = warps): the warp's lanes order their
+// prior work (tcgen05 fences included) before lane 0's release-arrive.
+#ifndef SKB_WARP_ARRIVE
+#define SKB_WARP_ARRIVE 1
+#endif
+constexpr int kMathArrivals = SKB_WARP_ARRIVE ? kMath / 32 : kMath;  // math-warp arrivals per phase
+__device__ __forceinline__ void warp_arrive(uint64_t* bar) {
+    if (!SKB_WARP_ARRIVE) {
+        mbar_arrive(bar);
+        return;
+    }
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(bar);
+}
 
 // Named barrier over the 256 math threads (id 1; 0 is __syncthreads).
 __device__ __forceinline__ void math_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
