@@ -81,6 +81,8 @@ struct BwdArgs {
     float* dq32;      // fused dQ: fp32 [B, L, H, D] accumulator of dS K (unscaled), reduced into by the key-major passes
     int2* sel_items;  // [B][cdiv(L,128)] {q_lo, nq} of the selected pass's key tiles
     int* sel_order;   // [B][L] ever-selected keys grouped by leave time (the selected pass's order)
+    int* uni_hi;      // [B][cdiv(L,128)] query end of each contiguous key tile (unified pass)
+    int uni;          // 1: dense sequences take the unified key-major pass (k_bwd_dkdv_win_tc<.., UNI>)
     int nqb, qb_cap;
     int B, L, H, w, T, R1;
     float scale, scale_log2;
@@ -513,7 +515,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_tc(const __grid_consta
 // tiles load while the current item finishes its last dV/dK MMAs and its
 // epilogue; K/V are released by the commit of an item's last S/dP MMA, the
 // dV/dK accumulators by the math warps once they are read out.
-template <int D, int QS = kQS, bool FQ = false>
+template <int D, int QS = kQS, bool FQ = false, bool UNI = false>
 struct KWSmem {
     static constexpr int kKV = 128 * D * 2;
     static constexpr int kQT = 64 * D * 2;
@@ -522,11 +524,11 @@ struct KWSmem {
     static constexpr int kQ = kV + kKV;           // [QS]
     static constexpr int kDO = kQ + QS * kQT;     // [QS]
     static constexpr int kPart = kDO + QS * kQT;  // dK then dV partials of the tile (part_off order);
-    static constexpr int kPartB = 128 * D * 2;    //   the epilogue stages its bf16 rows in place
+    static constexpr int kPartB = UNI ? 0 : 128 * D * 2;  //   the epilogue stages its bf16 rows in place
     static constexpr int kDS = kPart + 2 * kPartB;         // fused dQ: dS^T of the tile, 128 keys x 64 queries
     static constexpr int kStage = kDS + (FQ ? 128 * 64 * 2 : 0);  // fused dQ: per-warp 16 x 32 fp32 transpose
-    static constexpr int kMeta = kStage + (FQ ? 8 * 2048 : 0);       // [QS][lse2|delta][64] f32
-    static constexpr int kBar = kMeta + QS * 2 * 64 * 4;
+    static constexpr int kMeta = kStage + (FQ ? 8 * 2048 : 0);       // [QS][lse2|delta(|tau)][64] f32
+    static constexpr int kBar = kMeta + QS * (UNI ? 3 : 2) * 64 * 4;
     static constexpr int kTmemSlot = kBar + 24 * 8;
     static constexpr int kAlloc = kTmemSlot + 16 + 1024;
     static_assert(kAlloc <= 232448, "smem");
@@ -592,10 +594,45 @@ __device__ __forceinline__ void ds_store(uint32_t ds_base, int r, int hf, const 
 // and the finished dK/dV rows out
 constexpr int kWinQProd = 64;
 
-template <int D, bool FQ>
+// The unified pass's elementwise step where some columns are gated: the
+// selected pass's arithmetic with gate 1 on the window columns c < cwc (which
+// makes them plain softmax-backward columns with no gate-gradient term).
+__device__ __forceinline__ float uni_frac_math(const BwdArgs& a, float uj, int cwc, const float* ml, const float* md,
+                                               const float* mt, float2 sl22, float* sv, float* dp) {
+    float2 csum2 = make_float2(0.f, 0.f);
+    const bool mst = a.mask_st != 0;
+#pragma unroll
+    for (int c = 0; c < 32; c += 2) {
+        const float2 l2 = *reinterpret_cast<const float2*>(ml + c);
+        const float2 d2 = *reinterpret_cast<const float2*>(md + c);
+        const float2 t2 = *reinterpret_cast<const float2*>(mt + c);
+        const float g0 = c < cwc ? 1.f : __saturatef(uj - t2.x);
+        const float g1 = c + 1 < cwc ? 1.f : __saturatef(uj - t2.y);
+        float2 p2 = __ffma2_rn(make_float2(sv[c], sv[c + 1]), sl22, make_float2(-l2.x, -l2.y));
+        p2.x = ex2(p2.x);  // masked: 0
+        p2.y = ex2(p2.y);
+        const float2 dp2 = make_float2(dp[c], dp[c + 1]);
+        const float2 nd2 = make_float2(-d2.x, -d2.y);
+        const float2 g2 = mst ? make_float2(1.f, 1.f) : make_float2(g0, g1);
+        const float2 cc2 = __fmul2_rn(p2, __ffma2_rn(g2, dp2, nd2));
+        const float2 fr2 = make_float2((__float_as_uint(g0) - 1u) < 0x3F7FFFFFu ? 1.f : 0.f,
+                                       (__float_as_uint(g1) - 1u) < 0x3F7FFFFFu ? 1.f : 0.f);
+        csum2 = __fadd2_rn(csum2, __fmul2_rn(__fmul2_rn(p2, dp2), fr2));
+        const float2 pw2 = __fmul2_rn(p2, g2);
+        sv[c] = pw2.x, sv[c + 1] = pw2.y;  // P~^T
+        dp[c] = cc2.x, dp[c + 1] = cc2.y;  // dS^T (scale applied in the epilogue)
+    }
+    return csum2.x + csum2.y;
+}
+
+template <int D, bool FQ, bool UNI = false>
 __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_win_tc(const __grid_constant__ BwdArgs a) {
-    constexpr int QS = FQ ? 2 : kQS;  // the fused-dQ build gives one Q/dO stage to the dS^T tile
-    using SM = KWSmem<D, QS, FQ>;
+    // the fused-dQ build gives one Q/dO stage to the dS^T tile; the unified
+    // pass has no partial buffer and spends it on a fourth stage
+    constexpr int QS = FQ ? 2 : (UNI ? 4 : kQS);
+    constexpr int kMN = UNI ? 3 : 2;  // per-query metadata arrays: lse2, delta (, tau)
+    using SM = KWSmem<D, QS, FQ, UNI>;
+    static_assert(!(UNI && FQ), "unified pass: no fused dQ");
     extern __shared__ __align__(16) uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const uint32_t sbase = smem_u32(smem);
@@ -618,18 +655,29 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_win_tc(const __grid_co
     const int nitems = ntk * a.H * a.B;
     // the queries reading key tile kt: [j0, hi) with hi = max over its keys of
     // min(key + w, chunk end) — both nondecreasing in key, so the last key's
-    auto item = [&](int wi, int& b, int& h, int& j0, int& nkeys, int& nq) {
+    // (unified pass: the window and the selection of every key of the tile,
+    // [j0, uni_hi) — dense sequences only; the window pass then skips them)
+    auto item = [&](int wi, int& b, int& h, int& j0, int& nkeys, int& nq) -> bool {
         const int kt = wi % ntk;
         const int bh = wi / ntk;
         h = bh % a.H;
         b = bh / a.H;
         j0 = kt * 128;
         nkeys = min(128, a.L - j0);
+        if (UNI || a.uni) {
+            const bool dense = 2 * __ldg(a.ever_count + b) > a.T;
+            if (dense != UNI) return false;
+            if (UNI) {
+                nq = (__ldg(a.uni_hi + b * ntk + kt) - j0 + 63) / 64;
+                return true;
+            }
+        }
         const int jl = j0 + nkeys - 1;
         int hi = jl + a.w;
         if (a.chunk_len > 0) hi = min(hi, (jl / a.chunk_len + 1) * a.chunk_len);
         hi = min(a.L, max(hi, jl + 1));
         nq = (hi - j0 + 63) / 64;
+        return true;
     };
     if (threadIdx.x == 0) {
         mbar_init(&bars[KW_KVFULL], 1);
@@ -661,6 +709,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_win_tc(const __grid_co
     const uint32_t tS = tmem, tP = tmem + 128, tDV = tmem + 256, tDK = tmem + 384;
 
     if (warp == kMmaWarp - 1) {
+        if (UNI) {  // no partials, the math warps store their rows
+        } else
         // the math warps stage tile n's bf16 rows (part_off order) in the
         // partial buffer; this lane stores them (one TMA store per 32-key
         // group and half), waits for the reads, then loads tile n+1's partials
@@ -682,7 +732,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_win_tc(const __grid_co
             };
             for (int wi = blockIdx.x; wi < nitems; wi += gridDim.x, ++it) {
                 int b, h, j0, nkeys, nq;
-                item(wi, b, h, j0, nkeys, nq);
+                if (!item(wi, b, h, j0, nkeys, nq)) {
+                    --it;
+                    continue;
+                }
                 if (it > 0) store_prev(it - 1);
                 pb_ = b, pj0 = j0, pnk = nkeys, ph = h;
                 if (tile_sel(j0)) {
@@ -705,7 +758,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_win_tc(const __grid_co
         int g = 0, it = 0, tr0 = 1 << 20;
         for (int wi = blockIdx.x; wi < nitems; wi += gridDim.x, ++it) {
             int b, h, j0, nkeys, nq;
-            item(wi, b, h, j0, nkeys, nq);
+            if (!item(wi, b, h, j0, nkeys, nq)) {
+                --it;
+                continue;
+            }
             if (it == 20) tr0 = g;
             if (ptid == 0) {
                 if (it > 0) mbar_wait(&bars[KW_KVEMPTY], (it - 1) & 1);
@@ -719,6 +775,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_win_tc(const __grid_co
             }
             const float* lse2 = a.lse2 + ((int64_t)b * a.H + h) * a.L;
             const float* dlt = a.delta + ((int64_t)b * a.H + h) * a.L;
+            const int64_t bl = (int64_t)b * a.L;
             for (int qt = 0; qt < nq; ++qt, ++g) {
                 const int s = g % QS;
                 if (ptid == 0) TRW(6, g, 0);
@@ -729,9 +786,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_win_tc(const __grid_co
                     const int c = ptid;
                     const int i = qs + c;
                     const bool ok = i < a.L;
-                    const uint32_t mb = smem_u32(qmeta + (s * 2) * 64 + c);
+                    const uint32_t mb = smem_u32(qmeta + (s * kMN) * 64 + c);
                     cp_async4(mb, lse2 + (ok ? i : 0), ok);
                     cp_async4(mb + 64 * 4, dlt + (ok ? i : 0), ok);
+                    if (UNI) {
+                        const int t = i - a.w;
+                        cp_async4(mb + 128 * 4, a.tauf + bl + (ok && t >= 0 ? t : 0), ok && t >= 0);
+                    }
                 }
                 cp_async_arrive_noinc(&bars[KW_QDFULL + s]);
                 if (ptid == 0) {
@@ -791,7 +852,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_win_tc(const __grid_co
             };
             for (int wi = blockIdx.x; wi < nitems; wi += gridDim.x, ++it) {
                 int b, h, j0, nkeys, nq;
-                item(wi, b, h, j0, nkeys, nq);
+                if (!item(wi, b, h, j0, nkeys, nq)) {
+                    --it;
+                    continue;
+                }
                 if (it == 20) tr0 = g;
                 mbar_wait_fast(&bars[KW_KVFULL], it & 1);
                 TRW(7, g, 4);
@@ -846,7 +910,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_win_tc(const __grid_co
         const bool trl = lane == 0 && (warp & 3) == 0;
         for (int wi = blockIdx.x; wi < nitems; wi += gridDim.x, ++it) {
             int b, h, j0, nkeys, nq;
-            item(wi, b, h, j0, nkeys, nq);
+            if (!item(wi, b, h, j0, nkeys, nq)) {
+                --it;
+                continue;
+            }
             if (it == 20) tr0 = g;
             const int64_t bl = (int64_t)b * a.L;
             const int key = r < nkeys ? j0 + r : -1;
@@ -855,7 +922,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_win_tc(const __grid_co
             // the key's chunk (proj/src/attention.cpp:228-234, 284-300)
             int hi_i = min(a.L, key + a.w);
             if (a.chunk_len > 0 && key >= 0) hi_i = min(hi_i, (key / a.chunk_len + 1) * a.chunk_len);
-            const bool has_sel = key >= 0 && key < a.T && tile_sel(j0) && __ldg(a.leave + bl + key) > key;
+            const bool has_sel = !UNI && key >= 0 && key < a.T && tile_sel(j0) && __ldg(a.leave + bl + key) > key;
+            // unified pass: the key's selection follows its window, queries
+            // [key + w, leave + w) (proj/src/cache.cpp:259-311), gated
+            bool sel_u = false;
+            float uj = 0.f, colsum = 0.f;
+            if (UNI && key >= 0 && key < a.T && a.R1 > 0) {
+                const int lv = __ldg(a.leave + bl + key);
+                sel_u = lv > key;
+                if (sel_u) {
+                    hi_i = min(a.L, lv + a.w);
+                    uj = __ldg(a.uf + bl + key);
+                }
+            }
             for (int qt = 0; qt < nq; ++qt, ++g) {
                 const int s = g & 1, qs3 = g % QS;
                 const int qs = j0 + qt * 64 + hf * 32;
@@ -870,7 +949,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_win_tc(const __grid_co
                 tmem_wait_ld();
                 tc_before_sync();
                 mbar_arrive(&bars[KW_SEMPTY + s]);  // fused dQ: the dP^T half is released after its dQ^T is read
-                const float* ml = qmeta + (qs3 * 2) * 64 + hf * 32;
+                const float* ml = qmeta + (qs3 * kMN) * 64 + hf * 32;
                 const float* md = ml + 64;
                 const int cmin = key >= 0 ? key - qs : 32;
                 const int cmax = key >= 0 ? hi_i - 1 - qs : -1;
@@ -878,6 +957,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_win_tc(const __grid_co
 #pragma unroll
                     for (int c = 0; c < 32; ++c) sv[c] = (c >= cmin && c <= cmax) ? sv[c] : -INFINITY;
                 }
+                bool plain = true;
+                if constexpr (UNI) {
+                    // columns c < cwc read the key from the window (gate 1); the
+                    // rest from the selection, all gates 1 once u_j >= tau + 1
+                    // over the tile's last query (tau nondecreasing)
+                    const float* mt = ml + 128;
+                    const int cwc = key + a.w - qs;
+                    const int clast = max(0, min(31, a.L - 1 - qs));
+                    plain = __all_sync(0xffffffffu, !sel_u || cwc > 31 || uj >= mt[clast] + 1.f);
+                    if (!plain) colsum += uni_frac_math(a, uj, cwc, ml, md, mt, sl22, sv, dp);
+                }
+                if (plain)
 #pragma unroll
                 for (int c = 0; c < 32; c += 4) {  // gates 1: plain softmax backward, packed fp32x2
                     const float4 l4 = *reinterpret_cast<const float4*>(ml + c);
@@ -958,6 +1049,26 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_win_tc(const __grid_co
             mbar_arrive(&bars[KW_ACCEMPTY]);
 #pragma unroll
             for (int e = 0; e < D / 2; ++e) dk[e] *= a.scale;
+            if constexpr (UNI) {  // final rows, straight from registers (no partials)
+                if (key < 0) continue;
+                if (colsum != 0.f) atomicAdd(a.colsum + bl + key, (double)colsum);
+                const int64_t ro = (((int64_t)b * a.L + key) * a.H + h) * D + hf * (D / 2);
+#pragma unroll
+                for (int e = 0; e < D / 2; e += 8) {
+                    uint4 x, y;
+                    x.x = pack_bf16(dk[e], dk[e + 1]);
+                    x.y = pack_bf16(dk[e + 2], dk[e + 3]);
+                    x.z = pack_bf16(dk[e + 4], dk[e + 5]);
+                    x.w = pack_bf16(dk[e + 6], dk[e + 7]);
+                    y.x = pack_bf16(dv[e], dv[e + 1]);
+                    y.y = pack_bf16(dv[e + 2], dv[e + 3]);
+                    y.z = pack_bf16(dv[e + 4], dv[e + 5]);
+                    y.w = pack_bf16(dv[e + 6], dv[e + 7]);
+                    *reinterpret_cast<uint4*>(a.dk + ro + e) = x;
+                    *reinterpret_cast<uint4*>(a.dv + ro + e) = y;
+                }
+                continue;
+            }
             // + the selected pass's partials (bulk-copied to smem in part_off
             // order: 32-key groups of [D/8][32][8]); the bf16 result is staged in
             // place and stored by the warpgroup as contiguous 16-byte row chunks
@@ -1091,6 +1202,24 @@ __global__ void k_sel_items(BwdArgs a, int ntk) {
     if (lane == 0) a.sel_items[wid] = res;
 }
 
+// The unified pass's query end per contiguous 128-key tile: max over its keys
+// of max(key, leave) + w (window, then selection), at least one query tile.
+__global__ void __launch_bounds__(128) k_uni_items(BwdArgs a, int ntk) {
+    __shared__ int wmax[4];
+    const int kt = blockIdx.x, b = blockIdx.y, j0 = kt * 128, j = j0 + threadIdx.x;
+    int hi = 0;
+    if (j < a.L) {
+        int lv = j;
+        if (j < a.T && a.R1 > 0) lv = max(j, __ldg(a.leave + (int64_t)b * a.L + j));
+        hi = min(a.L, lv + a.w);
+    }
+    hi = warp_max_i(hi);
+    if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = hi;
+    __syncthreads();
+    if (threadIdx.x == 0)
+        a.uni_hi[b * ntk + kt] = max(max(max(wmax[0], wmax[1]), max(wmax[2], wmax[3])), j0 + 1);
+}
+
 // Selected pass, persistent: work item = (128-entry tile of the ever-selected
 // list, head); the rings run across items as in the window pass, so the next
 // tile's row gathers and first query tiles load under the current tile's last
@@ -1128,6 +1257,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_sel_tc(const __grid_co
         b = bh / a.H;
         const int ec = __ldg(a.ever_count + b);
         if (kt * 128 >= ec) return false;
+        if (a.uni && 2 * ec > a.T) return false;  // the unified pass has it
         nkeys = min(128, ec - kt * 128);
         const int2 info = a.sel_items[b * ntk + kt];
         q_lo = info.x;
@@ -1708,6 +1838,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         b = bh / a.H;
         const int ec = __ldg(a.ever_count + b);
         if (kt2 * 256 >= ec) return false;
+        if (a.uni && 2 * ec > a.T) return false;
         const int n0 = min(128, ec - kt2 * 256), n1 = max(0, min(128, ec - kt2 * 256 - 128));
         nkeys = rank ? n1 : n0;
         int lo = INT_MAX, hi = 0;
@@ -2756,20 +2887,30 @@ inline bool sel_pair() {
     static const int on = getenv("SKB_BWD_PAIR") ? atoi(getenv("SKB_BWD_PAIR")) : 0;
     return on != 0;
 }
+// unified key-major pass for sequences whose ever-selected set is dense
+// (SKB_BWD_UNI=0: the selected + window passes for every sequence)
+inline bool uni_pass() {
+    static const int on = getenv("SKB_BWD_UNI") ? atoi(getenv("SKB_BWD_UNI")) : 1;
+    return on != 0;
+}
 inline bool fused_dq(int D, int chunk_len) {
     static const int fused = getenv("SKB_BWD_FUSEDQ") ? atoi(getenv("SKB_BWD_FUSEDQ")) : 0;
     return D == 128 && fused && chunk_len == 0;
 }
 
 template <int D, bool KS>
-void launch_bwd(const BwdArgs& a, const skb_attn_desc& d, cudaStream_t st) {
+void launch_bwd(const BwdArgs& a0, const skb_attn_desc& d, cudaStream_t st) {
     constexpr bool kFQ = D == 128;
+    BwdArgs a = a0;
     const bool fq = fused_dq(D, a.chunk_len);
+    static const int persist_sel = getenv("SKB_SEL_PERSIST") ? atoi(getenv("SKB_SEL_PERSIST")) : 1;
+    a.uni = (uni_pass() && !KS && !fq && persist_sel && !sel_pair() && a.chunk_len == 0 && a.R1 > 0 && a.T > 0) ? 1 : 0;
     static uint64_t attr = 0;
     if (first_on_device(&attr)) {
         set_smem(k_bwd_dkdv_tc<D, true, KS>, KSmem<D>::kAlloc);
         set_smem(k_bwd_dkdv_sel_tc<D, KS, false>, KSmem<D, kSelQS>::kAlloc);
         set_smem(k_bwd_dkdv_win_tc<D, false>, KWSmem<D>::kAlloc);
+        set_smem(k_bwd_dkdv_win_tc<D, false, true>, KWSmem<D, 4, false, true>::kAlloc);
         if constexpr (kFQ) {
             set_smem(k_bwd_dkdv_sel_tc<D, KS, true>, KSmem<D, kQS, true>::kAlloc);
             set_smem(k_bwd_dkdv_win_tc<D, true>, KWSmem<D, 2, true>::kAlloc);
@@ -2790,6 +2931,13 @@ void launch_bwd(const BwdArgs& a, const skb_attn_desc& d, cudaStream_t st) {
             SKB_CHECK_LAUNCH();
             k_sel_items<<<(unsigned)cdiv((int64_t)a.B * ntk * 32, 256), 256, 0, st>>>(a, ntk);
             SKB_CHECK_LAUNCH();
+            if (a.uni) {  // dense sequences: window + selection in one key-major pass
+                k_uni_items<<<dim3((unsigned)ntk, (unsigned)a.B), 128, 0, st>>>(a, ntk);
+                SKB_CHECK_LAUNCH();
+                const int ug = persist_grid((int64_t)ntk * d.heads * d.batch);
+                k_bwd_dkdv_win_tc<D, false, true><<<ug, kThreads, KWSmem<D, 4, false, true>::kAlloc, st>>>(a);
+                SKB_CHECK_LAUNCH();
+            }
             const int64_t items = (int64_t)ntk * d.heads * d.batch;
             const int grid = persist_grid(items);
             if constexpr (kFQ) {
@@ -2893,6 +3041,8 @@ void run_attn_bwd_tc(const skb_attn_desc& d, const void* q, const void* k, const
     a.sel_items = reinterpret_cast<int2*>(base + bl.sel_items);
     a.dq32 = reinterpret_cast<float*>(base + bl.dq32);
     a.sel_order = reinterpret_cast<int*>(base + bl.sel_order);
+    a.uni_hi = reinterpret_cast<int*>(base + bl.uni_hi);
+    a.uni = 0;
     a.nqb = s.nqb;
     a.qb_cap = s.qb_cap;
     a.B = (int)d.batch;

@@ -64,7 +64,7 @@ struct SelView {
 SelView sel_view(const skb_attn_desc& d, const void* ws);
 
 struct BwdLayout {
-    uint64_t rowsum, colsum, mean_prefix, chunk_sums, dk_acc, dv_acc, dq_acc, sel_items, sel_order, dq32, total;
+    uint64_t rowsum, colsum, mean_prefix, chunk_sums, dk_acc, dv_acc, dq_acc, sel_items, sel_order, dq32, uni_hi, total;
 };
 void bwd_layout(const skb_attn_desc& d, BwdLayout& o);
 

@@ -145,6 +145,8 @@ void bwd_layout(const skb_attn_desc& d, BwdLayout& o) {
     o.sel_order = take(tc ? BL * 4 : 0);
     // fused dQ (D = 128): the fp32 dS K accumulator the key-major passes reduce into
     o.dq32 = take(tc && d.head_dim == 128 ? N * 4 : 0);
+    // unified key-major pass: the query end of every contiguous 128-key tile
+    o.uni_hi = take(tc ? (uint64_t)d.batch * ((d.seq_len + 127) / 128) * 4 : 0);
     o.total = off;
 }
 

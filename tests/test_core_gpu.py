@@ -319,6 +319,24 @@ def test_fused_dq_backward_opt_in(cuda, cap):
     assert r.returncode == 0, r.stdout + r.stderr
 
 
+@pytest.mark.parametrize("uni", ["0", "1"])
+def test_unified_and_two_pass_key_major_backward(cuda, uni):
+    """Dense sequences take the unified key-major pass (window + selection of a
+    contiguous key tile in one kernel, SKB_BWD_UNI=1, the default); SKB_BWD_UNI=0
+    keeps the selected + window passes with bf16 partials. Both against the
+    gather path, with capped persistent grids so every ring wraps (the recency
+    cases are dense, the iid ones sparse, the chunked one never unified)."""
+    import os
+    import subprocess
+    import sys
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    env = dict(os.environ, SKB_BWD_UNI=uni, SKB_MAX_CTAS="5")
+    r = subprocess.run([sys.executable, os.path.join(here, "scripts", "persist_check.py")], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
 @pytest.mark.parametrize("cap", ["2", "7"])
 def test_persistent_grids_many_items_per_cta(cuda, cap):
     """The persistent kernels with their grid capped (SKB_MAX_CTAS): each CTA
