@@ -2441,8 +2441,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_tc(const __grid_constant
     if (warp == kMmaWarp) tmem_dealloc<512>(tmem);
 }
 
-template <int D, bool KEY_SOFT>
-__global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_p(const __grid_constant__ BwdArgs a) {
+// NQ math warpgroups (2 or 4) each own 128/NQ of a tile's 128 key columns; with
+// four, every SMSP holds four math warps (the per-tile math is latency-bound
+// with two: TMEM loads, MUFU and the dependent packing hide better).
+template <int D, bool KEY_SOFT, int NQ>
+__global__ void __launch_bounds__((4 * NQ + 4) * 32, 1) k_bwd_dq_p(const __grid_constant__ BwdArgs a) {
+    constexpr int kMW = 4 * NQ;          // math warps
+    constexpr int kMT = kMW * 32;        // math threads
+    constexpr int kPW0 = kMW;            // first producer warp
+    constexpr int kMMA = kMW + 3;        // the MMA warp
+    constexpr int kColsT = 128 / NQ;     // key columns per math thread
+    constexpr int kQW = D / (2 * NQ);    // 32-bit words of Q per math thread (its share of the row)
+    static_assert(kQW == 16 || kQW == 32, "Q share");
     using SM = QSmem<D>;
     static_assert(QB_DQEMPTY < SM::kNumBars, "barrier slots");
     extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -2485,37 +2495,37 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_p(const __grid_constant_
     };
 
     if (threadIdx.x == 0) {
-        mbar_init(&bars[QB_QFULL], kMath);
+        mbar_init(&bars[QB_QFULL], kMT);
         mbar_init(&bars[QB_DOFULL], 1);
         for (int s = 0; s < kNS; ++s) {
             mbar_init(&bars[QB_KVFULL + s], kProducers + 1);
             mbar_init(&bars[QB_KVEMPTY + s], 1);
             mbar_init(&bars[QB_MFULL + s], kProducers);
-            mbar_init(&bars[QB_MEMPTY + s], kMath);
+            mbar_init(&bars[QB_MEMPTY + s], kMT);
         }
         for (int s = 0; s < kNV; ++s) {
             mbar_init(&bars[QB_VFULL + s], kProducers + 1);
             mbar_init(&bars[QB_VEMPTY + s], 1);
         }
         mbar_init(&bars[QB_SFULL], 1);
-        mbar_init(&bars[QB_SEMPTY], kMath);
-        mbar_init(&bars[QB_DSFULL], kMath);
+        mbar_init(&bars[QB_SEMPTY], kMT);
+        mbar_init(&bars[QB_DSFULL], kMT);
         mbar_init(&bars[QB_DSEMPTY], 1);
         mbar_init(&bars[QB_DQDONE], 1);
         mbar_init(&bars[QB_QDOEMPTY], 1);
-        mbar_init(&bars[QB_DQEMPTY], kMath);
+        mbar_init(&bars[QB_DQEMPTY], kMT);
         mbar_fence_init();
     }
-    if (warp == kMmaWarp) tmem_alloc<512>(tmem_slot);
+    if (warp == kMMA) tmem_alloc<512>(tmem_slot);
     tc_before_sync();
     __syncthreads();
     tc_after_sync();
     const uint32_t tmem = *tmem_slot;
     const uint32_t tQ = tmem, tDS = tmem + 64, tS = tmem + 128, tP = tmem + 256, tDQ = tmem + 384;
 
-    if (warp >= kProdWarp0 && warp < kMmaWarp) {
+    if (warp >= kPW0 && warp < kMMA) {
         constexpr int kAtoms = D / 64;
-        const int pw = warp - kProdWarp0, ptid = threadIdx.x - kProdWarp0 * 32;
+        const int pw = warp - kPW0, ptid = threadIdx.x - kPW0 * 32;
         const int ma = ptid >> 5, mc = ptid & 31;  // metadata: array x 16-byte chunk (96 threads)
         const int* msrc = ma == 0 ? a.qb_list : ma == 1 ? a.qb_leave : reinterpret_cast<const int*>(a.qb_uf);
         int J = 0, it = 0, tr0 = 1 << 28;
@@ -2570,7 +2580,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_p(const __grid_constant_
                 if (jt + 1 < n_sel) kcur.fetch(pw, lane, [&](int r) { return __ldg(list + (jt + 1) * 128 + r); });
             }
         }
-    } else if (warp == kMmaWarp) {
+    } else if (warp == kMMA) {
         if (lane == 0) {
             constexpr uint32_t id_s = umma_idesc(128, 128, false, false);
             constexpr uint32_t id_dq = umma_idesc(128, D, false, true);
@@ -2632,7 +2642,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_p(const __grid_constant_
             }
         }
         __syncwarp();
-    } else if (warp < kProdWarp0) {
+    } else if (warp < kPW0) {
         // query rows: two math warpgroups, each owning 64 of the 128 key columns
         const int hf = warp >> 2;
         const int r = ((warp & 3) << 5) | lane;
@@ -2641,15 +2651,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_p(const __grid_constant_
         // packed columns of its half of the row
         auto load_q = [&](const Item& I) {
             const int i = I.i0 + r;
-            const __nv_bfloat16* src = a.q + ((I.bl + (i < a.L ? i : 0)) * a.H + I.h) * D + hf * (D / 2);
-            uint32_t wq[D / 4];
+            const __nv_bfloat16* src = a.q + ((I.bl + (i < a.L ? i : 0)) * a.H + I.h) * D + hf * (D / NQ);
+            uint32_t wq[kQW];
 #pragma unroll
-            for (int c = 0; c < D / 16; ++c) {
+            for (int c = 0; c < kQW / 4; ++c) {
                 uint4 x = make_uint4(0u, 0u, 0u, 0u);
                 if (i < a.L) x = *reinterpret_cast<const uint4*>(src + c * 8);
                 wq[4 * c] = x.x, wq[4 * c + 1] = x.y, wq[4 * c + 2] = x.z, wq[4 * c + 3] = x.w;
             }
-            if constexpr (D == 128) tmem_st32u(tQ + lane_off + hf * 32, wq);
+            if constexpr (kQW == 32) tmem_st32u(tQ + lane_off + hf * 32, wq);
             else tmem_st16u(tQ + lane_off + hf * 16, wq);
             tmem_wait_st();
             tc_before_sync();
@@ -2669,9 +2679,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_p(const __grid_constant_
             const int ni = N.i0 + r;
             if (ni < a.L) {
                 const char* src =
-                    reinterpret_cast<const char*>(a.q + ((N.bl + ni) * a.H + N.h) * D + hf * (D / 2));
+                    reinterpret_cast<const char*>(a.q + ((N.bl + ni) * a.H + N.h) * D + hf * (D / NQ));
 #pragma unroll
-                for (int c = 0; c < D; c += 128) prefetch_l2(src + c);
+                for (int c = 0; c < 2 * D / NQ; c += 128) prefetch_l2(src + c);
             }
         }
         const int t = i - a.w;
@@ -2682,7 +2692,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_p(const __grid_constant_
         const float dlt = i < a.L ? a.delta[hl + i] : 0.f;
         const float sl2 = a.scale_log2;
         const float2 sl22 = make_float2(sl2, sl2), nl2 = make_float2(nlse2, nlse2), ndl = make_float2(-dlt, -dlt);
-        const int c0 = hf * 64;
+        const int c0 = hf * kColsT;
         float rsum = 0.f;
         for (int jt = 0; jt < n; ++jt, ++J) {
             const bool is_sel = jt < n_sel;
@@ -2692,11 +2702,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_p(const __grid_constant_
             mbar_wait(&bars[QB_MFULL + ks], (J / kNS) & 1);  // every phase observed (window tiles too)
             if (trl) TRQ(hf, J, 0);
             tc_after_sync();
-            float sv[64], dp[64];
-            tmem_ld32(tS + lane_off + c0, sv);
-            tmem_ld32(tS + lane_off + c0 + 32, sv + 32);
-            tmem_ld32(tP + lane_off + c0, dp);
-            tmem_ld32(tP + lane_off + c0 + 32, dp + 32);
+            float sv[kColsT], dp[kColsT];
+#pragma unroll
+            for (int c = 0; c < kColsT; c += 32) {
+                tmem_ld32(tS + lane_off + c0 + c, sv + c);
+                tmem_ld32(tP + lane_off + c0 + c, dp + c);
+            }
             tmem_wait_ld();
             tc_before_sync();
             mbar_arrive(&bars[QB_SEMPTY]);  // S/dP of the next tile may overwrite now
@@ -2708,7 +2719,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_p(const __grid_constant_
                 const int fl = tflags[ks * 4];
                 if (!(fl & 1)) {  // per-key interval mask j <= t < leave_j: (unsigned)(t - j) < leave_j - j
 #pragma unroll
-                    for (int c = 0; c < 64; c += 4) {
+                    for (int c = 0; c < kColsT; c += 4) {
                         const int4 kj = *reinterpret_cast<const int4*>(mk + c);
                         const int4 ex = *reinterpret_cast<const int4*>(ml + c);
                         sv[c + 0] = ((unsigned)(t - kj.x) < (unsigned)ex.x) ? sv[c + 0] : -INFINITY;
@@ -2725,7 +2736,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_p(const __grid_constant_
                             constexpr bool kMst = decltype(mst_c)::value;
                             float2 rs2 = make_float2(0.f, 0.f);
 #pragma unroll
-                            for (int c = 0; c < 64; c += 2) {
+                            for (int c = 0; c < kColsT; c += 2) {
                                 const float2 uu = *reinterpret_cast<const float2*>(mu + c);
                                 const float g0 = __saturatef(uu.x - tau_i), g1 = __saturatef(uu.y - tau_i);
                                 float2 p2 = __ffma2_rn(make_float2(sv[c], sv[c + 1]), sl22, nl2);
@@ -2748,7 +2759,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_p(const __grid_constant_
                         else frac_loop(std::false_type{});
                     } else {
 #pragma unroll
-                    for (int c = 0; c < 64; c += 4) {
+                    for (int c = 0; c < kColsT; c += 4) {
                         const float4 uu = *reinterpret_cast<const float4*>(mu + c);
                         const float ua[4] = {uu.x, uu.y, uu.z, uu.w};
 #pragma unroll
@@ -2773,14 +2784,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_p(const __grid_constant_
                 const int kb = jw0 + (jt - n_sel) * 128 + c0;
                 const int cmin = lo_win - kb;
                 const int cmax = i - kb;
-                if (__any_sync(0xffffffffu, cmin > 0 || cmax < 63)) {
+                if (__any_sync(0xffffffffu, cmin > 0 || cmax < kColsT - 1)) {
 #pragma unroll
-                    for (int c = 0; c < 64; ++c) sv[c] = (c >= cmin && c <= cmax) ? sv[c] : -INFINITY;
+                    for (int c = 0; c < kColsT; ++c) sv[c] = (c >= cmin && c <= cmax) ? sv[c] : -INFINITY;
                 }
             }
             if (plain) {  // all gates 1: plain softmax backward, packed fp32x2
 #pragma unroll
-                for (int c = 0; c < 64; c += 2) {
+                for (int c = 0; c < kColsT; c += 2) {
                     float2 x = __ffma2_rn(make_float2(sv[c], sv[c + 1]), sl22, nl2);
                     if ((c & 7) == 6 && kDqPoly) {  // one pair in four on the FMA pipe (MUFU relief)
                         x = ex2_poly2(x);
@@ -2799,11 +2810,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_p(const __grid_constant_
             {
                 uint32_t pk[16];
 #pragma unroll
-                for (int e = 0; e < 16; ++e) pk[e] = pack_bf16(dp[2 * e], dp[2 * e + 1]);
-                tmem_st16u(tDS + lane_off + hf * 32, pk);
+                for (int part = 0; part < kColsT / 32; ++part) {
 #pragma unroll
-                for (int e = 0; e < 16; ++e) pk[e] = pack_bf16(dp[32 + 2 * e], dp[33 + 2 * e]);
-                tmem_st16u(tDS + lane_off + hf * 32 + 16, pk);
+                    for (int e = 0; e < 16; ++e) pk[e] = pack_bf16(dp[32 * part + 2 * e], dp[32 * part + 2 * e + 1]);
+                    tmem_st16u(tDS + lane_off + hf * (kColsT / 2) + part * 16, pk);
+                }
                 tmem_wait_st();
             }
             tc_before_sync();
@@ -2818,16 +2829,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_p(const __grid_constant_
         if (trl) TRQ(hf, J - 1, 6);
         tc_after_sync();
         if (i < a.L && t >= 0 && a.R1 > 0 && rsum != 0.f) atomicAdd(a.rowsum + bl + t, (double)rsum);
-        __nv_bfloat16* orow = a.dq + ((bl + (i < a.L ? i : 0)) * a.H + h) * D + hf * (D / 2);
-        float xq[D / 2];
+        __nv_bfloat16* orow = a.dq + ((bl + (i < a.L ? i : 0)) * a.H + h) * D + hf * (D / NQ);
+        float xq[D / NQ];
 #pragma unroll
-        for (int c = 0; c < D / 64; ++c) tmem_ld32(tDQ + lane_off + hf * (D / 2) + c * 32, xq + c * 32);
+        for (int c = 0; c < D / (32 * NQ); ++c) tmem_ld32(tDQ + lane_off + hf * (D / NQ) + c * 32, xq + c * 32);
         tmem_wait_ld();
         tc_before_sync();
         mbar_arrive(&bars[QB_DQEMPTY]);
         if (trl) TRQ(hf, J - 1, 7);
 #pragma unroll
-        for (int c = 0; c < D / 64; ++c) {
+        for (int c = 0; c < D / (32 * NQ); ++c) {
             const float* x = xq + c * 32;
             if (i < a.L) {
 #pragma unroll
@@ -2846,7 +2857,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd_dq_p(const __grid_constant_
     tc_before_sync();
     __syncthreads();
     tc_after_sync();
-    if (warp == kMmaWarp) tmem_dealloc<512>(tmem);
+    if (warp == kMMA) tmem_dealloc<512>(tmem);
 #undef TRQ
 }
 
@@ -2916,7 +2927,8 @@ void launch_bwd(const BwdArgs& a0, const skb_attn_desc& d, cudaStream_t st) {
             set_smem(k_bwd_dkdv_win_tc<D, true>, KWSmem<D, 2, true>::kAlloc);
         }
         set_smem(k_bwd_dq_tc<D, KS>, QSmem<D>::kAlloc);
-        set_smem(k_bwd_dq_p<D, KS>, QSmem<D>::kAlloc);
+        set_smem(k_bwd_dq_p<D, KS, 2>, QSmem<D>::kAlloc);
+        if constexpr (D == 128) set_smem(k_bwd_dq_p<D, KS, 4>, QSmem<D>::kAlloc);
     }
     const int64_t ndq = (int64_t)a.B * a.L * a.H * D;
     if (fq) SKB_CHECK_CUDA(cudaMemsetAsync(a.dq32, 0, (size_t)ndq * sizeof(float), st));
@@ -2981,7 +2993,9 @@ void launch_bwd(const BwdArgs& a0, const skb_attn_desc& d, cudaStream_t st) {
     if (dq_persist) {
         const int64_t items = (int64_t)a.nqb * d.heads * d.batch;
         const int grid = persist_grid(items);
-        k_bwd_dq_p<D, KS><<<grid, kThreads, QSmem<D>::kAlloc, st>>>(a);
+        static const int quarters = getenv("SKB_DQ_QUARTERS") ? atoi(getenv("SKB_DQ_QUARTERS")) : 0;  // measured +1 %
+        if (D == 128 && quarters) k_bwd_dq_p<D, KS, (D == 128 ? 4 : 2)><<<grid, 20 * 32, QSmem<D>::kAlloc, st>>>(a);
+        else k_bwd_dq_p<D, KS, 2><<<grid, kThreads, QSmem<D>::kAlloc, st>>>(a);
     } else {
         dim3 gq((unsigned)a.nqb, (unsigned)d.heads, (unsigned)d.batch);
         k_bwd_dq_tc<D, KS><<<gq, kThreads, QSmem<D>::kAlloc, st>>>(a);
