@@ -60,6 +60,7 @@ struct BwdArgs {
     CUtensorMap tm_k64, tm_v64;
     CUtensorMap tm_q64, tm_do64;
     CUtensorMap tm_q32, tm_do32;  // 32-row boxes (the pair pass's per-CTA query halves)
+    CUtensorMap tm_q96, tm_do96;  // 96-row boxes (the unified pass's query tiles)
     CUtensorMap tm_k128, tm_v128;
     CUtensorMap tm_dk_st, tm_dv_st;  // 32-key group stores (tmap_groups4d)
     const __nv_bfloat16 *q, *k, *v, *dout;
@@ -1764,6 +1765,407 @@ __device__ __forceinline__ float sel_tile_math(const BwdArgs& a, bool sat, float
     return colsum;
 }
 
+// ------------------------------------------------------------ unified pass, 128-query tiles
+// The unified key-major pass (dense sequences, D = 128) with N = 128 query
+// tiles. A tcgen05.mma with N <= 128 costs the same ~64-75 cycles
+// (tools/probes/mma_rate.cu), so the 64-query tiles of the passes above run
+// their S^T/dP^T at half rate. Here one 128-column TMEM region R holds S^T and
+// then dP^T of a tile in turn (each read into registers by the math warps and
+// released at once), P~^T and dS^T (bf16) sit in a second 128-column region,
+// and dV/dK take the other 256 — 32 MMAs per 128 queries instead of 48:
+//   MMA:  S^T(g) -> R | dV,dK(g-1) | [R free] dP^T(g) -> R | [R free] S^T(g+1) ...
+//   math: [S(g)] P = exp2(S - lse), P~ = P g -> TMEM | [dP(g)] dS = P (g dP - delta) -> TMEM
+// The dV/dK MMAs of tile g-1 run while the math warps load S(g); P is kept in
+// registers (64 columns per thread) until dP arrives.
+// NQT = 128: two Q/dO stages (64 KB each) — a stage is busy from its load to
+// the tile's dV/dK, which follow the next tile's S^T, so two stages leave the
+// loads ~one tile of lead and the ring, not the MMAs, sets the period
+// (tools/trace_kmaj.py). NQT = 96: three 48 KB stages.
+template <int NQT>
+struct KQSmem {
+    static constexpr int kStages = NQT == 128 ? 2 : 3;
+    static constexpr int kKV = 128 * 128 * 2;  // 128 keys x 128 columns
+    static constexpr int kT = NQT * 128 * 2;   // NQT queries x 128 columns
+    static constexpr int kK = 0;
+    static constexpr int kV = kK + kKV;
+    static constexpr int kQ = kV + kKV;                  // [kStages]
+    static constexpr int kDO = kQ + kStages * kT;        // [kStages]
+    static constexpr int kMeta = kDO + kStages * kT;     // [kStages][lse2|delta|tau][NQT] f32
+    static constexpr int kBar = kMeta + kStages * 3 * NQT * 4;
+    static constexpr int kNumBars = 18;
+    static constexpr int kTmemSlot = kBar + kNumBars * 8;
+    static constexpr int kAlloc = kTmemSlot + 16 + 1024;
+    static_assert(kAlloc <= 232448, "smem");
+};
+enum { KQ_KVFULL = 0, KQ_KVEMPTY = 1, KQ_QDFULL = 2, KQ_QDEMPTY = 5, KQ_MFULL = 8, KQ_SFULL = 11, KQ_DPFULL = 12,
+       KQ_REMPTY = 13, KQ_PDEMPTY = 14, KQ_PDSFULL = 15, KQ_ACCDONE = 16, KQ_ACCEMPTY = 17 };  // 18 (<= 3 stages)
+
+// Per math thread: CT = NQT / 2 query columns of every tile. NQT = 128: warp-
+// group hf owns columns [64 hf, 64 hf + 64); NQT = 96: [32 hf, 32 hf + 32) and
+// [64 + 16 hf, 80 + 16 hf) (TMEM loads of 32 and 16 columns at aligned
+// offsets). qc(c) maps the thread's column index to the tile's.
+template <int NQT>
+__global__ void __launch_bounds__(kThreads, 1) k_bwd_kmaj_q(const __grid_constant__ BwdArgs a) {
+    using SM = KQSmem<NQT>;
+    constexpr int D = 128;
+    constexpr int QS = SM::kStages;
+    constexpr int CT = NQT / 2;
+    static_assert(NQT == 128 || NQT == 96, "query tile");
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    const uint32_t sbase = smem_u32(smem);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SM::kBar);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + SM::kTmemSlot);
+    float* qmeta = reinterpret_cast<float*>(smem + SM::kMeta);  // [stage][lse2|delta|tau][128]
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef SKB_TRACE_KMAJ  // tiles 12.. of CTA 100 (tools/trace_kmaj.py)
+#define TRK(role, gg, ev) \
+    if ((gg) >= 12) SKB_TRB(role, (gg) - 12, ev)
+#else
+#define TRK(role, gg, ev) \
+    do {                  \
+    } while (0)
+#endif
+    const int ntk = (a.L + 127) / 128;
+    const int nitems = ntk * a.H * a.B;
+    // item wi -> (key tile fastest, h, b); dense sequences only, queries [j0, uni_hi)
+    auto item = [&](int wi, int& b, int& h, int& j0, int& nq) -> bool {
+        const int kt = wi % ntk;
+        const int bh = wi / ntk;
+        h = bh % a.H;
+        b = bh / a.H;
+        j0 = kt * 128;
+        if (2 * __ldg(a.ever_count + b) <= a.T) return false;
+        nq = (__ldg(a.uni_hi + b * ntk + kt) - j0 + NQT - 1) / NQT;
+        return true;
+    };
+    if (threadIdx.x == 0) {
+        mbar_init(&bars[KQ_KVFULL], 1);
+        mbar_init(&bars[KQ_KVEMPTY], 1);
+        for (int s = 0; s < QS; ++s) {
+            mbar_init(&bars[KQ_QDFULL + s], 1);
+            mbar_init(&bars[KQ_QDEMPTY + s], 1);
+            mbar_init(&bars[KQ_MFULL + s], kProducers + 1);
+        }
+        mbar_init(&bars[KQ_SFULL], 1);
+        mbar_init(&bars[KQ_DPFULL], 1);
+        mbar_init(&bars[KQ_REMPTY], kMath / 32);
+        mbar_init(&bars[KQ_PDEMPTY], 1);
+        mbar_init(&bars[KQ_PDSFULL], kMath / 32);
+        mbar_init(&bars[KQ_ACCDONE], 1);
+        mbar_init(&bars[KQ_ACCEMPTY], kMath / 32);
+        mbar_fence_init();
+    }
+    if (warp == kMmaWarp) tmem_alloc<512>(tmem_slot);
+    tc_before_sync();
+    __syncthreads();
+    tc_after_sync();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t tR = tmem, tPS = tmem + 128, tDV = tmem + 256, tDK = tmem + 384;
+
+    if (warp >= kProdWarp0 && warp < kMmaWarp) {
+        const int ptid = threadIdx.x - kProdWarp0 * 32;
+        int g = 0, it = 0;
+        for (int wi = blockIdx.x; wi < nitems; wi += gridDim.x) {
+            int b, h, j0, nq;
+            if (!item(wi, b, h, j0, nq)) continue;
+            if (ptid == 0) {
+                if (it > 0) mbar_wait(&bars[KQ_KVEMPTY], (it - 1) & 1);
+                mbar_expect_tx(&bars[KQ_KVFULL], 2 * SM::kKV);
+#pragma unroll
+                for (int at = 0; at < 2; ++at) {
+                    tma_load_3d(sbase + SM::kK + at * 128 * 128, &a.tm_k128, h * D + at * 64, j0, b, &bars[KQ_KVFULL]);
+                    tma_load_3d(sbase + SM::kV + at * 128 * 128, &a.tm_v128, h * D + at * 64, j0, b, &bars[KQ_KVFULL]);
+                }
+            }
+            ++it;
+            if (ptid == 32) {  // the next item's K/V rows into L2 while this item runs
+                int nb, nh, nj0, nnq;
+                for (int nw = wi + gridDim.x; nw < nitems; nw += gridDim.x)
+                    if (item(nw, nb, nh, nj0, nnq)) {
+#pragma unroll
+                        for (int at = 0; at < 2; ++at) {
+                            tma_prefetch_3d(&a.tm_k128, nh * D + at * 64, nj0, nb);
+                            tma_prefetch_3d(&a.tm_v128, nh * D + at * 64, nj0, nb);
+                        }
+                        break;
+                    }
+            }
+            const float* lse2 = a.lse2 + ((int64_t)b * a.H + h) * a.L;
+            const float* dlt = a.delta + ((int64_t)b * a.H + h) * a.L;
+            const int64_t bl = (int64_t)b * a.L;
+            const CUtensorMap* tmq = NQT == 128 ? &a.tm_q128 : &a.tm_q96;
+            const CUtensorMap* tmo = NQT == 128 ? &a.tm_do128 : &a.tm_do96;
+            for (int qt = 0; qt < nq; ++qt, ++g) {
+                const int s = g % QS;
+                const int qs = j0 + qt * NQT;
+                if (ptid == 32 && qt + QS < nq) {  // this item's tile QS ahead into L2
+#pragma unroll
+                    for (int at = 0; at < 2; ++at) {
+                        tma_prefetch_3d(tmq, h * D + at * 64, qs + QS * NQT, b);
+                        tma_prefetch_3d(tmo, h * D + at * 64, qs + QS * NQT, b);
+                    }
+                }
+                if (g >= QS) mbar_wait(&bars[KQ_QDEMPTY + s], ((g - QS) / QS) & 1);
+                for (int c = ptid; c < NQT; c += kProducers) {
+                    const int i = qs + c;
+                    const bool ok = i < a.L;
+                    const int t = i - a.w;
+                    const uint32_t mb = smem_u32(qmeta + (s * 3) * NQT + c);
+                    cp_async4(mb, lse2 + (ok ? i : 0), ok);
+                    cp_async4(mb + NQT * 4, dlt + (ok ? i : 0), ok);
+                    cp_async4(mb + 2 * NQT * 4, a.tauf + bl + (ok && t >= 0 ? t : 0), ok && t >= 0);
+                }
+                cp_async_arrive_noinc(&bars[KQ_MFULL + s]);
+                if (ptid == 0) {
+                    mbar_arrive(&bars[KQ_MFULL + s]);
+                    mbar_expect_tx(&bars[KQ_QDFULL + s], 2 * SM::kT);
+#pragma unroll
+                    for (int at = 0; at < 2; ++at) {
+                        tma_load_3d(sbase + SM::kQ + s * SM::kT + at * NQT * 128, tmq, h * D + at * 64, qs, b,
+                                    &bars[KQ_QDFULL + s]);
+                        tma_load_3d(sbase + SM::kDO + s * SM::kT + at * NQT * 128, tmo, h * D + at * 64, qs, b,
+                                    &bars[KQ_QDFULL + s]);
+                    }
+                }
+            }
+        }
+    } else if (warp == kMmaWarp) {
+        if (lane == 0) {
+            constexpr uint32_t id_s = umma_idesc(128, NQT, false, false);
+            constexpr uint32_t id_acc = umma_idesc(128, D, false, true);
+            int g = 0, it = 0, rp = 0;  // rp: REMPTY phases consumed
+            // dV += P~^T dO, dK += dS^T Q for global tile gj (item tile qj)
+            auto acc = [&](int gj, int qj, int itn) {
+                const int s = gj % QS;
+                mbar_wait_fast(&bars[KQ_PDSFULL], gj & 1);
+                TRK(7, gj, 2);
+                if (qj == 0 && itn > 0) mbar_wait_fast(&bars[KQ_ACCEMPTY], (itn - 1) & 1);
+                tc_after_sync();
+                const uint32_t qb = sbase + SM::kQ + s * SM::kT, dob = sbase + SM::kDO + s * SM::kT;
+#pragma unroll
+                for (int kk = 0; kk < NQT / 16; ++kk) {
+                    umma_f16_ts(tDV, tPS + kk * 8, desc_mnmajor(dob, NQT, kk), id_acc, (qj > 0 || kk > 0) ? 1u : 0u);
+                    umma_f16_ts(tDK, tPS + NQT / 2 + kk * 8, desc_mnmajor(qb, NQT, kk), id_acc,
+                                (qj > 0 || kk > 0) ? 1u : 0u);
+                }
+                umma_commit(&bars[KQ_PDEMPTY]);
+                umma_commit(&bars[KQ_QDEMPTY + s]);
+            };
+            for (int wi = blockIdx.x; wi < nitems; wi += gridDim.x) {
+                int b, h, j0, nq;
+                if (!item(wi, b, h, j0, nq)) continue;
+                mbar_wait_fast(&bars[KQ_KVFULL], it & 1);
+                tc_after_sync();
+                for (int qt = 0; qt < nq; ++qt, ++g) {
+                    const int s = g % QS;
+                    mbar_wait_fast(&bars[KQ_QDFULL + s], (g / QS) & 1);
+                    TRK(7, g, 0);
+                    if (g > 0) mbar_wait_fast(&bars[KQ_REMPTY], (rp++) & 1);  // dP(g-1) read out of R
+                    TRK(7, g, 5);
+                    tc_after_sync();
+                    const uint32_t qb = sbase + SM::kQ + s * SM::kT, dob = sbase + SM::kDO + s * SM::kT;
+#pragma unroll
+                    for (int kk = 0; kk < D / 16; ++kk)
+                        umma_f16(tR, desc_kmajor(sbase + SM::kK, 128, kk), desc_kmajor(qb, NQT, kk), id_s,
+                                 kk > 0 ? 1u : 0u);
+                    umma_commit(&bars[KQ_SFULL]);
+                    TRK(7, g, 1);
+                    if (qt >= 1) acc(g - 1, qt - 1, it);
+                    TRK(7, g, 6);
+                    mbar_wait_fast(&bars[KQ_REMPTY], (rp++) & 1);  // S(g) read out of R
+                    TRK(7, g, 7);
+                    tc_after_sync();
+#pragma unroll
+                    for (int kk = 0; kk < D / 16; ++kk)
+                        umma_f16(tR, desc_kmajor(sbase + SM::kV, 128, kk), desc_kmajor(dob, NQT, kk), id_s,
+                                 kk > 0 ? 1u : 0u);
+                    umma_commit(&bars[KQ_DPFULL]);
+                    TRK(7, g, 3);
+                    if (qt == nq - 1) umma_commit(&bars[KQ_KVEMPTY]);
+                }
+                acc(g - 1, nq - 1, it);
+                umma_commit(&bars[KQ_ACCDONE]);
+                ++it;
+            }
+        }
+        __syncwarp();
+    } else if (warp < kProdWarp0) {
+        const int hf = warp >> 2;
+        // tile column of the thread's column c (c even pairs stay in one group)
+        auto qc = [&](int c) { return NQT == 128 ? 64 * hf + c : (c < 32 ? 32 * hf + c : 32 + 16 * hf + c); };
+        const int r = ((warp & 3) << 5) | lane;
+        const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+        const float sl2 = a.scale_log2;
+        const float2 sl22 = make_float2(sl2, sl2);
+        const bool mst = a.mask_st != 0;
+        int g = 0, it = 0;
+        const bool trl = lane == 0 && (warp & 3) == 0;
+        for (int wi = blockIdx.x; wi < nitems; wi += gridDim.x) {
+            int b, h, j0, nq;
+            if (!item(wi, b, h, j0, nq)) continue;
+            const int64_t bl = (int64_t)b * a.L;
+            const int key = j0 + r < a.L ? j0 + r : -1;
+            // queries [key, key + w) read the key from the window, [key + w,
+            // leave + w) from the selection (proj/src/cache.cpp:259-311)
+            int hi_i = key >= 0 ? min(a.L, key + a.w) : 0;
+            bool sel_u = false;
+            float uj = 0.f, colsum = 0.f;
+            if (key >= 0 && key < a.T && a.R1 > 0) {
+                const int lv = __ldg(a.leave + bl + key);
+                sel_u = lv > key;
+                if (sel_u) {
+                    hi_i = min(a.L, lv + a.w);
+                    uj = __ldg(a.uf + bl + key);
+                }
+            }
+            for (int qt = 0; qt < nq; ++qt, ++g) {
+                const int s = g % QS;
+                const int qs = j0 + qt * NQT;  // the tile's first query
+                if (trl) TRK(4 + hf, g, 9);
+                mbar_wait(&bars[KQ_SFULL], g & 1);
+                mbar_wait(&bars[KQ_MFULL + s], (g / QS) & 1);
+                tc_after_sync();
+                float sv[CT], dp[CT];
+                auto ld_r = [&](float* v) {
+                    if constexpr (NQT == 128) {
+                        tmem_ld32(tR + lane_off + hf * 64, v);
+                        tmem_ld32(tR + lane_off + hf * 64 + 32, v + 32);
+                    } else {
+                        tmem_ld32(tR + lane_off + hf * 32, v);
+                        tmem_ld16(tR + lane_off + 64 + hf * 16, v + 32);
+                    }
+                };
+                ld_r(sv);
+                tmem_wait_ld();
+                tc_before_sync();
+                warp_arrive(&bars[KQ_REMPTY]);
+                if (trl) TRK(4 + hf, g, 0);
+                const float* ml = qmeta + (s * 3) * NQT;  // indexed by tile column
+                const float* md = ml + NQT;
+                const float* mt = ml + 2 * NQT;
+                const int cmin = key >= 0 ? key - qs : NQT;
+                const int cmax = key >= 0 ? hi_i - 1 - qs : -1;
+                if (!__all_sync(0xffffffffu, cmin <= 0 && cmax >= NQT - 1)) {
+#pragma unroll
+                    for (int c = 0; c < CT; ++c) sv[c] = (qc(c) >= cmin && qc(c) <= cmax) ? sv[c] : -INFINITY;
+                }
+                const int cwc = key + a.w - qs;  // tile columns < cwc: window, gate 1
+                const int clast = max(0, min(NQT - 1, a.L - 1 - qs));
+                const bool plain = __all_sync(0xffffffffu, !sel_u || cwc > NQT - 1 || uj >= mt[clast] + 1.f);
+                uint32_t pk[CT / 2];
+                // P (ungated, kept for dS) and P~ = P g -> TMEM
+#pragma unroll
+                for (int c = 0; c < CT; c += 2) {
+                    const float2 l2 = *reinterpret_cast<const float2*>(ml + qc(c));
+                    float2 p2 = __ffma2_rn(make_float2(sv[c], sv[c + 1]), sl22, make_float2(-l2.x, -l2.y));
+                    p2.x = ex2(p2.x);  // masked: 0
+                    p2.y = ex2(p2.y);
+                    sv[c] = p2.x, sv[c + 1] = p2.y;
+                    float2 pw = p2;
+                    if (!plain && !mst) {
+                        const float2 t2 = *reinterpret_cast<const float2*>(mt + qc(c));
+                        const float g0 = qc(c) < cwc ? 1.f : __saturatef(uj - t2.x);
+                        const float g1 = qc(c) + 1 < cwc ? 1.f : __saturatef(uj - t2.y);
+                        pw = __fmul2_rn(p2, make_float2(g0, g1));
+                    }
+                    pk[c >> 1] = pack_bf16(pw.x, pw.y);
+                }
+                if (trl) TRK(4 + hf, g, 1);
+                if (g >= 1) mbar_wait(&bars[KQ_PDEMPTY], (g - 1) & 1);  // dV/dK(g-1) have read P~/dS
+                if (trl) TRK(4 + hf, g, 2);
+                tc_after_sync();
+                // packed column = tile column / 2
+                auto st_ps = [&](uint32_t base) {
+                    if constexpr (NQT == 128) {
+                        tmem_st16u(base + lane_off + hf * 32, pk);
+                        tmem_st16u(base + lane_off + hf * 32 + 16, pk + 16);
+                    } else {
+                        tmem_st16u(base + lane_off + hf * 16, pk);
+                        tmem_st8u(base + lane_off + 32 + hf * 8, pk + 16);
+                    }
+                };
+                st_ps(tPS);
+                mbar_wait(&bars[KQ_DPFULL], g & 1);
+                if (trl) TRK(4 + hf, g, 3);
+                tc_after_sync();
+                ld_r(dp);
+                tmem_wait_ld();
+                tc_before_sync();
+                warp_arrive(&bars[KQ_REMPTY]);
+                // dS = P (g dP - delta) (unscaled); colsum: the gate gradient on the fractional support
+                if (plain) {
+#pragma unroll
+                    for (int c = 0; c < CT; c += 2) {
+                        const float2 d2 = *reinterpret_cast<const float2*>(md + qc(c));
+                        const float2 cc = __fmul2_rn(make_float2(sv[c], sv[c + 1]),
+                                                     __fadd2_rn(make_float2(dp[c], dp[c + 1]), make_float2(-d2.x, -d2.y)));
+                        pk[c >> 1] = pack_bf16(cc.x, cc.y);
+                    }
+                } else {
+                    float2 csum2 = make_float2(0.f, 0.f);
+#pragma unroll
+                    for (int c = 0; c < CT; c += 2) {
+                        const float2 d2 = *reinterpret_cast<const float2*>(md + qc(c));
+                        const float2 t2 = *reinterpret_cast<const float2*>(mt + qc(c));
+                        const float g0 = qc(c) < cwc ? 1.f : __saturatef(uj - t2.x);
+                        const float g1 = qc(c) + 1 < cwc ? 1.f : __saturatef(uj - t2.y);
+                        const float2 p2 = make_float2(sv[c], sv[c + 1]);
+                        const float2 dp2 = make_float2(dp[c], dp[c + 1]);
+                        const float2 g2 = mst ? make_float2(1.f, 1.f) : make_float2(g0, g1);
+                        const float2 cc = __fmul2_rn(p2, __ffma2_rn(g2, dp2, make_float2(-d2.x, -d2.y)));
+                        // 0 < g < 1 <=> (bits(g) - 1) < bits(1.0) - 1 (g in [0, 1])
+                        const float2 fr2 = make_float2((__float_as_uint(g0) - 1u) < 0x3F7FFFFFu ? 1.f : 0.f,
+                                                       (__float_as_uint(g1) - 1u) < 0x3F7FFFFFu ? 1.f : 0.f);
+                        csum2 = __ffma2_rn(__fmul2_rn(p2, dp2), fr2, csum2);
+                        pk[c >> 1] = pack_bf16(cc.x, cc.y);
+                    }
+                    colsum += csum2.x + csum2.y;
+                }
+                st_ps(tPS + NQT / 2);
+                tmem_wait_st();
+                tc_before_sync();
+                warp_arrive(&bars[KQ_PDSFULL]);
+                if (trl) TRK(4 + hf, g, 4);
+            }
+            mbar_wait(&bars[KQ_ACCDONE], it & 1);
+            tc_after_sync();
+            float dv[64], dk[64];
+            tmem_ld32(tDV + lane_off + hf * 64, dv);
+            tmem_ld32(tDV + lane_off + hf * 64 + 32, dv + 32);
+            tmem_ld32(tDK + lane_off + hf * 64, dk);
+            tmem_ld32(tDK + lane_off + hf * 64 + 32, dk + 32);
+            tmem_wait_ld();
+            tc_before_sync();
+            warp_arrive(&bars[KQ_ACCEMPTY]);
+            ++it;
+            if (key < 0) continue;
+            if (colsum != 0.f) atomicAdd(a.colsum + bl + key, (double)colsum);
+            const int64_t ro = (((int64_t)b * a.L + key) * a.H + h) * D + hf * 64;
+#pragma unroll
+            for (int e = 0; e < 64; e += 8) {
+                uint4 x, y;
+                x.x = pack_bf16(dk[e] * a.scale, dk[e + 1] * a.scale);
+                x.y = pack_bf16(dk[e + 2] * a.scale, dk[e + 3] * a.scale);
+                x.z = pack_bf16(dk[e + 4] * a.scale, dk[e + 5] * a.scale);
+                x.w = pack_bf16(dk[e + 6] * a.scale, dk[e + 7] * a.scale);
+                y.x = pack_bf16(dv[e], dv[e + 1]);
+                y.y = pack_bf16(dv[e + 2], dv[e + 3]);
+                y.z = pack_bf16(dv[e + 4], dv[e + 5]);
+                y.w = pack_bf16(dv[e + 6], dv[e + 7]);
+                *reinterpret_cast<uint4*>(a.dk + ro + e) = x;
+                *reinterpret_cast<uint4*>(a.dv + ro + e) = y;
+            }
+        }
+    }
+    tc_before_sync();
+    __syncthreads();
+    tc_after_sync();
+    if (warp == kMmaWarp) tmem_dealloc<512>(tmem);
+#undef TRK
+}
+
 // ------------------------------------------------------------ selected pass on CTA pairs
 // The selected pass (D = 128) as cta_group::2 MMAs on a cluster of two CTAs:
 // a work item is 256 entries of the ever-selected order (128 per CTA) and the
@@ -2947,7 +3349,18 @@ void launch_bwd(const BwdArgs& a0, const skb_attn_desc& d, cudaStream_t st) {
                 k_uni_items<<<dim3((unsigned)ntk, (unsigned)a.B), 128, 0, st>>>(a, ntk);
                 SKB_CHECK_LAUNCH();
                 const int ug = persist_grid((int64_t)ntk * d.heads * d.batch);
-                k_bwd_dkdv_win_tc<D, false, true><<<ug, kThreads, KWSmem<D, 4, false, true>::kAlloc, st>>>(a);
+                static const int q128 = getenv("SKB_BWD_QTILE") ? atoi(getenv("SKB_BWD_QTILE")) : 0;  // 96 / 128: k_bwd_kmaj_q (measured slower)
+                if (D == 128 && q128 == 96) {
+                    static uint64_t kattr = 0;
+                    if (first_on_device(&kattr)) set_smem(k_bwd_kmaj_q<96>, KQSmem<96>::kAlloc);
+                    k_bwd_kmaj_q<96><<<ug, kThreads, KQSmem<96>::kAlloc, st>>>(a);
+                } else if (D == 128 && q128 == 128) {
+                    static uint64_t kattr = 0;
+                    if (first_on_device(&kattr)) set_smem(k_bwd_kmaj_q<128>, KQSmem<128>::kAlloc);
+                    k_bwd_kmaj_q<128><<<ug, kThreads, KQSmem<128>::kAlloc, st>>>(a);
+                } else {
+                    k_bwd_dkdv_win_tc<D, false, true><<<ug, kThreads, KWSmem<D, 4, false, true>::kAlloc, st>>>(a);
+                }
                 SKB_CHECK_LAUNCH();
             }
             const int64_t items = (int64_t)ntk * d.heads * d.batch;
@@ -3021,6 +3434,8 @@ void run_attn_bwd_tc(const skb_attn_desc& d, const void* q, const void* k, const
         a.tm_q64 = tmap_rows3d(q, d.batch, d.seq_len, HD, 64);
         a.tm_do64 = tmap_rows3d(dout, d.batch, d.seq_len, HD, 64);
         a.tm_q32 = tmap_rows3d(q, d.batch, d.seq_len, HD, 32);
+        a.tm_q96 = tmap_rows3d(q, d.batch, d.seq_len, HD, 96);
+        a.tm_do96 = tmap_rows3d(dout, d.batch, d.seq_len, HD, 96);
         a.tm_do32 = tmap_rows3d(dout, d.batch, d.seq_len, HD, 32);
         a.tm_k128 = tmap_rows3d(k, d.batch, d.seq_len, HD, 128);
         a.tm_v128 = tmap_rows3d(v, d.batch, d.seq_len, HD, 128);

@@ -319,11 +319,12 @@ def test_fused_dq_backward_opt_in(cuda, cap):
     assert r.returncode == 0, r.stdout + r.stderr
 
 
-@pytest.mark.parametrize("uni", ["0", "1"])
+@pytest.mark.parametrize("uni", ["0", "1", "q96", "q128"])
 def test_unified_and_two_pass_key_major_backward(cuda, uni):
     """Dense sequences take the unified key-major pass (window + selection of a
     contiguous key tile in one kernel, SKB_BWD_UNI=1, the default); SKB_BWD_UNI=0
-    keeps the selected + window passes with bf16 partials. Both against the
+    keeps the selected + window passes with bf16 partials; SKB_BWD_QTILE=96/128
+    runs the unified pass with taller query tiles. All against the
     gather path, with capped persistent grids so every ring wraps (the recency
     cases are dense, the iid ones sparse, the chunked one never unified)."""
     import os
@@ -331,7 +332,11 @@ def test_unified_and_two_pass_key_major_backward(cuda, uni):
     import sys
 
     here = os.path.dirname(os.path.abspath(__file__))
-    env = dict(os.environ, SKB_BWD_UNI=uni, SKB_MAX_CTAS="5")
+    env = dict(os.environ, SKB_MAX_CTAS="5")
+    if uni.startswith("q"):  # the unified pass with 96- / 128-query tiles (k_bwd_kmaj_q, opt-in)
+        env.update(SKB_BWD_UNI="1", SKB_BWD_QTILE=uni[1:])
+    else:
+        env["SKB_BWD_UNI"] = uni
     r = subprocess.run([sys.executable, os.path.join(here, "scripts", "persist_check.py")], env=env,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
