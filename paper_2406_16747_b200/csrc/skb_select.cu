@@ -267,7 +267,10 @@ __device__ void tau_chunk_tail(const TauArgs& a, int b, int chunk, const double*
 // (256 threads x 8 keys) whose scratch aliases the prefix-sum array P; wider
 // bands (the large-cap passes) by the shared-memory bitonic sort.
 constexpr int kRadixItems = 8;
-using BandSort = cub::BlockRadixSort<double, kTauThreads, kRadixItems>;
+#ifndef SKB_TAU_RADIX_BITS
+#define SKB_TAU_RADIX_BITS 4
+#endif
+using BandSort = cub::BlockRadixSort<double, kTauThreads, kRadixItems, cub::NullType, SKB_TAU_RADIX_BITS>;
 constexpr int kRadixMax = kTauThreads * kRadixItems;
 
 __device__ int tau_band(const TauArgs& a, int b, int t0, double* bz, int cap, double* red_d,
@@ -1087,8 +1090,12 @@ void run_select(const skb_attn_desc& d, const double* u, void* ws, cudaStream_t 
         if (cap_big > a.cap) {
             TauArgs a2 = a;
             a2.cap = cap_big;
-            dim3 gs((unsigned)cdiv(nch, kSegChunks), (unsigned)B);
-            k_tau_segments<false><<<gs, kTauThreads, (size_t)cap_big * 3 * sizeof(double) + 16, st>>>(a2, nch, kSegChunks,
+            // segments sized so the flagged chunks spread over every SM: a segment's
+            // CTA walks its chunks serially (one sort, then per-chunk merges), so
+            // at B = 1 (a strong-scaling rank) 4-chunk segments halve the latency
+            const int seg = (int)std::min<int64_t>(kSegChunks, std::max<int64_t>(1, cdiv((int64_t)nch * B, num_sms())));
+            dim3 gs((unsigned)cdiv(nch, seg), (unsigned)B);
+            k_tau_segments<false><<<gs, kTauThreads, (size_t)cap_big * 3 * sizeof(double) + 16, st>>>(a2, nch, seg,
                                                                                                     q2, q2 + 1);
             SKB_CHECK_LAUNCH();
             a.ovf_count = q2;  // the global-scratch pass serves what is left
