@@ -496,7 +496,10 @@ __device__ void tau_chunk_tail(const TauArgs& a, int b, int chunk, const double*
     TTAU(t0, a.T, 6);
 }
 
-__global__ void __launch_bounds__(kTauThreads) k_tau_chunks(TauArgs a) {
+#ifndef SKB_TAU_MINB  // resident CTAs per SM asked of ptxas for the first tau pass
+#define SKB_TAU_MINB 4
+#endif
+__global__ void __launch_bounds__(kTauThreads, SKB_TAU_MINB) k_tau_chunks(TauArgs a) {
     extern __shared__ double smem[];
     // latest chunks first: their prefixes are the longest (the scans and the
     // band grow with t0), so they must not be left to a trailing partial wave
