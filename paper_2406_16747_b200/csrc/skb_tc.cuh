@@ -99,8 +99,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     mbar_wait_slow(bar, parity);
 }
 // (kept for the call sites on MMA-issuing threads)
+#ifndef SKB_MMA_SPIN  // 1: the MMA-issuing thread polls with test_wait (no suspend window)
+#define SKB_MMA_SPIN 0
+#endif
 __device__ __forceinline__ void mbar_wait_fast(uint64_t* bar, uint32_t parity) {
     if (SKB_WAIT_TEST_FIRST && mbar_test(bar, parity)) return;
+    if (SKB_MMA_SPIN) {
+        uint32_t spins = 0;
+        while (!mbar_test(bar, parity))
+            if (++spins > (1u << 28)) __trap();
+        return;
+    }
     mbar_wait_slow(bar, parity);
 }
 // cp.async completion of this thread's prior copies arrives on the barrier.
