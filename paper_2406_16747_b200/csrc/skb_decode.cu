@@ -363,30 +363,36 @@ struct CacheArgs {
     int64_t row_bytes;  // H * p * esize
 };
 
-__device__ __forceinline__ void warp_copy_row(uint8_t* dst, const uint8_t* src, int64_t bytes) {
-    const int lane = threadIdx.x & 31;
+// threads [tid, nthr) of the caller copy one row
+__device__ __forceinline__ void copy_row(uint8_t* dst, const uint8_t* src, int64_t bytes, int tid, int nthr) {
     if (((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src) | (uintptr_t)bytes) & 15) == 0) {
         const uint4* s = reinterpret_cast<const uint4*>(src);
         uint4* d = reinterpret_cast<uint4*>(dst);
-        for (int64_t i = lane; i < bytes / 16; i += 32) d[i] = s[i];
+        for (int64_t i = tid; i < bytes / 16; i += nthr) d[i] = s[i];
     } else {
         const uint16_t* s = reinterpret_cast<const uint16_t*>(src);
         uint16_t* d = reinterpret_cast<uint16_t*>(dst);
-        for (int64_t i = lane; i < bytes / 2; i += 32) d[i] = s[i];
+        for (int64_t i = tid; i < bytes / 2; i += nthr) d[i] = s[i];
     }
+}
+__device__ __forceinline__ void warp_copy_row(uint8_t* dst, const uint8_t* src, int64_t bytes) {
+    copy_row(dst, src, bytes, threadIdx.x & 31, 32);
 }
 
 // One position of forward_chunk's pass 1 (proj/src/cache.cpp:259-311) for one
 // sequence, uniformly on one warp. kv_src: this position's K/V rows (null in
 // a prefill replay: the rows are copied once at the end). Builds the
 // attended list when `emit` is set.
-__device__ void warp_cache_advance(const CacheArgs& A, int b, CacheCtl& c, double u_new,
-                                   const uint8_t* k_src, const uint8_t* v_src, bool emit) {
+// One position through the cache, phase 1 (one warp): the row enters the
+// window ring, the exiting position's stream push (selection, tau), the
+// retained-row peak. freed[] receives the positions whose slots phase 3 frees.
+__device__ bool warp_cache_push(const CacheArgs& A, int b, CacheCtl& c, double u_new, const uint8_t* k_src,
+                                const uint8_t* v_src, int* slot_out, int freed[2]) {
     const int lane = threadIdx.x & 31;
     const int64_t bL = (int64_t)b * A.Lmax, bS = (int64_t)b * A.S;
     if (c.t >= A.Lmax) {
         c.error = 2;
-        return;
+        return false;
     }
     const int pos = (int)c.t;
     StreamArr sa{A.sv + bL, A.si + bL, A.fv + bL, A.fi + bL, nullptr, nullptr, nullptr};
@@ -404,7 +410,8 @@ __device__ void warp_cache_advance(const CacheArgs& A, int b, CacheCtl& c, doubl
     }
     const long long ring_before = c.t < A.w ? c.t : A.w;
     c.peak = max(c.peak, ring_before + 1 + c.nsel);  // note_peak after ring push
-    int freed[2] = {-1, -1};
+    freed[0] = freed[1] = -1;
+    *slot_out = slot;
     __syncwarp();
     if (c.t + 1 > A.w) {  // ring_.size() > window: exit_window(ring_.front())
         const int e = pos - A.w;
@@ -431,47 +438,61 @@ __device__ void warp_cache_advance(const CacheArgs& A, int b, CacheCtl& c, doubl
     }
     const long long ring_after = (c.t + 1) < A.w ? (c.t + 1) : A.w;
     c.peak = max(c.peak, ring_after + c.nsel);
-    // attended list (snapshot): selected (survivor order), then the window ring
-    if (emit) {
-        const double tau = c.st.tau;
-        const int ns = c.nsel;
-        for (int r = lane; r < ns; r += 32) {
-            const int jp = sa.si[r];
-            const double g = fmin(1.0, fmax(0.0, sa.sv[r] - tau));
-            A.att_slot[bS + r] = A.slot_of[bL + jp];
-            A.att_kg[bS + r] = A.key_soft ? g : 1.0;
-            A.att_vg[bS + r] = A.mask_st ? 1.0 : g;
-        }
-        int n = ns;
-        if (A.w > 0) {
-            const int r0 = max(0, pos - A.w + 1);
-            for (int jp = r0 + lane; jp <= pos; jp += 32) {
-                const int r = ns + (jp - r0);
-                A.att_slot[bS + r] = A.slot_of[bL + jp];
-                A.att_kg[bS + r] = 1.0;
-                A.att_vg[bS + r] = 1.0;
-            }
-            n += pos - r0 + 1;
-        }
-        if (A.w == 0 && !A.lin) {
-            // nothing window-resident: the query reads itself unless selected
-            bool selected = false;
-            for (int r = lane; r < ns; r += 32) selected |= sa.si[r] == pos;
-            selected = __any_sync(0xffffffffu, selected);
-            if (!selected) {
-                if (lane == 0) {
-                    A.att_slot[bS + n] = slot;
-                    A.att_kg[bS + n] = 1.0;
-                    A.att_vg[bS + n] = 1.0;
-                }
-                n += 1;
-            }
-        }
-        if (lane == 0) A.att_n[b] = n;
+    return true;
+}
+
+// Phase 2: the attended list (snapshot): selected (survivor order), then the
+// window ring. Threads [tid, nthr) of the caller stride over the entries; the
+// w = 0 self-read test is a warp vote (callers with nthr > 32 run it on warp 0).
+__device__ void cache_emit(const CacheArgs& A, int b, const CacheCtl& c, int slot, int tid, int nthr) {
+    const int lane = threadIdx.x & 31;
+    const int64_t bL = (int64_t)b * A.Lmax, bS = (int64_t)b * A.S;
+    const int pos = (int)c.t;
+    StreamArr sa{A.sv + bL, A.si + bL, A.fv + bL, A.fi + bL, nullptr, nullptr, nullptr};
+    const double tau = c.st.tau;
+    const int ns = c.nsel;
+    for (int r = tid; r < ns; r += nthr) {
+        const int jp = sa.si[r];
+        const double g = fmin(1.0, fmax(0.0, sa.sv[r] - tau));
+        A.att_slot[bS + r] = A.slot_of[bL + jp];
+        A.att_kg[bS + r] = A.key_soft ? g : 1.0;
+        A.att_vg[bS + r] = A.mask_st ? 1.0 : g;
     }
+    int n = ns;
+    if (A.w > 0) {
+        const int r0 = max(0, pos - A.w + 1);
+        for (int jp = r0 + tid; jp <= pos; jp += nthr) {
+            const int r = ns + (jp - r0);
+            A.att_slot[bS + r] = A.slot_of[bL + jp];
+            A.att_kg[bS + r] = 1.0;
+            A.att_vg[bS + r] = 1.0;
+        }
+        n += pos - r0 + 1;
+    }
+    if (tid >= 32) return;  // warp 0: the self-read test and the count
+    if (A.w == 0 && !A.lin) {
+        // nothing window-resident: the query reads itself unless selected
+        bool selected = false;
+        for (int r = lane; r < ns; r += 32) selected |= sa.si[r] == pos;
+        selected = __any_sync(0xffffffffu, selected);
+        if (!selected) {
+            if (lane == 0) {
+                A.att_slot[bS + n] = slot;
+                A.att_kg[bS + n] = 1.0;
+                A.att_vg[bS + n] = 1.0;
+            }
+            n += 1;
+        }
+    }
+    if (lane == 0) A.att_n[b] = n;
+}
+
+// Phase 3 (one warp): drop_kv frees the slots now (the attention of this step
+// reads only the attended list; slots are reallocated by the next control).
+__device__ void warp_cache_drop(const CacheArgs& A, int b, CacheCtl& c, const int freed[2]) {
+    const int lane = threadIdx.x & 31;
+    const int64_t bL = (int64_t)b * A.Lmax, bS = (int64_t)b * A.S;
     __syncwarp();
-    // drop_kv: free the slots now (the attention of this step reads only the
-    // attended list, and slots are reallocated by the next step's control)
     for (int f = 0; f < 2; ++f) {
         const int fp = freed[f];
         if (fp < 0) continue;
@@ -487,6 +508,15 @@ __device__ void warp_cache_advance(const CacheArgs& A, int b, CacheCtl& c, doubl
     }
     c.t += 1;
     if (c.st.error) c.error = 1;
+}
+
+
+__device__ void warp_cache_advance(const CacheArgs& A, int b, CacheCtl& c, double u_new,
+                                   const uint8_t* k_src, const uint8_t* v_src, bool emit) {
+    int slot, freed[2];
+    if (!warp_cache_push(A, b, c, u_new, k_src, v_src, &slot, freed)) return;
+    if (emit) cache_emit(A, b, c, slot, threadIdx.x & 31, 32);
+    warp_cache_drop(A, b, c, freed);
 }
 
 __global__ void k_cache_init(CacheArgs A, double k) {
@@ -508,15 +538,46 @@ __global__ void k_cache_init(CacheArgs A, double k) {
 }
 
 // one decode step: a warp per sequence
-__global__ void k_cache_control(CacheArgs A, int B, const uint8_t* __restrict__ k_new,
-                                const uint8_t* __restrict__ v_new, const double* __restrict__ u_new) {
-    const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (b >= B) return;
-    CacheCtl c = A.ctl[b];
-    if (c.error == 0)
-        warp_cache_advance(A, b, c, u_new[b], k_new + (int64_t)b * A.row_bytes, v_new + (int64_t)b * A.row_bytes,
-                           true);
-    if ((threadIdx.x & 31) == 0) A.ctl[b] = c;
+// One step's control, a CTA per sequence: warp 0 runs the stream push (the
+// reference's serial arithmetic), then all kControlThreads threads write the
+// attended list (its dependent slot_of gathers were the control's latency
+// with one warp), then warp 0 frees the dropped slots.
+constexpr int kControlThreads = 256;
+__global__ void __launch_bounds__(kControlThreads) k_cache_control(CacheArgs A, int B, const uint8_t* __restrict__ k_new,
+                                                                   const uint8_t* __restrict__ v_new,
+                                                                   const double* __restrict__ u_new) {
+    const int b = blockIdx.x;
+    __shared__ CacheCtl cs;
+    __shared__ int s_slot, s_freed[2], s_ok;
+    if (threadIdx.x < 32) {
+        CacheCtl c = A.ctl[b];
+        int slot = -1, freed[2] = {-1, -1};
+        bool ok = false;
+        if (c.error == 0) ok = warp_cache_push(A, b, c, u_new[b], nullptr, nullptr, &slot, freed);
+        if (threadIdx.x == 0) {
+            cs = c;
+            s_slot = slot;
+            s_freed[0] = freed[0];
+            s_freed[1] = freed[1];
+            s_ok = ok ? 1 : 0;
+        }
+    }
+    __syncthreads();
+    if (s_ok) {  // the new K/V rows into their slot (the attention of this step reads them), the attended list
+        const int64_t dst = ((int64_t)b * A.S + s_slot) * A.row_bytes;
+        copy_row(A.kpool + dst, k_new + (int64_t)b * A.row_bytes, A.row_bytes, threadIdx.x, blockDim.x);
+        copy_row(A.vpool + dst, v_new + (int64_t)b * A.row_bytes, A.row_bytes, threadIdx.x, blockDim.x);
+        cache_emit(A, b, cs, s_slot, threadIdx.x, blockDim.x);
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        CacheCtl c = cs;
+        if (s_ok) {
+            const int freed[2] = {s_freed[0], s_freed[1]};
+            warp_cache_drop(A, b, c, freed);
+        }
+        if (threadIdx.x == 0) A.ctl[b] = c;
+    }
 }
 
 // prefill replay: n positions per sequence, no attention; rows copied after.
@@ -878,29 +939,56 @@ k_cache_attn_bf16(CacheArgs A, const __nv_bfloat16* __restrict__ q, int H, float
 }
 
 template <class T>
-__global__ void k_cache_combine(const void* po_, const void* pm_, const void* pl_,
-                                const int* __restrict__ att_n, int H, int p, int nsplit, T* __restrict__ o) {
+__global__ void __launch_bounds__(128) k_cache_combine(const void* po_, const void* pm_, const void* pl_,
+                                                       const int* __restrict__ att_n, int H, int p, int nsplit,
+                                                       T* __restrict__ o) {
+    // the chunks' weights exp(m_s - M) once per (sequence, head) in shared
+    // memory, then every output element's sum over the chunks with its loads
+    // in flight together (the per-element loop was latency-bound)
     using Acc = AccOf<T>;
+    extern __shared__ __align__(16) uint8_t csm[];
+    Acc* wsp = reinterpret_cast<Acc*>(csm);  // [nsplit]
+    __shared__ Acc red[4];
     const Acc* po = static_cast<const Acc*>(po_);
     const Acc* pm = static_cast<const Acc*>(pm_);
     const Acc* pl = static_cast<const Acc*>(pl_);
     const int h = blockIdx.x, b = blockIdx.y;
     const int used = min(nsplit, (att_n[b] + kSlotsPerCta - 1) / kSlotsPerCta);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     Acc M = -INFINITY;
-    for (int s = 0; s < used; ++s) M = fmax(M, pm[((int64_t)b * nsplit + s) * H + h]);
-    Acc Lsum = 0;
-    for (int s = 0; s < used; ++s) {
+    for (int s = threadIdx.x; s < used; s += blockDim.x) M = fmax(M, pm[((int64_t)b * nsplit + s) * H + h]);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) M = fmax(M, __shfl_xor_sync(0xffffffffu, M, off));
+    if (lane == 0) red[warp] = M;
+    __syncthreads();
+    M = fmax(fmax(red[0], red[1]), fmax(red[2], red[3]));
+    __syncthreads();
+    Acc ls = 0;
+    for (int s = threadIdx.x; s < used; s += blockDim.x) {
         const int64_t i = ((int64_t)b * nsplit + s) * H + h;
-        if (pm[i] > -INFINITY) Lsum += pl[i] * exp_acc(pm[i] - M);
+        const Acc w = pm[i] > -INFINITY ? exp_acc(pm[i] - M) : Acc(0);
+        wsp[s] = w;
+        ls += pl[i] * w;
     }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) ls += __shfl_xor_sync(0xffffffffu, ls, off);
+    if (lane == 0) red[warp] = ls;
+    __syncthreads();
+    const Acc Lsum = (red[0] + red[1]) + (red[2] + red[3]);
     const Acc inv = Lsum > 0 ? Acc(1) / Lsum : Acc(0);
     for (int c = threadIdx.x; c < p; c += blockDim.x) {
-        Acc acc = 0;
-        for (int s = 0; s < used; ++s) {
-            const int64_t i = ((int64_t)b * nsplit + s) * H + h;
-            if (pm[i] > -INFINITY) acc += po[i * p + c] * exp_acc(pm[i] - M);
+        const Acc* src = po + ((int64_t)b * nsplit * H + h) * p + c;  // + s * H * p
+        const int64_t step = (int64_t)H * p;
+        Acc a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+        int s = 0;
+        for (; s + 4 <= used; s += 4) {
+            a0 += src[(s + 0) * step] * wsp[s + 0];
+            a1 += src[(s + 1) * step] * wsp[s + 1];
+            a2 += src[(s + 2) * step] * wsp[s + 2];
+            a3 += src[(s + 3) * step] * wsp[s + 3];
         }
-        o[((int64_t)b * H + h) * p + c] = (T)(acc * inv);
+        for (; s < used; ++s) a0 += src[s * step] * wsp[s];
+        o[((int64_t)b * H + h) * p + c] = (T)(((a0 + a1) + (a2 + a3)) * inv);
     }
 }
 
@@ -1560,8 +1648,8 @@ static void cache_attend(skb_cache* c, const void* q, void* o, cudaStream_t st) 
     else if (c->vec == 2) launch(k_cache_attn<T, 2>);
     else launch(k_cache_attn<T, 1>);
     SKB_CHECK_LAUNCH();
-    k_cache_combine<T><<<dim3((unsigned)H, (unsigned)d.batch), 128, 0, st>>>(c->po, c->pm, c->pl, c->A.att_n, H,
-                                                                             p, c->nsplit, static_cast<T*>(o));
+    k_cache_combine<T><<<dim3((unsigned)H, (unsigned)d.batch), 128, (size_t)c->nsplit * sizeof(AccOf<T>), st>>>(
+        c->po, c->pm, c->pl, c->A.att_n, H, p, c->nsplit, static_cast<T*>(o));
     SKB_CHECK_LAUNCH();
 }
 
@@ -1577,8 +1665,8 @@ int skb_cache_step(skb_cache* c, const void* q, const void* k, const void* v, co
     const int B = (int)c->d.batch;
     const double* uu = u;
     if (!uu) uu = c->zeros;  // k = 0: scores idle (proj/src/cache.cpp:219-227)
-    k_cache_control<<<(unsigned)cdiv(B, 4), 128, 0, st>>>(c->A, B, static_cast<const uint8_t*>(k),
-                                                          static_cast<const uint8_t*>(v), uu);
+    k_cache_control<<<(unsigned)B, kControlThreads, 0, st>>>(c->A, B, static_cast<const uint8_t*>(k),
+                                                             static_cast<const uint8_t*>(v), uu);
     SKB_CHECK_LAUNCH();
     if (c->d.dtype == SKB_BF16) cache_attend<__nv_bfloat16>(c, q, o, st);
     else if (c->d.dtype == SKB_F32) cache_attend<float>(c, q, o, st);
@@ -1621,8 +1709,8 @@ int skb_cache_linmix_step(skb_cache* c, const void* q, const void* k, const void
     const int B = (int)c->d.batch, H = (int)c->d.heads, p = (int)c->d.head_dim;
     SKB_REQUIRE(p <= 256, SKB_ESHAPE, "linear mix: head_dim must be <= 256");
     const double* uu = u ? u : c->zeros;
-    k_cache_control<<<(unsigned)cdiv(B, 4), 128, 0, st>>>(c->A, B, static_cast<const uint8_t*>(k),
-                                                          static_cast<const uint8_t*>(v), uu);
+    k_cache_control<<<(unsigned)B, kControlThreads, 0, st>>>(c->A, B, static_cast<const uint8_t*>(k),
+                                                             static_cast<const uint8_t*>(v), uu);
     SKB_CHECK_LAUNCH();
     // pass 1 of the position: its phi(k) row and the prefix state include it (cache.cpp:267-278)
     k_lin_fill_phi<<<dim3((unsigned)c->A.S, (unsigned)B), 128, 0, st>>>(c->A, phk, 1, H, p, c->lphk);
