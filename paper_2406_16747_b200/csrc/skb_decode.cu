@@ -387,7 +387,7 @@ __device__ __forceinline__ void warp_copy_row(uint8_t* dst, const uint8_t* src, 
 // window ring, the exiting position's stream push (selection, tau), the
 // retained-row peak. freed[] receives the positions whose slots phase 3 frees.
 __device__ bool warp_cache_push(const CacheArgs& A, int b, CacheCtl& c, double u_new, const uint8_t* k_src,
-                                const uint8_t* v_src, int* slot_out, int freed[2]) {
+                                const uint8_t* v_src, int* slot_out, int freed[2], const StreamArr* arr = nullptr) {
     const int lane = threadIdx.x & 31;
     const int64_t bL = (int64_t)b * A.Lmax, bS = (int64_t)b * A.S;
     if (c.t >= A.Lmax) {
@@ -395,7 +395,7 @@ __device__ bool warp_cache_push(const CacheArgs& A, int b, CacheCtl& c, double u
         return false;
     }
     const int pos = (int)c.t;
-    StreamArr sa{A.sv + bL, A.si + bL, A.fv + bL, A.fi + bL, nullptr, nullptr, nullptr};
+    const StreamArr sa = arr ? *arr : StreamArr{A.sv + bL, A.si + bL, A.fv + bL, A.fi + bL, nullptr, nullptr, nullptr};
     if (lane == 0) A.u_hist[bL + pos] = u_new;
     // the new row enters the window ring (kv_.emplace + ring_.push_back)
     const int slot = A.free_stack[bS + c.free_top - 1];
@@ -444,11 +444,12 @@ __device__ bool warp_cache_push(const CacheArgs& A, int b, CacheCtl& c, double u
 // Phase 2: the attended list (snapshot): selected (survivor order), then the
 // window ring. Threads [tid, nthr) of the caller stride over the entries; the
 // w = 0 self-read test is a warp vote (callers with nthr > 32 run it on warp 0).
-__device__ void cache_emit(const CacheArgs& A, int b, const CacheCtl& c, int slot, int tid, int nthr) {
+__device__ void cache_emit(const CacheArgs& A, int b, const CacheCtl& c, int slot, int tid, int nthr,
+                           const StreamArr* arr = nullptr) {
     const int lane = threadIdx.x & 31;
     const int64_t bL = (int64_t)b * A.Lmax, bS = (int64_t)b * A.S;
     const int pos = (int)c.t;
-    StreamArr sa{A.sv + bL, A.si + bL, A.fv + bL, A.fi + bL, nullptr, nullptr, nullptr};
+    const StreamArr sa = arr ? *arr : StreamArr{A.sv + bL, A.si + bL, A.fv + bL, A.fi + bL, nullptr, nullptr, nullptr};
     const double tau = c.st.tau;
     const int ns = c.nsel;
     for (int r = tid; r < ns; r += nthr) {
@@ -538,22 +539,50 @@ __global__ void k_cache_init(CacheArgs A, double k) {
 }
 
 // one decode step: a warp per sequence
-// One step's control, a CTA per sequence: warp 0 runs the stream push (the
-// reference's serial arithmetic), then all kControlThreads threads write the
-// attended list (its dependent slot_of gathers were the control's latency
-// with one warp), then warp 0 frees the dropped slots.
+// One step's control, a CTA per sequence: the sequence's survivor and
+// saturated arrays (sorted, ~floor(k) entries) are staged in shared memory,
+// warp 0 runs the stream push on them (the reference's serial arithmetic;
+// the insert shifts and the pop loop's dependent reads were global round
+// trips), then all kControlThreads threads write the new K/V rows, the
+// attended list and the arrays back, and warp 0 frees the dropped slots.
+// Sequences whose arrays outgrow kCtlSmemEntries keep them in global memory.
 constexpr int kControlThreads = 256;
+constexpr int kCtlSmemEntries = 4096;
+constexpr size_t kCtlSmemBytes = (size_t)kCtlSmemEntries * 2 * (sizeof(double) + sizeof(int));
 __global__ void __launch_bounds__(kControlThreads) k_cache_control(CacheArgs A, int B, const uint8_t* __restrict__ k_new,
                                                                    const uint8_t* __restrict__ v_new,
                                                                    const double* __restrict__ u_new) {
+    extern __shared__ __align__(16) uint8_t ctl_smem[];
+    double* s_sv = reinterpret_cast<double*>(ctl_smem);
+    double* s_fv = s_sv + kCtlSmemEntries;
+    int* s_si = reinterpret_cast<int*>(s_fv + kCtlSmemEntries);
+    int* s_fi = s_si + kCtlSmemEntries;
     const int b = blockIdx.x;
+    const int64_t bL = (int64_t)b * A.Lmax;
     __shared__ CacheCtl cs;
     __shared__ int s_slot, s_freed[2], s_ok;
+    const CacheCtl c0 = A.ctl[b];
+    // one push adds at most one entry to each array
+    const bool staged = c0.error == 0 && c0.st.nS + 1 <= kCtlSmemEntries && c0.st.nF + 1 <= kCtlSmemEntries;
+    if (staged) {
+        for (int i = threadIdx.x; i < c0.st.nS; i += blockDim.x) {
+            s_sv[i] = A.sv[bL + i];
+            s_si[i] = A.si[bL + i];
+        }
+        for (int i = threadIdx.x; i < c0.st.nF; i += blockDim.x) {
+            s_fv[i] = A.fv[bL + i];
+            s_fi[i] = A.fi[bL + i];
+        }
+    }
+    __syncthreads();
+    const StreamArr glob{A.sv + bL, A.si + bL, A.fv + bL, A.fi + bL, nullptr, nullptr, nullptr};
+    const StreamArr shar{s_sv, s_si, s_fv, s_fi, nullptr, nullptr, nullptr};
+    const StreamArr* arr = staged ? &shar : &glob;
     if (threadIdx.x < 32) {
-        CacheCtl c = A.ctl[b];
+        CacheCtl c = c0;
         int slot = -1, freed[2] = {-1, -1};
         bool ok = false;
-        if (c.error == 0) ok = warp_cache_push(A, b, c, u_new[b], nullptr, nullptr, &slot, freed);
+        if (c.error == 0) ok = warp_cache_push(A, b, c, u_new[b], nullptr, nullptr, &slot, freed, arr);
         if (threadIdx.x == 0) {
             cs = c;
             s_slot = slot;
@@ -567,7 +596,17 @@ __global__ void __launch_bounds__(kControlThreads) k_cache_control(CacheArgs A, 
         const int64_t dst = ((int64_t)b * A.S + s_slot) * A.row_bytes;
         copy_row(A.kpool + dst, k_new + (int64_t)b * A.row_bytes, A.row_bytes, threadIdx.x, blockDim.x);
         copy_row(A.vpool + dst, v_new + (int64_t)b * A.row_bytes, A.row_bytes, threadIdx.x, blockDim.x);
-        cache_emit(A, b, cs, s_slot, threadIdx.x, blockDim.x);
+        cache_emit(A, b, cs, s_slot, threadIdx.x, blockDim.x, arr);
+    }
+    if (staged) {  // the arrays back (entries past the new lengths were popped)
+        for (int i = threadIdx.x; i < cs.st.nS; i += blockDim.x) {
+            A.sv[bL + i] = s_sv[i];
+            A.si[bL + i] = s_si[i];
+        }
+        for (int i = threadIdx.x; i < cs.st.nF; i += blockDim.x) {
+            A.fv[bL + i] = s_fv[i];
+            A.fi[bL + i] = s_fi[i];
+        }
     }
     __syncthreads();
     if (threadIdx.x < 32) {
@@ -1652,6 +1691,16 @@ static void cache_attend(skb_cache* c, const void* q, void* o, cudaStream_t st) 
         c->po, c->pm, c->pl, c->A.att_n, H, p, c->nsplit, static_cast<T*>(o));
     SKB_CHECK_LAUNCH();
 }
+// the control launch (dynamic shared memory above 48 KB is a per-device attribute)
+static void launch_control(skb_cache* c, int B, const void* k, const void* v, const double* uu, cudaStream_t st) {
+    static uint64_t attr = 0;
+    if (first_on_device(&attr))
+        SKB_CHECK_CUDA(cudaFuncSetAttribute(k_cache_control, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)kCtlSmemBytes));
+    k_cache_control<<<(unsigned)B, kControlThreads, kCtlSmemBytes, st>>>(c->A, B, static_cast<const uint8_t*>(k),
+                                                                         static_cast<const uint8_t*>(v), uu);
+}
+
 
 extern "C" {
 
@@ -1665,8 +1714,7 @@ int skb_cache_step(skb_cache* c, const void* q, const void* k, const void* v, co
     const int B = (int)c->d.batch;
     const double* uu = u;
     if (!uu) uu = c->zeros;  // k = 0: scores idle (proj/src/cache.cpp:219-227)
-    k_cache_control<<<(unsigned)B, kControlThreads, 0, st>>>(c->A, B, static_cast<const uint8_t*>(k),
-                                                             static_cast<const uint8_t*>(v), uu);
+    launch_control(c, B, k, v, uu, st);
     SKB_CHECK_LAUNCH();
     if (c->d.dtype == SKB_BF16) cache_attend<__nv_bfloat16>(c, q, o, st);
     else if (c->d.dtype == SKB_F32) cache_attend<float>(c, q, o, st);
@@ -1709,8 +1757,7 @@ int skb_cache_linmix_step(skb_cache* c, const void* q, const void* k, const void
     const int B = (int)c->d.batch, H = (int)c->d.heads, p = (int)c->d.head_dim;
     SKB_REQUIRE(p <= 256, SKB_ESHAPE, "linear mix: head_dim must be <= 256");
     const double* uu = u ? u : c->zeros;
-    k_cache_control<<<(unsigned)B, kControlThreads, 0, st>>>(c->A, B, static_cast<const uint8_t*>(k),
-                                                             static_cast<const uint8_t*>(v), uu);
+    launch_control(c, B, k, v, uu, st);
     SKB_CHECK_LAUNCH();
     // pass 1 of the position: its phi(k) row and the prefix state include it (cache.cpp:267-278)
     k_lin_fill_phi<<<dim3((unsigned)c->A.S, (unsigned)B), 128, 0, st>>>(c->A, phk, 1, H, p, c->lphk);
