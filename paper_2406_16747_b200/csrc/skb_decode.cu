@@ -806,8 +806,11 @@ k_cache_attn(CacheArgs A, const T* __restrict__ q, int H, int p, double scale_d,
 // row (HPL heads); warp w owns head groups j = w, w+8, ... for all entries of
 // the chunk, so the K and V streams are fully coalesced with many loads in
 // flight per lane.
-template <int D>
-__global__ void __launch_bounds__(kAttnThreads)
+#ifndef SKB_DEC_MINB  // resident CTAs per SM asked of ptxas (2 at 104 registers)
+#define SKB_DEC_MINB 3
+#endif
+template <int D, int JMAX = 4>
+__global__ void __launch_bounds__(kAttnThreads, SKB_DEC_MINB)
 k_cache_attn_bf16(CacheArgs A, const __nv_bfloat16* __restrict__ q, int H, float scale, float* __restrict__ po,
                   float* __restrict__ pm, float* __restrict__ pl, int nsplit, int hs, int* __restrict__ done,
                   __nv_bfloat16* __restrict__ o) {
@@ -817,7 +820,7 @@ k_cache_attn_bf16(CacheArgs A, const __nv_bfloat16* __restrict__ q, int H, float
     // merges the split softmax of every chunk (no separate combine launch).
     constexpr int LPH = D / 8;     // lanes per head row (16 B each)
     constexpr int HPL = 32 / LPH;  // heads per warp load
-    constexpr int JMAX = 4;        // head groups per warp (H <= 32 * HPL / 8 * JMAX)
+    // JMAX: head groups per warp (hs <= 8 warps * HPL * JMAX)
     extern __shared__ float sm[];
     float* sp = sm;                                           // [hs][kSlotsPerCta]
     int* ss = reinterpret_cast<int*>(sp + hs * kSlotsPerCta);  // [kSlotsPerCta]
@@ -1679,8 +1682,15 @@ static void cache_attend(skb_cache* c, const void* q, void* o, cudaStream_t st) 
                                                   fuse ? static_cast<__nv_bfloat16*>(o) : nullptr);
         };
         SKB_REQUIRE(H % hs == 0, SKB_ECONFIG, "cache: heads must be a multiple of the decode head group");
-        if (p == 128) run(k_cache_attn_bf16<128>);
-        else run(k_cache_attn_bf16<64>);
+        // the head groups a warp covers: hs / hpl over 8 warps
+        const bool j2 = hs / hpl <= 2 * (kAttnThreads / 32);
+        if (p == 128) {
+            if (j2) run(k_cache_attn_bf16<128, 2>);
+            else run(k_cache_attn_bf16<128, 4>);
+        } else {
+            if (j2) run(k_cache_attn_bf16<64, 2>);
+            else run(k_cache_attn_bf16<64, 4>);
+        }
         SKB_CHECK_LAUNCH();
         if (fuse) return;  // the last chunk CTA of each (sequence, head group) wrote o
     } else if (c->vec == 4) launch(k_cache_attn<T, 4>);
