@@ -272,6 +272,27 @@ constexpr int kRadixItems = 8;
 #endif
 using BandSort = cub::BlockRadixSort<double, kTauThreads, kRadixItems, cub::NullType, SKB_TAU_RADIX_BITS>;
 constexpr int kRadixMax = kTauThreads * kRadixItems;
+// narrower bands take a sort with fewer keys per thread (the passes cost the
+// same per key slot, so an 8-slot sort of a 400-key band is mostly padding)
+template <int ITEMS>
+__device__ __forceinline__ void band_radix_sort(double* bz, int mcount, void* sort_tmp) {
+    using Sort = cub::BlockRadixSort<double, kTauThreads, ITEMS, cub::NullType, SKB_TAU_RADIX_BITS>;
+    static_assert(sizeof(typename Sort::TempStorage) <= sizeof(BandSort::TempStorage), "scratch");
+    double keys[ITEMS];
+#pragma unroll
+    for (int e = 0; e < ITEMS; ++e) {
+        const int idx = threadIdx.x * ITEMS + e;
+        keys[e] = idx < mcount ? bz[idx] : -CUDART_INF;
+    }
+    Sort(*static_cast<typename Sort::TempStorage*>(sort_tmp)).SortDescending(keys);
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < ITEMS; ++e) {
+        const int idx = threadIdx.x * ITEMS + e;
+        if (idx < mcount) bz[idx] = keys[e];
+    }
+    __syncthreads();
+}
 
 __device__ int tau_band(const TauArgs& a, int b, int t0, double* bz, int cap, double* red_d,
                         void* sort_tmp = nullptr) {
@@ -332,20 +353,9 @@ __device__ int tau_band(const TauArgs& a, int b, int t0, double* bz, int cap, do
     TTAU(t0, a.T, 2);
     if (mcount > cap) return -1;
     if (sort_tmp != nullptr && mcount <= kRadixMax && blockDim.x == kTauThreads) {
-        double keys[kRadixItems];
-#pragma unroll
-        for (int e = 0; e < kRadixItems; ++e) {
-            const int idx = threadIdx.x * kRadixItems + e;
-            keys[e] = idx < mcount ? bz[idx] : -CUDART_INF;
-        }
-        BandSort(*static_cast<typename BandSort::TempStorage*>(sort_tmp)).SortDescending(keys);
-        __syncthreads();
-#pragma unroll
-        for (int e = 0; e < kRadixItems; ++e) {
-            const int idx = threadIdx.x * kRadixItems + e;
-            if (idx < mcount) bz[idx] = keys[e];
-        }
-        __syncthreads();
+        if (mcount <= kTauThreads * 2) band_radix_sort<2>(bz, mcount, sort_tmp);
+        else if (mcount <= kTauThreads * 4) band_radix_sort<4>(bz, mcount, sort_tmp);
+        else band_radix_sort<kRadixItems>(bz, mcount, sort_tmp);
         TTAU(t0, a.T, 3);
         return mcount;
     }
