@@ -1138,6 +1138,7 @@ __global__ void __launch_bounds__(kOrdThreads) k_sel_order(BwdArgs a) {
     int* out = a.sel_order + (int64_t)b * a.L;
     if (2 * n > a.T) {  // dense (most keys are selected at some point): key order keeps the
         // gathers and the 32-key partial groups contiguous, which measured faster
+        if (a.uni) return;  // (the unified key-major pass covers dense sequences)
         for (int e = t; e < n; e += kOrdThreads) out[e] = el[e];
         return;
     }
@@ -1184,7 +1185,7 @@ __global__ void k_sel_items(BwdArgs a, int ntk) {
     const int b = wid / ntk, kt = wid % ntk;
     const int ec = a.ever_count[b];
     int2 res = make_int2(0, 0);
-    if (kt * 128 < ec) {
+    if (kt * 128 < ec && !(a.uni && 2 * ec > a.T)) {  // (dense + unified: no selected pass, no order)
         const int* el = a.sel_order + (int64_t)b * a.L + kt * 128;
         const int n = min(128, ec - kt * 128);
         int hi = 0, kmin = INT_MAX;
