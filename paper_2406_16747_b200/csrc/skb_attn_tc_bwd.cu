@@ -595,6 +595,15 @@ __device__ __forceinline__ void ds_store(uint32_t ds_base, int r, int hf, const 
 // and the finished dK/dV rows out
 constexpr int kWinQProd = 64;
 
+// Under the unified pass the selected/window passes serve the sparse
+// sequences only: nothing to do (return before any setup) when none is sparse.
+__device__ __forceinline__ bool no_sparse_sequence(const BwdArgs& a) {
+    if (!a.uni) return false;
+    for (int b = 0; b < a.B; ++b)
+        if (2 * __ldg(a.ever_count + b) <= a.T) return false;
+    return true;
+}
+
 // The unified pass's elementwise step where some columns are gated: the
 // selected pass's arithmetic with gate 1 on the window columns c < cwc (which
 // makes them plain softmax-backward columns with no gate-gradient term).
@@ -628,6 +637,7 @@ __device__ __forceinline__ float uni_frac_math(const BwdArgs& a, float uj, int c
 
 template <int D, bool FQ, bool UNI = false>
 __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_win_tc(const __grid_constant__ BwdArgs a) {
+    if (!UNI && no_sparse_sequence(a)) return;
     // the fused-dQ build gives one Q/dO stage to the dS^T tile; the unified
     // pass has no partial buffer and spends it on a fourth stage
     constexpr int QS = FQ ? 2 : (UNI ? 4 : kQS);
@@ -1229,6 +1239,7 @@ __global__ void __launch_bounds__(128) k_uni_items(BwdArgs a, int ntk) {
 // item's last S/dP MMA releases the buffer.
 template <int D, bool KEY_SOFT, bool FQ>
 __global__ void __launch_bounds__(kThreads, 1) k_bwd_dkdv_sel_tc(const __grid_constant__ BwdArgs a) {
+    if (no_sparse_sequence(a)) return;
     constexpr int QS = FQ ? kQS : kSelQS;
     using SM = KSmem<D, QS, FQ>;
     static_assert(KW_DQFULL + 1 < SM::kNumBars, "barrier slots");
