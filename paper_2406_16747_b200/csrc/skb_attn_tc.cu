@@ -643,8 +643,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_p(const __grid_constant__ F
                     for (int kk = 0; kk < 4; ++kk)
                         umma_f16_ts(tO + hf * 128, pa + kk * 8, desc_mnmajor(vb, 128, hf * 4 + kk), idesc_pv,
                                     (j > 0 || kk > 0) ? 1u : 0u);
-                    umma_commit(&bars[B_PVDONE + hf]);
                 }
+                // one completion for both halves (a commit costs the issuing thread ~90
+                // cycles; the math waits on it only to rescale O, rarely)
+                umma_commit(&bars[B_PVDONE]);
                 umma_commit(&bars[B_VEMPTY + (J & 1)]);
             };
             int J = 0, it = 0;
@@ -807,7 +809,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_p(const __grid_constant__ F
             if (__any_sync(0xffffffffu, need)) {
                 // O_h must hold PV(jt-1) before it is rescaled; PV(jt-2) is
                 // already complete (S(jt) was committed after it)
-                mbar_wait(&bars[B_PVDONE + hf], (J - 1) & 1);
+                mbar_wait(&bars[B_PVDONE], (J - 1) & 1);
                 tc_after_sync();
                 float ov[32];
 #pragma unroll
