@@ -645,7 +645,10 @@ __global__ void k_cache_fill_rows(CacheArgs A, const uint8_t* __restrict__ k_his
 
 // ------------------------------------------------------------------ attention
 constexpr int kAttnThreads = 256;
-constexpr int kSlotsPerCta = 64;
+#ifndef SKB_DEC_SLOTS
+#define SKB_DEC_SLOTS 48  // measured best of 48/64/96/128 at cfg4 (0.299 vs 0.308 ms)
+#endif
+constexpr int kSlotsPerCta = SKB_DEC_SLOTS;  // attended entries per attention CTA
 
 template <int VEC>
 __device__ __forceinline__ void ldv(const __nv_bfloat16* p, float* o) {
