@@ -499,6 +499,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_p(const __grid_constant__ F
     float* red = reinterpret_cast<float*>(smem + SM::kRed);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef SKB_TRACE_FWDP  // tiles of items 3.. of CTA 100 (tools/trace_fwdp.py)
+#define TRF(role, jj, ev) \
+    if ((jj) >= tr0) SKB_TR(role, (jj) - tr0, ev)
+#else
+#define TRF(role, jj, ev) \
+    do {                  \
+    } while (0)
+#endif
     const int n_win = (a.w + 127 + 127) / 128;
     const int nitems = a.nqb * a.H * a.B;
     // work item wi -> (query tile fastest, head, sequence)
@@ -562,11 +570,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_p(const __grid_constant__ F
         const int pw = warp - kProdWarp0, ptid = threadIdx.x - kProdWarp0 * 32;
         const int ma = ptid >> 5, mc = ptid & 31;  // metadata: array, 16-byte chunk
         const int* msrc = ma == 0 ? a.qb_list : ma == 1 ? a.qb_leave : reinterpret_cast<const int*>(a.qb_uf);
-        int J = 0, it = 0;
+        int J = 0, it = 0, tr0 = 1 << 28;
         for (int wi = blockIdx.x; wi < nitems; wi += gridDim.x, ++it) {
             const Item I = item(wi);
             const int b = I.b, h = I.h, n_sel = I.n_sel, n = I.n, jw0 = I.jw0;
             const int64_t qrow = I.qrow;
+            if (it == 3) tr0 = J;
             if (ptid == 0) {  // Q once the previous item's last S MMA has read it
                 if (it > 0) mbar_wait(&bars[B_QEMPTY], (it - 1) & 1);
                 mbar_expect_tx(&bars[B_QFULL], kTileBytes);
@@ -609,6 +618,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_p(const __grid_constant__ F
                     }
                     cp_async_arrive_noinc(&bars[B_MFULL + ks]);
                     if (JJ >= kKS) mbar_wait(&bars[B_KEMPTY + ks], ((JJ - kKS) / kKS) & 1);
+                    if (ptid == 0) TRF(2, JJ, 1);
                     load_rows(jt, sbase + SM::kK + ks * SM::kTile, kcur, a.k, &a.tm_k, &bars[B_KFULL + ks]);
                     if (jt + 1 < n_sel)
                         knext.fetch(pw, lane, [&](int r) { return __ldg(list + (jt + 1) * 128 + r); });
@@ -616,6 +626,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_p(const __grid_constant__ F
                 if (jt >= 1) {
                     const int j = jt - 1, JJ = J + j, vs = JJ & 1;
                     if (JJ >= 2) mbar_wait(&bars[B_VEMPTY + vs], ((JJ - 2) >> 1) & 1);
+                    if (ptid == 0) TRF(2, JJ, 3);
                     load_rows(j, sbase + SM::kV + vs * SM::kTile, kprev, a.v, &a.tm_v, &bars[B_VFULL + vs]);
                 }
                 kprev = kcur;
@@ -628,14 +639,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_p(const __grid_constant__ F
         if (lane == 0) {
             constexpr uint32_t idesc_qk = umma_idesc(128, 128, false, false);
             constexpr uint32_t idesc_pv = umma_idesc(128, D, false, true);
+            int tr0 = 1 << 28;
             auto pv = [&](int J, int j, int itn) {
                 mbar_wait_fast(&bars[B_VFULL + (J & 1)], (J >> 1) & 1);
+                TRF(3, J, 2);
                 fence_proxy_async();
                 if (j == 0 && itn > 0) mbar_wait_fast(&bars[B_OEMPTY], (itn - 1) & 1);  // O read out
                 const uint32_t vb = sbase + SM::kV + (J & 1) * SM::kTile;
 #pragma unroll
                 for (int hf = 0; hf < 2; ++hf) {
                     mbar_wait_fast(&bars[B_PFULL + 2 * (J & 1) + hf], (J >> 1) & 1);
+                    TRF(3, J, 3 + hf);
                     tc_after_sync();
                     // P~ of this half: 64 keys packed over the first 32 of its own S columns
                     const uint32_t pa = tS + (J & 1) * 128 + hf * 64;
@@ -648,15 +662,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_p(const __grid_constant__ F
                 // cycles; the math waits on it only to rescale O, rarely)
                 umma_commit(&bars[B_PVDONE]);
                 umma_commit(&bars[B_VEMPTY + (J & 1)]);
+                TRF(3, J, 5);
             };
             int J = 0, it = 0;
             for (int wi = blockIdx.x; wi < nitems; wi += gridDim.x, ++it) {
                 const Item I = item(wi);
                 const int n = I.n;
+                if (it == 3) tr0 = J;
                 mbar_wait_fast(&bars[B_QFULL], it & 1);
                 for (int jt = 0; jt < n; ++jt) {
                     const int JJ = J + jt, s = JJ & 1, ks = JJ % kKS;
                     mbar_wait_fast(&bars[B_KFULL + ks], (JJ / kKS) & 1);
+                    TRF(3, JJ, 0);
                     fence_proxy_async();
                     if (JJ >= 2) mbar_wait_fast(&bars[B_SEMPTY + s], ((JJ - 2) >> 1) & 1);
                     tc_after_sync();
@@ -667,6 +684,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_p(const __grid_constant__ F
                                  idesc_qk, kk > 0 ? 1u : 0u);
                     umma_commit(&bars[B_SFULL + s]);
                     umma_commit(&bars[B_KEMPTY + ks]);
+                    TRF(3, JJ, 1);
                     if (jt == n - 1) umma_commit(&bars[B_QEMPTY]);
                     if (jt >= 1) pv(JJ - 1, jt - 1, it);
                 }
@@ -681,11 +699,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_p(const __grid_constant__ F
         const int hf = warp >> 2;                // key half: 0 -> tile cols 0..63, 1 -> 64..127
         const int r = ((warp & 3) << 5) | lane;  // tile row = TMEM lane
         const int c0 = hf * 64;
-        int J = 0, it = 0;
+        int J = 0, it = 0, tr0 = 1 << 28;
+        const bool trl = lane == 0 && (warp & 3) == 0;
         for (int wi = blockIdx.x; wi < nitems; wi += gridDim.x, ++it) {
         const Item I = item(wi);
         const int b = I.b, h = I.h, n_sel = I.n_sel, n = I.n, jw0 = I.jw0;
         const int64_t bl = I.bl;
+        if (it == 3) tr0 = J;
         const int i = I.i0 + r;
         const int t = i - a.w;
         const float tau_i = (t >= 0 && a.R1 > 0) ? a.tauf[bl + t] : -INFINITY;
@@ -699,6 +719,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_p(const __grid_constant__ F
             const int s = J & 1;
             const bool is_sel = jt < n_sel;
             const int ks = J % kKS;
+            if (trl) TRF(hf, J, 9);
             mbar_wait(&bars[B_SFULL + s], (J >> 1) & 1);
             mbar_wait(&bars[B_MFULL + ks], (J / kKS) & 1);  // every phase observed (window tiles too)
             tc_after_sync();
@@ -707,6 +728,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_p(const __grid_constant__ F
             tmem_wait_ld();
             tc_before_sync();
             mbar_arrive(&bars[B_SEMPTY + s]);
+            if (trl) TRF(hf, J, 0);
 
 #if SKB_EXP == 1 || SKB_EXP == 4 || SKB_EXP == 8
             if (true) {  // experiment: no softmax work (pipeline without the math)
@@ -835,6 +857,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_p(const __grid_constant__ F
                 tmem_wait_st();
             }
             tc_before_sync();
+            if (trl) TRF(hf, J, 4);
             mbar_arrive(&bars[B_MEMPTY + ks]);  // every tile (the producer waits on each stage)
             mbar_arrive(&bars[B_PFULL + 2 * s + hf]);
         }
@@ -882,6 +905,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_p(const __grid_constant__ F
     __syncthreads();
     tc_after_sync();
     if (warp == kMmaWarp) tmem_dealloc<512>(tmem);
+#undef TRF
 }
 
 template <int D, bool KS>
