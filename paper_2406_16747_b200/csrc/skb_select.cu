@@ -557,12 +557,21 @@ __global__ void __launch_bounds__(kTauThreads) k_tau_segments(TauArgs a, int nch
     __syncthreads();
     const int cf = s_lim[0], cl = s_lim[1];
     if (cf < 0) return;
+    // phase clocks of the segment holding sequence 0's last chunk (tools/trace_tau.py)
+    const bool trs = blockIdx.y == 0 && c_lo <= (a.T - 1) / kChunk && (a.T - 1) / kChunk < c_hi;
+#define TSEG(ev)                                                      \
+    do {                                                              \
+        if (trs) TTAU((a.T - 1) / kChunk * kChunk, a.T, ev);          \
+    } while (0)
+    TSEG(7);
     double* bz = smem;
     double* bz2 = smem + a.cap;
     double* P = smem + 2 * a.cap;
     const double* ub = a.u + (int64_t)b * a.L;
     int m = tau_band(a, b, cf * kChunk, bz, a.cap, red_d);
+    TSEG(8);
     for (int c = cf; c <= cl; ++c) {
+        if (c == cl) TSEG(9);
         if (c > cf) {
             const int tp = (c - 1) * kChunk;
             const int nv = min(kChunk, a.T - tp);
@@ -592,6 +601,7 @@ __global__ void __launch_bounds__(kTauThreads) k_tau_segments(TauArgs a, int nch
                 m = n_gt(bz, m, theta - 1.0);
             }
         }
+        if (c == cl) TSEG(10);
         if (m < 0) {  // beyond the cap: the next pass takes the rest
             if (threadIdx.x == 0)
                 for (int cc = c; cc <= cl; ++cc) {
@@ -607,6 +617,7 @@ __global__ void __launch_bounds__(kTauThreads) k_tau_segments(TauArgs a, int nch
         if (P1 || fl[c]) tau_chunk_tail(a, b, c, bz, P, m, red_d);
     }
 }
+#undef TSEG
 
 // Second pass over the chunks whose band exceeded the first pass's small
 // shared-memory cap, with the large cap; its own overflows go to queue 2.

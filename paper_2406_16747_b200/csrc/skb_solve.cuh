@@ -51,17 +51,19 @@ __device__ T block_reduce(T v, T* sbuf, bool is_max) {
 
 // Descending bitonic sort of z[0..n2), n2 a power of two (pad with -inf).
 __device__ inline void bitonic_desc(double* z, int n2) {
+    // one thread per compare-exchange pair (n2 / 2 per stage, none idle):
+    // pair p -> i = p with a zero bit inserted at jj, partner i | jj
+    const int np = n2 >> 1;
     for (int kk = 2; kk <= n2; kk <<= 1) {
         for (int jj = kk >> 1; jj > 0; jj >>= 1) {
-            for (int i = threadIdx.x; i < n2; i += blockDim.x) {
-                const int ixj = i ^ jj;
-                if (ixj > i) {
-                    const double x = z[i], y = z[ixj];
-                    const bool desc = (i & kk) == 0;
-                    if (desc ? (x < y) : (x > y)) {
-                        z[i] = y;
-                        z[ixj] = x;
-                    }
+            for (int p = threadIdx.x; p < np; p += blockDim.x) {
+                const int i = ((p & ~(jj - 1)) << 1) | (p & (jj - 1));
+                const int ixj = i | jj;
+                const double x = z[i], y = z[ixj];
+                const bool desc = (i & kk) == 0;
+                if (desc ? (x < y) : (x > y)) {
+                    z[i] = y;
+                    z[ixj] = x;
                 }
             }
             __syncthreads();
