@@ -272,12 +272,18 @@ constexpr int kRadixItems = 8;
 #endif
 using BandSort = cub::BlockRadixSort<double, kTauThreads, kRadixItems, cub::NullType, SKB_TAU_RADIX_BITS>;
 constexpr int kRadixMax = kTauThreads * kRadixItems;
+// the segmented pass sorts bands up to 8192 keys with 32 keys per thread; its
+// scratch aliases P, sized max(cap_big doubles, this)
+constexpr size_t kBigSortBytes =
+    sizeof(cub::BlockRadixSort<double, kTauThreads, 32, cub::NullType, SKB_TAU_RADIX_BITS>::TempStorage);
 // narrower bands take a sort with fewer keys per thread (the passes cost the
 // same per key slot, so an 8-slot sort of a 400-key band is mostly padding)
 template <int ITEMS>
 __device__ __forceinline__ void band_radix_sort(double* bz, int mcount, void* sort_tmp) {
     using Sort = cub::BlockRadixSort<double, kTauThreads, ITEMS, cub::NullType, SKB_TAU_RADIX_BITS>;
-    static_assert(sizeof(typename Sort::TempStorage) <= sizeof(BandSort::TempStorage), "scratch");
+    // (callers: ITEMS <= 8 alias the first pass's P (>= cap + 1 doubles), 32 the
+    // segmented pass's P (kRadixBig doubles))
+    static_assert(ITEMS > 8 || sizeof(typename Sort::TempStorage) <= sizeof(BandSort::TempStorage), "scratch");
     double keys[ITEMS];
 #pragma unroll
     for (int e = 0; e < ITEMS; ++e) {
@@ -294,6 +300,7 @@ __device__ __forceinline__ void band_radix_sort(double* bz, int mcount, void* so
     __syncthreads();
 }
 
+template <bool BIG = false>
 __device__ int tau_band(const TauArgs& a, int b, int t0, double* bz, int cap, double* red_d,
                         void* sort_tmp = nullptr) {
     __shared__ int s_m;
@@ -358,6 +365,13 @@ __device__ int tau_band(const TauArgs& a, int b, int t0, double* bz, int cap, do
         else band_radix_sort<kRadixItems>(bz, mcount, sort_tmp);
         TTAU(t0, a.T, 3);
         return mcount;
+    }
+    if constexpr (BIG) {
+        if (sort_tmp != nullptr && mcount <= kTauThreads * 32 && blockDim.x == kTauThreads) {
+            band_radix_sort<32>(bz, mcount, sort_tmp);  // wide bands (the segmented pass)
+            TTAU(t0, a.T, 3);
+            return mcount;
+        }
     }
     int n2 = 1;
     while (n2 < mcount) n2 <<= 1;
@@ -568,7 +582,8 @@ __global__ void __launch_bounds__(kTauThreads) k_tau_segments(TauArgs a, int nch
     double* bz2 = smem + a.cap;
     double* P = smem + 2 * a.cap;
     const double* ub = a.u + (int64_t)b * a.L;
-    int m = tau_band(a, b, cf * kChunk, bz, a.cap, red_d);
+    // the radix scratch aliases P (cap_big doubles), written only after the sort
+    int m = tau_band<true>(a, b, cf * kChunk, bz, a.cap, red_d, a.cap >= 8192 ? P : nullptr);
     TSEG(8);
     for (int c = cf; c <= cl; ++c) {
         if (c == cl) TSEG(9);
@@ -1094,7 +1109,8 @@ void run_select(const skb_attn_desc& d, const double* u, void* ws, cudaStream_t 
             SKB_CHECK_CUDA(cudaFuncSetAttribute(k_tau_chunks_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                 (int)(8192 * 2 * sizeof(double) + 16)));
             SKB_CHECK_CUDA(cudaFuncSetAttribute(k_tau_segments<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                (int)(8192 * 3 * sizeof(double) + 16)));
+                                                (int)(8192 * 2 * sizeof(double) +
+                                                      std::max(8192 * sizeof(double), kBigSortBytes) + 16)));
             SKB_CHECK_CUDA(cudaFuncSetAttribute(k_tau_segments<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                 (int)(8192 * 3 * sizeof(double) + 16)));
         }
@@ -1119,8 +1135,9 @@ void run_select(const skb_attn_desc& d, const double* u, void* ws, cudaStream_t 
             // at B = 1 (a strong-scaling rank) 4-chunk segments halve the latency
             const int seg = (int)std::min<int64_t>(kSegChunks, std::max<int64_t>(1, cdiv((int64_t)nch * B, num_sms())));
             dim3 gs((unsigned)cdiv(nch, seg), (unsigned)B);
-            k_tau_segments<false><<<gs, kTauThreads, (size_t)cap_big * 3 * sizeof(double) + 16, st>>>(a2, nch, seg,
-                                                                                                    q2, q2 + 1);
+            const size_t seg_smem = (size_t)cap_big * 2 * sizeof(double) +
+                                    std::max((size_t)cap_big * sizeof(double), cap_big >= 8192 ? kBigSortBytes : 0) + 16;
+            k_tau_segments<false><<<gs, kTauThreads, seg_smem, st>>>(a2, nch, seg, q2, q2 + 1);
             SKB_CHECK_LAUNCH();
             a.ovf_count = q2;  // the global-scratch pass serves what is left
             a.ovf_items = q2 + 1;
