@@ -300,6 +300,10 @@ __device__ __forceinline__ void band_radix_sort(double* bz, int mcount, void* so
     __syncthreads();
 }
 
+#ifndef SKB_TAU_SCAN_ILP  // prefix loads in flight per thread in the band scans
+#define SKB_TAU_SCAN_ILP 8
+#endif
+constexpr int kScanILP = SKB_TAU_SCAN_ILP;
 template <bool BIG = false>
 __device__ int tau_band(const TauArgs& a, int b, int t0, double* bz, int cap, double* red_d,
                         void* sort_tmp = nullptr) {
@@ -313,17 +317,17 @@ __device__ int tau_band(const TauArgs& a, int b, int t0, double* bz, int cap, do
     if (t0 >= a.R2 && a.R2 > 0) {
         double mn = CUDART_INF;
         // 4 independent load pairs in flight per thread (the pass is latency-bound)
-        for (int j0 = threadIdx.x; j0 < t0; j0 += 4 * blockDim.x) {
-            int lvv[4];
-            double uv[4];
+        for (int j0 = threadIdx.x; j0 < t0; j0 += kScanILP * blockDim.x) {
+            int lvv[kScanILP];
+            double uv[kScanILP];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
+            for (int q = 0; q < kScanILP; ++q) {
                 const int j = j0 + q * blockDim.x;
                 lvv[q] = j < t0 ? lv[j] : -1;
                 uv[q] = j < t0 ? ub[j] : CUDART_INF;
             }
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
+            for (int q = 0; q < kScanILP; ++q)
                 if (lvv[q] >= t0) mn = fmin(mn, uv[q]);
         }
         theta = block_reduce<double>(mn, red_d, false);
@@ -335,15 +339,15 @@ __device__ int tau_band(const TauArgs& a, int b, int t0, double* bz, int cap, do
     // one pass: warp-aggregated slots, stores only below the cap (an oversized
     // band is reported after the pass; the order is irrelevant, bz is sorted next)
     const int lane = threadIdx.x & 31;
-    for (int j0 = 0; j0 < t0; j0 += 4 * blockDim.x) {
-        double xv[4];
+    for (int j0 = 0; j0 < t0; j0 += kScanILP * blockDim.x) {
+        double xv[kScanILP];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < kScanILP; ++q) {
             const int j = j0 + q * blockDim.x + threadIdx.x;
             xv[q] = j < t0 ? ub[j] : -CUDART_INF;
         }
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < kScanILP; ++q) {
             const double x = xv[q];
             const bool p = x > cut;
             const unsigned m = __ballot_sync(0xffffffffu, p);
@@ -361,7 +365,10 @@ __device__ int tau_band(const TauArgs& a, int b, int t0, double* bz, int cap, do
     if (mcount > cap) return -1;
     if (sort_tmp != nullptr && mcount <= kRadixMax && blockDim.x == kTauThreads) {
         if (mcount <= kTauThreads * 2) band_radix_sort<2>(bz, mcount, sort_tmp);
+        else if (mcount <= kTauThreads * 3) band_radix_sort<3>(bz, mcount, sort_tmp);
         else if (mcount <= kTauThreads * 4) band_radix_sort<4>(bz, mcount, sort_tmp);
+        else if (mcount <= kTauThreads * 5) band_radix_sort<5>(bz, mcount, sort_tmp);
+        else if (mcount <= kTauThreads * 6) band_radix_sort<6>(bz, mcount, sort_tmp);
         else band_radix_sort<kRadixItems>(bz, mcount, sort_tmp);
         TTAU(t0, a.T, 3);
         return mcount;
