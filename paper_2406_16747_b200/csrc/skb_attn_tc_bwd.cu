@@ -101,28 +101,36 @@ __device__ __forceinline__ int64_t part_off(const BwdArgs& a, int b, int h, int 
     return ((((int64_t)(b * a.H + h) * ng + (key >> 5)) * (D / 8) + c8) * 32 + (key & 31)) * 8;
 }
 
-// One (b, i, h) row per D/8 threads: 16-byte loads of O and dO, a
+// One (b, i, h) row per D/(8 VPT) threads: VPT 16-byte loads of O and dO per
+// thread (cfg3: 84 us = 6.4 TB/s with two in flight per tensor, 115 us with one), a
 // shuffle-reduced dot product, lse converted to log2 units. HBM-bound.
-template <int D>
+template <int D, int VPT = 2>
 __global__ void __launch_bounds__(256) k_bwd_prep(const __nv_bfloat16* __restrict__ o,
                                                   const __nv_bfloat16* __restrict__ dout,
                                                   const double* __restrict__ lse, float* __restrict__ lse2,
                                                   float* __restrict__ delta, int B, int L, int H) {
-    constexpr int kTpr = D / 8;  // threads per row
+    constexpr int kTpr = D / (8 * VPT);  // threads per row
     const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t row = gt / kTpr;  // (b, i, h)
     const int sub = (int)(gt % kTpr);
     const bool ok = row < (int64_t)B * L * H;
     float acc = 0.f;
     if (ok) {
-        const uint4 x = *reinterpret_cast<const uint4*>(o + row * D + sub * 8);
-        const uint4 g = *reinterpret_cast<const uint4*>(dout + row * D + sub * 8);
-        const uint32_t xs[4] = {x.x, x.y, x.z, x.w}, gs[4] = {g.x, g.y, g.z, g.w};
+        uint4 x[VPT], g[VPT];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const float2 a2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xs[e]));
-            const float2 b2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&gs[e]));
-            acc = fmaf(a2.x, b2.x, fmaf(a2.y, b2.y, acc));
+        for (int v = 0; v < VPT; ++v) {
+            x[v] = *reinterpret_cast<const uint4*>(o + row * D + (sub * VPT + v) * 8);
+            g[v] = *reinterpret_cast<const uint4*>(dout + row * D + (sub * VPT + v) * 8);
+        }
+#pragma unroll
+        for (int v = 0; v < VPT; ++v) {
+            const uint32_t xs[4] = {x[v].x, x[v].y, x[v].z, x[v].w}, gs[4] = {g[v].x, g[v].y, g[v].z, g[v].w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const float2 a2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xs[e]));
+                const float2 b2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&gs[e]));
+                acc = fmaf(a2.x, b2.x, fmaf(a2.y, b2.y, acc));
+            }
         }
     }
 #pragma unroll
@@ -3498,7 +3506,7 @@ void run_attn_bwd_tc(const skb_attn_desc& d, const void* q, const void* k, const
     a.mask_st = d.mask_mode;
     a.chunk_len = (int)d.chunk_len;
     const int64_t rows = d.batch * d.seq_len * d.heads;
-    const unsigned pg = (unsigned)cdiv(rows * (d.head_dim / 8), 256);
+    const unsigned pg = (unsigned)cdiv(rows * (d.head_dim / 16), 256);  // k_bwd_prep: 2 x 16 B per thread
     if (d.head_dim == 128)
         k_bwd_prep<128><<<pg, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(o), a.dout, lse, lse2, delta,
                                             a.B, a.L, a.H);
