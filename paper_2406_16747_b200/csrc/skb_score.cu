@@ -44,7 +44,10 @@ __global__ void k_score_raw(const S* __restrict__ x, const double* __restrict__ 
 // read), and thread r then walks its row's slice in column order — the
 // reference's left-to-right, unfused float64 accumulation, so raw stays
 // bit-identical (proj/include/sparsek/selection.hpp:72-74).
-constexpr int kRawRows = 128;
+#ifndef SKB_K1_ROWS
+#define SKB_K1_ROWS 32  // cfg3 x: 62.5 us vs 76.7 at 128 rows (more CTAs, shorter staging)
+#endif
+constexpr int kRawRows = SKB_K1_ROWS;  // rows (threads) per CTA
 constexpr int kRawStages = 4;
 constexpr int kRawPitch = 144;  // 128 B slice + 16 B pad: 16-byte row reads spread over the banks
 
