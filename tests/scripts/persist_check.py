@@ -19,6 +19,8 @@ CASES = [  # L, H, D, k, w, kind, chunk_len
     (2500, 2, 64, 120.0, 64, "iid", 0),
     (3000, 2, 128, 256.0, 300, "iid", 512),
     (1777, 2, 128, 90.5, 33, "recency", 0),
+    (2300, 2, 128, 150.0, 128, "mixed", 0),  # one dense, one sparse sequence: both backward paths at once
+    (1900, 2, 64, 120.5, 96, "mixed", 0),
 ]
 bad = 0
 for L, H, D, k, w, kind, chunk in CASES:
@@ -28,6 +30,8 @@ for L, H, D, k, w, kind, chunk in CASES:
     u = torch.randn((2, L), generator=g, device=dev, dtype=torch.float64)
     if kind == "recency":
         u += 0.01 * torch.arange(L, device=dev, dtype=torch.float64)
+    elif kind == "mixed":
+        u[0] += 0.01 * torch.arange(L, device=dev, dtype=torch.float64)
     res = {}
     for fg in (False, True):
         cfg = ops.AttnConfig(k=k, window=w, chunk_len=chunk, force_gather=fg)
