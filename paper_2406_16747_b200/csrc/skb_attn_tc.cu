@@ -86,7 +86,10 @@ struct FwdArgs {
     int mask_st;
 };
 
-constexpr int kKS = 3;  // K + metadata ring depth (V ring: 2)
+#ifndef SKB_FWD_KS
+#define SKB_FWD_KS 3
+#endif
+constexpr int kKS = SKB_FWD_KS;  // K + metadata ring depth (V ring: 2)
 
 template <int D>
 struct FwdSmem {
