@@ -43,6 +43,9 @@ CASES = [
     (2, 120, 2, 32, 0.5, 6, "soft", "soft", "iid", 0),          # floor(k) = 0, stream on
     (1, 90, 4, 128, 7.0, 5, "hard", "soft", "constant", 30),
     (2, 40, 2, 8, 8.0, 64, "hard", "soft", "iid", 10),          # never leaves the window
+    # survivor arrays outgrow the control kernel's shared-memory staging
+    # (4096 entries) part-way: both the staged and the global-array push
+    (1, 4600, 1, 16, 4300.0, 8, "hard", "soft", "recency", 200),
 ]
 
 
