@@ -538,20 +538,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_p(const __grid_constant__ F
             mbar_init(&bars[B_KFULL + s], kProducers + 1);
             mbar_init(&bars[B_KEMPTY + s], 1);
             mbar_init(&bars[B_MFULL + s], kProducers);
-            mbar_init(&bars[B_MEMPTY + s], kMath);
+            mbar_init(&bars[B_MEMPTY + s], kMathArrivals);
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(&bars[B_VFULL + s], kProducers + 1);
             mbar_init(&bars[B_VEMPTY + s], 1);
             mbar_init(&bars[B_SFULL + s], 1);
-            mbar_init(&bars[B_SEMPTY + s], kMath);
-            mbar_init(&bars[B_PFULL + 2 * s], kMath / 2);
-            mbar_init(&bars[B_PFULL + 2 * s + 1], kMath / 2);
+            mbar_init(&bars[B_SEMPTY + s], kMathArrivals);
+            mbar_init(&bars[B_PFULL + 2 * s], kMathArrivals / 2);
+            mbar_init(&bars[B_PFULL + 2 * s + 1], kMathArrivals / 2);
             mbar_init(&bars[B_PVDONE + s], 1);
         }
         mbar_init(&bars[B_ODONE], 1);
         mbar_init(&bars[B_QEMPTY], 1);
-        mbar_init(&bars[B_OEMPTY], kMath);
+        mbar_init(&bars[B_OEMPTY], kMathArrivals);
         mbar_fence_init();
     }
     if (warp == kMmaWarp) tmem_alloc<512>(tmem_slot);
@@ -730,14 +730,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_p(const __grid_constant__ F
             tmem_ld32(tS + lane_off + s * 128 + c0 + 32, sv + 32);
             tmem_wait_ld();
             tc_before_sync();
-            mbar_arrive(&bars[B_SEMPTY + s]);
+            warp_arrive(&bars[B_SEMPTY + s]);
             if (trl) TRF(hf, J, 0);
 
 #if SKB_EXP == 1 || SKB_EXP == 4 || SKB_EXP == 8
             if (true) {  // experiment: no softmax work (pipeline without the math)
                 tc_before_sync();
                 mbar_arrive(&bars[B_MEMPTY + ks]);
-                mbar_arrive(&bars[B_PFULL + 2 * s + hf]);
+                warp_arrive(&bars[B_PFULL + 2 * s + hf]);
                 continue;
             }
 #endif
@@ -861,8 +861,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_p(const __grid_constant__ F
             }
             tc_before_sync();
             if (trl) TRF(hf, J, 4);
-            mbar_arrive(&bars[B_MEMPTY + ks]);  // every tile (the producer waits on each stage)
-            mbar_arrive(&bars[B_PFULL + 2 * s + hf]);
+            warp_arrive(&bars[B_MEMPTY + ks]);  // every tile (the producer waits on each stage)
+            warp_arrive(&bars[B_PFULL + 2 * s + hf]);
         }
         // epilogue: merge the two halves' softmaxes; half h writes O columns
         // [h*D/2, (h+1)*D/2) = (O_0 f_0 + O_1 f_1) / (l_0 f_0 + l_1 f_1)
@@ -900,7 +900,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd_p(const __grid_constant__ F
             }
         }
         tc_before_sync();
-        mbar_arrive(&bars[B_OEMPTY]);
+        warp_arrive(&bars[B_OEMPTY]);
         if (hf == 0 && i < a.L) a.lse[((int64_t)b * a.H + h) * a.L + i] = (double)((M + __log2f(lrow)) * kLn2);
         }
     }
